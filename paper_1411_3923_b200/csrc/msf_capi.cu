@@ -1,0 +1,744 @@
+// C ABI of the B200 MsFEM-PCG library (include/msfem_b200.h): host-side plan, workspace
+// carving, PCG driver (one PCG iteration captured once as a CUDA graph), design step.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "msf_internal.cuh"
+
+int apply_partials_needed(const Dims& d);
+size_t eig_smem_bytes(int mlmax, int mb);
+
+static thread_local std::string g_err;
+
+int msf_fail(msf_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  g_err = msg;
+  return code;
+}
+
+int msf_cuda_check(msf_ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return MSF_OK;
+  return msf_fail(c, MSF_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                                      \
+  do {                                                                \
+    int _rc = msf_cuda_check(c, (call), #call);                       \
+    if (_rc != MSF_OK) return _rc;                                    \
+  } while (0)
+#define CKL(where)                                                    \
+  do {                                                                \
+    int _rc = msf_cuda_check(c, cudaGetLastError(), where);           \
+    if (_rc != MSF_OK) return _rc;                                    \
+  } while (0)
+
+namespace {
+
+struct Plan {
+  Dims d{};
+  std::vector<int> cls_of_agg;
+  std::vector<EigClass> classes;
+  int mb = 0;
+  long long eig_doubles = 0;
+  std::vector<int> fdx, fdy;
+  std::vector<double> fw;
+  double wsum = 1.0;
+  std::vector<CrLevel> cr;
+  size_t jobs_bytes = 0;
+  int max_partials = 0;
+  size_t total = 0;
+};
+
+int validate(const msf_problem* p, std::string& msg) {
+  if (!p) { msg = "null problem"; return MSF_ERR_ARG; }
+  if (p->nelx < 1 || p->nely < 1) { msg = "nelx, nely must be >= 1"; return MSF_ERR_ARG; }
+  if (p->cx < 1 || p->cy < 1 || p->nelx % p->cx || p->nely % p->cy) {
+    msg = "coarse cell size must divide the grid (nelx % cx == 0, nely % cy == 0)";
+    return MSF_ERR_ARG;
+  }
+  if (p->tile_x < 1 || p->tile_y < 1 || p->nelx % p->tile_x || p->nely % p->tile_y) {
+    msg = "design tile must divide the grid";
+    return MSF_ERR_ARG;
+  }
+  if (p->n_rhs < 1 || p->n_rhs > MSF_MAX_RHS) { msg = "n_rhs must be 1..4"; return MSF_ERR_ARG; }
+  if (p->dilated < 0 || p->dilated >= p->n_rhs) { msg = "dilated index out of range"; return MSF_ERR_ARG; }
+  if (p->n_modes < 1 || p->n_modes > MSF_MAX_MODES) { msg = "n_modes must be 1..16"; return MSF_ERR_ARG; }
+  if (2 * (2 * p->cy + 1) > 100) { msg = "cy > 24 unsupported (agglomerate block exceeds shared memory)"; return MSF_ERR_ARG; }
+  if (!(p->nu >= 0.0 && p->nu < 0.5)) { msg = "nu must be in [0, 0.5)"; return MSF_ERR_ARG; }
+  if (!(p->Emin > 0.0) || !(p->E0 > p->Emin)) { msg = "need 0 < Emin < E0"; return MSF_ERR_ARG; }
+  return MSF_OK;
+}
+
+inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& msg) {
+  int rc = validate(p, msg);
+  if (rc) return rc;
+  if (!fixed) { msg = "fixed_mask is null"; return MSF_ERR_ARG; }
+  Dims& d = P.d;
+  d.nelx = p->nelx; d.nely = p->nely;
+  d.nnx = p->nelx + 1; d.nny = p->nely + 1;
+  d.nn = d.nnx * d.nny; d.ne = d.nelx * d.nely;
+  d.tile_x = p->tile_x; d.tile_y = p->tile_y; d.nt = p->tile_x * p->tile_y;
+  d.cx = p->cx; d.cy = p->cy;
+  d.ncx = p->nelx / p->cx; d.ncy = p->nely / p->cy;
+  d.kmax = p->n_modes;
+  d.bx = 2 * p->cx + 1; d.by = 2 * p->cy + 1; d.box_nodes = d.bx * d.by;
+  d.n_agg = (d.ncx + 1) * (d.ncy + 1);
+  d.mc = (d.ncy + 1) * d.kmax;
+  d.nbc = d.ncx + 1;
+  d.R = p->n_rhs;
+
+  // density-filter offsets in the oracle's order (dx outer, dy inner)
+  P.fdx.clear(); P.fdy.clear(); P.fw.clear();
+  const int r = p->rmin >= 1.0 ? (int)std::ceil(p->rmin) - 1 : 0;
+  P.wsum = 0.0;
+  for (int dx = -r; dx <= r; ++dx)
+    for (int dy = -r; dy <= r; ++dy) {
+      const double w = std::max(0.0, p->rmin - std::hypot((double)dx, (double)dy));
+      if (w > 0.0) { P.fdx.push_back(dx); P.fdy.push_back(dy); P.fw.push_back(w); P.wsum += w; }
+    }
+  if (P.fw.empty()) { P.fdx = {0}; P.fdy = {0}; P.fw = {1.0}; P.wsum = 1.0; }
+
+  // agglomerate classes (§2.4.1): identical local problems share a basis
+  std::map<std::vector<int>, int> sig2cls;
+  P.cls_of_agg.assign(d.n_agg, 0);
+  P.classes.clear();
+  int min_free = 1 << 30;
+  for (int I = 0; I <= d.ncx; ++I)
+    for (int J = 0; J <= d.ncy; ++J) {
+      const int bx0 = std::max(0, (I - 1) * d.cx), bx1 = std::min(d.nelx, (I + 1) * d.cx);
+      const int by0 = std::max(0, (J - 1) * d.cy), by1 = std::min(d.nely, (J + 1) * d.cy);
+      std::vector<int> sig = {bx1 - bx0, by1 - by0, bx0 % d.tile_x, by0 % d.tile_y,
+                              bx0 - (I * d.cx - d.cx), by0 - (J * d.cy - d.cy)};
+      int nfree = 0;
+      for (int ix = bx0; ix <= bx1; ++ix)
+        for (int iy = by0; iy <= by1; ++iy) {
+          const size_t n = (size_t)ix * d.nny + iy;
+          const int m = (fixed[2 * n] ? 1 : 0) | (fixed[2 * n + 1] ? 2 : 0);
+          sig.push_back(m);
+          nfree += (m & 1 ? 0 : 1) + (m & 2 ? 0 : 1);
+        }
+      const int agg = I * (d.ncy + 1) + J;
+      auto it = sig2cls.find(sig);
+      if (it == sig2cls.end()) {
+        EigClass C{};
+        C.rep_agg = agg;
+        C.bx0 = bx0; C.by0 = by0;
+        C.nbx = bx1 - bx0 + 1; C.nby = by1 - by0 + 1;
+        C.iters = 0; C.nkept = 0;
+        sig2cls.emplace(sig, (int)P.classes.size());
+        P.cls_of_agg[agg] = (int)P.classes.size();
+        P.classes.push_back(C);
+        min_free = std::min(min_free, nfree);
+      } else {
+        P.cls_of_agg[agg] = it->second;
+      }
+    }
+  P.mb = std::min(d.kmax + 8, MSF_MAX_BLOCK_EIG);
+  P.mb = std::min(P.mb, min_free);
+  if (P.mb < d.kmax) { msg = "an agglomerate has fewer free DOFs than n_modes"; return MSF_ERR_ARG; }
+  P.eig_doubles = 0;
+  for (EigClass& C : P.classes) {
+    const long long ml = 2 * C.nby, n = (long long)C.nbx * ml;
+    C.off = P.eig_doubles;
+    P.eig_doubles += 2LL * C.nbx * ml * ml + 3LL * n * P.mb + n;
+    P.eig_doubles = (P.eig_doubles + 31) & ~31LL;
+  }
+  // coarse cyclic-reduction levels
+  P.cr.clear();
+  size_t ptrs = 0, ints = 0;
+  for (int s = 1; s < d.nbc; s *= 2) {
+    CrLevel L;
+    L.s = s;
+    for (int k = s; k < d.nbc; k += 2 * s) L.elim.push_back(k);
+    if (L.elim.empty()) break;
+    for (int i = 0; i < d.nbc; i += 2 * s)
+      if (i - s >= 0 || i + s < d.nbc) L.surv.push_back(i);
+    int nq = 0;
+    for (int k : L.elim) nq += (k + s < d.nbc) ? 1 : 0;
+    L.n_inv = (int)L.elim.size() * d.R;
+    L.nP = (int)L.elim.size() * d.R;
+    L.nQ = nq * d.R;
+    L.nDl = (int)L.elim.size() * d.R;
+    L.nDr = nq * d.R;
+    L.nU = nq * d.R;
+    ptrs += 2 * L.n_inv + 3 * (L.nP + L.nQ + L.nDl + L.nDr + L.nU);
+    ints += L.elim.size() + L.surv.size();
+    P.cr.push_back(L);
+  }
+  {
+    CrLevel L;
+    L.s = 0;
+    L.elim.push_back(0);
+    L.n_inv = d.R;
+    ptrs += 2 * L.n_inv;
+    ints += 1;
+    P.cr.push_back(L);
+  }
+  P.jobs_bytes = align_up(ptrs * sizeof(double*)) + align_up(ints * sizeof(int));
+  P.max_partials = apply_partials_needed(d);
+
+  // workspace size
+  const size_t R = d.R, nn = d.nn, ne = d.ne, nt = d.nt;
+  size_t t = 0;
+  auto add = [&](size_t bytes) { t += align_up(bytes); };
+  add(nn);                                   // fixn
+  add(2 * nn * 8);                           // f
+  add(nt * 8 * 5);                           // x_tile, xt, dF, dg, x_new
+  add(R * nt * 8);                           // xbar
+  add(4 * nt * 8);                           // tile_tmp
+  add(std::max(ne, 2 * nt) * 8);             // dc_el
+  add(R * ne * 8);                           // E
+  add(6 * R * 2 * nn * 8);                   // u r z p q t
+  add(P.fw.size() * (8 + 4 + 4));            // filter
+  add(d.n_agg * 4);                          // cls_of_agg
+  add(P.classes.size() * sizeof(EigClass));  // classes
+  add(P.classes.size() * d.kmax * d.box_nodes * 2 * 8);  // phi
+  add(P.classes.size() * d.kmax * 8);        // lam
+  add((size_t)P.eig_doubles * 8);            // eig work
+  add(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);     // Kcell
+  add(5 * R * d.nbc * (size_t)d.mc * d.mc * 8);           // Dc Uc Dinv Pc Qc
+  add(R * d.nbc * (size_t)d.mc * 8);         // cb
+  add(P.jobs_bytes);
+  add(2 * MSF_MAX_RHS * 4);                  // factor_status
+  add(R * sizeof(PcgScalars));
+  add(R * (size_t)P.max_partials * 8);
+  add(R * 8 * 4);                            // counters
+  add(64 * 8);                               // scal
+  P.total = t + 256;
+  return MSF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* msf_last_error(const msf_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+int msf_workspace_bytes(const msf_problem* p, const uint8_t* fixed_mask, size_t* bytes) {
+  Plan P;
+  std::string msg;
+  int rc = make_plan(p, fixed_mask, P, msg);
+  if (rc) return msf_fail(nullptr, rc, msg);
+  if (bytes) *bytes = P.total;
+  return MSF_OK;
+}
+
+int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double* load,
+                   void* workspace, size_t workspace_bytes, void* stream, msf_ctx** out) {
+  if (!out) return msf_fail(nullptr, MSF_ERR_ARG, "out is null");
+  *out = nullptr;
+  if (!load) return msf_fail(nullptr, MSF_ERR_ARG, "load is null");
+  Plan P;
+  std::string msg;
+  int rc = make_plan(p, fixed_mask, P, msg);
+  if (rc) return msf_fail(nullptr, rc, msg);
+  if (!workspace || workspace_bytes < P.total)
+    return msf_fail(nullptr, MSF_ERR_SPACE, "workspace smaller than msf_workspace_bytes()");
+  int dev = -1;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return msf_fail(nullptr, MSF_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(ce));
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, dev);
+  if (prop.major != 10) return msf_fail(nullptr, MSF_ERR_CUDA, "device is not sm_100 (B200)");
+
+  msf_ctx* c = new msf_ctx();
+  c->p = *p;
+  c->d = P.d;
+  c->K0 = make_K0(p->nu);
+  c->stream = (cudaStream_t)stream;
+  c->ws = (char*)workspace;
+  c->ws_bytes = workspace_bytes;
+  c->cls_of_agg = P.cls_of_agg;
+  c->classes = P.classes;
+  c->n_cls = (int)P.classes.size();
+  c->mb = P.mb;
+  c->eig_work_doubles = P.eig_doubles;
+  c->cr = P.cr;
+  c->filt_dx = P.fdx; c->filt_dy = P.fdy; c->filt_w = P.fw;
+  c->n_filt = (int)P.fw.size();
+  c->filt_wsum = P.wsum;
+  c->max_partials = P.max_partials;
+  c->periodic = (p->tile_x != p->nelx || p->tile_y != p->nely);
+
+  const Dims& d = c->d;
+  const size_t R = d.R, nn = d.nn, ne = d.ne, nt = d.nt;
+  char* cur = (char*)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
+  auto take = [&](size_t bytes) { char* r = cur; cur += align_up(bytes); return (void*)r; };
+  c->fixn = (uint8_t*)take(nn);
+  c->f = (double*)take(2 * nn * 8);
+  c->x_tile = (double*)take(nt * 8 * 5);
+  c->xt_tile = c->x_tile + nt;
+  c->dF = c->xt_tile + nt;
+  c->dg = c->dF + nt;
+  c->x_new = c->dg + nt;
+  c->xbar_tile = (double*)take(R * nt * 8);
+  c->tile_tmp = (double*)take(4 * nt * 8);
+  c->dc_el = (double*)take(std::max(ne, 2 * nt) * 8);
+  c->E = (double*)take(R * ne * 8);
+  double* vec = (double*)take(6 * R * 2 * nn * 8);
+  c->u = vec;
+  c->r = vec + 1 * R * 2 * nn;
+  c->z = vec + 2 * R * 2 * nn;
+  c->pv = vec + 3 * R * 2 * nn;
+  c->q = vec + 4 * R * 2 * nn;
+  c->t = vec + 5 * R * 2 * nn;
+  char* fb = (char*)take(P.fw.size() * (8 + 4 + 4));
+  c->filt_w_d = (double*)fb;
+  c->filt_dx_d = (int*)(fb + P.fw.size() * 8);
+  c->filt_dy_d = c->filt_dx_d + P.fw.size();
+  c->cls_of_agg_d = (int*)take(d.n_agg * 4);
+  c->classes_d = (EigClass*)take(c->n_cls * sizeof(EigClass));
+  c->phi = (double*)take((size_t)c->n_cls * d.kmax * d.box_nodes * 2 * 8);
+  c->lam = (double*)take((size_t)c->n_cls * d.kmax * 8);
+  c->eig_work = (double*)take((size_t)P.eig_doubles * 8);
+  c->Kcell = (double*)take(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);
+  const size_t blk = R * d.nbc * (size_t)d.mc * d.mc;
+  double* cm = (double*)take(5 * blk * 8);
+  c->Dc = cm; c->Uc = cm + blk; c->Dinv = cm + 2 * blk; c->Pc = cm + 3 * blk; c->Qc = cm + 4 * blk;
+  c->cb = (double*)take(R * d.nbc * (size_t)d.mc * 8);
+  c->jobs_d = (char*)take(P.jobs_bytes);
+  c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
+  c->sc = (PcgScalars*)take(R * sizeof(PcgScalars));
+  c->partials = (double*)take(R * (size_t)P.max_partials * 8);
+  c->counters = (unsigned*)take(R * 8 * 4);
+  c->scal = (double*)take(64 * 8);
+  if ((size_t)(cur - (char*)workspace) > workspace_bytes) {
+    delete c;
+    return msf_fail(nullptr, MSF_ERR_SPACE, "internal: workspace carve overflow");
+  }
+
+  // CR pointer tables
+  {
+    std::vector<double*> ptrs;
+    std::vector<int> ints;
+    const size_t per = (size_t)d.mc * d.mc;
+    auto B = [&](double* base, int rhs, int k) { return base + ((size_t)rhs * d.nbc + k) * per; };
+    struct Fix { size_t inv, P, Q, Dl, Dr, U, elim, surv; };
+    std::vector<Fix> fixes;
+    for (CrLevel& L : c->cr) {
+      Fix F{};
+      const int s = L.s;
+      F.inv = ptrs.size();
+      for (int rhs = 0; rhs < d.R; ++rhs)
+        for (int k : L.elim) ptrs.push_back(B(c->Dinv, rhs, k));
+      for (int rhs = 0; rhs < d.R; ++rhs)
+        for (int k : L.elim) ptrs.push_back(B(c->Dc, rhs, k));
+      if (s > 0) {
+        F.P = ptrs.size();
+        std::vector<double*> a, b, cc;
+        for (int rhs = 0; rhs < d.R; ++rhs)
+          for (int k : L.elim) { a.push_back(B(c->Uc, rhs, k - s)); b.push_back(B(c->Dinv, rhs, k)); cc.push_back(B(c->Pc, rhs, k)); }
+        ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
+        a.clear(); b.clear(); cc.clear();
+        F.Q = ptrs.size();
+        for (int rhs = 0; rhs < d.R; ++rhs)
+          for (int k : L.elim) if (k + s < d.nbc) { a.push_back(B(c->Uc, rhs, k)); b.push_back(B(c->Dinv, rhs, k)); cc.push_back(B(c->Qc, rhs, k)); }
+        ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
+        a.clear(); b.clear(); cc.clear();
+        F.Dl = ptrs.size();
+        for (int rhs = 0; rhs < d.R; ++rhs)
+          for (int k : L.elim) { a.push_back(B(c->Pc, rhs, k)); b.push_back(B(c->Uc, rhs, k - s)); cc.push_back(B(c->Dc, rhs, k - s)); }
+        ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
+        a.clear(); b.clear(); cc.clear();
+        F.Dr = ptrs.size();
+        for (int rhs = 0; rhs < d.R; ++rhs)
+          for (int k : L.elim) if (k + s < d.nbc) { a.push_back(B(c->Qc, rhs, k)); b.push_back(B(c->Uc, rhs, k)); cc.push_back(B(c->Dc, rhs, k + s)); }
+        ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
+        a.clear(); b.clear(); cc.clear();
+        F.U = ptrs.size();
+        for (int rhs = 0; rhs < d.R; ++rhs)
+          for (int k : L.elim) if (k + s < d.nbc) { a.push_back(B(c->Pc, rhs, k)); b.push_back(B(c->Uc, rhs, k)); cc.push_back(B(c->Uc, rhs, k - s)); }
+        ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
+      }
+      F.elim = ints.size();
+      ints.insert(ints.end(), L.elim.begin(), L.elim.end());
+      F.surv = ints.size();
+      ints.insert(ints.end(), L.surv.begin(), L.surv.end());
+      fixes.push_back(F);
+    }
+    double** pd = (double**)c->jobs_d;
+    int* id = (int*)(c->jobs_d + align_up(ptrs.size() * sizeof(double*)));
+    for (size_t i = 0; i < c->cr.size(); ++i) {
+      CrLevel& L = c->cr[i];
+      const Fix& F = fixes[i];
+      L.inv = pd + F.inv; L.invsrc = L.inv + L.n_inv;
+      if (L.s > 0) {
+        L.pA = pd + F.P; L.pB = L.pA + L.nP; L.pC = L.pB + L.nP;
+        L.qA = pd + F.Q; L.qB = L.qA + L.nQ; L.qC = L.qB + L.nQ;
+        L.dlA = pd + F.Dl; L.dlB = L.dlA + L.nDl; L.dlC = L.dlB + L.nDl;
+        L.drA = pd + F.Dr; L.drB = L.drA + L.nDr; L.drC = L.drB + L.nDr;
+        L.uA = pd + F.U; L.uB = L.uA + L.nU; L.uC = L.uB + L.nU;
+      }
+      L.elim_d = id + F.elim;
+      L.surv_d = id + F.surv;
+    }
+    cudaMemcpyAsync(c->jobs_d, ptrs.data(), ptrs.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(id, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  }
+
+  // fixed mask per node, load, filter table, classes
+  std::vector<uint8_t> fixn(nn);
+  for (size_t n = 0; n < nn; ++n) fixn[n] = (fixed_mask[2 * n] ? 1 : 0) | (fixed_mask[2 * n + 1] ? 2 : 0);
+  ce = cudaMemcpyAsync(c->fixn, fixn.data(), nn, cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->f, load, 2 * nn * 8, cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_w_d, P.fw.data(), P.fw.size() * 8, cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_dx_d, P.fdx.data(), P.fdx.size() * 4, cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_dy_d, P.fdy.data(), P.fdy.size() * 4, cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->cls_of_agg_d, P.cls_of_agg.data(), d.n_agg * 4, cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->classes_d, P.classes.data(), c->n_cls * sizeof(EigClass), cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->factor_status, 0, 2 * MSF_MAX_RHS * 4, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->counters, 0, R * 8 * 4, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->sc, 0, R * sizeof(PcgScalars), c->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->scal, 0, 64 * 8, c->stream);
+  if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->sc_host, MSF_MAX_RHS * sizeof(PcgScalars));
+  if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->scal_host, 80 * 8);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
+  if (ce != cudaSuccess) {
+    std::string m = std::string("setup: ") + cudaGetErrorString(ce);
+    if (c->sc_host) cudaFreeHost(c->sc_host);
+    if (c->scal_host) cudaFreeHost(c->scal_host);
+    delete c;
+    return msf_fail(nullptr, MSF_ERR_CUDA, m);
+  }
+  *out = c;
+  return MSF_OK;
+}
+
+int msf_destroy(msf_ctx* c) {
+  if (!c) return MSF_OK;
+  if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
+  if (c->sc_host) cudaFreeHost(c->sc_host);
+  if (c->scal_host) cudaFreeHost(c->scal_host);
+  delete c;
+  return MSF_OK;
+}
+
+int msf_set_stream(msf_ctx* c, void* stream) {
+  if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
+  c->stream = (cudaStream_t)stream;
+  if (c->iter_graph) {
+    cudaGraphExecDestroy(c->iter_graph);
+    c->iter_graph = nullptr;
+    c->iter_graph_R = -1;
+  }
+  return MSF_OK;
+}
+
+int msf_filter_project(msf_ctx* c, const double* x_tile) {
+  if (!c || !x_tile) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (x_tile != c->x_tile)
+    CK(cudaMemcpyAsync(c->x_tile, x_tile, c->d.nt * 8, cudaMemcpyDeviceToDevice, c->stream));
+  launch_filter_project(c, c->x_tile);
+  CKL("filter_project");
+  c->have_E = true;
+  c->have_basis = c->have_coarse = false;
+  return MSF_OK;
+}
+
+int msf_set_physical(msf_ctx* c, int rhs, const double* xbar_el) {
+  if (!c || !xbar_el) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (c->periodic) return msf_fail(c, MSF_ERR_ARG, "set_physical requires tile == whole grid");
+  if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
+  launch_set_physical(c, rhs, xbar_el);
+  CKL("set_physical");
+  c->have_E = true;
+  c->have_basis = c->have_coarse = false;
+  return MSF_OK;
+}
+
+int msf_build_coarse_basis(msf_ctx* c) {
+  if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
+  if (!c->have_E) return msf_fail(c, MSF_ERR_STATE, "build_coarse_basis before filter_project/set_physical");
+  launch_build_basis(c);
+  CKL("build_coarse_basis");
+  c->have_basis = true;
+  c->have_coarse = false;
+  return MSF_OK;
+}
+
+int msf_assemble_coarse(msf_ctx* c) {
+  if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
+  if (!c->have_basis) return msf_fail(c, MSF_ERR_STATE, "assemble_coarse before build_coarse_basis");
+  launch_assemble_coarse(c);
+  CKL("assemble_coarse");
+  c->have_coarse = true;
+  return MSF_OK;
+}
+
+// two-level V-cycle z = M^{-1} r for realisations [0, nr) (reading R8)
+static void enqueue_vcycle(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated) {
+  const size_t vb = (size_t)2 * c->d.nn * 8;
+  cudaMemsetAsync(z + (size_t)rhs0 * 2 * c->d.nn, 0, nr * vb, c->stream);
+  launch_sgs(c, rhs0, nr, r, z, gated);
+  launch_residual(c, rhs0, nr, r, z, c->t, gated);
+  launch_restrict(c, rhs0, nr, c->t, gated);
+  launch_coarse_solve(c, rhs0, nr, gated);
+  launch_prolong(c, rhs0, nr, z, gated);
+  launch_sgs(c, rhs0, nr, r, z, gated);
+}
+
+static void enqueue_iteration(msf_ctx* c, int nr) {
+  launch_matvec(c, 0, nr, c->pv, c->q, true, true);
+  launch_pcg_update_xr(c, nr);
+  enqueue_vcycle(c, 0, nr, c->r, c->z, true);
+  launch_pcg_rz(c, nr, false);
+  launch_pcg_p(c, nr, false);
+}
+
+static int read_scalars(msf_ctx* c, int nr) {
+  CK(cudaMemcpyAsync(c->sc_host, c->sc, nr * sizeof(PcgScalars), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->scal_host + 64, c->factor_status, 2 * MSF_MAX_RHS * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const int* fs = (const int*)(c->scal_host + 64);
+  for (int k = 0; k < 2 * MSF_MAX_RHS; ++k)
+    if (fs[k])
+      return msf_fail(c, MSF_ERR_FACTOR, "non-positive pivot in a dense SPD factorisation (code " + std::to_string(fs[k]) + ")");
+  return MSF_OK;
+}
+
+int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int32_t* iters,
+                  double* compliance) {
+  if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
+  if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "pcg_solve before assemble_coarse");
+  if (n_rhs < 1 || n_rhs > c->d.R) return msf_fail(c, MSF_ERR_ARG, "n_rhs out of range");
+  if (!(tol > 0.0) || max_it < 1) return msf_fail(c, MSF_ERR_ARG, "need tol > 0, max_it >= 1");
+  const int nr = n_rhs;
+  const long long l0 = c->launches;
+  launch_pcg_init(c, nr, tol, max_it);
+  enqueue_vcycle(c, 0, nr, c->r, c->z, true);
+  launch_pcg_rz(c, nr, true);
+  launch_pcg_p(c, nr, true);
+  CKL("pcg init");
+  // one PCG iteration as a CUDA graph (captured once per realisation count)
+  if (!c->iter_graph || c->iter_graph_R != nr) {
+    if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
+    c->iter_graph = nullptr;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const long long before = c->launches;
+    enqueue_iteration(c, nr);
+    c->pcg_launches = c->launches - before;
+    c->launches = before;
+    CK(cudaStreamEndCapture(c->stream, &g));
+    CK(cudaGraphInstantiate(&c->iter_graph, g, 0));
+    cudaGraphDestroy(g);
+    c->iter_graph_R = nr;
+  }
+  const int check_every = 4;
+  int done = 0;
+  for (int it = 0; it < max_it + check_every && !done; it += check_every) {
+    for (int j = 0; j < check_every; ++j) {
+      CK(cudaGraphLaunch(c->iter_graph, c->stream));
+      c->launches += c->pcg_launches;
+    }
+    int rc = read_scalars(c, nr);
+    if (rc) return rc;
+    done = 1;
+    for (int k = 0; k < nr; ++k)
+      if (c->sc_host[k].active) done = 0;
+  }
+  launch_compliance(c, nr);
+  CKL("compliance");
+  int rc = read_scalars(c, nr);
+  if (rc) return rc;
+  int noconv = 0;
+  for (int k = 0; k < nr; ++k) {
+    c->last_iters[k] = c->sc_host[k].iters;
+    if (iters) iters[k] = c->sc_host[k].iters;
+    if (compliance) compliance[k] = c->sc_host[k].comp;
+    noconv |= c->sc_host[k].noconv;
+  }
+  if (u) CK(cudaMemcpyAsync(u, c->u, (size_t)nr * 2 * c->d.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+  c->have_solution = true;
+  (void)l0;
+  if (noconv) return msf_fail(c, MSF_ERR_NOCONV, "PCG reached max_it");
+  return MSF_OK;
+}
+
+int msf_sensitivities(msf_ctx* c, double kappa, double volfrac, double* dF, double* dg,
+                      double* F, double* g, double* compliance) {
+  if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
+  if (!c->have_solution) return msf_fail(c, MSF_ERR_STATE, "sensitivities before pcg_solve");
+  if (!(volfrac > 0.0)) return msf_fail(c, MSF_ERR_ARG, "volfrac must be > 0");
+  launch_sensitivities(c, kappa, volfrac);
+  CKL("sensitivities");
+  const size_t tb = (size_t)c->d.nt * 8;
+  if (dF && dF != c->dF) CK(cudaMemcpyAsync(dF, c->dF, tb, cudaMemcpyDeviceToDevice, c->stream));
+  if (dg && dg != c->dg) CK(cudaMemcpyAsync(dg, c->dg, tb, cudaMemcpyDeviceToDevice, c->stream));
+  if (F || g || compliance) {
+    CK(cudaMemcpyAsync(c->scal_host, c->scal, 64 * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (F) *F = c->scal_host[0];
+    if (g) *g = c->scal_host[3];
+    if (compliance)
+      for (int k = 0; k < c->d.R; ++k) compliance[k] = c->scal_host[16 + k];
+  }
+  return MSF_OK;
+}
+
+int msf_oc_update(msf_ctx* c, const double* x, const double* dF, const double* dg,
+                  double volfrac, double move, double* x_new) {
+  if (!c || !x || !dF || !dg || !x_new) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (x == x_new) return msf_fail(c, MSF_ERR_ARG, "x_new may not alias x");
+  if (!(volfrac > 0.0) || !(move > 0.0)) return msf_fail(c, MSF_ERR_ARG, "volfrac, move must be > 0");
+  launch_oc(c, x, dF, dg, volfrac, move, x_new);
+  CKL("oc_update");
+  return MSF_OK;
+}
+
+int msf_design_iteration(msf_ctx* c, const double* x, double* x_new, double tol, int max_it,
+                         double kappa, double volfrac, double move, int32_t* iters,
+                         double* compliance, double* F, double* g) {
+  int rc;
+  if ((rc = msf_filter_project(c, x))) return rc;
+  if ((rc = msf_build_coarse_basis(c))) return rc;
+  if ((rc = msf_assemble_coarse(c))) return rc;
+  rc = msf_pcg_solve(c, c->d.R, tol, max_it, nullptr, iters, nullptr);
+  if (rc && rc != MSF_ERR_NOCONV) return rc;
+  const int rc_pcg = rc;
+  if ((rc = msf_sensitivities(c, kappa, volfrac, c->dF, c->dg, F, g, compliance))) return rc;
+  if ((rc = msf_oc_update(c, c->x_tile, c->dF, c->dg, volfrac, move, x_new))) return rc;
+  return rc_pcg;
+}
+
+int msf_design_iteration_host(msf_ctx* c, const double* x_host, double* x_new_host, double tol,
+                              int max_it, double kappa, double volfrac, double move,
+                              int32_t* iters, double* compliance, double* F, double* g) {
+  if (!c || !x_host || !x_new_host) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  const size_t tb = (size_t)c->d.nt * 8;
+  CK(cudaMemcpyAsync(c->x_tile, x_host, tb, cudaMemcpyHostToDevice, c->stream));
+  int rc = msf_design_iteration(c, c->x_tile, c->x_new, tol, max_it, kappa, volfrac, move, iters,
+                                compliance, F, g);
+  if (rc && rc != MSF_ERR_NOCONV) return rc;
+  CK(cudaMemcpyAsync(x_new_host, c->x_new, tb, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return rc;
+}
+
+// ---------------------------------------------------------------------------- diagnostics
+int msf_matvec(msf_ctx* c, int rhs, const double* x, double* y) {
+  if (!c || !x || !y) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (!c->have_E) return msf_fail(c, MSF_ERR_STATE, "matvec before filter_project");
+  if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
+  const size_t off = (size_t)rhs * 2 * c->d.nn;
+  launch_mask_copy(c, x, c->t + off, c->d.nn);
+  launch_matvec(c, rhs, 1, c->t, c->q, false, false);
+  CK(cudaMemcpyAsync(y, c->q + off, (size_t)2 * c->d.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CKL("matvec");
+  return MSF_OK;
+}
+
+int msf_precond_apply(msf_ctx* c, int rhs, const double* r, double* z) {
+  if (!c || !r || !z) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "precond before assemble_coarse");
+  if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
+  const size_t off = (size_t)rhs * 2 * c->d.nn;
+  launch_mask_copy(c, r, c->r + off, c->d.nn);
+  enqueue_vcycle(c, rhs, 1, c->r, c->z, false);
+  CK(cudaMemcpyAsync(z, c->z + off, (size_t)2 * c->d.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CKL("precond_apply");
+  return MSF_OK;
+}
+
+int msf_sgs(msf_ctx* c, int rhs, const double* r, double* z) {
+  if (!c || !r || !z) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (!c->have_E) return msf_fail(c, MSF_ERR_STATE, "sgs before filter_project");
+  if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
+  const size_t off = (size_t)rhs * 2 * c->d.nn;
+  launch_mask_copy(c, r, c->r + off, c->d.nn);
+  launch_mask_copy(c, z, c->z + off, c->d.nn);
+  launch_sgs(c, rhs, 1, c->r, c->z, false);
+  CK(cudaMemcpyAsync(z, c->z + off, (size_t)2 * c->d.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CKL("sgs");
+  return MSF_OK;
+}
+
+int msf_coarse_solve(msf_ctx* c, int rhs, const double* b, double* x) {
+  if (!c || !b || !x) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "coarse_solve before assemble_coarse");
+  if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
+  const size_t n = (size_t)c->d.nbc * c->d.mc;
+  CK(cudaMemcpyAsync(c->cb + rhs * n, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  launch_coarse_solve(c, rhs, 1, false);
+  CK(cudaMemcpyAsync(x, c->cb + rhs * n, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CKL("coarse_solve");
+  int rc = read_scalars(c, 1);
+  return rc;
+}
+
+int msf_get_basis(msf_ctx* c, double* phi_host, int32_t* nkept_host, double* lam_host) {
+  if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
+  if (!c->have_basis) return msf_fail(c, MSF_ERR_STATE, "get_basis before build_coarse_basis");
+  const Dims& d = c->d;
+  const size_t per = (size_t)d.kmax * d.box_nodes * 2;
+  std::vector<double> ph((size_t)c->n_cls * per), lm((size_t)c->n_cls * d.kmax);
+  std::vector<EigClass> cl(c->n_cls);
+  CK(cudaMemcpyAsync(ph.data(), c->phi, ph.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(lm.data(), c->lam, lm.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(cl.data(), c->classes_d, cl.size() * sizeof(EigClass), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int mx = 0;
+  for (const auto& C : cl) mx = std::max(mx, C.iters);
+  c->eig_iters_used = mx;
+  for (int a = 0; a < d.n_agg; ++a) {
+    const int k = c->cls_of_agg[a];
+    if (phi_host) std::memcpy(phi_host + (size_t)a * per, ph.data() + (size_t)k * per, per * 8);
+    if (nkept_host) nkept_host[a] = cl[k].nkept;
+    if (lam_host) std::memcpy(lam_host + (size_t)a * d.kmax, lm.data() + (size_t)k * d.kmax, d.kmax * 8);
+  }
+  int rc = read_scalars(c, 1);
+  return rc;
+}
+
+int msf_get_coarse_blocks(msf_ctx* c, int rhs, double* D_host, double* U_host) {
+  if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
+  if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "get_coarse_blocks before assemble_coarse");
+  if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
+  const size_t n = (size_t)c->d.nbc * c->d.mc * c->d.mc;
+  // Dc/Uc are overwritten by the factorisation: re-gather, copy out, re-factorise.
+  launch_coarse_galerkin(c);
+  if (D_host) CK(cudaMemcpyAsync(D_host, c->Dc + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (U_host) CK(cudaMemcpyAsync(U_host, c->Uc + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  launch_assemble_coarse(c);
+  CKL("get_coarse_blocks");
+  CK(cudaStreamSynchronize(c->stream));
+  return MSF_OK;
+}
+
+int msf_get_physical(msf_ctx* c, int rhs, double* E_el, double* xbar_tile) {
+  if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
+  if (!c->have_E) return msf_fail(c, MSF_ERR_STATE, "get_physical before filter_project");
+  if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
+  if (E_el) CK(cudaMemcpyAsync(E_el, c->E + (size_t)rhs * c->d.ne, (size_t)c->d.ne * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (xbar_tile) CK(cudaMemcpyAsync(xbar_tile, c->xbar_tile + (size_t)rhs * c->d.nt, (size_t)c->d.nt * 8, cudaMemcpyDeviceToDevice, c->stream));
+  return MSF_OK;
+}
+
+int msf_info(msf_ctx* c, int64_t* info) {
+  if (!c || !info) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  const Dims& d = c->d;
+  info[0] = 2LL * d.nn; info[1] = d.ne; info[2] = d.n_agg; info[3] = c->n_cls;
+  info[4] = d.ncx; info[5] = d.ncy; info[6] = d.mc; info[7] = (int64_t)d.nbc * d.mc;
+  info[8] = d.box_nodes; info[9] = c->eig_iters_used;
+  for (int k = 0; k < 4; ++k) info[10 + k] = c->last_iters[k];
+  info[14] = c->pcg_launches; info[15] = (int64_t)c->ws_bytes;
+  return MSF_OK;
+}
+
+int msf_launch_count(msf_ctx* c, int64_t* count, int reset) {
+  if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
+  if (count) *count = c->launches;
+  if (reset) c->launches = 0;
+  return MSF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,516 @@
+// Coarse space of the two-level preconditioner (§2.4, Eq. 10, §2.4.2
+// line 146):
+//   * restriction c = R_c t and prolongation z += R_c^T c with R_c^T = [phi_1 ... phi_Nt],
+//     phi_{i,a} = chi_i psi_a^{omega_i} stored per agglomerate class on a padded
+//     (2cx+1)x(2cy+1)-node box (periodic classes share storage, §2.4.1);
+//   * Galerkin K_c = R_c K R_c^T per realisation, assembled from per-coarse-cell dense
+//     (4k x 4k) products Phi_C^T K_C Phi_C (the dense contraction of the path);
+//   * K_c is block tridiagonal over coarse-node columns (block size m = (ncy+1) k);
+//     exact coarse solve by block cyclic reduction: per level the odd blocks are
+//     eliminated with explicit SPD inverses (batched sweep operator) and batched GEMMs,
+//     so every level is parallel across blocks and realisations.
+#include "msf_internal.cuh"
+
+#include <algorithm>
+
+namespace {
+
+constexpr int NT = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ restriction
+// one CTA per (agglomerate, realisation): c[slot(I,J,a)] = sum_n phi_{I,J,a}(n) . t(n)
+__global__ void __launch_bounds__(NT) k_restrict(Dims d, const double2* __restrict__ tall,
+                                                 const double* __restrict__ phi,
+                                                 const int* __restrict__ cls_of_agg,
+                                                 double* cball, const PcgScalars* sc, int rhs0,
+                                                 int gated) {
+  const int rhs = rhs0 + blockIdx.y;
+  if (gated && !sc[rhs].active) return;
+  __shared__ double red[MSF_MAX_MODES][NT / 32];
+  const int agg = blockIdx.x;
+  const int I = agg / (d.ncy + 1), J = agg - (agg / (d.ncy + 1)) * (d.ncy + 1);
+  const int cls = cls_of_agg[agg];
+  const double* ph = phi + (size_t)cls * d.kmax * d.box_nodes * 2;
+  const double2* t = tall + (size_t)rhs * d.nn;
+  const int gx0 = I * d.cx - d.cx, gy0 = J * d.cy - d.cy;
+  double acc[MSF_MAX_MODES];
+#pragma unroll
+  for (int a = 0; a < MSF_MAX_MODES; ++a) acc[a] = 0.0;
+  // interior of the padded box (chi vanishes on its boundary ring)
+  const int ix_lo = max(1, -gx0), ix_hi = min(d.bx - 2, d.nnx - 1 - gx0);
+  const int iy_lo = max(1, -gy0), iy_hi = min(d.by - 2, d.nny - 1 - gy0);
+  const int w = iy_hi - iy_lo + 1, h = ix_hi - ix_lo + 1;
+  for (int k = threadIdx.x; k < w * h; k += NT) {
+    const int px = ix_lo + k / w, py = iy_lo + (k - (k / w) * w);
+    const double2 tv = t[(size_t)(gx0 + px) * d.nny + (gy0 + py)];
+    const int bn = px * d.by + py;
+#pragma unroll
+    for (int a = 0; a < MSF_MAX_MODES; ++a) {
+      if (a < d.kmax) {
+        const double2 pv = *reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2);
+        acc[a] = fma(pv.x, tv.x, fma(pv.y, tv.y, acc[a]));
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < MSF_MAX_MODES; ++a) {
+    if (a < d.kmax) {
+      const double v = warp_sum(acc[a]);
+      if (lane == 0) red[a][wid] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < d.kmax) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < NT / 32; ++w2) s += red[threadIdx.x][w2];
+    cball[(size_t)rhs * d.nbc * d.mc + (size_t)agg * d.kmax + threadIdx.x] = s;
+  }
+}
+
+// ------------------------------------------------------------------ prolongation
+// z(n) += sum_{I,J,a} phi_{I,J,a}(n) c[slot(I,J,a)]
+__global__ void __launch_bounds__(NT) k_prolong(Dims d, const double* __restrict__ phi,
+                                                const int* __restrict__ cls_of_agg,
+                                                const double* __restrict__ cball, double2* zall,
+                                                const PcgScalars* sc, int rhs0, int gated) {
+  const int rhs = rhs0 + blockIdx.z;
+  if (gated && !sc[rhs].active) return;
+  const int iy = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int ix = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (ix >= d.nnx || iy >= d.nny) return;
+  const double* cb = cball + (size_t)rhs * d.nbc * d.mc;
+  double sx = 0.0, sy = 0.0;
+  const int I0 = ix / d.cx, J0 = iy / d.cy;
+#pragma unroll
+  for (int di = 0; di < 2; ++di) {
+    const int I = I0 + di;
+    if (I > d.ncx) continue;
+    const int px = ix - (I * d.cx - d.cx);
+    if (px < 0 || px >= d.bx) continue;
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj) {
+      const int J = J0 + dj;
+      if (J > d.ncy) continue;
+      const int py = iy - (J * d.cy - d.cy);
+      if (py < 0 || py >= d.by) continue;
+      const int agg = I * (d.ncy + 1) + J;
+      const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2;
+      const int bn = px * d.by + py;
+      const double* cc = cb + (size_t)agg * d.kmax;
+      for (int a = 0; a < d.kmax; ++a) {
+        const double2 pv = *reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2);
+        const double cv = cc[a];
+        sx = fma(pv.x, cv, sx);
+        sy = fma(pv.y, cv, sy);
+      }
+    }
+  }
+  double2* z = zall + (size_t)rhs * d.nn;
+  const size_t n = (size_t)ix * d.nny + iy;
+  double2 zv = z[n];
+  zv.x += sx;
+  zv.y += sy;
+  z[n] = zv;
+}
+
+// ------------------------------------------------------------------ Galerkin cell products
+// Kcell[rhs][cell][p][q] = sum_{e in cell} E_e Phi_e[:,p]^T K0 Phi_e[:,q],  p,q in 0..4k-1,
+// p = corner*k + a, corner = ci*2 + cj for coarse node (CI+ci, CJ+cj).
+__global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const double* __restrict__ Eall,
+                                                      const double* __restrict__ phi,
+                                                      const int* __restrict__ cls_of_agg,
+                                                      double* Kcell) {
+  extern __shared__ double sm[];
+  const int rhs = blockIdx.y;
+  const int cell = blockIdx.x;
+  const int CI = cell / d.ncy, CJ = cell - (cell / d.ncy) * d.ncy;
+  const int km = d.kmax, P = 4 * km;
+  const int ncn_y = d.cy + 1, ncn = (d.cx + 1) * (d.cy + 1);
+  double* PhiC = sm;                          // [ncn][2][P]
+  double* V = PhiC + (size_t)ncn * 2 * P;     // [16][8][P]
+  double* Ech = V + 16 * 8 * P;               // [16]
+  // load Phi_C
+  for (int k = threadIdx.x; k < ncn * 2 * P; k += NT) {
+    const int p = k % P;
+    const int nc = k / P;                     // node*2 + comp
+    const int comp = nc & 1, node = nc >> 1;
+    const int lx = node / ncn_y, ly = node - (node / ncn_y) * ncn_y;
+    const int corner = p / km, a = p - (p / km) * km;
+    const int I = CI + (corner >> 1), J = CJ + (corner & 1);
+    const int px = CI * d.cx + lx - (I * d.cx - d.cx), py = CJ * d.cy + ly - (J * d.cy - d.cy);
+    const int agg = I * (d.ncy + 1) + J;
+    PhiC[k] = phi[(((size_t)cls_of_agg[agg] * d.kmax + a) * d.box_nodes + px * d.by + py) * 2 + comp];
+  }
+  const double* E = Eall + (size_t)rhs * d.ne;
+  const int nel = d.cx * d.cy;
+  const int nent = P * P;
+  double acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+  __syncthreads();
+  for (int e0 = 0; e0 < nel; e0 += 16) {
+    const int ne = min(16, nel - e0);
+    // V_e = K0 Phi_e for the chunk
+    for (int k = threadIdx.x; k < ne * 8 * P; k += NT) {
+      const int p = k % P, rest = k / P;
+      const int i = rest & 7, el = rest >> 3;
+      const int le = e0 + el;
+      const int lex = le / d.cy, ley = le - (le / d.cy) * d.cy;
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int b = j >> 1, comp = j & 1;
+        const int nx = lex + ((b == 1 || b == 2) ? 1 : 0), ny = ley + ((b >= 2) ? 1 : 0);
+        s = fma(K.v[i * 8 + j], PhiC[((nx * ncn_y + ny) * 2 + comp) * P + p], s);
+      }
+      V[(el * 8 + i) * P + p] = s;
+    }
+    for (int el = threadIdx.x; el < ne; el += NT) {
+      const int le = e0 + el;
+      const int lex = le / d.cy, ley = le - (le / d.cy) * d.cy;
+      Ech[el] = E[(size_t)(CI * d.cx + lex) * d.nely + CJ * d.cy + ley];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int ent = threadIdx.x + s * NT;
+      if (ent < nent) {
+        const int p = ent / P, q = ent - (ent / P) * P;
+        double a = acc[s];
+        for (int el = 0; el < ne; ++el) {
+          const int le = e0 + el;
+          const int lex = le / d.cy, ley = le - (le / d.cy) * d.cy;
+          double t = 0.0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int b = i >> 1, comp = i & 1;
+            const int nx = lex + ((b == 1 || b == 2) ? 1 : 0), ny = ley + ((b >= 2) ? 1 : 0);
+            t = fma(PhiC[((nx * ncn_y + ny) * 2 + comp) * P + p], V[(el * 8 + i) * P + q], t);
+          }
+          a = fma(Ech[el], t, a);
+        }
+        acc[s] = a;
+      }
+    }
+    __syncthreads();
+  }
+  double* out = Kcell + ((size_t)rhs * d.ncx * d.ncy + cell) * nent;
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    const int ent = threadIdx.x + s * NT;
+    if (ent < nent) out[ent] = acc[s];
+  }
+}
+
+// Gather the cell products into the block-tridiagonal K_c (D_I, U_I = K_c[I, I+1]);
+// unused eigen-slots (a >= nkept) carry identity rows.
+__global__ void k_coarse_gather(Dims d, const double* __restrict__ Kcell,
+                                const int* __restrict__ cls_of_agg,
+                                const EigClass* __restrict__ cls, double* Dall, double* Uall) {
+  const int km = d.kmax, P = 4 * km, m = d.mc;
+  const size_t per = (size_t)m * m;
+  const size_t total = (size_t)2 * d.nbc * per;
+  const int rhs = blockIdx.y;
+  const double* Kc = Kcell + (size_t)rhs * d.ncx * d.ncy * P * P;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int isU = idx >= (size_t)d.nbc * per;
+    const size_t li = isU ? idx - (size_t)d.nbc * per : idx;
+    const int I = (int)(li / per);
+    const int e = (int)(li - (size_t)I * per);
+    const int row = e / m, col = e - (e / m) * m;
+    const int J = row / km, a = row - (row / km) * km;
+    const int Jp = col / km, b = col - (col / km) * km;
+    double v = 0.0;
+    const int Ir = I, Ic = isU ? I + 1 : I;
+    bool valid = !(isU && I + 1 > d.ncx);
+    if (valid) {
+      const int nka = cls[cls_of_agg[Ir * (d.ncy + 1) + J]].nkept;
+      const int nkb = cls[cls_of_agg[Ic * (d.ncy + 1) + Jp]].nkept;
+      if (a >= nka || b >= nkb) {
+        v = (!isU && row == col) ? 1.0 : 0.0;
+      } else if (abs(J - Jp) <= 1) {
+        const int CIlo = isU ? I : max(I - 1, 0), CIhi = isU ? I : min(I, d.ncx - 1);
+        const int CJlo = max(max(J, Jp) - 1, 0), CJhi = min(min(J, Jp), d.ncy - 1);
+        for (int CI = CIlo; CI <= CIhi; ++CI)
+          for (int CJ = CJlo; CJ <= CJhi; ++CJ) {
+            const int pr = ((Ir - CI) * 2 + (J - CJ)) * km + a;
+            const int pc = ((Ic - CI) * 2 + (Jp - CJ)) * km + b;
+            v += Kc[((size_t)CI * d.ncy + CJ) * P * P + (size_t)pr * P + pc];
+          }
+      }
+    }
+    double* dst = (isU ? Uall : Dall) + ((size_t)rhs * d.nbc + I) * per;
+    dst[e] = v;
+  }
+}
+
+// ------------------------------------------------------------------ dense batched kernels
+// In-place inverse of SPD blocks by the sweep operator (all pivots), then negation:
+// sweep(k): a_kk <- -1/a_kk, a_ik <- a_ik/a_kk, a_kj <- a_kj/a_kk, a_ij <- a_ij - a_ik a_kj/a_kk
+__global__ void __launch_bounds__(1024) k_spd_inverse(double** mats, int m, int* status) {
+  extern __shared__ double sm[];
+  double* rowk = sm;           // [m]
+  double* colk = sm + m;       // [m]
+  double* A = mats[blockIdx.x];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (int k = 0; k < m; ++k) {
+    for (int i = tid; i < m; i += nth) {
+      rowk[i] = A[(size_t)k * m + i];
+      colk[i] = A[(size_t)i * m + k];
+    }
+    __syncthreads();
+    const double piv = rowk[k];
+    if (!(piv > 0.0)) {
+      if (tid == 0) atomicExch(status, 1);
+    }
+    const double ip = 1.0 / piv;
+    for (size_t e = tid; e < (size_t)m * m; e += nth) {
+      const int i = (int)(e / m), j = (int)(e - (e / m) * m);
+      double v;
+      if (i == k && j == k) v = -ip;
+      else if (i == k) v = rowk[j] * ip;
+      else if (j == k) v = colk[i] * ip;
+      else v = A[e] - colk[i] * rowk[j] * ip;
+      A[e] = v;
+    }
+    __syncthreads();
+  }
+  for (size_t e = tid; e < (size_t)m * m; e += nth) A[e] = -A[e];
+}
+
+__global__ void k_copy_blocks(double** src, double** dst, int m) {
+  const double* s = src[blockIdx.y];
+  double* t = dst[blockIdx.y];
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)m * m;
+       e += (size_t)gridDim.x * blockDim.x)
+    t[e] = s[e];
+}
+
+// Batched C = alpha op(A) op(B) + beta C, m x m row-major blocks, 64x64 tiles.
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) k_gemm(double** As, double** Bs, double** Cs, int m,
+                                              double alpha, double beta) {
+  constexpr int BM = 64, BK = 16;
+  __shared__ double sA[BK][BM + 1];
+  __shared__ double sB[BK][BM + 1];
+  const double* A = As[blockIdx.z];
+  const double* B = Bs[blockIdx.z];
+  double* C = Cs[blockIdx.z];
+  const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BM;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < m; k0 += BK) {
+    for (int e = threadIdx.x; e < BK * BM; e += 256) {
+      const int kk = e / BM, rr = e - (e / BM) * BM;
+      const int gr = row0 + rr, gk = k0 + kk;
+      double va = 0.0, vb = 0.0;
+      if (gr < m && gk < m) va = TA ? A[(size_t)gk * m + gr] : A[(size_t)gr * m + gk];
+      const int gc = col0 + rr;
+      if (gc < m && gk < m) vb = TB ? B[(size_t)gc * m + gk] : B[(size_t)gk * m + gc];
+      sA[kk][rr] = va;
+      sB[kk][rr] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sA[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = sB[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = row0 + ty * 4 + i, cc = col0 + tx * 4 + j;
+      if (r < m && cc < m) {
+        const size_t o = (size_t)r * m + cc;
+        C[o] = alpha * acc[i][j] + (beta == 0.0 ? 0.0 : beta * C[o]);
+      }
+    }
+}
+
+__global__ void k_zero_blocks(double** dst, int m) {
+  double* t = dst[blockIdx.y];
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)m * m;
+       e += (size_t)gridDim.x * blockDim.x)
+    t[e] = 0.0;
+}
+
+// ------------------------------------------------------------------ cyclic-reduction solve
+// forward, survivors i: b_i -= Q_{i-s} b_{i-s} + P_{i+s} b_{i+s}   (warp per row)
+__global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restrict__ surv, int s,
+                                                    const double* __restrict__ Qall,
+                                                    const double* __restrict__ Pall,
+                                                    double* cball, const PcgScalars* sc,
+                                                    int rhs0, int gated) {
+  const int rhs = rhs0 + blockIdx.y;
+  if (gated && !sc[rhs].active) return;
+  extern __shared__ double sv[];  // [2][m]
+  const int m = d.mc;
+  const int i = surv[blockIdx.x];
+  double* cb = cball + (size_t)rhs * d.nbc * m;
+  const size_t per = (size_t)m * m;
+  const bool hl = i - s >= 0, hr = i + s < d.nbc;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
+    sv[k] = hl ? cb[(size_t)(i - s) * m + k] : 0.0;
+    sv[m + k] = hr ? cb[(size_t)(i + s) * m + k] : 0.0;
+  }
+  __syncthreads();
+  const double* Q = Qall + ((size_t)rhs * d.nbc + (i - s)) * per;
+  const double* P = Pall + ((size_t)rhs * d.nbc + (i + s)) * per;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = wid; r < m; r += nw) {
+    double acc = 0.0;
+    if (hl)
+      for (int c = lane; c < m; c += 32) acc = fma(Q[(size_t)r * m + c], sv[c], acc);
+    if (hr)
+      for (int c = lane; c < m; c += 32) acc = fma(P[(size_t)r * m + c], sv[m + c], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) cb[(size_t)i * m + r] -= acc;
+  }
+}
+
+// back, eliminated k: x_k = Dinv_k b_k - P_k^T x_{k-s} - Q_k^T x_{k+s}  (thread per row)
+__global__ void __launch_bounds__(256) k_cr_back(Dims d, const int* __restrict__ elim, int s,
+                                                 const double* __restrict__ Dinv,
+                                                 const double* __restrict__ Pall,
+                                                 const double* __restrict__ Qall,
+                                                 double* cball, const PcgScalars* sc, int rhs0,
+                                                 int gated) {
+  const int rhs = rhs0 + blockIdx.y;
+  if (gated && !sc[rhs].active) return;
+  extern __shared__ double sv[];  // [3][m]
+  const int m = d.mc;
+  const int k = elim[blockIdx.x];
+  double* cb = cball + (size_t)rhs * d.nbc * m;
+  const size_t per = (size_t)m * m;
+  const bool hl = k - s >= 0, hr = k + s < d.nbc;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    sv[j] = cb[(size_t)k * m + j];
+    sv[m + j] = hl ? cb[(size_t)(k - s) * m + j] : 0.0;
+    sv[2 * m + j] = hr ? cb[(size_t)(k + s) * m + j] : 0.0;
+  }
+  __syncthreads();
+  const double* Di = Dinv + ((size_t)rhs * d.nbc + k) * per;
+  const double* P = Pall + ((size_t)rhs * d.nbc + k) * per;
+  const double* Q = Qall + ((size_t)rhs * d.nbc + k) * per;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < m; ++c) acc = fma(Di[(size_t)c * m + r], sv[c], acc);   // Dinv symmetric
+    if (hl)
+      for (int c = 0; c < m; ++c) acc = fma(-P[(size_t)c * m + r], sv[m + c], acc);
+    if (hr)
+      for (int c = 0; c < m; ++c) acc = fma(-Q[(size_t)c * m + r], sv[2 * m + c], acc);
+    cb[(size_t)k * m + r] = acc;
+  }
+}
+
+}  // namespace
+
+// ================================================================== host side
+void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) {
+  k_restrict<<<dim3(c->d.n_agg, nr), NT, 0, c->stream>>>(c->d, (const double2*)t, c->phi,
+                                                         c->cls_of_agg_d, c->cb, c->sc, rhs0,
+                                                         gated ? 1 : 0);
+  MSF_LAUNCHED(c);
+}
+
+void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
+  const Dims& d = c->d;
+  dim3 g((d.nny + 31) / 32, (d.nnx + 7) / 8, nr);
+  k_prolong<<<g, NT, 0, c->stream>>>(d, c->phi, c->cls_of_agg_d, c->cb, (double2*)z, c->sc,
+                                     rhs0, gated ? 1 : 0);
+  MSF_LAUNCHED(c);
+}
+
+void launch_coarse_galerkin(msf_ctx* c) {
+  const Dims& d = c->d;
+  const int P = 4 * d.kmax;
+  const size_t smem = ((size_t)(d.cx + 1) * (d.cy + 1) * 2 * P + 16 * 8 * P + 16) * sizeof(double);
+  cudaFuncSetAttribute(k_cell_galerkin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_cell_galerkin<<<dim3(d.ncx * d.ncy, d.R), NT, smem, c->stream>>>(d, c->K0, c->E, c->phi,
+                                                                     c->cls_of_agg_d, c->Kcell);
+  MSF_LAUNCHED(c);
+  {
+    const size_t total = (size_t)2 * d.nbc * d.mc * d.mc;
+    int blocks = (int)std::min<size_t>((total + 255) / 256, 65535);
+    k_coarse_gather<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->Kcell, c->cls_of_agg_d,
+                                                              c->classes_d, c->Dc, c->Uc);
+    MSF_LAUNCHED(c);
+  }
+}
+
+void launch_assemble_coarse(msf_ctx* c) {
+  launch_coarse_galerkin(c);
+  const Dims& d = c->d;
+  const int m = d.mc;
+  const size_t inv_smem = 2 * (size_t)m * sizeof(double);
+  const dim3 gt((m + 63) / 64, (m + 63) / 64);
+  for (const CrLevel& L : c->cr) {
+    k_copy_blocks<<<dim3(64, L.n_inv), 256, 0, c->stream>>>(L.invsrc, L.inv, m);
+    MSF_LAUNCHED(c);
+    k_spd_inverse<<<L.n_inv, 1024, inv_smem, c->stream>>>(L.inv, m, c->factor_status);
+    MSF_LAUNCHED(c);
+    if (L.s == 0) continue;
+    if (L.nP) {
+      k_gemm<false, false><<<dim3(gt.x, gt.y, L.nP), 256, 0, c->stream>>>(L.pA, L.pB, L.pC, m, 1.0, 0.0);
+      MSF_LAUNCHED(c);
+    }
+    if (L.nQ) {
+      k_gemm<true, false><<<dim3(gt.x, gt.y, L.nQ), 256, 0, c->stream>>>(L.qA, L.qB, L.qC, m, 1.0, 0.0);
+      MSF_LAUNCHED(c);
+    }
+    if (L.nDl) {
+      k_gemm<false, true><<<dim3(gt.x, gt.y, L.nDl), 256, 0, c->stream>>>(L.dlA, L.dlB, L.dlC, m, -1.0, 1.0);
+      MSF_LAUNCHED(c);
+    }
+    if (L.nDr) {
+      k_gemm<false, false><<<dim3(gt.x, gt.y, L.nDr), 256, 0, c->stream>>>(L.drA, L.drB, L.drC, m, -1.0, 1.0);
+      MSF_LAUNCHED(c);
+    }
+    if (L.nU) {
+      k_gemm<false, false><<<dim3(gt.x, gt.y, L.nU), 256, 0, c->stream>>>(L.uA, L.uB, L.uC, m, -1.0, 0.0);
+      MSF_LAUNCHED(c);
+    }
+  }
+}
+
+// c <- K_c^{-1} c for realisations [rhs0, rhs0+nr): forward elimination over the levels,
+// final block, back substitution in reverse level order.
+void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
+  const Dims& d = c->d;
+  const int m = d.mc;
+  const int nthr = 256;
+  for (const CrLevel& L : c->cr) {
+    if (L.s == 0) continue;
+    if (!L.surv.empty()) {
+      k_cr_forward<<<dim3((unsigned)L.surv.size(), nr), nthr, 2 * m * sizeof(double), c->stream>>>(
+          d, L.surv_d, L.s, c->Qc, c->Pc, c->cb, c->sc, rhs0, gated ? 1 : 0);
+      MSF_LAUNCHED(c);
+    }
+  }
+  // final level: x_0 = Dinv_0 b_0 (k_cr_back with no neighbours: s = nbc)
+  for (auto it = c->cr.rbegin(); it != c->cr.rend(); ++it) {
+    const CrLevel& L = *it;
+    const int s = L.s == 0 ? d.nbc : L.s;
+    k_cr_back<<<dim3((unsigned)L.elim.size(), nr), nthr, 3 * m * sizeof(double), c->stream>>>(
+        d, L.elim_d, s, c->Dinv, c->Pc, c->Qc, c->cb, c->sc, rhs0, gated ? 1 : 0);
+    MSF_LAUNCHED(c);
+  }
+}

@@ -1,0 +1,195 @@
+// Internal declarations of the B200 MsFEM-PCG library (not part of the C ABI).
+// Design notes: DESIGN.md.  Paper citations: PAPER.md line numbers (arxiv 1411.3923).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/msfem_b200.h"
+
+#define MSF_MAX_BLOCK_EIG 24   // subspace-iteration block size cap (n_modes + guard)
+
+// Q4 plane-stress element matrix for unit modulus, passed by value so that the unrolled
+// stencil loops read it from the kernel-parameter constant bank (Eq. 5: K0).
+struct K0Mat {
+  double v[64];
+};
+
+// Grid geometry passed by value to every kernel.
+struct Dims {
+  int nelx, nely;      // fine elements
+  int nnx, nny;        // nodes per direction (nelx+1, nely+1)
+  int nn, ne;          // node / element counts
+  int tile_x, tile_y;  // design tile
+  int nt;              // tile size
+  int cx, cy;          // fine elements per coarse cell
+  int ncx, ncy;        // coarse cells per direction
+  int kmax;            // eigen-slots per agglomerate
+  int bx, by;          // padded agglomerate box in nodes (2cx+1, 2cy+1)
+  int box_nodes;       // bx*by
+  int n_agg;           // (ncx+1)*(ncy+1)
+  int mc;              // coarse block size (ncy+1)*kmax
+  int nbc;             // coarse blocks (ncx+1)
+  int R;               // realisations
+};
+
+// Per-realisation PCG scalars living in device memory (reading R9).
+struct PcgScalars {
+  double rz;      // r.z of the current iterate
+  double pq;      // p.Ap
+  double rr;      // ||r||^2
+  double fnorm2;  // ||f||^2
+  double alpha, beta;
+  double tol2;    // tol^2
+  double comp;    // compliance f.u
+  int iters;
+  int active;     // 1 while iterating
+  int max_it;
+  int noconv;
+};
+
+// Per-class eigen-solve bookkeeping (device).
+struct EigClass {
+  int rep_agg;      // representative agglomerate index
+  int bx0, by0;     // clipped box origin (global node coords)
+  int nbx, nby;     // clipped box nodes per direction
+  long long off;    // offset (doubles) of this class's work area
+  int iters;        // subspace iterations used (written by the kernel)
+  int nkept;        // kept modes (written by the kernel)
+};
+
+// One level of the coarse block cyclic reduction.  Pointer tables (device) cover all
+// realisations; index lists (device) are per realisation.
+struct CrLevel {
+  int s = 0;                   // stride 2^l; 0 marks the final single-block level
+  std::vector<int> elim;       // eliminated blocks (host copy)
+  std::vector<int> surv;       // survivors with an eliminated neighbour (host copy)
+  int* elim_d = nullptr;
+  int* surv_d = nullptr;
+  int n_inv = 0;  double** inv = nullptr;  double** invsrc = nullptr;
+  int nP = 0;     double** pA = nullptr;   double** pB = nullptr;  double** pC = nullptr;
+  int nQ = 0;     double** qA = nullptr;   double** qB = nullptr;  double** qC = nullptr;
+  int nDl = 0;    double** dlA = nullptr;  double** dlB = nullptr; double** dlC = nullptr;
+  int nDr = 0;    double** drA = nullptr;  double** drB = nullptr; double** drC = nullptr;
+  int nU = 0;     double** uA = nullptr;   double** uB = nullptr;  double** uC = nullptr;
+};
+
+struct msf_ctx {
+  msf_problem p{};
+  Dims d{};
+  K0Mat K0{};
+  cudaStream_t stream = nullptr;
+  std::string err;
+  size_t ws_bytes = 0;
+  char* ws = nullptr;
+
+  // host plan
+  std::vector<int> cls_of_agg;
+  std::vector<EigClass> classes;
+  int n_cls = 0;
+  int mb = 0;  // eigensolver block size
+  long long eig_work_doubles = 0;
+  std::vector<CrLevel> cr;
+  std::vector<int> filt_dx, filt_dy;
+  std::vector<double> filt_w;
+  bool periodic = false;
+
+  // device buffers (carved from the workspace)
+  uint8_t* fixn = nullptr;      // per-node bitmask: bit0 x fixed, bit1 y fixed
+  double* f = nullptr;          // load [2*nn]
+  double* x_tile = nullptr;     // design [nt]
+  double* xt_tile = nullptr;    // filtered [nt]
+  double* xbar_tile = nullptr;  // projected [R*nt]
+  double* E = nullptr;          // element moduli [R*ne]
+  double* u = nullptr;          // solutions [R*2nn]
+  double* r = nullptr;
+  double* z = nullptr;
+  double* pv = nullptr;
+  double* q = nullptr;
+  double* t = nullptr;
+  double* tile_tmp = nullptr;   // [4*nt] scratch (sensitivities / OC)
+  double* dc_el = nullptr;      // [ne] scratch
+  double* dF = nullptr;         // [nt]
+  double* dg = nullptr;         // [nt]
+  double* x_new = nullptr;      // [nt] staging for the host entry point
+  int* filt_dx_d = nullptr;
+  int* filt_dy_d = nullptr;
+  double* filt_w_d = nullptr;
+  int n_filt = 0;
+  double filt_wsum = 1.0;
+
+  int* cls_of_agg_d = nullptr;
+  EigClass* classes_d = nullptr;
+  double* phi = nullptr;        // [n_cls][kmax][box_nodes][2]
+  double* lam = nullptr;        // [n_cls][kmax]
+  double* eig_work = nullptr;
+  int* nkept_agg = nullptr;     // [n_agg] (per agglomerate, from its class)
+
+  double* Kcell = nullptr;      // [R][ncells][(4k)^2]
+  double* Dc = nullptr;         // [R][nbc][mc*mc]
+  double* Uc = nullptr;         // [R][nbc][mc*mc]
+  double* Dinv = nullptr;       // [R][nbc][mc*mc]
+  double* Pc = nullptr;         // [R][nbc][mc*mc]
+  double* Qc = nullptr;         // [R][nbc][mc*mc]
+  double* cb = nullptr;         // [R][nbc*mc] coarse rhs / solution
+  char* jobs_d = nullptr;       // CR job tables
+  int* factor_status = nullptr; // [R] nonzero on failed pivot
+
+  PcgScalars* sc = nullptr;     // [R]
+  double* partials = nullptr;   // [R][max_blocks]
+  unsigned* counters = nullptr; // [R*8]
+  int max_partials = 0;
+  double* scal = nullptr;       // misc device scalars [64]
+
+  PcgScalars* sc_host = nullptr;  // pinned mirror
+  double* scal_host = nullptr;    // pinned [64]
+
+  // state
+  bool have_E = false, have_basis = false, have_coarse = false, have_solution = false;
+  int last_iters[MSF_MAX_RHS] = {0, 0, 0, 0};
+  long long launches = 0;
+  long long pcg_launches = 0;
+  int eig_iters_used = 0;
+
+  cudaGraphExec_t iter_graph = nullptr;
+  int iter_graph_R = -1;
+};
+
+// ---------------------------------------------------------------- launch bookkeeping
+#define MSF_LAUNCHED(ctx) ((ctx)->launches++)
+
+// ---------------------------------------------------------------- kernels (fem / pcg)
+void launch_matvec(msf_ctx* c, int rhs0, int nr, const double* x, double* y, bool gated,
+                   bool dot_pq);
+void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double* x, double* y,
+                     bool gated);
+void launch_sgs(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated);
+void launch_mask_copy(msf_ctx* c, const double* x, double* y, int n2nn);
+void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it);
+void launch_pcg_update_xr(msf_ctx* c, int nr);
+void launch_pcg_rz(msf_ctx* c, int nr, bool init);
+void launch_pcg_p(msf_ctx* c, int nr, bool init);
+void launch_compliance(msf_ctx* c, int nr);
+
+// ---------------------------------------------------------------- filter / design
+void launch_filter_project(msf_ctx* c, const double* x_tile);
+void launch_set_physical(msf_ctx* c, int rhs, const double* xbar_el);
+void launch_sensitivities(msf_ctx* c, double kappa, double volfrac);
+void launch_oc(msf_ctx* c, const double* x, const double* dF, const double* dg, double volfrac,
+               double move, double* x_new);
+
+// ---------------------------------------------------------------- coarse space
+void launch_build_basis(msf_ctx* c);
+void launch_assemble_coarse(msf_ctx* c);
+void launch_coarse_galerkin(msf_ctx* c);
+void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated);
+void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated);
+void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated);
+
+// ---------------------------------------------------------------- helpers
+int msf_fail(msf_ctx* c, int code, const std::string& msg);
+int msf_cuda_check(msf_ctx* c, cudaError_t e, const char* where);
+K0Mat make_K0(double nu);

@@ -1,0 +1,352 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded
+inputs.  Tolerances: operators element-wise 1e-12 relative; basis
+spans (principal angles) 1e-7; PCG iteration counts +-1 at tol 1e-8, relative displacement
+error <= 1e-8 and relative compliance error <= 1e-10 at the solve tolerance 1e-12."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import design, fem, filters, msfem, pcg, problem
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU, skipped there
+    pytest.skip("no GPU", allow_module_level=True)
+
+from paper_1411_3923_b200 import Msfem, build  # noqa: E402
+
+build.build()
+DEV = torch.device("cuda")
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=DEV)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def ctx_for(spec, x=None):
+    m = Msfem.from_spec(spec)
+    x = W.design_tile(spec) if x is None else x
+    m.filter_project(dev(x))
+    return m, x
+
+
+def oracle_setup(spec, x):
+    fx, f = W.fixed_mask(spec), W.load_vector(spec)
+    K0 = fem.element_stiffness(spec.nu)
+    xt, xbars, xb_el, E = problem.element_moduli(spec, x)
+    A = [fem.constrained_operator(fem.assemble(spec.nelx, spec.nely, e, K0), fx) for e in E]
+    return fx, f, K0, E, A, xbars
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+SPECS = {
+    "cant_16x8": W.small_spec(nelx=16, nely=8, cx=4, cy=4, seed=21),
+    "mbb_24x12": W.small_spec(nelx=24, nely=12, cx=4, cy=4, bc="mbb", seed=22),
+    "robust_32x16": W.small_spec(nelx=32, nely=16, cx=8, cy=8, tile=(8, 8), rmin=2.5, beta=8.0,
+                                 etas=(0.7, 0.5, 0.3), dilated=2, bc="mbb", seed=23, Emin=1e-6),
+    "ragged_36x20": W.small_spec(nelx=36, nely=20, cx=4, cy=4, tile=(12, 10), rmin=1.5, beta=4.0,
+                                 etas=(0.6, 0.4), dilated=1, seed=24, n_modes=5),
+}
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_filter_project_moduli(name):
+    spec = SPECS[name]
+    m, x = ctx_for(spec)
+    fx, f, K0, E, A, xbars = oracle_setup(spec, x)
+    for k in range(spec.n_rhs):
+        Eg = torch.empty(spec.n_el, dtype=torch.float64, device=DEV)
+        xb = torch.empty(spec.tile_x * spec.tile_y, dtype=torch.float64, device=DEV)
+        m.get_physical(k, Eg, xb)
+        assert np.abs(host(xb) - xbars[k]).max() <= 1e-14
+        assert rel(host(Eg), E[k]) <= 1e-14
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_matvec(name):
+    spec = SPECS[name]
+    m, x = ctx_for(spec)
+    fx, f, K0, E, A, _ = oracle_setup(spec, x)
+    V = W.random_vectors(spec.n_dof, 3, seed=5)
+    for k in range(spec.n_rhs):
+        for v in V:
+            y = torch.empty(spec.n_dof, dtype=torch.float64, device=DEV)
+            m.matvec(k, dev(v), y)
+            ref = A[k] @ v
+            assert np.abs(host(y) - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name", ["cant_16x8", "mbb_24x12", "ragged_36x20"])
+def test_symmetric_gauss_seidel(name):
+    spec = SPECS[name]
+    m, x = ctx_for(spec)
+    fx, f, K0, E, A, _ = oracle_setup(spec, x)
+    groups = msfem.gs_groups(spec.nelx, spec.nely, fx)
+    r, z0 = W.random_vectors(spec.n_dof, 2, seed=6)
+    r[fx == 1] = 0
+    z0[fx == 1] = 0
+    z = dev(z0)
+    m.sgs(0, dev(r), z)
+    ref = msfem.symmetric_gauss_seidel(A[0], z0, r, groups)
+    assert np.abs(host(z) - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def gpu_basis_matrix(m, spec):
+    """Dense R_c rows (kept modes only) from the GPU's padded-box basis."""
+    phi, nk, lam = m.get_basis()
+    ncx, ncy = spec.nelx // spec.cx, spec.nely // spec.cy
+    rows, info = [], []
+    for I in range(ncx + 1):
+        for J in range(ncy + 1):
+            agg = I * (ncy + 1) + J
+            for a in range(nk[agg]):
+                v = np.zeros(spec.n_dof)
+                P = phi[agg, a]
+                for px in range(2 * spec.cx + 1):
+                    ix = I * spec.cx - spec.cx + px
+                    if ix < 0 or ix > spec.nelx:
+                        continue
+                    for py in range(2 * spec.cy + 1):
+                        iy = J * spec.cy - spec.cy + py
+                        if iy < 0 or iy > spec.nely:
+                            continue
+                        n = ix * (spec.nely + 1) + iy
+                        v[2 * n:2 * n + 2] = P[px, py]
+                rows.append(v)
+                info.append((I, J, a))
+    return np.array(rows), nk, lam
+
+
+def span_distance(A, B):
+    """max principal-angle sine between row spaces of A and B."""
+    Qa, _ = np.linalg.qr(A.T)
+    Qb, _ = np.linalg.qr(B.T)
+    s = np.linalg.svd(Qa.T @ Qb, compute_uv=False)
+    return np.sqrt(max(0.0, 1.0 - s.min() ** 2))
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_coarse_basis_spans_and_eigenvalues(name):
+    spec = SPECS[name]
+    m, x = ctx_for(spec)
+    m.build_coarse_basis()
+    fx, f, K0, E, A, _ = oracle_setup(spec, x)
+    Rg, nk, lam = gpu_basis_matrix(m, spec)
+    ncx, ncy = spec.nelx // spec.cx, spec.nely // spec.cy
+    for I in range(ncx + 1):
+        for J in range(ncy + 1):
+            agg = I * (ncy + 1) + J
+            Kl, D, gdof, dix, diy = msfem.local_problem(I, J, spec.nelx, spec.nely, spec.cx,
+                                                       spec.cy, E[spec.dilated], K0, fx)
+            lo, psi = msfem.local_eigenpairs(Kl, D, spec.n_modes)
+            assert nk[agg] == spec.n_modes
+            scale = max(1.0, abs(lo).max())
+            assert np.abs(lam[agg] - lo).max() <= 1e-9 * scale
+            chi = msfem.partition_of_unity(I, J, dix, diy, spec.cx, spec.cy)
+            ref = np.zeros((psi.shape[1], spec.n_dof))
+            ref[:, gdof] = (chi[:, None] * psi).T
+            start = sum(nk[:agg])
+            got = Rg[start:start + nk[agg]]
+            assert span_distance(got, ref) <= 1e-7, (I, J)
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_galerkin_coarse_matrix(name):
+    """K_c blocks equal R_g A R_g^T computed by the oracle's sparse product from the
+    GPU basis (checks the per-cell dense contraction and the block gather)."""
+    spec = SPECS[name]
+    m, x = ctx_for(spec)
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    fx, f, K0, E, A, _ = oracle_setup(spec, x)
+    Rg, nk, lam = gpu_basis_matrix(m, spec)
+    ncy = spec.nely // spec.cy
+    km = spec.n_modes
+    for k in range(spec.n_rhs):
+        D, U = m.get_coarse_blocks(k)
+        Kc = Rg @ (A[k] @ Rg.T)
+        slots = []
+        for I in range(spec.nelx // spec.cx + 1):
+            for J in range(ncy + 1):
+                for a in range(nk[I * (ncy + 1) + J]):
+                    slots.append((I, J * km + a))
+        sc = np.abs(Kc).max()
+        for p, (Ip, rp) in enumerate(slots):
+            for q, (Iq, rq) in enumerate(slots):
+                if Iq == Ip:
+                    g = D[Ip][rp, rq]
+                elif Iq == Ip + 1:
+                    g = U[Ip][rp, rq]
+                elif Ip == Iq + 1:
+                    g = U[Iq][rq, rp]
+                else:
+                    assert abs(Kc[p, q]) <= 1e-13 * sc
+                    continue
+                assert abs(g - Kc[p, q]) <= 1e-12 * sc
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_coarse_solve(name):
+    spec = SPECS[name]
+    m, x = ctx_for(spec)
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    inf = m.info()
+    nb, mm = inf["ncx"] + 1, inf["m"]
+    for k in range(spec.n_rhs):
+        D, U = m.get_coarse_blocks(k)
+        Kc = np.zeros((nb * mm, nb * mm))
+        for I in range(nb):
+            Kc[I * mm:(I + 1) * mm, I * mm:(I + 1) * mm] = D[I]
+            if I + 1 < nb:
+                Kc[I * mm:(I + 1) * mm, (I + 1) * mm:(I + 2) * mm] = U[I]
+                Kc[(I + 1) * mm:(I + 2) * mm, I * mm:(I + 1) * mm] = U[I].T
+        b = W.random_vectors(nb * mm, 1, seed=9)[0]
+        c = torch.empty(nb * mm, dtype=torch.float64, device=DEV)
+        m.coarse_solve(k, dev(b), c)
+        ref = np.linalg.solve(Kc, b)
+        assert rel(host(c), ref) <= 1e-9
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_two_level_preconditioner(name):
+    spec = SPECS[name]
+    m, x = ctx_for(spec)
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    fx, f, K0, E, A, _ = oracle_setup(spec, x)
+    R, _ = msfem.build_coarse_basis(spec.nelx, spec.nely, spec.cx, spec.cy, spec.n_modes,
+                                    E[spec.dilated], K0, fx)
+    groups = msfem.gs_groups(spec.nelx, spec.nely, fx)
+    for k in range(spec.n_rhs):
+        M = msfem.TwoLevelPreconditioner(A[k], R, groups, fx)
+        r = W.random_vectors(spec.n_dof, 1, seed=10 + k)[0]
+        r[fx == 1] = 0
+        z = torch.empty(spec.n_dof, dtype=torch.float64, device=DEV)
+        m.precond_apply(k, dev(r), z)
+        assert rel(host(z), M(r)) <= 1e-7
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_pcg_parity(name):
+    spec = SPECS[name]
+    m, x = ctx_for(spec)
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    fx, f = W.fixed_mask(spec), W.load_vector(spec)
+    ref = problem.solve(spec, x, fx, f, tol=1e-8)
+    its, comps, noconv = m.pcg_solve(tol=1e-8)
+    assert not noconv
+    for k in range(spec.n_rhs):
+        assert abs(its[k] - ref["iters"][k]) <= 1, (its, ref["iters"])
+    # tight solve: displacement and compliance parity
+    ref = problem.solve(spec, x, fx, f, tol=1e-12)
+    u = torch.empty(spec.n_rhs * spec.n_dof, dtype=torch.float64, device=DEV)
+    its, comps, noconv = m.pcg_solve(tol=1e-12, u=u)
+    ug = host(u).reshape(spec.n_rhs, spec.n_dof)
+    for k in range(spec.n_rhs):
+        assert rel(ug[k], ref["us"][k]) <= 1e-8
+        assert abs(comps[k] - ref["comps"][k]) <= 1e-10 * abs(ref["comps"][k])
+
+
+def test_config0_full_size_pcg():
+    """BASELINE configs[0] (96x48 cantilever, iid densities, 8x8 coarse cells, 4 modes),
+    single fp64 PCG solve to relative residual 1e-8."""
+    spec = W.CONFIGS["c0_cantilever_96x48"]
+    m, x = ctx_for(spec)
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    fx, f = W.fixed_mask(spec), W.load_vector(spec)
+    ref = problem.solve(spec, x, fx, f, tol=spec.tol)
+    its, comps, noconv = m.pcg_solve(tol=spec.tol)
+    assert abs(its[0] - ref["iters"][0]) <= 1
+    u = torch.empty(spec.n_dof, dtype=torch.float64, device=DEV)
+    its, comps, _ = m.pcg_solve(tol=1e-12, u=u)
+    ref = problem.solve(spec, x, fx, f, tol=1e-12)
+    assert rel(host(u), ref["us"][0]) <= 1e-8
+    assert abs(comps[0] - ref["comps"][0]) <= 1e-10 * ref["comps"][0]
+
+
+@pytest.mark.parametrize("name", ["robust_32x16", "ragged_36x20"])
+def test_sensitivities_and_oc(name):
+    spec = SPECS[name].replace(volfrac=0.5)
+    m, x = ctx_for(spec)
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    fx, f = W.fixed_mask(spec), W.load_vector(spec)
+    ref = problem.solve(spec, x, fx, f, tol=1e-12)
+    F, c, g, dF, dg = design.design_gradients(spec, x, ref["us"], f, ref["K0"])
+    m.pcg_solve(tol=1e-12)
+    nt = spec.tile_x * spec.tile_y
+    dFg = torch.empty(nt, dtype=torch.float64, device=DEV)
+    dgg = torch.empty(nt, dtype=torch.float64, device=DEV)
+    Fg, gg, cg = m.sensitivities(kappa=spec.kappa, volfrac=spec.volfrac, dF=dFg, dg=dgg)
+    assert abs(Fg - F) <= 1e-10 * abs(F)
+    assert abs(gg - g) <= 1e-12
+    assert np.abs(host(dFg) - dF).max() <= 1e-8 * np.abs(dF).max()
+    assert np.abs(host(dgg) - dg).max() <= 1e-12 * np.abs(dg).max()
+    xn = torch.empty(nt, dtype=torch.float64, device=DEV)
+    m.oc_update(dev(x), dFg, dgg, volfrac=spec.volfrac, move=0.2, x_new=xn)
+    ref_x = design.oc_update(spec, x, dF, dg)
+    assert np.abs(host(xn) - ref_x).max() <= 1e-6
+
+
+def test_design_iteration_host_equals_device():
+    spec = SPECS["robust_32x16"]
+    m, x = ctx_for(spec)
+    xn_d = torch.empty(spec.tile_x * spec.tile_y, dtype=torch.float64, device=DEV)
+    its_d, comp_d, F_d, g_d = m.design_iteration(dev(x), xn_d, tol=1e-10)
+    xh = torch.as_tensor(x).pin_memory()
+    xn_h = torch.empty(spec.tile_x * spec.tile_y, dtype=torch.float64).pin_memory()
+    its_h, comp_h, F_h, g_h = m.design_iteration_host(xh, xn_h, tol=1e-10)
+    assert its_d == its_h and comp_d == comp_h and F_d == F_h
+    assert np.array_equal(host(xn_d), xn_h.numpy())
+
+
+def test_periodic_classes_dedup():
+    """Periodic tile: far fewer eigen-solves than agglomerates (§2.4.1), and the
+    result equals the non-deduplicated solve of the same field."""
+    spec = W.small_spec(nelx=64, nely=32, cx=8, cy=8, tile=(16, 16), rmin=2.0, beta=4.0,
+                        etas=(0.5,), seed=31, Emin=1e-6)
+    m, x = ctx_for(spec)
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    inf = m.info()
+    assert inf["n_classes"] < inf["n_agg"] // 2
+    fx, f = W.fixed_mask(spec), W.load_vector(spec)
+    ref = problem.solve(spec, x, fx, f, tol=1e-8)
+    its, comps, _ = m.pcg_solve(tol=1e-8)
+    assert abs(its[0] - ref["iters"][0]) <= 1
+
+
+def test_threshold_mode_contrast_flat():
+    """lambda_Omega selection: counts match the oracle, and iteration
+    counts stay flat over contrasts 1e-3..1e-9 for a connected binary microstructure."""
+    base = W.small_spec(nelx=64, nely=32, cx=8, cy=8, tile=(32, 16), design="binary",
+                        n_modes=16, seed=41, lam_threshold=5e-3)
+    x = W.design_tile(base)
+    fx, f = W.fixed_mask(base), W.load_vector(base)
+    its = []
+    for Emin in (1e-3, 1e-6, 1e-9):
+        spec = base.replace(Emin=Emin)
+        m, _ = ctx_for(spec, x)
+        m.build_coarse_basis()
+        _, nk, lam = m.get_basis()
+        m.assemble_coarse()
+        ref = problem.solve(spec, x, fx, f, tol=1e-8)
+        ncy = spec.nely // spec.cy
+        for (I, J), lo in ref["eigvals"].items():
+            assert nk[I * (ncy + 1) + J] == lo.size
+        it, _, _ = m.pcg_solve(tol=1e-8)
+        assert abs(it[0] - ref["iters"][0]) <= 1
+        its.append(it[0])
+    assert max(its) - min(its) <= 0.2 * max(its) + 2
