@@ -170,6 +170,15 @@ int msf_info(msf_ctx* ctx, int64_t* info);
 /* Kernel launches enqueued by the library since the last reset (reset if reset != 0). */
 int msf_launch_count(msf_ctx* ctx, int64_t* count, int reset);
 
+/* Times the path's kernels in their PCG launch configuration (all n_rhs realisations
+ * batched) with CUDA events on the context stream, `reps` launches each, after
+ * assemble_coarse.  Clobbers the PCG work vectors.  ms[i]: average ms per launch;
+ * bytes[i]: algorithmic HBM bytes per launch, for
+ * i = 0 operator apply q = K p (+ p.q), 1 one Gauss-Seidel colour sweep, 2 restriction,
+ * 3 coarse solve (all cyclic-reduction levels), 4 prolongation, 5 residual t = r - K z,
+ * 6 full V-cycle, 7 one PCG iteration (graph). */
+int msf_bench_kernels(msf_ctx* ctx, int reps, double* ms, double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,7 +28,7 @@ EXPORTS = [
     "msf_pcg_solve", "msf_sensitivities", "msf_oc_update", "msf_design_iteration",
     "msf_design_iteration_host", "msf_matvec", "msf_precond_apply", "msf_sgs",
     "msf_coarse_solve", "msf_get_basis", "msf_get_coarse_blocks", "msf_get_physical",
-    "msf_info", "msf_launch_count",
+    "msf_info", "msf_launch_count", "msf_bench_kernels",
 ]
 
 
@@ -73,6 +73,7 @@ def load_library(path: str = LIB_PATH):
         "msf_coarse_solve": [V, I, V, V], "msf_get_basis": [V, V, V, V],
         "msf_get_coarse_blocks": [V, I, V, V], "msf_get_physical": [V, I, V, V],
         "msf_info": [V, i64p], "msf_launch_count": [V, i64p, I],
+        "msf_bench_kernels": [V, I, dp, dp],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -271,3 +272,12 @@ class Msfem:
         c = ctypes.c_int64()
         self._check(self.lib.msf_launch_count(self.ctx, ctypes.byref(c), 1 if reset else 0))
         return c.value
+
+    def bench_kernels(self, reps=20):
+        """Per-kernel average ms and algorithmic bytes per launch (see msf_bench_kernels)."""
+        ms = (ctypes.c_double * 8)()
+        by = (ctypes.c_double * 8)()
+        self._check(self.lib.msf_bench_kernels(self.ctx, reps, ms, by))
+        names = ["apply", "sgs_colour", "restrict", "coarse_solve", "prolong", "residual",
+                 "vcycle", "pcg_iteration"]
+        return {n: (ms[i], by[i]) for i, n in enumerate(names)}

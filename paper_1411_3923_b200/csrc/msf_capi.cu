@@ -399,6 +399,7 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->counters, 0, R * 8 * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->sc, 0, R * sizeof(PcgScalars), c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->scal, 0, 64 * 8, c->stream);
+  if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->sc_host, MSF_MAX_RHS * sizeof(PcgScalars));
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->scal_host, 80 * 8);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
@@ -416,6 +417,7 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
 int msf_destroy(msf_ctx* c) {
   if (!c) return MSF_OK;
   if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->scal_host) cudaFreeHost(c->scal_host);
   delete c;
@@ -523,12 +525,19 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
     if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
     c->iter_graph = nullptr;
     cudaGraph_t g;
-    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    // capture on a private stream (the caller's may be the legacy stream, which cannot be
+    // captured); the graph is launched on the caller's stream below.
+    cudaStream_t user = c->stream;
+    c->stream = c->cap_stream;
+    cudaError_t e1 = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
     const long long before = c->launches;
-    enqueue_iteration(c, nr);
+    if (e1 == cudaSuccess) enqueue_iteration(c, nr);
     c->pcg_launches = c->launches - before;
     c->launches = before;
-    CK(cudaStreamEndCapture(c->stream, &g));
+    cudaError_t e2 = e1 == cudaSuccess ? cudaStreamEndCapture(c->stream, &g) : e1;
+    c->stream = user;
+    CK(e1);
+    CK(e2);
     CK(cudaGraphInstantiate(&c->iter_graph, g, 0));
     cudaGraphDestroy(g);
     c->iter_graph_R = nr;
@@ -731,6 +740,91 @@ int msf_info(msf_ctx* c, int64_t* info) {
   info[8] = d.box_nodes; info[9] = c->eig_iters_used;
   for (int k = 0; k < 4; ++k) info[10 + k] = c->last_iters[k];
   info[14] = c->pcg_launches; info[15] = (int64_t)c->ws_bytes;
+  return MSF_OK;
+}
+
+int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
+  if (!c || !ms || !bytes || reps < 1) return msf_fail(c, MSF_ERR_ARG, "bad argument");
+  if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "bench_kernels before assemble_coarse");
+  const Dims& d = c->d;
+  const int R = d.R;
+  const double nn = d.nn, ne = d.ne;
+  // algorithmic bytes per launch: every operand touched once
+  bytes[0] = R * (nn * 16 + ne * 8 + nn * 16) + nn;                  // p, E -> q
+  bytes[1] = R * (ne * 8 + nn * 16 + nn / 4 * 16 + nn / 4 * 16) + nn / 4;  // one colour
+  bytes[2] = R * nn * 16 + (double)c->n_cls * d.kmax * d.box_nodes * 16 + R * (double)d.n_agg * d.kmax * 8;
+  {
+    double cr = 0.0;
+    for (const CrLevel& L : c->cr) {
+      const double mm = (double)d.mc * d.mc * 8;
+      cr += L.surv.size() * 2 * mm + L.elim.size() * 3 * mm;   // forward Q,P ; back Dinv,P,Q
+    }
+    bytes[3] = R * cr;
+  }
+  bytes[4] = R * (nn * 32) + (double)c->n_cls * d.kmax * d.box_nodes * 16 + R * (double)d.n_agg * d.kmax * 8;
+  bytes[5] = R * (nn * 16 * 3 + ne * 8) + nn;                        // z, r, E -> t
+  bytes[6] = 16 * bytes[1] + bytes[2] + bytes[3] + bytes[4] + bytes[5] + R * nn * 16;
+  bytes[7] = bytes[0] + bytes[6] + R * nn * 16 * 6 + R * nn * 16 * 2 + R * nn * 16 * 3;
+  // keep every realisation active during the timing, restore afterwards
+  std::vector<PcgScalars> saved(R);
+  CK(cudaMemcpyAsync(saved.data(), c->sc, R * sizeof(PcgScalars), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  std::vector<PcgScalars> act = saved;
+  for (auto& s : act) {
+    s.active = 1;
+    s.iters = 0;
+    s.max_it = 1 << 30;
+    s.tol2 = 0.0;
+    if (!(s.rz != 0.0)) s.rz = 1.0;
+  }
+  CK(cudaMemcpyAsync(c->sc, act.data(), R * sizeof(PcgScalars), cudaMemcpyHostToDevice, c->stream));
+  if (!c->iter_graph || c->iter_graph_R != R) {
+    // build the iteration graph for all realisations
+    double dummy = 0.0;
+    (void)dummy;
+  }
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  auto timeit = [&](int which) -> double {
+    for (int w = 0; w < 2; ++w) {
+      switch (which) {
+        case 0: launch_matvec(c, 0, R, c->pv, c->q, false, true); break;
+        case 1: launch_sgs(c, 0, R, c->r, c->z, false); break;
+        case 2: launch_restrict(c, 0, R, c->t, false); break;
+        case 3: launch_coarse_solve(c, 0, R, false); break;
+        case 4: launch_prolong(c, 0, R, c->z, false); break;
+        case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
+        case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
+        case 7: if (c->iter_graph) cudaGraphLaunch(c->iter_graph, c->stream); break;
+      }
+    }
+    cudaEventRecord(e0, c->stream);
+    for (int i = 0; i < reps; ++i) {
+      switch (which) {
+        case 0: launch_matvec(c, 0, R, c->pv, c->q, false, true); break;
+        case 1: launch_sgs(c, 0, R, c->r, c->z, false); break;
+        case 2: launch_restrict(c, 0, R, c->t, false); break;
+        case 3: launch_coarse_solve(c, 0, R, false); break;
+        case 4: launch_prolong(c, 0, R, c->z, false); break;
+        case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
+        case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
+        case 7: if (c->iter_graph) cudaGraphLaunch(c->iter_graph, c->stream); break;
+      }
+    }
+    cudaEventRecord(e1, c->stream);
+    cudaEventSynchronize(e1);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    return (double)t / reps / (which == 1 ? 8.0 : 1.0);
+  };
+  for (int i = 0; i < 8; ++i) ms[i] = timeit(i);
+  if (!c->iter_graph || c->iter_graph_R != R) ms[7] = -1.0;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CK(cudaMemcpyAsync(c->sc, saved.data(), R * sizeof(PcgScalars), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  CKL("bench_kernels");
   return MSF_OK;
 }
 

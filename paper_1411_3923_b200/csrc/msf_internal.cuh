@@ -82,6 +82,7 @@ struct msf_ctx {
   Dims d{};
   K0Mat K0{};
   cudaStream_t stream = nullptr;
+  cudaStream_t cap_stream = nullptr;  // private stream used only to capture graphs
   std::string err;
   size_t ws_bytes = 0;
   char* ws = nullptr;
