@@ -238,7 +238,7 @@ def run_ours(args, spec):
 
     # ---- roofline of the dominant kernel (live CUDA-event timing, PCG launch config)
     kb = m.bench_kernels(reps=20)
-    per_iter_count = {"apply": 1, "sgs_colour": 16, "restrict": 1, "coarse_solve": 1,
+    per_iter_count = {"apply": 1, "sgs_colour": 2, "restrict": 1, "coarse_solve": 1,
                       "prolong": 1, "residual": 1}
     share = {k: kb[k][0] * n for k, n in per_iter_count.items()}
     dom = max(share, key=share.get)

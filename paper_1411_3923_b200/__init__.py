@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmsfem_b200.so")
+LIB_PATH = os.environ.get("MSF_LIB_PATH", os.path.join(HERE, "libmsfem_b200.so"))
 
 MSF_OK, MSF_ERR_ARG, MSF_ERR_CUDA, MSF_ERR_STATE, MSF_ERR_NOCONV, MSF_ERR_FACTOR, MSF_ERR_SPACE = \
     0, -1, -2, -3, -4, -5, -6

@@ -13,6 +13,8 @@
 #include "msf_internal.cuh"
 
 int apply_partials_needed(const Dims& d);
+int sgs_partials_needed(const Dims& d);
+int sgs_colour_partials_needed(const Dims& d);
 size_t eig_smem_bytes(int mlmax, int mb);
 
 static thread_local std::string g_err;
@@ -184,7 +186,8 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     P.cr.push_back(L);
   }
   P.jobs_bytes = align_up(ptrs * sizeof(double*)) + align_up(ints * sizeof(int));
-  P.max_partials = apply_partials_needed(d);
+  P.max_partials = std::max(apply_partials_needed(d),
+                            std::max(sgs_partials_needed(d), sgs_colour_partials_needed(d)));
 
   // workspace size
   const size_t R = d.R, nn = d.nn, ne = d.ne, nt = d.nt;
@@ -205,8 +208,9 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   add(P.classes.size() * d.kmax * 8);        // lam
   add((size_t)P.eig_doubles * 8);            // eig work
   add(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);     // Kcell
-  add(5 * R * d.nbc * (size_t)d.mc * d.mc * 8);           // Dc Uc Dinv Pc Qc
-  add(R * d.nbc * (size_t)d.mc * 8);         // cb
+  add(7 * R * d.nbc * (size_t)d.mc * d.mc * 8);           // Dc Uc Dinv Pc Qc PTc QTc
+  add(2 * R * d.nbc * (size_t)d.mc * 8);     // cb, cx
+  add((size_t)(3 * (d.n_agg + P.classes.size()) + d.n_agg) * 4);  // chunks, agg_by_cls
   add(P.jobs_bytes);
   add(2 * MSF_MAX_RHS * 4);                  // factor_status
   add(R * sizeof(PcgScalars));
@@ -302,9 +306,31 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   c->eig_work = (double*)take((size_t)P.eig_doubles * 8);
   c->Kcell = (double*)take(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);
   const size_t blk = R * d.nbc * (size_t)d.mc * d.mc;
-  double* cm = (double*)take(5 * blk * 8);
+  double* cm = (double*)take(7 * blk * 8);
   c->Dc = cm; c->Uc = cm + blk; c->Dinv = cm + 2 * blk; c->Pc = cm + 3 * blk; c->Qc = cm + 4 * blk;
-  c->cb = (double*)take(R * d.nbc * (size_t)d.mc * 8);
+  c->PTc = cm + 5 * blk; c->QTc = cm + 6 * blk;
+  c->cb = (double*)take(2 * R * d.nbc * (size_t)d.mc * 8);
+  c->cx = c->cb + R * d.nbc * (size_t)d.mc;
+  {
+    // restriction work list: agglomerates grouped by class, chunks of <= 16 per CTA
+    std::vector<std::vector<int>> members(c->n_cls);
+    for (int a = 0; a < d.n_agg; ++a) members[P.cls_of_agg[a]].push_back(a);
+    c->agg_by_cls_h.clear();
+    c->chunks_h.clear();
+    for (int k = 0; k < c->n_cls; ++k) {
+      const int base = (int)c->agg_by_cls_h.size();
+      c->agg_by_cls_h.insert(c->agg_by_cls_h.end(), members[k].begin(), members[k].end());
+      for (int s0 = 0; s0 < (int)members[k].size(); s0 += 16) {
+        c->chunks_h.push_back(k);
+        c->chunks_h.push_back(base + s0);
+        c->chunks_h.push_back(std::min(16, (int)members[k].size() - s0));
+      }
+    }
+    c->n_chunks = (int)c->chunks_h.size() / 3;
+    int* ib = (int*)take((size_t)(3 * (d.n_agg + P.classes.size()) + d.n_agg) * 4);
+    c->chunks_d = ib;
+    c->agg_by_cls_d = ib + 3 * (d.n_agg + P.classes.size());
+  }
   c->jobs_d = (char*)take(P.jobs_bytes);
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
   c->sc = (PcgScalars*)take(R * sizeof(PcgScalars));
@@ -395,6 +421,8 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_dy_d, P.fdy.data(), P.fdy.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->cls_of_agg_d, P.cls_of_agg.data(), d.n_agg * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->classes_d, P.classes.data(), c->n_cls * sizeof(EigClass), cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->chunks_d, c->chunks_h.data(), c->chunks_h.size() * 4, cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->agg_by_cls_d, c->agg_by_cls_h.data(), c->agg_by_cls_h.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->factor_status, 0, 2 * MSF_MAX_RHS * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->counters, 0, R * 8 * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->sc, 0, R * sizeof(PcgScalars), c->stream);
@@ -477,22 +505,21 @@ int msf_assemble_coarse(msf_ctx* c) {
 }
 
 // two-level V-cycle z = M^{-1} r for realisations [0, nr) (reading R8)
-static void enqueue_vcycle(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated) {
-  const size_t vb = (size_t)2 * c->d.nn * 8;
-  cudaMemsetAsync(z + (size_t)rhs0 * 2 * c->d.nn, 0, nr * vb, c->stream);
-  launch_sgs(c, rhs0, nr, r, z, gated);
-  launch_residual(c, rhs0, nr, r, z, c->t, gated);
+// rz_mode (fused into the post-smoothing): 0 none, 1 rz at PCG init, 2 rz + beta
+static void enqueue_vcycle(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
+                           int rz_mode = 0) {
+  launch_sgs_sweep(c, rhs0, nr, r, z, gated, true, 0);        // z = SGS(0; r)
+  launch_residual(c, rhs0, nr, r, z, c->t, gated);             // t = r - K z
   launch_restrict(c, rhs0, nr, c->t, gated);
   launch_coarse_solve(c, rhs0, nr, gated);
   launch_prolong(c, rhs0, nr, z, gated);
-  launch_sgs(c, rhs0, nr, r, z, gated);
+  launch_sgs_sweep(c, rhs0, nr, r, z, gated, false, rz_mode); // z = SGS(z; r) (+ r.z, beta)
 }
 
 static void enqueue_iteration(msf_ctx* c, int nr) {
   launch_matvec(c, 0, nr, c->pv, c->q, true, true);
   launch_pcg_update_xr(c, nr);
-  enqueue_vcycle(c, 0, nr, c->r, c->z, true);
-  launch_pcg_rz(c, nr, false);
+  enqueue_vcycle(c, 0, nr, c->r, c->z, true, 2);
   launch_pcg_p(c, nr, false);
 }
 
@@ -516,8 +543,7 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
   const int nr = n_rhs;
   const long long l0 = c->launches;
   launch_pcg_init(c, nr, tol, max_it);
-  enqueue_vcycle(c, 0, nr, c->r, c->z, true);
-  launch_pcg_rz(c, nr, true);
+  enqueue_vcycle(c, 0, nr, c->r, c->z, true, 1);
   launch_pcg_p(c, nr, true);
   CKL("pcg init");
   // one PCG iteration as a CUDA graph (captured once per realisation count)
@@ -678,7 +704,7 @@ int msf_coarse_solve(msf_ctx* c, int rhs, const double* b, double* x) {
   const size_t n = (size_t)c->d.nbc * c->d.mc;
   CK(cudaMemcpyAsync(c->cb + rhs * n, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
   launch_coarse_solve(c, rhs, 1, false);
-  CK(cudaMemcpyAsync(x, c->cb + rhs * n, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(x, c->cx + rhs * n, n * 8, cudaMemcpyDeviceToDevice, c->stream));
   CKL("coarse_solve");
   int rc = read_scalars(c, 1);
   return rc;
@@ -751,7 +777,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   const double nn = d.nn, ne = d.ne;
   // algorithmic bytes per launch: every operand touched once
   bytes[0] = R * (nn * 16 + ne * 8 + nn * 16) + nn;                  // p, E -> q
-  bytes[1] = R * (ne * 8 + nn * 16 + nn / 4 * 16 + nn / 4 * 16) + nn / 4;  // one colour
+  bytes[1] = 7 * (R * (ne * 8 + nn * 16 + nn / 4 * 16 * 2) + nn / 4);  // 7 colour launches
   bytes[2] = R * nn * 16 + (double)c->n_cls * d.kmax * d.box_nodes * 16 + R * (double)d.n_agg * d.kmax * 8;
   {
     double cr = 0.0;
@@ -763,7 +789,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   }
   bytes[4] = R * (nn * 32) + (double)c->n_cls * d.kmax * d.box_nodes * 16 + R * (double)d.n_agg * d.kmax * 8;
   bytes[5] = R * (nn * 16 * 3 + ne * 8) + nn;                        // z, r, E -> t
-  bytes[6] = 16 * bytes[1] + bytes[2] + bytes[3] + bytes[4] + bytes[5] + R * nn * 16;
+  bytes[6] = 2 * bytes[1] + bytes[2] + bytes[3] + bytes[4] + bytes[5];
   bytes[7] = bytes[0] + bytes[6] + R * nn * 16 * 6 + R * nn * 16 * 2 + R * nn * 16 * 3;
   // keep every realisation active during the timing, restore afterwards
   std::vector<PcgScalars> saved(R);
@@ -816,7 +842,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
     cudaEventSynchronize(e1);
     float t = 0.f;
     cudaEventElapsedTime(&t, e0, e1);
-    return (double)t / reps / (which == 1 ? 8.0 : 1.0);
+    return (double)t / reps;
   };
   for (int i = 0; i < 8; ++i) ms[i] = timeit(i);
   if (!c->iter_graph || c->iter_graph_R != R) ms[7] = -1.0;

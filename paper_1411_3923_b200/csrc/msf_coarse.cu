@@ -24,69 +24,91 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ------------------------------------------------------------------ restriction
-// one CTA per (agglomerate, realisation): c[slot(I,J,a)] = sum_n phi_{I,J,a}(n) . t(n)
+// c[slot(I,J,a)] = sum_n phi_{I,J,a}(n) . t(n) for every active realisation at once: one CTA
+// per agglomerate (launched in class order, agg_by_cls, so consecutive CTAs share the
+// class basis in L2), each box node's basis values are loaded once and applied to all
+// realisations (Phi_i^T [t_1 .. t_R]).
+template <int KM>
 __global__ void __launch_bounds__(NT) k_restrict(Dims d, const double2* __restrict__ tall,
                                                  const double* __restrict__ phi,
                                                  const int* __restrict__ cls_of_agg,
+                                                 const int* __restrict__ agg_by_cls,
                                                  double* cball, const PcgScalars* sc, int rhs0,
-                                                 int gated) {
-  const int rhs = rhs0 + blockIdx.y;
-  if (gated && !sc[rhs].active) return;
-  __shared__ double red[MSF_MAX_MODES][NT / 32];
-  const int agg = blockIdx.x;
-  const int I = agg / (d.ncy + 1), J = agg - (agg / (d.ncy + 1)) * (d.ncy + 1);
-  const int cls = cls_of_agg[agg];
-  const double* ph = phi + (size_t)cls * d.kmax * d.box_nodes * 2;
-  const double2* t = tall + (size_t)rhs * d.nn;
-  const int gx0 = I * d.cx - d.cx, gy0 = J * d.cy - d.cy;
-  double acc[MSF_MAX_MODES];
+                                                 int nr, int gated) {
+  __shared__ double red[NT / 32][MSF_MAX_RHS * KM];
+  bool act[MSF_MAX_RHS];
+  bool any = false;
 #pragma unroll
-  for (int a = 0; a < MSF_MAX_MODES; ++a) acc[a] = 0.0;
+  for (int r = 0; r < MSF_MAX_RHS; ++r) {
+    act[r] = r < nr && (!gated || sc[rhs0 + r].active);
+    any |= act[r];
+  }
+  if (!any) return;
+  const int agg = agg_by_cls[blockIdx.x];
+  const int I = agg / (d.ncy + 1), J = agg - (agg / (d.ncy + 1)) * (d.ncy + 1);
+  const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2;
+  const int gx0 = I * d.cx - d.cx, gy0 = J * d.cy - d.cy;
   // interior of the padded box (chi vanishes on its boundary ring)
   const int ix_lo = max(1, -gx0), ix_hi = min(d.bx - 2, d.nnx - 1 - gx0);
   const int iy_lo = max(1, -gy0), iy_hi = min(d.by - 2, d.nny - 1 - gy0);
   const int w = iy_hi - iy_lo + 1, h = ix_hi - ix_lo + 1;
+  double acc[MSF_MAX_RHS][KM];
+#pragma unroll
+  for (int r = 0; r < MSF_MAX_RHS; ++r)
+#pragma unroll
+    for (int a = 0; a < KM; ++a) acc[r][a] = 0.0;
   for (int k = threadIdx.x; k < w * h; k += NT) {
     const int px = ix_lo + k / w, py = iy_lo + (k - (k / w) * w);
-    const double2 tv = t[(size_t)(gx0 + px) * d.nny + (gy0 + py)];
+    const size_t n = (size_t)(gx0 + px) * d.nny + (gy0 + py);
+    double2 tv[MSF_MAX_RHS];
+#pragma unroll
+    for (int r = 0; r < MSF_MAX_RHS; ++r)
+      tv[r] = act[r] ? tall[(size_t)(rhs0 + r) * d.nn + n] : make_double2(0.0, 0.0);
     const int bn = px * d.by + py;
 #pragma unroll
-    for (int a = 0; a < MSF_MAX_MODES; ++a) {
+    for (int a = 0; a < KM; ++a) {
       if (a < d.kmax) {
         const double2 pv = *reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2);
-        acc[a] = fma(pv.x, tv.x, fma(pv.y, tv.y, acc[a]));
+#pragma unroll
+        for (int r = 0; r < MSF_MAX_RHS; ++r) acc[r][a] = fma(pv.x, tv[r].x, fma(pv.y, tv[r].y, acc[r][a]));
       }
     }
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int a = 0; a < MSF_MAX_MODES; ++a) {
-    if (a < d.kmax) {
-      const double v = warp_sum(acc[a]);
-      if (lane == 0) red[a][wid] = v;
+  for (int r = 0; r < MSF_MAX_RHS; ++r)
+#pragma unroll
+    for (int a = 0; a < KM; ++a) {
+      if (act[r] && a < d.kmax) {
+        const double v = warp_sum(acc[r][a]);
+        if (lane == 0) red[wid][r * KM + a] = v;
+      }
     }
-  }
   __syncthreads();
-  if (threadIdx.x < d.kmax) {
+  const int r = threadIdx.x / KM, a = threadIdx.x - (threadIdx.x / KM) * KM;
+  if (r < nr && a < d.kmax && act[r < MSF_MAX_RHS ? r : 0]) {
     double s = 0.0;
-    for (int w2 = 0; w2 < NT / 32; ++w2) s += red[threadIdx.x][w2];
-    cball[(size_t)rhs * d.nbc * d.mc + (size_t)agg * d.kmax + threadIdx.x] = s;
+    for (int w2 = 0; w2 < NT / 32; ++w2) s += red[w2][r * KM + a];
+    cball[(size_t)(rhs0 + r) * d.nbc * d.mc + (size_t)agg * d.kmax + a] = s;
   }
 }
 
 // ------------------------------------------------------------------ prolongation
-// z(n) += sum_{I,J,a} phi_{I,J,a}(n) c[slot(I,J,a)]
+// z(n) += sum_{I,J,a} phi_{I,J,a}(n) x_c[slot(I,J,a)], all active realisations per thread
 __global__ void __launch_bounds__(NT) k_prolong(Dims d, const double* __restrict__ phi,
                                                 const int* __restrict__ cls_of_agg,
-                                                const double* __restrict__ cball, double2* zall,
-                                                const PcgScalars* sc, int rhs0, int gated) {
-  const int rhs = rhs0 + blockIdx.z;
-  if (gated && !sc[rhs].active) return;
+                                                const double* __restrict__ cxall, double2* zall,
+                                                const PcgScalars* sc, int rhs0, int nr, int gated) {
   const int iy = blockIdx.x * 32 + (threadIdx.x & 31);
   const int ix = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (ix >= d.nnx || iy >= d.nny) return;
-  const double* cb = cball + (size_t)rhs * d.nbc * d.mc;
-  double sx = 0.0, sy = 0.0;
+  bool act[MSF_MAX_RHS];
+  double sx[MSF_MAX_RHS], sy[MSF_MAX_RHS];
+#pragma unroll
+  for (int r = 0; r < MSF_MAX_RHS; ++r) {
+    act[r] = r < nr && (!gated || sc[rhs0 + r].active);
+    sx[r] = sy[r] = 0.0;
+  }
   const int I0 = ix / d.cx, J0 = iy / d.cy;
 #pragma unroll
   for (int di = 0; di < 2; ++di) {
@@ -103,21 +125,30 @@ __global__ void __launch_bounds__(NT) k_prolong(Dims d, const double* __restrict
       const int agg = I * (d.ncy + 1) + J;
       const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2;
       const int bn = px * d.by + py;
-      const double* cc = cb + (size_t)agg * d.kmax;
       for (int a = 0; a < d.kmax; ++a) {
         const double2 pv = *reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2);
-        const double cv = cc[a];
-        sx = fma(pv.x, cv, sx);
-        sy = fma(pv.y, cv, sy);
+#pragma unroll
+        for (int r = 0; r < MSF_MAX_RHS; ++r) {
+          if (act[r]) {
+            const double cv = cxall[(size_t)(rhs0 + r) * d.nbc * d.mc + (size_t)agg * d.kmax + a];
+            sx[r] = fma(pv.x, cv, sx[r]);
+            sy[r] = fma(pv.y, cv, sy[r]);
+          }
+        }
       }
     }
   }
-  double2* z = zall + (size_t)rhs * d.nn;
   const size_t n = (size_t)ix * d.nny + iy;
-  double2 zv = z[n];
-  zv.x += sx;
-  zv.y += sy;
-  z[n] = zv;
+#pragma unroll
+  for (int r = 0; r < MSF_MAX_RHS; ++r) {
+    if (act[r]) {
+      double2* z = zall + (size_t)(rhs0 + r) * d.nn;
+      double2 zv = z[n];
+      zv.x += sx[r];
+      zv.y += sy[r];
+      z[n] = zv;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ Galerkin cell products
@@ -353,17 +384,21 @@ __global__ void k_zero_blocks(double** dst, int m) {
 }
 
 // ------------------------------------------------------------------ cyclic-reduction solve
-// forward, survivors i: b_i -= Q_{i-s} b_{i-s} + P_{i+s} b_{i+s}   (warp per row)
+// Row-chunked GEMVs: each CTA owns CR_ROWS rows of one block, one warp per row, lanes over
+// the (row-major, coalesced) columns; the neighbour vectors are staged in shared memory.
+constexpr int CR_ROWS = 16;
+
+// forward, survivors i: b_i -= Q_{i-s} b_{i-s} + P_{i+s} b_{i+s}
 __global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restrict__ surv, int s,
                                                     const double* __restrict__ Qall,
                                                     const double* __restrict__ Pall,
                                                     double* cball, const PcgScalars* sc,
                                                     int rhs0, int gated) {
-  const int rhs = rhs0 + blockIdx.y;
+  const int rhs = rhs0 + blockIdx.z;
   if (gated && !sc[rhs].active) return;
   extern __shared__ double sv[];  // [2][m]
   const int m = d.mc;
-  const int i = surv[blockIdx.x];
+  const int i = surv[blockIdx.y];
   double* cb = cball + (size_t)rhs * d.nbc * m;
   const size_t per = (size_t)m * m;
   const bool hl = i - s >= 0, hr = i + s < d.nbc;
@@ -375,49 +410,101 @@ __global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restric
   const double* Q = Qall + ((size_t)rhs * d.nbc + (i - s)) * per;
   const double* P = Pall + ((size_t)rhs * d.nbc + (i + s)) * per;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int r = wid; r < m; r += nw) {
-    double acc = 0.0;
-    if (hl)
-      for (int c = lane; c < m; c += 32) acc = fma(Q[(size_t)r * m + c], sv[c], acc);
-    if (hr)
-      for (int c = lane; c < m; c += 32) acc = fma(P[(size_t)r * m + c], sv[m + c], acc);
-    acc = warp_sum(acc);
+  const int r0 = blockIdx.x * CR_ROWS, r1 = min(m, r0 + CR_ROWS);
+  for (int r = r0 + wid; r < r1; r += nw) {
+    // independent accumulators keep several row loads in flight per lane
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const double* Qr = Q + (size_t)r * m;
+    const double* Pr = P + (size_t)r * m;
+    int c = lane;
+    for (; c + 32 < m; c += 64) {
+      if (hl) {
+        a0 = fma(Qr[c], sv[c], a0);
+        a1 = fma(Qr[c + 32], sv[c + 32], a1);
+      }
+      if (hr) {
+        a2 = fma(Pr[c], sv[m + c], a2);
+        a3 = fma(Pr[c + 32], sv[m + c + 32], a3);
+      }
+    }
+    for (; c < m; c += 32) {
+      if (hl) a0 = fma(Qr[c], sv[c], a0);
+      if (hr) a2 = fma(Pr[c], sv[m + c], a2);
+    }
+    const double acc = warp_sum((a0 + a1) + (a2 + a3));
     if (lane == 0) cb[(size_t)i * m + r] -= acc;
   }
 }
 
-// back, eliminated k: x_k = Dinv_k b_k - P_k^T x_{k-s} - Q_k^T x_{k+s}  (thread per row)
+// back, eliminated k: x_k = Dinv_k b_k - P_k^T x_{k-s} - Q_k^T x_{k+s}
 __global__ void __launch_bounds__(256) k_cr_back(Dims d, const int* __restrict__ elim, int s,
                                                  const double* __restrict__ Dinv,
-                                                 const double* __restrict__ Pall,
-                                                 const double* __restrict__ Qall,
-                                                 double* cball, const PcgScalars* sc, int rhs0,
-                                                 int gated) {
-  const int rhs = rhs0 + blockIdx.y;
+                                                 const double* __restrict__ PTall,
+                                                 const double* __restrict__ QTall,
+                                                 const double* __restrict__ cball, double* cxall,
+                                                 const PcgScalars* sc, int rhs0, int gated) {
+  const int rhs = rhs0 + blockIdx.z;
   if (gated && !sc[rhs].active) return;
   extern __shared__ double sv[];  // [3][m]
   const int m = d.mc;
-  const int k = elim[blockIdx.x];
-  double* cb = cball + (size_t)rhs * d.nbc * m;
+  const int k = elim[blockIdx.y];
+  const double* cb = cball + (size_t)rhs * d.nbc * m;
+  double* cx = cxall + (size_t)rhs * d.nbc * m;
   const size_t per = (size_t)m * m;
   const bool hl = k - s >= 0, hr = k + s < d.nbc;
   for (int j = threadIdx.x; j < m; j += blockDim.x) {
     sv[j] = cb[(size_t)k * m + j];
-    sv[m + j] = hl ? cb[(size_t)(k - s) * m + j] : 0.0;
-    sv[2 * m + j] = hr ? cb[(size_t)(k + s) * m + j] : 0.0;
+    sv[m + j] = hl ? cx[(size_t)(k - s) * m + j] : 0.0;
+    sv[2 * m + j] = hr ? cx[(size_t)(k + s) * m + j] : 0.0;
   }
   __syncthreads();
   const double* Di = Dinv + ((size_t)rhs * d.nbc + k) * per;
-  const double* P = Pall + ((size_t)rhs * d.nbc + k) * per;
-  const double* Q = Qall + ((size_t)rhs * d.nbc + k) * per;
-  for (int r = threadIdx.x; r < m; r += blockDim.x) {
-    double acc = 0.0;
-    for (int c = 0; c < m; ++c) acc = fma(Di[(size_t)c * m + r], sv[c], acc);   // Dinv symmetric
-    if (hl)
-      for (int c = 0; c < m; ++c) acc = fma(-P[(size_t)c * m + r], sv[m + c], acc);
-    if (hr)
-      for (int c = 0; c < m; ++c) acc = fma(-Q[(size_t)c * m + r], sv[2 * m + c], acc);
-    cb[(size_t)k * m + r] = acc;
+  const double* PT = PTall + ((size_t)rhs * d.nbc + k) * per;
+  const double* QT = QTall + ((size_t)rhs * d.nbc + k) * per;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int r0 = blockIdx.x * CR_ROWS, r1 = min(m, r0 + CR_ROWS);
+  for (int r = r0 + wid; r < r1; r += nw) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0;
+    const double* Dr = Di + (size_t)r * m;
+    const double* Pr = PT + (size_t)r * m;
+    const double* Qr = QT + (size_t)r * m;
+    int c = lane;
+    for (; c + 32 < m; c += 64) {
+      a0 = fma(Dr[c], sv[c], a0);
+      a1 = fma(Dr[c + 32], sv[c + 32], a1);
+      if (hl) {
+        a2 = fma(Pr[c], sv[m + c], a2);
+        a3 = fma(Pr[c + 32], sv[m + c + 32], a3);
+      }
+      if (hr) {
+        a4 = fma(Qr[c], sv[2 * m + c], a4);
+        a5 = fma(Qr[c + 32], sv[2 * m + c + 32], a5);
+      }
+    }
+    for (; c < m; c += 32) {
+      a0 = fma(Dr[c], sv[c], a0);
+      if (hl) a2 = fma(Pr[c], sv[m + c], a2);
+      if (hr) a4 = fma(Qr[c], sv[2 * m + c], a4);
+    }
+    const double acc = warp_sum((a0 + a1) - (a2 + a3) - (a4 + a5));
+    if (lane == 0) cx[(size_t)k * m + r] = acc;
+  }
+}
+
+// batched transpose dst = src^T for blocks given by src pointers; dst = dst_base + (src - src_base)
+__global__ void k_transpose_blocks(double** src, const double* src_base, double* dst_base, int m) {
+  __shared__ double tile[32][33];
+  const double* S = src[blockIdx.z];
+  double* D = dst_base + (S - src_base);
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int r = by + j, c = bx + threadIdx.x;
+    if (r < m && c < m) tile[j][threadIdx.x] = S[(size_t)r * m + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int r = bx + j, c = by + threadIdx.x;
+    if (r < m && c < m) D[(size_t)r * m + c] = tile[threadIdx.x][j];
   }
 }
 
@@ -425,17 +512,23 @@ __global__ void __launch_bounds__(256) k_cr_back(Dims d, const int* __restrict__
 
 // ================================================================== host side
 void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) {
-  k_restrict<<<dim3(c->d.n_agg, nr), NT, 0, c->stream>>>(c->d, (const double2*)t, c->phi,
-                                                         c->cls_of_agg_d, c->cb, c->sc, rhs0,
-                                                         gated ? 1 : 0);
+  const Dims& d = c->d;
+#define MSF_RESTRICT(KM)                                                                       \
+  k_restrict<KM><<<d.n_agg, NT, 0, c->stream>>>(d, (const double2*)t, c->phi, c->cls_of_agg_d, \
+                                               c->agg_by_cls_d, c->cb, c->sc, rhs0, nr,       \
+                                               gated ? 1 : 0)
+  if (d.kmax <= 4) MSF_RESTRICT(4);
+  else if (d.kmax <= 8) MSF_RESTRICT(8);
+  else MSF_RESTRICT(16);
+#undef MSF_RESTRICT
   MSF_LAUNCHED(c);
 }
 
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
   const Dims& d = c->d;
-  dim3 g((d.nny + 31) / 32, (d.nnx + 7) / 8, nr);
-  k_prolong<<<g, NT, 0, c->stream>>>(d, c->phi, c->cls_of_agg_d, c->cb, (double2*)z, c->sc,
-                                     rhs0, gated ? 1 : 0);
+  dim3 g((d.nny + 31) / 32, (d.nnx + 7) / 8, 1);
+  k_prolong<<<g, NT, 0, c->stream>>>(d, c->phi, c->cls_of_agg_d, c->cx, (double2*)z, c->sc,
+                                     rhs0, nr, gated ? 1 : 0);
   MSF_LAUNCHED(c);
 }
 
@@ -476,6 +569,16 @@ void launch_assemble_coarse(msf_ctx* c) {
       k_gemm<true, false><<<dim3(gt.x, gt.y, L.nQ), 256, 0, c->stream>>>(L.qA, L.qB, L.qC, m, 1.0, 0.0);
       MSF_LAUNCHED(c);
     }
+    {
+      const dim3 tg((m + 31) / 32, (m + 31) / 32, L.nP);
+      k_transpose_blocks<<<tg, dim3(32, 8), 0, c->stream>>>(L.pC, c->Pc, c->PTc, m);
+      MSF_LAUNCHED(c);
+      if (L.nQ) {
+        const dim3 tq((m + 31) / 32, (m + 31) / 32, L.nQ);
+        k_transpose_blocks<<<tq, dim3(32, 8), 0, c->stream>>>(L.qC, c->Qc, c->QTc, m);
+        MSF_LAUNCHED(c);
+      }
+    }
     if (L.nDl) {
       k_gemm<false, true><<<dim3(gt.x, gt.y, L.nDl), 256, 0, c->stream>>>(L.dlA, L.dlB, L.dlC, m, -1.0, 1.0);
       MSF_LAUNCHED(c);
@@ -500,8 +603,8 @@ void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
   for (const CrLevel& L : c->cr) {
     if (L.s == 0) continue;
     if (!L.surv.empty()) {
-      k_cr_forward<<<dim3((unsigned)L.surv.size(), nr), nthr, 2 * m * sizeof(double), c->stream>>>(
-          d, L.surv_d, L.s, c->Qc, c->Pc, c->cb, c->sc, rhs0, gated ? 1 : 0);
+      k_cr_forward<<<dim3((m + 15) / 16, (unsigned)L.surv.size(), nr), nthr, 2 * m * sizeof(double),
+                     c->stream>>>(d, L.surv_d, L.s, c->Qc, c->Pc, c->cb, c->sc, rhs0, gated ? 1 : 0);
       MSF_LAUNCHED(c);
     }
   }
@@ -509,8 +612,9 @@ void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
   for (auto it = c->cr.rbegin(); it != c->cr.rend(); ++it) {
     const CrLevel& L = *it;
     const int s = L.s == 0 ? d.nbc : L.s;
-    k_cr_back<<<dim3((unsigned)L.elim.size(), nr), nthr, 3 * m * sizeof(double), c->stream>>>(
-        d, L.elim_d, s, c->Dinv, c->Pc, c->Qc, c->cb, c->sc, rhs0, gated ? 1 : 0);
+    k_cr_back<<<dim3((m + 15) / 16, (unsigned)L.elim.size(), nr), nthr, 3 * m * sizeof(double),
+                c->stream>>>(d, L.elim_d, s, c->Dinv, c->PTc, c->QTc, c->cb, c->cx, c->sc, rhs0,
+                             gated ? 1 : 0);
     MSF_LAUNCHED(c);
   }
 }

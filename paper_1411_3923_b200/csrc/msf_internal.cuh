@@ -135,7 +135,14 @@ struct msf_ctx {
   double* Dinv = nullptr;       // [R][nbc][mc*mc]
   double* Pc = nullptr;         // [R][nbc][mc*mc]
   double* Qc = nullptr;         // [R][nbc][mc*mc]
-  double* cb = nullptr;         // [R][nbc*mc] coarse rhs / solution
+  double* PTc = nullptr;        // [R][nbc][mc*mc]  P_k^T (back substitution, row-major)
+  double* QTc = nullptr;        // [R][nbc][mc*mc]  Q_k^T
+  double* cb = nullptr;         // [R][nbc*mc] coarse rhs (modified by the forward sweep)
+  double* cx = nullptr;         // [R][nbc*mc] coarse solution
+  int* chunks_d = nullptr;      // restriction work list: [n_chunks][3] = class, start, count
+  int* agg_by_cls_d = nullptr;  // agglomerates grouped by class
+  int n_chunks = 0;
+  std::vector<int> chunks_h, agg_by_cls_h;
   char* jobs_d = nullptr;       // CR job tables
   int* factor_status = nullptr; // [R] nonzero on failed pivot
 
@@ -168,6 +175,12 @@ void launch_matvec(msf_ctx* c, int rhs0, int nr, const double* x, double* y, boo
 void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double* x, double* y,
                      bool gated);
 void launch_sgs(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated);
+void launch_sgs_sweep(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
+                      bool zero_start, int rz_mode);
+// fused symmetric GS sweep; mode 0: z = SGS(0; r) and t = r - K z, mode 1: z = SGS(z; r)
+// with rz_mode 0 none / 1 rz init (beta = 0) / 2 rz + beta
+void launch_sgs_fused(msf_ctx* c, int rhs0, int nr, const double* r, double* z, double* t,
+                      int mode, bool gated, int rz_mode);
 void launch_mask_copy(msf_ctx* c, const double* x, double* y, int n2nn);
 void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it);
 void launch_pcg_update_xr(msf_ctx* c, int nr);
