@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -13,7 +14,6 @@
 #include "msf_internal.cuh"
 
 int apply_partials_needed(const Dims& d);
-int sgs_partials_needed(const Dims& d);
 int sgs_colour_partials_needed(const Dims& d);
 size_t eig_smem_bytes(int mlmax, int mb);
 
@@ -186,8 +186,7 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     P.cr.push_back(L);
   }
   P.jobs_bytes = align_up(ptrs * sizeof(double*)) + align_up(ints * sizeof(int));
-  P.max_partials = std::max(apply_partials_needed(d),
-                            std::max(sgs_partials_needed(d), sgs_colour_partials_needed(d)));
+  P.max_partials = std::max(apply_partials_needed(d), sgs_colour_partials_needed(d));
 
   // workspace size
   const size_t R = d.R, nn = d.nn, ne = d.ne, nt = d.nt;
@@ -214,7 +213,8 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   add(P.jobs_bytes);
   add(2 * MSF_MAX_RHS * 4);                  // factor_status
   add(R * sizeof(PcgScalars));
-  add(R * (size_t)P.max_partials * 8);
+  add((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
+  add(cr_levels_dev_bytes((int)P.cr.size()));
   add(R * 8 * 4);                            // counters
   add(64 * 8);                               // scal
   P.total = t + 256;
@@ -272,6 +272,15 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   c->filt_wsum = P.wsum;
   c->max_partials = P.max_partials;
   c->periodic = (p->tile_x != p->nelx || p->tile_y != p->nely);
+  {
+    const char* mode = std::getenv("MSF_PCG_MODE");
+    // default: graph-launched iterations (measured faster); opt-in persistent
+    c->persistent = (mode && std::string(mode) == "persistent");
+    if (std::getenv("MSF_PERSIST_PROFILE")) {   // debug only: phase timeline buffer
+      cudaMalloc(&c->prof_d, 32 * 64 * sizeof(unsigned long long));
+      cudaMemset(c->prof_d, 0, 32 * 64 * sizeof(unsigned long long));
+    }
+  }
 
   const Dims& d = c->d;
   const size_t R = d.R, nn = d.nn, ne = d.ne, nt = d.nt;
@@ -334,7 +343,8 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   c->jobs_d = (char*)take(P.jobs_bytes);
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
   c->sc = (PcgScalars*)take(R * sizeof(PcgScalars));
-  c->partials = (double*)take(R * (size_t)P.max_partials * 8);
+  c->partials = (double*)take((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
+  c->cr_levels_d = take(cr_levels_dev_bytes((int)c->cr.size()));
   c->counters = (unsigned*)take(R * 8 * 4);
   c->scal = (double*)take(64 * 8);
   if ((size_t)(cur - (char*)workspace) > workspace_bytes) {
@@ -409,6 +419,10 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
     }
     cudaMemcpyAsync(c->jobs_d, ptrs.data(), ptrs.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(id, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream);
+    std::vector<char> lv(cr_levels_dev_bytes((int)c->cr.size()));
+    fill_cr_levels_dev(c->cr, lv.data());
+    cudaMemcpyAsync(c->cr_levels_d, lv.data(), lv.size(), cudaMemcpyHostToDevice, c->stream);
+    cudaStreamSynchronize(c->stream);   // host staging buffers go out of scope
   }
 
   // fixed mask per node, load, filter table, classes
@@ -534,6 +548,8 @@ static int read_scalars(msf_ctx* c, int nr) {
   return MSF_OK;
 }
 
+static int run_graph_iterations(msf_ctx* c, int nr, int max_it);
+
 int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int32_t* iters,
                   double* compliance) {
   if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
@@ -546,7 +562,46 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
   enqueue_vcycle(c, 0, nr, c->r, c->z, true, 1);
   launch_pcg_p(c, nr, true);
   CKL("pcg init");
-  // one PCG iteration as a CUDA graph (captured once per realisation count)
+  if (c->persistent) {
+    // all iterations in one cooperative launch (msf_persist.cu), no host round trips
+    int rc = launch_pcg_persistent(c, nr);
+    if (rc) return rc;
+    if (c->prof_d) {
+      std::vector<unsigned long long> pr(32 * 64);
+      CK(cudaMemcpy(pr.data(), c->prof_d, pr.size() * 8, cudaMemcpyDeviceToHost));
+      for (int it = 1; it < 4; ++it) {
+        std::fprintf(stderr, "persistent PCG iteration %d phase ends (us since start):", it);
+        const unsigned long long t0 = pr[it * 64 + 63];
+        for (int ph = 0; ph < 40 && pr[it * 64 + ph] > t0; ++ph)
+          std::fprintf(stderr, " %.1f", (pr[it * 64 + ph] - t0) * 1e-3);
+        std::fprintf(stderr, "\n");
+      }
+    }
+  } else {
+    int rc = run_graph_iterations(c, nr, max_it);
+    if (rc) return rc;
+  }
+  launch_compliance(c, nr);
+  CKL("compliance");
+  int rc = read_scalars(c, nr);
+  if (rc) return rc;
+  int noconv = 0;
+  for (int k = 0; k < nr; ++k) {
+    c->last_iters[k] = c->sc_host[k].iters;
+    if (iters) iters[k] = c->sc_host[k].iters;
+    if (compliance) compliance[k] = c->sc_host[k].comp;
+    noconv |= c->sc_host[k].noconv;
+  }
+  if (u) CK(cudaMemcpyAsync(u, c->u, (size_t)nr * 2 * c->d.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+  c->have_solution = true;
+  (void)l0;
+  if (noconv) return msf_fail(c, MSF_ERR_NOCONV, "PCG reached max_it");
+  return MSF_OK;
+}
+
+// PCG iterations as CUDA-graph launches of one captured iteration; the host polls the
+// device-side `active` flags every 4 iterations (converged realisations are no-ops).
+static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
   if (!c->iter_graph || c->iter_graph_R != nr) {
     if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
     c->iter_graph = nullptr;
@@ -581,21 +636,6 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
     for (int k = 0; k < nr; ++k)
       if (c->sc_host[k].active) done = 0;
   }
-  launch_compliance(c, nr);
-  CKL("compliance");
-  int rc = read_scalars(c, nr);
-  if (rc) return rc;
-  int noconv = 0;
-  for (int k = 0; k < nr; ++k) {
-    c->last_iters[k] = c->sc_host[k].iters;
-    if (iters) iters[k] = c->sc_host[k].iters;
-    if (compliance) compliance[k] = c->sc_host[k].comp;
-    noconv |= c->sc_host[k].noconv;
-  }
-  if (u) CK(cudaMemcpyAsync(u, c->u, (size_t)nr * 2 * c->d.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
-  c->have_solution = true;
-  (void)l0;
-  if (noconv) return msf_fail(c, MSF_ERR_NOCONV, "PCG reached max_it");
   return MSF_OK;
 }
 

@@ -9,19 +9,15 @@
 //     exact coarse solve by block cyclic reduction: per level the odd blocks are
 //     eliminated with explicit SPD inverses (batched sweep operator) and batched GEMMs,
 //     so every level is parallel across blocks and realisations.
-#include "msf_internal.cuh"
+#include "msf_kern.cuh"
 
 #include <algorithm>
+
+using namespace msfk;
 
 namespace {
 
 constexpr int NT = 256;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  return v;
-}
 
 // ------------------------------------------------------------------ restriction
 // c[slot(I,J,a)] = sum_n phi_{I,J,a}(n) . t(n) for every active realisation at once: one CTA
@@ -40,57 +36,12 @@ __global__ void __launch_bounds__(NT) k_restrict(Dims d, const double2* __restri
   bool any = false;
 #pragma unroll
   for (int r = 0; r < MSF_MAX_RHS; ++r) {
-    act[r] = r < nr && (!gated || sc[rhs0 + r].active);
+    act[r] = r >= rhs0 && r < rhs0 + nr && (!gated || sc[r].active);
     any |= act[r];
   }
   if (!any) return;
-  const int agg = agg_by_cls[blockIdx.x];
-  const int I = agg / (d.ncy + 1), J = agg - (agg / (d.ncy + 1)) * (d.ncy + 1);
-  const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2;
-  const int gx0 = I * d.cx - d.cx, gy0 = J * d.cy - d.cy;
-  // interior of the padded box (chi vanishes on its boundary ring)
-  const int ix_lo = max(1, -gx0), ix_hi = min(d.bx - 2, d.nnx - 1 - gx0);
-  const int iy_lo = max(1, -gy0), iy_hi = min(d.by - 2, d.nny - 1 - gy0);
-  const int w = iy_hi - iy_lo + 1, h = ix_hi - ix_lo + 1;
-  double acc[MSF_MAX_RHS][KM];
-#pragma unroll
-  for (int r = 0; r < MSF_MAX_RHS; ++r)
-#pragma unroll
-    for (int a = 0; a < KM; ++a) acc[r][a] = 0.0;
-  for (int k = threadIdx.x; k < w * h; k += NT) {
-    const int px = ix_lo + k / w, py = iy_lo + (k - (k / w) * w);
-    const size_t n = (size_t)(gx0 + px) * d.nny + (gy0 + py);
-    double2 tv[MSF_MAX_RHS];
-#pragma unroll
-    for (int r = 0; r < MSF_MAX_RHS; ++r)
-      tv[r] = act[r] ? tall[(size_t)(rhs0 + r) * d.nn + n] : make_double2(0.0, 0.0);
-    const int bn = px * d.by + py;
-#pragma unroll
-    for (int a = 0; a < KM; ++a) {
-      if (a < d.kmax) {
-        const double2 pv = *reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2);
-#pragma unroll
-        for (int r = 0; r < MSF_MAX_RHS; ++r) acc[r][a] = fma(pv.x, tv[r].x, fma(pv.y, tv[r].y, acc[r][a]));
-      }
-    }
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int r = 0; r < MSF_MAX_RHS; ++r)
-#pragma unroll
-    for (int a = 0; a < KM; ++a) {
-      if (act[r] && a < d.kmax) {
-        const double v = warp_sum(acc[r][a]);
-        if (lane == 0) red[wid][r * KM + a] = v;
-      }
-    }
-  __syncthreads();
-  const int r = threadIdx.x / KM, a = threadIdx.x - (threadIdx.x / KM) * KM;
-  if (r < nr && a < d.kmax && act[r < MSF_MAX_RHS ? r : 0]) {
-    double s = 0.0;
-    for (int w2 = 0; w2 < NT / 32; ++w2) s += red[w2][r * KM + a];
-    cball[(size_t)(rhs0 + r) * d.nbc * d.mc + (size_t)agg * d.kmax + a] = s;
-  }
+  restrict_agg<KM>(d, tall, phi, cls_of_agg, cball, agg_by_cls[blockIdx.x], act, NT,
+                   threadIdx.x, red);
 }
 
 // ------------------------------------------------------------------ prolongation
@@ -103,52 +54,9 @@ __global__ void __launch_bounds__(NT) k_prolong(Dims d, const double* __restrict
   const int ix = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (ix >= d.nnx || iy >= d.nny) return;
   bool act[MSF_MAX_RHS];
-  double sx[MSF_MAX_RHS], sy[MSF_MAX_RHS];
 #pragma unroll
-  for (int r = 0; r < MSF_MAX_RHS; ++r) {
-    act[r] = r < nr && (!gated || sc[rhs0 + r].active);
-    sx[r] = sy[r] = 0.0;
-  }
-  const int I0 = ix / d.cx, J0 = iy / d.cy;
-#pragma unroll
-  for (int di = 0; di < 2; ++di) {
-    const int I = I0 + di;
-    if (I > d.ncx) continue;
-    const int px = ix - (I * d.cx - d.cx);
-    if (px < 0 || px >= d.bx) continue;
-#pragma unroll
-    for (int dj = 0; dj < 2; ++dj) {
-      const int J = J0 + dj;
-      if (J > d.ncy) continue;
-      const int py = iy - (J * d.cy - d.cy);
-      if (py < 0 || py >= d.by) continue;
-      const int agg = I * (d.ncy + 1) + J;
-      const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2;
-      const int bn = px * d.by + py;
-      for (int a = 0; a < d.kmax; ++a) {
-        const double2 pv = *reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2);
-#pragma unroll
-        for (int r = 0; r < MSF_MAX_RHS; ++r) {
-          if (act[r]) {
-            const double cv = cxall[(size_t)(rhs0 + r) * d.nbc * d.mc + (size_t)agg * d.kmax + a];
-            sx[r] = fma(pv.x, cv, sx[r]);
-            sy[r] = fma(pv.y, cv, sy[r]);
-          }
-        }
-      }
-    }
-  }
-  const size_t n = (size_t)ix * d.nny + iy;
-#pragma unroll
-  for (int r = 0; r < MSF_MAX_RHS; ++r) {
-    if (act[r]) {
-      double2* z = zall + (size_t)(rhs0 + r) * d.nn;
-      double2 zv = z[n];
-      zv.x += sx[r];
-      zv.y += sy[r];
-      z[n] = zv;
-    }
-  }
+  for (int r = 0; r < MSF_MAX_RHS; ++r) act[r] = r >= rhs0 && r < rhs0 + nr && (!gated || sc[r].active);
+  prolong_node(d, phi, cls_of_agg, cxall, zall, ix, iy, act);
 }
 
 // ------------------------------------------------------------------ Galerkin cell products
@@ -376,18 +284,7 @@ __global__ void __launch_bounds__(256) k_gemm(double** As, double** Bs, double**
     }
 }
 
-__global__ void k_zero_blocks(double** dst, int m) {
-  double* t = dst[blockIdx.y];
-  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)m * m;
-       e += (size_t)gridDim.x * blockDim.x)
-    t[e] = 0.0;
-}
-
 // ------------------------------------------------------------------ cyclic-reduction solve
-// Row-chunked GEMVs: each CTA owns CR_ROWS rows of one block, one warp per row, lanes over
-// the (row-major, coalesced) columns; the neighbour vectors are staged in shared memory.
-constexpr int CR_ROWS = 16;
-
 // forward, survivors i: b_i -= Q_{i-s} b_{i-s} + P_{i+s} b_{i+s}
 __global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restrict__ surv, int s,
                                                     const double* __restrict__ Qall,
@@ -397,43 +294,11 @@ __global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restric
   const int rhs = rhs0 + blockIdx.z;
   if (gated && !sc[rhs].active) return;
   extern __shared__ double sv[];  // [2][m]
-  const int m = d.mc;
   const int i = surv[blockIdx.y];
-  double* cb = cball + (size_t)rhs * d.nbc * m;
-  const size_t per = (size_t)m * m;
-  const bool hl = i - s >= 0, hr = i + s < d.nbc;
-  for (int k = threadIdx.x; k < m; k += blockDim.x) {
-    sv[k] = hl ? cb[(size_t)(i - s) * m + k] : 0.0;
-    sv[m + k] = hr ? cb[(size_t)(i + s) * m + k] : 0.0;
-  }
-  __syncthreads();
-  const double* Q = Qall + ((size_t)rhs * d.nbc + (i - s)) * per;
-  const double* P = Pall + ((size_t)rhs * d.nbc + (i + s)) * per;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int r0 = blockIdx.x * CR_ROWS, r1 = min(m, r0 + CR_ROWS);
-  for (int r = r0 + wid; r < r1; r += nw) {
-    // independent accumulators keep several row loads in flight per lane
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    const double* Qr = Q + (size_t)r * m;
-    const double* Pr = P + (size_t)r * m;
-    int c = lane;
-    for (; c + 32 < m; c += 64) {
-      if (hl) {
-        a0 = fma(Qr[c], sv[c], a0);
-        a1 = fma(Qr[c + 32], sv[c + 32], a1);
-      }
-      if (hr) {
-        a2 = fma(Pr[c], sv[m + c], a2);
-        a3 = fma(Pr[c + 32], sv[m + c + 32], a3);
-      }
-    }
-    for (; c < m; c += 32) {
-      if (hl) a0 = fma(Qr[c], sv[c], a0);
-      if (hr) a2 = fma(Pr[c], sv[m + c], a2);
-    }
-    const double acc = warp_sum((a0 + a1) + (a2 + a3));
-    if (lane == 0) cb[(size_t)i * m + r] -= acc;
-  }
+  const size_t per = (size_t)d.mc * d.mc;
+  cr_forward_rows(d, i, s, blockIdx.x * CR_ROWS, Qall + ((size_t)rhs * d.nbc + (i - s)) * per,
+                  Pall + ((size_t)rhs * d.nbc + (i + s)) * per, cball + (size_t)rhs * d.nbc * d.mc,
+                  sv, threadIdx.x, blockDim.x);
 }
 
 // back, eliminated k: x_k = Dinv_k b_k - P_k^T x_{k-s} - Q_k^T x_{k+s}
@@ -446,49 +311,12 @@ __global__ void __launch_bounds__(256) k_cr_back(Dims d, const int* __restrict__
   const int rhs = rhs0 + blockIdx.z;
   if (gated && !sc[rhs].active) return;
   extern __shared__ double sv[];  // [3][m]
-  const int m = d.mc;
   const int k = elim[blockIdx.y];
-  const double* cb = cball + (size_t)rhs * d.nbc * m;
-  double* cx = cxall + (size_t)rhs * d.nbc * m;
-  const size_t per = (size_t)m * m;
-  const bool hl = k - s >= 0, hr = k + s < d.nbc;
-  for (int j = threadIdx.x; j < m; j += blockDim.x) {
-    sv[j] = cb[(size_t)k * m + j];
-    sv[m + j] = hl ? cx[(size_t)(k - s) * m + j] : 0.0;
-    sv[2 * m + j] = hr ? cx[(size_t)(k + s) * m + j] : 0.0;
-  }
-  __syncthreads();
-  const double* Di = Dinv + ((size_t)rhs * d.nbc + k) * per;
-  const double* PT = PTall + ((size_t)rhs * d.nbc + k) * per;
-  const double* QT = QTall + ((size_t)rhs * d.nbc + k) * per;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int r0 = blockIdx.x * CR_ROWS, r1 = min(m, r0 + CR_ROWS);
-  for (int r = r0 + wid; r < r1; r += nw) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0;
-    const double* Dr = Di + (size_t)r * m;
-    const double* Pr = PT + (size_t)r * m;
-    const double* Qr = QT + (size_t)r * m;
-    int c = lane;
-    for (; c + 32 < m; c += 64) {
-      a0 = fma(Dr[c], sv[c], a0);
-      a1 = fma(Dr[c + 32], sv[c + 32], a1);
-      if (hl) {
-        a2 = fma(Pr[c], sv[m + c], a2);
-        a3 = fma(Pr[c + 32], sv[m + c + 32], a3);
-      }
-      if (hr) {
-        a4 = fma(Qr[c], sv[2 * m + c], a4);
-        a5 = fma(Qr[c + 32], sv[2 * m + c + 32], a5);
-      }
-    }
-    for (; c < m; c += 32) {
-      a0 = fma(Dr[c], sv[c], a0);
-      if (hl) a2 = fma(Pr[c], sv[m + c], a2);
-      if (hr) a4 = fma(Qr[c], sv[2 * m + c], a4);
-    }
-    const double acc = warp_sum((a0 + a1) - (a2 + a3) - (a4 + a5));
-    if (lane == 0) cx[(size_t)k * m + r] = acc;
-  }
+  const size_t per = (size_t)d.mc * d.mc;
+  const size_t blk = ((size_t)rhs * d.nbc + k) * per;
+  cr_back_rows(d, k, s, blockIdx.x * CR_ROWS, Dinv + blk, PTall + blk, QTall + blk,
+               cball + (size_t)rhs * d.nbc * d.mc, cxall + (size_t)rhs * d.nbc * d.mc, sv,
+               threadIdx.x, blockDim.x);
 }
 
 // batched transpose dst = src^T for blocks given by src pointers; dst = dst_base + (src - src_base)

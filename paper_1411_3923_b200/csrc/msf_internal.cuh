@@ -143,6 +143,9 @@ struct msf_ctx {
   int* agg_by_cls_d = nullptr;  // agglomerates grouped by class
   int n_chunks = 0;
   std::vector<int> chunks_h, agg_by_cls_h;
+  void* cr_levels_d = nullptr;  // CrLevelDev[n levels] for the persistent PCG kernel
+  bool persistent = true;       // PCG driver: persistent cooperative kernel (else CUDA graph)
+  void* prof_d = nullptr;       // debug phase timeline of the persistent kernel (env MSF_PERSIST_PROFILE)
   char* jobs_d = nullptr;       // CR job tables
   int* factor_status = nullptr; // [R] nonzero on failed pivot
 
@@ -177,10 +180,6 @@ void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double
 void launch_sgs(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated);
 void launch_sgs_sweep(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
                       bool zero_start, int rz_mode);
-// fused symmetric GS sweep; mode 0: z = SGS(0; r) and t = r - K z, mode 1: z = SGS(z; r)
-// with rz_mode 0 none / 1 rz init (beta = 0) / 2 rz + beta
-void launch_sgs_fused(msf_ctx* c, int rhs0, int nr, const double* r, double* z, double* t,
-                      int mode, bool gated, int rz_mode);
 void launch_mask_copy(msf_ctx* c, const double* x, double* y, int n2nn);
 void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it);
 void launch_pcg_update_xr(msf_ctx* c, int nr);
@@ -200,6 +199,11 @@ void launch_build_basis(msf_ctx* c);
 void launch_assemble_coarse(msf_ctx* c);
 void launch_coarse_galerkin(msf_ctx* c);
 void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated);
+// persistent cooperative PCG iterations (msf_persist.cu); returns MSF_OK or an error code
+int launch_pcg_persistent(msf_ctx* c, int nr);
+size_t cr_levels_dev_bytes(int nlev);
+void fill_cr_levels_dev(const std::vector<CrLevel>& cr, void* host_buf);
+constexpr int MSF_PERSIST_PARTIALS = 3 * MSF_MAX_RHS * 4 * 160;  // 3 slots x 4 rhs x grid
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated);
 void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated);
 

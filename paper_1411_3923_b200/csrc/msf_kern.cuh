@@ -1,0 +1,420 @@
+// Device-side building blocks of the B200 MsFEM-PCG path, shared by the single-purpose
+// kernels (msf_fem.cu, msf_coarse.cu) and the persistent PCG kernel (msf_persist.cu) so
+// that both execute the same arithmetic.  All functions are called by a whole CTA unless
+// stated otherwise.
+#pragma once
+
+#include "msf_internal.cuh"
+
+namespace msfk {
+
+// ------------------------------------------------------------------ Q4 node stencil
+// local index a of the centre node inside element (sx,sy) = (ix-1+sx, iy-1+sy)
+__device__ __forceinline__ constexpr int a_of(int sx, int sy) {
+  return (sx == 0 && sy == 0) ? 2 : (sx == 1 && sy == 0) ? 3 : (sx == 0 && sy == 1) ? 1 : 0;
+}
+__device__ __forceinline__ constexpr int DXB(int b) { return (b == 1 || b == 2) ? 1 : 0; }
+__device__ __forceinline__ constexpr int DYB(int b) { return (b >= 2) ? 1 : 0; }
+
+// (K z)_node and the node's own 2x2 diagonal block from the 4 element moduli E[sx][sy]
+// and the 3x3 neighbourhood z[i][j] = node (ix-1+i, iy-1+j)  (Eq. 4-5).
+__device__ __forceinline__ void apply_node(const K0Mat& K, const double (&E)[2][2],
+                                           const double2 (&z)[3][3], double& ox, double& oy,
+                                           double& dxx, double& dxy, double& dyx, double& dyy) {
+  ox = oy = dxx = dxy = dyx = dyy = 0.0;
+#pragma unroll
+  for (int sx = 0; sx < 2; ++sx)
+#pragma unroll
+    for (int sy = 0; sy < 2; ++sy) {
+      const int a = a_of(sx, sy);
+      double ax = 0.0, ay = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const double2 v = z[sx + DXB(b)][sy + DYB(b)];
+        ax = fma(K.v[(2 * a) * 8 + 2 * b], v.x, ax);
+        ax = fma(K.v[(2 * a) * 8 + 2 * b + 1], v.y, ax);
+        ay = fma(K.v[(2 * a + 1) * 8 + 2 * b], v.x, ay);
+        ay = fma(K.v[(2 * a + 1) * 8 + 2 * b + 1], v.y, ay);
+      }
+      const double e = E[sx][sy];
+      ox = fma(e, ax, ox);
+      oy = fma(e, ay, oy);
+      dxx = fma(e, K.v[(2 * a) * 8 + 2 * a], dxx);
+      dxy = fma(e, K.v[(2 * a) * 8 + 2 * a + 1], dxy);
+      dyx = fma(e, K.v[(2 * a + 1) * 8 + 2 * a], dyx);
+      dyy = fma(e, K.v[(2 * a + 1) * 8 + 2 * a + 1], dyy);
+    }
+}
+
+// ------------------------------------------------------------------ reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-order block reduction; result valid in every thread.  nthreads multiple of 32,
+// sm >= nthreads/32 + 1 doubles.
+__device__ __forceinline__ double block_sum_all(double v, double* sm, int tid, int nthreads) {
+  v = warp_sum(v);
+  if ((tid & 31) == 0) sm[tid >> 5] = v;
+  __syncthreads();
+  const int nw = nthreads >> 5;
+  if (tid < 32) {
+    double s = (tid < nw) ? sm[tid] : 0.0;
+    s = warp_sum(s);
+    if (tid == 0) sm[nw] = s;   // broadcast slot
+  }
+  __syncthreads();
+  const double s = sm[nw];
+  __syncthreads();
+  return s;
+}
+
+// ------------------------------------------------------------------ operator tile
+// y = P K P x (MODE 0) or y = b - P K P x (MODE 1) on one 8x32-node tile (ix0, iy0) with a
+// one-node halo staged in shared memory; returns this thread's x.y contribution.
+constexpr int TX = 8;
+constexpr int TY = 32;
+constexpr int TILE_THREADS = TX * TY;
+struct TileSmem {
+  double2 xs[TX + 2][TY + 2];
+  double Es[TX + 1][TY + 1];
+};
+
+template <int MODE>
+__device__ __forceinline__ double apply_tile(const Dims& d, const K0Mat& K, const double* __restrict__ E,
+                                             const double2* __restrict__ x, double2* __restrict__ y,
+                                             const double2* __restrict__ b,
+                                             const uint8_t* __restrict__ fixn, int ix0, int iy0,
+                                             int tid, TileSmem& S) {
+  for (int k = tid; k < (TX + 2) * (TY + 2); k += TILE_THREADS) {
+    const int i = k / (TY + 2), j = k - i * (TY + 2);
+    const int gx = ix0 - 1 + i, gy = iy0 - 1 + j;
+    double2 v = make_double2(0.0, 0.0);
+    if (gx >= 0 && gx < d.nnx && gy >= 0 && gy < d.nny) v = x[(size_t)gx * d.nny + gy];
+    S.xs[i][j] = v;
+  }
+  for (int k = tid; k < (TX + 1) * (TY + 1); k += TILE_THREADS) {
+    const int i = k / (TY + 1), j = k - i * (TY + 1);
+    const int ex = ix0 - 1 + i, ey = iy0 - 1 + j;
+    S.Es[i][j] = (ex >= 0 && ex < d.nelx && ey >= 0 && ey < d.nely) ? E[(size_t)ex * d.nely + ey] : 0.0;
+  }
+  __syncthreads();
+  const int li = tid / TY, lj = tid - (tid / TY) * TY;
+  const int ix = ix0 + li, iy = iy0 + lj;
+  double dv = 0.0;
+  if (ix < d.nnx && iy < d.nny) {
+    double Eloc[2][2];
+    double2 zloc[3][3];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) Eloc[a][c] = S.Es[li + a][lj + c];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) zloc[a][c] = S.xs[li + a][lj + c];
+    double ox, oy, dxx, dxy, dyx, dyy;
+    apply_node(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
+    const size_t n = (size_t)ix * d.nny + iy;
+    const uint8_t fm = fixn[n];
+    double2 out;
+    if (MODE == 1) {
+      const double2 bb = b[n];
+      out = make_double2(bb.x - ox, bb.y - oy);
+    } else {
+      out = make_double2(ox, oy);
+    }
+    if (fm & 1) out.x = 0.0;
+    if (fm & 2) out.y = 0.0;
+    y[n] = out;
+    dv = zloc[1][1].x * out.x + zloc[1][1].y * out.y;
+  }
+  __syncthreads();   // smem reused by the next tile
+  return dv;
+}
+
+// ------------------------------------------------------------------ Gauss-Seidel quad
+// One colour phase (reading R7) for node quad (qx, qy): updates the quad's node of
+// `colour`.  FWD: x then y ; BWD: y then x ; both: the F3B3 phase.  ZERO: first forward
+// phase from z = 0 (writes zeros to the quad's other nodes).  Returns r.z over the whole
+// quad when RZ (after the final backward phase).  Per-thread.
+template <bool FWD, bool BWD, bool ZERO, bool RZ>
+__device__ __forceinline__ double sgs_quad(const Dims& d, const K0Mat& K, const double* __restrict__ E,
+                                           const double2* __restrict__ r, double2* z,
+                                           const uint8_t* __restrict__ fixn, int qx, int qy,
+                                           int colour) {
+  const int ix = 2 * qx + (colour & 1), iy = 2 * qy + (colour >> 1);
+  double dot = 0.0;
+  if (ZERO) {
+#pragma unroll
+    for (int dn = 0; dn < 4; ++dn) {
+      const int gx = 2 * qx + (dn & 1), gy = 2 * qy + (dn >> 1);
+      if (dn != colour && gx < d.nnx && gy < d.nny) z[(size_t)gx * d.nny + gy] = make_double2(0.0, 0.0);
+    }
+  }
+  if (ix < d.nnx && iy < d.nny) {
+    double Eloc[2][2];
+    double2 zloc[3][3];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int ex = ix - 1 + a, ey = iy - 1 + b;
+        Eloc[a][b] = (ex >= 0 && ex < d.nelx && ey >= 0 && ey < d.nely) ? __ldg(E + (size_t)ex * d.nely + ey) : 0.0;
+      }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int gx = ix - 1 + a, gy = iy - 1 + b;
+        zloc[a][b] = (!ZERO && gx >= 0 && gx < d.nnx && gy >= 0 && gy < d.nny)
+                         ? z[(size_t)gx * d.nny + gy]
+                         : make_double2(0.0, 0.0);
+      }
+    double ox, oy, dxx, dxy, dyx, dyy;
+    apply_node(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
+    const size_t n = (size_t)ix * d.nny + iy;
+    const double2 rv = r[n];
+    const uint8_t fm = fixn[n];
+    double2 zn = zloc[1][1];
+    double rx = rv.x - ox, ry = rv.y - oy;
+    if (FWD) {
+      if (!(fm & 1)) {
+        const double dz = rx / dxx;
+        zn.x += dz;
+        ry -= dyx * dz;
+        rx -= dxx * dz;
+      }
+      if (!(fm & 2)) {
+        const double dz = ry / dyy;
+        zn.y += dz;
+        rx -= dxy * dz;
+        ry -= dyy * dz;
+      }
+    }
+    if (BWD) {
+      if (!(fm & 2)) {
+        const double dz = ry / dyy;
+        zn.y += dz;
+        rx -= dxy * dz;
+      }
+      if (!(fm & 1)) zn.x += rx / dxx;
+    }
+    z[n] = zn;
+    if (RZ) dot = rv.x * zn.x + rv.y * zn.y;
+  }
+  if (RZ) {
+#pragma unroll
+    for (int dn = 0; dn < 4; ++dn) {
+      const int gx = 2 * qx + (dn & 1), gy = 2 * qy + (dn >> 1);
+      if (dn != colour && gx < d.nnx && gy < d.nny) {
+        const size_t m = (size_t)gx * d.nny + gy;
+        const double2 a = r[m], b = z[m];
+        dot += a.x * b.x + a.y * b.y;
+      }
+    }
+  }
+  return dot;
+}
+
+// ------------------------------------------------------------------ restriction
+// c[rhs][agg*kmax + a] = sum_n phi_{agg,a}(n) . t_rhs(n) for the realisations in act[].
+template <int KM>
+__device__ __forceinline__ void restrict_agg(const Dims& d, const double2* __restrict__ tall,
+                                             const double* __restrict__ phi,
+                                             const int* __restrict__ cls_of_agg, double* cball,
+                                             int agg, const bool (&act)[MSF_MAX_RHS], int nthreads,
+                                             int tid, double (*red)[MSF_MAX_RHS * KM]) {
+  const int I = agg / (d.ncy + 1), J = agg - (agg / (d.ncy + 1)) * (d.ncy + 1);
+  const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2;
+  const int gx0 = I * d.cx - d.cx, gy0 = J * d.cy - d.cy;
+  // interior of the padded box (chi vanishes on its boundary ring)
+  const int ix_lo = max(1, -gx0), ix_hi = min(d.bx - 2, d.nnx - 1 - gx0);
+  const int iy_lo = max(1, -gy0), iy_hi = min(d.by - 2, d.nny - 1 - gy0);
+  const int w = iy_hi - iy_lo + 1, h = ix_hi - ix_lo + 1;
+  double acc[MSF_MAX_RHS][KM];
+#pragma unroll
+  for (int r = 0; r < MSF_MAX_RHS; ++r)
+#pragma unroll
+    for (int a = 0; a < KM; ++a) acc[r][a] = 0.0;
+  for (int k = tid; k < w * h; k += nthreads) {
+    const int px = ix_lo + k / w, py = iy_lo + (k - (k / w) * w);
+    const size_t n = (size_t)(gx0 + px) * d.nny + (gy0 + py);
+    double2 tv[MSF_MAX_RHS];
+#pragma unroll
+    for (int r = 0; r < MSF_MAX_RHS; ++r) tv[r] = act[r] ? tall[(size_t)r * d.nn + n] : make_double2(0.0, 0.0);
+    const int bn = px * d.by + py;
+#pragma unroll
+    for (int a = 0; a < KM; ++a) {
+      if (a < d.kmax) {
+        const double2 pv = *reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2);
+#pragma unroll
+        for (int r = 0; r < MSF_MAX_RHS; ++r) acc[r][a] = fma(pv.x, tv[r].x, fma(pv.y, tv[r].y, acc[r][a]));
+      }
+    }
+  }
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int r = 0; r < MSF_MAX_RHS; ++r)
+#pragma unroll
+    for (int a = 0; a < KM; ++a) {
+      if (act[r] && a < d.kmax) {
+        const double v = warp_sum(acc[r][a]);
+        if (lane == 0) red[wid][r * KM + a] = v;
+      }
+    }
+  __syncthreads();
+  const int r = tid / KM, a = tid - (tid / KM) * KM;
+  if (r < MSF_MAX_RHS && a < d.kmax && act[r]) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < nthreads / 32; ++w2) s += red[w2][r * KM + a];
+    cball[(size_t)r * d.nbc * d.mc + (size_t)agg * d.kmax + a] = s;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ prolongation
+// z(n) += sum_{I,J,a} phi_{I,J,a}(n) x_c[slot(I,J,a)] for the realisations in act[].
+// Per-thread (node ix, iy).
+__device__ __forceinline__ void prolong_node(const Dims& d, const double* __restrict__ phi,
+                                             const int* __restrict__ cls_of_agg,
+                                             const double* __restrict__ cxall, double2* zall,
+                                             int ix, int iy, const bool (&act)[MSF_MAX_RHS]) {
+  double sx[MSF_MAX_RHS], sy[MSF_MAX_RHS];
+#pragma unroll
+  for (int r = 0; r < MSF_MAX_RHS; ++r) sx[r] = sy[r] = 0.0;
+  const int I0 = ix / d.cx, J0 = iy / d.cy;
+#pragma unroll
+  for (int di = 0; di < 2; ++di) {
+    const int I = I0 + di;
+    if (I > d.ncx) continue;
+    const int px = ix - (I * d.cx - d.cx);
+    if (px < 0 || px >= d.bx) continue;
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj) {
+      const int J = J0 + dj;
+      if (J > d.ncy) continue;
+      const int py = iy - (J * d.cy - d.cy);
+      if (py < 0 || py >= d.by) continue;
+      const int agg = I * (d.ncy + 1) + J;
+      const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2;
+      const int bn = px * d.by + py;
+      for (int a = 0; a < d.kmax; ++a) {
+        const double2 pv = *reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2);
+#pragma unroll
+        for (int r = 0; r < MSF_MAX_RHS; ++r) {
+          if (act[r]) {
+            const double cv = cxall[(size_t)r * d.nbc * d.mc + (size_t)agg * d.kmax + a];
+            sx[r] = fma(pv.x, cv, sx[r]);
+            sy[r] = fma(pv.y, cv, sy[r]);
+          }
+        }
+      }
+    }
+  }
+  const size_t n = (size_t)ix * d.nny + iy;
+#pragma unroll
+  for (int r = 0; r < MSF_MAX_RHS; ++r) {
+    if (act[r]) {
+      double2* z = zall + (size_t)r * d.nn;
+      double2 zv = z[n];
+      zv.x += sx[r];
+      zv.y += sy[r];
+      z[n] = zv;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ cyclic reduction
+// Row-chunked GEMVs: a CTA owns CR_ROWS rows of one block, one warp per row, lanes over
+// the (row-major, coalesced) columns; the neighbour vectors are staged in shared memory.
+constexpr int CR_ROWS = 16;
+
+// forward, survivor i, rows [r0, r0+CR_ROWS): b_i -= Q_{i-s} b_{i-s} + P_{i+s} b_{i+s}
+__device__ __forceinline__ void cr_forward_rows(const Dims& d, int i, int s, int r0,
+                                                const double* __restrict__ Q,
+                                                const double* __restrict__ P, double* cb,
+                                                double* sv, int tid, int nthreads) {
+  const int m = d.mc;
+  const bool hl = i - s >= 0, hr = i + s < d.nbc;
+  for (int k = tid; k < m; k += nthreads) {
+    sv[k] = hl ? cb[(size_t)(i - s) * m + k] : 0.0;
+    sv[m + k] = hr ? cb[(size_t)(i + s) * m + k] : 0.0;
+  }
+  __syncthreads();
+  const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
+  const int r1 = min(m, r0 + CR_ROWS);
+  for (int r = r0 + wid; r < r1; r += nw) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const double* Qr = Q + (size_t)r * m;
+    const double* Pr = P + (size_t)r * m;
+    int c = lane;
+    for (; c + 32 < m; c += 64) {
+      if (hl) {
+        a0 = fma(Qr[c], sv[c], a0);
+        a1 = fma(Qr[c + 32], sv[c + 32], a1);
+      }
+      if (hr) {
+        a2 = fma(Pr[c], sv[m + c], a2);
+        a3 = fma(Pr[c + 32], sv[m + c + 32], a3);
+      }
+    }
+    for (; c < m; c += 32) {
+      if (hl) a0 = fma(Qr[c], sv[c], a0);
+      if (hr) a2 = fma(Pr[c], sv[m + c], a2);
+    }
+    const double acc = warp_sum((a0 + a1) + (a2 + a3));
+    if (lane == 0) cb[(size_t)i * m + r] -= acc;
+  }
+  __syncthreads();
+}
+
+// back, eliminated k, rows [r0, r0+CR_ROWS): x_k = Dinv_k b_k - P_k^T x_{k-s} - Q_k^T x_{k+s}
+__device__ __forceinline__ void cr_back_rows(const Dims& d, int k, int s, int r0,
+                                             const double* __restrict__ Di,
+                                             const double* __restrict__ PT,
+                                             const double* __restrict__ QT,
+                                             const double* __restrict__ cb, double* cx,
+                                             double* sv, int tid, int nthreads) {
+  const int m = d.mc;
+  const bool hl = k - s >= 0, hr = k + s < d.nbc;
+  for (int j = tid; j < m; j += nthreads) {
+    sv[j] = cb[(size_t)k * m + j];
+    sv[m + j] = hl ? cx[(size_t)(k - s) * m + j] : 0.0;
+    sv[2 * m + j] = hr ? cx[(size_t)(k + s) * m + j] : 0.0;
+  }
+  __syncthreads();
+  const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
+  const int r1 = min(m, r0 + CR_ROWS);
+  for (int r = r0 + wid; r < r1; r += nw) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0;
+    const double* Dr = Di + (size_t)r * m;
+    const double* Pr = PT + (size_t)r * m;
+    const double* Qr = QT + (size_t)r * m;
+    int c = lane;
+    for (; c + 32 < m; c += 64) {
+      a0 = fma(Dr[c], sv[c], a0);
+      a1 = fma(Dr[c + 32], sv[c + 32], a1);
+      if (hl) {
+        a2 = fma(Pr[c], sv[m + c], a2);
+        a3 = fma(Pr[c + 32], sv[m + c + 32], a3);
+      }
+      if (hr) {
+        a4 = fma(Qr[c], sv[2 * m + c], a4);
+        a5 = fma(Qr[c + 32], sv[2 * m + c + 32], a5);
+      }
+    }
+    for (; c < m; c += 32) {
+      a0 = fma(Dr[c], sv[c], a0);
+      if (hl) a2 = fma(Pr[c], sv[m + c], a2);
+      if (hr) a4 = fma(Qr[c], sv[2 * m + c], a4);
+    }
+    const double acc = warp_sum((a0 + a1) - (a2 + a3) - (a4 + a5));
+    if (lane == 0) cx[(size_t)k * m + r] = acc;
+  }
+  __syncthreads();
+}
+
+}  // namespace msfk
