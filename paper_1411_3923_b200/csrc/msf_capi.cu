@@ -520,20 +520,21 @@ int msf_assemble_coarse(msf_ctx* c) {
 
 // two-level V-cycle z = M^{-1} r for realisations [0, nr) (reading R8)
 // rz_mode (fused into the post-smoothing): 0 none, 1 rz at PCG init, 2 rz + beta
+// f0_done: the zero-start colour-0 phase already ran (fused into the PCG update).
 static void enqueue_vcycle(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
-                           int rz_mode = 0) {
-  launch_sgs_sweep(c, rhs0, nr, r, z, gated, true, 0);        // z = SGS(0; r)
-  launch_residual(c, rhs0, nr, r, z, c->t, gated);             // t = r - K z
+                           int rz_mode = 0, bool f0_done = false) {
+  launch_sgs_sweep(c, rhs0, nr, r, z, gated, !f0_done, 0, f0_done);  // z = SGS(0; r)
+  launch_residual(c, rhs0, nr, r, z, c->t, gated);                    // t = r - K z
   launch_restrict(c, rhs0, nr, c->t, gated);
   launch_coarse_solve(c, rhs0, nr, gated);
   launch_prolong(c, rhs0, nr, z, gated);
-  launch_sgs_sweep(c, rhs0, nr, r, z, gated, false, rz_mode); // z = SGS(z; r) (+ r.z, beta)
+  launch_sgs_sweep(c, rhs0, nr, r, z, gated, false, rz_mode, false); // z = SGS(z; r) (+ r.z)
 }
 
 static void enqueue_iteration(msf_ctx* c, int nr) {
-  launch_matvec(c, 0, nr, c->pv, c->q, true, true);
-  launch_pcg_update_xr(c, nr);
-  enqueue_vcycle(c, 0, nr, c->r, c->z, true, 2);
+  launch_matvec(c, 0, nr, c->pv, c->q, true, true);   // q = K p, alpha
+  launch_update_f0(c, nr);                             // u, r, ||r||, z = F0(0; r)
+  enqueue_vcycle(c, 0, nr, c->r, c->z, true, 2, true);
   launch_pcg_p(c, nr, false);
 }
 
@@ -623,7 +624,7 @@ static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
     cudaGraphDestroy(g);
     c->iter_graph_R = nr;
   }
-  const int check_every = 4;
+  const int check_every = 8;
   int done = 0;
   for (int it = 0; it < max_it + check_every && !done; it += check_every) {
     for (int j = 0; j < check_every; ++j) {

@@ -220,6 +220,63 @@ __global__ void __launch_bounds__(VB) k_pcg_update_xr(Dims d, double2* uall, dou
   }
 }
 
+// Fused PCG update + first pre-smoothing colour: thread per node quad, u += alpha p,
+// r -= alpha q on the quad's 4 nodes, ||r||^2 (-> convergence, last block), then the
+// zero-start forward Gauss-Seidel phase of colour 0 (msfk::sgs_quad<.., ZERO>) with the new r.
+__global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const double* __restrict__ Eall,
+                                                    double2* uall, double2* rall,
+                                                    const double2* __restrict__ pall,
+                                                    const double2* __restrict__ qall, double2* zall,
+                                                    const uint8_t* __restrict__ fixn, PcgScalars* sc,
+                                                    double* partials, unsigned* counters,
+                                                    int max_partials) {
+  const int rhs = blockIdx.z;
+  if (!sc[rhs].active) return;
+  __shared__ double red[NTHR / 32 + 1];
+  const int qx = blockIdx.y * blockDim.y + threadIdx.y;
+  const int qy = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const double alpha = sc[rhs].alpha;
+  const size_t off = (size_t)rhs * d.nn;
+  double s = 0.0;
+#pragma unroll
+  for (int dn = 0; dn < 4; ++dn) {
+    const int gx = 2 * qx + (dn & 1), gy = 2 * qy + (dn >> 1);
+    if (gx < d.nnx && gy < d.nny) {
+      const size_t n = off + (size_t)gx * d.nny + gy;
+      const double2 pv = pall[n], qv = qall[n];
+      double2 uv = uall[n], rv = rall[n];
+      uv.x = fma(alpha, pv.x, uv.x);
+      uv.y = fma(alpha, pv.y, uv.y);
+      rv.x = fma(-alpha, qv.x, rv.x);
+      rv.y = fma(-alpha, qv.y, rv.y);
+      uall[n] = uv;
+      rall[n] = rv;
+      s += rv.x * rv.x + rv.y * rv.y;
+    }
+  }
+  sgs_quad<true, false, true, false>(d, K, Eall + (size_t)rhs * d.ne, rall + off, zall + off,
+                                     fixn, qx, qy, 0);
+  s = block_sum_all(s, red, tid, NTHR);
+  const unsigned nblk = gridDim.x * gridDim.y;
+  const int slot = blockIdx.y * gridDim.x + blockIdx.x;
+  if (arrive_last(s, partials + (size_t)rhs * max_partials, slot, counters + rhs * 8, nblk, tid)) {
+    const double tot = reduce_partials(partials + (size_t)rhs * max_partials, nblk, red, tid, NTHR);
+    if (tid == 0) {
+      PcgScalars& S = sc[rhs];
+      S.rr = tot;
+      S.iters += 1;
+      if (tot <= S.tol2 * S.fnorm2) {
+        S.active = 0;
+      } else if (S.iters >= S.max_it) {
+        S.active = 0;
+        S.noconv = 1;
+      }
+      counters[rhs * 8] = 0;
+    }
+  }
+}
+
 // p = z + beta p  (p = z at init)
 __global__ void __launch_bounds__(VB) k_pcg_p(Dims d, const double2* __restrict__ zall,
                                               double2* pall, const PcgScalars* sc, int init) {
@@ -323,7 +380,7 @@ void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double
 // One symmetric GS sweep as 7 colour launches F0 F1 F2 F3B3 B2 B1 B0.  zero_start: z = 0 on
 // entry (fused into F0); rz_mode != 0: r.z and beta fused into B0.
 void launch_sgs_sweep(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
-                      bool zero_start, int rz_mode) {
+                      bool zero_start, int rz_mode, bool skip_f0) {
   const Dims& d = c->d;
   const int hx = (d.nnx + 1) / 2, hy = (d.nny + 1) / 2;
   dim3 blk(32, 8);
@@ -337,7 +394,7 @@ void launch_sgs_sweep(msf_ctx* c, int rhs0, int nr, const double* r, double* z, 
   MSF_LAUNCHED(c)
   if (zero_start) {
     MSF_SGS(true, false, true, false, 0);
-  } else {
+  } else if (!skip_f0) {
     MSF_SGS(true, false, false, false, 0);
   }
   MSF_SGS(true, false, false, false, 1);
@@ -354,7 +411,18 @@ void launch_sgs_sweep(msf_ctx* c, int rhs0, int nr, const double* r, double* z, 
 }
 
 void launch_sgs(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated) {
-  launch_sgs_sweep(c, rhs0, nr, r, z, gated, false, 0);
+  launch_sgs_sweep(c, rhs0, nr, r, z, gated, false, 0, false);
+}
+
+void launch_update_f0(msf_ctx* c, int nr) {
+  const Dims& d = c->d;
+  const int hx = (d.nnx + 1) / 2, hy = (d.nny + 1) / 2;
+  dim3 grd((hy + 31) / 32, (hx + 7) / 8, nr);
+  k_update_f0<<<grd, dim3(32, 8), 0, c->stream>>>(
+      d, c->K0, c->E, (double2*)c->u, (double2*)c->r, (const double2*)c->pv,
+      (const double2*)c->q, (double2*)c->z, c->fixn, c->sc, c->partials, c->counters,
+      c->max_partials);
+  MSF_LAUNCHED(c);
 }
 
 void launch_mask_copy(msf_ctx* c, const double* x, double* y, int nn) {

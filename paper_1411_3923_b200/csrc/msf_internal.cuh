@@ -179,7 +179,9 @@ void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double
                      bool gated);
 void launch_sgs(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated);
 void launch_sgs_sweep(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
-                      bool zero_start, int rz_mode);
+                      bool zero_start, int rz_mode, bool skip_f0);
+// fused u/r update + ||r||^2 + zero-start forward GS colour 0 (PCG iteration)
+void launch_update_f0(msf_ctx* c, int nr);
 void launch_mask_copy(msf_ctx* c, const double* x, double* y, int n2nn);
 void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it);
 void launch_pcg_update_xr(msf_ctx* c, int nr);

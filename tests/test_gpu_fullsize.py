@@ -1,0 +1,127 @@
+"""GPU checks at BASELINE.json's full size (configs[1]: 1024x512 MBB, 1,051,650 DOF, 3 robust
+realisations) in the launch configuration bench.py times.  The oracle cannot run the whole
+solve at this size, so the checks are (a) outputs the oracle computes independently --
+projected tiles, K x via its assembled sparse K, local spectra of sampled agglomerates --
+and (b) properties that hold at any size: preconditioner symmetry/positivity, true residual
+of the returned solution under the oracle's operator, the energy identity f.u = u.K.u and
+the projection ordering of the realisations."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import fem, filters, msfem, problem
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+
+from paper_1411_3923_b200 import Msfem, build  # noqa: E402
+
+build.build()
+DEV = torch.device("cuda")
+SPEC = W.CONFIGS["c1_mbb_1024x512"]
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    m = Msfem.from_spec(SPEC)
+    x = W.design_tile(SPEC)
+    m.filter_project(torch.as_tensor(x, device=DEV))
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    return m, x
+
+
+@pytest.fixture(scope="module")
+def oracle_ops():
+    x = W.design_tile(SPEC)
+    fx, f = W.fixed_mask(SPEC), W.load_vector(SPEC)
+    K0 = fem.element_stiffness(SPEC.nu)
+    xt, xbars, xb_el, E = problem.element_moduli(SPEC, x)
+    A = [fem.constrained_operator(fem.assemble(SPEC.nelx, SPEC.nely, e, K0), fx) for e in E]
+    return dict(x=x, fx=fx, f=f, K0=K0, xbars=xbars, E=E, A=A)
+
+
+def test_fullsize_projection_and_moduli(ctx, oracle_ops):
+    m, _ = ctx
+    for k in range(SPEC.n_rhs):
+        xb = torch.empty(SPEC.tile_x * SPEC.tile_y, dtype=torch.float64, device=DEV)
+        Eg = torch.empty(SPEC.n_el, dtype=torch.float64, device=DEV)
+        m.get_physical(k, Eg, xb)
+        assert np.abs(host(xb) - oracle_ops["xbars"][k]).max() <= 1e-14
+        idx = np.random.default_rng(k).choice(SPEC.n_el, 5000, replace=False)
+        assert np.abs(host(Eg)[idx] - oracle_ops["E"][k][idx]).max() <= 1e-14 * SPEC.E0
+    # dilated embeds intermediate embeds eroded (etas 0.7, 0.5, 0.3)
+    xb = oracle_ops["xbars"]
+    assert np.all(xb[2] >= xb[1] - 1e-15) and np.all(xb[1] >= xb[0] - 1e-15)
+
+
+def test_fullsize_operator(ctx, oracle_ops):
+    m, _ = ctx
+    v = W.random_vectors(SPEC.n_dof, 1, seed=3)[0]
+    for k in range(SPEC.n_rhs):
+        y = torch.empty(SPEC.n_dof, dtype=torch.float64, device=DEV)
+        m.matvec(k, torch.as_tensor(v, device=DEV), y)
+        ref = oracle_ops["A"][k] @ v
+        assert np.abs(host(y) - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_fullsize_sampled_local_spectra(ctx, oracle_ops):
+    """Eigenvalues of sampled agglomerates (corner, edge, clamped-edge, interior classes)
+    against the oracle's dense generalised eigensolver."""
+    m, _ = ctx
+    _, nk, lam = m.get_basis()
+    ncx, ncy = SPEC.nelx // SPEC.cx, SPEC.nely // SPEC.cy
+    samples = [(0, 0), (0, ncy // 2), (ncx, 0), (ncx // 2, ncy), (17, 9), (40, 20)]
+    for I, J in samples:
+        Kl, D, *_ = msfem.local_problem(I, J, SPEC.nelx, SPEC.nely, SPEC.cx, SPEC.cy,
+                                        oracle_ops["E"][SPEC.dilated], oracle_ops["K0"],
+                                        oracle_ops["fx"])
+        lo, _ = msfem.local_eigenpairs(Kl, D, SPEC.n_modes)
+        agg = I * (ncy + 1) + J
+        assert nk[agg] == SPEC.n_modes
+        assert np.abs(lam[agg] - lo).max() <= 1e-9 * max(1.0, np.abs(lo).max()), (I, J)
+
+
+def test_fullsize_preconditioner_spd(ctx, oracle_ops):
+    m, _ = ctx
+    fx = oracle_ops["fx"]
+    V = W.random_vectors(SPEC.n_dof, 3, seed=11)
+    V[:, fx == 1] = 0
+    for k in range(SPEC.n_rhs):
+        Z = []
+        for v in V:
+            z = torch.empty(SPEC.n_dof, dtype=torch.float64, device=DEV)
+            m.precond_apply(k, torch.as_tensor(v, device=DEV), z)
+            Z.append(host(z))
+        for i in range(3):
+            assert Z[i] @ V[i] > 0
+            for j in range(i):
+                a, b = Z[i] @ V[j], Z[j] @ V[i]
+                assert abs(a - b) <= 1e-9 * max(abs(a), abs(b))
+
+
+def test_fullsize_pcg_residual_and_energy(ctx, oracle_ops):
+    m, _ = ctx
+    u = torch.empty(SPEC.n_rhs * SPEC.n_dof, dtype=torch.float64, device=DEV)
+    its, comps, noconv = m.pcg_solve(tol=SPEC.tol, max_it=5000, u=u)
+    assert not noconv
+    U = host(u).reshape(SPEC.n_rhs, SPEC.n_dof)
+    f = oracle_ops["f"]
+    for k in range(SPEC.n_rhs):
+        A = oracle_ops["A"][k]
+        r = f - A @ U[k]
+        # recursive residual <= tol; the true residual may differ by rounding drift only
+        assert np.linalg.norm(r) <= 10 * SPEC.tol * np.linalg.norm(f)
+        assert abs(comps[k] - f @ U[k]) <= 1e-12 * abs(comps[k])
+        e = U[k] @ (A @ U[k])
+        assert abs(e - comps[k]) <= 1e-6 * abs(comps[k])
+    # eroded (0.7) realisation is the most compliant, dilated (0.3) the stiffest
+    assert comps[0] > comps[1] > comps[2] > 0
