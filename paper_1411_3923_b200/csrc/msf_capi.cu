@@ -53,6 +53,8 @@ struct Plan {
   std::vector<double> fw;
   double wsum = 1.0;
   std::vector<CrLevel> cr;
+  std::vector<int> top_blocks;
+  size_t top_ptrs = 0;
   size_t jobs_bytes = 0;
   int max_partials = 0;
   size_t total = 0;
@@ -157,7 +159,18 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   // coarse cyclic-reduction levels
   P.cr.clear();
   size_t ptrs = 0, ints = 0;
+  // truncated: stop once at most top_max active blocks (multiples of s) remain; they form a
+  // dense top system inverted explicitly.  Default 1 block (plain cyclic reduction): a
+  // multi-block explicit inverse loses accuracy at high contrast (measured rel. error 7e-2 on
+  // a cond 3e12 K_c with 9 blocks), the per-level m x m Schur inverses do not.
+  int top_max = 1;
+  if (const char* e = std::getenv("MSF_TOP_BLOCKS")) top_max = std::max(1, std::atoi(e));
+  int s_top = 1;
   for (int s = 1; s < d.nbc; s *= 2) {
+    const int active = (d.nbc + s - 1) / s;
+    s_top = s;
+    if (active <= top_max || (long long)active * d.mc <= 0) break;
+    s_top = 2 * s;
     CrLevel L;
     L.s = s;
     for (int k = s; k < d.nbc; k += 2 * s) L.elim.push_back(k);
@@ -176,14 +189,12 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     ints += L.elim.size() + L.surv.size();
     P.cr.push_back(L);
   }
+  P.top_blocks.clear();
+  for (int i = 0; i < d.nbc; i += s_top) P.top_blocks.push_back(i);
   {
-    CrLevel L;
-    L.s = 0;
-    L.elim.push_back(0);
-    L.n_inv = d.R;
-    ptrs += 2 * L.n_inv;
-    ints += 1;
-    P.cr.push_back(L);
+    const long long T = (long long)P.top_blocks.size(), R = d.R;
+    P.top_ptrs = (size_t)T * (2 * R + 3 * R * (T - 1) + 3 * R * (T - 1) * (T - 1) +
+                              3 * R * (T - 1) + 2 * R);
   }
   P.jobs_bytes = align_up(ptrs * sizeof(double*)) + align_up(ints * sizeof(int));
   P.max_partials = std::max(apply_partials_needed(d), sgs_colour_partials_needed(d));
@@ -211,6 +222,14 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   add(2 * R * d.nbc * (size_t)d.mc * 8);     // cb, cx
   add((size_t)(3 * (d.n_agg + P.classes.size()) + d.n_agg) * 4);  // chunks, agg_by_cls
   add(P.jobs_bytes);
+  {
+    const size_t T = P.top_blocks.size(), mm = (size_t)d.mc * d.mc;
+    add(R * T * T * mm * 8);                 // Atop
+    add(R * mm * 8);                         // Pk
+    add(R * T * mm * 8);                     // W
+    add(P.top_ptrs * sizeof(double*));       // top job tables
+    add(T * 4);                              // top block list
+  }
   add(2 * MSF_MAX_RHS * 4);                  // factor_status
   add(R * sizeof(PcgScalars));
   add((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
@@ -341,6 +360,16 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
     c->agg_by_cls_d = ib + 3 * (d.n_agg + P.classes.size());
   }
   c->jobs_d = (char*)take(P.jobs_bytes);
+  {
+    const size_t T = P.top_blocks.size(), mm = (size_t)d.mc * d.mc;
+    c->top_blocks = P.top_blocks;
+    c->top_T = (int)T;
+    c->Atop = (double*)take(R * T * T * mm * 8);
+    c->top_Pk = (double*)take(R * mm * 8);
+    c->top_W = (double*)take(R * T * mm * 8);
+    c->top_jobs_d = (char*)take(P.top_ptrs * sizeof(double*));
+    c->top_blocks_d = (int*)take(T * 4);
+  }
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
   c->sc = (PcgScalars*)take(R * sizeof(PcgScalars));
   c->partials = (double*)take((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
@@ -422,6 +451,45 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
     std::vector<char> lv(cr_levels_dev_bytes((int)c->cr.size()));
     fill_cr_levels_dev(c->cr, lv.data());
     cudaMemcpyAsync(c->cr_levels_d, lv.data(), lv.size(), cudaMemcpyHostToDevice, c->stream);
+    // top-system Gauss-Jordan tables: step k pivots on block k
+    const int T = c->top_T;
+    const size_t mmb = (size_t)d.mc * d.mc;
+    auto At = [&](int rhs, int i, int j) { return c->Atop + (((size_t)rhs * T + i) * T + j) * mmb; };
+    auto Pk = [&](int rhs) { return c->top_Pk + (size_t)rhs * mmb; };
+    auto Wi = [&](int rhs, int i) { return c->top_W + ((size_t)rhs * T + i) * mmb; };
+    std::vector<double*> tp;
+    struct Off { size_t invsrc, inv, wA, wB, wC, uA, uB, uC, cps, cpd, tpd, ngs, ngd; };
+    std::vector<Off> offs;
+    for (int k = 0; k < T; ++k) {
+      Off o{};
+      o.invsrc = tp.size(); for (int r = 0; r < d.R; ++r) tp.push_back(At(r, k, k));
+      o.inv = tp.size();    for (int r = 0; r < d.R; ++r) tp.push_back(Pk(r));
+      o.wA = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(At(r, i, k));
+      o.wB = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(Pk(r));
+      o.wC = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(Wi(r, i));
+      o.uA = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) for (int j = 0; j < T; ++j) if (i != k && j != k) tp.push_back(Wi(r, i));
+      o.uB = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) for (int j = 0; j < T; ++j) if (i != k && j != k) tp.push_back(At(r, k, j));
+      o.uC = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) for (int j = 0; j < T; ++j) if (i != k && j != k) tp.push_back(At(r, i, j));
+      o.cps = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(Wi(r, i));
+      o.cpd = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(At(r, i, k));
+      o.tpd = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(At(r, k, i));
+      o.ngs = tp.size(); for (int r = 0; r < d.R; ++r) tp.push_back(Pk(r));
+      o.ngd = tp.size(); for (int r = 0; r < d.R; ++r) tp.push_back(At(r, k, k));
+      offs.push_back(o);
+    }
+    double** base = (double**)c->top_jobs_d;
+    c->top_steps.assign(T, TopStep());
+    for (int k = 0; k < T; ++k) {
+      TopStep& S = c->top_steps[k];
+      const Off& o = offs[k];
+      S.nI = d.R; S.invsrc = base + o.invsrc; S.inv = base + o.inv;
+      S.nW = d.R * (T - 1); S.wA = base + o.wA; S.wB = base + o.wB; S.wC = base + o.wC;
+      S.nU = d.R * (T - 1) * (T - 1); S.uA = base + o.uA; S.uB = base + o.uB; S.uC = base + o.uC;
+      S.nC = d.R * (T - 1); S.cps = base + o.cps; S.cpd = base + o.cpd; S.tpd = base + o.tpd;
+      S.ngs = base + o.ngs; S.ngd = base + o.ngd;
+    }
+    cudaMemcpyAsync(c->top_jobs_d, tp.data(), tp.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(c->top_blocks_d, c->top_blocks.data(), c->top_blocks.size() * 4, cudaMemcpyHostToDevice, c->stream);
     cudaStreamSynchronize(c->stream);   // host staging buffers go out of scope
   }
 

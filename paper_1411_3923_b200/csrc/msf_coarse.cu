@@ -336,6 +336,63 @@ __global__ void k_transpose_blocks(double** src, const double* src_base, double*
   }
 }
 
+// ------------------------------------------------------------------ dense top system
+// Top (T*m x T*m, block-major) from the diagonal / coupling blocks of the active blocks tb[]
+// left after the truncated cyclic reduction.
+__global__ void k_build_top(Dims d, const int* __restrict__ tb, int T, const double* __restrict__ Dall,
+                            const double* __restrict__ Uall, double* Atop) {
+  const int rhs = blockIdx.y, m = d.mc;
+  const size_t mm = (size_t)m * m, per = (size_t)T * T * mm;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < per;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const int blk = (int)(e / mm), w = (int)(e - (size_t)blk * mm);
+    const int bi = blk / T, bj = blk - bi * T, rr = w / m, cc = w - (w / m) * m;
+    double v = 0.0;
+    const size_t base = (size_t)rhs * d.nbc;
+    if (bi == bj) v = Dall[(base + tb[bi]) * mm + (size_t)rr * m + cc];
+    else if (bj == bi + 1) v = Uall[(base + tb[bi]) * mm + (size_t)rr * m + cc];
+    else if (bi == bj + 1) v = Uall[(base + tb[bj]) * mm + (size_t)cc * m + rr];
+    Atop[(size_t)rhs * per + e] = v;
+  }
+}
+
+// dst = scale * src^T (trans) or dst = scale * src, for pointer-table block batches
+template <bool TRANS>
+__global__ void k_copy_blocks_ex(double** src, double** dst, int m, double scale) {
+  __shared__ double tile[32][33];
+  const double* S = src[blockIdx.z];
+  double* D = dst[blockIdx.z];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int r = by + j, c = bx + threadIdx.x;
+    if (r < m && c < m) tile[j][threadIdx.x] = S[(size_t)r * m + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    if (TRANS) {
+      const int r = bx + j, c = by + threadIdx.x;
+      if (r < m && c < m) D[(size_t)r * m + c] = scale * tile[threadIdx.x][j];
+    } else {
+      const int r = by + j, c = bx + threadIdx.x;
+      if (r < m && c < m) D[(size_t)r * m + c] = scale * tile[j][threadIdx.x];
+    }
+  }
+}
+
+// x_top = -A b_top  (A = -Top^{-1})
+__global__ void __launch_bounds__(256) k_top_solve(Dims d, const int* __restrict__ tb, int T,
+                                                   const double* __restrict__ Atop,
+                                                   const double* __restrict__ cball, double* cxall,
+                                                   const PcgScalars* sc, int rhs0, int gated) {
+  const int rhs = rhs0 + blockIdx.y;
+  if (gated && !sc[rhs].active) return;
+  extern __shared__ double sv[];   // [T*m]
+  const size_t mm = (size_t)d.mc * d.mc;
+  top_solve_rows(d, tb, T, Atop + (size_t)rhs * T * T * mm, cball + (size_t)rhs * d.nbc * d.mc,
+                 cxall + (size_t)rhs * d.nbc * d.mc, blockIdx.x * CR_ROWS, sv, threadIdx.x,
+                 blockDim.x);
+}
+
 }  // namespace
 
 // ================================================================== host side
@@ -420,6 +477,39 @@ void launch_assemble_coarse(msf_ctx* c) {
       MSF_LAUNCHED(c);
     }
   }
+  // dense inverse of the remaining top system by block Gauss-Jordan (block sweep operator):
+  // pivot k: Pk = A_kk^-1, W_i = A_ik Pk, A_ij -= W_i A_kj, A_ik = W_i, A_ki = W_i^T,
+  // A_kk = -Pk; after all pivots A = -Top^-1.
+  const int T = c->top_T;
+  {
+    const size_t per = (size_t)T * T * m * m;
+    const int blocks = (int)std::min<size_t>((per + 255) / 256, 65535);
+    k_build_top<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->top_blocks_d, T, c->Dc, c->Uc, c->Atop);
+    MSF_LAUNCHED(c);
+  }
+  const dim3 tg((m + 31) / 32, (m + 31) / 32);
+  for (const TopStep& S : c->top_steps) {
+    k_copy_blocks<<<dim3(64, S.nI), 256, 0, c->stream>>>(S.invsrc, S.inv, m);
+    MSF_LAUNCHED(c);
+    k_spd_inverse<<<S.nI, 1024, inv_smem, c->stream>>>(S.inv, m, c->factor_status);
+    MSF_LAUNCHED(c);
+    if (S.nW) {
+      k_gemm<false, false><<<dim3(gt.x, gt.y, S.nW), 256, 0, c->stream>>>(S.wA, S.wB, S.wC, m, 1.0, 0.0);
+      MSF_LAUNCHED(c);
+    }
+    if (S.nU) {
+      k_gemm<false, false><<<dim3(gt.x, gt.y, S.nU), 256, 0, c->stream>>>(S.uA, S.uB, S.uC, m, -1.0, 1.0);
+      MSF_LAUNCHED(c);
+    }
+    if (S.nC) {
+      k_copy_blocks_ex<false><<<dim3(tg.x, tg.y, S.nC), dim3(32, 8), 0, c->stream>>>(S.cps, S.cpd, m, 1.0);
+      MSF_LAUNCHED(c);
+      k_copy_blocks_ex<true><<<dim3(tg.x, tg.y, S.nC), dim3(32, 8), 0, c->stream>>>(S.cps, S.tpd, m, 1.0);
+      MSF_LAUNCHED(c);
+    }
+    k_copy_blocks_ex<false><<<dim3(tg.x, tg.y, S.nI), dim3(32, 8), 0, c->stream>>>(S.ngs, S.ngd, m, -1.0);
+    MSF_LAUNCHED(c);
+  }
 }
 
 // c <- K_c^{-1} c for realisations [rhs0, rhs0+nr): forward elimination over the levels,
@@ -429,19 +519,23 @@ void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
   const int m = d.mc;
   const int nthr = 256;
   for (const CrLevel& L : c->cr) {
-    if (L.s == 0) continue;
     if (!L.surv.empty()) {
       k_cr_forward<<<dim3((m + 15) / 16, (unsigned)L.surv.size(), nr), nthr, 2 * m * sizeof(double),
                      c->stream>>>(d, L.surv_d, L.s, c->Qc, c->Pc, c->cb, c->sc, rhs0, gated ? 1 : 0);
       MSF_LAUNCHED(c);
     }
   }
-  // final level: x_0 = Dinv_0 b_0 (k_cr_back with no neighbours: s = nbc)
+  // dense top system: one row-chunked GEMV
+  {
+    const int T = c->top_T, n = T * m;
+    k_top_solve<<<dim3((n + CR_ROWS - 1) / CR_ROWS, nr), nthr, (size_t)n * sizeof(double), c->stream>>>(
+        d, c->top_blocks_d, T, c->Atop, c->cb, c->cx, c->sc, rhs0, gated ? 1 : 0);
+    MSF_LAUNCHED(c);
+  }
   for (auto it = c->cr.rbegin(); it != c->cr.rend(); ++it) {
     const CrLevel& L = *it;
-    const int s = L.s == 0 ? d.nbc : L.s;
     k_cr_back<<<dim3((m + 15) / 16, (unsigned)L.elim.size(), nr), nthr, 3 * m * sizeof(double),
-                c->stream>>>(d, L.elim_d, s, c->Dinv, c->PTc, c->QTc, c->cb, c->cx, c->sc, rhs0,
+                c->stream>>>(d, L.elim_d, L.s, c->Dinv, c->PTc, c->QTc, c->cb, c->cx, c->sc, rhs0,
                              gated ? 1 : 0);
     MSF_LAUNCHED(c);
   }

@@ -77,6 +77,17 @@ struct CrLevel {
   int nU = 0;     double** uA = nullptr;   double** uB = nullptr;  double** uC = nullptr;
 };
 
+// One block Gauss-Jordan step (pivot block k) of the dense inverse of the top system left
+// after the truncated cyclic reduction.  Pointer tables (device) cover all realisations.
+struct TopStep {
+  int nI = 0;  double** invsrc = nullptr; double** inv = nullptr;           // Pk = inv(A_kk)
+  int nW = 0;  double** wA = nullptr; double** wB = nullptr; double** wC = nullptr;  // W_i = A_ik Pk
+  int nU = 0;  double** uA = nullptr; double** uB = nullptr; double** uC = nullptr;  // A_ij -= W_i A_kj
+  int nC = 0;  double** cps = nullptr; double** cpd = nullptr;                        // A_ik = W_i
+               double** tpd = nullptr;                                             // A_ki = W_i^T
+  double** ngs = nullptr; double** ngd = nullptr;                                  // A_kk = -Pk
+};
+
 struct msf_ctx {
   msf_problem p{};
   Dims d{};
@@ -143,6 +154,16 @@ struct msf_ctx {
   int* agg_by_cls_d = nullptr;  // agglomerates grouped by class
   int n_chunks = 0;
   std::vector<int> chunks_h, agg_by_cls_h;
+  // top system after the truncated cyclic reduction: T active blocks (stride top_stride),
+  // dense inverse stored block-major [R][T][T][mc*mc] as -Top^{-1}
+  std::vector<int> top_blocks;
+  int top_T = 0;
+  int* top_blocks_d = nullptr;
+  double* Atop = nullptr;       // [R][T*T][mc*mc]
+  double* top_Pk = nullptr;     // [R][mc*mc] scratch
+  double* top_W = nullptr;      // [R][T][mc*mc] scratch
+  std::vector<TopStep> top_steps;
+  char* top_jobs_d = nullptr;
   void* cr_levels_d = nullptr;  // CrLevelDev[n levels] for the persistent PCG kernel
   bool persistent = true;       // PCG driver: persistent cooperative kernel (else CUDA graph)
   void* prof_d = nullptr;       // debug phase timeline of the persistent kernel (env MSF_PERSIST_PROFILE)
@@ -205,6 +226,7 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated);
 int launch_pcg_persistent(msf_ctx* c, int nr);
 size_t cr_levels_dev_bytes(int nlev);
 void fill_cr_levels_dev(const std::vector<CrLevel>& cr, void* host_buf);
+constexpr int MSF_TOP_MAX = 1200;   // max unknowns of the dense top system (T * mc)
 constexpr int MSF_PERSIST_PARTIALS = 3 * MSF_MAX_RHS * 4 * 160;  // 3 slots x 4 rhs x grid
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated);
 void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated);

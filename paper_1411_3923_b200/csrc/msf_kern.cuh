@@ -417,4 +417,39 @@ __device__ __forceinline__ void cr_back_rows(const Dims& d, int k, int s, int r0
   __syncthreads();
 }
 
+// top system after the truncated cyclic reduction, rows [r0, r0+CR_ROWS) of
+// x_top = -A b_top with A = -Top^{-1} stored block-major (T x T blocks of m x m); b_top is
+// gathered from the active blocks tb[] of cb, x_top scattered into cx.
+__device__ __forceinline__ void top_solve_rows(const Dims& d, const int* __restrict__ tb, int T,
+                                               const double* __restrict__ A,
+                                               const double* __restrict__ cb, double* cx, int r0,
+                                               double* sv, int tid, int nthreads) {
+  const int m = d.mc, n = T * m;
+  const size_t mm = (size_t)m * m;
+  for (int j = tid; j < n; j += nthreads) {
+    const int bj = j / m;
+    sv[j] = cb[(size_t)tb[bj] * m + (j - bj * m)];
+  }
+  __syncthreads();
+  const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
+  const int r1 = min(n, r0 + CR_ROWS);
+  for (int r = r0 + wid; r < r1; r += nw) {
+    const int bi = r / m, rr = r - bi * m;
+    double a0 = 0.0, a1 = 0.0;
+    for (int bj = 0; bj < T; ++bj) {
+      const double* Ar = A + ((size_t)bi * T + bj) * mm + (size_t)rr * m;
+      const double* v = sv + bj * m;
+      int c = lane;
+      for (; c + 32 < m; c += 64) {
+        a0 = fma(Ar[c], v[c], a0);
+        a1 = fma(Ar[c + 32], v[c + 32], a1);
+      }
+      for (; c < m; c += 32) a0 = fma(Ar[c], v[c], a0);
+    }
+    const double acc = warp_sum(a0 + a1);
+    if (lane == 0) cx[(size_t)tb[bi] * m + rr] = -acc;
+  }
+  __syncthreads();
+}
+
 }  // namespace msfk

@@ -63,6 +63,9 @@ struct PersistArgs {
   const double* QTc;
   const CrLevelDev* levels;
   int nlev;
+  const int* top_blocks;   // active blocks of the dense top system
+  int topT;
+  const double* Atop;      // [R][T*T][mc*mc], -Top^{-1}
   PcgScalars* sc;
   double* part;   // [3][MSF_MAX_RHS][gridDim.x]
   int nr;
@@ -292,9 +295,20 @@ __global__ void __launch_bounds__(PT, PMINB) k_pcg_persistent(PersistArgs A, K0M
       }
       gsync();
     }
+    {
+      const int n = A.topT * d.mc, nrt = (n + CR_ROWS - 1) / CR_ROWS;
+      for (int item = b; item < nrt * nr; item += G) {
+        const int k = item / nrt, rc = item - k * nrt;
+        if (!act[k]) continue;
+        top_solve_rows(d, A.top_blocks, A.topT, A.Atop + (size_t)k * A.topT * A.topT * per,
+                       A.cb + (size_t)k * d.nbc * d.mc, A.cx + (size_t)k * d.nbc * d.mc,
+                       rc * CR_ROWS, sv, tid, PT);
+      }
+      gsync();
+    }
     for (int l = A.nlev - 1; l >= 0; --l) {
       const CrLevelDev L = A.levels[l];
-      const int s = L.s == 0 ? d.nbc : L.s;
+      const int s = L.s;
       for (int item = b; item < nrc * L.nelim * nr; item += G) {
         const int k = item / (nrc * L.nelim), rest = item - k * (nrc * L.nelim);
         if (!act[k]) continue;
@@ -384,7 +398,8 @@ __global__ void __launch_bounds__(PT, PMINB) k_pcg_persistent(PersistArgs A, K0M
 template <int KM>
 int launch_persistent_km(msf_ctx* c, int nr) {
   const Dims& d = c->d;
-  const size_t smem = std::max(sizeof(TileSmem), (size_t)3 * d.mc * sizeof(double));
+  const size_t smem = std::max(sizeof(TileSmem),
+                               (size_t)std::max(3, c->top_T) * d.mc * sizeof(double));
   cudaFuncSetAttribute(k_pcg_persistent<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
@@ -419,6 +434,9 @@ int launch_persistent_km(msf_ctx* c, int nr) {
   A.QTc = c->QTc;
   A.levels = (const CrLevelDev*)c->cr_levels_d;
   A.nlev = (int)c->cr.size();
+  A.top_blocks = c->top_blocks_d;
+  A.topT = c->top_T;
+  A.Atop = c->Atop;
   A.sc = c->sc;
   A.part = c->partials;
   A.nr = nr;
