@@ -61,45 +61,59 @@ __global__ void __launch_bounds__(NT) k_prolong(Dims d, const double* __restrict
 
 // ------------------------------------------------------------------ Galerkin cell products
 // Kcell[rhs][cell][p][q] = sum_{e in cell} E_e Phi_e[:,p]^T K0 Phi_e[:,q],  p,q in 0..4k-1,
-// p = corner*k + a, corner = ci*2 + cj for coarse node (CI+ci, CJ+cj).
-__global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const double* __restrict__ Eall,
-                                                      const double* __restrict__ phi,
-                                                      const int* __restrict__ cls_of_agg,
-                                                      double* Kcell) {
-  extern __shared__ double sm[];
-  const int rhs = blockIdx.y;
-  const int cell = blockIdx.x;
-  const int CI = cell / d.ncy, CJ = cell - (cell / d.ncy) * d.ncy;
-  const int km = d.kmax, P = 4 * km;
-  const int ncn_y = d.cy + 1, ncn = (d.cx + 1) * (d.cy + 1);
-  double* PhiC = sm;                          // [ncn][2][P]
-  double* V = PhiC + (size_t)ncn * 2 * P;     // [16][8][P]
-  double* Ech = V + 16 * 8 * P;               // [16]
-  // load Phi_C
-  for (int k = threadIdx.x; k < ncn * 2 * P; k += NT) {
-    const int p = k % P;
-    const int nc = k / P;                     // node*2 + comp
+// p = corner*k + a, corner = ci*2 + cj for coarse node (CI+ci, CJ+cj).  The (4k)x(4k) output
+// is computed in CH x CH chunks (blockIdx.z = chunk pair) so the staged cell bases fit in
+// shared memory for any mode count; with a single chunk Phi_p and Phi_q coincide.
+__device__ __forceinline__ void stage_cell_cols(const Dims& d, const double* __restrict__ phi,
+                                                const int* __restrict__ cls_of_agg, int CI, int CJ,
+                                                int c0, int cw, int CH, double* S) {
+  const int km = d.kmax, ncn_y = d.cy + 1, ncn = (d.cx + 1) * (d.cy + 1);
+  for (int k = threadIdx.x; k < ncn * 2 * CH; k += NT) {
+    const int j = k % CH, nc = k / CH;          // column j, node*2 + comp
+    if (j >= cw) continue;
     const int comp = nc & 1, node = nc >> 1;
     const int lx = node / ncn_y, ly = node - (node / ncn_y) * ncn_y;
+    const int p = c0 + j;
     const int corner = p / km, a = p - (p / km) * km;
     const int I = CI + (corner >> 1), J = CJ + (corner & 1);
     const int px = CI * d.cx + lx - (I * d.cx - d.cx), py = CJ * d.cy + ly - (J * d.cy - d.cy);
     const int agg = I * (d.ncy + 1) + J;
-    PhiC[k] = phi[(((size_t)cls_of_agg[agg] * d.kmax + a) * d.box_nodes + px * d.by + py) * 2 + comp];
+    S[k] = phi[(((size_t)cls_of_agg[agg] * d.kmax + a) * d.box_nodes + px * d.by + py) * 2 + comp];
   }
+}
+
+__global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const double* __restrict__ Eall,
+                                                      const double* __restrict__ phi,
+                                                      const int* __restrict__ cls_of_agg,
+                                                      double* Kcell, int CH) {
+  extern __shared__ double sm[];
+  const int rhs = blockIdx.y;
+  const int cell = blockIdx.x;
+  const int CI = cell / d.ncy, CJ = cell - (cell / d.ncy) * d.ncy;
+  const int P = 4 * d.kmax;
+  const int nch = (P + CH - 1) / CH;
+  const int pc = blockIdx.z / nch, qc = blockIdx.z - pc * nch;
+  const int p0 = pc * CH, q0 = qc * CH, pw = min(CH, P - p0), qw = min(CH, P - q0);
+  const int ncn_y = d.cy + 1, ncn = (d.cx + 1) * (d.cy + 1);
+  const bool single = nch == 1;
+  double* PhiP = sm;                                       // [ncn][2][CH]
+  double* PhiQ = single ? PhiP : PhiP + (size_t)ncn * 2 * CH;
+  double* V = PhiQ + (size_t)ncn * 2 * CH;                 // [16][8][CH]
+  double* Ech = V + 16 * 8 * CH;                           // [16]
+  stage_cell_cols(d, phi, cls_of_agg, CI, CJ, p0, pw, CH, PhiP);
+  if (!single) stage_cell_cols(d, phi, cls_of_agg, CI, CJ, q0, qw, CH, PhiQ);
   const double* E = Eall + (size_t)rhs * d.ne;
   const int nel = d.cx * d.cy;
-  const int nent = P * P;
-  double acc[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+  const int nent = CH * CH;   // <= NT
+  double acc = 0.0;
   __syncthreads();
   for (int e0 = 0; e0 < nel; e0 += 16) {
     const int ne = min(16, nel - e0);
-    // V_e = K0 Phi_e for the chunk
-    for (int k = threadIdx.x; k < ne * 8 * P; k += NT) {
-      const int p = k % P, rest = k / P;
+    // V_e = K0 Phi_e[:, q-chunk] for the element chunk
+    for (int k = threadIdx.x; k < ne * 8 * CH; k += NT) {
+      const int q = k % CH, rest = k / CH;
       const int i = rest & 7, el = rest >> 3;
+      if (q >= qw) continue;
       const int le = e0 + el;
       const int lex = le / d.cy, ley = le - (le / d.cy) * d.cy;
       double s = 0.0;
@@ -107,9 +121,9 @@ __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const dou
       for (int j = 0; j < 8; ++j) {
         const int b = j >> 1, comp = j & 1;
         const int nx = lex + ((b == 1 || b == 2) ? 1 : 0), ny = ley + ((b >= 2) ? 1 : 0);
-        s = fma(K.v[i * 8 + j], PhiC[((nx * ncn_y + ny) * 2 + comp) * P + p], s);
+        s = fma(K.v[i * 8 + j], PhiQ[((nx * ncn_y + ny) * 2 + comp) * CH + q], s);
       }
-      V[(el * 8 + i) * P + p] = s;
+      V[(el * 8 + i) * CH + q] = s;
     }
     for (int el = threadIdx.x; el < ne; el += NT) {
       const int le = e0 + el;
@@ -117,12 +131,10 @@ __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const dou
       Ech[el] = E[(size_t)(CI * d.cx + lex) * d.nely + CJ * d.cy + ley];
     }
     __syncthreads();
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-      const int ent = threadIdx.x + s * NT;
-      if (ent < nent) {
-        const int p = ent / P, q = ent - (ent / P) * P;
-        double a = acc[s];
+    const int ent = threadIdx.x;
+    if (ent < nent) {
+      const int p = ent / CH, q = ent - (ent / CH) * CH;
+      if (p < pw && q < qw) {
         for (int el = 0; el < ne; ++el) {
           const int le = e0 + el;
           const int lex = le / d.cy, ley = le - (le / d.cy) * d.cy;
@@ -131,20 +143,19 @@ __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const dou
           for (int i = 0; i < 8; ++i) {
             const int b = i >> 1, comp = i & 1;
             const int nx = lex + ((b == 1 || b == 2) ? 1 : 0), ny = ley + ((b >= 2) ? 1 : 0);
-            t = fma(PhiC[((nx * ncn_y + ny) * 2 + comp) * P + p], V[(el * 8 + i) * P + q], t);
+            t = fma(PhiP[((nx * ncn_y + ny) * 2 + comp) * CH + p], V[(el * 8 + i) * CH + q], t);
           }
-          a = fma(Ech[el], t, a);
+          acc = fma(Ech[el], t, acc);
         }
-        acc[s] = a;
       }
     }
     __syncthreads();
   }
-  double* out = Kcell + ((size_t)rhs * d.ncx * d.ncy + cell) * nent;
-#pragma unroll
-  for (int s = 0; s < 16; ++s) {
-    const int ent = threadIdx.x + s * NT;
-    if (ent < nent) out[ent] = acc[s];
+  const int ent = threadIdx.x;
+  if (ent < nent) {
+    const int p = ent / CH, q = ent - (ent / CH) * CH;
+    if (p < pw && q < qw)
+      Kcell[((size_t)rhs * d.ncx * d.ncy + cell) * P * P + (size_t)(p0 + p) * P + (q0 + q)] = acc;
   }
 }
 
@@ -420,10 +431,19 @@ void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
 void launch_coarse_galerkin(msf_ctx* c) {
   const Dims& d = c->d;
   const int P = 4 * d.kmax;
-  const size_t smem = ((size_t)(d.cx + 1) * (d.cy + 1) * 2 * P + 16 * 8 * P + 16) * sizeof(double);
+  const size_t ncn2 = (size_t)(d.cx + 1) * (d.cy + 1) * 2;
+  // largest column chunk whose staged bases fit in shared memory (<= 16 so CH^2 <= NT)
+  int CH = std::min(P, 16);
+  auto smem_for = [&](int ch) {
+    const bool single = ch >= P;
+    return ((single ? 1 : 2) * ncn2 * ch + 16 * 8 * (size_t)ch + 16) * sizeof(double);
+  };
+  while (CH > 2 && smem_for(CH) > 220 * 1024) CH /= 2;
+  const size_t smem = smem_for(CH);
+  const int nch = (P + CH - 1) / CH;
   cudaFuncSetAttribute(k_cell_galerkin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_cell_galerkin<<<dim3(d.ncx * d.ncy, d.R), NT, smem, c->stream>>>(d, c->K0, c->E, c->phi,
-                                                                     c->cls_of_agg_d, c->Kcell);
+  k_cell_galerkin<<<dim3(d.ncx * d.ncy, d.R, nch * nch), NT, smem, c->stream>>>(
+      d, c->K0, c->E, c->phi, c->cls_of_agg_d, c->Kcell, CH);
   MSF_LAUNCHED(c);
   {
     const size_t total = (size_t)2 * d.nbc * d.mc * d.mc;
@@ -518,6 +538,13 @@ void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
   const Dims& d = c->d;
   const int m = d.mc;
   const int nthr = 256;
+  if (3 * (size_t)m * sizeof(double) > 48 * 1024 ||
+      (size_t)c->top_T * m * sizeof(double) > 48 * 1024) {
+    const int need = (int)(std::max<size_t>(3, c->top_T) * m * sizeof(double));
+    cudaFuncSetAttribute(k_cr_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
+    cudaFuncSetAttribute(k_cr_back, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
+    cudaFuncSetAttribute(k_top_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
+  }
   for (const CrLevel& L : c->cr) {
     if (!L.surv.empty()) {
       k_cr_forward<<<dim3((m + 15) / 16, (unsigned)L.surv.size(), nr), nthr, 2 * m * sizeof(double),

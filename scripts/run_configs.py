@@ -1,0 +1,40 @@
+"""Runs one full design iteration of every BASELINE config on cuda:0 and reports PCG
+iterations, compliances and wall times per phase (smoke test of the whole path at scale)."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import workloads as W
+from paper_1411_3923_b200 import Msfem
+
+def run(spec, emin=None):
+    if emin is not None:
+        spec = spec.replace(Emin=emin)
+    t0 = time.perf_counter()
+    m = Msfem.from_spec(spec)
+    x = torch.as_tensor(W.design_tile(spec), device="cuda")
+    xn = torch.empty_like(x)
+    torch.cuda.synchronize(); t1 = time.perf_counter()
+    def timed(f):
+        torch.cuda.synchronize(); a = time.perf_counter(); r = f(); torch.cuda.synchronize()
+        return r, time.perf_counter() - a
+    _, tf = timed(lambda: m.filter_project(x))
+    _, tb = timed(m.build_coarse_basis)
+    _, ta = timed(m.assemble_coarse)
+    (its, comps, nc), tp = timed(lambda: m.pcg_solve(tol=spec.tol, max_it=20000))
+    (F, g, c), ts = timed(lambda: m.sensitivities(kappa=spec.kappa, volfrac=spec.volfrac))
+    out = dict(config=spec.name, emin=spec.Emin, n_dof=spec.n_dof, setup_s=round(t1 - t0, 3),
+               filter_s=round(tf, 4), basis_s=round(tb, 4), assemble_s=round(ta, 4), pcg_s=round(tp, 3),
+               sens_s=round(ts, 4), iters=its, noconv=nc, compliance=[float("%.6e" % v) for v in comps],
+               dof_iter_per_s=spec.n_dof * sum(its) / tp, info={k: v for k, v in m.info().items() if k in ("n_classes", "m", "coarse_slots", "eig_iters", "workspace_bytes")})
+    print(json.dumps(out), flush=True)
+    del m
+    torch.cuda.empty_cache()
+
+names = sys.argv[1:] or list(W.CONFIGS)
+for n in names:
+    spec = W.CONFIGS[n]
+    if n.startswith("c3"):
+        for e in (1e-3, 1e-6, 1e-9):
+            run(spec, e)
+    else:
+        run(spec)

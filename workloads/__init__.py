@@ -175,11 +175,13 @@ CONFIGS = {
         name="c2_cantilever_2048x1024", nelx=2048, nely=1024, cx=16, cy=16, n_modes=6,
         tile_x=64, tile_y=1, bc="cantilever", design="iid", Emin=1e-9, penal=3.0,
         rmin=2.5, beta=8.0, etas=(0.7, 0.5, 0.3), dilated=2, volfrac=0.5, tol=1e-8, seed=3),
-    # configs[3]: contrast sweep 2048x2048 binary periodic 32x32 cells (solid 0.4)
+    # configs[3]: contrast sweep 2048x2048 binary periodic 32x32 cells (solid 0.4); the
+    # paper's lambda_Omega selection with a 16-mode cap (reading R5):
+    # a fixed 4 modes is not contrast-independent for a binary microstructure
     "c3_square_2048": ProblemSpec(
-        name="c3_square_2048", nelx=2048, nely=2048, cx=16, cy=16, n_modes=4,
+        name="c3_square_2048", nelx=2048, nely=2048, cx=16, cy=16, n_modes=16,
         tile_x=32, tile_y=32, bc="cantilever", design="binary", Emin=1e-9, penal=3.0,
-        etas=(0.5,), dilated=0, tol=1e-8, seed=4),
+        etas=(0.5,), dilated=0, tol=1e-8, seed=4, lam_threshold=5e-3),
     # configs[4]: MBB 5120x2560 (~26.2M DOF), 40x40 cells, 20x20 coarse, 3 robust RHS
     "c4_mbb_5120x2560": ProblemSpec(
         name="c4_mbb_5120x2560", nelx=5120, nely=2560, cx=20, cy=20, n_modes=4,
