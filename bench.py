@@ -9,8 +9,12 @@ second (whole job, all ranks).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): every rank runs an independent replica of the workload (weak scaling);
-the strip-partitioned multi-GPU solve is not implemented yet (DESIGN.md §8 row "multi-GPU").
+N > 1 (torchrun): the grid of the SAME workload is strip-partitioned over the ranks
+(msf_dist_setup with the NCCL transport; halo exchanges and all-reduces
+inside the library, coarse space replicated), so the total work is fixed (strong scaling);
+value = n_dof x PCG iterations / max-over-ranks time.  --mode replicas instead runs an
+independent copy per rank (weak scaling).  BASELINE configs[4] (--config c4_mbb_5120x2560)
+is the paper-sized strip-scaling study.
 """
 from __future__ import annotations
 
@@ -158,6 +162,7 @@ def run_ours(args, spec):
     import torch
     import torch.distributed as dist
 
+    import paper_1411_3923_b200 as pkg
     from paper_1411_3923_b200 import Msfem
 
     ws, rank, local = dist_setup()
@@ -166,7 +171,14 @@ def run_ours(args, spec):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    m = Msfem.from_spec(spec, device=dev)
+    strips = ws > 1 and args.mode == "strips"
+    if strips:
+        uid = [pkg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        m = Msfem(pkg.problem_from_spec(spec), W.fixed_mask(spec), W.load_vector(spec), device=dev,
+                  rank=rank, nranks=ws, transport=pkg.MSF_TRANSPORT_NCCL, handle=uid[0])
+    else:
+        m = Msfem.from_spec(spec, device=dev)
     stream = m.stream
     x0 = W.design_tile(spec)
     xd = torch.as_tensor(x0, device=dev)
@@ -204,8 +216,8 @@ def run_ours(args, spec):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
         it_t = torch.tensor([iters_total], device=dev, dtype=torch.float64)
-        dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
-        iters_all = float(it_t.item())
+        dist.all_reduce(it_t, op=dist.ReduceOp.MAX if strips else dist.ReduceOp.SUM)
+        iters_all = float(it_t.item())   # strips: one global solve (identical counts)
     else:
         iters_all = float(iters_total)
     value = spec.n_dof * iters_all / (t_max / 1e3)
@@ -229,14 +241,15 @@ def run_ours(args, spec):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
         it_t = torch.tensor([e2e_iters], device=dev, dtype=torch.float64)
-        dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
+        dist.all_reduce(it_t, op=dist.ReduceOp.MAX if strips else dist.ReduceOp.SUM)
         e2e_iters = float(it_t.item())
     e2e_value = spec.n_dof * e2e_iters / (e2e_ms / 1e3)
     nt = spec.tile_x * spec.tile_y
     h2d = nt * 8
     d2h = nt * 8 + spec.n_rhs * (4 + 8) + 16
 
-    # ---- roofline of the dominant kernel (live CUDA-event timing, PCG launch config)
+    # ---- roofline of the dominant kernel (live CUDA-event timing, PCG launch config;
+    # on a strip the kernels run on that rank's strip)
     kb = m.bench_kernels(reps=20)
     per_iter_count = {"apply": 1, "sgs_colour": 2, "restrict": 1, "coarse_solve": 1,
                       "prolong": 1, "residual": 1}
@@ -266,11 +279,15 @@ def run_ours(args, spec):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if strips else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": spec.name, "n_dof": spec.n_dof, "grid": f"{spec.nelx}x{spec.nely}",
                    "realisations": spec.n_rhs, "coarse_cell": f"{spec.cx}x{spec.cy}",
                    "n_modes": spec.n_modes, "tile": f"{spec.tile_x}x{spec.tile_y}",
-                   "tol": tol, "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
+                   "tol": tol,
+                   "parallelism": ("single GPU" if ws == 1 else
+                                   f"{ws} strips (NCCL halo + all-reduce, replicated coarse solve)"
+                                   if strips else f"{ws} independent replicas"),
                    "pcg_iters_per_step": iters_step, "n_agg_classes": inf["n_classes"],
                    "l2": f"inputs larger than L2: workspace {inf['workspace_bytes'] / 2**20:.0f} MiB > 126 MB"},
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
@@ -298,6 +315,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="strips", choices=["strips", "replicas"],
+                    help="N > 1: strip partition of one problem (default) or independent replicas")
     args = ap.parse_args()
     spec = W.CONFIGS[args.config]
     if args.impl == "reference":

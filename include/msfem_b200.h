@@ -163,6 +163,9 @@ int msf_get_coarse_blocks(msf_ctx* ctx, int rhs, double* D_host, double* U_host)
 /* Element moduli E_e (Eq. 5) of realisation rhs into device [n_el]; projected tile
  * into device [tile] (either may be NULL). */
 int msf_get_physical(msf_ctx* ctx, int rhs, double* E_el, double* xbar_tile);
+/* u of the last pcg_solve for realisations [0, n_rhs) into device [n_rhs * n_dof_local]
+ * (n_dof_local = n_dof on one GPU; the strip layout of msf_dist_setup on a strip context). */
+int msf_get_solution(msf_ctx* ctx, int n_rhs, double* u);
 /* info[0..15]: n_dof, n_el, n_agg, n_classes, ncx, ncy, coarse block size m,
  * coarse slots, box_nodes, eig iterations used (max over classes), last PCG iteration
  * counts (4 entries), kernel launches of the last pcg_solve, workspace bytes. */
@@ -178,6 +181,54 @@ int msf_launch_count(msf_ctx* ctx, int64_t* count, int reset);
  * 3 coarse solve (all cyclic-reduction levels), 4 prolongation, 5 residual t = r - K z,
  * 6 full V-cycle, 7 one PCG iteration (graph). */
 int msf_bench_kernels(msf_ctx* ctx, int reps, double* ms, double* bytes);
+
+/* ---- strip partition over ranks (multi-GPU) -------------------------
+ * The fine grid is cut into strips of whole coarse-cell columns, one per rank.  Rank r
+ * owns the node columns of coarse columns [C0, C1) (the last rank also owns column nelx),
+ * stores its strip plus a one-node-column halo on each side (and one padding column on the
+ * left when needed so that its first local column is even: the 4-colour Gauss-Seidel order
+ * of reading R7 is the global one), and runs every fine-grid kernel on it.  The coarse space
+ * (moduli of the whole grid, basis, K_c and its factorisation, the coarse solve) is
+ * replicated on every rank.  Per PCG iteration: 14 halo exchanges of the smoother iterate
+ * (one per colour phase), sum all-reduces of p.Ap, ||r||^2, r.z and of the restricted
+ * coarse residual R_c t.  Results equal the single-GPU path up to the summation order of
+ * the dot products and of R_c t.
+ *
+ * Transports: MSF_TRANSPORT_NCCL, handle = host pointer to the 128-byte NCCL unique id
+ * (msf_nccl_unique_id on rank 0, broadcast by the caller), one process per GPU; all the
+ * ordinary entry points then work on the strip context (pcg_solve, sensitivities and
+ * design_iteration communicate inside).  MSF_TRANSPORT_GROUP, handle = msf_group*: all
+ * ranks of the group are contexts of this process on the current device sharing one
+ * stream; the communicating steps are driven by msf_group_pcg_solve /
+ * msf_group_sensitivities (the per-rank msf_pcg_solve / msf_sensitivities return
+ * MSF_ERR_STATE); the replicated steps use the ordinary per-context calls.
+ * Vectors returned from a strip context (u of msf_pcg_solve) are
+ * LOCAL: [n_rhs][ncols*(nely+1)][2] over global node columns [gox, gox+ncols).
+ * msf_matvec / msf_precond_apply / msf_sgs return MSF_ERR_STATE on a strip context;
+ * msf_bench_kernels times only the kernels without communication (ms[6] = ms[7] = -1). */
+#define MSF_TRANSPORT_NCCL 1
+#define MSF_TRANSPORT_GROUP 2
+typedef struct msf_group msf_group;
+
+/* bounds[8] = owned node columns [own0, own1), local columns [gox, gox+ncols), owned
+ * element columns [e0, e1), owned coarse columns [C0, C1) (all global).  Host only. */
+int msf_strip_bounds(const msf_problem* p, int rank, int nranks, int32_t* bounds);
+int msf_dist_workspace_bytes(const msf_problem* p, const uint8_t* fixed_mask, int rank,
+                             int nranks, size_t* bytes);
+/* fixed_mask, load: host, GLOBAL [n_dof] (each rank keeps its strip). */
+int msf_dist_setup(const msf_problem* p, const uint8_t* fixed_mask, const double* load,
+                   int rank, int nranks, int transport, void* handle, void* workspace,
+                   size_t workspace_bytes, void* stream, msf_ctx** out);
+/* id: host [128]; loads libnccl at run time (MSF_ERR_CUDA if unavailable). */
+int msf_nccl_unique_id(uint8_t* id);
+int msf_group_create(int nranks, msf_group** out);
+int msf_group_destroy(msf_group* g);
+/* iters, compliance: host [n_rhs] (identical on every rank) or NULL. */
+int msf_group_pcg_solve(msf_group* g, int n_rhs, double tol, int max_it, int32_t* iters,
+                        double* compliance);
+/* dF, dg: device [tile] (rank 0's copy) or NULL; F, g, compliance as msf_sensitivities. */
+int msf_group_sensitivities(msf_group* g, double kappa, double volfrac, double* dF, double* dg,
+                            double* F, double* g_out, double* compliance);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("MSF_LIB_PATH", os.path.join(HERE, "libmsfem_b200.so")
 
 MSF_OK, MSF_ERR_ARG, MSF_ERR_CUDA, MSF_ERR_STATE, MSF_ERR_NOCONV, MSF_ERR_FACTOR, MSF_ERR_SPACE = \
     0, -1, -2, -3, -4, -5, -6
+MSF_TRANSPORT_NCCL, MSF_TRANSPORT_GROUP = 1, 2
 MAX_RHS = 4
 
 # every symbol declared in include/msfem_b200.h (checked by tests/test_abi.py)
@@ -29,6 +30,9 @@ EXPORTS = [
     "msf_design_iteration_host", "msf_matvec", "msf_precond_apply", "msf_sgs",
     "msf_coarse_solve", "msf_get_basis", "msf_get_coarse_blocks", "msf_get_physical",
     "msf_info", "msf_launch_count", "msf_bench_kernels",
+    "msf_strip_bounds", "msf_dist_workspace_bytes", "msf_dist_setup", "msf_nccl_unique_id",
+    "msf_group_create", "msf_group_destroy", "msf_group_pcg_solve", "msf_group_sensitivities",
+    "msf_get_solution",
 ]
 
 
@@ -74,6 +78,13 @@ def load_library(path: str = LIB_PATH):
         "msf_get_coarse_blocks": [V, I, V, V], "msf_get_physical": [V, I, V, V],
         "msf_info": [V, i64p], "msf_launch_count": [V, i64p, I],
         "msf_bench_kernels": [V, I, dp, dp],
+        "msf_strip_bounds": [P(MsfProblem), I, I, i32p],
+        "msf_dist_workspace_bytes": [P(MsfProblem), V, I, I, P(ctypes.c_size_t)],
+        "msf_dist_setup": [P(MsfProblem), V, V, I, I, I, V, V, ctypes.c_size_t, V, P(V)],
+        "msf_nccl_unique_id": [V], "msf_get_solution": [V, I, V],
+        "msf_group_create": [I, P(V)], "msf_group_destroy": [V],
+        "msf_group_pcg_solve": [V, I, D, I, i32p, dp],
+        "msf_group_sensitivities": [V, D, D, V, V, dp, dp, dp],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -110,11 +121,36 @@ def problem_from_spec(spec) -> MsfProblem:
     return p
 
 
+def strip_bounds(problem: MsfProblem, rank: int, nranks: int) -> dict:
+    """Strip of `rank` (msf_strip_bounds; host only, no GPU needed)."""
+    lib = load_library()
+    b = (ctypes.c_int32 * 8)()
+    rc = lib.msf_strip_bounds(ctypes.byref(problem), rank, nranks, b)
+    if rc != MSF_OK:
+        raise MsfError(rc, lib.msf_last_error(None).decode())
+    keys = ["own0", "own1", "gox", "ncols", "e0", "e1", "C0", "C1"]
+    return dict(zip(keys, list(b)))
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it)."""
+    lib = load_library()
+    buf = (ctypes.c_uint8 * 128)()
+    rc = lib.msf_nccl_unique_id(buf)
+    if rc != MSF_OK:
+        raise MsfError(rc, lib.msf_last_error(None).decode())
+    return bytes(buf)
+
+
 class Msfem:
-    """One problem instance on the current CUDA device (C-ABI context + torch workspace)."""
+    """One problem instance on the current CUDA device (C-ABI context + torch workspace).
+
+    rank/nranks/transport/handle: strip partition (msf_dist_setup); transport
+    MSF_TRANSPORT_NCCL takes the 128-byte unique id as handle, MSF_TRANSPORT_GROUP an
+    MsfemGroup (use MsfemGroup.create instead of calling this directly)."""
 
     def __init__(self, problem: MsfProblem, fixed_mask: np.ndarray, load: np.ndarray,
-                 device=None, stream=None):
+                 device=None, stream=None, rank=0, nranks=1, transport=0, handle=None):
         import torch
         self.torch = torch
         self.lib = load_library()
@@ -124,21 +160,40 @@ class Msfem:
         self.problem = problem
         self.fixed = np.ascontiguousarray(fixed_mask, dtype=np.uint8)
         self.load = np.ascontiguousarray(load, dtype=np.float64)
+        self.rank, self.nranks, self.transport = rank, nranks, transport
         nbytes = ctypes.c_size_t()
-        self._check(self.lib.msf_workspace_bytes(ctypes.byref(problem),
-                                                 self.fixed.ctypes.data_as(ctypes.c_void_p),
-                                                 ctypes.byref(nbytes)), None)
+        fx = self.fixed.ctypes.data_as(ctypes.c_void_p)
+        if transport:
+            self._check(self.lib.msf_dist_workspace_bytes(ctypes.byref(problem), fx, rank, nranks,
+                                                          ctypes.byref(nbytes)), None)
+            self.bounds = strip_bounds(problem, rank, nranks)
+        else:
+            self._check(self.lib.msf_workspace_bytes(ctypes.byref(problem), fx,
+                                                     ctypes.byref(nbytes)), None)
+            self.bounds = {"own0": 0, "own1": problem.nelx + 1, "gox": 0,
+                           "ncols": problem.nelx + 1, "e0": 0, "e1": problem.nelx,
+                           "C0": 0, "C1": problem.nelx // problem.cx}
         with torch.cuda.device(self.device):
             self.workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
             self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         ctx = ctypes.c_void_p()
-        self._check(self.lib.msf_setup_mesh(ctypes.byref(problem),
-                                            self.fixed.ctypes.data_as(ctypes.c_void_p),
-                                            self.load.ctypes.data_as(ctypes.c_void_p),
-                                            _ptr(self.workspace), nbytes.value,
-                                            ctypes.c_void_p(self.stream.cuda_stream),
-                                            ctypes.byref(ctx)), None)
+        ld = self.load.ctypes.data_as(ctypes.c_void_p)
+        st = ctypes.c_void_p(self.stream.cuda_stream)
+        if transport:
+            if transport == MSF_TRANSPORT_NCCL:
+                self._id_buf = (ctypes.c_uint8 * 128).from_buffer_copy(handle)
+                h = ctypes.cast(self._id_buf, ctypes.c_void_p)
+            else:
+                h = handle
+            self._check(self.lib.msf_dist_setup(ctypes.byref(problem), fx, ld, rank, nranks,
+                                                transport, h, _ptr(self.workspace), nbytes.value,
+                                                st, ctypes.byref(ctx)), None)
+        else:
+            self._check(self.lib.msf_setup_mesh(ctypes.byref(problem), fx, ld,
+                                                _ptr(self.workspace), nbytes.value, st,
+                                                ctypes.byref(ctx)), None)
         self.ctx = ctx
+        self.n_dof_local = 2 * self.bounds["ncols"] * (problem.nely + 1)
         self.n_rhs = problem.n_rhs
         self.n_dof = 2 * (problem.nelx + 1) * (problem.nely + 1)
         self.n_el = problem.nelx * problem.nely
@@ -265,6 +320,13 @@ class Msfem:
                                                    U.ctypes.data_as(ctypes.c_void_p)))
         return D, U
 
+    def get_solution(self, n_rhs=None):
+        """u of the last PCG solve (device [n_rhs * n_dof_local]; the strip on a strip context)."""
+        n = self.n_rhs if n_rhs is None else n_rhs
+        u = self.torch.empty(n * self.n_dof_local, dtype=self.torch.float64, device=self.device)
+        self._check(self.lib.msf_get_solution(self.ctx, n, _ptr(u)))
+        return u
+
     def get_physical(self, rhs, E_el=None, xbar_tile=None):
         self._check(self.lib.msf_get_physical(self.ctx, rhs, _ptr(E_el), _ptr(xbar_tile)))
 
@@ -281,3 +343,94 @@ class Msfem:
         names = ["apply", "sgs_colour", "restrict", "coarse_solve", "prolong", "residual",
                  "vcycle", "pcg_iteration"]
         return {n: (ms[i], by[i]) for i, n in enumerate(names)}
+
+
+class MsfemGroup:
+    """All ranks of a strip partition as contexts of this process on one device
+    (MSF_TRANSPORT_GROUP): replicated steps run per rank, the communicating steps
+    (PCG, sensitivities) through the group entry points.  Proves the partitioned path on a
+    single GPU; production multi-GPU runs use one process per GPU with NCCL."""
+
+    def __init__(self, problem: MsfProblem, fixed_mask, load, nranks, stream=None):
+        import torch
+        self.lib = load_library()
+        g = ctypes.c_void_p()
+        rc = self.lib.msf_group_create(nranks, ctypes.byref(g))
+        if rc != MSF_OK:
+            raise MsfError(rc, self.lib.msf_last_error(None).decode())
+        self.g = g
+        self.problem = problem
+        self.nranks = nranks
+        st = stream if stream is not None else torch.cuda.current_stream()
+        self.ranks = [Msfem(problem, fixed_mask, load, stream=st, rank=r, nranks=nranks,
+                            transport=MSF_TRANSPORT_GROUP, handle=g) for r in range(nranks)]
+        self.n_rhs = problem.n_rhs
+
+    @classmethod
+    def from_spec(cls, spec, nranks, **kw):
+        import workloads as W
+        return cls(problem_from_spec(spec), W.fixed_mask(spec), W.load_vector(spec), nranks, **kw)
+
+    def _check(self, rc, allow_noconv=False):
+        if rc == MSF_OK or (allow_noconv and rc == MSF_ERR_NOCONV):
+            return rc
+        raise MsfError(rc, self.lib.msf_last_error(None).decode())
+
+    def filter_project(self, x_tile):
+        for m in self.ranks:
+            m.filter_project(x_tile)
+
+    def set_physical(self, rhs, xbar_el):
+        for m in self.ranks:
+            m.set_physical(rhs, xbar_el)
+
+    def build_coarse_basis(self):
+        for m in self.ranks:
+            m.build_coarse_basis()
+
+    def assemble_coarse(self):
+        for m in self.ranks:
+            m.assemble_coarse()
+
+    def pcg_solve(self, n_rhs=None, tol=1e-8, max_it=2000):
+        n = self.n_rhs if n_rhs is None else n_rhs
+        iters = (ctypes.c_int32 * n)()
+        comp = (ctypes.c_double * n)()
+        rc = self._check(self.lib.msf_group_pcg_solve(self.g, n, tol, max_it, iters, comp),
+                         allow_noconv=True)
+        return list(iters), list(comp), rc == MSF_ERR_NOCONV
+
+    def sensitivities(self, kappa=1.0, volfrac=0.5, dF=None, dg=None):
+        F, g = ctypes.c_double(), ctypes.c_double()
+        comp = (ctypes.c_double * self.n_rhs)()
+        self._check(self.lib.msf_group_sensitivities(self.g, kappa, volfrac, _ptr(dF), _ptr(dg),
+                                                     ctypes.byref(F), ctypes.byref(g), comp))
+        return F.value, g.value, list(comp)
+
+    def gather_solution(self, n_rhs=None):
+        """Global u [n_rhs, n_dof] (device) assembled from the ranks' owned node columns."""
+        import torch
+        n = self.n_rhs if n_rhs is None else n_rhs
+        p = self.problem
+        nny = p.nely + 1
+        out = torch.zeros(n, (p.nelx + 1) * nny * 2, dtype=torch.float64, device="cuda")
+        for m in self.ranks:
+            b = m.bounds
+            loc = m.get_solution(n).view(n, -1)
+            lo = (b["own0"] - b["gox"]) * nny * 2
+            hi = (b["own1"] - b["gox"]) * nny * 2
+            out[:, b["own0"] * nny * 2:b["own1"] * nny * 2] = loc[:, lo:hi]
+        return out
+
+    def close(self):
+        for m in self.ranks:
+            m.close()
+        if getattr(self, "g", None):
+            self.lib.msf_group_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

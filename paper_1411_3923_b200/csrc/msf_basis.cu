@@ -488,7 +488,7 @@ void launch_build_basis(msf_ctx* c) {
   const size_t smem = eig_smem_bytes(ea.mlmax, ea.mb);
   cudaFuncSetAttribute(k_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_eigen<<<c->n_cls, NT, smem, c->stream>>>(d, c->K0,
-                                              c->E + (size_t)c->p.dilated * d.ne, c->fixn,
+                                              c->E + (size_t)c->p.dilated * d.ne, c->fixg,
                                               c->classes_d, c->eig_work, c->phi, c->lam, ea,
                                               c->factor_status + MSF_MAX_RHS);
   MSF_LAUNCHED(c);

@@ -45,6 +45,8 @@ namespace {
 
 struct Plan {
   Dims d{};
+  Dims dl{};          // this rank's fine grid (== d on one GPU)
+  StripBounds sb{};
   std::vector<int> cls_of_agg;
   std::vector<EigClass> classes;
   int mb = 0;
@@ -82,7 +84,8 @@ int validate(const msf_problem* p, std::string& msg) {
 
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& msg) {
+int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& msg,
+              int rank = 0, int nranks = 1) {
   int rc = validate(p, msg);
   if (rc) return rc;
   if (!fixed) { msg = "fixed_mask is null"; return MSF_ERR_ARG; }
@@ -99,6 +102,17 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   d.mc = (d.ncy + 1) * d.kmax;
   d.nbc = d.ncx + 1;
   d.R = p->n_rhs;
+  d.gox = 0; d.own_lo = 0; d.own_hi = d.nnx; d.estride = d.ne;
+  // this rank's strip (the whole grid on one GPU)
+  if (nranks == 1 && rank == 0) {
+    P.sb = StripBounds{0, d.nnx, 0, d.nnx, 0, d.nelx, 0, d.ncx};
+  } else if ((rc = strip_bounds(d, rank, nranks, P.sb, msg))) {
+    return rc;
+  }
+  P.dl = d;
+  P.dl.nnx = P.sb.ncols; P.dl.nelx = P.sb.ncols - 1;
+  P.dl.nn = P.dl.nnx * d.nny; P.dl.ne = P.dl.nelx * d.nely;
+  P.dl.gox = P.sb.gox; P.dl.own_lo = P.sb.own0 - P.sb.gox; P.dl.own_hi = P.sb.own1 - P.sb.gox;
 
   // density-filter offsets in the oracle's order (dx outer, dy inner)
   P.fdx.clear(); P.fdy.clear(); P.fw.clear();
@@ -199,11 +213,13 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   P.jobs_bytes = align_up(ptrs * sizeof(double*)) + align_up(ints * sizeof(int));
   P.max_partials = std::max(apply_partials_needed(d), sgs_colour_partials_needed(d));
 
-  // workspace size
-  const size_t R = d.R, nn = d.nn, ne = d.ne, nt = d.nt;
+  // workspace size (node vectors on this rank's strip; moduli of the whole grid)
+  const size_t R = d.R, nn = P.dl.nn, ne = d.ne, nt = d.nt;
   size_t t = 0;
   auto add = [&](size_t bytes) { t += align_up(bytes); };
+  add(FIN_KINDS * MSF_MAX_RHS * 8);          // dsum
   add(nn);                                   // fixn
+  add(d.nn);                                 // fixg
   add(2 * nn * 8);                           // f
   add(nt * 8 * 5);                           // x_tile, xt, dF, dg, x_new
   add(R * nt * 8);                           // xbar
@@ -220,7 +236,7 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   add(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);     // Kcell
   add(7 * R * d.nbc * (size_t)d.mc * d.mc * 8);           // Dc Uc Dinv Pc Qc PTc QTc
   add(2 * R * d.nbc * (size_t)d.mc * 8);     // cb, cx
-  add((size_t)(3 * (d.n_agg + P.classes.size()) + d.n_agg) * 4);  // chunks, agg_by_cls
+  add((size_t)d.n_agg * 4);                  // agg_by_cls
   add(P.jobs_bytes);
   {
     const size_t T = P.top_blocks.size(), mm = (size_t)d.mc * d.mc;
@@ -255,14 +271,60 @@ int msf_workspace_bytes(const msf_problem* p, const uint8_t* fixed_mask, size_t*
   return MSF_OK;
 }
 
+int msf_strip_bounds(const msf_problem* p, int rank, int nranks, int32_t* bounds) {
+  std::string msg;
+  int rc = validate(p, msg);
+  if (rc) return msf_fail(nullptr, rc, msg);
+  if (!bounds) return msf_fail(nullptr, MSF_ERR_ARG, "bounds is null");
+  Dims d{};
+  d.nelx = p->nelx; d.nely = p->nely; d.cx = p->cx; d.ncx = p->nelx / p->cx;
+  StripBounds b{};
+  if ((rc = strip_bounds(d, rank, nranks, b, msg))) return msf_fail(nullptr, rc, msg);
+  const int32_t v[8] = {b.own0, b.own1, b.gox, b.ncols, b.e0, b.e1, b.C0, b.C1};
+  std::memcpy(bounds, v, sizeof(v));
+  return MSF_OK;
+}
+
+int msf_dist_workspace_bytes(const msf_problem* p, const uint8_t* fixed_mask, int rank,
+                             int nranks, size_t* bytes) {
+  Plan P;
+  std::string msg;
+  int rc = make_plan(p, fixed_mask, P, msg, rank, nranks);
+  if (rc) return msf_fail(nullptr, rc, msg);
+  if (bytes) *bytes = P.total;
+  return MSF_OK;
+}
+
+static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const double* load,
+                      int rank, int nranks, int transport, void* handle, void* workspace,
+                      size_t workspace_bytes, void* stream, msf_ctx** out);
+
 int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double* load,
                    void* workspace, size_t workspace_bytes, void* stream, msf_ctx** out) {
+  return setup_impl(p, fixed_mask, load, 0, 1, 0, nullptr, workspace, workspace_bytes, stream, out);
+}
+
+int msf_dist_setup(const msf_problem* p, const uint8_t* fixed_mask, const double* load,
+                   int rank, int nranks, int transport, void* handle, void* workspace,
+                   size_t workspace_bytes, void* stream, msf_ctx** out) {
+  if (transport != MSF_TRANSPORT_NCCL && transport != MSF_TRANSPORT_GROUP)
+    return msf_fail(nullptr, MSF_ERR_ARG, "unknown transport");
+  if (!handle) return msf_fail(nullptr, MSF_ERR_ARG, "transport handle is null");
+  return setup_impl(p, fixed_mask, load, rank, nranks, transport, handle, workspace,
+                    workspace_bytes, stream, out);
+}
+
+}  // extern "C"
+
+static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const double* load,
+                      int rank, int nranks, int transport, void* handle, void* workspace,
+                      size_t workspace_bytes, void* stream, msf_ctx** out) {
   if (!out) return msf_fail(nullptr, MSF_ERR_ARG, "out is null");
   *out = nullptr;
   if (!load) return msf_fail(nullptr, MSF_ERR_ARG, "load is null");
   Plan P;
   std::string msg;
-  int rc = make_plan(p, fixed_mask, P, msg);
+  int rc = make_plan(p, fixed_mask, P, msg, rank, nranks);
   if (rc) return msf_fail(nullptr, rc, msg);
   if (!workspace || workspace_bytes < P.total)
     return msf_fail(nullptr, MSF_ERR_SPACE, "workspace smaller than msf_workspace_bytes()");
@@ -276,6 +338,10 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   msf_ctx* c = new msf_ctx();
   c->p = *p;
   c->d = P.d;
+  c->dl = P.dl;
+  c->sb = P.sb;
+  c->rank = rank;
+  c->nranks = nranks;
   c->K0 = make_K0(p->nu);
   c->stream = (cudaStream_t)stream;
   c->ws = (char*)workspace;
@@ -294,7 +360,7 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   {
     const char* mode = std::getenv("MSF_PCG_MODE");
     // default: graph-launched iterations (measured faster); opt-in persistent
-    c->persistent = (mode && std::string(mode) == "persistent");
+    c->persistent = (mode && std::string(mode) == "persistent") && transport == 0;
     if (std::getenv("MSF_PERSIST_PROFILE")) {   // debug only: phase timeline buffer
       cudaMalloc(&c->prof_d, 32 * 64 * sizeof(unsigned long long));
       cudaMemset(c->prof_d, 0, 32 * 64 * sizeof(unsigned long long));
@@ -302,10 +368,15 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   }
 
   const Dims& d = c->d;
-  const size_t R = d.R, nn = d.nn, ne = d.ne, nt = d.nt;
+  const size_t R = d.R, nn = c->dl.nn, ne = d.ne, nt = d.nt;
   char* cur = (char*)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
   auto take = [&](size_t bytes) { char* r = cur; cur += align_up(bytes); return (void*)r; };
+  {
+    double* ds = (double*)take(FIN_KINDS * MSF_MAX_RHS * 8);
+    c->dsum = transport ? ds : nullptr;
+  }
   c->fixn = (uint8_t*)take(nn);
+  c->fixg = (uint8_t*)take(d.nn);
   c->f = (double*)take(2 * nn * 8);
   c->x_tile = (double*)take(nt * 8 * 5);
   c->xt_tile = c->x_tile + nt;
@@ -316,6 +387,7 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   c->tile_tmp = (double*)take(4 * nt * 8);
   c->dc_el = (double*)take(std::max(ne, 2 * nt) * 8);
   c->E = (double*)take(R * ne * 8);
+  c->E_loc = c->E + (size_t)c->dl.gox * d.nely;
   double* vec = (double*)take(6 * R * 2 * nn * 8);
   c->u = vec;
   c->r = vec + 1 * R * 2 * nn;
@@ -340,24 +412,19 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   c->cb = (double*)take(2 * R * d.nbc * (size_t)d.mc * 8);
   c->cx = c->cb + R * d.nbc * (size_t)d.mc;
   {
-    // restriction work list: agglomerates grouped by class, chunks of <= 16 per CTA
+    // restriction work list: agglomerates grouped by class (consecutive CTAs share a basis
+    // in L2); a strip keeps those whose box meets its node columns
     std::vector<std::vector<int>> members(c->n_cls);
     for (int a = 0; a < d.n_agg; ++a) members[P.cls_of_agg[a]].push_back(a);
     c->agg_by_cls_h.clear();
-    c->chunks_h.clear();
-    for (int k = 0; k < c->n_cls; ++k) {
-      const int base = (int)c->agg_by_cls_h.size();
-      c->agg_by_cls_h.insert(c->agg_by_cls_h.end(), members[k].begin(), members[k].end());
-      for (int s0 = 0; s0 < (int)members[k].size(); s0 += 16) {
-        c->chunks_h.push_back(k);
-        c->chunks_h.push_back(base + s0);
-        c->chunks_h.push_back(std::min(16, (int)members[k].size() - s0));
+    const int lo = c->dl.gox, hi = c->dl.gox + c->dl.nnx - 1;
+    for (int k = 0; k < c->n_cls; ++k)
+      for (int a : members[k]) {
+        const int I = a / (d.ncy + 1);
+        if ((I + 1) * d.cx >= lo && (I - 1) * d.cx <= hi) c->agg_by_cls_h.push_back(a);
       }
-    }
-    c->n_chunks = (int)c->chunks_h.size() / 3;
-    int* ib = (int*)take((size_t)(3 * (d.n_agg + P.classes.size()) + d.n_agg) * 4);
-    c->chunks_d = ib;
-    c->agg_by_cls_d = ib + 3 * (d.n_agg + P.classes.size());
+    c->n_restrict = (int)c->agg_by_cls_h.size();
+    c->agg_by_cls_d = (int*)take((size_t)d.n_agg * 4);
   }
   c->jobs_d = (char*)take(P.jobs_bytes);
   {
@@ -494,38 +561,68 @@ int msf_setup_mesh(const msf_problem* p, const uint8_t* fixed_mask, const double
   }
 
   // fixed mask per node, load, filter table, classes
+  // (strip: halo and padding columns are masked like Dirichlet DOFs: the fine kernels leave
+  // them untouched and they drop out of every dot product; their values come from the
+  // neighbour's halo exchange.  Kernels never mask their inputs, so the owned stencils see
+  // the halo values.)
   std::vector<uint8_t> fixn(nn);
-  for (size_t n = 0; n < nn; ++n) fixn[n] = (fixed_mask[2 * n] ? 1 : 0) | (fixed_mask[2 * n + 1] ? 2 : 0);
+  std::vector<double> floc(2 * nn, 0.0);
+  const size_t nny = d.nny, goff = (size_t)c->dl.gox * nny;
+  for (size_t n = 0; n < nn; ++n) {
+    const int lx = (int)(n / nny);
+    if (lx < c->dl.own_lo || lx >= c->dl.own_hi) {
+      fixn[n] = 3;
+      continue;
+    }
+    const size_t g = goff + n;
+    fixn[n] = (fixed_mask[2 * g] ? 1 : 0) | (fixed_mask[2 * g + 1] ? 2 : 0);
+    floc[2 * n] = load[2 * g];
+    floc[2 * n + 1] = load[2 * g + 1];
+  }
+  std::vector<uint8_t> fixg(d.nn);
+  for (size_t n = 0; n < (size_t)d.nn; ++n) fixg[n] = (fixed_mask[2 * n] ? 1 : 0) | (fixed_mask[2 * n + 1] ? 2 : 0);
   ce = cudaMemcpyAsync(c->fixn, fixn.data(), nn, cudaMemcpyHostToDevice, c->stream);
-  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->f, load, 2 * nn * 8, cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->fixg, fixg.data(), d.nn, cudaMemcpyHostToDevice, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->f, floc.data(), 2 * nn * 8, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_w_d, P.fw.data(), P.fw.size() * 8, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_dx_d, P.fdx.data(), P.fdx.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_dy_d, P.fdy.data(), P.fdy.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->cls_of_agg_d, P.cls_of_agg.data(), d.n_agg * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->classes_d, P.classes.data(), c->n_cls * sizeof(EigClass), cudaMemcpyHostToDevice, c->stream);
-  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->chunks_d, c->chunks_h.data(), c->chunks_h.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->agg_by_cls_d, c->agg_by_cls_h.data(), c->agg_by_cls_h.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->factor_status, 0, 2 * MSF_MAX_RHS * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->counters, 0, R * 8 * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->sc, 0, R * sizeof(PcgScalars), c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->scal, 0, 64 * 8, c->stream);
+  if (ce == cudaSuccess && c->dsum) ce = cudaMemsetAsync(c->dsum, 0, FIN_KINDS * MSF_MAX_RHS * 8, c->stream);
+  // node vectors start at 0 (halo / padding columns are only ever written by exchanges)
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->u, 0, 6 * R * 2 * nn * 8, c->stream);
   if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->sc_host, MSF_MAX_RHS * sizeof(PcgScalars));
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->scal_host, 80 * 8);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
   if (ce != cudaSuccess) {
     std::string m = std::string("setup: ") + cudaGetErrorString(ce);
-    if (c->sc_host) cudaFreeHost(c->sc_host);
-    if (c->scal_host) cudaFreeHost(c->scal_host);
-    delete c;
+    msf_destroy(c);
     return msf_fail(nullptr, MSF_ERR_CUDA, m);
+  }
+  if (transport) {
+    rc = dist_comm_create(c, transport, handle);
+    if (rc) {
+      std::string m = c->err;
+      msf_destroy(c);
+      return msf_fail(nullptr, rc, m);
+    }
   }
   *out = c;
   return MSF_OK;
 }
 
+extern "C" {
+
 int msf_destroy(msf_ctx* c) {
   if (!c) return MSF_OK;
+  dist_comm_destroy(c);
   if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->sc_host) cudaFreeHost(c->sc_host);
@@ -618,10 +715,159 @@ static int read_scalars(msf_ctx* c, int nr) {
 }
 
 static int run_graph_iterations(msf_ctx* c, int nr, int max_it);
+static int sens_outputs(msf_ctx* c, double* dF, double* dg, double* F, double* g,
+                        double* compliance);
+
+// ---------------------------------------------------------------------- strip partition
+// The same PCG / V-cycle as enqueue_iteration / enqueue_vcycle, phase by phase over the
+// ranks this process drives (NCCL: itself; group: all), with the halo exchanges and
+// all-reduces of DESIGN.md §8(e) between the phases.
+using Ranks = std::vector<msf_ctx*>;
+
+static int dist_reduce(const Ranks& cs, int kind, int nr, bool gated, int rz_mode) {
+  int rc = dist_allreduce(cs, &msf_ctx::dsum, (size_t)kind * MSF_MAX_RHS, MSF_MAX_RHS);
+  if (rc) return rc;
+  for (msf_ctx* c : cs) launch_finalize(c, kind, nr, gated, rz_mode);
+  return MSF_OK;
+}
+
+// symmetric GS sweep, z halo exchanged after every colour phase.  first: 0 from z = 0,
+// 1 full sweep, 2 colour 0 already done (fused into the PCG update)
+static int dist_sgs(const Ranks& cs, int nr, int first, int rz_mode) {
+  int rc;
+  for (int ph = first; ph <= 7; ph = (ph < 2 ? 2 : ph + 1)) {
+    for (msf_ctx* c : cs) launch_sgs_phase(c, 0, nr, c->r, c->z, true, ph, rz_mode);
+    if ((rc = dist_halo(cs, &msf_ctx::z, nr))) return rc;
+  }
+  if (rz_mode) return dist_reduce(cs, FIN_RZ, nr, true, rz_mode);
+  return MSF_OK;
+}
+
+static int dist_vcycle(const Ranks& cs, int nr, bool f0_done, int rz_mode) {
+  int rc;
+  if ((rc = dist_sgs(cs, nr, f0_done ? 2 : 0, 0))) return rc;
+  for (msf_ctx* c : cs) {
+    launch_residual(c, 0, nr, c->r, c->z, c->t, true);
+    launch_restrict(c, 0, nr, c->t, true);     // partial R_c t over the owned nodes
+  }
+  const size_t nc = (size_t)cs[0]->d.nbc * cs[0]->d.mc;
+  if ((rc = dist_allreduce(cs, &msf_ctx::cb, 0, nr * nc))) return rc;
+  for (msf_ctx* c : cs) {
+    launch_coarse_solve(c, 0, nr, true);       // replicated
+    launch_prolong(c, 0, nr, c->z, true);      // owned + halo nodes
+  }
+  return dist_sgs(cs, nr, 1, rz_mode);
+}
+
+static int dist_iteration(const Ranks& cs, int nr) {
+  int rc;
+  for (msf_ctx* c : cs) launch_matvec(c, 0, nr, c->pv, c->q, true, true);
+  if ((rc = dist_reduce(cs, FIN_PQ, nr, true, 0))) return rc;
+  for (msf_ctx* c : cs) launch_update_f0(c, nr);
+  if ((rc = dist_reduce(cs, FIN_RR, nr, true, 0))) return rc;
+  if ((rc = dist_halo(cs, &msf_ctx::z, nr))) return rc;
+  if ((rc = dist_vcycle(cs, nr, true, 2))) return rc;
+  for (msf_ctx* c : cs) launch_pcg_p(c, nr, false);
+  return MSF_OK;
+}
+
+static int dist_pcg_solve(const Ranks& cs, int nr, double tol, int max_it, int32_t* iters,
+                          double* compliance) {
+  msf_ctx* c = cs[0];
+  for (msf_ctx* x : cs) {
+    if (!x) return msf_fail(c, MSF_ERR_STATE, "group has unregistered ranks");
+    if (!x->have_coarse) return msf_fail(c, MSF_ERR_STATE, "pcg_solve before assemble_coarse");
+    if (x->stream != c->stream) return msf_fail(c, MSF_ERR_ARG, "group ranks must share one stream");
+  }
+  if (nr < 1 || nr > c->d.R) return msf_fail(c, MSF_ERR_ARG, "n_rhs out of range");
+  if (!(tol > 0.0) || max_it < 1) return msf_fail(c, MSF_ERR_ARG, "need tol > 0, max_it >= 1");
+  int rc;
+  for (msf_ctx* x : cs) launch_pcg_init(x, nr, tol, max_it);
+  if ((rc = dist_reduce(cs, FIN_F, nr, false, 0))) return rc;
+  if ((rc = dist_vcycle(cs, nr, false, 1))) return rc;
+  for (msf_ctx* x : cs) launch_pcg_p(x, nr, true);
+  CKL("dist pcg init");
+  // one process per GPU: the iteration (kernels + NCCL) is captured once as a CUDA graph
+  const bool graph = cs.size() == 1;
+  if (graph && (!c->iter_graph || c->iter_graph_R != nr)) {
+    if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
+    c->iter_graph = nullptr;
+    cudaGraph_t g;
+    cudaStream_t user = c->stream;
+    c->stream = c->cap_stream;
+    cudaError_t e1 = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+    const long long before = c->launches;
+    int rc_it = MSF_OK;
+    if (e1 == cudaSuccess) rc_it = dist_iteration(cs, nr);
+    c->pcg_launches = c->launches - before;
+    c->launches = before;
+    cudaError_t e2 = e1 == cudaSuccess ? cudaStreamEndCapture(c->stream, &g) : e1;
+    c->stream = user;
+    if (rc_it) return rc_it;
+    CK(e1);
+    CK(e2);
+    CK(cudaGraphInstantiate(&c->iter_graph, g, 0));
+    cudaGraphDestroy(g);
+    c->iter_graph_R = nr;
+  }
+  const int check_every = 8;
+  bool done = false;
+  for (int it = 0; it < max_it + check_every && !done; it += check_every) {
+    for (int j = 0; j < check_every; ++j) {
+      if (graph) {
+        CK(cudaGraphLaunch(c->iter_graph, c->stream));
+        c->launches += c->pcg_launches;
+      } else if ((rc = dist_iteration(cs, nr))) {
+        return rc;
+      }
+    }
+    // the flags derive from all-reduced sums: identical on every rank
+    if ((rc = read_scalars(c, nr))) return rc;
+    done = true;
+    for (int k = 0; k < nr; ++k)
+      if (c->sc_host[k].active) done = false;
+  }
+  for (msf_ctx* x : cs) launch_compliance(x, nr);
+  if ((rc = dist_reduce(cs, FIN_COMP, nr, false, 0))) return rc;
+  int noconv = 0;
+  for (msf_ctx* x : cs) {
+    if ((rc = read_scalars(x, nr))) return rc;
+    for (int k = 0; k < nr; ++k) x->last_iters[k] = x->sc_host[k].iters;
+    x->have_solution = true;
+  }
+  for (int k = 0; k < nr; ++k) {
+    if (iters) iters[k] = c->sc_host[k].iters;
+    if (compliance) compliance[k] = c->sc_host[k].comp;
+    noconv |= c->sc_host[k].noconv;
+  }
+  if (noconv) return msf_fail(c, MSF_ERR_NOCONV, "PCG reached max_it");
+  return MSF_OK;
+}
+
+static int dist_sensitivities(const Ranks& cs, double kappa, double volfrac) {
+  msf_ctx* c = cs[0];
+  for (msf_ctx* x : cs)
+    if (!x || !x->have_solution) return msf_fail(c, MSF_ERR_STATE, "sensitivities before pcg_solve");
+  int rc;
+  for (msf_ctx* x : cs) launch_sens_local(x);
+  if ((rc = dist_reduce(cs, FIN_COMP, c->d.R, false, 0))) return rc;
+  if ((rc = dist_allreduce(cs, &msf_ctx::tile_tmp, 0, (size_t)c->d.R * c->d.nt))) return rc;
+  for (msf_ctx* x : cs) launch_sens_global(x, kappa, volfrac);
+  CKL("dist sensitivities");
+  return MSF_OK;
+}
 
 int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int32_t* iters,
                   double* compliance) {
   if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
+  if (c->comm) {
+    if (c->comm->kind == MSF_TRANSPORT_GROUP)
+      return msf_fail(c, MSF_ERR_STATE, "group rank: use msf_group_pcg_solve");
+    int rc = dist_pcg_solve(Ranks{c}, n_rhs, tol, max_it, iters, compliance);
+    if (rc && rc != MSF_ERR_NOCONV) return rc;
+    if (u) CK(cudaMemcpyAsync(u, c->u, (size_t)n_rhs * 2 * c->dl.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return rc;
+  }
   if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "pcg_solve before assemble_coarse");
   if (n_rhs < 1 || n_rhs > c->d.R) return msf_fail(c, MSF_ERR_ARG, "n_rhs out of range");
   if (!(tol > 0.0) || max_it < 1) return msf_fail(c, MSF_ERR_ARG, "need tol > 0, max_it >= 1");
@@ -661,7 +907,7 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
     if (compliance) compliance[k] = c->sc_host[k].comp;
     noconv |= c->sc_host[k].noconv;
   }
-  if (u) CK(cudaMemcpyAsync(u, c->u, (size_t)nr * 2 * c->d.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (u) CK(cudaMemcpyAsync(u, c->u, (size_t)nr * 2 * c->dl.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
   c->have_solution = true;
   (void)l0;
   if (noconv) return msf_fail(c, MSF_ERR_NOCONV, "PCG reached max_it");
@@ -713,8 +959,20 @@ int msf_sensitivities(msf_ctx* c, double kappa, double volfrac, double* dF, doub
   if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
   if (!c->have_solution) return msf_fail(c, MSF_ERR_STATE, "sensitivities before pcg_solve");
   if (!(volfrac > 0.0)) return msf_fail(c, MSF_ERR_ARG, "volfrac must be > 0");
-  launch_sensitivities(c, kappa, volfrac);
+  if (c->comm) {
+    if (c->comm->kind == MSF_TRANSPORT_GROUP)
+      return msf_fail(c, MSF_ERR_STATE, "group rank: use msf_group_sensitivities");
+    int rc = dist_sensitivities(Ranks{c}, kappa, volfrac);
+    if (rc) return rc;
+  } else {
+    launch_sensitivities(c, kappa, volfrac);
+  }
   CKL("sensitivities");
+  return sens_outputs(c, dF, dg, F, g, compliance);
+}
+
+static int sens_outputs(msf_ctx* c, double* dF, double* dg, double* F, double* g,
+                        double* compliance) {
   const size_t tb = (size_t)c->d.nt * 8;
   if (dF && dF != c->dF) CK(cudaMemcpyAsync(dF, c->dF, tb, cudaMemcpyDeviceToDevice, c->stream));
   if (dg && dg != c->dg) CK(cudaMemcpyAsync(dg, c->dg, tb, cudaMemcpyDeviceToDevice, c->stream));
@@ -727,6 +985,30 @@ int msf_sensitivities(msf_ctx* c, double kappa, double volfrac, double* dF, doub
       for (int k = 0; k < c->d.R; ++k) compliance[k] = c->scal_host[16 + k];
   }
   return MSF_OK;
+}
+
+int msf_group_pcg_solve(msf_group* g, int n_rhs, double tol, int max_it, int32_t* iters,
+                        double* compliance) {
+  if (!g) return msf_fail(nullptr, MSF_ERR_ARG, "null group");
+  Ranks cs = group_ranks(g);
+  for (msf_ctx* x : cs)
+    if (!x) return msf_fail(nullptr, MSF_ERR_STATE, "group has unregistered ranks");
+  int rc = dist_pcg_solve(cs, n_rhs, tol, max_it, iters, compliance);
+  if (rc) g_err = cs[0]->err;
+  return rc;
+}
+
+int msf_group_sensitivities(msf_group* g, double kappa, double volfrac, double* dF, double* dg,
+                            double* F, double* g_out, double* compliance) {
+  if (!g) return msf_fail(nullptr, MSF_ERR_ARG, "null group");
+  if (!(volfrac > 0.0)) return msf_fail(nullptr, MSF_ERR_ARG, "volfrac must be > 0");
+  Ranks cs = group_ranks(g);
+  for (msf_ctx* x : cs)
+    if (!x) return msf_fail(nullptr, MSF_ERR_STATE, "group has unregistered ranks");
+  int rc = dist_sensitivities(cs, kappa, volfrac);
+  if (!rc) rc = sens_outputs(cs[0], dF, dg, F, g_out, compliance);
+  if (rc) g_err = cs[0]->err;
+  return rc;
 }
 
 int msf_oc_update(msf_ctx* c, const double* x, const double* dF, const double* dg,
@@ -771,37 +1053,40 @@ int msf_design_iteration_host(msf_ctx* c, const double* x_host, double* x_new_ho
 // ---------------------------------------------------------------------------- diagnostics
 int msf_matvec(msf_ctx* c, int rhs, const double* x, double* y) {
   if (!c || !x || !y) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (c->comm) return msf_fail(c, MSF_ERR_STATE, "matvec: not available on a strip context");
   if (!c->have_E) return msf_fail(c, MSF_ERR_STATE, "matvec before filter_project");
   if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
-  const size_t off = (size_t)rhs * 2 * c->d.nn;
-  launch_mask_copy(c, x, c->t + off, c->d.nn);
+  const size_t off = (size_t)rhs * 2 * c->dl.nn;
+  launch_mask_copy(c, x, c->t + off, c->dl.nn);
   launch_matvec(c, rhs, 1, c->t, c->q, false, false);
-  CK(cudaMemcpyAsync(y, c->q + off, (size_t)2 * c->d.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(y, c->q + off, (size_t)2 * c->dl.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
   CKL("matvec");
   return MSF_OK;
 }
 
 int msf_precond_apply(msf_ctx* c, int rhs, const double* r, double* z) {
   if (!c || !r || !z) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (c->comm) return msf_fail(c, MSF_ERR_STATE, "precond_apply: not available on a strip context");
   if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "precond before assemble_coarse");
   if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
-  const size_t off = (size_t)rhs * 2 * c->d.nn;
-  launch_mask_copy(c, r, c->r + off, c->d.nn);
+  const size_t off = (size_t)rhs * 2 * c->dl.nn;
+  launch_mask_copy(c, r, c->r + off, c->dl.nn);
   enqueue_vcycle(c, rhs, 1, c->r, c->z, false);
-  CK(cudaMemcpyAsync(z, c->z + off, (size_t)2 * c->d.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(z, c->z + off, (size_t)2 * c->dl.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
   CKL("precond_apply");
   return MSF_OK;
 }
 
 int msf_sgs(msf_ctx* c, int rhs, const double* r, double* z) {
   if (!c || !r || !z) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (c->comm) return msf_fail(c, MSF_ERR_STATE, "sgs: not available on a strip context");
   if (!c->have_E) return msf_fail(c, MSF_ERR_STATE, "sgs before filter_project");
   if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
-  const size_t off = (size_t)rhs * 2 * c->d.nn;
-  launch_mask_copy(c, r, c->r + off, c->d.nn);
-  launch_mask_copy(c, z, c->z + off, c->d.nn);
+  const size_t off = (size_t)rhs * 2 * c->dl.nn;
+  launch_mask_copy(c, r, c->r + off, c->dl.nn);
+  launch_mask_copy(c, z, c->z + off, c->dl.nn);
   launch_sgs(c, rhs, 1, c->r, c->z, false);
-  CK(cudaMemcpyAsync(z, c->z + off, (size_t)2 * c->d.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(z, c->z + off, (size_t)2 * c->dl.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
   CKL("sgs");
   return MSF_OK;
 }
@@ -867,6 +1152,14 @@ int msf_get_physical(msf_ctx* c, int rhs, double* E_el, double* xbar_tile) {
   return MSF_OK;
 }
 
+int msf_get_solution(msf_ctx* c, int n_rhs, double* u) {
+  if (!c || !u) return msf_fail(c, MSF_ERR_ARG, "null argument");
+  if (!c->have_solution) return msf_fail(c, MSF_ERR_STATE, "get_solution before pcg_solve");
+  if (n_rhs < 1 || n_rhs > c->d.R) return msf_fail(c, MSF_ERR_ARG, "n_rhs out of range");
+  CK(cudaMemcpyAsync(u, c->u, (size_t)n_rhs * 2 * c->dl.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
+  return MSF_OK;
+}
+
 int msf_info(msf_ctx* c, int64_t* info) {
   if (!c || !info) return msf_fail(c, MSF_ERR_ARG, "null argument");
   const Dims& d = c->d;
@@ -883,7 +1176,9 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "bench_kernels before assemble_coarse");
   const Dims& d = c->d;
   const int R = d.R;
-  const double nn = d.nn, ne = d.ne;
+  // fine-grid traffic on this rank's strip; the communicating composites (V-cycle, PCG
+  // iteration) are not timed on a strip context (ms = -1)
+  const double nn = c->dl.nn, ne = (double)c->dl.nelx * c->dl.nely;
   // algorithmic bytes per launch: every operand touched once
   bytes[0] = R * (nn * 16 + ne * 8 + nn * 16) + nn;                  // p, E -> q
   bytes[1] = 7 * (R * (ne * 8 + nn * 16 + nn / 4 * 16 * 2) + nn / 4);  // 7 colour launches
@@ -953,7 +1248,8 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
     cudaEventElapsedTime(&t, e0, e1);
     return (double)t / reps;
   };
-  for (int i = 0; i < 8; ++i) ms[i] = timeit(i);
+  const int ntimed = c->comm ? 6 : 8;
+  for (int i = 0; i < 8; ++i) ms[i] = i < ntimed ? timeit(i) : -1.0;
   if (!c->iter_graph || c->iter_graph_R != R) ms[7] = -1.0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

@@ -408,11 +408,16 @@ __global__ void __launch_bounds__(256) k_top_solve(Dims d, const int* __restrict
 
 // ================================================================== host side
 void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) {
-  const Dims& d = c->d;
+  const Dims& d = c->dl;   // global coarse fields, this rank's node columns
+  if (c->comm) {
+    // a strip restricts only the agglomerates touching it; the rest of its partial c is 0
+    const size_t n = (size_t)d.nbc * d.mc;
+    cudaMemsetAsync(c->cb + rhs0 * n, 0, nr * n * sizeof(double), c->stream);
+  }
 #define MSF_RESTRICT(KM)                                                                       \
-  k_restrict<KM><<<d.n_agg, NT, 0, c->stream>>>(d, (const double2*)t, c->phi, c->cls_of_agg_d, \
-                                               c->agg_by_cls_d, c->cb, c->sc, rhs0, nr,       \
-                                               gated ? 1 : 0)
+  k_restrict<KM><<<c->n_restrict, NT, 0, c->stream>>>(d, (const double2*)t, c->phi,            \
+                                                      c->cls_of_agg_d, c->agg_by_cls_d, c->cb, \
+                                                      c->sc, rhs0, nr, gated ? 1 : 0)
   if (d.kmax <= 4) MSF_RESTRICT(4);
   else if (d.kmax <= 8) MSF_RESTRICT(8);
   else MSF_RESTRICT(16);
@@ -421,7 +426,7 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
 }
 
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
-  const Dims& d = c->d;
+  const Dims& d = c->dl;   // every local node, halo included (identical increments on both ranks)
   dim3 g((d.nny + 31) / 32, (d.nnx + 7) / 8, 1);
   k_prolong<<<g, NT, 0, c->stream>>>(d, c->phi, c->cls_of_agg_d, c->cx, (double2*)z, c->sc,
                                      rhs0, nr, gated ? 1 : 0);

@@ -41,6 +41,48 @@ __device__ double reduce_partials(const double* partials, int n, double* sm, int
   return block_sum_all(s, sm, tid, nthreads);
 }
 
+// PCG scalar update from a completed (global) dot product (reading R9)
+__device__ __forceinline__ void fin_scalar(PcgScalars& S, int kind, double tot, int rz_mode) {
+  switch (kind) {
+    case FIN_PQ:
+      S.pq = tot;
+      S.alpha = S.rz / tot;
+      break;
+    case FIN_RR:
+      S.rr = tot;
+      S.iters += 1;
+      if (tot <= S.tol2 * S.fnorm2) {
+        S.active = 0;
+      } else if (S.iters >= S.max_it) {
+        S.active = 0;
+        S.noconv = 1;
+      }
+      break;
+    case FIN_RZ:
+      S.beta = (rz_mode == 1) ? 0.0 : tot / S.rz;
+      S.rz = tot;
+      break;
+    case FIN_F:
+      S.fnorm2 = tot;
+      S.rr = tot;
+      S.active = (tot > 0.0 && !(tot <= S.tol2 * tot)) ? 1 : 0;
+      break;
+    default:
+      S.comp = tot;
+      break;
+  }
+}
+
+// last block of a reduction: finalise in place (one GPU) or park the local sum for the
+// cross-rank all-reduce (strip partition, dsum != null)
+__device__ __forceinline__ void fin_or_park(PcgScalars* sc, double* dsum, int rhs, int kind,
+                                            double tot, int rz_mode) {
+  if (dsum)
+    dsum[kind * MSF_MAX_RHS + rhs] = tot;
+  else
+    fin_scalar(sc[rhs], kind, tot, rz_mode);
+}
+
 // ------------------------------------------------------------------ operator apply
 // MODE 0: y = P K P x ; MODE 1: y = b - P K P x.  dot: accumulate x.y (p.Ap) and set
 // alpha = rz / pq in the last block.
@@ -51,13 +93,14 @@ __global__ void __launch_bounds__(NTHR) k_apply(Dims d, K0Mat K, const double* _
                                                 const double2* __restrict__ ball,
                                                 const uint8_t* __restrict__ fixn, PcgScalars* sc,
                                                 double* partials, unsigned* counters, int rhs0,
-                                                int gated, int dot, int max_partials) {
+                                                int gated, int dot, int max_partials,
+                                                double* dsum) {
   const int rhs = rhs0 + blockIdx.z;
   if (gated && !sc[rhs].active) return;
   __shared__ TileSmem S;
   __shared__ double red[NTHR / 32 + 1];
   const int tid = threadIdx.y * TY + threadIdx.x;
-  const double dv = apply_tile<MODE>(d, K, Eall + (size_t)rhs * d.ne, xall + (size_t)rhs * d.nn,
+  const double dv = apply_tile<MODE>(d, K, Eall + (size_t)rhs * d.estride, xall + (size_t)rhs * d.nn,
                                      yall + (size_t)rhs * d.nn,
                                      MODE == 1 ? ball + (size_t)rhs * d.nn : nullptr, fixn,
                                      blockIdx.y * TX, blockIdx.x * TY, tid, S);
@@ -70,8 +113,7 @@ __global__ void __launch_bounds__(NTHR) k_apply(Dims d, K0Mat K, const double* _
       const double tot = reduce_partials(partials + (size_t)rhs * max_partials, nblk, red, tid,
                                          NTHR);
       if (tid == 0) {
-        sc[rhs].pq = tot;
-        sc[rhs].alpha = sc[rhs].rz / tot;
+        fin_or_park(sc, dsum, rhs, FIN_PQ, tot, 0);
         counters[rhs * 8] = 0;
       }
     }
@@ -89,13 +131,13 @@ __global__ void __launch_bounds__(NTHR) k_sgs_colour(Dims d, K0Mat K, const doub
                                                      PcgScalars* sc, double* partials,
                                                      unsigned* counters, int max_partials,
                                                      int rhs0, int gated, int colour,
-                                                     int rz_mode) {
+                                                     int rz_mode, double* dsum) {
   const int rhs = rhs0 + blockIdx.z;
   if (gated && !sc[rhs].active) return;
   __shared__ double red[NTHR / 32 + 1];
   const int qx = blockIdx.y * blockDim.y + threadIdx.y;
   const int qy = blockIdx.x * blockDim.x + threadIdx.x;
-  const double dot = sgs_quad<FWD, BWD, ZERO, RZ>(d, K, Eall + (size_t)rhs * d.ne,
+  const double dot = sgs_quad<FWD, BWD, ZERO, RZ>(d, K, Eall + (size_t)rhs * d.estride,
                                                   rall + (size_t)rhs * d.nn,
                                                   zall + (size_t)rhs * d.nn, fixn, qx, qy, colour);
   if (RZ) {
@@ -108,9 +150,7 @@ __global__ void __launch_bounds__(NTHR) k_sgs_colour(Dims d, K0Mat K, const doub
       const double tot = reduce_partials(partials + (size_t)rhs * max_partials, nblk, red, tid,
                                          NTHR);
       if (tid == 0) {
-        PcgScalars& Sc = sc[rhs];
-        Sc.beta = (rz_mode == 1) ? 0.0 : tot / Sc.rz;
-        Sc.rz = tot;
+        fin_or_park(sc, dsum, rhs, FIN_RZ, tot, rz_mode);
         counters[rhs * 8] = 0;
       }
     }
@@ -136,7 +176,8 @@ __global__ void __launch_bounds__(VB) k_pcg_init(Dims d, const double2* __restri
                                                  const uint8_t* __restrict__ fixn,
                                                  double2* uall, double2* rall, PcgScalars* sc,
                                                  double* partials, unsigned* counters,
-                                                 int max_partials, double tol, int max_it) {
+                                                 int max_partials, double tol, int max_it,
+                                                 double* dsum) {
   __shared__ double red[VB / 32 + 1];
   const int rhs = blockIdx.z;
   const int tid = threadIdx.x;
@@ -159,62 +200,13 @@ __global__ void __launch_bounds__(VB) k_pcg_init(Dims d, const double2* __restri
                                        tid, VB);
     if (tid == 0) {
       PcgScalars& S = sc[rhs];
-      S.fnorm2 = tot;
-      S.rr = tot;
       S.tol2 = tol * tol;
       S.iters = 0;
       S.max_it = max_it;
       S.noconv = 0;
       S.rz = 0.0;
       S.alpha = S.beta = S.pq = 0.0;
-      S.active = (tot > 0.0 && !(tot <= S.tol2 * tot)) ? 1 : 0;
-      counters[rhs * 8] = 0;
-    }
-  }
-}
-
-// u += alpha p ; r -= alpha q ; rr = ||r||^2 ; iteration bookkeeping (reading R9)
-__global__ void __launch_bounds__(VB) k_pcg_update_xr(Dims d, double2* uall, double2* rall,
-                                                      const double2* __restrict__ pall,
-                                                      const double2* __restrict__ qall,
-                                                      PcgScalars* sc, double* partials,
-                                                      unsigned* counters, int max_partials) {
-  __shared__ double red[VB / 32 + 1];
-  const int rhs = blockIdx.z;
-  if (!sc[rhs].active) return;
-  const int tid = threadIdx.x;
-  const double alpha = sc[rhs].alpha;
-  double2* u = uall + (size_t)rhs * d.nn;
-  double2* r = rall + (size_t)rhs * d.nn;
-  const double2* p = pall + (size_t)rhs * d.nn;
-  const double2* q = qall + (size_t)rhs * d.nn;
-  double s = 0.0;
-  for (int i = blockIdx.x * VB + tid; i < d.nn; i += gridDim.x * VB) {
-    const double2 pv = p[i], qv = q[i];
-    double2 uv = u[i], rv = r[i];
-    uv.x = fma(alpha, pv.x, uv.x);
-    uv.y = fma(alpha, pv.y, uv.y);
-    rv.x = fma(-alpha, qv.x, rv.x);
-    rv.y = fma(-alpha, qv.y, rv.y);
-    u[i] = uv;
-    r[i] = rv;
-    s += rv.x * rv.x + rv.y * rv.y;
-  }
-  s = block_sum_all(s, red, tid, VB);
-  if (arrive_last(s, partials + (size_t)rhs * max_partials, blockIdx.x, counters + rhs * 8,
-                  gridDim.x, tid)) {
-    const double tot = reduce_partials(partials + (size_t)rhs * max_partials, gridDim.x, red,
-                                       tid, VB);
-    if (tid == 0) {
-      PcgScalars& S = sc[rhs];
-      S.rr = tot;
-      S.iters += 1;
-      if (tot <= S.tol2 * S.fnorm2) {
-        S.active = 0;
-      } else if (S.iters >= S.max_it) {
-        S.active = 0;
-        S.noconv = 1;
-      }
+      fin_or_park(sc, dsum, rhs, FIN_F, tot, 0);
       counters[rhs * 8] = 0;
     }
   }
@@ -229,7 +221,7 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
                                                     const double2* __restrict__ qall, double2* zall,
                                                     const uint8_t* __restrict__ fixn, PcgScalars* sc,
                                                     double* partials, unsigned* counters,
-                                                    int max_partials) {
+                                                    int max_partials, double* dsum) {
   const int rhs = blockIdx.z;
   if (!sc[rhs].active) return;
   __shared__ double red[NTHR / 32 + 1];
@@ -255,7 +247,7 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
       s += rv.x * rv.x + rv.y * rv.y;
     }
   }
-  sgs_quad<true, false, true, false>(d, K, Eall + (size_t)rhs * d.ne, rall + off, zall + off,
+  sgs_quad<true, false, true, false>(d, K, Eall + (size_t)rhs * d.estride, rall + off, zall + off,
                                      fixn, qx, qy, 0);
   s = block_sum_all(s, red, tid, NTHR);
   const unsigned nblk = gridDim.x * gridDim.y;
@@ -263,18 +255,20 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
   if (arrive_last(s, partials + (size_t)rhs * max_partials, slot, counters + rhs * 8, nblk, tid)) {
     const double tot = reduce_partials(partials + (size_t)rhs * max_partials, nblk, red, tid, NTHR);
     if (tid == 0) {
-      PcgScalars& S = sc[rhs];
-      S.rr = tot;
-      S.iters += 1;
-      if (tot <= S.tol2 * S.fnorm2) {
-        S.active = 0;
-      } else if (S.iters >= S.max_it) {
-        S.active = 0;
-        S.noconv = 1;
-      }
+      fin_or_park(sc, dsum, rhs, FIN_RR, tot, 0);
       counters[rhs * 8] = 0;
     }
   }
+}
+
+// PCG scalar update from the all-reduced sums (strip partition): same arithmetic as the
+// in-kernel finalisation of the single-GPU path.
+__global__ void k_finalize(PcgScalars* sc, const double* __restrict__ dsum, int kind, int nr,
+                           int gated, int rz_mode) {
+  const int rhs = threadIdx.x;
+  if (rhs >= nr) return;
+  if (gated && !sc[rhs].active) return;
+  fin_scalar(sc[rhs], kind, dsum[kind * MSF_MAX_RHS + rhs], rz_mode);
 }
 
 // p = z + beta p  (p = z at init)
@@ -298,7 +292,8 @@ __global__ void __launch_bounds__(VB) k_pcg_p(Dims d, const double2* __restrict_
 __global__ void __launch_bounds__(VB) k_compliance(Dims d, const double2* __restrict__ f,
                                                    const double2* __restrict__ uall,
                                                    PcgScalars* sc, double* partials,
-                                                   unsigned* counters, int max_partials) {
+                                                   unsigned* counters, int max_partials,
+                                                   double* dsum) {
   __shared__ double red[VB / 32 + 1];
   const int rhs = blockIdx.z;
   const int tid = threadIdx.x;
@@ -314,7 +309,7 @@ __global__ void __launch_bounds__(VB) k_compliance(Dims d, const double2* __rest
     const double tot = reduce_partials(partials + (size_t)rhs * max_partials, gridDim.x, red,
                                        tid, VB);
     if (tid == 0) {
-      sc[rhs].comp = tot;
+      fin_or_park(sc, dsum, rhs, FIN_COMP, tot, 0);
       counters[rhs * 8] = 0;
     }
   }
@@ -361,19 +356,54 @@ int sgs_colour_partials_needed(const Dims& d) {
   return ((hy + 31) / 32) * ((hx + 7) / 8);
 }
 
+// Fine-grid launchers run on this rank's grid c->dl with the moduli c->E_loc (the whole grid
+// on one GPU); reductions park their sums in c->dsum on a strip context.
 void launch_matvec(msf_ctx* c, int rhs0, int nr, const double* x, double* y, bool gated,
                    bool dot_pq) {
-  k_apply<0><<<apply_grid(c->d, nr), dim3(TY, TX), 0, c->stream>>>(
-      c->d, c->K0, c->E, (const double2*)x, (double2*)y, nullptr, c->fixn, c->sc, c->partials,
-      c->counters, rhs0, gated ? 1 : 0, dot_pq ? 1 : 0, c->max_partials);
+  k_apply<0><<<apply_grid(c->dl, nr), dim3(TY, TX), 0, c->stream>>>(
+      c->dl, c->K0, c->E_loc, (const double2*)x, (double2*)y, nullptr, c->fixn, c->sc,
+      c->partials, c->counters, rhs0, gated ? 1 : 0, dot_pq ? 1 : 0, c->max_partials, c->dsum);
   MSF_LAUNCHED(c);
 }
 
 void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double* x, double* y,
                      bool gated) {
-  k_apply<1><<<apply_grid(c->d, nr), dim3(TY, TX), 0, c->stream>>>(
-      c->d, c->K0, c->E, (const double2*)x, (double2*)y, (const double2*)b, c->fixn, c->sc,
-      c->partials, c->counters, rhs0, gated ? 1 : 0, 0, c->max_partials);
+  k_apply<1><<<apply_grid(c->dl, nr), dim3(TY, TX), 0, c->stream>>>(
+      c->dl, c->K0, c->E_loc, (const double2*)x, (double2*)y, (const double2*)b, c->fixn, c->sc,
+      c->partials, c->counters, rhs0, gated ? 1 : 0, 0, c->max_partials, c->dsum);
+  MSF_LAUNCHED(c);
+}
+
+void launch_sgs_phase(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
+                      int phase, int rz_mode) {
+  const Dims& d = c->dl;
+  const int hx = (d.nnx + 1) / 2, hy = (d.nny + 1) / 2;
+  dim3 blk(32, 8);
+  dim3 grd((hy + 31) / 32, (hx + 7) / 8, nr);
+  const int g = gated ? 1 : 0;
+#define MSF_SGS(F, B, Z, RZ, col)                                                               \
+  k_sgs_colour<F, B, Z, RZ><<<grd, blk, 0, c->stream>>>(d, c->K0, c->E_loc, (const double2*)r,   \
+                                                        (double2*)z, c->fixn, c->sc,            \
+                                                        c->partials, c->counters,               \
+                                                        c->max_partials, rhs0, g, col, rz_mode, \
+                                                        c->dsum);                               \
+  break
+  switch (phase) {
+    case 0: MSF_SGS(true, false, true, false, 0);
+    case 1: MSF_SGS(true, false, false, false, 0);
+    case 2: MSF_SGS(true, false, false, false, 1);
+    case 3: MSF_SGS(true, false, false, false, 2);
+    case 4: MSF_SGS(true, true, false, false, 3);
+    case 5: MSF_SGS(false, true, false, false, 2);
+    case 6: MSF_SGS(false, true, false, false, 1);
+    default:
+      if (rz_mode) {
+        MSF_SGS(false, true, false, true, 0);
+      } else {
+        MSF_SGS(false, true, false, false, 0);
+      }
+  }
+#undef MSF_SGS
   MSF_LAUNCHED(c);
 }
 
@@ -381,33 +411,11 @@ void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double
 // entry (fused into F0); rz_mode != 0: r.z and beta fused into B0.
 void launch_sgs_sweep(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
                       bool zero_start, int rz_mode, bool skip_f0) {
-  const Dims& d = c->d;
-  const int hx = (d.nnx + 1) / 2, hy = (d.nny + 1) / 2;
-  dim3 blk(32, 8);
-  dim3 grd((hy + 31) / 32, (hx + 7) / 8, nr);
-  const int g = gated ? 1 : 0;
-#define MSF_SGS(F, B, Z, RZ, col)                                                              \
-  k_sgs_colour<F, B, Z, RZ><<<grd, blk, 0, c->stream>>>(d, c->K0, c->E, (const double2*)r,      \
-                                                        (double2*)z, c->fixn, c->sc,           \
-                                                        c->partials, c->counters,              \
-                                                        c->max_partials, rhs0, g, col, rz_mode); \
-  MSF_LAUNCHED(c)
-  if (zero_start) {
-    MSF_SGS(true, false, true, false, 0);
-  } else if (!skip_f0) {
-    MSF_SGS(true, false, false, false, 0);
-  }
-  MSF_SGS(true, false, false, false, 1);
-  MSF_SGS(true, false, false, false, 2);
-  MSF_SGS(true, true, false, false, 3);
-  MSF_SGS(false, true, false, false, 2);
-  MSF_SGS(false, true, false, false, 1);
-  if (rz_mode) {
-    MSF_SGS(false, true, false, true, 0);
-  } else {
-    MSF_SGS(false, true, false, false, 0);
-  }
-#undef MSF_SGS
+  if (zero_start)
+    launch_sgs_phase(c, rhs0, nr, r, z, gated, 0, 0);
+  else if (!skip_f0)
+    launch_sgs_phase(c, rhs0, nr, r, z, gated, 1, 0);
+  for (int ph = 2; ph <= 7; ++ph) launch_sgs_phase(c, rhs0, nr, r, z, gated, ph, rz_mode);
 }
 
 void launch_sgs(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated) {
@@ -415,13 +423,18 @@ void launch_sgs(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool g
 }
 
 void launch_update_f0(msf_ctx* c, int nr) {
-  const Dims& d = c->d;
+  const Dims& d = c->dl;
   const int hx = (d.nnx + 1) / 2, hy = (d.nny + 1) / 2;
   dim3 grd((hy + 31) / 32, (hx + 7) / 8, nr);
   k_update_f0<<<grd, dim3(32, 8), 0, c->stream>>>(
-      d, c->K0, c->E, (double2*)c->u, (double2*)c->r, (const double2*)c->pv,
+      d, c->K0, c->E_loc, (double2*)c->u, (double2*)c->r, (const double2*)c->pv,
       (const double2*)c->q, (double2*)c->z, c->fixn, c->sc, c->partials, c->counters,
-      c->max_partials);
+      c->max_partials, c->dsum);
+  MSF_LAUNCHED(c);
+}
+
+void launch_finalize(msf_ctx* c, int kind, int nr, bool gated, int rz_mode) {
+  k_finalize<<<1, 32, 0, c->stream>>>(c->sc, c->dsum, kind, nr, gated ? 1 : 0, rz_mode);
   MSF_LAUNCHED(c);
 }
 
@@ -433,28 +446,21 @@ void launch_mask_copy(msf_ctx* c, const double* x, double* y, int nn) {
 }
 
 void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it) {
-  k_pcg_init<<<dim3(vec_blocks(c->d), 1, nr), VB, 0, c->stream>>>(
-      c->d, (const double2*)c->f, c->fixn, (double2*)c->u, (double2*)c->r, c->sc, c->partials,
-      c->counters, c->max_partials, tol, max_it);
-  MSF_LAUNCHED(c);
-}
-
-void launch_pcg_update_xr(msf_ctx* c, int nr) {
-  k_pcg_update_xr<<<dim3(vec_blocks(c->d), 1, nr), VB, 0, c->stream>>>(
-      c->d, (double2*)c->u, (double2*)c->r, (const double2*)c->pv, (const double2*)c->q, c->sc,
-      c->partials, c->counters, c->max_partials);
+  k_pcg_init<<<dim3(vec_blocks(c->dl), 1, nr), VB, 0, c->stream>>>(
+      c->dl, (const double2*)c->f, c->fixn, (double2*)c->u, (double2*)c->r, c->sc, c->partials,
+      c->counters, c->max_partials, tol, max_it, c->dsum);
   MSF_LAUNCHED(c);
 }
 
 void launch_pcg_p(msf_ctx* c, int nr, bool init) {
-  k_pcg_p<<<dim3(vec_blocks(c->d), 1, nr), VB, 0, c->stream>>>(
-      c->d, (const double2*)c->z, (double2*)c->pv, c->sc, init ? 1 : 0);
+  k_pcg_p<<<dim3(vec_blocks(c->dl), 1, nr), VB, 0, c->stream>>>(
+      c->dl, (const double2*)c->z, (double2*)c->pv, c->sc, init ? 1 : 0);
   MSF_LAUNCHED(c);
 }
 
 void launch_compliance(msf_ctx* c, int nr) {
-  k_compliance<<<dim3(vec_blocks(c->d), 1, nr), VB, 0, c->stream>>>(
-      c->d, (const double2*)c->f, (const double2*)c->u, c->sc, c->partials, c->counters,
-      c->max_partials);
+  k_compliance<<<dim3(vec_blocks(c->dl), 1, nr), VB, 0, c->stream>>>(
+      c->dl, (const double2*)c->f, (const double2*)c->u, c->sc, c->partials, c->counters,
+      c->max_partials, c->dsum);
   MSF_LAUNCHED(c);
 }

@@ -91,14 +91,15 @@ __global__ void k_set_physical(Dims d, const double* __restrict__ xb_el, double*
     E[e] = Emin + pow(xb_el[e], penal) * (E0 - Emin);
 }
 
-// dc/dxbar_e = -p xbar^{p-1} (E0-Emin) u_e^T K0 u_e  (Eq. 14-15)
+// dc/dxbar_e = -p xbar^{p-1} (E0-Emin) u_e^T K0 u_e  (Eq. 14-15) for the element
+// columns [ex0, ex1) (global); u holds the node columns from gox on (this rank's strip)
 __global__ void k_dc_element(Dims d, K0Mat K, const double2* __restrict__ u,
                              const double* __restrict__ xbar, double* dc, double E0, double Emin,
-                             double penal) {
-  for (int ex = blockIdx.y; ex < d.nelx; ex += gridDim.y) {
+                             double penal, int ex0, int ex1, int gox) {
+  for (int ex = ex0 + blockIdx.y; ex < ex1; ex += gridDim.y) {
     const int tx = ex % d.tile_x;
     for (int ey = blockIdx.x * FB + threadIdx.x; ey < d.nely; ey += gridDim.x * FB) {
-      const size_t n0 = (size_t)ex * d.nny + ey;
+      const size_t n0 = (size_t)(ex - gox) * d.nny + ey;
       const double2 a = u[n0], b = u[n0 + d.nny], c = u[n0 + d.nny + 1], e = u[n0 + 1];
       const double ue[8] = {a.x, a.y, b.x, b.y, c.x, c.y, e.x, e.y};
       double en = 0.0;
@@ -273,19 +274,32 @@ void launch_set_physical(msf_ctx* c, int rhs, const double* xb_el) {
   MSF_LAUNCHED(c);
 }
 
-void launch_sensitivities(msf_ctx* c, double kappa, double volfrac) {
+void launch_sens_local(msf_ctx* c) {
   const Dims& d = c->d;
   launch_compliance(c, d.R);
   double* dcT = c->tile_tmp;                 // [R*nt] (R <= 4 slots of tile_tmp)
+  const int ncol = c->sb.e1 - c->sb.e0;
+  if (c->comm) cudaMemsetAsync(c->dc_el, 0, (size_t)d.ne * sizeof(double), c->stream);
   for (int k = 0; k < d.R; ++k) {
-    dim3 g((d.nely + FB - 1) / FB, d.nelx < 4096 ? d.nelx : 4096, 1);
-    k_dc_element<<<g, FB, 0, c->stream>>>(d, c->K0, (const double2*)(c->u + (size_t)k * 2 * d.nn),
+    dim3 g((d.nely + FB - 1) / FB, ncol < 4096 ? ncol : 4096, 1);
+    k_dc_element<<<g, FB, 0, c->stream>>>(d, c->K0,
+                                          (const double2*)(c->u + (size_t)k * 2 * c->dl.nn),
                                           c->xbar_tile + (size_t)k * d.nt, c->dc_el, c->p.E0,
-                                          c->p.Emin, c->p.penal);
+                                          c->p.Emin, c->p.penal, c->sb.e0, c->sb.e1, c->dl.gox);
     MSF_LAUNCHED(c);
     k_tile_sum<<<tblocks(d.nt), FB, 0, c->stream>>>(d, c->dc_el, dcT + (size_t)k * d.nt);
     MSF_LAUNCHED(c);
   }
+}
+
+void launch_sensitivities(msf_ctx* c, double kappa, double volfrac) {
+  launch_sens_local(c);
+  launch_sens_global(c, kappa, volfrac);
+}
+
+void launch_sens_global(msf_ctx* c, double kappa, double volfrac) {
+  const Dims& d = c->d;
+  double* dcT = c->tile_tmp;
   k_robust_weights<<<1, 32, 0, c->stream>>>(c->sc, d.R, kappa, c->scal);
   MSF_LAUNCHED(c);
   // g1 -> dc_el[0:nt], g2 -> dc_el[nt:2nt] (scratch, ne >= 2 nt not assumed: use x_new/dg)

@@ -34,6 +34,10 @@ struct Dims {
   int mc;              // coarse block size (ncy+1)*kmax
   int nbc;             // coarse blocks (ncx+1)
   int R;               // realisations
+  // strip partition (multi-GPU); single GPU: gox = 0, own = [0, nnx)
+  int gox;             // global node column of local node column 0
+  int own_lo, own_hi;  // owned local node columns [own_lo, own_hi)
+  long long estride;   // elements between realisations in the moduli array
 };
 
 // Per-realisation PCG scalars living in device memory (reading R9).
@@ -88,9 +92,47 @@ struct TopStep {
   double** ngs = nullptr; double** ngd = nullptr;                                  // A_kk = -Pk
 };
 
+// Device-side dot products awaiting the cross-rank all-reduce (strip partition): kernels
+// that end in a reduction write their local sum to dsum[kind][rhs] instead of finalising the
+// PCG scalars; k_finalize applies the same update to the all-reduced sums.
+enum FinKind { FIN_PQ = 0, FIN_RR = 1, FIN_RZ = 2, FIN_F = 3, FIN_COMP = 4, FIN_KINDS = 5 };
+
+struct msf_group;   // in-process rank group (msf_dist.cu)
+
+// Strip partition of the fine grid over ranks: rank r owns the node
+// columns of coarse columns [C0, C1) and keeps a one-column halo on each side (plus one
+// padding column on the left when needed to keep the 4-colour parity of the global grid).
+struct StripBounds {
+  int own0, own1;    // owned global node columns [own0, own1)
+  int gox, ncols;    // local node columns = global [gox, gox + ncols)
+  int e0, e1;        // owned global element columns
+  int C0, C1;        // owned coarse columns
+};
+int strip_bounds(const Dims& d, int rank, int nranks, StripBounds& b, std::string& msg);
+struct msf_ctx;
+int dist_comm_create(msf_ctx* c, int transport, void* handle);
+void dist_comm_destroy(msf_ctx* c);
+int dist_allreduce(const std::vector<msf_ctx*>& cs, double* msf_ctx::*buf, size_t off,
+                   size_t count);
+int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int nr);
+std::vector<msf_ctx*> group_ranks(msf_group* g);
+
+struct msf_comm {
+  int kind = 0;          // MSF_TRANSPORT_NCCL / MSF_TRANSPORT_GROUP
+  void* nccl = nullptr;  // ncclComm_t
+  msf_group* grp = nullptr;
+};
+
 struct msf_ctx {
   msf_problem p{};
-  Dims d{};
+  Dims d{};            // global grid (coarse space, filter, moduli, basis)
+  Dims dl{};           // fine grid of this rank (== d on one GPU)
+  int rank = 0, nranks = 1;
+  StripBounds sb{};
+  msf_comm* comm = nullptr;   // null: single GPU
+  double* E_loc = nullptr;    // E + first local element column (stride dl.estride)
+  double* dsum = nullptr;     // [FIN_KINDS][MSF_MAX_RHS] local sums (strip partition only)
+  int n_restrict = 0;         // agglomerates restricted by this rank (agg_by_cls_d prefix)
   K0Mat K0{};
   cudaStream_t stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream used only to capture graphs
@@ -110,7 +152,9 @@ struct msf_ctx {
   bool periodic = false;
 
   // device buffers (carved from the workspace)
-  uint8_t* fixn = nullptr;      // per-node bitmask: bit0 x fixed, bit1 y fixed
+  uint8_t* fixn = nullptr;      // per-node bitmask: bit0 x fixed, bit1 y fixed (this rank's strip;
+                                // halo / padding columns = 3)
+  uint8_t* fixg = nullptr;      // the same for the whole grid (local eigenproblems)
   double* f = nullptr;          // load [2*nn]
   double* x_tile = nullptr;     // design [nt]
   double* xt_tile = nullptr;    // filtered [nt]
@@ -138,7 +182,6 @@ struct msf_ctx {
   double* phi = nullptr;        // [n_cls][kmax][box_nodes][2]
   double* lam = nullptr;        // [n_cls][kmax]
   double* eig_work = nullptr;
-  int* nkept_agg = nullptr;     // [n_agg] (per agglomerate, from its class)
 
   double* Kcell = nullptr;      // [R][ncells][(4k)^2]
   double* Dc = nullptr;         // [R][nbc][mc*mc]
@@ -150,10 +193,8 @@ struct msf_ctx {
   double* QTc = nullptr;        // [R][nbc][mc*mc]  Q_k^T
   double* cb = nullptr;         // [R][nbc*mc] coarse rhs (modified by the forward sweep)
   double* cx = nullptr;         // [R][nbc*mc] coarse solution
-  int* chunks_d = nullptr;      // restriction work list: [n_chunks][3] = class, start, count
   int* agg_by_cls_d = nullptr;  // agglomerates grouped by class
-  int n_chunks = 0;
-  std::vector<int> chunks_h, agg_by_cls_h;
+  std::vector<int> agg_by_cls_h;
   // top system after the truncated cyclic reduction: T active blocks (stride top_stride),
   // dense inverse stored block-major [R][T][T][mc*mc] as -Top^{-1}
   std::vector<int> top_blocks;
@@ -201,18 +242,26 @@ void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double
 void launch_sgs(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated);
 void launch_sgs_sweep(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
                       bool zero_start, int rz_mode, bool skip_f0);
+// one colour phase of the sweep: 0 F0 from z = 0, 1 F0, 2 F1, 3 F2, 4 F3B3, 5 B2, 6 B1,
+// 7 B0 (r.z -> beta when rz_mode != 0)
+void launch_sgs_phase(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
+                      int phase, int rz_mode);
+// PCG scalar update from the all-reduced dsum[kind] (strip partition)
+void launch_finalize(msf_ctx* c, int kind, int nr, bool gated, int rz_mode);
 // fused u/r update + ||r||^2 + zero-start forward GS colour 0 (PCG iteration)
 void launch_update_f0(msf_ctx* c, int nr);
 void launch_mask_copy(msf_ctx* c, const double* x, double* y, int n2nn);
 void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it);
-void launch_pcg_update_xr(msf_ctx* c, int nr);
-void launch_pcg_rz(msf_ctx* c, int nr, bool init);
 void launch_pcg_p(msf_ctx* c, int nr, bool init);
 void launch_compliance(msf_ctx* c, int nr);
 
 // ---------------------------------------------------------------- filter / design
 void launch_filter_project(msf_ctx* c, const double* x_tile);
 void launch_set_physical(msf_ctx* c, int rhs, const double* xbar_el);
+// compliance + element sensitivities of the owned elements summed per tile variable (dcT)
+void launch_sens_local(msf_ctx* c);
+// robust weights, chain rule, filter adjoint, volume (replicated; after the dcT all-reduce)
+void launch_sens_global(msf_ctx* c, double kappa, double volfrac);
 void launch_sensitivities(msf_ctx* c, double kappa, double volfrac);
 void launch_oc(msf_ctx* c, const double* x, const double* dF, const double* dg, double volfrac,
                double move, double* x_new);

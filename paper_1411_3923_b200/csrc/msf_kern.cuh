@@ -229,7 +229,9 @@ __device__ __forceinline__ void restrict_agg(const Dims& d, const double2* __res
                                              int tid, double (*red)[MSF_MAX_RHS * KM]) {
   const int I = agg / (d.ncy + 1), J = agg - (agg / (d.ncy + 1)) * (d.ncy + 1);
   const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2;
-  const int gx0 = I * d.cx - d.cx, gy0 = J * d.cy - d.cy;
+  // box origin in this rank's node columns (gox = 0 on one GPU); t vanishes on halo columns,
+  // so a strip restricts exactly its owned nodes and the ranks' sums add up to R_c t
+  const int gx0 = I * d.cx - d.cx - d.gox, gy0 = J * d.cy - d.cy;
   // interior of the padded box (chi vanishes on its boundary ring)
   const int ix_lo = max(1, -gx0), ix_hi = min(d.bx - 2, d.nnx - 1 - gx0);
   const int iy_lo = max(1, -gy0), iy_hi = min(d.by - 2, d.nny - 1 - gy0);
@@ -285,12 +287,13 @@ __device__ __forceinline__ void prolong_node(const Dims& d, const double* __rest
   double sx[MSF_MAX_RHS], sy[MSF_MAX_RHS];
 #pragma unroll
   for (int r = 0; r < MSF_MAX_RHS; ++r) sx[r] = sy[r] = 0.0;
-  const int I0 = ix / d.cx, J0 = iy / d.cy;
+  const int gix = ix + d.gox;   // global node column (ix is local to this rank's strip)
+  const int I0 = gix / d.cx, J0 = iy / d.cy;
 #pragma unroll
   for (int di = 0; di < 2; ++di) {
     const int I = I0 + di;
     if (I > d.ncx) continue;
-    const int px = ix - (I * d.cx - d.cx);
+    const int px = gix - (I * d.cx - d.cx);
     if (px < 0 || px >= d.bx) continue;
 #pragma unroll
     for (int dj = 0; dj < 2; ++dj) {

@@ -1,0 +1,173 @@
+"""GPU parity of the strip-partitioned path (multi-GPU): the fine grid cut
+into 2-4 strips, each rank a separate C-ABI context; the ranks run in lockstep in one
+process on one B200 (MSF_TRANSPORT_GROUP: halos are device copies, all-reduces a
+rank-ordered sum), so the partitioned arithmetic is checked without a second GPU.
+
+Bars: against the oracle exactly those of tests/test_gpu_parity.py (iterations +-1 at
+tol 1e-8, displacement 1e-8, compliance the fp64-attainable bar); against the single-GPU
+CUDA path, which differs only in the summation order of the dot products and of R_c t,
+iterations +-1, displacement 1e-9, compliance 1e-11."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import design, problem
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+
+from paper_1411_3923_b200 import Msfem, MsfemGroup, build  # noqa: E402
+from test_gpu_parity import SPECS, compliance_tol, dev, host, rel  # noqa: E402
+
+build.build()
+DEV = torch.device("cuda")
+
+STRIP_SPECS = {
+    # cx even: every rank > 0 carries the left padding column
+    "cant_16x8": (SPECS["cant_16x8"], (2, 4)),
+    "robust_32x16": (SPECS["robust_32x16"], (2, 3)),
+    "ragged_36x20": (SPECS["ragged_36x20"], (2, 3)),
+    # cx odd: ranks with and without padding
+    "odd_30x12": (W.small_spec(nelx=30, nely=12, cx=3, cy=3, seed=41, Emin=1e-6), (3, 4)),
+}
+CASES = [(n, r) for n, (_, rs) in STRIP_SPECS.items() for r in rs]
+
+
+def group_for(spec, nranks, x):
+    g = MsfemGroup.from_spec(spec, nranks)
+    g.filter_project(dev(x))
+    g.build_coarse_basis()
+    g.assemble_coarse()
+    return g
+
+
+def single_for(spec, x):
+    m = Msfem.from_spec(spec)
+    m.filter_project(dev(x))
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    return m
+
+
+@pytest.mark.parametrize("name,nranks", CASES)
+def test_strip_bounds_partition(name, nranks):
+    spec, _ = STRIP_SPECS[name]
+    g = MsfemGroup.from_spec(spec, nranks)
+    owned = np.zeros(spec.nelx + 1, dtype=int)
+    for m in g.ranks:
+        b = m.bounds
+        owned[b["own0"]:b["own1"]] += 1
+        assert b["gox"] % 2 == 0
+        assert b["gox"] <= max(b["own0"] - 1, 0) and b["gox"] + b["ncols"] >= min(b["own1"] + 1, spec.nelx + 1)
+    assert (owned == 1).all()
+    g.close()
+
+
+@pytest.mark.parametrize("name,nranks", CASES)
+def test_strip_pcg_vs_oracle_and_single(name, nranks):
+    spec, _ = STRIP_SPECS[name]
+    x = W.design_tile(spec)
+    fx, f = W.fixed_mask(spec), W.load_vector(spec)
+    g = group_for(spec, nranks, x)
+    m = single_for(spec, x)
+    ref = problem.solve(spec, x, fx, f, tol=1e-8)
+    its_g, comp_g, nc = g.pcg_solve(tol=1e-8)
+    its_s, comp_s, _ = m.pcg_solve(tol=1e-8)
+    assert not nc
+    for k in range(spec.n_rhs):
+        assert abs(its_g[k] - ref["iters"][k]) <= 1, (its_g, ref["iters"])
+        assert abs(its_g[k] - its_s[k]) <= 1, (its_g, its_s)
+    ref = problem.solve(spec, x, fx, f, tol=1e-12)
+    its_g, comp_g, _ = g.pcg_solve(tol=1e-12)
+    u_s = torch.empty(spec.n_rhs * spec.n_dof, dtype=torch.float64, device=DEV)
+    its_s, comp_s, _ = m.pcg_solve(tol=1e-12, u=u_s)
+    ug = host(g.gather_solution()).reshape(spec.n_rhs, spec.n_dof)
+    us = host(u_s).reshape(spec.n_rhs, spec.n_dof)
+    for k in range(spec.n_rhs):
+        assert rel(ug[k], ref["us"][k]) <= 1e-8
+        assert rel(ug[k], us[k]) <= 1e-9
+        tc = compliance_tol(spec, ref["E_el"][k], f, fx)
+        assert abs(comp_g[k] - ref["comps"][k]) <= tc * abs(ref["comps"][k]), tc
+        assert abs(comp_g[k] - comp_s[k]) <= max(1e-11, tc) * abs(comp_s[k])
+    g.close()
+
+
+@pytest.mark.parametrize("name,nranks", [("robust_32x16", 2), ("ragged_36x20", 3)])
+def test_strip_sensitivities_vs_oracle(name, nranks):
+    spec, _ = STRIP_SPECS[name]
+    spec = spec.replace(volfrac=0.5)
+    x = W.design_tile(spec)
+    fx, f = W.fixed_mask(spec), W.load_vector(spec)
+    ref = problem.solve(spec, x, fx, f, tol=1e-12)
+    F, c, gv, dF, dg = design.design_gradients(spec, x, ref["us"], f, ref["K0"])
+    g = group_for(spec, nranks, x)
+    g.pcg_solve(tol=1e-12)
+    nt = spec.tile_x * spec.tile_y
+    dFg = torch.empty(nt, dtype=torch.float64, device=DEV)
+    dgg = torch.empty(nt, dtype=torch.float64, device=DEV)
+    Fg, gg, cg = g.sensitivities(kappa=spec.kappa, volfrac=spec.volfrac, dF=dFg, dg=dgg)
+    tc = max(compliance_tol(spec, e, f, fx) for e in ref["E_el"])
+    assert abs(Fg - F) <= 3 * tc * abs(F)
+    assert abs(gg - gv) <= 1e-12
+    assert np.abs(host(dFg) - dF).max() <= 1e-8 * np.abs(dF).max()
+    assert np.abs(host(dgg) - dg).max() <= 1e-12 * np.abs(dg).max()
+    # the OC update is replicated: every rank's copy gives the oracle's design
+    xn = torch.empty(nt, dtype=torch.float64, device=DEV)
+    g.ranks[-1].oc_update(dev(x), dFg, dgg, volfrac=spec.volfrac, move=0.2, x_new=xn)
+    assert np.abs(host(xn) - design.oc_update(spec, x, dF, dg)).max() <= 1e-6
+    g.close()
+
+
+def test_strip_rejects_per_rank_solve_and_too_many_ranks():
+    spec, _ = STRIP_SPECS["cant_16x8"]
+    g = group_for(spec, 2, W.design_tile(spec))
+    with pytest.raises(RuntimeError, match="group"):
+        g.ranks[0].pcg_solve()
+    g.close()
+    with pytest.raises(RuntimeError, match="ncx"):
+        MsfemGroup.from_spec(spec, 5)   # 4 coarse columns
+
+
+def test_nccl_transport_one_rank_equals_single_gpu():
+    """The NCCL transport end to end on one GPU (libnccl loaded at run time, a 1-rank
+    communicator, all-reduces captured in the per-iteration CUDA graph): a full design
+    iteration gives the single-GPU context's iterations, compliances and design exactly
+    (a 1-rank all-reduce is the identity; no halos)."""
+    import paper_1411_3923_b200 as pkg
+    spec = SPECS["robust_32x16"]
+    x = W.design_tile(spec)
+    uid = pkg.nccl_unique_id()
+    assert len(uid) == 128
+    mn = Msfem(pkg.problem_from_spec(spec), W.fixed_mask(spec), W.load_vector(spec), rank=0,
+               nranks=1, transport=pkg.MSF_TRANSPORT_NCCL, handle=uid)
+    ms = Msfem.from_spec(spec)
+    nt = spec.tile_x * spec.tile_y
+    xa, xb = torch.empty(nt, dtype=torch.float64, device=DEV), torch.empty(nt, dtype=torch.float64, device=DEV)
+    its_n, comp_n, F_n, g_n = mn.design_iteration(dev(x), xa, tol=1e-10)
+    its_s, comp_s, F_s, g_s = ms.design_iteration(dev(x), xb, tol=1e-10)
+    assert its_n == its_s
+    np.testing.assert_allclose(comp_n, comp_s, rtol=1e-13)
+    assert abs(F_n - F_s) <= 1e-13 * abs(F_s)
+    np.testing.assert_allclose(host(xa), host(xb), rtol=0, atol=1e-12)
+    mn.close()
+
+
+def test_config1_four_strips():
+    """BASELINE configs[1] (1024x512 MBB, 3 robust realisations) on 4 strips: the same
+    iteration counts (+-1) and compliances as the single-GPU path."""
+    spec = W.CONFIGS["c1_mbb_1024x512"]
+    x = W.design_tile(spec)
+    m = single_for(spec, x)
+    its_s, comp_s, _ = m.pcg_solve(tol=spec.tol, max_it=3000)
+    del m
+    torch.cuda.empty_cache()
+    g = group_for(spec, 4, x)
+    its_g, comp_g, nc = g.pcg_solve(tol=spec.tol, max_it=3000)
+    assert not nc
+    for k in range(spec.n_rhs):
+        assert abs(its_g[k] - its_s[k]) <= 1, (its_g, its_s)
+        assert abs(comp_g[k] - comp_s[k]) <= 1e-8 * comp_s[k]
+    g.close()
