@@ -19,6 +19,12 @@ size_t eig_smem_bytes(int mlmax, int mb);
 
 static thread_local std::string g_err;
 
+// programmatic dependent launch for the PCG kernels (launch_k); MSF_PDL=0 disables
+bool g_msf_pdl = [] {
+  const char* e = std::getenv("MSF_PDL");
+  return !(e && std::string(e) == "0");
+}();
+
 int msf_fail(msf_ctx* c, int code, const std::string& msg) {
   if (c) c->err = msg;
   g_err = msg;
@@ -361,6 +367,10 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     const char* mode = std::getenv("MSF_PCG_MODE");
     // default: graph-launched iterations (measured faster); opt-in persistent
     c->persistent = (mode && std::string(mode) == "persistent") && transport == 0;
+    c->stream_iters = mode && std::string(mode) == "stream";
+    if (const char* gi = std::getenv("MSF_GRAPH_ITERS")) c->graph_iters = std::max(1, std::min(64, std::atoi(gi)));
+    const char* cc = std::getenv("MSF_COARSE_COOP");
+    c->coarse_coop = transport == 0 && cc && std::string(cc) == "1";   // opt-in: measured slower
     if (std::getenv("MSF_PERSIST_PROFILE")) {   // debug only: phase timeline buffer
       cudaMalloc(&c->prof_d, 32 * 64 * sizeof(unsigned long long));
       cudaMemset(c->prof_d, 0, 32 * 64 * sizeof(unsigned long long));
@@ -689,10 +699,15 @@ int msf_assemble_coarse(msf_ctx* c) {
 static void enqueue_vcycle(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
                            int rz_mode = 0, bool f0_done = false) {
   launch_sgs_sweep(c, rhs0, nr, r, z, gated, !f0_done, 0, f0_done);  // z = SGS(0; r)
-  launch_residual(c, rhs0, nr, r, z, c->t, gated);                    // t = r - K z
-  launch_restrict(c, rhs0, nr, c->t, gated);
-  launch_coarse_solve(c, rhs0, nr, gated);
-  launch_prolong(c, rhs0, nr, z, gated);
+  if (c->coarse_coop) {
+    launch_residual(c, rhs0, nr, r, z, c->t, gated);                  // t = r - K z
+    launch_coarse_coop(c, rhs0, nr, c->t, z, gated);                  // z += R^T Kc^-1 R t
+  } else {
+    launch_residual(c, rhs0, nr, r, z, c->t, gated);                  // t = r - K z
+    launch_restrict(c, rhs0, nr, c->t, gated);                        // c = R t
+    launch_coarse_solve(c, rhs0, nr, gated);
+    launch_prolong(c, rhs0, nr, z, gated);                            // z += R^T c
+  }
   launch_sgs_sweep(c, rhs0, nr, r, z, gated, false, rz_mode, false); // z = SGS(z; r) (+ r.z)
 }
 
@@ -917,6 +932,21 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
 // PCG iterations as CUDA-graph launches of one captured iteration; the host polls the
 // device-side `active` flags every 4 iterations (converged realisations are no-ops).
 static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
+  if (c->stream_iters) {
+    // kernels launched directly on the stream (programmatic dependent launches chain them)
+    const int check_every = 8;
+    int done = 0;
+    for (int it = 0; it < max_it + check_every && !done; it += check_every) {
+      for (int j = 0; j < check_every; ++j) enqueue_iteration(c, nr);
+      CKL("pcg iterations");
+      int rc = read_scalars(c, nr);
+      if (rc) return rc;
+      done = 1;
+      for (int k = 0; k < nr; ++k)
+        if (c->sc_host[k].active) done = 0;
+    }
+    return MSF_OK;
+  }
   if (!c->iter_graph || c->iter_graph_R != nr) {
     if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
     c->iter_graph = nullptr;
@@ -927,8 +957,10 @@ static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
     c->stream = c->cap_stream;
     cudaError_t e1 = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
     const long long before = c->launches;
-    if (e1 == cudaSuccess) enqueue_iteration(c, nr);
-    c->pcg_launches = c->launches - before;
+    // graph_iters iterations per graph (converged realisations are no-ops inside it)
+    if (e1 == cudaSuccess)
+      for (int j = 0; j < c->graph_iters; ++j) enqueue_iteration(c, nr);
+    c->pcg_launches = (c->launches - before) / c->graph_iters;
     c->launches = before;
     cudaError_t e2 = e1 == cudaSuccess ? cudaStreamEndCapture(c->stream, &g) : e1;
     c->stream = user;
@@ -938,12 +970,12 @@ static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
     cudaGraphDestroy(g);
     c->iter_graph_R = nr;
   }
-  const int check_every = 8;
+  const int check_every = std::max(8, c->graph_iters);
   int done = 0;
   for (int it = 0; it < max_it + check_every && !done; it += check_every) {
-    for (int j = 0; j < check_every; ++j) {
+    for (int j = 0; j < check_every; j += c->graph_iters) {
       CK(cudaGraphLaunch(c->iter_graph, c->stream));
-      c->launches += c->pcg_launches;
+      c->launches += c->pcg_launches * c->graph_iters;
     }
     int rc = read_scalars(c, nr);
     if (rc) return rc;
@@ -1250,6 +1282,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   };
   const int ntimed = c->comm ? 6 : 8;
   for (int i = 0; i < 8; ++i) ms[i] = i < ntimed ? timeit(i) : -1.0;
+  if (ms[7] > 0) ms[7] /= c->graph_iters;   // the graph holds graph_iters iterations
   if (!c->iter_graph || c->iter_graph_R != R) ms[7] = -1.0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

@@ -31,6 +31,8 @@ __global__ void __launch_bounds__(NT) k_restrict(Dims d, const double2* __restri
                                                  const int* __restrict__ agg_by_cls,
                                                  double* cball, const PcgScalars* sc, int rhs0,
                                                  int nr, int gated) {
+  pdl_launch();
+  pdl_wait();
   __shared__ double red[NT / 32][MSF_MAX_RHS * KM];
   bool act[MSF_MAX_RHS];
   bool any = false;
@@ -50,6 +52,8 @@ __global__ void __launch_bounds__(NT) k_prolong(Dims d, const double* __restrict
                                                 const int* __restrict__ cls_of_agg,
                                                 const double* __restrict__ cxall, double2* zall,
                                                 const PcgScalars* sc, int rhs0, int nr, int gated) {
+  pdl_launch();
+  pdl_wait();
   const int iy = blockIdx.x * 32 + (threadIdx.x & 31);
   const int ix = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (ix >= d.nnx || iy >= d.nny) return;
@@ -302,14 +306,14 @@ __global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restric
                                                     const double* __restrict__ Pall,
                                                     double* cball, const PcgScalars* sc,
                                                     int rhs0, int gated) {
+  pdl_launch();
   const int rhs = rhs0 + blockIdx.z;
-  if (gated && !sc[rhs].active) return;
   extern __shared__ double sv[];  // [2][m]
   const int i = surv[blockIdx.y];
   const size_t per = (size_t)d.mc * d.mc;
   cr_forward_rows(d, i, s, blockIdx.x * CR_ROWS, Qall + ((size_t)rhs * d.nbc + (i - s)) * per,
                   Pall + ((size_t)rhs * d.nbc + (i + s)) * per, cball + (size_t)rhs * d.nbc * d.mc,
-                  sv, threadIdx.x, blockDim.x);
+                  sv, threadIdx.x, blockDim.x, gated ? &sc[rhs].active : nullptr);
 }
 
 // back, eliminated k: x_k = Dinv_k b_k - P_k^T x_{k-s} - Q_k^T x_{k+s}
@@ -319,15 +323,15 @@ __global__ void __launch_bounds__(256) k_cr_back(Dims d, const int* __restrict__
                                                  const double* __restrict__ QTall,
                                                  const double* __restrict__ cball, double* cxall,
                                                  const PcgScalars* sc, int rhs0, int gated) {
+  pdl_launch();
   const int rhs = rhs0 + blockIdx.z;
-  if (gated && !sc[rhs].active) return;
   extern __shared__ double sv[];  // [3][m]
   const int k = elim[blockIdx.y];
   const size_t per = (size_t)d.mc * d.mc;
   const size_t blk = ((size_t)rhs * d.nbc + k) * per;
   cr_back_rows(d, k, s, blockIdx.x * CR_ROWS, Dinv + blk, PTall + blk, QTall + blk,
                cball + (size_t)rhs * d.nbc * d.mc, cxall + (size_t)rhs * d.nbc * d.mc, sv,
-               threadIdx.x, blockDim.x);
+               threadIdx.x, blockDim.x, gated ? &sc[rhs].active : nullptr);
 }
 
 // batched transpose dst = src^T for blocks given by src pointers; dst = dst_base + (src - src_base)
@@ -395,6 +399,8 @@ __global__ void __launch_bounds__(256) k_top_solve(Dims d, const int* __restrict
                                                    const double* __restrict__ Atop,
                                                    const double* __restrict__ cball, double* cxall,
                                                    const PcgScalars* sc, int rhs0, int gated) {
+  pdl_launch();
+  pdl_wait();
   const int rhs = rhs0 + blockIdx.y;
   if (gated && !sc[rhs].active) return;
   extern __shared__ double sv[];   // [T*m]
@@ -414,10 +420,10 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
     const size_t n = (size_t)d.nbc * d.mc;
     cudaMemsetAsync(c->cb + rhs0 * n, 0, nr * n * sizeof(double), c->stream);
   }
-#define MSF_RESTRICT(KM)                                                                       \
-  k_restrict<KM><<<c->n_restrict, NT, 0, c->stream>>>(d, (const double2*)t, c->phi,            \
-                                                      c->cls_of_agg_d, c->agg_by_cls_d, c->cb, \
-                                                      c->sc, rhs0, nr, gated ? 1 : 0)
+#define MSF_RESTRICT(KM)                                                                        \
+  launch_k(k_restrict<KM>, dim3(c->n_restrict), dim3(NT), 0, c->stream, d, (const double2*)t,    \
+           (const double*)c->phi, (const int*)c->cls_of_agg_d, (const int*)c->agg_by_cls_d,      \
+           c->cb, (const PcgScalars*)c->sc, rhs0, nr, gated ? 1 : 0)
   if (d.kmax <= 4) MSF_RESTRICT(4);
   else if (d.kmax <= 8) MSF_RESTRICT(8);
   else MSF_RESTRICT(16);
@@ -428,8 +434,9 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
   const Dims& d = c->dl;   // every local node, halo included (identical increments on both ranks)
   dim3 g((d.nny + 31) / 32, (d.nnx + 7) / 8, 1);
-  k_prolong<<<g, NT, 0, c->stream>>>(d, c->phi, c->cls_of_agg_d, c->cx, (double2*)z, c->sc,
-                                     rhs0, nr, gated ? 1 : 0);
+  launch_k(k_prolong, g, dim3(NT), 0, c->stream, d, (const double*)c->phi,
+           (const int*)c->cls_of_agg_d, (const double*)c->cx, (double2*)z, (const PcgScalars*)c->sc,
+           rhs0, nr, gated ? 1 : 0);
   MSF_LAUNCHED(c);
 }
 
@@ -552,23 +559,27 @@ void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
   }
   for (const CrLevel& L : c->cr) {
     if (!L.surv.empty()) {
-      k_cr_forward<<<dim3((m + 15) / 16, (unsigned)L.surv.size(), nr), nthr, 2 * m * sizeof(double),
-                     c->stream>>>(d, L.surv_d, L.s, c->Qc, c->Pc, c->cb, c->sc, rhs0, gated ? 1 : 0);
+      launch_k(k_cr_forward, dim3((m + CR_ROWS - 1) / CR_ROWS, (unsigned)L.surv.size(), nr),
+               dim3(nthr), 2 * m * sizeof(double), c->stream, d, (const int*)L.surv_d, L.s,
+               (const double*)c->Qc, (const double*)c->Pc, c->cb, (const PcgScalars*)c->sc, rhs0,
+               gated ? 1 : 0);
       MSF_LAUNCHED(c);
     }
   }
   // dense top system: one row-chunked GEMV
   {
     const int T = c->top_T, n = T * m;
-    k_top_solve<<<dim3((n + CR_ROWS - 1) / CR_ROWS, nr), nthr, (size_t)n * sizeof(double), c->stream>>>(
-        d, c->top_blocks_d, T, c->Atop, c->cb, c->cx, c->sc, rhs0, gated ? 1 : 0);
+    launch_k(k_top_solve, dim3((n + CR_ROWS - 1) / CR_ROWS, nr), dim3(nthr), (size_t)n * sizeof(double),
+             c->stream, d, (const int*)c->top_blocks_d, T, (const double*)c->Atop,
+             (const double*)c->cb, c->cx, (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
     MSF_LAUNCHED(c);
   }
   for (auto it = c->cr.rbegin(); it != c->cr.rend(); ++it) {
     const CrLevel& L = *it;
-    k_cr_back<<<dim3((m + 15) / 16, (unsigned)L.elim.size(), nr), nthr, 3 * m * sizeof(double),
-                c->stream>>>(d, L.elim_d, L.s, c->Dinv, c->PTc, c->QTc, c->cb, c->cx, c->sc, rhs0,
-                             gated ? 1 : 0);
+    launch_k(k_cr_back, dim3((m + CR_ROWS - 1) / CR_ROWS, (unsigned)L.elim.size(), nr), dim3(nthr),
+             3 * m * sizeof(double), c->stream, d, (const int*)L.elim_d, L.s, (const double*)c->Dinv,
+             (const double*)c->PTc, (const double*)c->QTc, (const double*)c->cb, c->cx,
+             (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
     MSF_LAUNCHED(c);
   }
 }

@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(NTHR) k_apply(Dims d, K0Mat K, const double* _
                                                 double* partials, unsigned* counters, int rhs0,
                                                 int gated, int dot, int max_partials,
                                                 double* dsum) {
+  pdl_launch();
+  pdl_wait();
   const int rhs = rhs0 + blockIdx.z;
   if (gated && !sc[rhs].active) return;
   __shared__ TileSmem S;
@@ -132,6 +134,8 @@ __global__ void __launch_bounds__(NTHR) k_sgs_colour(Dims d, K0Mat K, const doub
                                                      unsigned* counters, int max_partials,
                                                      int rhs0, int gated, int colour,
                                                      int rz_mode, double* dsum) {
+  pdl_launch();
+  pdl_wait();
   const int rhs = rhs0 + blockIdx.z;
   if (gated && !sc[rhs].active) return;
   __shared__ double red[NTHR / 32 + 1];
@@ -222,6 +226,8 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
                                                     const uint8_t* __restrict__ fixn, PcgScalars* sc,
                                                     double* partials, unsigned* counters,
                                                     int max_partials, double* dsum) {
+  pdl_launch();
+  pdl_wait();
   const int rhs = blockIdx.z;
   if (!sc[rhs].active) return;
   __shared__ double red[NTHR / 32 + 1];
@@ -265,6 +271,8 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
 // in-kernel finalisation of the single-GPU path.
 __global__ void k_finalize(PcgScalars* sc, const double* __restrict__ dsum, int kind, int nr,
                            int gated, int rz_mode) {
+  pdl_launch();
+  pdl_wait();
   const int rhs = threadIdx.x;
   if (rhs >= nr) return;
   if (gated && !sc[rhs].active) return;
@@ -274,6 +282,8 @@ __global__ void k_finalize(PcgScalars* sc, const double* __restrict__ dsum, int 
 // p = z + beta p  (p = z at init)
 __global__ void __launch_bounds__(VB) k_pcg_p(Dims d, const double2* __restrict__ zall,
                                               double2* pall, const PcgScalars* sc, int init) {
+  pdl_launch();
+  pdl_wait();
   const int rhs = blockIdx.z;
   if (!sc[rhs].active) return;
   const double beta = init ? 0.0 : sc[rhs].beta;
@@ -360,17 +370,18 @@ int sgs_colour_partials_needed(const Dims& d) {
 // on one GPU); reductions park their sums in c->dsum on a strip context.
 void launch_matvec(msf_ctx* c, int rhs0, int nr, const double* x, double* y, bool gated,
                    bool dot_pq) {
-  k_apply<0><<<apply_grid(c->dl, nr), dim3(TY, TX), 0, c->stream>>>(
-      c->dl, c->K0, c->E_loc, (const double2*)x, (double2*)y, nullptr, c->fixn, c->sc,
-      c->partials, c->counters, rhs0, gated ? 1 : 0, dot_pq ? 1 : 0, c->max_partials, c->dsum);
+  launch_k(k_apply<0>, apply_grid(c->dl, nr), dim3(TY, TX), 0, c->stream,
+           c->dl, c->K0, c->E_loc, (const double2*)x, (double2*)y, (const double2*)nullptr, c->fixn,
+           c->sc, c->partials, c->counters, rhs0, gated ? 1 : 0, dot_pq ? 1 : 0, c->max_partials,
+           c->dsum);
   MSF_LAUNCHED(c);
 }
 
 void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double* x, double* y,
                      bool gated) {
-  k_apply<1><<<apply_grid(c->dl, nr), dim3(TY, TX), 0, c->stream>>>(
-      c->dl, c->K0, c->E_loc, (const double2*)x, (double2*)y, (const double2*)b, c->fixn, c->sc,
-      c->partials, c->counters, rhs0, gated ? 1 : 0, 0, c->max_partials, c->dsum);
+  launch_k(k_apply<1>, apply_grid(c->dl, nr), dim3(TY, TX), 0, c->stream,
+           c->dl, c->K0, c->E_loc, (const double2*)x, (double2*)y, (const double2*)b, c->fixn,
+           c->sc, c->partials, c->counters, rhs0, gated ? 1 : 0, 0, c->max_partials, c->dsum);
   MSF_LAUNCHED(c);
 }
 
@@ -382,11 +393,9 @@ void launch_sgs_phase(msf_ctx* c, int rhs0, int nr, const double* r, double* z, 
   dim3 grd((hy + 31) / 32, (hx + 7) / 8, nr);
   const int g = gated ? 1 : 0;
 #define MSF_SGS(F, B, Z, RZ, col)                                                               \
-  k_sgs_colour<F, B, Z, RZ><<<grd, blk, 0, c->stream>>>(d, c->K0, c->E_loc, (const double2*)r,   \
-                                                        (double2*)z, c->fixn, c->sc,            \
-                                                        c->partials, c->counters,               \
-                                                        c->max_partials, rhs0, g, col, rz_mode, \
-                                                        c->dsum);                               \
+  launch_k(k_sgs_colour<F, B, Z, RZ>, grd, blk, 0, c->stream, d, c->K0, c->E_loc,              \
+           (const double2*)r, (double2*)z, c->fixn, c->sc, c->partials, c->counters,            \
+           c->max_partials, rhs0, g, (int)(col), rz_mode, c->dsum);                               \
   break
   switch (phase) {
     case 0: MSF_SGS(true, false, true, false, 0);
@@ -426,15 +435,16 @@ void launch_update_f0(msf_ctx* c, int nr) {
   const Dims& d = c->dl;
   const int hx = (d.nnx + 1) / 2, hy = (d.nny + 1) / 2;
   dim3 grd((hy + 31) / 32, (hx + 7) / 8, nr);
-  k_update_f0<<<grd, dim3(32, 8), 0, c->stream>>>(
-      d, c->K0, c->E_loc, (double2*)c->u, (double2*)c->r, (const double2*)c->pv,
-      (const double2*)c->q, (double2*)c->z, c->fixn, c->sc, c->partials, c->counters,
-      c->max_partials, c->dsum);
+  launch_k(k_update_f0, grd, dim3(32, 8), 0, c->stream,
+           d, c->K0, c->E_loc, (double2*)c->u, (double2*)c->r, (const double2*)c->pv,
+           (const double2*)c->q, (double2*)c->z, c->fixn, c->sc, c->partials, c->counters,
+           c->max_partials, c->dsum);
   MSF_LAUNCHED(c);
 }
 
 void launch_finalize(msf_ctx* c, int kind, int nr, bool gated, int rz_mode) {
-  k_finalize<<<1, 32, 0, c->stream>>>(c->sc, c->dsum, kind, nr, gated ? 1 : 0, rz_mode);
+  launch_k(k_finalize, dim3(1), dim3(32), 0, c->stream, c->sc, (const double*)c->dsum, kind, nr,
+           gated ? 1 : 0, rz_mode);
   MSF_LAUNCHED(c);
 }
 
@@ -453,8 +463,8 @@ void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it) {
 }
 
 void launch_pcg_p(msf_ctx* c, int nr, bool init) {
-  k_pcg_p<<<dim3(vec_blocks(c->dl), 1, nr), VB, 0, c->stream>>>(
-      c->dl, (const double2*)c->z, (double2*)c->pv, c->sc, init ? 1 : 0);
+  launch_k(k_pcg_p, dim3(vec_blocks(c->dl), 1, nr), dim3(VB), 0, c->stream,
+           c->dl, (const double2*)c->z, (double2*)c->pv, (const PcgScalars*)c->sc, init ? 1 : 0);
   MSF_LAUNCHED(c);
 }
 

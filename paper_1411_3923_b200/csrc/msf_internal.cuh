@@ -207,6 +207,10 @@ struct msf_ctx {
   char* top_jobs_d = nullptr;
   void* cr_levels_d = nullptr;  // CrLevelDev[n levels] for the persistent PCG kernel
   bool persistent = true;       // PCG driver: persistent cooperative kernel (else CUDA graph)
+  int graph_iters = 1;          // PCG iterations per captured graph (env MSF_GRAPH_ITERS)
+  bool stream_iters = false;    // PCG iterations launched on the stream instead of a graph
+  bool coarse_coop = true;      // V-cycle coarse part as one cooperative launch (single GPU)
+  int coop_grid = 0;            // its grid size (0: not yet computed)
   void* prof_d = nullptr;       // debug phase timeline of the persistent kernel (env MSF_PERSIST_PROFILE)
   char* jobs_d = nullptr;       // CR job tables
   int* factor_status = nullptr; // [R] nonzero on failed pivot
@@ -233,6 +237,26 @@ struct msf_ctx {
 
 // ---------------------------------------------------------------- launch bookkeeping
 #define MSF_LAUNCHED(ctx) ((ctx)->launches++)
+
+// Kernel launch with programmatic dependent launch (msfk::pdl_wait / pdl_launch) when
+// g_msf_pdl is set (env MSF_PDL=0 disables).  Only for kernels that call pdl_wait before
+// reading anything a predecessor writes.
+extern bool g_msf_pdl;
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_msf_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // ---------------------------------------------------------------- kernels (fem / pcg)
 void launch_matvec(msf_ctx* c, int rhs0, int nr, const double* x, double* y, bool gated,
@@ -279,6 +303,8 @@ constexpr int MSF_TOP_MAX = 1200;   // max unknowns of the dense top system (T *
 constexpr int MSF_PERSIST_PARTIALS = 3 * MSF_MAX_RHS * 4 * 160;  // 3 slots x 4 rhs x grid
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated);
 void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated);
+// restriction + coarse solve + prolongation in one cooperative launch (msf_persist.cu)
+int launch_coarse_coop(msf_ctx* c, int rhs0, int nr, const double* t, double* z, bool gated);
 
 // ---------------------------------------------------------------- helpers
 int msf_fail(msf_ctx* c, int code, const std::string& msg);

@@ -8,6 +8,16 @@
 
 namespace msfk {
 
+// Programmatic dependent launch (PDL): kernels of the PCG iteration are launched with the
+// programmatic-serialisation attribute (launch_k, msf_internal.cuh).  pdl_launch lets the
+// next kernel's CTAs be scheduled once every CTA of this grid has started; pdl_wait blocks
+// until the previous grid has completed and its writes are visible.  Every such kernel
+// calls pdl_wait before touching data a predecessor writes (including the PCG scalars);
+// only loads of data that is constant during PCG (moduli, coarse blocks) may precede it.
+// Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ Q4 node stencil
 // local index a of the centre node inside element (sx,sy) = (ix-1+sx, iy-1+sy)
 __device__ __forceinline__ constexpr int a_of(int sx, int sy) {
@@ -331,44 +341,58 @@ __device__ __forceinline__ void prolong_node(const Dims& d, const double* __rest
 }
 
 // ------------------------------------------------------------------ cyclic reduction
-// Row-chunked GEMVs: a CTA owns CR_ROWS rows of one block, one warp per row, lanes over
-// the (row-major, coalesced) columns; the neighbour vectors are staged in shared memory.
-constexpr int CR_ROWS = 16;
+// Row-chunked GEMVs: a CTA owns CR_ROWS rows of one block, one warp per row, lanes over the
+// (row-major, coalesced) columns; the neighbour vectors are staged in shared memory.  Each
+// level is latency-bound (a few m x m blocks), so every warp loads the first CR_PF*32
+// columns of its row into registers BEFORE the staging barrier: the matrix and the vector
+// round trips to DRAM overlap and a level costs about one memory latency.
+constexpr int CR_ROWS = 8;    // == warps of the 256-thread CTAs that run these routines
+constexpr int CR_PF = 5;      // columns per lane held in registers per pass (160 per warp)
 
 // forward, survivor i, rows [r0, r0+CR_ROWS): b_i -= Q_{i-s} b_{i-s} + P_{i+s} b_{i+s}
+// active: realisation flag checked after pdl_wait (nullptr: caller already checked)
 __device__ __forceinline__ void cr_forward_rows(const Dims& d, int i, int s, int r0,
                                                 const double* __restrict__ Q,
                                                 const double* __restrict__ P, double* cb,
-                                                double* sv, int tid, int nthreads) {
+                                                double* sv, int tid, int nthreads,
+                                                const int* active = nullptr) {
   const int m = d.mc;
   const bool hl = i - s >= 0, hr = i + s < d.nbc;
+  const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
+  const int r1 = min(m, r0 + CR_ROWS);
+  double qv[CR_PF], pv[CR_PF];
+  auto load = [&](int r, int c0) {
+    const double* Qr = Q + (size_t)r * m;
+    const double* Pr = P + (size_t)r * m;
+#pragma unroll
+    for (int j = 0; j < CR_PF; ++j) {
+      const int c = c0 + lane + 32 * j;
+      qv[j] = (hl && c < m) ? __ldg(Qr + c) : 0.0;
+      pv[j] = (hr && c < m) ? __ldg(Pr + c) : 0.0;
+    }
+  };
+  if (r0 + wid < r1) load(r0 + wid, 0);   // constant during PCG: before the PDL wait
+  pdl_wait();
+  if (active && !*active) return;
   for (int k = tid; k < m; k += nthreads) {
     sv[k] = hl ? cb[(size_t)(i - s) * m + k] : 0.0;
     sv[m + k] = hr ? cb[(size_t)(i + s) * m + k] : 0.0;
   }
   __syncthreads();
-  const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
-  const int r1 = min(m, r0 + CR_ROWS);
   for (int r = r0 + wid; r < r1; r += nw) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    const double* Qr = Q + (size_t)r * m;
-    const double* Pr = P + (size_t)r * m;
-    int c = lane;
-    for (; c + 32 < m; c += 64) {
-      if (hl) {
-        a0 = fma(Qr[c], sv[c], a0);
-        a1 = fma(Qr[c + 32], sv[c + 32], a1);
-      }
-      if (hr) {
-        a2 = fma(Pr[c], sv[m + c], a2);
-        a3 = fma(Pr[c + 32], sv[m + c + 32], a3);
+    double a0 = 0.0, a1 = 0.0;
+    for (int c0 = 0; c0 < m; c0 += 32 * CR_PF) {
+      if (c0 > 0 || r != r0 + wid) load(r, c0);
+#pragma unroll
+      for (int j = 0; j < CR_PF; ++j) {
+        const int c = c0 + lane + 32 * j;
+        if (c < m) {
+          a0 = fma(qv[j], sv[c], a0);
+          a1 = fma(pv[j], sv[m + c], a1);
+        }
       }
     }
-    for (; c < m; c += 32) {
-      if (hl) a0 = fma(Qr[c], sv[c], a0);
-      if (hr) a2 = fma(Pr[c], sv[m + c], a2);
-    }
-    const double acc = warp_sum((a0 + a1) + (a2 + a3));
+    const double acc = warp_sum(a0 + a1);
     if (lane == 0) cb[(size_t)i * m + r] -= acc;
   }
   __syncthreads();
@@ -380,41 +404,49 @@ __device__ __forceinline__ void cr_back_rows(const Dims& d, int k, int s, int r0
                                              const double* __restrict__ PT,
                                              const double* __restrict__ QT,
                                              const double* __restrict__ cb, double* cx,
-                                             double* sv, int tid, int nthreads) {
+                                             double* sv, int tid, int nthreads,
+                                             const int* active = nullptr) {
   const int m = d.mc;
   const bool hl = k - s >= 0, hr = k + s < d.nbc;
+  const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
+  const int r1 = min(m, r0 + CR_ROWS);
+  double dv[CR_PF], pv[CR_PF], qv[CR_PF];
+  auto load = [&](int r, int c0) {
+    const double* Dr = Di + (size_t)r * m;
+    const double* Pr = PT + (size_t)r * m;
+    const double* Qr = QT + (size_t)r * m;
+#pragma unroll
+    for (int j = 0; j < CR_PF; ++j) {
+      const int c = c0 + lane + 32 * j;
+      dv[j] = (c < m) ? __ldg(Dr + c) : 0.0;
+      pv[j] = (hl && c < m) ? __ldg(Pr + c) : 0.0;
+      qv[j] = (hr && c < m) ? __ldg(Qr + c) : 0.0;
+    }
+  };
+  if (r0 + wid < r1) load(r0 + wid, 0);   // constant during PCG: before the PDL wait
+  pdl_wait();
+  if (active && !*active) return;
   for (int j = tid; j < m; j += nthreads) {
     sv[j] = cb[(size_t)k * m + j];
     sv[m + j] = hl ? cx[(size_t)(k - s) * m + j] : 0.0;
     sv[2 * m + j] = hr ? cx[(size_t)(k + s) * m + j] : 0.0;
   }
   __syncthreads();
-  const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
-  const int r1 = min(m, r0 + CR_ROWS);
   for (int r = r0 + wid; r < r1; r += nw) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0;
-    const double* Dr = Di + (size_t)r * m;
-    const double* Pr = PT + (size_t)r * m;
-    const double* Qr = QT + (size_t)r * m;
-    int c = lane;
-    for (; c + 32 < m; c += 64) {
-      a0 = fma(Dr[c], sv[c], a0);
-      a1 = fma(Dr[c + 32], sv[c + 32], a1);
-      if (hl) {
-        a2 = fma(Pr[c], sv[m + c], a2);
-        a3 = fma(Pr[c + 32], sv[m + c + 32], a3);
-      }
-      if (hr) {
-        a4 = fma(Qr[c], sv[2 * m + c], a4);
-        a5 = fma(Qr[c + 32], sv[2 * m + c + 32], a5);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int c0 = 0; c0 < m; c0 += 32 * CR_PF) {
+      if (c0 > 0 || r != r0 + wid) load(r, c0);
+#pragma unroll
+      for (int j = 0; j < CR_PF; ++j) {
+        const int c = c0 + lane + 32 * j;
+        if (c < m) {
+          a0 = fma(dv[j], sv[c], a0);
+          a1 = fma(pv[j], sv[m + c], a1);
+          a2 = fma(qv[j], sv[2 * m + c], a2);
+        }
       }
     }
-    for (; c < m; c += 32) {
-      a0 = fma(Dr[c], sv[c], a0);
-      if (hl) a2 = fma(Pr[c], sv[m + c], a2);
-      if (hr) a4 = fma(Qr[c], sv[2 * m + c], a4);
-    }
-    const double acc = warp_sum((a0 + a1) - (a2 + a3) - (a4 + a5));
+    const double acc = warp_sum(a0 - a1 - a2);
     if (lane == 0) cx[(size_t)k * m + r] = acc;
   }
   __syncthreads();

@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "msf_kern.cuh"
 
@@ -395,6 +396,151 @@ __global__ void __launch_bounds__(PT, PMINB) k_pcg_persistent(PersistArgs A, K0M
   }
 }
 
+// ------------------------------------------------------------------ coarse correction in one launch
+// The coarse part of the V-cycle (restriction c = R_c t, cyclic-reduction forward levels, top
+// solve, back levels, prolongation z += R_c^T x_c) as ONE cooperative launch with grid-wide
+// barriers between the phases.  The phases are latency-bound (later reduction levels touch a
+// few m x m blocks), so a 1.2 us barrier replaces a ~4 us kernel boundary per level.
+struct CoarseArgs {
+  Dims d;
+  const double2* t;
+  double2* z;
+  const double* phi;
+  const int* cls_of_agg;
+  const int* agg_by_cls;
+  int n_restrict;
+  double* cb;
+  double* cx;
+  const double* Dinv;
+  const double* Pc;
+  const double* Qc;
+  const double* PTc;
+  const double* QTc;
+  const CrLevelDev* levels;
+  int nlev;
+  const int* top_blocks;
+  int topT;
+  const double* Atop;
+  const PcgScalars* sc;
+  int rhs0, nr, gated;
+};
+
+template <int KM>
+__global__ void __launch_bounds__(PT) k_coarse_coop(CoarseArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sv[];
+  __shared__ double rred[PT / 32][MSF_MAX_RHS * KM];
+  const Dims& d = A.d;
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  bool act[MSF_MAX_RHS];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < MSF_MAX_RHS; ++k) {
+    act[k] = k >= A.rhs0 && k < A.rhs0 + A.nr && (!A.gated || A.sc[k].active);
+    any |= act[k];
+  }
+  if (!any) return;   // identical decision in every CTA: no barrier is reached
+  // restriction
+  for (int item = b; item < A.n_restrict; item += G)
+    restrict_agg<KM>(d, A.t, A.phi, A.cls_of_agg, A.cb, A.agg_by_cls[item], act, PT, tid, rred);
+  grid.sync();
+  const int nrc = (d.mc + CR_ROWS - 1) / CR_ROWS;
+  const size_t per = (size_t)d.mc * d.mc;
+  const int k0 = A.rhs0, nk = A.nr;
+  for (int l = 0; l < A.nlev; ++l) {
+    const CrLevelDev L = A.levels[l];
+    if (L.s == 0) continue;
+    for (int item = b; item < nrc * L.nsurv * nk; item += G) {
+      const int k = k0 + item / (nrc * L.nsurv), rest = item - (k - k0) * (nrc * L.nsurv);
+      if (!act[k]) continue;
+      const int si = rest / nrc, rc = rest - (rest / nrc) * nrc;
+      const int i = L.surv[si];
+      cr_forward_rows(d, i, L.s, rc * CR_ROWS, A.Qc + ((size_t)k * d.nbc + (i - L.s)) * per,
+                      A.Pc + ((size_t)k * d.nbc + (i + L.s)) * per, A.cb + (size_t)k * d.nbc * d.mc,
+                      sv, tid, PT);
+    }
+    grid.sync();
+  }
+  {
+    const int n = A.topT * d.mc, nrt = (n + CR_ROWS - 1) / CR_ROWS;
+    for (int item = b; item < nrt * nk; item += G) {
+      const int k = k0 + item / nrt, rc = item - (k - k0) * nrt;
+      if (!act[k]) continue;
+      top_solve_rows(d, A.top_blocks, A.topT, A.Atop + (size_t)k * A.topT * A.topT * per,
+                     A.cb + (size_t)k * d.nbc * d.mc, A.cx + (size_t)k * d.nbc * d.mc,
+                     rc * CR_ROWS, sv, tid, PT);
+    }
+    grid.sync();
+  }
+  for (int l = A.nlev - 1; l >= 0; --l) {
+    const CrLevelDev L = A.levels[l];
+    const int s = L.s;
+    for (int item = b; item < nrc * L.nelim * nk; item += G) {
+      const int k = k0 + item / (nrc * L.nelim), rest = item - (k - k0) * (nrc * L.nelim);
+      if (!act[k]) continue;
+      const int ei = rest / nrc, rc = rest - (rest / nrc) * nrc;
+      const int kb = L.elim[ei];
+      const size_t blk = ((size_t)k * d.nbc + kb) * per;
+      cr_back_rows(d, kb, s, rc * CR_ROWS, A.Dinv + blk, A.PTc + blk, A.QTc + blk,
+                   A.cb + (size_t)k * d.nbc * d.mc, A.cx + (size_t)k * d.nbc * d.mc, sv, tid, PT);
+    }
+    grid.sync();
+  }
+  // prolongation, one node per thread (all active realisations)
+  const int nnchunks = (d.nn + PT - 1) / PT;
+  for (int item = b; item < nnchunks; item += G) {
+    const int n = item * PT + tid;
+    if (n < d.nn) prolong_node(d, A.phi, A.cls_of_agg, A.cx, A.z, n / d.nny, n - (n / d.nny) * d.nny, act);
+  }
+}
+
+template <int KM>
+int launch_coarse_coop_km(msf_ctx* c, int rhs0, int nr, const double* t, double* z, bool gated) {
+  const Dims& d = c->dl;
+  const size_t smem = (size_t)std::max(3, c->top_T) * d.mc * sizeof(double);
+  int& G = c->coop_grid;   // CTAs per launch (all resident), computed once per context
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_coarse_coop<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (G == 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_coarse_coop<KM>, PT, smem);
+    int cap = 4;
+    if (const char* e = std::getenv("MSF_COARSE_COOP_CTAS")) cap = std::max(1, std::atoi(e));
+    G = sms * std::max(1, std::min(per, cap));
+  }
+  CoarseArgs A;
+  A.d = d;
+  A.t = (const double2*)t;
+  A.z = (double2*)z;
+  A.phi = c->phi;
+  A.cls_of_agg = c->cls_of_agg_d;
+  A.agg_by_cls = c->agg_by_cls_d;
+  A.n_restrict = c->n_restrict;
+  A.cb = c->cb;
+  A.cx = c->cx;
+  A.Dinv = c->Dinv;
+  A.Pc = c->Pc;
+  A.Qc = c->Qc;
+  A.PTc = c->PTc;
+  A.QTc = c->QTc;
+  A.levels = (const CrLevelDev*)c->cr_levels_d;
+  A.nlev = (int)c->cr.size();
+  A.top_blocks = c->top_blocks_d;
+  A.topT = c->top_T;
+  A.Atop = c->Atop;
+  A.sc = c->sc;
+  A.rhs0 = rhs0;
+  A.nr = nr;
+  A.gated = gated ? 1 : 0;
+  void* args[] = {&A};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)k_coarse_coop<KM>, dim3(G), dim3(PT), args,
+                                              smem, c->stream);
+  MSF_LAUNCHED(c);
+  return msf_cuda_check(c, e, "cudaLaunchCooperativeKernel(k_coarse_coop)");
+}
+
 template <int KM>
 int launch_persistent_km(msf_ctx* c, int nr) {
   const Dims& d = c->d;
@@ -463,6 +609,12 @@ void fill_cr_levels_dev(const std::vector<CrLevel>& cr, void* host_buf) {
     h[l].surv = cr[l].surv_d;
     h[l].elim = cr[l].elim_d;
   }
+}
+
+int launch_coarse_coop(msf_ctx* c, int rhs0, int nr, const double* t, double* z, bool gated) {
+  if (c->d.kmax <= 4) return launch_coarse_coop_km<4>(c, rhs0, nr, t, z, gated);
+  if (c->d.kmax <= 8) return launch_coarse_coop_km<8>(c, rhs0, nr, t, z, gated);
+  return launch_coarse_coop_km<16>(c, rhs0, nr, t, z, gated);
 }
 
 int launch_pcg_persistent(msf_ctx* c, int nr) {
