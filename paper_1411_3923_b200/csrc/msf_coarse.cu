@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(NT) k_restrict(Dims d, const double2* __restri
 
 // ------------------------------------------------------------------ prolongation
 // z(n) += sum_{I,J,a} phi_{I,J,a}(n) x_c[slot(I,J,a)], all active realisations per thread
+template <int KM>
 __global__ void __launch_bounds__(NT) k_prolong(Dims d, const double* __restrict__ phi,
                                                 const int* __restrict__ cls_of_agg,
                                                 const double* __restrict__ cxall, double2* zall,
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(NT) k_prolong(Dims d, const double* __restrict
   bool act[MSF_MAX_RHS];
 #pragma unroll
   for (int r = 0; r < MSF_MAX_RHS; ++r) act[r] = r >= rhs0 && r < rhs0 + nr && (!gated || sc[r].active);
-  prolong_node(d, phi, cls_of_agg, cxall, zall, ix, iy, act);
+  prolong_node<KM>(d, phi, cls_of_agg, cxall, zall, ix, iy, act);
 }
 
 // ------------------------------------------------------------------ Galerkin cell products
@@ -434,9 +435,14 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
   const Dims& d = c->dl;   // every local node, halo included (identical increments on both ranks)
   dim3 g((d.nny + 31) / 32, (d.nnx + 7) / 8, 1);
-  launch_k(k_prolong, g, dim3(NT), 0, c->stream, d, (const double*)c->phi,
-           (const int*)c->cls_of_agg_d, (const double*)c->cx, (double2*)z, (const PcgScalars*)c->sc,
-           rhs0, nr, gated ? 1 : 0);
+#define MSF_PROLONG(KM)                                                                           \
+  launch_k(k_prolong<KM>, g, dim3(NT), 0, c->stream, d, (const double*)c->phi,                      \
+           (const int*)c->cls_of_agg_d, (const double*)c->cx, (double2*)z, (const PcgScalars*)c->sc, \
+           rhs0, nr, gated ? 1 : 0)
+  if (d.kmax <= 4) MSF_PROLONG(4);
+  else if (d.kmax <= 8) MSF_PROLONG(8);
+  else MSF_PROLONG(16);
+#undef MSF_PROLONG
   MSF_LAUNCHED(c);
 }
 

@@ -289,7 +289,9 @@ __device__ __forceinline__ void restrict_agg(const Dims& d, const double2* __res
 
 // ------------------------------------------------------------------ prolongation
 // z(n) += sum_{I,J,a} phi_{I,J,a}(n) x_c[slot(I,J,a)] for the realisations in act[].
-// Per-thread (node ix, iy).
+// Per-thread (node ix, iy).  KM >= kmax: the mode loop is unrolled so that all basis and
+// coarse-value loads of the node are in flight together (one memory latency per node).
+template <int KM>
 __device__ __forceinline__ void prolong_node(const Dims& d, const double* __restrict__ phi,
                                              const int* __restrict__ cls_of_agg,
                                              const double* __restrict__ cxall, double2* zall,
@@ -314,14 +316,17 @@ __device__ __forceinline__ void prolong_node(const Dims& d, const double* __rest
       const int agg = I * (d.ncy + 1) + J;
       const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2;
       const int bn = px * d.by + py;
-      for (int a = 0; a < d.kmax; ++a) {
-        const double2 pv = *reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2);
 #pragma unroll
-        for (int r = 0; r < MSF_MAX_RHS; ++r) {
-          if (act[r]) {
-            const double cv = cxall[(size_t)r * d.nbc * d.mc + (size_t)agg * d.kmax + a];
-            sx[r] = fma(pv.x, cv, sx[r]);
-            sy[r] = fma(pv.y, cv, sy[r]);
+      for (int a = 0; a < KM; ++a) {
+        if (a < d.kmax) {
+          const double2 pv = __ldg(reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2));
+#pragma unroll
+          for (int r = 0; r < MSF_MAX_RHS; ++r) {
+            if (act[r]) {
+              const double cv = cxall[(size_t)r * d.nbc * d.mc + (size_t)agg * d.kmax + a];
+              sx[r] = fma(pv.x, cv, sx[r]);
+              sy[r] = fma(pv.y, cv, sy[r]);
+            }
           }
         }
       }

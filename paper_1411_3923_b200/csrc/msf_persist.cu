@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(PT, PMINB) k_pcg_persistent(PersistArgs A, K0M
     // ---------------- G: prolongation
     for (int item = b; item < nnchunks; item += G) {
       const int n = item * PT + tid;
-      if (n < d.nn) prolong_node(d, A.phi, A.cls_of_agg, A.cx, A.z, n / d.nny, n - (n / d.nny) * d.nny, act);
+      if (n < d.nn) prolong_node<KM>(d, A.phi, A.cls_of_agg, A.cx, A.z, n / d.nny, n - (n / d.nny) * d.nny, act);
     }
     gsync();
 
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(PT) k_coarse_coop(CoarseArgs A) {
   const int nnchunks = (d.nn + PT - 1) / PT;
   for (int item = b; item < nnchunks; item += G) {
     const int n = item * PT + tid;
-    if (n < d.nn) prolong_node(d, A.phi, A.cls_of_agg, A.cx, A.z, n / d.nny, n - (n / d.nny) * d.nny, act);
+    if (n < d.nn) prolong_node<KM>(d, A.phi, A.cls_of_agg, A.cx, A.z, n / d.nny, n - (n / d.nny) * d.nny, act);
   }
 }
 
