@@ -19,49 +19,108 @@ namespace {
 
 constexpr int NT = 256;
 
-// ------------------------------------------------------------------ restriction
-// c[slot(I,J,a)] = sum_n phi_{I,J,a}(n) . t(n) for every active realisation at once: one CTA
-// per agglomerate (launched in class order, agg_by_cls, so consecutive CTAs share the
-// class basis in L2), each box node's basis values are loaded once and applied to all
-// realisations (Phi_i^T [t_1 .. t_R]).
+// ------------------------------------------------------------------ per-realisation restriction
+// One CTA per (agglomerate, realisation): the cost follows the number of ACTIVE realisations
+// (most PCG iterations run the slowest-converging realisation alone).  Agglomerates in
+// class order (consecutive CTAs share the class basis in L2).
 template <int KM>
-__global__ void __launch_bounds__(NT) k_restrict(Dims d, const double2* __restrict__ tall,
-                                                 const double* __restrict__ phi,
-                                                 const int* __restrict__ cls_of_agg,
-                                                 const int* __restrict__ agg_by_cls,
-                                                 double* cball, const PcgScalars* sc, int rhs0,
-                                                 int nr, int gated) {
+__global__ void __launch_bounds__(NT) k_restrict1(Dims d, const double2* __restrict__ tall,
+                                                  const double* __restrict__ phi,
+                                                  const int* __restrict__ cls_of_agg,
+                                                  const int* __restrict__ agg_by_cls,
+                                                  double* cball, const PcgScalars* sc, int rhs0,
+                                                  int gated) {
   pdl_launch();
   pdl_wait();
-  __shared__ double red[NT / 32][MSF_MAX_RHS * KM];
-  bool act[MSF_MAX_RHS];
-  bool any = false;
+  const int rhs = rhs0 + blockIdx.y;
+  if (gated && !sc[rhs].active) return;
+  __shared__ double red[NT / 32][KM];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int agg = agg_by_cls[blockIdx.x];
+  const int I = agg / (d.ncy + 1), J = agg - (agg / (d.ncy + 1)) * (d.ncy + 1);
+  const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2;
+  const double2* t = tall + (size_t)rhs * d.nn;
+  const int gx0 = I * d.cx - d.cx - d.gox, gy0 = J * d.cy - d.cy;
+  // interior of the padded box (chi vanishes on its boundary ring), clipped to the strip
+  const int ix_lo = max(1, -gx0), ix_hi = min(d.bx - 2, d.nnx - 1 - gx0);
+  const int iy_lo = max(1, -gy0), iy_hi = min(d.by - 2, d.nny - 1 - gy0);
+  const int w = iy_hi - iy_lo + 1, h = ix_hi - ix_lo + 1;
+  double acc[KM];
 #pragma unroll
-  for (int r = 0; r < MSF_MAX_RHS; ++r) {
-    act[r] = r >= rhs0 && r < rhs0 + nr && (!gated || sc[r].active);
-    any |= act[r];
+  for (int a = 0; a < KM; ++a) acc[a] = 0.0;
+  for (int k = tid; k < w * h; k += NT) {
+    const int px = ix_lo + k / w, py = iy_lo + (k - (k / w) * w);
+    const double2 tv = t[(size_t)(gx0 + px) * d.nny + (gy0 + py)];
+    const int bn = px * d.by + py;
+#pragma unroll
+    for (int a = 0; a < KM; ++a) {
+      if (a < d.kmax) {
+        const double2 pv = __ldg(reinterpret_cast<const double2*>(ph + ((size_t)a * d.box_nodes + bn) * 2));
+        acc[a] = fma(pv.x, tv.x, fma(pv.y, tv.y, acc[a]));
+      }
+    }
   }
-  if (!any) return;
-  restrict_agg<KM>(d, tall, phi, cls_of_agg, cball, agg_by_cls[blockIdx.x], act, NT,
-                   threadIdx.x, red);
+#pragma unroll
+  for (int a = 0; a < KM; ++a) {
+    if (a < d.kmax) {
+      const double v = warp_sum(acc[a]);
+      if (lane == 0) red[wid][a] = v;
+    }
+  }
+  __syncthreads();
+  if (tid < d.kmax) {
+    double s2 = 0.0;
+    for (int w2 = 0; w2 < NT / 32; ++w2) s2 += red[w2][tid];
+    cball[(size_t)rhs * d.nbc * d.mc + (size_t)agg * d.kmax + tid] = s2;
+  }
 }
 
-// ------------------------------------------------------------------ prolongation
-// z(n) += sum_{I,J,a} phi_{I,J,a}(n) x_c[slot(I,J,a)], all active realisations per thread
+// ------------------------------------------------------------------ per-realisation prolongation
+// z(n) += sum_{I,J,a} phi_{I,J,a}(n) x_c[slot(I,J,a)], one (node, realisation) per thread.
 template <int KM>
-__global__ void __launch_bounds__(NT) k_prolong(Dims d, const double* __restrict__ phi,
-                                                const int* __restrict__ cls_of_agg,
-                                                const double* __restrict__ cxall, double2* zall,
-                                                const PcgScalars* sc, int rhs0, int nr, int gated) {
+__global__ void __launch_bounds__(NT) k_prolong1(Dims d, const double* __restrict__ phi,
+                                                 const int* __restrict__ cls_of_agg,
+                                                 const double* __restrict__ cxall, double2* zall,
+                                                 const PcgScalars* sc, int rhs0, int gated) {
   pdl_launch();
   pdl_wait();
+  const int rhs = rhs0 + blockIdx.z;
+  if (gated && !sc[rhs].active) return;
   const int iy = blockIdx.x * 32 + (threadIdx.x & 31);
   const int ix = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (ix >= d.nnx || iy >= d.nny) return;
-  bool act[MSF_MAX_RHS];
+  const double* xc = cxall + (size_t)rhs * d.nbc * d.mc;
+  const int gix = ix + d.gox;
+  const int I0 = gix / d.cx, J0 = iy / d.cy;
+  double sx = 0.0, sy = 0.0;
 #pragma unroll
-  for (int r = 0; r < MSF_MAX_RHS; ++r) act[r] = r >= rhs0 && r < rhs0 + nr && (!gated || sc[r].active);
-  prolong_node<KM>(d, phi, cls_of_agg, cxall, zall, ix, iy, act);
+  for (int di = 0; di < 2; ++di) {
+    const int I = I0 + di;
+    const int px = gix - (I * d.cx - d.cx);
+    if (I > d.ncx || px >= d.bx) continue;
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj) {
+      const int J = J0 + dj;
+      const int py = iy - (J * d.cy - d.cy);
+      if (J > d.ncy || py >= d.by) continue;
+      const int agg = I * (d.ncy + 1) + J;
+      const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2 + (size_t)(px * d.by + py) * 2;
+#pragma unroll
+      for (int a = 0; a < KM; ++a) {
+        if (a < d.kmax) {
+          const double2 pv = __ldg(reinterpret_cast<const double2*>(ph + (size_t)a * d.box_nodes * 2));
+          const double cv = __ldg(xc + (size_t)agg * d.kmax + a);
+          sx = fma(pv.x, cv, sx);
+          sy = fma(pv.y, cv, sy);
+        }
+      }
+    }
+  }
+  double2* z = zall + (size_t)rhs * d.nn + (size_t)ix * d.nny + iy;
+  double2 zv = *z;
+  zv.x += sx;
+  zv.y += sy;
+  *z = zv;
 }
 
 // ------------------------------------------------------------------ Galerkin cell products
@@ -422,9 +481,9 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
     cudaMemsetAsync(c->cb + rhs0 * n, 0, nr * n * sizeof(double), c->stream);
   }
 #define MSF_RESTRICT(KM)                                                                        \
-  launch_k(k_restrict<KM>, dim3(c->n_restrict), dim3(NT), 0, c->stream, d, (const double2*)t,    \
+  launch_k(k_restrict1<KM>, dim3(c->n_restrict, nr), dim3(NT), 0, c->stream, d, (const double2*)t, \
            (const double*)c->phi, (const int*)c->cls_of_agg_d, (const int*)c->agg_by_cls_d,      \
-           c->cb, (const PcgScalars*)c->sc, rhs0, nr, gated ? 1 : 0)
+           c->cb, (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0)
   if (d.kmax <= 4) MSF_RESTRICT(4);
   else if (d.kmax <= 8) MSF_RESTRICT(8);
   else MSF_RESTRICT(16);
@@ -436,9 +495,9 @@ void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
   const Dims& d = c->dl;   // every local node, halo included (identical increments on both ranks)
   dim3 g((d.nny + 31) / 32, (d.nnx + 7) / 8, 1);
 #define MSF_PROLONG(KM)                                                                           \
-  launch_k(k_prolong<KM>, g, dim3(NT), 0, c->stream, d, (const double*)c->phi,                      \
+  launch_k(k_prolong1<KM>, dim3(g.x, g.y, nr), dim3(NT), 0, c->stream, d, (const double*)c->phi,    \
            (const int*)c->cls_of_agg_d, (const double*)c->cx, (double2*)z, (const PcgScalars*)c->sc, \
-           rhs0, nr, gated ? 1 : 0)
+           rhs0, gated ? 1 : 0)
   if (d.kmax <= 4) MSF_PROLONG(4);
   else if (d.kmax <= 8) MSF_PROLONG(8);
   else MSF_PROLONG(16);
