@@ -1207,7 +1207,10 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   if (!c || !ms || !bytes || reps < 1) return msf_fail(c, MSF_ERR_ARG, "bad argument");
   if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "bench_kernels before assemble_coarse");
   const Dims& d = c->d;
-  const int R = d.R;
+  // MSF_BENCH_NR: time with only the first realisations active (the single-realisation
+  // regime most PCG iterations run in)
+  int R = d.R;
+  if (const char* e = std::getenv("MSF_BENCH_NR")) R = std::max(1, std::min(R, std::atoi(e)));
   // fine-grid traffic on this rank's strip; the communicating composites (V-cycle, PCG
   // iteration) are not timed on a strip context (ms = -1)
   const double nn = c->dl.nn, ne = (double)c->dl.nelx * c->dl.nely;

@@ -33,12 +33,19 @@ __device__ bool arrive_last(double v, double* partials, int slot, unsigned* coun
   return s_ticket == total - 1;
 }
 
-// In the last block: deterministic sum of partials[0..n).
+// In the last block: deterministic sum of partials[0..n).  Eight independent loads per
+// thread are in flight at once (the last block is the serial tail of every PCG reduction).
 __device__ double reduce_partials(const double* partials, int n, double* sm, int tid,
                                   int nthreads) {
-  double s = 0.0;
-  for (int i = tid; i < n; i += nthreads) s += __ldcg(partials + i);
-  return block_sum_all(s, sm, tid, nthreads);
+  double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int i = tid;
+  for (; i + 7 * nthreads < n; i += 8 * nthreads) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] += __ldcg(partials + i + j * nthreads);
+  }
+  for (int j = 0; i < n; i += nthreads, ++j) s[j & 7] += __ldcg(partials + i);
+  const double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  return block_sum_all(t, sm, tid, nthreads);
 }
 
 // PCG scalar update from a completed (global) dot product (reading R9)
