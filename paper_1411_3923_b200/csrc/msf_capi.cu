@@ -63,6 +63,7 @@ struct Plan {
   std::vector<CrLevel> cr;
   std::vector<int> top_blocks;
   size_t top_ptrs = 0;
+  size_t binv_n = 1;          // matrices per blocked-inverse batch (scratch sizing)
   size_t jobs_bytes = 0;
   int max_partials = 0;
   size_t total = 0;
@@ -253,6 +254,14 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     add(T * 4);                              // top block list
   }
   add(2 * MSF_MAX_RHS * 4);                  // factor_status
+  {
+    // blocked-inverse scratch for the largest batch (a reduction level or the top pivots)
+    size_t nmax = (size_t)d.R;
+    for (const CrLevel& L : P.cr) nmax = std::max(nmax, (size_t)L.n_inv);
+    P.binv_n = nmax;
+    add(nmax * 64 * 64 * 8);
+    add(nmax * 64 * (size_t)d.mc * 8);
+  }
   add(R * sizeof(PcgScalars));
   add((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
   add(cr_levels_dev_bytes((int)P.cr.size()));
@@ -448,6 +457,9 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     c->top_blocks_d = (int*)take(T * 4);
   }
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
+  c->binv_P = (double*)take(P.binv_n * 64 * 64 * 8);
+  c->binv_R = (double*)take(P.binv_n * 64 * (size_t)d.mc * 8);
+  if (const char* e = std::getenv("MSF_BLOCKED_INV_MIN")) c->blocked_inv_min = std::max(1, std::atoi(e));
   c->sc = (PcgScalars*)take(R * sizeof(PcgScalars));
   c->partials = (double*)take((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
   c->cr_levels_d = take(cr_levels_dev_bytes((int)c->cr.size()));

@@ -300,6 +300,164 @@ __global__ void __launch_bounds__(1024) k_spd_inverse(double** mats, int m, int*
   for (size_t e = tid; e < (size_t)m * m; e += nth) A[e] = -A[e];
 }
 
+// ------------------------------------------------------------------ blocked SPD inverse
+// In-place inverse of a batch of SPD m x m matrices by block Gauss-Jordan with GB x GB
+// pivot blocks (the blocked form of the sweep above, for large m where one CTA per matrix
+// is O(m^3) on a single SM).  Pivot block p (rows/cols [p0, p0+pb)):
+//   P = A_pp^-1 ;  R_j = P A_pj ;  A_ij -= A_ip R_j (i, j != p) ;  A_ip = -A_ip P ;
+//   A_pj = R_j ;  A_pp = P.
+// After all pivots A holds A^-1.  Pivots are checked > 0 (SPD).
+constexpr int GB = 64;
+
+// acc(4x4 per thread) += A[0:64, 0:K] (lda) * B[0:K, 0:64] (ldb) for a 64x64 output tile;
+// rows >= M / cols >= N / k >= K are zero-padded.  256 threads: rows (tid/16)*4.., cols (tid%16)*4..
+__device__ __forceinline__ void gemm_tile_acc(const double* __restrict__ A, int lda,
+                                              const double* __restrict__ B, int ldb, int M, int N,
+                                              int K, double (&acc)[4][4], double (*As)[33],
+                                              double (*Bs)[65]) {
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    for (int e = tid; e < 64 * 32; e += 256) {
+      const int r = e >> 5, kk = e & 31;
+      As[r][kk] = (r < M && k0 + kk < K) ? A[(size_t)r * lda + k0 + kk] : 0.0;
+    }
+    for (int e = tid; e < 32 * 64; e += 256) {
+      const int kk = e >> 6, c = e & 63;
+      Bs[kk][c] = (k0 + kk < K && c < N) ? B[(size_t)(k0 + kk) * ldb + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[tr * 4 + i][kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tc * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+}
+
+// C (ldc, M x N valid) = alpha * acc + beta * C
+__device__ __forceinline__ void gemm_tile_store(double* C, int ldc, int M, int N,
+                                                const double (&acc)[4][4], double alpha,
+                                                double beta) {
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = tr * 4 + i;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = tc * 4 + j;
+      if (c >= N) continue;
+      double* p = C + (size_t)r * ldc + c;
+      *p = alpha * acc[i][j] + (beta != 0.0 ? beta * *p : 0.0);
+    }
+  }
+}
+
+// P = A_pp^-1 by the scalar sweep in shared memory (pb <= GB)
+__global__ void __launch_bounds__(256) k_binv_pivot(double** mats, int m, int p0, int pb,
+                                                    double* Pbuf, int* status) {
+  __shared__ double a[GB][GB + 1];
+  __shared__ double rowk[GB], colk[GB];
+  const double* A = mats[blockIdx.x];
+  double* P = Pbuf + (size_t)blockIdx.x * GB * GB;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < pb * pb; e += 256) {
+    const int i = e / pb, j = e - (e / pb) * pb;
+    a[i][j] = A[(size_t)(p0 + i) * m + p0 + j];
+  }
+  __syncthreads();
+  for (int k = 0; k < pb; ++k) {
+    for (int i = tid; i < pb; i += 256) {
+      rowk[i] = a[k][i];
+      colk[i] = a[i][k];
+    }
+    __syncthreads();
+    const double piv = rowk[k];
+    if (!(piv > 0.0) && tid == 0) atomicExch(status, 1);
+    const double ip = 1.0 / piv;
+    for (int e = tid; e < pb * pb; e += 256) {
+      const int i = e / pb, j = e - (e / pb) * pb;
+      double v;
+      if (i == k && j == k) v = -ip;
+      else if (i == k) v = rowk[j] * ip;
+      else if (j == k) v = colk[i] * ip;
+      else v = a[i][j] - colk[i] * rowk[j] * ip;
+      a[i][j] = v;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < pb * pb; e += 256) {
+    const int i = e / pb, j = e - (e / pb) * pb;
+    P[i * GB + j] = -a[i][j];
+  }
+}
+
+// R[0:pb, j-tile] = P A[p rows, j-tile]   (Rbuf per matrix: GB x m, ld m)
+__global__ void __launch_bounds__(256) k_binv_rowpanel(double** mats, int m, int p0, int pb,
+                                                       const double* Pbuf, double* Rbuf) {
+  __shared__ double As[64][33];
+  __shared__ double Bs[32][65];
+  const double* A = mats[blockIdx.y];
+  const int j0 = blockIdx.x * 64;
+  double acc[4][4] = {};
+  gemm_tile_acc(Pbuf + (size_t)blockIdx.y * GB * GB, GB, A + (size_t)p0 * m + j0, m, pb,
+                min(64, m - j0), pb, acc, As, Bs);
+  gemm_tile_store(Rbuf + (size_t)blockIdx.y * GB * m + j0, m, pb, min(64, m - j0), acc, 1.0, 0.0);
+}
+
+// A[i-tile, j-tile] -= A[i-tile, p cols] R[:, j-tile]  for i-tile, j-tile != p
+__global__ void __launch_bounds__(256) k_binv_trailing(double** mats, int m, int p0, int pb,
+                                                       const double* Rbuf) {
+  const int it = blockIdx.y, jt = blockIdx.x, pt = p0 / GB;
+  if (it == pt || jt == pt) return;
+  __shared__ double As[64][33];
+  __shared__ double Bs[32][65];
+  double* A = mats[blockIdx.z];
+  const int i0 = it * 64, j0 = jt * 64;
+  double acc[4][4] = {};
+  gemm_tile_acc(A + (size_t)i0 * m + p0, m, Rbuf + (size_t)blockIdx.z * GB * m + j0, m,
+                min(64, m - i0), min(64, m - j0), pb, acc, As, Bs);
+  gemm_tile_store(A + (size_t)i0 * m + j0, m, min(64, m - i0), min(64, m - j0), acc, -1.0, 1.0);
+}
+
+// y = 0: A[i-tile, p cols] = -A[i-tile, p cols] P (i-tile != p), A_pp = P (i-tile == p)
+// y = 1: A[p rows, j-tile] = R[:, j-tile] (j-tile != p)
+__global__ void __launch_bounds__(256) k_binv_panels(double** mats, int m, int p0, int pb,
+                                                     const double* Pbuf, const double* Rbuf) {
+  __shared__ double As[64][33];
+  __shared__ double Bs[32][65];
+  double* A = mats[blockIdx.z];
+  const double* P = Pbuf + (size_t)blockIdx.z * GB * GB;
+  const int t = blockIdx.x, pt = p0 / GB, t0 = t * 64, tn = min(64, m - t0);
+  if (blockIdx.y == 0) {
+    if (t == pt) {
+      for (int e = threadIdx.x; e < pb * pb; e += 256) {
+        const int i = e / pb, j = e - (e / pb) * pb;
+        A[(size_t)(p0 + i) * m + p0 + j] = P[i * GB + j];
+      }
+      return;
+    }
+    double acc[4][4] = {};
+    gemm_tile_acc(A + (size_t)t0 * m + p0, m, P, GB, tn, pb, pb, acc, As, Bs);
+    gemm_tile_store(A + (size_t)t0 * m + p0, m, tn, pb, acc, -1.0, 0.0);
+  } else {
+    if (t == pt) return;
+    const double* R = Rbuf + (size_t)blockIdx.z * GB * m;
+    for (int e = threadIdx.x; e < pb * tn; e += 256) {
+      const int i = e / tn, j = e - (e / tn) * tn;
+      A[(size_t)(p0 + i) * m + t0 + j] = R[(size_t)i * m + t0 + j];
+    }
+  }
+}
+
 __global__ void k_copy_blocks(double** src, double** dst, int m) {
   const double* s = src[blockIdx.y];
   double* t = dst[blockIdx.y];
@@ -531,17 +689,34 @@ void launch_coarse_galerkin(msf_ctx* c) {
   }
 }
 
+// In-place inverses of n SPD m x m matrices (device pointer table mats): the one-CTA sweep for
+// small m, the blocked Gauss-Jordan above for m >= blocked_inv_min.
+static void launch_spd_inverse(msf_ctx* c, double** mats, int n, int m) {
+  if (m >= c->blocked_inv_min) {
+    const int T = (m + GB - 1) / GB;
+    for (int pt = 0; pt < T; ++pt) {
+      const int p0 = pt * GB, pb = std::min(GB, m - p0);
+      k_binv_pivot<<<n, 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_P, c->factor_status);
+      k_binv_rowpanel<<<dim3(T, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_P, c->binv_R);
+      k_binv_trailing<<<dim3(T, T, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_R);
+      k_binv_panels<<<dim3(T, 2, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_P, c->binv_R);
+      c->launches += 4;
+    }
+  } else {
+    k_spd_inverse<<<n, 1024, 2 * (size_t)m * sizeof(double), c->stream>>>(mats, m, c->factor_status);
+    MSF_LAUNCHED(c);
+  }
+}
+
 void launch_assemble_coarse(msf_ctx* c) {
   launch_coarse_galerkin(c);
   const Dims& d = c->d;
   const int m = d.mc;
-  const size_t inv_smem = 2 * (size_t)m * sizeof(double);
   const dim3 gt((m + 63) / 64, (m + 63) / 64);
   for (const CrLevel& L : c->cr) {
     k_copy_blocks<<<dim3(64, L.n_inv), 256, 0, c->stream>>>(L.invsrc, L.inv, m);
     MSF_LAUNCHED(c);
-    k_spd_inverse<<<L.n_inv, 1024, inv_smem, c->stream>>>(L.inv, m, c->factor_status);
-    MSF_LAUNCHED(c);
+    launch_spd_inverse(c, L.inv, L.n_inv, m);
     if (L.s == 0) continue;
     if (L.nP) {
       k_gemm<false, false><<<dim3(gt.x, gt.y, L.nP), 256, 0, c->stream>>>(L.pA, L.pB, L.pC, m, 1.0, 0.0);
@@ -588,7 +763,7 @@ void launch_assemble_coarse(msf_ctx* c) {
   for (const TopStep& S : c->top_steps) {
     k_copy_blocks<<<dim3(64, S.nI), 256, 0, c->stream>>>(S.invsrc, S.inv, m);
     MSF_LAUNCHED(c);
-    k_spd_inverse<<<S.nI, 1024, inv_smem, c->stream>>>(S.inv, m, c->factor_status);
+    launch_spd_inverse(c, S.inv, S.nI, m);
     MSF_LAUNCHED(c);
     if (S.nW) {
       k_gemm<false, false><<<dim3(gt.x, gt.y, S.nW), 256, 0, c->stream>>>(S.wA, S.wB, S.wC, m, 1.0, 0.0);

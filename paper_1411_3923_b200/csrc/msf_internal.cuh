@@ -214,6 +214,9 @@ struct msf_ctx {
   void* prof_d = nullptr;       // debug phase timeline of the persistent kernel (env MSF_PERSIST_PROFILE)
   char* jobs_d = nullptr;       // CR job tables
   int* factor_status = nullptr; // [R] nonzero on failed pivot
+  double* binv_P = nullptr;     // blocked inverse scratch: [n_max][64*64] pivot inverses
+  double* binv_R = nullptr;     //                          [n_max][64*m] row panels
+  int blocked_inv_min = 256;    // m from which SPD block inverses use the blocked path
 
   PcgScalars* sc = nullptr;     // [R]
   double* partials = nullptr;   // [R][max_blocks]
