@@ -460,6 +460,7 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   c->binv_P = (double*)take(P.binv_n * 64 * 64 * 8);
   c->binv_R = (double*)take(P.binv_n * 64 * (size_t)d.mc * 8);
   if (const char* e = std::getenv("MSF_BLOCKED_INV_MIN")) c->blocked_inv_min = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("MSF_RESTRICT_THREADS")) c->restrict_threads = std::atoi(e);
   c->sc = (PcgScalars*)take(R * sizeof(PcgScalars));
   c->partials = (double*)take((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
   c->cr_levels_d = take(cr_levels_dev_bytes((int)c->cr.size()));

@@ -23,8 +23,8 @@ constexpr int NT = 256;
 // One CTA per (agglomerate, realisation): the cost follows the number of ACTIVE realisations
 // (most PCG iterations run the slowest-converging realisation alone).  Agglomerates in
 // class order (consecutive CTAs share the class basis in L2).
-template <int KM>
-__global__ void __launch_bounds__(NT) k_restrict1(Dims d, const double2* __restrict__ tall,
+template <int KM, int NTR>
+__global__ void __launch_bounds__(NTR) k_restrict1(Dims d, const double2* __restrict__ tall,
                                                   const double* __restrict__ phi,
                                                   const int* __restrict__ cls_of_agg,
                                                   const int* __restrict__ agg_by_cls,
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(NT) k_restrict1(Dims d, const double2* __restr
   pdl_wait();
   const int rhs = rhs0 + blockIdx.y;
   if (gated && !sc[rhs].active) return;
-  __shared__ double red[NT / 32][KM];
+  __shared__ double red[NTR / 32][KM];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int agg = agg_by_cls[blockIdx.x];
   const int I = agg / (d.ncy + 1), J = agg - (agg / (d.ncy + 1)) * (d.ncy + 1);
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(NT) k_restrict1(Dims d, const double2* __restr
   double acc[KM];
 #pragma unroll
   for (int a = 0; a < KM; ++a) acc[a] = 0.0;
-  for (int k = tid; k < w * h; k += NT) {
+  for (int k = tid; k < w * h; k += NTR) {
     const int px = ix_lo + k / w, py = iy_lo + (k - (k / w) * w);
     const double2 tv = t[(size_t)(gx0 + px) * d.nny + (gy0 + py)];
     const int bn = px * d.by + py;
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(NT) k_restrict1(Dims d, const double2* __restr
   __syncthreads();
   if (tid < d.kmax) {
     double s2 = 0.0;
-    for (int w2 = 0; w2 < NT / 32; ++w2) s2 += red[w2][tid];
+    for (int w2 = 0; w2 < NTR / 32; ++w2) s2 += red[w2][tid];
     cball[(size_t)rhs * d.nbc * d.mc + (size_t)agg * d.kmax + tid] = s2;
   }
 }
@@ -638,13 +638,23 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
     const size_t n = (size_t)d.nbc * d.mc;
     cudaMemsetAsync(c->cb + rhs0 * n, 0, nr * n * sizeof(double), c->stream);
   }
-#define MSF_RESTRICT(KM)                                                                        \
-  launch_k(k_restrict1<KM>, dim3(c->n_restrict, nr), dim3(NT), 0, c->stream, d, (const double2*)t, \
-           (const double*)c->phi, (const int*)c->cls_of_agg_d, (const int*)c->agg_by_cls_d,      \
-           c->cb, (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0)
-  if (d.kmax <= 4) MSF_RESTRICT(4);
-  else if (d.kmax <= 8) MSF_RESTRICT(8);
-  else MSF_RESTRICT(16);
+#define MSF_RESTRICT(KM, NTR)                                                                   \
+  launch_k(k_restrict1<KM, NTR>, dim3(c->n_restrict, nr), dim3(NTR), 0, c->stream, d,            \
+           (const double2*)t, (const double*)c->phi, (const int*)c->cls_of_agg_d,                \
+           (const int*)c->agg_by_cls_d, c->cb, (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0)
+#define MSF_RESTRICT_T(NTR)                     \
+  do {                                          \
+    if (d.kmax <= 4) MSF_RESTRICT(4, NTR);      \
+    else if (d.kmax <= 8) MSF_RESTRICT(8, NTR); \
+    else MSF_RESTRICT(16, NTR);                 \
+  } while (0)
+  // threads per agglomerate CTA: 256 measured fastest (512 / 1024: 19 / 40 us vs 15 us at one
+  // realisation on configs[1]; larger block reductions, fewer CTAs per SM)
+  const int ntr = c->restrict_threads > 0 ? c->restrict_threads : 256;
+  if (ntr >= 1024) MSF_RESTRICT_T(1024);
+  else if (ntr >= 512) MSF_RESTRICT_T(512);
+  else MSF_RESTRICT_T(256);
+#undef MSF_RESTRICT_T
 #undef MSF_RESTRICT
   MSF_LAUNCHED(c);
 }

@@ -216,7 +216,8 @@ struct msf_ctx {
   int* factor_status = nullptr; // [R] nonzero on failed pivot
   double* binv_P = nullptr;     // blocked inverse scratch: [n_max][64*64] pivot inverses
   double* binv_R = nullptr;     //                          [n_max][64*m] row panels
-  int blocked_inv_min = 256;    // m from which SPD block inverses use the blocked path
+  int blocked_inv_min = 256;
+  int restrict_threads = 0;     // threads per agglomerate CTA (0: from the box size)    // m from which SPD block inverses use the blocked path
 
   PcgScalars* sc = nullptr;     // [R]
   double* partials = nullptr;   // [R][max_blocks]
