@@ -19,6 +19,17 @@ size_t eig_smem_bytes(int mlmax, int mb);
 
 static thread_local std::string g_err;
 
+static void destroy_graphs(msf_ctx* c) {
+  if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
+  c->iter_graph = nullptr;
+  c->iter_graph_R = -1;
+  for (auto& row : c->range_graph)
+    for (auto& g : row) {
+      if (g) cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+}
+
 // programmatic dependent launch for the PCG kernels (launch_k); MSF_PDL=0 disables
 bool g_msf_pdl = [] {
   const char* e = std::getenv("MSF_PDL");
@@ -646,7 +657,7 @@ extern "C" {
 int msf_destroy(msf_ctx* c) {
   if (!c) return MSF_OK;
   dist_comm_destroy(c);
-  if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
+  destroy_graphs(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->scal_host) cudaFreeHost(c->scal_host);
@@ -657,11 +668,7 @@ int msf_destroy(msf_ctx* c) {
 int msf_set_stream(msf_ctx* c, void* stream) {
   if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
   c->stream = (cudaStream_t)stream;
-  if (c->iter_graph) {
-    cudaGraphExecDestroy(c->iter_graph);
-    c->iter_graph = nullptr;
-    c->iter_graph_R = -1;
-  }
+  destroy_graphs(c);
   return MSF_OK;
 }
 
@@ -724,12 +731,14 @@ static void enqueue_vcycle(msf_ctx* c, int rhs0, int nr, const double* r, double
   launch_sgs_sweep(c, rhs0, nr, r, z, gated, false, rz_mode, false); // z = SGS(z; r) (+ r.z)
 }
 
-static void enqueue_iteration(msf_ctx* c, int nr) {
-  launch_matvec(c, 0, nr, c->pv, c->q, true, true);   // q = K p, alpha
-  launch_update_f0(c, nr);                             // u, r, ||r||, z = F0(0; r)
-  enqueue_vcycle(c, 0, nr, c->r, c->z, true, 2, true);
-  launch_pcg_p(c, nr, false);
+// one PCG iteration for the realisations [rhs0, rhs0 + nr)
+static void enqueue_iteration(msf_ctx* c, int rhs0, int nr) {
+  launch_matvec(c, rhs0, nr, c->pv, c->q, true, true);   // q = K p, alpha
+  launch_update_f0(c, rhs0, nr);                         // u, r, ||r||, z = F0(0; r)
+  enqueue_vcycle(c, rhs0, nr, c->r, c->z, true, 2, true);
+  launch_pcg_p(c, rhs0, nr, false);
 }
+
 
 static int read_scalars(msf_ctx* c, int nr) {
   CK(cudaMemcpyAsync(c->sc_host, c->sc, nr * sizeof(PcgScalars), cudaMemcpyDeviceToHost, c->stream));
@@ -791,11 +800,11 @@ static int dist_iteration(const Ranks& cs, int nr) {
   int rc;
   for (msf_ctx* c : cs) launch_matvec(c, 0, nr, c->pv, c->q, true, true);
   if ((rc = dist_reduce(cs, FIN_PQ, nr, true, 0))) return rc;
-  for (msf_ctx* c : cs) launch_update_f0(c, nr);
+  for (msf_ctx* c : cs) launch_update_f0(c, 0, nr);
   if ((rc = dist_reduce(cs, FIN_RR, nr, true, 0))) return rc;
   if ((rc = dist_halo(cs, &msf_ctx::z, nr))) return rc;
   if ((rc = dist_vcycle(cs, nr, true, 2))) return rc;
-  for (msf_ctx* c : cs) launch_pcg_p(c, nr, false);
+  for (msf_ctx* c : cs) launch_pcg_p(c, 0, nr, false);
   return MSF_OK;
 }
 
@@ -813,7 +822,7 @@ static int dist_pcg_solve(const Ranks& cs, int nr, double tol, int max_it, int32
   for (msf_ctx* x : cs) launch_pcg_init(x, nr, tol, max_it);
   if ((rc = dist_reduce(cs, FIN_F, nr, false, 0))) return rc;
   if ((rc = dist_vcycle(cs, nr, false, 1))) return rc;
-  for (msf_ctx* x : cs) launch_pcg_p(x, nr, true);
+  for (msf_ctx* x : cs) launch_pcg_p(x, 0, nr, true);
   CKL("dist pcg init");
   // one process per GPU: the iteration (kernels + NCCL) is captured once as a CUDA graph
   const bool graph = cs.size() == 1;
@@ -903,7 +912,7 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
   const long long l0 = c->launches;
   launch_pcg_init(c, nr, tol, max_it);
   enqueue_vcycle(c, 0, nr, c->r, c->z, true, 1);
-  launch_pcg_p(c, nr, true);
+  launch_pcg_p(c, 0, nr, true);
   CKL("pcg init");
   if (c->persistent) {
     // all iterations in one cooperative launch (msf_persist.cu), no host round trips
@@ -942,6 +951,32 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
   return MSF_OK;
 }
 
+// Graph of graph_iters PCG iterations for the realisations [rhs0, rhs0 + nr), captured on
+// first use on a private stream (the caller's may be the legacy stream, which cannot be
+// captured) and launched on the caller's stream.
+static int range_graph(msf_ctx* c, int rhs0, int nr, cudaGraphExec_t* out) {
+  cudaGraphExec_t& slot = c->range_graph[rhs0][nr];
+  if (!slot) {
+    cudaGraph_t g;
+    cudaStream_t user = c->stream;
+    c->stream = c->cap_stream;
+    cudaError_t e1 = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+    const long long before = c->launches;
+    if (e1 == cudaSuccess)
+      for (int j = 0; j < c->graph_iters; ++j) enqueue_iteration(c, rhs0, nr);
+    c->pcg_launches = (c->launches - before) / c->graph_iters;
+    c->launches = before;
+    cudaError_t e2 = e1 == cudaSuccess ? cudaStreamEndCapture(c->stream, &g) : e1;
+    c->stream = user;
+    CK(e1);
+    CK(e2);
+    CK(cudaGraphInstantiate(&slot, g, 0));
+    cudaGraphDestroy(g);
+  }
+  *out = slot;
+  return MSF_OK;
+}
+
 // PCG iterations as CUDA-graph launches of one captured iteration; the host polls the
 // device-side `active` flags every 4 iterations (converged realisations are no-ops).
 static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
@@ -950,7 +985,7 @@ static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
     const int check_every = 8;
     int done = 0;
     for (int it = 0; it < max_it + check_every && !done; it += check_every) {
-      for (int j = 0; j < check_every; ++j) enqueue_iteration(c, nr);
+      for (int j = 0; j < check_every; ++j) enqueue_iteration(c, 0, nr);
       CKL("pcg iterations");
       int rc = read_scalars(c, nr);
       if (rc) return rc;
@@ -960,41 +995,28 @@ static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
     }
     return MSF_OK;
   }
-  if (!c->iter_graph || c->iter_graph_R != nr) {
-    if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
-    c->iter_graph = nullptr;
-    cudaGraph_t g;
-    // capture on a private stream (the caller's may be the legacy stream, which cannot be
-    // captured); the graph is launched on the caller's stream below.
-    cudaStream_t user = c->stream;
-    c->stream = c->cap_stream;
-    cudaError_t e1 = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
-    const long long before = c->launches;
-    // graph_iters iterations per graph (converged realisations are no-ops inside it)
-    if (e1 == cudaSuccess)
-      for (int j = 0; j < c->graph_iters; ++j) enqueue_iteration(c, nr);
-    c->pcg_launches = (c->launches - before) / c->graph_iters;
-    c->launches = before;
-    cudaError_t e2 = e1 == cudaSuccess ? cudaStreamEndCapture(c->stream, &g) : e1;
-    c->stream = user;
-    CK(e1);
-    CK(e2);
-    CK(cudaGraphInstantiate(&c->iter_graph, g, 0));
-    cudaGraphDestroy(g);
-    c->iter_graph_R = nr;
-  }
+  // active realisations are a contiguous range most of the time (the eroded realisation
+  // converges last); each poll narrows [lo, hi) and switches to that range's graph
+  int lo = 0, hi = nr;
   const int check_every = std::max(8, c->graph_iters);
-  int done = 0;
-  for (int it = 0; it < max_it + check_every && !done; it += check_every) {
+  for (int it = 0; it < max_it + check_every; it += check_every) {
+    cudaGraphExec_t g = nullptr;
+    int rc = range_graph(c, lo, hi - lo, &g);
+    if (rc) return rc;
     for (int j = 0; j < check_every; j += c->graph_iters) {
-      CK(cudaGraphLaunch(c->iter_graph, c->stream));
+      CK(cudaGraphLaunch(g, c->stream));
       c->launches += c->pcg_launches * c->graph_iters;
     }
-    int rc = read_scalars(c, nr);
+    rc = read_scalars(c, nr);
     if (rc) return rc;
-    done = 1;
+    lo = nr;
+    hi = -1;
     for (int k = 0; k < nr; ++k)
-      if (c->sc_host[k].active) done = 0;
+      if (c->sc_host[k].active) {
+        lo = std::min(lo, k);
+        hi = std::max(hi, k + 1);
+      }
+    if (hi < 0) break;
   }
   return MSF_OK;
 }
@@ -1256,10 +1278,10 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
     if (!(s.rz != 0.0)) s.rz = 1.0;
   }
   CK(cudaMemcpyAsync(c->sc, act.data(), R * sizeof(PcgScalars), cudaMemcpyHostToDevice, c->stream));
-  if (!c->iter_graph || c->iter_graph_R != R) {
-    // build the iteration graph for all realisations
-    double dummy = 0.0;
-    (void)dummy;
+  cudaGraphExec_t gR = nullptr;
+  if (!c->comm) {
+    int rc = range_graph(c, 0, R, &gR);
+    if (rc) return rc;
   }
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
@@ -1274,7 +1296,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
         case 4: launch_prolong(c, 0, R, c->z, false); break;
         case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
         case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
-        case 7: if (c->iter_graph) cudaGraphLaunch(c->iter_graph, c->stream); break;
+        case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
       }
     }
     cudaEventRecord(e0, c->stream);
@@ -1287,7 +1309,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
         case 4: launch_prolong(c, 0, R, c->z, false); break;
         case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
         case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
-        case 7: if (c->iter_graph) cudaGraphLaunch(c->iter_graph, c->stream); break;
+        case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
       }
     }
     cudaEventRecord(e1, c->stream);
@@ -1299,7 +1321,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   const int ntimed = c->comm ? 6 : 8;
   for (int i = 0; i < 8; ++i) ms[i] = i < ntimed ? timeit(i) : -1.0;
   if (ms[7] > 0) ms[7] /= c->graph_iters;   // the graph holds graph_iters iterations
-  if (!c->iter_graph || c->iter_graph_R != R) ms[7] = -1.0;
+  if (!gR) ms[7] = -1.0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   CK(cudaMemcpyAsync(c->sc, saved.data(), R * sizeof(PcgScalars), cudaMemcpyHostToDevice, c->stream));

@@ -232,10 +232,10 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
                                                     const double2* __restrict__ qall, double2* zall,
                                                     const uint8_t* __restrict__ fixn, PcgScalars* sc,
                                                     double* partials, unsigned* counters,
-                                                    int max_partials, double* dsum) {
+                                                    int max_partials, double* dsum, int rhs0) {
   pdl_launch();
   pdl_wait();
-  const int rhs = blockIdx.z;
+  const int rhs = rhs0 + blockIdx.z;
   if (!sc[rhs].active) return;
   __shared__ double red[NTHR / 32 + 1];
   const int qx = blockIdx.y * blockDim.y + threadIdx.y;
@@ -288,10 +288,11 @@ __global__ void k_finalize(PcgScalars* sc, const double* __restrict__ dsum, int 
 
 // p = z + beta p  (p = z at init)
 __global__ void __launch_bounds__(VB) k_pcg_p(Dims d, const double2* __restrict__ zall,
-                                              double2* pall, const PcgScalars* sc, int init) {
+                                              double2* pall, const PcgScalars* sc, int init,
+                                              int rhs0) {
   pdl_launch();
   pdl_wait();
-  const int rhs = blockIdx.z;
+  const int rhs = rhs0 + blockIdx.z;
   if (!sc[rhs].active) return;
   const double beta = init ? 0.0 : sc[rhs].beta;
   const double2* z = zall + (size_t)rhs * d.nn;
@@ -438,14 +439,14 @@ void launch_sgs(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool g
   launch_sgs_sweep(c, rhs0, nr, r, z, gated, false, 0, false);
 }
 
-void launch_update_f0(msf_ctx* c, int nr) {
+void launch_update_f0(msf_ctx* c, int rhs0, int nr) {
   const Dims& d = c->dl;
   const int hx = (d.nnx + 1) / 2, hy = (d.nny + 1) / 2;
   dim3 grd((hy + 31) / 32, (hx + 7) / 8, nr);
   launch_k(k_update_f0, grd, dim3(32, 8), 0, c->stream,
            d, c->K0, c->E_loc, (double2*)c->u, (double2*)c->r, (const double2*)c->pv,
            (const double2*)c->q, (double2*)c->z, c->fixn, c->sc, c->partials, c->counters,
-           c->max_partials, c->dsum);
+           c->max_partials, c->dsum, rhs0);
   MSF_LAUNCHED(c);
 }
 
@@ -469,9 +470,10 @@ void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it) {
   MSF_LAUNCHED(c);
 }
 
-void launch_pcg_p(msf_ctx* c, int nr, bool init) {
+void launch_pcg_p(msf_ctx* c, int rhs0, int nr, bool init) {
   launch_k(k_pcg_p, dim3(vec_blocks(c->dl), 1, nr), dim3(VB), 0, c->stream,
-           c->dl, (const double2*)c->z, (double2*)c->pv, (const PcgScalars*)c->sc, init ? 1 : 0);
+           c->dl, (const double2*)c->z, (double2*)c->pv, (const PcgScalars*)c->sc, init ? 1 : 0,
+           rhs0);
   MSF_LAUNCHED(c);
 }
 

@@ -235,8 +235,11 @@ struct msf_ctx {
   long long pcg_launches = 0;
   int eig_iters_used = 0;
 
-  cudaGraphExec_t iter_graph = nullptr;
+  cudaGraphExec_t iter_graph = nullptr;   // strip partition: one iteration for all realisations
   int iter_graph_R = -1;
+  // one graph per contiguous active realisation range [rhs0, rhs0 + nr): converged
+  // realisations drop out of the launch grids instead of exiting from every CTA
+  cudaGraphExec_t range_graph[MSF_MAX_RHS][MSF_MAX_RHS + 1] = {};
 };
 
 // ---------------------------------------------------------------- launch bookkeeping
@@ -277,10 +280,10 @@ void launch_sgs_phase(msf_ctx* c, int rhs0, int nr, const double* r, double* z, 
 // PCG scalar update from the all-reduced dsum[kind] (strip partition)
 void launch_finalize(msf_ctx* c, int kind, int nr, bool gated, int rz_mode);
 // fused u/r update + ||r||^2 + zero-start forward GS colour 0 (PCG iteration)
-void launch_update_f0(msf_ctx* c, int nr);
+void launch_update_f0(msf_ctx* c, int rhs0, int nr);
 void launch_mask_copy(msf_ctx* c, const double* x, double* y, int n2nn);
 void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it);
-void launch_pcg_p(msf_ctx* c, int nr, bool init);
+void launch_pcg_p(msf_ctx* c, int rhs0, int nr, bool init);
 void launch_compliance(msf_ctx* c, int nr);
 
 // ---------------------------------------------------------------- filter / design
