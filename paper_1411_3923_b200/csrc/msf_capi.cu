@@ -275,6 +275,7 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   }
   add(R * sizeof(PcgScalars));
   add((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
+  add(R * (size_t)P.max_partials * 8);       // apart
   add(cr_levels_dev_bytes((int)P.cr.size()));
   add(R * 8 * 4);                            // counters
   add(64 * 8);                               // scal
@@ -472,8 +473,10 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   c->binv_R = (double*)take(P.binv_n * 64 * (size_t)d.mc * 8);
   if (const char* e = std::getenv("MSF_BLOCKED_INV_MIN")) c->blocked_inv_min = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("MSF_RESTRICT_THREADS")) c->restrict_threads = std::atoi(e);
+  if (const char* e = std::getenv("MSF_APPLY_DIRECT")) c->apply_direct = std::string(e) != "0";
   c->sc = (PcgScalars*)take(R * sizeof(PcgScalars));
   c->partials = (double*)take((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
+  c->apart = (double*)take(R * (size_t)P.max_partials * 8);
   c->cr_levels_d = take(cr_levels_dev_bytes((int)c->cr.size()));
   c->counters = (unsigned*)take(R * 8 * 4);
   c->scal = (double*)take(64 * 8);

@@ -129,6 +129,82 @@ __global__ void __launch_bounds__(NTHR) k_apply(Dims d, K0Mat K, const double* _
   }
 }
 
+// ------------------------------------------------------------------ direct-load operator apply
+// One node per thread, neighbourhood and moduli loaded straight from global memory through
+// L1 (the access pattern of the Gauss-Seidel colour kernel), no shared-memory staging or
+// block barrier before the stencil.
+template <int MODE>
+__global__ void __launch_bounds__(NTHR) k_apply_direct(Dims d, K0Mat K, const double* __restrict__ Eall,
+                                                       const double2* __restrict__ xall,
+                                                       double2* __restrict__ yall,
+                                                       const double2* __restrict__ ball,
+                                                       const uint8_t* __restrict__ fixn, PcgScalars* sc,
+                                                       double* partials, unsigned* counters, int rhs0,
+                                                       int gated, int dot, int max_partials,
+                                                       double* dsum, double* apart) {
+  pdl_launch();
+  pdl_wait();
+  const int rhs = rhs0 + blockIdx.z;
+  if (gated && !sc[rhs].active) return;
+  __shared__ double red[NTHR / 32 + 1];
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int ix = blockIdx.y * blockDim.y + threadIdx.y;
+  const int iy = blockIdx.x * blockDim.x + threadIdx.x;
+  const double* E = Eall + (size_t)rhs * d.estride;
+  const double2* x = xall + (size_t)rhs * d.nn;
+  double dv = 0.0;
+  if (ix < d.nnx && iy < d.nny) {
+    double Eloc[2][2];
+    double2 zloc[3][3];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int ex = ix - 1 + a, ey = iy - 1 + c;
+        Eloc[a][c] = (ex >= 0 && ex < d.nelx && ey >= 0 && ey < d.nely) ? __ldg(E + (size_t)ex * d.nely + ey) : 0.0;
+      }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int gx = ix - 1 + a, gy = iy - 1 + c;
+        zloc[a][c] = (gx >= 0 && gx < d.nnx && gy >= 0 && gy < d.nny) ? __ldg(x + (size_t)gx * d.nny + gy)
+                                                                      : make_double2(0.0, 0.0);
+      }
+    double ox, oy, dxx, dxy, dyx, dyy;
+    apply_node(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
+    const size_t n = (size_t)ix * d.nny + iy;
+    const uint8_t fm = fixn[n];
+    double2 out;
+    if (MODE == 1) {
+      const double2 bb = ball[(size_t)rhs * d.nn + n];
+      out = make_double2(bb.x - ox, bb.y - oy);
+    } else {
+      out = make_double2(ox, oy);
+    }
+    if (fm & 1) out.x = 0.0;
+    if (fm & 2) out.y = 0.0;
+    yall[(size_t)rhs * d.nn + n] = out;
+    dv = zloc[1][1].x * out.x + zloc[1][1].y * out.y;
+  }
+  if (dot == 2) {
+    // partial only (no fence / ticket): the consumer (k_update_f0) reduces the partials
+    const double s = block_sum_all(dv, red, tid, NTHR);
+    if (tid == 0) apart[(size_t)rhs * max_partials + blockIdx.y * gridDim.x + blockIdx.x] = s;
+  } else if (dot) {
+    const double s = block_sum_all(dv, red, tid, NTHR);
+    const unsigned nblk = gridDim.x * gridDim.y;
+    const int slot = blockIdx.y * gridDim.x + blockIdx.x;
+    if (arrive_last(s, partials + (size_t)rhs * max_partials, slot, counters + rhs * 8, nblk, tid)) {
+      const double tot = reduce_partials(partials + (size_t)rhs * max_partials, nblk, red, tid, NTHR);
+      if (tid == 0) {
+        fin_or_park(sc, dsum, rhs, FIN_PQ, tot, 0);
+        counters[rhs * 8] = 0;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ Gauss-Seidel colour phase
 // Thread per node quad; see msfk::sgs_quad.  RZ: r.z of the final iterate -> beta (rz_mode 1:
 // PCG init, beta = 0; 2: iteration).
@@ -232,7 +308,8 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
                                                     const double2* __restrict__ qall, double2* zall,
                                                     const uint8_t* __restrict__ fixn, PcgScalars* sc,
                                                     double* partials, unsigned* counters,
-                                                    int max_partials, double* dsum, int rhs0) {
+                                                    int max_partials, double* dsum, int rhs0,
+                                                    const double* __restrict__ apart, int napart) {
   pdl_launch();
   pdl_wait();
   const int rhs = rhs0 + blockIdx.z;
@@ -241,25 +318,50 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
   const int qx = blockIdx.y * blockDim.y + threadIdx.y;
   const int qy = blockIdx.x * blockDim.x + threadIdx.x;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  const double alpha = sc[rhs].alpha;
   const size_t off = (size_t)rhs * d.nn;
+  // the quad's p, q, u, r are loaded before alpha is known
+  double2 pv[4], qv[4], uv[4], rv[4];
+#pragma unroll
+  for (int dn = 0; dn < 4; ++dn) {
+    const int gx = 2 * qx + (dn & 1), gy = 2 * qy + (dn >> 1);
+    if (gx < d.nnx && gy < d.nny) {
+      const size_t n = off + (size_t)gx * d.nny + gy;
+      pv[dn] = pall[n];
+      qv[dn] = qall[n];
+      uv[dn] = uall[n];
+      rv[dn] = rall[n];
+    }
+  }
+  double alpha;
+  if (napart > 0) {
+    // p.Ap from the operator's per-CTA partials: every CTA sums them in the same fixed order
+    // (identical alpha everywhere); CTA 0 records pq and alpha
+    const double pq = reduce_partials(apart + (size_t)rhs * max_partials, napart, red, tid, NTHR);
+    alpha = sc[rhs].rz / pq;
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+      sc[rhs].pq = pq;
+      sc[rhs].alpha = alpha;
+    }
+  } else {
+    alpha = sc[rhs].alpha;
+  }
   double s = 0.0;
 #pragma unroll
   for (int dn = 0; dn < 4; ++dn) {
     const int gx = 2 * qx + (dn & 1), gy = 2 * qy + (dn >> 1);
     if (gx < d.nnx && gy < d.nny) {
       const size_t n = off + (size_t)gx * d.nny + gy;
-      const double2 pv = pall[n], qv = qall[n];
-      double2 uv = uall[n], rv = rall[n];
-      uv.x = fma(alpha, pv.x, uv.x);
-      uv.y = fma(alpha, pv.y, uv.y);
-      rv.x = fma(-alpha, qv.x, rv.x);
-      rv.y = fma(-alpha, qv.y, rv.y);
-      uall[n] = uv;
-      rall[n] = rv;
-      s += rv.x * rv.x + rv.y * rv.y;
+      double2 u2 = uv[dn], r2 = rv[dn];
+      u2.x = fma(alpha, pv[dn].x, u2.x);
+      u2.y = fma(alpha, pv[dn].y, u2.y);
+      r2.x = fma(-alpha, qv[dn].x, r2.x);
+      r2.y = fma(-alpha, qv[dn].y, r2.y);
+      uall[n] = u2;
+      rall[n] = r2;
+      s += r2.x * r2.x + r2.y * r2.y;
     }
   }
+  __syncthreads();   // red[] reused below
   sgs_quad<true, false, true, false>(d, K, Eall + (size_t)rhs * d.estride, rall + off, zall + off,
                                      fixn, qx, qy, 0);
   s = block_sum_all(s, red, tid, NTHR);
@@ -376,8 +478,27 @@ int sgs_colour_partials_needed(const Dims& d) {
 
 // Fine-grid launchers run on this rank's grid c->dl with the moduli c->E_loc (the whole grid
 // on one GPU); reductions park their sums in c->dsum on a strip context.
+// direct-load apply (default; MSF_APPLY_DIRECT=0 selects the shared-memory tile kernel)
+template <int MODE>
+static bool launch_apply_direct(msf_ctx* c, int rhs0, int nr, const double* x, double* y,
+                                const double* bvec, bool gated, bool dot) {
+  if (!c->apply_direct) return false;
+  const Dims& d = c->dl;
+  // p.Ap on one GPU: partials only, reduced by the next kernel (k_update_f0); strips need the
+  // all-reduce, so the last-block finalisation parks the local sum
+  const int dmode = !dot ? 0 : c->comm ? 1 : 2;
+  launch_k(k_apply_direct<MODE>, dim3((d.nny + 31) / 32, (d.nnx + 7) / 8, nr), dim3(32, 8), 0,
+           c->stream, d, c->K0, (const double*)c->E_loc, (const double2*)x, (double2*)y,
+           (const double2*)bvec, c->fixn, c->sc, c->partials, c->counters, rhs0, gated ? 1 : 0,
+           dmode, c->max_partials, c->dsum, c->apart);
+  c->apart_n = dmode == 2 ? ((d.nny + 31) / 32) * ((d.nnx + 7) / 8) : 0;
+  MSF_LAUNCHED(c);
+  return true;
+}
+
 void launch_matvec(msf_ctx* c, int rhs0, int nr, const double* x, double* y, bool gated,
                    bool dot_pq) {
+  if (launch_apply_direct<0>(c, rhs0, nr, x, y, nullptr, gated, dot_pq)) return;
   launch_k(k_apply<0>, apply_grid(c->dl, nr), dim3(TY, TX), 0, c->stream,
            c->dl, c->K0, c->E_loc, (const double2*)x, (double2*)y, (const double2*)nullptr, c->fixn,
            c->sc, c->partials, c->counters, rhs0, gated ? 1 : 0, dot_pq ? 1 : 0, c->max_partials,
@@ -387,6 +508,7 @@ void launch_matvec(msf_ctx* c, int rhs0, int nr, const double* x, double* y, boo
 
 void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double* x, double* y,
                      bool gated) {
+  if (launch_apply_direct<1>(c, rhs0, nr, x, y, b, gated, false)) return;
   launch_k(k_apply<1>, apply_grid(c->dl, nr), dim3(TY, TX), 0, c->stream,
            c->dl, c->K0, c->E_loc, (const double2*)x, (double2*)y, (const double2*)b, c->fixn,
            c->sc, c->partials, c->counters, rhs0, gated ? 1 : 0, 0, c->max_partials, c->dsum);
@@ -443,10 +565,13 @@ void launch_update_f0(msf_ctx* c, int rhs0, int nr) {
   const Dims& d = c->dl;
   const int hx = (d.nnx + 1) / 2, hy = (d.nny + 1) / 2;
   dim3 grd((hy + 31) / 32, (hx + 7) / 8, nr);
+  // alpha from the operator's partials when the preceding matvec left them (one GPU)
+  const int napart = c->apart_n;
+  c->apart_n = 0;
   launch_k(k_update_f0, grd, dim3(32, 8), 0, c->stream,
            d, c->K0, c->E_loc, (double2*)c->u, (double2*)c->r, (const double2*)c->pv,
            (const double2*)c->q, (double2*)c->z, c->fixn, c->sc, c->partials, c->counters,
-           c->max_partials, c->dsum, rhs0);
+           c->max_partials, c->dsum, rhs0, (const double*)c->apart, napart);
   MSF_LAUNCHED(c);
 }
 

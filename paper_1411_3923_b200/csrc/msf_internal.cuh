@@ -217,7 +217,10 @@ struct msf_ctx {
   double* binv_P = nullptr;     // blocked inverse scratch: [n_max][64*64] pivot inverses
   double* binv_R = nullptr;     //                          [n_max][64*m] row panels
   int blocked_inv_min = 256;
-  int restrict_threads = 0;     // threads per agglomerate CTA (0: from the box size)    // m from which SPD block inverses use the blocked path
+  int restrict_threads = 0;
+  bool apply_direct = true;     // operator apply with direct (L1) neighbourhood loads
+  double* apart = nullptr;      // [R][max_partials] operator p.Ap partials (one GPU)
+  int apart_n = 0;              // partial count left by the last matvec (0: none pending)     // threads per agglomerate CTA (0: from the box size)    // m from which SPD block inverses use the blocked path
 
   PcgScalars* sc = nullptr;     // [R]
   double* partials = nullptr;   // [R][max_blocks]
