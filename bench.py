@@ -298,7 +298,11 @@ def run_ours(args, spec):
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
                      "peak_source": peak_src},
-        "kernels": {k: {"ms": v[0], "alg_GBps": v[1] / (v[0] / 1e3) / 1e9 if v[0] > 0 else None}
+        # every timed kernel (all realisations active, PCG launch configuration): average ms per
+        # launch-set, algorithmic GB/s and its fraction of the measured HBM peak
+        "kernels": {k: {"ms": v[0],
+                        "alg_GBps": v[1] / (v[0] / 1e3) / 1e9 if v[0] > 0 else None,
+                        "hbm_frac": v[1] / (v[0] / 1e3) / 1e9 / peak if v[0] > 0 else None}
                     for k, v in kb.items()},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,

@@ -179,7 +179,8 @@ int msf_launch_count(msf_ctx* ctx, int64_t* count, int reset);
  * bytes[i]: algorithmic HBM bytes per launch, for
  * i = 0 operator apply q = K p (+ p.q), 1 one Gauss-Seidel colour sweep, 2 restriction,
  * 3 coarse solve (all cyclic-reduction levels), 4 prolongation, 5 residual t = r - K z,
- * 6 full V-cycle, 7 one PCG iteration (graph). */
+ * 6 full V-cycle, 7 one PCG iteration (graph), 8 PCG update fused with the zero-start colour-0
+ * phase, 9 p update.  ms and bytes hold 10 entries. */
 int msf_bench_kernels(msf_ctx* ctx, int reps, double* ms, double* bytes);
 
 /* ---- strip partition over ranks (multi-GPU) -------------------------

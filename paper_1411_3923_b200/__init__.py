@@ -337,11 +337,11 @@ class Msfem:
 
     def bench_kernels(self, reps=20):
         """Per-kernel average ms and algorithmic bytes per launch (see msf_bench_kernels)."""
-        ms = (ctypes.c_double * 8)()
-        by = (ctypes.c_double * 8)()
+        ms = (ctypes.c_double * 10)()
+        by = (ctypes.c_double * 10)()
         self._check(self.lib.msf_bench_kernels(self.ctx, reps, ms, by))
         names = ["apply", "sgs_colour", "restrict", "coarse_solve", "prolong", "residual",
-                 "vcycle", "pcg_iteration"]
+                 "vcycle", "pcg_iteration", "update_f0", "p_update"]
         return {n: (ms[i], by[i]) for i, n in enumerate(names)}
 
 

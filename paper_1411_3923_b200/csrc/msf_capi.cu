@@ -1268,6 +1268,8 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   bytes[5] = R * (nn * 16 * 3 + ne * 8) + nn;                        // z, r, E -> t
   bytes[6] = 2 * bytes[1] + bytes[2] + bytes[3] + bytes[4] + bytes[5];
   bytes[7] = bytes[0] + bytes[6] + R * nn * 16 * 6 + R * nn * 16 * 2 + R * nn * 16 * 3;
+  bytes[8] = R * (nn * 16 * 6 + ne * 8 + nn / 4 * 16 * 2) + nn / 4;    // p q u r -> u r, F0
+  bytes[9] = R * nn * 16 * 3;                                          // z, p -> p
   // keep every realisation active during the timing, restore afterwards
   std::vector<PcgScalars> saved(R);
   CK(cudaMemcpyAsync(saved.data(), c->sc, R * sizeof(PcgScalars), cudaMemcpyDeviceToHost, c->stream));
@@ -1300,6 +1302,8 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
         case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
         case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
         case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
+        case 8: launch_update_f0(c, 0, R); break;
+        case 9: launch_pcg_p(c, 0, R, false); break;
       }
     }
     cudaEventRecord(e0, c->stream);
@@ -1313,6 +1317,8 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
         case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
         case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
         case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
+        case 8: launch_update_f0(c, 0, R); break;
+        case 9: launch_pcg_p(c, 0, R, false); break;
       }
     }
     cudaEventRecord(e1, c->stream);
@@ -1322,7 +1328,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
     return (double)t / reps;
   };
   const int ntimed = c->comm ? 6 : 8;
-  for (int i = 0; i < 8; ++i) ms[i] = i < ntimed ? timeit(i) : -1.0;
+  for (int i = 0; i < 10; ++i) ms[i] = (i < ntimed || i >= 8) ? timeit(i) : -1.0;
   if (ms[7] > 0) ms[7] /= c->graph_iters;   // the graph holds graph_iters iterations
   if (!gR) ms[7] = -1.0;
   cudaEventDestroy(e0);

@@ -436,8 +436,10 @@ __global__ void __launch_bounds__(VB) k_compliance(Dims d, const double2* __rest
 }
 
 inline int vec_blocks(const Dims& d) {
+  // about one node per thread: every thread's loads are in flight at once (a grid-stride loop
+  // over a 592-CTA grid chains ~4 dependent round trips per thread at configs[1] size)
   int b = (d.nn + VB - 1) / VB;
-  return b < 592 ? b : 592;  // 148 SMs x 4
+  return b < 65535 ? b : 65535;
 }
 
 dim3 apply_grid(const Dims& d, int nr) {
