@@ -171,10 +171,13 @@ def run_ours(args, spec):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    strips = ws > 1 and args.mode == "strips"
+    # auto: strips when N > 1; "strips" forces the NCCL strip path even at N = 1 (a 1-rank
+    # communicator: exercises the multi-GPU code path on one GPU)
+    strips = (ws > 1 and args.mode == "auto") or args.mode == "strips"
     if strips:
         uid = [pkg.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if ws > 1:
+            dist.broadcast_object_list(uid, src=0)
         m = Msfem(pkg.problem_from_spec(spec), W.fixed_mask(spec), W.load_vector(spec), device=dev,
                   rank=rank, nranks=ws, transport=pkg.MSF_TRANSPORT_NCCL, handle=uid[0])
     else:
@@ -282,15 +285,15 @@ def run_ours(args, spec):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-        "scaling": "strong" if strips else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if strips and ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": spec.name, "n_dof": spec.n_dof, "grid": f"{spec.nelx}x{spec.nely}",
                    "realisations": spec.n_rhs, "coarse_cell": f"{spec.cx}x{spec.cy}",
                    "n_modes": spec.n_modes, "tile": f"{spec.tile_x}x{spec.tile_y}",
                    "tol": tol,
-                   "parallelism": ("single GPU" if ws == 1 else
-                                   f"{ws} strips (NCCL halo + all-reduce, replicated coarse solve)"
-                                   if strips else f"{ws} independent replicas"),
+                   "parallelism": (f"{ws} strips (NCCL halo + all-reduce, replicated coarse solve)"
+                                   if strips else "single GPU" if ws == 1
+                                   else f"{ws} independent replicas"),
                    "pcg_iters_per_step": iters_step, "n_agg_classes": inf["n_classes"],
                    "l2": f"inputs larger than L2: workspace {inf['workspace_bytes'] / 2**20:.0f} MiB > 126 MB"},
         "roofline": {"kernel": dom if dom != "sgs_colour" else "k_sgs_colour (one colour phase)",
@@ -323,8 +326,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", default="strips", choices=["strips", "replicas"],
-                    help="N > 1: strip partition of one problem (default) or independent replicas")
+    ap.add_argument("--mode", default="auto", choices=["auto", "strips", "replicas"],
+                    help="auto: strip partition when N > 1; strips: NCCL strip path even at N = 1; "
+                         "replicas: independent copies per rank")
     args = ap.parse_args()
     spec = W.CONFIGS[args.config]
     if args.impl == "reference":
