@@ -764,50 +764,76 @@ static int sens_outputs(msf_ctx* c, double* dF, double* dg, double* F, double* g
 // all-reduces of DESIGN.md §8(e) between the phases.
 using Ranks = std::vector<msf_ctx*>;
 
-static int dist_reduce(const Ranks& cs, int kind, int nr, bool gated, int rz_mode) {
+static int dist_reduce(const Ranks& cs, int kind, int rhs0, int nr, bool gated, int rz_mode) {
   int rc = dist_allreduce(cs, &msf_ctx::dsum, (size_t)kind * MSF_MAX_RHS, MSF_MAX_RHS);
   if (rc) return rc;
-  for (msf_ctx* c : cs) launch_finalize(c, kind, nr, gated, rz_mode);
+  for (msf_ctx* c : cs) launch_finalize(c, kind, rhs0, nr, gated, rz_mode);
   return MSF_OK;
 }
 
 // symmetric GS sweep, z halo exchanged after every colour phase.  first: 0 from z = 0,
 // 1 full sweep, 2 colour 0 already done (fused into the PCG update)
-static int dist_sgs(const Ranks& cs, int nr, int first, int rz_mode) {
+static int dist_sgs(const Ranks& cs, int rhs0, int nr, int first, int rz_mode) {
   int rc;
   for (int ph = first; ph <= 7; ph = (ph < 2 ? 2 : ph + 1)) {
-    for (msf_ctx* c : cs) launch_sgs_phase(c, 0, nr, c->r, c->z, true, ph, rz_mode);
-    if ((rc = dist_halo(cs, &msf_ctx::z, nr))) return rc;
+    for (msf_ctx* c : cs) launch_sgs_phase(c, rhs0, nr, c->r, c->z, true, ph, rz_mode);
+    if ((rc = dist_halo(cs, &msf_ctx::z, rhs0, nr))) return rc;
   }
-  if (rz_mode) return dist_reduce(cs, FIN_RZ, nr, true, rz_mode);
+  if (rz_mode) return dist_reduce(cs, FIN_RZ, rhs0, nr, true, rz_mode);
   return MSF_OK;
 }
 
-static int dist_vcycle(const Ranks& cs, int nr, bool f0_done, int rz_mode) {
+static int dist_vcycle(const Ranks& cs, int rhs0, int nr, bool f0_done, int rz_mode) {
   int rc;
-  if ((rc = dist_sgs(cs, nr, f0_done ? 2 : 0, 0))) return rc;
+  if ((rc = dist_sgs(cs, rhs0, nr, f0_done ? 2 : 0, 0))) return rc;
   for (msf_ctx* c : cs) {
-    launch_residual(c, 0, nr, c->r, c->z, c->t, true);
-    launch_restrict(c, 0, nr, c->t, true);     // partial R_c t over the owned nodes
+    launch_residual(c, rhs0, nr, c->r, c->z, c->t, true);
+    launch_restrict(c, rhs0, nr, c->t, true);     // partial R_c t over the owned nodes
   }
   const size_t nc = (size_t)cs[0]->d.nbc * cs[0]->d.mc;
-  if ((rc = dist_allreduce(cs, &msf_ctx::cb, 0, nr * nc))) return rc;
+  if ((rc = dist_allreduce(cs, &msf_ctx::cb, rhs0 * nc, nr * nc))) return rc;
   for (msf_ctx* c : cs) {
-    launch_coarse_solve(c, 0, nr, true);       // replicated
-    launch_prolong(c, 0, nr, c->z, true);      // owned + halo nodes
+    launch_coarse_solve(c, rhs0, nr, true);       // replicated
+    launch_prolong(c, rhs0, nr, c->z, true);      // owned + halo nodes
   }
-  return dist_sgs(cs, nr, 1, rz_mode);
+  return dist_sgs(cs, rhs0, nr, 1, rz_mode);
 }
 
-static int dist_iteration(const Ranks& cs, int nr) {
+static int dist_iteration(const Ranks& cs, int rhs0, int nr) {
   int rc;
-  for (msf_ctx* c : cs) launch_matvec(c, 0, nr, c->pv, c->q, true, true);
-  if ((rc = dist_reduce(cs, FIN_PQ, nr, true, 0))) return rc;
-  for (msf_ctx* c : cs) launch_update_f0(c, 0, nr);
-  if ((rc = dist_reduce(cs, FIN_RR, nr, true, 0))) return rc;
-  if ((rc = dist_halo(cs, &msf_ctx::z, nr))) return rc;
-  if ((rc = dist_vcycle(cs, nr, true, 2))) return rc;
-  for (msf_ctx* c : cs) launch_pcg_p(c, 0, nr, false);
+  for (msf_ctx* c : cs) launch_matvec(c, rhs0, nr, c->pv, c->q, true, true);
+  if ((rc = dist_reduce(cs, FIN_PQ, rhs0, nr, true, 0))) return rc;
+  for (msf_ctx* c : cs) launch_update_f0(c, rhs0, nr);
+  if ((rc = dist_reduce(cs, FIN_RR, rhs0, nr, true, 0))) return rc;
+  if ((rc = dist_halo(cs, &msf_ctx::z, rhs0, nr))) return rc;
+  if ((rc = dist_vcycle(cs, rhs0, nr, true, 2))) return rc;
+  for (msf_ctx* c : cs) launch_pcg_p(c, rhs0, nr, false);
+  return MSF_OK;
+}
+
+// graph of one strip-partition iteration for realisations [rhs0, rhs0 + nr) (kernels + NCCL)
+static int dist_range_graph(const Ranks& cs, int rhs0, int nr, cudaGraphExec_t* out) {
+  msf_ctx* c = cs[0];
+  cudaGraphExec_t& slot = c->range_graph[rhs0][nr];
+  if (!slot) {
+    cudaGraph_t g;
+    cudaStream_t user = c->stream;
+    c->stream = c->cap_stream;
+    cudaError_t e1 = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+    const long long before = c->launches;
+    int rc_it = MSF_OK;
+    if (e1 == cudaSuccess) rc_it = dist_iteration(cs, rhs0, nr);
+    c->pcg_launches = c->launches - before;
+    c->launches = before;
+    cudaError_t e2 = e1 == cudaSuccess ? cudaStreamEndCapture(c->stream, &g) : e1;
+    c->stream = user;
+    if (rc_it) return rc_it;
+    CK(e1);
+    CK(e2);
+    CK(cudaGraphInstantiate(&slot, g, 0));
+    cudaGraphDestroy(g);
+  }
+  *out = slot;
   return MSF_OK;
 }
 
@@ -823,52 +849,38 @@ static int dist_pcg_solve(const Ranks& cs, int nr, double tol, int max_it, int32
   if (!(tol > 0.0) || max_it < 1) return msf_fail(c, MSF_ERR_ARG, "need tol > 0, max_it >= 1");
   int rc;
   for (msf_ctx* x : cs) launch_pcg_init(x, nr, tol, max_it);
-  if ((rc = dist_reduce(cs, FIN_F, nr, false, 0))) return rc;
-  if ((rc = dist_vcycle(cs, nr, false, 1))) return rc;
+  if ((rc = dist_reduce(cs, FIN_F, 0, nr, false, 0))) return rc;
+  if ((rc = dist_vcycle(cs, 0, nr, false, 1))) return rc;
   for (msf_ctx* x : cs) launch_pcg_p(x, 0, nr, true);
   CKL("dist pcg init");
-  // one process per GPU: the iteration (kernels + NCCL) is captured once as a CUDA graph
+  // one process per GPU: each active range's iteration (kernels + NCCL) is a CUDA graph; the
+  // active flags derive from all-reduced sums, so every rank narrows the range identically
   const bool graph = cs.size() == 1;
-  if (graph && (!c->iter_graph || c->iter_graph_R != nr)) {
-    if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
-    c->iter_graph = nullptr;
-    cudaGraph_t g;
-    cudaStream_t user = c->stream;
-    c->stream = c->cap_stream;
-    cudaError_t e1 = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
-    const long long before = c->launches;
-    int rc_it = MSF_OK;
-    if (e1 == cudaSuccess) rc_it = dist_iteration(cs, nr);
-    c->pcg_launches = c->launches - before;
-    c->launches = before;
-    cudaError_t e2 = e1 == cudaSuccess ? cudaStreamEndCapture(c->stream, &g) : e1;
-    c->stream = user;
-    if (rc_it) return rc_it;
-    CK(e1);
-    CK(e2);
-    CK(cudaGraphInstantiate(&c->iter_graph, g, 0));
-    cudaGraphDestroy(g);
-    c->iter_graph_R = nr;
-  }
   const int check_every = 8;
-  bool done = false;
-  for (int it = 0; it < max_it + check_every && !done; it += check_every) {
+  int lo = 0, hi = nr;
+  for (int it = 0; it < max_it + check_every; it += check_every) {
+    cudaGraphExec_t g = nullptr;
+    if (graph && (rc = dist_range_graph(cs, lo, hi - lo, &g))) return rc;
     for (int j = 0; j < check_every; ++j) {
       if (graph) {
-        CK(cudaGraphLaunch(c->iter_graph, c->stream));
+        CK(cudaGraphLaunch(g, c->stream));
         c->launches += c->pcg_launches;
-      } else if ((rc = dist_iteration(cs, nr))) {
+      } else if ((rc = dist_iteration(cs, lo, hi - lo))) {
         return rc;
       }
     }
-    // the flags derive from all-reduced sums: identical on every rank
     if ((rc = read_scalars(c, nr))) return rc;
-    done = true;
+    lo = nr;
+    hi = -1;
     for (int k = 0; k < nr; ++k)
-      if (c->sc_host[k].active) done = false;
+      if (c->sc_host[k].active) {
+        lo = std::min(lo, k);
+        hi = std::max(hi, k + 1);
+      }
+    if (hi < 0) break;
   }
   for (msf_ctx* x : cs) launch_compliance(x, nr);
-  if ((rc = dist_reduce(cs, FIN_COMP, nr, false, 0))) return rc;
+  if ((rc = dist_reduce(cs, FIN_COMP, 0, nr, false, 0))) return rc;
   int noconv = 0;
   for (msf_ctx* x : cs) {
     if ((rc = read_scalars(x, nr))) return rc;
@@ -890,7 +902,7 @@ static int dist_sensitivities(const Ranks& cs, double kappa, double volfrac) {
     if (!x || !x->have_solution) return msf_fail(c, MSF_ERR_STATE, "sensitivities before pcg_solve");
   int rc;
   for (msf_ctx* x : cs) launch_sens_local(x);
-  if ((rc = dist_reduce(cs, FIN_COMP, c->d.R, false, 0))) return rc;
+  if ((rc = dist_reduce(cs, FIN_COMP, 0, c->d.R, false, 0))) return rc;
   if ((rc = dist_allreduce(cs, &msf_ctx::tile_tmp, 0, (size_t)c->d.R * c->d.nt))) return rc;
   for (msf_ctx* x : cs) launch_sens_global(x, kappa, volfrac);
   CKL("dist sensitivities");

@@ -189,9 +189,9 @@ int dist_allreduce(const std::vector<msf_ctx*>& cs, double* msf_ctx::*buf, size_
   return msf_cuda_check(c0, cudaGetLastError(), "group all-reduce");
 }
 
-// halo exchange of the node vector ctx->*vec for realisations [0, nr): every rank sends its
+// halo exchange of the node vector ctx->*vec for realisations [rhs0, rhs0 + nr): every rank sends its
 // first / last owned node column to the left / right neighbour's halo column
-int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int nr) {
+int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int rhs0, int nr) {
   msf_ctx* c0 = cs[0];
   if (c0->comm->kind == MSF_TRANSPORT_NCCL) {
     NcclApi& A = nccl();
@@ -201,7 +201,7 @@ int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int nr) {
     ncclComm_t comm = (ncclComm_t)c->comm->nccl;
     int rc = nccl_check(c, A.GroupStart(), "ncclGroupStart");
     if (rc) return rc;
-    for (int k = 0; k < nr; ++k) {
+    for (int k = rhs0; k < rhs0 + nr; ++k) {
       double* v = c->*vec + (size_t)k * 2 * d.nn;
       if (c->rank > 0) {
         A.Send(v + (size_t)d.own_lo * col, col, ncclDouble, c->rank - 1, comm, c->stream);
@@ -219,8 +219,8 @@ int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int nr) {
     msf_ctx* b = cs[r + 1];
     const size_t colb = (size_t)2 * a->dl.nny * sizeof(double);
     const size_t pa = (size_t)2 * a->dl.nn * sizeof(double), pb = (size_t)2 * b->dl.nn * sizeof(double);
-    char* va = (char*)(a->*vec);
-    char* vb = (char*)(b->*vec);
+    char* va = (char*)(a->*vec) + (size_t)rhs0 * pa;
+    char* vb = (char*)(b->*vec) + (size_t)rhs0 * pb;
     // a's last owned column -> b's left halo ; b's first owned column -> a's right halo
     cudaError_t e = cudaMemcpy2DAsync(vb + (size_t)(b->dl.own_lo - 1) * colb, pb,
                                       va + (size_t)(a->dl.own_hi - 1) * colb, pa, colb, nr,

@@ -378,12 +378,12 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
 
 // PCG scalar update from the all-reduced sums (strip partition): same arithmetic as the
 // in-kernel finalisation of the single-GPU path.
-__global__ void k_finalize(PcgScalars* sc, const double* __restrict__ dsum, int kind, int nr,
-                           int gated, int rz_mode) {
+__global__ void k_finalize(PcgScalars* sc, const double* __restrict__ dsum, int kind, int rhs0,
+                           int nr, int gated, int rz_mode) {
   pdl_launch();
   pdl_wait();
-  const int rhs = threadIdx.x;
-  if (rhs >= nr) return;
+  const int rhs = rhs0 + threadIdx.x;
+  if (threadIdx.x >= nr) return;
   if (gated && !sc[rhs].active) return;
   fin_scalar(sc[rhs], kind, dsum[kind * MSF_MAX_RHS + rhs], rz_mode);
 }
@@ -577,9 +577,9 @@ void launch_update_f0(msf_ctx* c, int rhs0, int nr) {
   MSF_LAUNCHED(c);
 }
 
-void launch_finalize(msf_ctx* c, int kind, int nr, bool gated, int rz_mode) {
-  launch_k(k_finalize, dim3(1), dim3(32), 0, c->stream, c->sc, (const double*)c->dsum, kind, nr,
-           gated ? 1 : 0, rz_mode);
+void launch_finalize(msf_ctx* c, int kind, int rhs0, int nr, bool gated, int rz_mode) {
+  launch_k(k_finalize, dim3(1), dim3(32), 0, c->stream, c->sc, (const double*)c->dsum, kind, rhs0,
+           nr, gated ? 1 : 0, rz_mode);
   MSF_LAUNCHED(c);
 }
 

@@ -114,7 +114,7 @@ int dist_comm_create(msf_ctx* c, int transport, void* handle);
 void dist_comm_destroy(msf_ctx* c);
 int dist_allreduce(const std::vector<msf_ctx*>& cs, double* msf_ctx::*buf, size_t off,
                    size_t count);
-int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int nr);
+int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int rhs0, int nr);
 std::vector<msf_ctx*> group_ranks(msf_group* g);
 
 struct msf_comm {
@@ -281,7 +281,7 @@ void launch_sgs_sweep(msf_ctx* c, int rhs0, int nr, const double* r, double* z, 
 void launch_sgs_phase(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
                       int phase, int rz_mode);
 // PCG scalar update from the all-reduced dsum[kind] (strip partition)
-void launch_finalize(msf_ctx* c, int kind, int nr, bool gated, int rz_mode);
+void launch_finalize(msf_ctx* c, int kind, int rhs0, int nr, bool gated, int rz_mode);
 // fused u/r update + ||r||^2 + zero-start forward GS colour 0 (PCG iteration)
 void launch_update_f0(msf_ctx* c, int rhs0, int nr);
 void launch_mask_copy(msf_ctx* c, const double* x, double* y, int n2nn);
