@@ -1,0 +1,59 @@
+"""GPU parity on degenerate and boundary configurations of the hot path (same bars as
+tests/test_gpu_parity.py): a single coarse cell (one agglomerate row / column, K_c of two
+blocks), one mode per agglomerate, the maximum of MSF_MAX_RHS = 4 realisations, odd coarse
+cells with a ragged design tile, a homogeneous solid design (E = E0 everywhere), and the
+lambda_Omega threshold at 16 modes."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import problem
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+
+from paper_1411_3923_b200 import Msfem, build  # noqa: E402
+from test_gpu_parity import compliance_tol, dev, host, rel  # noqa: E402
+
+build.build()
+DEV = torch.device("cuda")
+
+EDGE = {
+    "one_coarse_cell_8x8": W.small_spec(nelx=8, nely=8, cx=8, cy=8, seed=51),
+    "one_mode_24x12": W.small_spec(nelx=24, nely=12, cx=4, cy=4, n_modes=1, bc="mbb", seed=52),
+    "four_realisations_24x16": W.small_spec(nelx=24, nely=16, cx=8, cy=8, tile=(8, 8), rmin=2.0,
+                                            beta=6.0, etas=(0.75, 0.6, 0.45, 0.3), dilated=3,
+                                            seed=53, Emin=1e-6),
+    "odd_cells_ragged_tile_30x21": W.small_spec(nelx=30, nely=21, cx=5, cy=7, tile=(10, 7), rmin=1.5,
+                                                beta=4.0, etas=(0.5,), seed=54, n_modes=3),
+    "solid_16x8": W.small_spec(nelx=16, nely=8, cx=4, cy=4, design="solid", seed=55),
+    "threshold_16_modes_32x16": W.small_spec(nelx=32, nely=16, cx=8, cy=8, n_modes=16, seed=56,
+                                             lam_threshold=5e-3, Emin=1e-6),
+}
+
+
+@pytest.mark.parametrize("name", list(EDGE))
+def test_edge_pcg_parity(name):
+    spec = EDGE[name]
+    x = W.design_tile(spec)
+    fx, f = W.fixed_mask(spec), W.load_vector(spec)
+    m = Msfem.from_spec(spec)
+    m.filter_project(dev(x))
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    ref = problem.solve(spec, x, fx, f, tol=1e-8)
+    its, comps, noconv = m.pcg_solve(tol=1e-8)
+    assert not noconv
+    for k in range(spec.n_rhs):
+        assert abs(its[k] - ref["iters"][k]) <= 1, (its, ref["iters"])
+    ref = problem.solve(spec, x, fx, f, tol=1e-12)
+    u = torch.empty(spec.n_rhs * spec.n_dof, dtype=torch.float64, device=DEV)
+    its, comps, noconv = m.pcg_solve(tol=1e-12, u=u)
+    ug = host(u).reshape(spec.n_rhs, spec.n_dof)
+    for k in range(spec.n_rhs):
+        assert rel(ug[k], ref["us"][k]) <= 1e-8, k
+        tc = compliance_tol(spec, ref["E_el"][k], f, fx)
+        assert abs(comps[k] - ref["comps"][k]) <= tc * abs(ref["comps"][k]), (k, tc)

@@ -107,6 +107,8 @@ def design_tile(spec: ProblemSpec, seed: int | None = None) -> np.ndarray:
         return rng.uniform(0.0, 1.0, size=n)
     if spec.design == "binary":
         return _connected_binary_cell(spec.tile_x, spec.tile_y, spec.solid_fraction, rng)
+    if spec.design == "solid":   # homogeneous material (edge case: no contrast at all)
+        return np.ones(n)
     raise ValueError(f"unknown design {spec.design!r}")
 
 
