@@ -319,17 +319,21 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
   const int qy = blockIdx.x * blockDim.x + threadIdx.x;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const size_t off = (size_t)rhs * d.nn;
-  // the quad's p, q, u, r are loaded before alpha is known
-  double2 pv[4], qv[4], uv[4], rv[4];
+#ifndef MSF_F0_PRELOAD
+#define MSF_F0_PRELOAD 0
+#endif
+  // MSF_F0_PRELOAD 1: the quad's p and q are loaded before alpha is known (overlaps the
+  // partial reduction); 0: alpha first (fewer live registers)
+  double2 pv[4], qv[4];
+  if (MSF_F0_PRELOAD) {
 #pragma unroll
-  for (int dn = 0; dn < 4; ++dn) {
-    const int gx = 2 * qx + (dn & 1), gy = 2 * qy + (dn >> 1);
-    if (gx < d.nnx && gy < d.nny) {
-      const size_t n = off + (size_t)gx * d.nny + gy;
-      pv[dn] = pall[n];
-      qv[dn] = qall[n];
-      uv[dn] = uall[n];
-      rv[dn] = rall[n];
+    for (int dn = 0; dn < 4; ++dn) {
+      const int gx = 2 * qx + (dn & 1), gy = 2 * qy + (dn >> 1);
+      if (gx < d.nnx && gy < d.nny) {
+        const size_t n = off + (size_t)gx * d.nny + gy;
+        pv[dn] = pall[n];
+        qv[dn] = qall[n];
+      }
     }
   }
   double alpha;
@@ -351,11 +355,13 @@ __global__ void __launch_bounds__(NTHR) k_update_f0(Dims d, K0Mat K, const doubl
     const int gx = 2 * qx + (dn & 1), gy = 2 * qy + (dn >> 1);
     if (gx < d.nnx && gy < d.nny) {
       const size_t n = off + (size_t)gx * d.nny + gy;
-      double2 u2 = uv[dn], r2 = rv[dn];
-      u2.x = fma(alpha, pv[dn].x, u2.x);
-      u2.y = fma(alpha, pv[dn].y, u2.y);
-      r2.x = fma(-alpha, qv[dn].x, r2.x);
-      r2.y = fma(-alpha, qv[dn].y, r2.y);
+      const double2 p2 = MSF_F0_PRELOAD ? pv[dn] : pall[n];
+      const double2 q2 = MSF_F0_PRELOAD ? qv[dn] : qall[n];
+      double2 u2 = uall[n], r2 = rall[n];
+      u2.x = fma(alpha, p2.x, u2.x);
+      u2.y = fma(alpha, p2.y, u2.y);
+      r2.x = fma(-alpha, q2.x, r2.x);
+      r2.y = fma(-alpha, q2.y, r2.y);
       uall[n] = u2;
       rall[n] = r2;
       s += r2.x * r2.x + r2.y * r2.y;
