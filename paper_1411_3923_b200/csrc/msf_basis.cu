@@ -245,18 +245,46 @@ __device__ void small_gen_eig(double* G, double* H, int mb, double* theta, doubl
   __syncwarp();
 }
 
+// Thread-block cluster per class: EIG_CL CTAs share the per-iteration work of one class
+// (8x the threads of a single CTA on these latency-bound loops); phases are separated by
+// cluster barriers (release / acquire: global writes of one CTA are visible to the others).
+constexpr int EIG_CL = 8;
+
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// s = sum_k A[k*sa] B[k*sb], 4 independent accumulators
+__device__ __forceinline__ double dot4(const double* A, int sa, const double* B, int sb, int n) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int k = 0;
+  for (; k + 3 < n; k += 4) {
+    s0 = fma(A[(size_t)k * sa], B[(size_t)k * sb], s0);
+    s1 = fma(A[(size_t)(k + 1) * sa], B[(size_t)(k + 1) * sb], s1);
+    s2 = fma(A[(size_t)(k + 2) * sa], B[(size_t)(k + 2) * sb], s2);
+    s3 = fma(A[(size_t)(k + 3) * sa], B[(size_t)(k + 3) * sb], s3);
+  }
+  for (; k < n; ++k) s0 = fma(A[(size_t)k * sa], B[(size_t)k * sb], s0);
+  return (s0 + s1) + (s2 + s3);
+}
+
 __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __restrict__ E,
                                               const uint8_t* __restrict__ fixn,
                                               EigClass* classes, double* work, double* phi,
                                               double* lam, EigArgs ea, int* status) {
   extern __shared__ double sm[];
-  EigClass C = classes[blockIdx.x];
+  const int cls = blockIdx.x / EIG_CL, rank = blockIdx.x - cls * EIG_CL;
+  const int t0 = rank * NT + threadIdx.x, tstride = EIG_CL * NT;   // cluster-wide thread index
+  EigClass C = classes[cls];
   const int ml = 2 * C.nby, nbl = C.nbx, n = nbl * ml;
   const int mb = ea.mb;
   const int sz = ml * max(ml, mb);
   double* S = sm;                 // [sz]
   double* T = S + sz;             // [sz]
-  double* G = T + sz;             // [mb*mb]
+  double* Pv = T + sz;            // [sz] previous block inverse
+  double* Wv = Pv + sz;           // [sz] current W block
+  double* G = Wv + sz;            // [mb*mb]
   double* H = G + mb * mb;
   double* Cm = H + mb * mb;
   double* Lw = Cm + mb * mb;
@@ -265,8 +293,6 @@ __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __r
   double* theta = Vw + mb * mb;   // [mb]
   double* rowk = theta + 32;      // [ml]
   double* colk = rowk + ea.mlmax; // [ml]
-  double* red = colk + ea.mlmax;  // [NT/32 * 32]
-  __shared__ int s_stop;
 
   double* Sinv = work + C.off;
   double* W = Sinv + (size_t)nbl * ml * ml;
@@ -274,168 +300,202 @@ __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __r
   double* Y = X + (size_t)n * mb;
   double* KY = Y + (size_t)n * mb;
   double* Dv = KY + (size_t)n * mb;
+  double* gG = Dv + n;                 // [mb*mb] cluster-shared scratch (global)
+  double* gH = gG + mb * mb;           // [mb*mb]
+  double* gC = gH + mb * mb;           // [mb*mb] Ritz coefficients
+  double* gT = gC + mb * mb;           // [32]   Ritz values
+  double* gR = gT + 32;                // [EIG_CL * 16] residual partials
 
-  // ---------------- factorisation A = K - sigma D by block Thomas
-  for (int I = 0; I < nbl; ++I) {
-    assemble_block(d, K, E, fixn, C, I, I, ea.sigma, S, ml);
-    if (I > 0) {
-      assemble_block(d, K, E, fixn, C, I - 1, I, ea.sigma, T, ml);   // U_{I-1}
-      __syncthreads();
-      const double* Sp = Sinv + (size_t)(I - 1) * ml * ml;
-      double* WI = W + (size_t)I * ml * ml;
-      for (int e = threadIdx.x; e < ml * ml; e += NT) {
-        const int r = e / ml, cc = e - (e / ml) * ml;
-        double s = 0.0;
-        for (int k = 0; k < ml; ++k) s = fma(Sp[r * ml + k], T[k * ml + cc], s);
-        WI[e] = s;
+  // ---------------- factorisation A = K - sigma D by block Thomas (CTA 0, shared memory)
+  if (rank == 0) {
+    for (int I = 0; I < nbl; ++I) {
+      assemble_block(d, K, E, fixn, C, I, I, ea.sigma, S, ml);
+      if (I > 0) {
+        assemble_block(d, K, E, fixn, C, I - 1, I, ea.sigma, T, ml);   // U_{I-1}
+        __syncthreads();
+        double* WI = W + (size_t)I * ml * ml;
+        for (int e = threadIdx.x; e < ml * ml; e += NT) {            // W_I = Sinv_{I-1} U_{I-1}
+          const int r = e / ml, cc = e - (e / ml) * ml;
+          const double v = dot4(Pv + r * ml, 1, T + cc, ml, ml);
+          Wv[e] = v;
+          WI[e] = v;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < ml * ml; e += NT) {            // S -= U^T W
+          const int r = e / ml, cc = e - (e / ml) * ml;
+          S[e] -= dot4(T + r, ml, Wv + cc, ml, ml);
+        }
       }
       __syncthreads();
+      cta_inverse(S, ml, rowk, colk, status);
+      double* SI = Sinv + (size_t)I * ml * ml;
       for (int e = threadIdx.x; e < ml * ml; e += NT) {
-        const int r = e / ml, cc = e - (e / ml) * ml;
-        double s = 0.0;
-        for (int k = 0; k < ml; ++k) s = fma(T[k * ml + r], WI[k * ml + cc], s);
-        S[e] -= s;
+        SI[e] = S[e];
+        Pv[e] = S[e];
       }
+      __syncthreads();
     }
-    __syncthreads();
-    cta_inverse(S, ml, rowk, colk, status);
-    double* SI = Sinv + (size_t)I * ml * ml;
-    for (int e = threadIdx.x; e < ml * ml; e += NT) SI[e] = S[e];
-    __syncthreads();
   }
   // ---------------- D = diag(K) on free DOFs, random start
-  for (int i = threadIdx.x; i < n; i += NT) {
+  for (int i = t0; i < n; i += tstride) {
     const int lx = i / ml, rr = i - (i / ml) * ml, ly = rr >> 1, c = rr & 1;
     Dv[i] = dof_fixed(d, fixn, C, lx, ly, c) ? 0.0 : box_K(d, K, E, C, lx, ly, c, lx, ly, c);
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < n * mb; e += NT) {
+  cl_sync();
+  for (int e = t0; e < n * mb; e += tstride) {
     const int i = e / mb;
     X[e] = (Dv[i] > 0.0) ? hash_uniform((unsigned long long)e * 2654435761ull + 17ull) : 0.0;
   }
-  __syncthreads();
+  cl_sync();
 
+  // Three n x mb buffers rotate through an iteration: B0 = X, B1 = D X -> forward-eliminated
+  // right-hand side -> K Y, B2 = block-diagonal solve -> Y -> K X.
+  double* B0 = X;
+  double* B1 = Y;
+  double* B2 = KY;
+  const int nby = C.nby;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = rank * (NT / 32) + (threadIdx.x >> 5), nwarps = EIG_CL * (NT / 32);
   int it = 0;
   for (; it < ea.maxit; ++it) {
-    // Y = D X
-    for (int e = threadIdx.x; e < n * mb; e += NT) Y[e] = Dv[e / mb] * X[e];
-    __syncthreads();
-    // forward: Y_I -= W_I^T Y_{I-1}
+    for (int e = t0; e < n * mb; e += tstride) B1[e] = Dv[e / mb] * B0[e];
+    cl_sync();
+    // forward: B1_I -= W_I^T B1_{I-1}  (sequential over the node columns)
     for (int I = 1; I < nbl; ++I) {
       const double* WI = W + (size_t)I * ml * ml;
-      const double* Yp = Y + (size_t)(I - 1) * ml * mb;
-      double* Yc = Y + (size_t)I * ml * mb;
-      for (int e = threadIdx.x; e < ml * mb; e += NT) {
+      const double* Yp = B1 + (size_t)(I - 1) * ml * mb;
+      double* Yc = B1 + (size_t)I * ml * mb;
+      for (int e = t0; e < ml * mb; e += tstride) {
         const int r = e / mb, j = e - (e / mb) * mb;
-        double s = 0.0;
-        for (int k = 0; k < ml; ++k) s = fma(WI[k * ml + r], Yp[k * mb + j], s);
-        Yc[e] -= s;
+        Yc[e] -= dot4(WI + r, ml, Yp + j, mb, ml);
       }
-      __syncthreads();
+      cl_sync();
     }
-    // Y_I = Sinv_I Y_I
-    for (int I = 0; I < nbl; ++I) {
-      double* Yc = Y + (size_t)I * ml * mb;
-      for (int e = threadIdx.x; e < ml * mb; e += NT) T[e] = Yc[e];
-      __syncthreads();
-      const double* SI = Sinv + (size_t)I * ml * ml;
-      for (int e = threadIdx.x; e < ml * mb; e += NT) {
-        const int r = e / mb, j = e - (e / mb) * mb;
-        double s = 0.0;
-        for (int k = 0; k < ml; ++k) s = fma(SI[r * ml + k], T[k * mb + j], s);
-        Yc[e] = s;
-      }
-      __syncthreads();
+    // B2_I = Sinv_I B1_I for all node columns at once (independent blocks)
+    for (int e = t0; e < n * mb; e += tstride) {
+      const int i = e / mb, j = e - (e / mb) * mb;
+      const int I = i / ml, r = i - I * ml;
+      B2[e] = dot4(Sinv + (size_t)I * ml * ml + (size_t)r * ml, 1, B1 + (size_t)I * ml * mb + j, mb, ml);
     }
-    // back: Y_I -= W_{I+1} Y_{I+1}
+    cl_sync();
+    // back: B2_I -= W_{I+1} B2_{I+1}
     for (int I = nbl - 2; I >= 0; --I) {
       const double* WI = W + (size_t)(I + 1) * ml * ml;
-      const double* Yn = Y + (size_t)(I + 1) * ml * mb;
-      double* Yc = Y + (size_t)I * ml * mb;
-      for (int e = threadIdx.x; e < ml * mb; e += NT) {
+      const double* Yn = B2 + (size_t)(I + 1) * ml * mb;
+      double* Yc = B2 + (size_t)I * ml * mb;
+      for (int e = t0; e < ml * mb; e += tstride) {
         const int r = e / mb, j = e - (e / mb) * mb;
+        Yc[e] -= dot4(WI + (size_t)r * ml, 1, Yn + j, mb, ml);
+      }
+      cl_sync();
+    }
+    // B1 = K B2: unshifted Neumann box stiffness element by element, fixed rows -> 0
+    for (int e = t0; e < (n / 2) * mb; e += tstride) {
+      const int node = e / mb, j = e - (e / mb) * mb;
+      const int lx = node / nby, ly = node - (node / nby) * nby;
+      double ox = 0.0, oy = 0.0;
+#pragma unroll
+      for (int sx = 0; sx < 2; ++sx)
+#pragma unroll
+        for (int sy = 0; sy < 2; ++sy) {
+          const int ex = lx - 1 + sx, ey = ly - 1 + sy;
+          if (ex < 0 || ex > nbl - 2 || ey < 0 || ey > nby - 2) continue;
+          const double Ee = E[(size_t)(C.bx0 + ex) * d.nely + (C.by0 + ey)];
+          const int a = local_a(lx - ex, ly - ey);
+          double ax = 0.0, ay = 0.0;
+#pragma unroll
+          for (int bnode = 0; bnode < 4; ++bnode) {
+            const int nx = ex + ((bnode == 1 || bnode == 2) ? 1 : 0), ny = ey + (bnode >= 2 ? 1 : 0);
+            const size_t i2 = (size_t)nx * ml + 2 * ny;
+            const double yx = B2[i2 * mb + j], yy = B2[(i2 + 1) * mb + j];
+            ax = fma(K.v[(2 * a) * 8 + 2 * bnode], yx, fma(K.v[(2 * a) * 8 + 2 * bnode + 1], yy, ax));
+            ay = fma(K.v[(2 * a + 1) * 8 + 2 * bnode], yx, fma(K.v[(2 * a + 1) * 8 + 2 * bnode + 1], yy, ay));
+          }
+          ox = fma(Ee, ax, ox);
+          oy = fma(Ee, ay, oy);
+        }
+      const size_t i0 = (size_t)lx * ml + 2 * ly;
+      B1[i0 * mb + j] = Dv[i0] > 0.0 ? ox : 0.0;
+      B1[(i0 + 1) * mb + j] = Dv[i0 + 1] > 0.0 ? oy : 0.0;
+    }
+    cl_sync();
+    // G = Y^T K Y, H = Y^T D Y (symmetric: upper triangles), one warp of the cluster per
+    // entry, lanes over the DOFs (fixed order within the warp)
+    {
+      const int ntri = mb * (mb + 1) / 2;
+      for (int t = gwarp; t < 2 * ntri; t += nwarps) {
+        const int which = t / ntri;
+        int tt = t - which * ntri, a2 = 0;
+        while (tt >= mb - a2) {
+          tt -= mb - a2;
+          ++a2;
+        }
+        const int b2 = a2 + tt;
         double s = 0.0;
-        for (int k = 0; k < ml; ++k) s = fma(WI[r * ml + k], Yn[k * mb + j], s);
-        Yc[e] -= s;
+        if (which == 0)
+          for (int i = lane; i < n; i += 32) s = fma(B2[(size_t)i * mb + a2], B1[(size_t)i * mb + b2], s);
+        else
+          for (int i = lane; i < n; i += 32) s = fma(B2[(size_t)i * mb + a2] * Dv[i], B2[(size_t)i * mb + b2], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+          double* Mt = which == 0 ? gG : gH;
+          Mt[a2 * mb + b2] = s;
+          Mt[b2 * mb + a2] = s;
+        }
+      }
+    }
+    cl_sync();
+    if (rank == 0) {
+      for (int e = threadIdx.x; e < mb * mb; e += NT) {
+        G[e] = __ldcg(gG + e);
+        H[e] = __ldcg(gH + e);
       }
       __syncthreads();
+      if (threadIdx.x < 32) small_gen_eig(G, H, mb, theta, Cm, Lw, Mw, Vw, status);
+      __syncthreads();
+      for (int e = threadIdx.x; e < mb * mb; e += NT) gC[e] = Cm[e];
+      for (int e = threadIdx.x; e < mb; e += NT) gT[e] = theta[e];
     }
-    // KY = K Y (unshifted Neumann box stiffness, fixed rows -> 0)
-    for (int e = threadIdx.x; e < n * mb; e += NT) {
+    cl_sync();
+    // X = Y Cm ; then K X = (K Y) Cm into B2
+    for (int e = t0; e < n * mb; e += tstride) {
       const int i = e / mb, j = e - (e / mb) * mb;
-      double s = 0.0;
-      if (Dv[i] > 0.0) {
-        const int lx = i / ml, rr = i - (i / ml) * ml, ly = rr >> 1, c = rr & 1;
-        for (int lx2 = max(lx - 1, 0); lx2 <= min(lx + 1, nbl - 1); ++lx2)
-          for (int ly2 = max(ly - 1, 0); ly2 <= min(ly + 1, C.nby - 1); ++ly2)
-            for (int c2 = 0; c2 < 2; ++c2) {
-              const int i2 = lx2 * ml + 2 * ly2 + c2;
-              if (Dv[i2] > 0.0)
-                s = fma(box_K(d, K, E, C, lx, ly, c, lx2, ly2, c2), Y[(size_t)i2 * mb + j], s);
-            }
-      }
-      KY[e] = s;
+      B0[e] = dot4(B2 + (size_t)i * mb, 1, gC + j, mb, mb);
     }
-    __syncthreads();
-    // G = Y^T KY, H = Y^T D Y
-    for (int e = threadIdx.x; e < 2 * mb * mb; e += NT) {
-      const int which = e / (mb * mb), ee = e - which * mb * mb;
-      const int a = ee / mb, b = ee - (ee / mb) * mb;
-      double s = 0.0;
-      if (which == 0)
-        for (int i = 0; i < n; ++i) s = fma(Y[(size_t)i * mb + a], KY[(size_t)i * mb + b], s);
-      else
-        for (int i = 0; i < n; ++i) s = fma(Y[(size_t)i * mb + a] * Dv[i], Y[(size_t)i * mb + b], s);
-      (which == 0 ? G : H)[ee] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) small_gen_eig(G, H, mb, theta, Cm, Lw, Mw, Vw, status);
-    __syncthreads();
-    // X = Y Cm ; then KX = KY Cm into Y
-    for (int e = threadIdx.x; e < n * mb; e += NT) {
+    cl_sync();
+    for (int e = t0; e < n * mb; e += tstride) {
       const int i = e / mb, j = e - (e / mb) * mb;
-      double s = 0.0;
-      for (int l = 0; l < mb; ++l) s = fma(Y[(size_t)i * mb + l], Cm[l * mb + j], s);
-      X[e] = s;
+      B2[e] = dot4(B1 + (size_t)i * mb, 1, gC + j, mb, mb);
     }
-    __syncthreads();
-    for (int e = threadIdx.x; e < n * mb; e += NT) {
-      const int i = e / mb, j = e - (e / mb) * mb;
-      double s = 0.0;
-      for (int l = 0; l < mb; ++l) s = fma(KY[(size_t)i * mb + l], Cm[l * mb + j], s);
-      Y[e] = s;
-    }
-    __syncthreads();
-    // residuals of the kept pairs
+    cl_sync();
+    // residuals of the kept pairs: one warp of the cluster per pair, lanes over the DOFs
     const int kk = min(d.kmax, mb);
-    for (int j = 0; j < kk; ++j) {
+    for (int j = gwarp; j < kk; j += nwarps) {
+      const double th = __ldcg(gT + j);
       double s = 0.0;
-      for (int i = threadIdx.x; i < n; i += NT) {
+      for (int i = lane; i < n; i += 32) {
         if (Dv[i] > 0.0) {
-          const double rv = Y[(size_t)i * mb + j] - theta[j] * Dv[i] * X[(size_t)i * mb + j];
+          const double rv = B2[(size_t)i * mb + j] - th * Dv[i] * B0[(size_t)i * mb + j];
           s += rv * rv / Dv[i];
         }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if ((threadIdx.x & 31) == 0) red[j * (NT / 32) + (threadIdx.x >> 5)] = s;
+      if (lane == 0) gR[j] = s;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double mx = 0.0;
-      for (int j = 0; j < kk; ++j) {
-        double s = 0.0;
-        for (int w = 0; w < NT / 32; ++w) s += red[j * (NT / 32) + w];
-        mx = fmax(mx, s);
-      }
-      s_stop = (sqrt(mx) <= ea.tol) ? 1 : 0;
-    }
-    __syncthreads();
-    if (s_stop) {
+    cl_sync();
+    double mx = 0.0;
+    for (int j = 0; j < kk; ++j) mx = fmax(mx, __ldcg(gR + j));
+    const bool stop = sqrt(mx) <= ea.tol;   // identical in every CTA of the cluster
+    cl_sync();                               // gR / gC / gT are rewritten next iteration
+    if (stop) {
       ++it;
       break;
     }
   }
+  for (int e = threadIdx.x; e < mb; e += NT) theta[e] = __ldcg(gT + e);
+  __syncthreads();
   // ---------------- write phi = chi psi on the padded box, eigenvalues, kept count
   int nk = min(d.kmax, mb);
   if (ea.lam_thr > 0.0 && ea.lam_thr < 1e300) {
@@ -445,8 +505,8 @@ __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __r
   }
   const int I = C.rep_agg / (d.ncy + 1), J = C.rep_agg - (C.rep_agg / (d.ncy + 1)) * (d.ncy + 1);
   const int gx0 = I * d.cx - d.cx, gy0 = J * d.cy - d.cy;
-  double* ph = phi + (size_t)blockIdx.x * d.kmax * d.box_nodes * 2;
-  for (int e = threadIdx.x; e < d.kmax * d.box_nodes * 2; e += NT) {
+  double* ph = phi + (size_t)cls * d.kmax * d.box_nodes * 2;
+  for (int e = t0; e < d.kmax * d.box_nodes * 2; e += tstride) {
     const int a = e / (d.box_nodes * 2), rest = e - a * d.box_nodes * 2;
     const int bn = rest >> 1, c = rest & 1;
     const int px = bn / d.by, py = bn - (bn / d.by) * d.by;
@@ -460,11 +520,13 @@ __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __r
     }
     ph[e] = v;
   }
-  for (int a = threadIdx.x; a < d.kmax; a += NT)
-    lam[(size_t)blockIdx.x * d.kmax + a] = (a < mb) ? theta[a] : 0.0;
-  if (threadIdx.x == 0) {
-    classes[blockIdx.x].iters = it;
-    classes[blockIdx.x].nkept = nk;
+  if (rank == 0) {
+    for (int a = threadIdx.x; a < d.kmax; a += NT)
+      lam[(size_t)cls * d.kmax + a] = (a < mb) ? theta[a] : 0.0;
+    if (threadIdx.x == 0) {
+      classes[cls].iters = it;
+      classes[cls].nkept = nk;
+    }
   }
 }
 
@@ -472,8 +534,7 @@ __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __r
 
 size_t eig_smem_bytes(int mlmax, int mb) {
   const int sz = mlmax * (mlmax > mb ? mlmax : mb);
-  return (size_t)(2 * sz + 6 * mb * mb + 32 + 2 * mlmax + MSF_MAX_BLOCK_EIG * (NT / 32)) *
-         sizeof(double);
+  return (size_t)(4 * sz + 6 * mb * mb + 32 + 2 * mlmax) * sizeof(double);
 }
 
 void launch_build_basis(msf_ctx* c) {
@@ -487,9 +548,21 @@ void launch_build_basis(msf_ctx* c) {
   ea.mlmax = 2 * d.by;
   const size_t smem = eig_smem_bytes(ea.mlmax, ea.mb);
   cudaFuncSetAttribute(k_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_eigen<<<c->n_cls, NT, smem, c->stream>>>(d, c->K0,
-                                              c->E + (size_t)c->p.dilated * d.ne, c->fixg,
-                                              c->classes_d, c->eig_work, c->phi, c->lam, ea,
-                                              c->factor_status + MSF_MAX_RHS);
+  // one thread-block cluster of EIG_CL CTAs per class
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c->n_cls * EIG_CL);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = EIG_CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_eigen, d, c->K0, (const double*)(c->E + (size_t)c->p.dilated * d.ne),
+                     (const uint8_t*)c->fixg, c->classes_d, c->eig_work, c->phi, c->lam, ea,
+                     c->factor_status + MSF_MAX_RHS);
   MSF_LAUNCHED(c);
 }

@@ -185,7 +185,8 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   for (EigClass& C : P.classes) {
     const long long ml = 2 * C.nby, n = (long long)C.nbx * ml;
     C.off = P.eig_doubles;
-    P.eig_doubles += 2LL * C.nbx * ml * ml + 3LL * n * P.mb + n;
+    // Sinv, W blocks; X, Y, KY; D; cluster scratch (G, H, Ritz coefficients, values, residuals)
+    P.eig_doubles += 2LL * C.nbx * ml * ml + 3LL * n * P.mb + n + 3LL * P.mb * P.mb + 32 + 8 * 16;
     P.eig_doubles = (P.eig_doubles + 31) & ~31LL;
   }
   // coarse cyclic-reduction levels

@@ -47,8 +47,13 @@ def test_edge_pcg_parity(name):
     ref = problem.solve(spec, x, fx, f, tol=1e-8)
     its, comps, noconv = m.pcg_solve(tol=1e-8)
     assert not noconv
-    for k in range(spec.n_rhs):
-        assert abs(its[k] - ref["iters"][k]) <= 1, (its, ref["iters"])
+    # With fewer than 3 modes the kept eigenvectors of interior agglomerates are arbitrary
+    # vectors of the 3-dimensional rigid-body eigenspace (lambda ~ 0, Neumann problem): the
+    # coarse space, hence the iteration count, is not unique (any rounding picks another
+    # vector).  Only the unique results -- solution and compliance below -- are compared.
+    if spec.n_modes >= 3:
+        for k in range(spec.n_rhs):
+            assert abs(its[k] - ref["iters"][k]) <= 1, (its, ref["iters"])
     ref = problem.solve(spec, x, fx, f, tol=1e-12)
     u = torch.empty(spec.n_rhs * spec.n_dof, dtype=torch.float64, device=DEV)
     its, comps, noconv = m.pcg_solve(tol=1e-12, u=u)
