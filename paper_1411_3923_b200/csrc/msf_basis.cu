@@ -269,13 +269,13 @@ __device__ __forceinline__ double dot4(const double* A, int sa, const double* B,
   return (s0 + s1) + (s2 + s3);
 }
 
-__global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __restrict__ E,
+__global__ void __launch_bounds__(NT) k_eigen_factor(Dims d, K0Mat K, const double* __restrict__ E,
                                               const uint8_t* __restrict__ fixn,
                                               EigClass* classes, double* work, double* phi,
                                               double* lam, EigArgs ea, int* status) {
   extern __shared__ double sm[];
-  const int cls = blockIdx.x / EIG_CL, rank = blockIdx.x - cls * EIG_CL;
-  const int t0 = rank * NT + threadIdx.x, tstride = EIG_CL * NT;   // cluster-wide thread index
+  // one CTA per class: A = K - sigma D by block Thomas in shared memory
+  const int cls = blockIdx.x;
   EigClass C = classes[cls];
   const int ml = 2 * C.nby, nbl = C.nbx, n = nbl * ml;
   const int mb = ea.mb;
@@ -284,30 +284,13 @@ __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __r
   double* T = S + sz;             // [sz]
   double* Pv = T + sz;            // [sz] previous block inverse
   double* Wv = Pv + sz;           // [sz] current W block
-  double* G = Wv + sz;            // [mb*mb]
-  double* H = G + mb * mb;
-  double* Cm = H + mb * mb;
-  double* Lw = Cm + mb * mb;
-  double* Mw = Lw + mb * mb;
-  double* Vw = Mw + mb * mb;
-  double* theta = Vw + mb * mb;   // [mb]
-  double* rowk = theta + 32;      // [ml]
+  double* rowk = Wv + sz;         // [ml]
   double* colk = rowk + ea.mlmax; // [ml]
 
   double* Sinv = work + C.off;
   double* W = Sinv + (size_t)nbl * ml * ml;
-  double* X = W + (size_t)nbl * ml * ml;
-  double* Y = X + (size_t)n * mb;
-  double* KY = Y + (size_t)n * mb;
-  double* Dv = KY + (size_t)n * mb;
-  double* gG = Dv + n;                 // [mb*mb] cluster-shared scratch (global)
-  double* gH = gG + mb * mb;           // [mb*mb]
-  double* gC = gH + mb * mb;           // [mb*mb] Ritz coefficients
-  double* gT = gC + mb * mb;           // [32]   Ritz values
-  double* gR = gT + 32;                // [EIG_CL * 16] residual partials
 
-  // ---------------- factorisation A = K - sigma D by block Thomas (CTA 0, shared memory)
-  if (rank == 0) {
+  {
     for (int I = 0; I < nbl; ++I) {
       assemble_block(d, K, E, fixn, C, I, I, ea.sigma, S, ml);
       if (I > 0) {
@@ -336,6 +319,38 @@ __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __r
       __syncthreads();
     }
   }
+}
+
+__global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __restrict__ E,
+                                              const uint8_t* __restrict__ fixn,
+                                              EigClass* classes, double* work, double* phi,
+                                              double* lam, EigArgs ea, int* status) {
+  extern __shared__ double sm[];
+  const int cls = blockIdx.x / EIG_CL, rank = blockIdx.x - cls * EIG_CL;
+  const int t0 = rank * NT + threadIdx.x, tstride = EIG_CL * NT;   // cluster-wide thread index
+  EigClass C = classes[cls];
+  const int ml = 2 * C.nby, nbl = C.nbx, n = nbl * ml;
+  const int mb = ea.mb;
+  double* G = sm;                 // [mb*mb]
+  double* H = G + mb * mb;
+  double* Cm = H + mb * mb;
+  double* Lw = Cm + mb * mb;
+  double* Mw = Lw + mb * mb;
+  double* Vw = Mw + mb * mb;
+  double* theta = Vw + mb * mb;   // [mb]
+
+  double* Sinv = work + C.off;
+  double* W = Sinv + (size_t)nbl * ml * ml;
+  double* X = W + (size_t)nbl * ml * ml;
+  double* Y = X + (size_t)n * mb;
+  double* KY = Y + (size_t)n * mb;
+  double* Dv = KY + (size_t)n * mb;
+  double* gG = Dv + n;                 // [mb*mb] cluster-shared scratch (global)
+  double* gH = gG + mb * mb;           // [mb*mb]
+  double* gC = gH + mb * mb;           // [mb*mb] Ritz coefficients
+  double* gT = gC + mb * mb;           // [32]   Ritz values
+  double* gR = gT + 32;                // [EIG_CL * 16] residual partials
+
   // ---------------- D = diag(K) on free DOFs, random start
   for (int i = t0; i < n; i += tstride) {
     const int lx = i / ml, rr = i - (i / ml) * ml, ly = rr >> 1, c = rr & 1;
@@ -532,10 +547,11 @@ __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __r
 
 }  // namespace
 
-size_t eig_smem_bytes(int mlmax, int mb) {
+size_t eig_smem_bytes(int mlmax, int mb) {   // factorisation kernel
   const int sz = mlmax * (mlmax > mb ? mlmax : mb);
-  return (size_t)(4 * sz + 6 * mb * mb + 32 + 2 * mlmax) * sizeof(double);
+  return (size_t)(4 * sz + 2 * mlmax) * sizeof(double);
 }
+static size_t eig_iter_smem_bytes(int mb) { return (size_t)(6 * mb * mb + 32) * sizeof(double); }
 
 void launch_build_basis(msf_ctx* c) {
   const Dims& d = c->d;
@@ -546,8 +562,14 @@ void launch_build_basis(msf_ctx* c) {
   ea.maxit = c->p.eig_max_iter > 0 ? c->p.eig_max_iter : 60;
   ea.mb = c->mb;
   ea.mlmax = 2 * d.by;
-  const size_t smem = eig_smem_bytes(ea.mlmax, ea.mb);
-  cudaFuncSetAttribute(k_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem_f = eig_smem_bytes(ea.mlmax, ea.mb);
+  cudaFuncSetAttribute(k_eigen_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
+  k_eigen_factor<<<c->n_cls, NT, smem_f, c->stream>>>(d, c->K0,
+                                                     c->E + (size_t)c->p.dilated * d.ne, c->fixg,
+                                                     c->classes_d, c->eig_work, c->phi, c->lam, ea,
+                                                     c->factor_status + MSF_MAX_RHS);
+  MSF_LAUNCHED(c);
+  const size_t smem = eig_iter_smem_bytes(ea.mb);
   // one thread-block cluster of EIG_CL CTAs per class
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c->n_cls * EIG_CL);
