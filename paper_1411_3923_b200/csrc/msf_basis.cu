@@ -14,6 +14,8 @@
 //   ||K x - theta D x||_{D^-1} <= eig_tol (x D-normalised).
 // The basis phi_{i,a} = chi_i psi_a (bilinear partition of unity, reading R6) is written on
 // the padded (2cx+1)x(2cy+1)-node box of the class.
+#include <algorithm>
+
 #include "msf_internal.cuh"
 
 namespace {
@@ -74,8 +76,11 @@ __device__ void assemble_block(const Dims& d, const K0Mat& K, const double* __re
   }
 }
 
-// in-place SPD inverse of S (m x m, shared memory) by the sweep operator
+// in-place SPD inverse of S (m x m, shared memory) by the sweep operator.  Threads are laid
+// out as NT/32 row groups x 32 column lanes, so no index division in the m sweep steps.
 __device__ void cta_inverse(double* S, int m, double* rowk, double* colk, int* status) {
+  const int jl = threadIdx.x & 31, ig = threadIdx.x >> 5;
+  constexpr int RG = NT / 32;
   for (int k = 0; k < m; ++k) {
     for (int i = threadIdx.x; i < m; i += NT) {
       rowk[i] = S[k * m + i];
@@ -85,14 +90,14 @@ __device__ void cta_inverse(double* S, int m, double* rowk, double* colk, int* s
     const double piv = rowk[k];
     if (!(piv > 0.0) && threadIdx.x == 0) atomicExch(status, 2);
     const double ip = 1.0 / piv;
-    for (int e = threadIdx.x; e < m * m; e += NT) {
-      const int i = e / m, j = e - (e / m) * m;
-      double v;
-      if (i == k && j == k) v = -ip;
-      else if (i == k) v = rowk[j] * ip;
-      else if (j == k) v = colk[i] * ip;
-      else v = S[e] - colk[i] * rowk[j] * ip;
-      S[e] = v;
+    for (int i = ig; i < m; i += RG) {
+      const double ci = colk[i] * ip;
+      double* Si = S + i * m;
+      if (i == k) {
+        for (int j = jl; j < m; j += 32) Si[j] = (j == k) ? -ip : rowk[j] * ip;
+      } else {
+        for (int j = jl; j < m; j += 32) Si[j] = (j == k) ? ci : fma(-ci, rowk[j], Si[j]);
+      }
     }
     __syncthreads();
   }
@@ -269,6 +274,58 @@ __device__ __forceinline__ double dot4(const double* A, int sa, const double* B,
   return (s0 + s1) + (s2 + s3);
 }
 
+// C[0:m,0:m] (ld m) = beta C + alpha A B, A element (r, k) at A[r*ar + k*ak], B (k, c) at
+// B[k*m + c], all in shared memory; 4x4 outputs per thread (0.5 shared loads per FMA).
+__device__ void smem_gemm44(const double* A, int ar, int ak, const double* B, double* C, int m,
+                            double alpha, double beta, double* C2 = nullptr) {
+  const int nt = (m + 3) / 4;
+  for (int tile = threadIdx.x; tile < nt * nt; tile += NT) {
+    const int r0 = (tile / nt) * 4, c0 = (tile - (tile / nt) * nt) * 4;
+    double acc[4][4] = {};
+    for (int k = 0; k < m; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = (r0 + i < m) ? A[(r0 + i) * ar + k * ak] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = (c0 + j < m) ? B[k * m + c0 + j] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (r0 + i < m && c0 + j < m) {
+          const int e = (r0 + i) * m + c0 + j;
+          const double v = (beta != 0.0 ? beta * C[e] : 0.0) + alpha * acc[i][j];
+          C[e] = v;
+          if (C2) C2[e] = v;
+        }
+  }
+}
+
+// All diagonal blocks D_I of A = K - sigma D and coupling blocks U_{I-1} of every class in
+// parallel (blockIdx.x = class * 2 * nbl_max + 2 I + {0: D_I -> Sinv slot I, 1: U_{I-1} -> W
+// slot I}); the sequential block-Thomas kernel then only multiplies and inverts.
+__global__ void __launch_bounds__(NT) k_eigen_blocks(Dims d, K0Mat K, const double* __restrict__ E,
+                                                     const uint8_t* __restrict__ fixn,
+                                                     const EigClass* __restrict__ classes,
+                                                     double* work, EigArgs ea, int nbl_max) {
+  const int cls = blockIdx.x / (2 * nbl_max), rest = blockIdx.x - cls * 2 * nbl_max;
+  const int I = rest >> 1, which = rest & 1;
+  const EigClass C = classes[cls];
+  const int ml = 2 * C.nby, nbl = C.nbx;
+  if (I >= nbl || (which == 1 && I == 0)) return;
+  double* Sinv = work + C.off;
+  double* W = Sinv + (size_t)nbl * ml * ml;
+  if (which == 0)
+    assemble_block(d, K, E, fixn, C, I, I, ea.sigma, Sinv + (size_t)I * ml * ml, ml);
+  else
+    assemble_block(d, K, E, fixn, C, I - 1, I, ea.sigma, W + (size_t)I * ml * ml, ml);
+}
+
 __global__ void __launch_bounds__(NT) k_eigen_factor(Dims d, K0Mat K, const double* __restrict__ E,
                                               const uint8_t* __restrict__ fixn,
                                               EigClass* classes, double* work, double* phi,
@@ -292,22 +349,17 @@ __global__ void __launch_bounds__(NT) k_eigen_factor(Dims d, K0Mat K, const doub
 
   {
     for (int I = 0; I < nbl; ++I) {
-      assemble_block(d, K, E, fixn, C, I, I, ea.sigma, S, ml);
+      // D_I and U_{I-1} were assembled by k_eigen_blocks into the Sinv / W slots of I
+      const double* DI = Sinv + (size_t)I * ml * ml;
+      for (int e = threadIdx.x; e < ml * ml; e += NT) S[e] = DI[e];
       if (I > 0) {
-        assemble_block(d, K, E, fixn, C, I - 1, I, ea.sigma, T, ml);   // U_{I-1}
+        const double* UI = W + (size_t)I * ml * ml;
+        for (int e = threadIdx.x; e < ml * ml; e += NT) T[e] = UI[e];
         __syncthreads();
         double* WI = W + (size_t)I * ml * ml;
-        for (int e = threadIdx.x; e < ml * ml; e += NT) {            // W_I = Sinv_{I-1} U_{I-1}
-          const int r = e / ml, cc = e - (e / ml) * ml;
-          const double v = dot4(Pv + r * ml, 1, T + cc, ml, ml);
-          Wv[e] = v;
-          WI[e] = v;
-        }
+        smem_gemm44(Pv, ml, 1, T, Wv, ml, 1.0, 0.0, WI);              // W_I = Sinv_{I-1} U_{I-1}
         __syncthreads();
-        for (int e = threadIdx.x; e < ml * ml; e += NT) {            // S -= U^T W
-          const int r = e / ml, cc = e - (e / ml) * ml;
-          S[e] -= dot4(T + r, ml, Wv + cc, ml, ml);
-        }
+        smem_gemm44(T, 1, ml, Wv, S, ml, -1.0, 1.0);                 // S -= U^T W
       }
       __syncthreads();
       cta_inverse(S, ml, rowk, colk, status);
@@ -380,9 +432,17 @@ __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __r
       const double* WI = W + (size_t)I * ml * ml;
       const double* Yp = B1 + (size_t)(I - 1) * ml * mb;
       double* Yc = B1 + (size_t)I * ml * mb;
-      for (int e = t0; e < ml * mb; e += tstride) {
-        const int r = e / mb, j = e - (e / mb) * mb;
-        Yc[e] -= dot4(WI + r, ml, Yp + j, mb, ml);
+      // two lanes per output (halves of the inner product), combined by a shuffle
+      for (int e2 = t0; e2 < 2 * ml * mb + (tstride - (2 * ml * mb) % tstride) % tstride; e2 += tstride) {
+        const int e = e2 >> 1, h = e2 & 1;
+        double v = 0.0;
+        if (e < ml * mb) {
+          const int r = e / mb, j = e - (e / mb) * mb;
+          const int k0 = h ? ml / 2 : 0, k1 = h ? ml : ml / 2;
+          v = dot4(WI + (size_t)k0 * ml + r, ml, Yp + (size_t)k0 * mb + j, mb, k1 - k0);
+        }
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (e < ml * mb && h == 0) Yc[e] -= v;
       }
       cl_sync();
     }
@@ -398,9 +458,16 @@ __global__ void __launch_bounds__(NT) k_eigen(Dims d, K0Mat K, const double* __r
       const double* WI = W + (size_t)(I + 1) * ml * ml;
       const double* Yn = B2 + (size_t)(I + 1) * ml * mb;
       double* Yc = B2 + (size_t)I * ml * mb;
-      for (int e = t0; e < ml * mb; e += tstride) {
-        const int r = e / mb, j = e - (e / mb) * mb;
-        Yc[e] -= dot4(WI + (size_t)r * ml, 1, Yn + j, mb, ml);
+      for (int e2 = t0; e2 < 2 * ml * mb + (tstride - (2 * ml * mb) % tstride) % tstride; e2 += tstride) {
+        const int e = e2 >> 1, h = e2 & 1;
+        double v = 0.0;
+        if (e < ml * mb) {
+          const int r = e / mb, j = e - (e / mb) * mb;
+          const int k0 = h ? ml / 2 : 0, k1 = h ? ml : ml / 2;
+          v = dot4(WI + (size_t)r * ml + k0, 1, Yn + (size_t)k0 * mb + j, mb, k1 - k0);
+        }
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (e < ml * mb && h == 0) Yc[e] -= v;
       }
       cl_sync();
     }
@@ -562,6 +629,11 @@ void launch_build_basis(msf_ctx* c) {
   ea.maxit = c->p.eig_max_iter > 0 ? c->p.eig_max_iter : 60;
   ea.mb = c->mb;
   ea.mlmax = 2 * d.by;
+  int nbl_max = 1;
+  for (const EigClass& C : c->classes) nbl_max = std::max(nbl_max, C.nbx);
+  k_eigen_blocks<<<c->n_cls * 2 * nbl_max, NT, 0, c->stream>>>(
+      d, c->K0, c->E + (size_t)c->p.dilated * d.ne, c->fixg, c->classes_d, c->eig_work, ea, nbl_max);
+  MSF_LAUNCHED(c);
   const size_t smem_f = eig_smem_bytes(ea.mlmax, ea.mb);
   cudaFuncSetAttribute(k_eigen_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
   k_eigen_factor<<<c->n_cls, NT, smem_f, c->stream>>>(d, c->K0,
