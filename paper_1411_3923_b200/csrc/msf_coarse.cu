@@ -458,6 +458,41 @@ __global__ void __launch_bounds__(256) k_binv_panels(double** mats, int m, int p
   }
 }
 
+// In-place inverse of a batch of SPD m x m matrices (m <= 158) by the sweep operator with the
+// matrix resident in shared memory (one CTA per matrix, 32 row groups x 32 column lanes, no
+// index division); each pivot step touches only shared memory.
+__global__ void __launch_bounds__(1024) k_spd_inverse_smem(double** mats, int m, int* status) {
+  extern __shared__ double smi[];
+  double* S = smi;              // [m*m]
+  double* rowk = S + m * m;     // [m]
+  double* colk = rowk + m;      // [m]
+  double* A = mats[blockIdx.x];
+  const int tid = threadIdx.x, jl = tid & 31, ig = tid >> 5;
+  for (int e = tid; e < m * m; e += 1024) S[e] = A[e];
+  __syncthreads();
+  for (int k = 0; k < m; ++k) {
+    for (int i = tid; i < m; i += 1024) {
+      rowk[i] = S[k * m + i];
+      colk[i] = S[i * m + k];
+    }
+    __syncthreads();
+    const double piv = rowk[k];
+    if (!(piv > 0.0) && tid == 0) atomicExch(status, 1);
+    const double ip = 1.0 / piv;
+    for (int i = ig; i < m; i += 32) {
+      const double ci = colk[i] * ip;
+      double* Si = S + i * m;
+      if (i == k) {
+        for (int j = jl; j < m; j += 32) Si[j] = (j == k) ? -ip : rowk[j] * ip;
+      } else {
+        for (int j = jl; j < m; j += 32) Si[j] = (j == k) ? ci : fma(-ci, rowk[j], Si[j]);
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < m * m; e += 1024) A[e] = -S[e];
+}
+
 __global__ void k_copy_blocks(double** src, double** dst, int m) {
   const double* s = src[blockIdx.y];
   double* t = dst[blockIdx.y];
@@ -712,6 +747,11 @@ static void launch_spd_inverse(msf_ctx* c, double** mats, int n, int m) {
       k_binv_panels<<<dim3(T, 2, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_P, c->binv_R);
       c->launches += 4;
     }
+  } else if ((size_t)(m * m + 2 * m) * sizeof(double) <= 200 * 1024) {
+    const size_t smem = (size_t)(m * m + 2 * m) * sizeof(double);
+    cudaFuncSetAttribute(k_spd_inverse_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_spd_inverse_smem<<<n, 1024, smem, c->stream>>>(mats, m, c->factor_status);
+    MSF_LAUNCHED(c);
   } else {
     k_spd_inverse<<<n, 1024, 2 * (size_t)m * sizeof(double), c->stream>>>(mats, m, c->factor_status);
     MSF_LAUNCHED(c);
