@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const dou
                                                       const int* __restrict__ cls_of_agg,
                                                       double* Kcell, int CH) {
   extern __shared__ double sm[];
-  const int rhs = blockIdx.y;
+  // all realisations in one CTA: V_e = K0 Phi_e and Phi_e^T V_e do not depend on the
+  // realisation, only the scalar modulus E_e does (R accumulators per output entry)
   const int cell = blockIdx.x;
   const int CI = cell / d.ncy, CJ = cell - (cell / d.ncy) * d.ncy;
   const int P = 4 * d.kmax;
@@ -163,13 +164,13 @@ __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const dou
   double* PhiP = sm;                                       // [ncn][2][CH]
   double* PhiQ = single ? PhiP : PhiP + (size_t)ncn * 2 * CH;
   double* V = PhiQ + (size_t)ncn * 2 * CH;                 // [16][8][CH]
-  double* Ech = V + 16 * 8 * CH;                           // [16]
+  double* Ech = V + 16 * 8 * CH;                           // [MSF_MAX_RHS][16]
   stage_cell_cols(d, phi, cls_of_agg, CI, CJ, p0, pw, CH, PhiP);
   if (!single) stage_cell_cols(d, phi, cls_of_agg, CI, CJ, q0, qw, CH, PhiQ);
-  const double* E = Eall + (size_t)rhs * d.ne;
+  const int R = d.R;
   const int nel = d.cx * d.cy;
   const int nent = CH * CH;   // <= NT
-  double acc = 0.0;
+  double acc[MSF_MAX_RHS] = {0.0, 0.0, 0.0, 0.0};
   __syncthreads();
   for (int e0 = 0; e0 < nel; e0 += 16) {
     const int ne = min(16, nel - e0);
@@ -189,10 +190,11 @@ __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const dou
       }
       V[(el * 8 + i) * CH + q] = s;
     }
-    for (int el = threadIdx.x; el < ne; el += NT) {
+    for (int k = threadIdx.x; k < ne * R; k += NT) {
+      const int r = k / ne, el = k - r * ne;
       const int le = e0 + el;
       const int lex = le / d.cy, ley = le - (le / d.cy) * d.cy;
-      Ech[el] = E[(size_t)(CI * d.cx + lex) * d.nely + CJ * d.cy + ley];
+      Ech[r * 16 + el] = Eall[(size_t)r * d.ne + (size_t)(CI * d.cx + lex) * d.nely + CJ * d.cy + ley];
     }
     __syncthreads();
     const int ent = threadIdx.x;
@@ -209,7 +211,9 @@ __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const dou
             const int nx = lex + ((b == 1 || b == 2) ? 1 : 0), ny = ley + ((b >= 2) ? 1 : 0);
             t = fma(PhiP[((nx * ncn_y + ny) * 2 + comp) * CH + p], V[(el * 8 + i) * CH + q], t);
           }
-          acc = fma(Ech[el], t, acc);
+#pragma unroll
+          for (int r = 0; r < MSF_MAX_RHS; ++r)
+            if (r < R) acc[r] = fma(Ech[r * 16 + el], t, acc[r]);
         }
       }
     }
@@ -219,7 +223,9 @@ __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const dou
   if (ent < nent) {
     const int p = ent / CH, q = ent - (ent / CH) * CH;
     if (p < pw && q < qw)
-      Kcell[((size_t)rhs * d.ncx * d.ncy + cell) * P * P + (size_t)(p0 + p) * P + (q0 + q)] = acc;
+#pragma unroll
+      for (int r = 0; r < MSF_MAX_RHS; ++r)
+        if (r < R) Kcell[((size_t)r * d.ncx * d.ncy + cell) * P * P + (size_t)(p0 + p) * P + (q0 + q)] = acc[r];
   }
 }
 
@@ -716,13 +722,13 @@ void launch_coarse_galerkin(msf_ctx* c) {
   int CH = std::min(P, 16);
   auto smem_for = [&](int ch) {
     const bool single = ch >= P;
-    return ((single ? 1 : 2) * ncn2 * ch + 16 * 8 * (size_t)ch + 16) * sizeof(double);
+    return ((single ? 1 : 2) * ncn2 * ch + 16 * 8 * (size_t)ch + 16 * MSF_MAX_RHS) * sizeof(double);
   };
   while (CH > 2 && smem_for(CH) > 220 * 1024) CH /= 2;
   const size_t smem = smem_for(CH);
   const int nch = (P + CH - 1) / CH;
   cudaFuncSetAttribute(k_cell_galerkin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_cell_galerkin<<<dim3(d.ncx * d.ncy, d.R, nch * nch), NT, smem, c->stream>>>(
+  k_cell_galerkin<<<dim3(d.ncx * d.ncy, 1, nch * nch), NT, smem, c->stream>>>(
       d, c->K0, c->E, c->phi, c->cls_of_agg_d, c->Kcell, CH);
   MSF_LAUNCHED(c);
   {
