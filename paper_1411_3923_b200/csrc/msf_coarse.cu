@@ -521,15 +521,19 @@ __global__ void __launch_bounds__(256) k_gemm(double** As, double** Bs, double**
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double acc[4][4] = {};
   for (int k0 = 0; k0 < m; k0 += BK) {
+    // tile loads mapped so that consecutive threads read consecutive addresses: along the
+    // row index for a transposed operand, along k for a row-major one
     for (int e = threadIdx.x; e < BK * BM; e += 256) {
-      const int kk = e / BM, rr = e - (e / BM) * BM;
+      int kk, rr;
+      if (TA) { kk = e / BM; rr = e - kk * BM; } else { rr = e / BK; kk = e - rr * BK; }
       const int gr = row0 + rr, gk = k0 + kk;
-      double va = 0.0, vb = 0.0;
-      if (gr < m && gk < m) va = TA ? A[(size_t)gk * m + gr] : A[(size_t)gr * m + gk];
-      const int gc = col0 + rr;
-      if (gc < m && gk < m) vb = TB ? B[(size_t)gc * m + gk] : B[(size_t)gk * m + gc];
-      sA[kk][rr] = va;
-      sB[kk][rr] = vb;
+      sA[kk][rr] = (gr < m && gk < m) ? (TA ? A[(size_t)gk * m + gr] : A[(size_t)gr * m + gk]) : 0.0;
+    }
+    for (int e = threadIdx.x; e < BK * BM; e += 256) {
+      int kk, cc;
+      if (TB) { cc = e / BK; kk = e - cc * BK; } else { kk = e / BM; cc = e - kk * BM; }
+      const int gc = col0 + cc, gk = k0 + kk;
+      sB[kk][cc] = (gc < m && gk < m) ? (TB ? B[(size_t)gc * m + gk] : B[(size_t)gk * m + gc]) : 0.0;
     }
     __syncthreads();
 #pragma unroll
