@@ -188,24 +188,31 @@ int msf_bench_kernels(msf_ctx* ctx, int reps, double* ms, double* bytes);
  * owns the node columns of coarse columns [C0, C1) (the last rank also owns column nelx),
  * stores its strip plus a one-node-column halo on each side (and one padding column on the
  * left when needed so that its first local column is even: the 4-colour Gauss-Seidel order
- * of reading R7 is the global one), and runs every fine-grid kernel on it.  The coarse space
- * (moduli of the whole grid, basis, K_c and its factorisation, the coarse solve) is
- * replicated on every rank.  Per PCG iteration: 14 halo exchanges of the smoother iterate
- * (one per colour phase), sum all-reduces of p.Ap, ||r||^2, r.z and of the restricted
- * coarse residual R_c t.  Results equal the single-GPU path up to the summation order of
- * the dot products and of R_c t.
+ * of reading R7 is the global one), and runs every fine-grid kernel on it.  The moduli of
+ * the whole grid and the spectral basis are replicated.  K_c is distributed by block
+ * columns: rank r computes the Galerkin products of its coarse cells and reduces its chain
+ * of blocks [C0, C1] (C1 = ncx on the last rank) to the chain's two end blocks; one sum
+ * all-reduce of the end blocks gives every rank the block-tridiagonal interface system on
+ * the nranks + 1 blocks C0_0 = 0, C0_1, ..., ncx, which is reduced (and later solved)
+ * redundantly on every rank.  Per PCG iteration: 15 halo exchanges of the smoother iterate
+ * (one per colour phase, one after the prolongation), sum all-reduces of p.Ap, ||r||^2,
+ * r.z and of the chain-end coarse rhs ((nranks + 1) * m doubles per realisation).  Results
+ * equal the single-GPU path up to the summation order of the dot products and the
+ * elimination order of K_c (the interface blocks are eliminated last).
  *
  * Transports: MSF_TRANSPORT_NCCL, handle = host pointer to the 128-byte NCCL unique id
  * (msf_nccl_unique_id on rank 0, broadcast by the caller), one process per GPU; all the
  * ordinary entry points then work on the strip context (pcg_solve, sensitivities and
  * design_iteration communicate inside).  MSF_TRANSPORT_GROUP, handle = msf_group*: all
  * ranks of the group are contexts of this process on the current device sharing one
- * stream; the communicating steps are driven by msf_group_pcg_solve /
- * msf_group_sensitivities (the per-rank msf_pcg_solve / msf_sensitivities return
- * MSF_ERR_STATE); the replicated steps use the ordinary per-context calls.
+ * stream; the communicating steps are driven by msf_group_assemble_coarse /
+ * msf_group_pcg_solve / msf_group_sensitivities (the per-rank msf_assemble_coarse /
+ * msf_pcg_solve / msf_sensitivities return MSF_ERR_STATE); the replicated steps use the
+ * ordinary per-context calls.
  * Vectors returned from a strip context (u of msf_pcg_solve) are
  * LOCAL: [n_rhs][ncols*(nely+1)][2] over global node columns [gox, gox+ncols).
- * msf_matvec / msf_precond_apply / msf_sgs return MSF_ERR_STATE on a strip context;
+ * msf_matvec / msf_precond_apply / msf_sgs / msf_coarse_solve / msf_get_coarse_blocks
+ * return MSF_ERR_STATE on a strip context of more than one rank;
  * msf_bench_kernels times only the kernels without communication (ms[6] = ms[7] = -1). */
 #define MSF_TRANSPORT_NCCL 1
 #define MSF_TRANSPORT_GROUP 2
@@ -224,6 +231,15 @@ int msf_dist_setup(const msf_problem* p, const uint8_t* fixed_mask, const double
 int msf_nccl_unique_id(uint8_t* id);
 int msf_group_create(int nranks, msf_group** out);
 int msf_group_destroy(msf_group* g);
+/* Distributed K_c assembly + factorisation of every rank of the group (after each rank's
+ * msf_build_coarse_basis). */
+int msf_group_assemble_coarse(msf_group* g);
+/* Parity diagnostic of the distributed coarse solve: c = K_c^{-1} b for realisation rhs,
+ * b and c device, GLOBAL [n_coarse_slots] (layout of msf_coarse_solve). */
+int msf_group_coarse_solve(msf_group* g, int rhs, const double* b, double* c);
+/* Parity diagnostic of the partitioned preconditioner: z = M^{-1} r (one V-cycle, reading
+ * R8) for realisation rhs; r, z device, GLOBAL [n_dof] (z written on every node). */
+int msf_group_precond_apply(msf_group* g, int rhs, const double* r, double* z);
 /* iters, compliance: host [n_rhs] (identical on every rank) or NULL. */
 int msf_group_pcg_solve(msf_group* g, int n_rhs, double tol, int max_it, int32_t* iters,
                         double* compliance);

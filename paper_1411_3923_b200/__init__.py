@@ -31,7 +31,7 @@ EXPORTS = [
     "msf_coarse_solve", "msf_get_basis", "msf_get_coarse_blocks", "msf_get_physical",
     "msf_info", "msf_launch_count", "msf_bench_kernels",
     "msf_strip_bounds", "msf_dist_workspace_bytes", "msf_dist_setup", "msf_nccl_unique_id",
-    "msf_group_create", "msf_group_destroy", "msf_group_pcg_solve", "msf_group_sensitivities",
+    "msf_group_create", "msf_group_destroy", "msf_group_assemble_coarse", "msf_group_coarse_solve", "msf_group_precond_apply", "msf_group_pcg_solve", "msf_group_sensitivities",
     "msf_get_solution",
 ]
 
@@ -83,6 +83,9 @@ def load_library(path: str = LIB_PATH):
         "msf_dist_setup": [P(MsfProblem), V, V, I, I, I, V, V, ctypes.c_size_t, V, P(V)],
         "msf_nccl_unique_id": [V], "msf_get_solution": [V, I, V],
         "msf_group_create": [I, P(V)], "msf_group_destroy": [V],
+        "msf_group_assemble_coarse": [V],
+        "msf_group_coarse_solve": [V, I, V, V],
+        "msf_group_precond_apply": [V, I, V, V],
         "msf_group_pcg_solve": [V, I, D, I, i32p, dp],
         "msf_group_sensitivities": [V, D, D, V, V, dp, dp, dp],
     }
@@ -389,8 +392,21 @@ class MsfemGroup:
             m.build_coarse_basis()
 
     def assemble_coarse(self):
-        for m in self.ranks:
-            m.assemble_coarse()
+        self._check(self.lib.msf_group_assemble_coarse(self.g))
+
+    def coarse_solve(self, rhs, b, x=None):
+        """Distributed K_c^{-1} b (parity diagnostic); b, x: device [n_coarse_slots]."""
+        import torch
+        x = torch.empty_like(b) if x is None else x
+        self._check(self.lib.msf_group_coarse_solve(self.g, rhs, _ptr(b), _ptr(x)))
+        return x
+
+    def precond_apply(self, rhs, r, z=None):
+        """Partitioned V-cycle z = M^{-1} r (parity diagnostic); r, z: device [n_dof]."""
+        import torch
+        z = torch.zeros_like(r) if z is None else z
+        self._check(self.lib.msf_group_precond_apply(self.g, rhs, _ptr(r), _ptr(z)))
+        return z
 
     def pcg_solve(self, n_rhs=None, tol=1e-8, max_it=2000):
         n = self.n_rhs if n_rhs is None else n_rhs

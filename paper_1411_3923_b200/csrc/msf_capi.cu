@@ -72,6 +72,8 @@ struct Plan {
   std::vector<double> fw;
   double wsum = 1.0;
   std::vector<CrLevel> cr;
+  int n_local = 0;            // chain levels (the rest: interface levels, strips only)
+  std::vector<int> iface;     // interface blocks (strips only)
   std::vector<int> top_blocks;
   size_t top_ptrs = 0;
   size_t binv_n = 1;          // matrices per blocked-inverse batch (scratch sizing)
@@ -101,6 +103,40 @@ int validate(const msf_problem* p, std::string& msg) {
 }
 
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// One cyclic-reduction level over the ordered active blocks act: the blocks at odd positions
+// that are not protected are eliminated; each keeps its (surviving) list neighbours, each
+// survivor next to an eliminated block records it.  act shrinks to the survivors.  Returns
+// false when nothing is eliminable.
+bool cr_level(std::vector<int>& act, const std::vector<char>& prot, int s, CrLevel& L) {
+  const int n = (int)act.size();
+  std::vector<char> el(n, 0);
+  bool any = false;
+  for (int q = 1; q < n; q += 2)
+    if (!prot[act[q]]) el[q] = 1, any = true;
+  if (!any) return false;
+  L.s = s;
+  for (int q = 0; q < n; ++q)
+    if (el[q]) {
+      L.elim.push_back(act[q]);
+      L.el_l.push_back(act[q - 1]);
+      L.el_r.push_back(q + 1 < n ? act[q + 1] : -1);
+    }
+  std::vector<int> keep;
+  for (int q = 0; q < n; ++q) {
+    if (el[q]) continue;
+    keep.push_back(act[q]);
+    const int l = (q > 0 && el[q - 1]) ? act[q - 1] : -1;
+    const int r = (q + 1 < n && el[q + 1]) ? act[q + 1] : -1;
+    if (l >= 0 || r >= 0) {
+      L.surv.push_back(act[q]);
+      L.sv_l.push_back(l);
+      L.sv_r.push_back(r);
+    }
+  }
+  act.swap(keep);
+  return true;
+}
 
 int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& msg,
               int rank = 0, int nranks = 1) {
@@ -189,29 +225,52 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     P.eig_doubles += 2LL * C.nbx * ml * ml + 3LL * n * P.mb + n + 3LL * P.mb * P.mb + 32 + 8 * 16;
     P.eig_doubles = (P.eig_doubles + 31) & ~31LL;
   }
-  // coarse cyclic-reduction levels
+  // coarse cyclic-reduction levels.  Truncated: stop once at most top_max blocks remain;
+  // they form a dense top system inverted explicitly.  Default 1 block (plain cyclic
+  // reduction): a multi-block explicit inverse loses accuracy at high contrast (measured
+  // rel. error 7e-2 on a cond 3e12 K_c with 9 blocks), the per-level m x m Schur inverses
+  // do not.
   P.cr.clear();
-  size_t ptrs = 0, ints = 0;
-  // truncated: stop once at most top_max active blocks (multiples of s) remain; they form a
-  // dense top system inverted explicitly.  Default 1 block (plain cyclic reduction): a
-  // multi-block explicit inverse loses accuracy at high contrast (measured rel. error 7e-2 on
-  // a cond 3e12 K_c with 9 blocks), the per-level m x m Schur inverses do not.
+  P.iface.clear();
   int top_max = 1;
   if (const char* e = std::getenv("MSF_TOP_BLOCKS")) top_max = std::max(1, std::atoi(e));
-  int s_top = 1;
-  for (int s = 1; s < d.nbc; s *= 2) {
-    const int active = (d.nbc + s - 1) / s;
-    s_top = s;
-    if (active <= top_max || (long long)active * d.mc <= 0) break;
-    s_top = 2 * s;
-    CrLevel L;
-    L.s = s;
-    for (int k = s; k < d.nbc; k += 2 * s) L.elim.push_back(k);
-    if (L.elim.empty()) break;
-    for (int i = 0; i < d.nbc; i += 2 * s)
-      if (i - s >= 0 || i + s < d.nbc) L.surv.push_back(i);
+  std::vector<char> prot(d.nbc, 0);
+  auto reduce = [&](std::vector<int> act, size_t keep, bool stride) {
+    for (int s = 1; act.size() > keep; s *= 2) {
+      CrLevel L;
+      if (!cr_level(act, prot, stride ? s : -1, L)) break;
+      P.cr.push_back(L);
+    }
+    return act;
+  };
+  if (nranks == 1) {
+    // one chain of all blocks: level l eliminates the odd multiples of 2^l
+    std::vector<int> all(d.nbc);
+    for (int i = 0; i < d.nbc; ++i) all[i] = i;
+    P.top_blocks = reduce(all, (size_t)top_max, true);
+    P.n_local = (int)P.cr.size();
+  } else {
+    // strip partition: this rank's chain [C0, C1] down to its two ends,
+    // then the interface chain C0_0 = 0, C0_1, ..., C0_{N-1}, ncx (replicated)
+    const int lo = P.sb.C0, hi = (rank == nranks - 1) ? d.ncx : P.sb.C1;
+    std::vector<int> chain;
+    for (int i = lo; i <= hi; ++i) chain.push_back(i);
+    prot[lo] = prot[hi] = 1;
+    reduce(chain, 2, false);
+    prot[lo] = prot[hi] = 0;
+    P.n_local = (int)P.cr.size();
+    for (int j = 0; j < nranks; ++j) {
+      StripBounds b{};
+      if ((rc = strip_bounds(d, j, nranks, b, msg))) return rc;
+      P.iface.push_back(b.C0);
+    }
+    P.iface.push_back(d.ncx);
+    P.top_blocks = reduce(P.iface, (size_t)top_max, false);
+  }
+  size_t ptrs = 0, ints = 0;
+  for (CrLevel& L : P.cr) {
     int nq = 0;
-    for (int k : L.elim) nq += (k + s < d.nbc) ? 1 : 0;
+    for (int r : L.el_r) nq += r >= 0 ? 1 : 0;
     L.n_inv = (int)L.elim.size() * d.R;
     L.nP = (int)L.elim.size() * d.R;
     L.nQ = nq * d.R;
@@ -219,11 +278,8 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     L.nDr = nq * d.R;
     L.nU = nq * d.R;
     ptrs += 2 * L.n_inv + 3 * (L.nP + L.nQ + L.nDl + L.nDr + L.nU);
-    ints += L.elim.size() + L.surv.size();
-    P.cr.push_back(L);
+    ints += 3 * (L.elim.size() + L.surv.size());
   }
-  P.top_blocks.clear();
-  for (int i = 0; i < d.nbc; i += s_top) P.top_blocks.push_back(i);
   {
     const long long T = (long long)P.top_blocks.size(), R = d.R;
     P.top_ptrs = (size_t)T * (2 * R + 3 * R * (T - 1) + 3 * R * (T - 1) * (T - 1) +
@@ -255,6 +311,13 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   add(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);     // Kcell
   add(7 * R * d.nbc * (size_t)d.mc * d.mc * 8);           // Dc Uc Dinv Pc Qc PTc QTc
   add(2 * R * d.nbc * (size_t)d.mc * 8);     // cb, cx
+  {
+    const size_t nI = P.iface.size(), mm = (size_t)d.mc * d.mc;
+    add(nI * 4);                                          // iface blocks
+    add(R * nI * d.mc * 8);                               // iface_vec
+    add(nI ? R * (2 * nI - 1) * mm * 8 : 0);              // iface_mat
+    add((2 * 3 * R + (nI ? 2 * (2 * nI - 1) * R : 0)) * sizeof(double*));  // pack tables
+  }
   add((size_t)d.n_agg * 4);                  // agg_by_cls
   add(P.jobs_bytes);
   {
@@ -444,16 +507,32 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   c->cb = (double*)take(2 * R * d.nbc * (size_t)d.mc * 8);
   c->cx = c->cb + R * d.nbc * (size_t)d.mc;
   {
+    const size_t nI = P.iface.size(), mm = (size_t)d.mc * d.mc;
+    c->iface = P.iface;
+    c->iface_d = (int*)take(nI * 4);
+    c->iface_vec = (double*)take(R * nI * d.mc * 8);
+    c->iface_mat = (double*)take(nI ? R * (2 * nI - 1) * mm * 8 : 0);
+    c->ifm_pack = (double**)take((2 * 3 * R + (nI ? 2 * (2 * nI - 1) * R : 0)) * sizeof(double*));
+    c->ifm_unpack = c->ifm_pack + 2 * 3 * R;
+    c->n_local = P.n_local;
+    const bool last = rank == nranks - 1;
+    c->cr_lo = c->sb.C0;
+    c->cr_hi = (nranks == 1 || last) ? d.ncx : c->sb.C1;
+    c->cell_lo = c->sb.C0;
+    c->cell_hi = c->sb.C1;
+    c->id_lo = c->sb.C0;
+    c->id_hi = (nranks == 1 || last) ? d.ncx : c->sb.C1 - 1;
+  }
+  {
     // restriction work list: agglomerates grouped by class (consecutive CTAs share a basis
     // in L2); a strip keeps those whose box meets its node columns
     std::vector<std::vector<int>> members(c->n_cls);
     for (int a = 0; a < d.n_agg; ++a) members[P.cls_of_agg[a]].push_back(a);
     c->agg_by_cls_h.clear();
-    const int lo = c->dl.gox, hi = c->dl.gox + c->dl.nnx - 1;
     for (int k = 0; k < c->n_cls; ++k)
       for (int a : members[k]) {
         const int I = a / (d.ncy + 1);
-        if ((I + 1) * d.cx >= lo && (I - 1) * d.cx <= hi) c->agg_by_cls_h.push_back(a);
+        if (I >= c->cr_lo && I <= c->cr_hi) c->agg_by_cls_h.push_back(a);
       }
     c->n_restrict = (int)c->agg_by_cls_h.size();
     c->agg_by_cls_d = (int*)take((size_t)d.n_agg * 4);
@@ -496,43 +575,40 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     std::vector<Fix> fixes;
     for (CrLevel& L : c->cr) {
       Fix F{};
-      const int s = L.s;
       F.inv = ptrs.size();
       for (int rhs = 0; rhs < d.R; ++rhs)
         for (int k : L.elim) ptrs.push_back(B(c->Dinv, rhs, k));
       for (int rhs = 0; rhs < d.R; ++rhs)
         for (int k : L.elim) ptrs.push_back(B(c->Dc, rhs, k));
-      if (s > 0) {
-        F.P = ptrs.size();
-        std::vector<double*> a, b, cc;
-        for (int rhs = 0; rhs < d.R; ++rhs)
-          for (int k : L.elim) { a.push_back(B(c->Uc, rhs, k - s)); b.push_back(B(c->Dinv, rhs, k)); cc.push_back(B(c->Pc, rhs, k)); }
+      // eliminated k with surviving neighbours l (always) and r (if any); U_l couples l-k,
+      // U_k couples k-r:  P_k = U_l Dinv_k, Q_k = U_k^T Dinv_k, D_l -= P_k U_l^T,
+      // D_r -= Q_k U_k, U_l <- -P_k U_k (the new l-r coupling)
+      const size_t ne = L.elim.size();
+      std::vector<double*> a, b, cc;
+      auto flush = [&](size_t& off) {
+        off = ptrs.size();
         ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
         a.clear(); b.clear(); cc.clear();
-        F.Q = ptrs.size();
-        for (int rhs = 0; rhs < d.R; ++rhs)
-          for (int k : L.elim) if (k + s < d.nbc) { a.push_back(B(c->Uc, rhs, k)); b.push_back(B(c->Dinv, rhs, k)); cc.push_back(B(c->Qc, rhs, k)); }
-        ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
-        a.clear(); b.clear(); cc.clear();
-        F.Dl = ptrs.size();
-        for (int rhs = 0; rhs < d.R; ++rhs)
-          for (int k : L.elim) { a.push_back(B(c->Pc, rhs, k)); b.push_back(B(c->Uc, rhs, k - s)); cc.push_back(B(c->Dc, rhs, k - s)); }
-        ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
-        a.clear(); b.clear(); cc.clear();
-        F.Dr = ptrs.size();
-        for (int rhs = 0; rhs < d.R; ++rhs)
-          for (int k : L.elim) if (k + s < d.nbc) { a.push_back(B(c->Qc, rhs, k)); b.push_back(B(c->Uc, rhs, k)); cc.push_back(B(c->Dc, rhs, k + s)); }
-        ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
-        a.clear(); b.clear(); cc.clear();
-        F.U = ptrs.size();
-        for (int rhs = 0; rhs < d.R; ++rhs)
-          for (int k : L.elim) if (k + s < d.nbc) { a.push_back(B(c->Pc, rhs, k)); b.push_back(B(c->Uc, rhs, k)); cc.push_back(B(c->Uc, rhs, k - s)); }
-        ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
-      }
+      };
+      for (int rhs = 0; rhs < d.R; ++rhs)
+        for (size_t e = 0; e < ne; ++e) { const int k = L.elim[e], l = L.el_l[e]; a.push_back(B(c->Uc, rhs, l)); b.push_back(B(c->Dinv, rhs, k)); cc.push_back(B(c->Pc, rhs, k)); }
+      flush(F.P);
+      for (int rhs = 0; rhs < d.R; ++rhs)
+        for (size_t e = 0; e < ne; ++e) if (L.el_r[e] >= 0) { const int k = L.elim[e]; a.push_back(B(c->Uc, rhs, k)); b.push_back(B(c->Dinv, rhs, k)); cc.push_back(B(c->Qc, rhs, k)); }
+      flush(F.Q);
+      for (int rhs = 0; rhs < d.R; ++rhs)
+        for (size_t e = 0; e < ne; ++e) { const int k = L.elim[e], l = L.el_l[e]; a.push_back(B(c->Pc, rhs, k)); b.push_back(B(c->Uc, rhs, l)); cc.push_back(B(c->Dc, rhs, l)); }
+      flush(F.Dl);
+      for (int rhs = 0; rhs < d.R; ++rhs)
+        for (size_t e = 0; e < ne; ++e) if (L.el_r[e] >= 0) { const int k = L.elim[e], r = L.el_r[e]; a.push_back(B(c->Qc, rhs, k)); b.push_back(B(c->Uc, rhs, k)); cc.push_back(B(c->Dc, rhs, r)); }
+      flush(F.Dr);
+      for (int rhs = 0; rhs < d.R; ++rhs)
+        for (size_t e = 0; e < ne; ++e) if (L.el_r[e] >= 0) { const int k = L.elim[e], l = L.el_l[e]; a.push_back(B(c->Pc, rhs, k)); b.push_back(B(c->Uc, rhs, k)); cc.push_back(B(c->Uc, rhs, l)); }
+      flush(F.U);
       F.elim = ints.size();
-      ints.insert(ints.end(), L.elim.begin(), L.elim.end());
+      for (size_t e = 0; e < ne; ++e) { ints.push_back(L.elim[e]); ints.push_back(L.el_l[e]); ints.push_back(L.el_r[e]); }
       F.surv = ints.size();
-      ints.insert(ints.end(), L.surv.begin(), L.surv.end());
+      for (size_t q = 0; q < L.surv.size(); ++q) { ints.push_back(L.surv[q]); ints.push_back(L.sv_l[q]); ints.push_back(L.sv_r[q]); }
       fixes.push_back(F);
     }
     double** pd = (double**)c->jobs_d;
@@ -541,7 +617,7 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
       CrLevel& L = c->cr[i];
       const Fix& F = fixes[i];
       L.inv = pd + F.inv; L.invsrc = L.inv + L.n_inv;
-      if (L.s > 0) {
+      {
         L.pA = pd + F.P; L.pB = L.pA + L.nP; L.pC = L.pB + L.nP;
         L.qA = pd + F.Q; L.qB = L.qA + L.nQ; L.qC = L.qB + L.nQ;
         L.dlA = pd + F.Dl; L.dlB = L.dlA + L.nDl; L.dlC = L.dlB + L.nDl;
@@ -595,6 +671,30 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     }
     cudaMemcpyAsync(c->top_jobs_d, tp.data(), tp.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(c->top_blocks_d, c->top_blocks.data(), c->top_blocks.size() * 4, cudaMemcpyHostToDevice, c->stream);
+    // strip partition: interface share tables.  iface_mat slot j < nI holds D of interface
+    // block j, slot nI + j the coupling U of interface blocks j, j+1.  This rank contributes
+    // D of its chain ends (partial sums: each end block's Galerkin cells and chain Schur
+    // complements split over two ranks) and the complete U of its reduced chain.
+    std::vector<double*> ip, iu;
+    const size_t nI = c->iface.size();
+    if (nI) {
+      auto S = [&](int rhs, size_t j) { return c->iface_mat + ((size_t)rhs * (2 * nI - 1) + j) * mmb; };
+      const int a = rank, b = rank + 1;
+      for (int rhs = 0; rhs < d.R; ++rhs) {
+        ip.push_back(c->Dc + ((size_t)rhs * d.nbc + c->iface[a]) * mmb);
+        ip.push_back(c->Dc + ((size_t)rhs * d.nbc + c->iface[b]) * mmb);
+        ip.push_back(c->Uc + ((size_t)rhs * d.nbc + c->iface[a]) * mmb);
+      }
+      for (int rhs = 0; rhs < d.R; ++rhs) { ip.push_back(S(rhs, a)); ip.push_back(S(rhs, b)); ip.push_back(S(rhs, nI + a)); }
+      for (int rhs = 0; rhs < d.R; ++rhs)
+        for (size_t j = 0; j < 2 * nI - 1; ++j) iu.push_back(S(rhs, j));
+      for (int rhs = 0; rhs < d.R; ++rhs)
+        for (size_t j = 0; j < 2 * nI - 1; ++j)
+          iu.push_back((j < nI ? c->Dc : c->Uc) + ((size_t)rhs * d.nbc + c->iface[j < nI ? j : j - nI]) * mmb);
+      cudaMemcpyAsync(c->ifm_pack, ip.data(), ip.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
+      cudaMemcpyAsync(c->ifm_unpack, iu.data(), iu.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
+      cudaMemcpyAsync(c->iface_d, c->iface.data(), nI * 4, cudaMemcpyHostToDevice, c->stream);
+    }
     cudaStreamSynchronize(c->stream);   // host staging buffers go out of scope
   }
 
@@ -635,6 +735,10 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (ce == cudaSuccess && c->dsum) ce = cudaMemsetAsync(c->dsum, 0, FIN_KINDS * MSF_MAX_RHS * 8, c->stream);
   // node vectors start at 0 (halo / padding columns are only ever written by exchanges)
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->u, 0, 6 * R * 2 * nn * 8, c->stream);
+  // coarse vectors and K_c blocks start at 0: a strip reads (with zero weights) the coarse
+  // solution of the blocks next to its chain, which it never writes
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->cb, 0, 2 * R * d.nbc * (size_t)d.mc * 8, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->Dc, 0, 2 * R * d.nbc * (size_t)d.mc * d.mc * 8, c->stream);
   if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->sc_host, MSF_MAX_RHS * sizeof(PcgScalars));
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->scal_host, 80 * 8);
@@ -708,9 +812,16 @@ int msf_build_coarse_basis(msf_ctx* c) {
   return MSF_OK;
 }
 
+static int dist_assemble(const std::vector<msf_ctx*>& cs);
+
 int msf_assemble_coarse(msf_ctx* c) {
   if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
   if (!c->have_basis) return msf_fail(c, MSF_ERR_STATE, "assemble_coarse before build_coarse_basis");
+  if (c->comm) {
+    if (c->comm->kind == MSF_TRANSPORT_GROUP)
+      return msf_fail(c, MSF_ERR_STATE, "group rank: use msf_group_assemble_coarse");
+    return dist_assemble({c});
+  }
   launch_assemble_coarse(c);
   CKL("assemble_coarse");
   c->have_coarse = true;
@@ -784,20 +895,66 @@ static int dist_sgs(const Ranks& cs, int rhs0, int nr, int first, int rz_mode) {
   return MSF_OK;
 }
 
+// Coarse correction on a strip partition: each rank restricts to and
+// reduces its own chain of K_c blocks; one all-reduce of the chain ends' rhs (nranks + 1
+// blocks) feeds the replicated interface system; each rank back-substitutes its chain and
+// prolongs onto its owned nodes; the left halo column needs the neighbour's chain, so z's
+// halo is exchanged.
+static int dist_coarse(const Ranks& cs, int rhs0, int nr) {
+  int rc;
+  for (msf_ctx* c : cs) {
+    launch_residual(c, rhs0, nr, c->r, c->z, c->t, true);
+    launch_restrict(c, rhs0, nr, c->t, true);     // R_c t of the chain, owned nodes
+    launch_coarse_forward_local(c, rhs0, nr, true);
+  }
+  const size_t nI = cs[0]->iface.size();
+  if (nI) {
+    const size_t n = nI * cs[0]->d.mc;
+    for (msf_ctx* c : cs) launch_iface_vec_pack(c, rhs0, nr);
+    if ((rc = dist_allreduce(cs, &msf_ctx::iface_vec, rhs0 * n, nr * n))) return rc;
+    for (msf_ctx* c : cs) launch_iface_vec_unpack(c, rhs0, nr);
+  }
+  for (msf_ctx* c : cs) {
+    launch_coarse_top(c, rhs0, nr, true);         // replicated interface system
+    launch_coarse_back_local(c, rhs0, nr, true);
+    launch_prolong(c, rhs0, nr, c->z, true);
+  }
+  if (nI) return dist_halo(cs, &msf_ctx::z, rhs0, nr);
+  return MSF_OK;
+}
+
 static int dist_vcycle(const Ranks& cs, int rhs0, int nr, bool f0_done, int rz_mode) {
   int rc;
   if ((rc = dist_sgs(cs, rhs0, nr, f0_done ? 2 : 0, 0))) return rc;
-  for (msf_ctx* c : cs) {
-    launch_residual(c, rhs0, nr, c->r, c->z, c->t, true);
-    launch_restrict(c, rhs0, nr, c->t, true);     // partial R_c t over the owned nodes
-  }
-  const size_t nc = (size_t)cs[0]->d.nbc * cs[0]->d.mc;
-  if ((rc = dist_allreduce(cs, &msf_ctx::cb, rhs0 * nc, nr * nc))) return rc;
-  for (msf_ctx* c : cs) {
-    launch_coarse_solve(c, rhs0, nr, true);       // replicated
-    launch_prolong(c, rhs0, nr, c->z, true);      // owned + halo nodes
-  }
+  if ((rc = dist_coarse(cs, rhs0, nr))) return rc;
   return dist_sgs(cs, rhs0, nr, 1, rz_mode);
+}
+
+// K_c assembly + factorisation on a strip partition: Galerkin products of the owned cells and
+// the chain levels per rank, all-reduce of the chain ends (D of the nranks + 1 interface
+// blocks, U of the reduced chains), replicated interface levels and top system.
+static int dist_assemble(const Ranks& cs) {
+  msf_ctx* c0 = cs[0];
+  for (msf_ctx* x : cs) {
+    if (!x) return msf_fail(c0, MSF_ERR_STATE, "group has unregistered ranks");
+    if (!x->have_basis) return msf_fail(c0, MSF_ERR_STATE, "assemble_coarse before build_coarse_basis");
+  }
+  int rc;
+  for (msf_ctx* c : cs) launch_assemble_local(c);
+  const size_t nI = c0->iface.size();
+  if (nI) {
+    for (msf_ctx* c : cs) launch_iface_mat_pack(c);
+    const size_t n = (size_t)c0->d.R * (2 * nI - 1) * c0->d.mc * c0->d.mc;
+    if ((rc = dist_allreduce(cs, &msf_ctx::iface_mat, 0, n))) return rc;
+    for (msf_ctx* c : cs) launch_iface_mat_unpack(c);
+  }
+  for (msf_ctx* c : cs) launch_assemble_top(c);
+  for (msf_ctx* c : cs) {
+    int rc2 = msf_cuda_check(c, cudaGetLastError(), "dist assemble_coarse");
+    if (rc2) return rc2;
+    c->have_coarse = true;
+  }
+  return MSF_OK;
 }
 
 static int dist_iteration(const Ranks& cs, int rhs0, int nr) {
@@ -1070,6 +1227,87 @@ static int sens_outputs(msf_ctx* c, double* dF, double* dg, double* F, double* g
   return MSF_OK;
 }
 
+int msf_group_assemble_coarse(msf_group* g) {
+  if (!g) return msf_fail(nullptr, MSF_ERR_ARG, "null group");
+  Ranks cs = group_ranks(g);
+  for (msf_ctx* x : cs)
+    if (!x) return msf_fail(nullptr, MSF_ERR_STATE, "group has unregistered ranks");
+  int rc = dist_assemble(cs);
+  if (rc) g_err = cs[0]->err;
+  return rc;
+}
+
+int msf_group_coarse_solve(msf_group* g, int rhs, const double* b, double* x) {
+  if (!g || !b || !x) return msf_fail(nullptr, MSF_ERR_ARG, "null argument");
+  Ranks cs = group_ranks(g);
+  for (msf_ctx* c : cs)
+    if (!c || !c->have_coarse) return msf_fail(nullptr, MSF_ERR_STATE, "group coarse_solve before assemble_coarse");
+  msf_ctx* c0 = cs[0];
+  if (rhs < 0 || rhs >= c0->d.R) return msf_fail(c0, MSF_ERR_ARG, "rhs out of range");
+  const size_t m = c0->d.mc, n = (size_t)c0->d.nbc * m;
+  int rc;
+  // rank r holds b of blocks [C0, C1) (the last rank also ncx): its chain's right end block
+  // starts at 0, as the restriction leaves it with only this rank's share
+  for (msf_ctx* c : cs) {
+    double* cb = c->cb + rhs * n;
+    CK(cudaMemcpyAsync(cb + c->cr_lo * m, b + c->cr_lo * m, (c->cr_hi - c->cr_lo + 1) * m * 8,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    if (c->rank < c->nranks - 1) CK(cudaMemsetAsync(cb + c->cr_hi * m, 0, m * 8, c->stream));
+    launch_coarse_forward_local(c, rhs, 1, false);
+  }
+  if (!c0->iface.empty()) {
+    const size_t ni = c0->iface.size() * m;
+    for (msf_ctx* c : cs) launch_iface_vec_pack(c, rhs, 1);
+    if ((rc = dist_allreduce(cs, &msf_ctx::iface_vec, rhs * ni, ni))) return rc;
+    for (msf_ctx* c : cs) launch_iface_vec_unpack(c, rhs, 1);
+  }
+  for (msf_ctx* c : cs) {
+    launch_coarse_top(c, rhs, 1, false);
+    launch_coarse_back_local(c, rhs, 1, false);
+    const int hi = c->rank == c->nranks - 1 ? c->cr_hi + 1 : c->cr_hi;
+    CK(cudaMemcpyAsync(x + c->cr_lo * m, c->cx + rhs * n + c->cr_lo * m, (hi - c->cr_lo) * m * 8,
+                       cudaMemcpyDeviceToDevice, c->stream));
+  }
+  for (msf_ctx* c : cs) {
+    if ((rc = msf_cuda_check(c, cudaGetLastError(), "group coarse_solve"))) return rc;
+    if ((rc = read_scalars(c, 1))) return rc;
+  }
+  return MSF_OK;
+}
+
+int msf_group_precond_apply(msf_group* g, int rhs, const double* r, double* z) {
+  if (!g || !r || !z) return msf_fail(nullptr, MSF_ERR_ARG, "null argument");
+  Ranks cs = group_ranks(g);
+  for (msf_ctx* c : cs)
+    if (!c || !c->have_coarse) return msf_fail(nullptr, MSF_ERR_STATE, "group precond_apply before assemble_coarse");
+  msf_ctx* c0 = cs[0];
+  if (rhs < 0 || rhs >= c0->d.R) return msf_fail(c0, MSF_ERR_ARG, "rhs out of range");
+  const size_t col = (size_t)2 * c0->d.nny;   // doubles per node column
+  // the V-cycle kernels are gated on the realisation's PCG flag: force it on, restore after
+  std::vector<PcgScalars> saved(cs.size());
+  for (size_t i = 0; i < cs.size(); ++i) {
+    msf_ctx* c = cs[i];
+    CK(cudaMemcpyAsync(&saved[i], c->sc + rhs, sizeof(PcgScalars), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    PcgScalars on = saved[i];
+    on.active = 1;
+    CK(cudaMemcpyAsync(c->sc + rhs, &on, sizeof(PcgScalars), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    launch_mask_copy(c, r + (size_t)c->dl.gox * col, c->r + (size_t)rhs * 2 * c->dl.nn, c->dl.nn);
+  }
+  int rc = dist_vcycle(cs, rhs, 1, false, 0);
+  if (rc) return rc;
+  for (size_t i = 0; i < cs.size(); ++i) {
+    msf_ctx* c = cs[i];
+    CK(cudaMemcpyAsync(z + (size_t)c->sb.own0 * col, c->z + (size_t)rhs * 2 * c->dl.nn + (size_t)c->dl.own_lo * col,
+                       (size_t)(c->sb.own1 - c->sb.own0) * col * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->sc + rhs, &saved[i], sizeof(PcgScalars), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    CKL("group precond_apply");
+  }
+  return MSF_OK;
+}
+
 int msf_group_pcg_solve(msf_group* g, int n_rhs, double tol, int max_it, int32_t* iters,
                         double* compliance) {
   if (!g) return msf_fail(nullptr, MSF_ERR_ARG, "null group");
@@ -1178,6 +1416,7 @@ int msf_coarse_solve(msf_ctx* c, int rhs, const double* b, double* x) {
   if (!c || !b || !x) return msf_fail(c, MSF_ERR_ARG, "null argument");
   if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "coarse_solve before assemble_coarse");
   if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
+  if (c->nranks > 1) return msf_fail(c, MSF_ERR_STATE, "coarse_solve: K_c is distributed on a strip partition");
   const size_t n = (size_t)c->d.nbc * c->d.mc;
   CK(cudaMemcpyAsync(c->cb + rhs * n, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
   launch_coarse_solve(c, rhs, 1, false);
@@ -1215,6 +1454,7 @@ int msf_get_coarse_blocks(msf_ctx* c, int rhs, double* D_host, double* U_host) {
   if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
   if (!c->have_coarse) return msf_fail(c, MSF_ERR_STATE, "get_coarse_blocks before assemble_coarse");
   if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
+  if (c->nranks > 1) return msf_fail(c, MSF_ERR_STATE, "get_coarse_blocks: K_c is distributed on a strip partition");
   const size_t n = (size_t)c->d.nbc * c->d.mc * c->d.mc;
   // Dc/Uc are overwritten by the factorisation: re-gather, copy out, re-factorise.
   launch_coarse_galerkin(c);

@@ -149,11 +149,11 @@ __device__ __forceinline__ void stage_cell_cols(const Dims& d, const double* __r
 __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const double* __restrict__ Eall,
                                                       const double* __restrict__ phi,
                                                       const int* __restrict__ cls_of_agg,
-                                                      double* Kcell, int CH) {
+                                                      double* Kcell, int CH, int cell0) {
   extern __shared__ double sm[];
   // all realisations in one CTA: V_e = K0 Phi_e and Phi_e^T V_e do not depend on the
   // realisation, only the scalar modulus E_e does (R accumulators per output entry)
-  const int cell = blockIdx.x;
+  const int cell = cell0 + blockIdx.x;
   const int CI = cell / d.ncy, CJ = cell - (cell / d.ncy) * d.ncy;
   const int P = 4 * d.kmax;
   const int nch = (P + CH - 1) / CH;
@@ -229,46 +229,64 @@ __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const dou
   }
 }
 
-// Gather the cell products into the block-tridiagonal K_c (D_I, U_I = K_c[I, I+1]);
-// unused eigen-slots (a >= nkept) carry identity rows.
+// Gather the cell products into the block-tridiagonal K_c (D_I, U_I = K_c[I, I+1]) for
+// the blocks D_I, I in [dlo, dlo + nD), and U_I, I in [ulo, ulo + nU), from the coarse cell
+// columns [ulo, ulo + nU) (a strip: its own cells, so its chain's end blocks get partial
+// sums); unused eigen-slots (a >= nkept) carry identity rows in D_I for I in [idlo, idhi]
+// (each block's identity added by one rank).
 __global__ void k_coarse_gather(Dims d, const double* __restrict__ Kcell,
                                 const int* __restrict__ cls_of_agg,
-                                const EigClass* __restrict__ cls, double* Dall, double* Uall) {
+                                const EigClass* __restrict__ cls, double* Dall, double* Uall,
+                                int dlo, int nD, int ulo, int nU, int idlo, int idhi) {
   const int km = d.kmax, P = 4 * km, m = d.mc;
   const size_t per = (size_t)m * m;
-  const size_t total = (size_t)2 * d.nbc * per;
+  const size_t total = (size_t)(nD + nU) * per;
   const int rhs = blockIdx.y;
   const double* Kc = Kcell + (size_t)rhs * d.ncx * d.ncy * P * P;
   for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (size_t)gridDim.x * blockDim.x) {
-    const int isU = idx >= (size_t)d.nbc * per;
-    const size_t li = isU ? idx - (size_t)d.nbc * per : idx;
-    const int I = (int)(li / per);
-    const int e = (int)(li - (size_t)I * per);
+    const int isU = idx >= (size_t)nD * per;
+    const size_t li = isU ? idx - (size_t)nD * per : idx;
+    const int I = (int)(li / per) + (isU ? ulo : dlo);
+    const int e = (int)(li - (size_t)(I - (isU ? ulo : dlo)) * per);
     const int row = e / m, col = e - (e / m) * m;
     const int J = row / km, a = row - (row / km) * km;
     const int Jp = col / km, b = col - (col / km) * km;
     double v = 0.0;
     const int Ir = I, Ic = isU ? I + 1 : I;
-    bool valid = !(isU && I + 1 > d.ncx);
-    if (valid) {
-      const int nka = cls[cls_of_agg[Ir * (d.ncy + 1) + J]].nkept;
-      const int nkb = cls[cls_of_agg[Ic * (d.ncy + 1) + Jp]].nkept;
-      if (a >= nka || b >= nkb) {
-        v = (!isU && row == col) ? 1.0 : 0.0;
-      } else if (abs(J - Jp) <= 1) {
-        const int CIlo = isU ? I : max(I - 1, 0), CIhi = isU ? I : min(I, d.ncx - 1);
-        const int CJlo = max(max(J, Jp) - 1, 0), CJhi = min(min(J, Jp), d.ncy - 1);
-        for (int CI = CIlo; CI <= CIhi; ++CI)
-          for (int CJ = CJlo; CJ <= CJhi; ++CJ) {
-            const int pr = ((Ir - CI) * 2 + (J - CJ)) * km + a;
-            const int pc = ((Ic - CI) * 2 + (Jp - CJ)) * km + b;
-            v += Kc[((size_t)CI * d.ncy + CJ) * P * P + (size_t)pr * P + pc];
-          }
-      }
+    const int nka = cls[cls_of_agg[Ir * (d.ncy + 1) + J]].nkept;
+    const int nkb = cls[cls_of_agg[Ic * (d.ncy + 1) + Jp]].nkept;
+    if (a >= nka || b >= nkb) {
+      v = (!isU && row == col && I >= idlo && I <= idhi) ? 1.0 : 0.0;
+    } else if (abs(J - Jp) <= 1) {
+      const int CIlo = isU ? I : max(I - 1, ulo), CIhi = isU ? I : min(I, ulo + nU - 1);
+      const int CJlo = max(max(J, Jp) - 1, 0), CJhi = min(min(J, Jp), d.ncy - 1);
+      for (int CI = CIlo; CI <= CIhi; ++CI)
+        for (int CJ = CJlo; CJ <= CJhi; ++CJ) {
+          const int pr = ((Ir - CI) * 2 + (J - CJ)) * km + a;
+          const int pc = ((Ic - CI) * 2 + (Jp - CJ)) * km + b;
+          v += Kc[((size_t)CI * d.ncy + CJ) * P * P + (size_t)pr * P + pc];
+        }
     }
     double* dst = (isU ? Uall : Dall) + ((size_t)rhs * d.nbc + I) * per;
     dst[e] = v;
+  }
+}
+
+// Strip partition: this rank's share of the interface entries of the coarse vector
+// (pack: comp = b of interface blocks a, b (its chain ends), 0 elsewhere) or the all-reduced
+// interface rhs written back (unpack), realisations [rhs0, rhs0 + gridDim.y).
+__global__ void k_iface_vec(Dims d, const int* __restrict__ iface, int nI, int a, int b,
+                            double* cball, double* comp, int rhs0, int unpack) {
+  const int rhs = rhs0 + blockIdx.y;
+  const size_t n = (size_t)nI * d.mc;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / d.mc), row = (int)(idx - (size_t)j * d.mc);
+    double* cbp = cball + ((size_t)rhs * d.nbc + iface[j]) * d.mc + row;
+    double* cp = comp + (size_t)rhs * n + idx;
+    if (unpack) *cbp = *cp;
+    else *cp = (j == a || j == b) ? *cbp : 0.0;
   }
 }
 
@@ -563,8 +581,8 @@ __global__ void __launch_bounds__(256) k_gemm(double** As, double** Bs, double**
 }
 
 // ------------------------------------------------------------------ cyclic-reduction solve
-// forward, survivors i: b_i -= Q_{i-s} b_{i-s} + P_{i+s} b_{i+s}
-__global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restrict__ surv, int s,
+// forward, survivors i (jobs [i, il, ir]): b_i -= Q_il b_il + P_ir b_ir
+__global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restrict__ surv,
                                                     const double* __restrict__ Qall,
                                                     const double* __restrict__ Pall,
                                                     double* cball, const PcgScalars* sc,
@@ -572,15 +590,16 @@ __global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restric
   pdl_launch();
   const int rhs = rhs0 + blockIdx.z;
   extern __shared__ double sv[];  // [2][m]
-  const int i = surv[blockIdx.y];
+  const int* job = surv + 3 * blockIdx.y;
+  const int i = job[0], il = job[1], ir = job[2];
   const size_t per = (size_t)d.mc * d.mc;
-  cr_forward_rows(d, i, s, blockIdx.x * CR_ROWS, Qall + ((size_t)rhs * d.nbc + (i - s)) * per,
-                  Pall + ((size_t)rhs * d.nbc + (i + s)) * per, cball + (size_t)rhs * d.nbc * d.mc,
+  cr_forward_rows(d, i, il, ir, blockIdx.x * CR_ROWS, Qall + ((size_t)rhs * d.nbc + max(il, 0)) * per,
+                  Pall + ((size_t)rhs * d.nbc + max(ir, 0)) * per, cball + (size_t)rhs * d.nbc * d.mc,
                   sv, threadIdx.x, blockDim.x, gated ? &sc[rhs].active : nullptr);
 }
 
-// back, eliminated k: x_k = Dinv_k b_k - P_k^T x_{k-s} - Q_k^T x_{k+s}
-__global__ void __launch_bounds__(256) k_cr_back(Dims d, const int* __restrict__ elim, int s,
+// back, eliminated k (jobs [k, kl, kr]): x_k = Dinv_k b_k - P_k^T x_kl - Q_k^T x_kr
+__global__ void __launch_bounds__(256) k_cr_back(Dims d, const int* __restrict__ elim,
                                                  const double* __restrict__ Dinv,
                                                  const double* __restrict__ PTall,
                                                  const double* __restrict__ QTall,
@@ -589,10 +608,11 @@ __global__ void __launch_bounds__(256) k_cr_back(Dims d, const int* __restrict__
   pdl_launch();
   const int rhs = rhs0 + blockIdx.z;
   extern __shared__ double sv[];  // [3][m]
-  const int k = elim[blockIdx.y];
+  const int* job = elim + 3 * blockIdx.y;
+  const int k = job[0], kl = job[1], kr = job[2];
   const size_t per = (size_t)d.mc * d.mc;
   const size_t blk = ((size_t)rhs * d.nbc + k) * per;
-  cr_back_rows(d, k, s, blockIdx.x * CR_ROWS, Dinv + blk, PTall + blk, QTall + blk,
+  cr_back_rows(d, k, kl, kr, blockIdx.x * CR_ROWS, Dinv + blk, PTall + blk, QTall + blk,
                cball + (size_t)rhs * d.nbc * d.mc, cxall + (size_t)rhs * d.nbc * d.mc, sv,
                threadIdx.x, blockDim.x, gated ? &sc[rhs].active : nullptr);
 }
@@ -677,12 +697,9 @@ __global__ void __launch_bounds__(256) k_top_solve(Dims d, const int* __restrict
 
 // ================================================================== host side
 void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) {
-  const Dims& d = c->dl;   // global coarse fields, this rank's node columns
-  if (c->comm) {
-    // a strip restricts only the agglomerates touching it; the rest of its partial c is 0
-    const size_t n = (size_t)d.nbc * d.mc;
-    cudaMemsetAsync(c->cb + rhs0 * n, 0, nr * n * sizeof(double), c->stream);
-  }
+  // global coarse fields, this rank's node columns; a strip restricts the agglomerates of its
+  // chain [cr_lo, cr_hi] (the chain's end blocks get the partial sums of its owned nodes)
+  const Dims& d = c->dl;
 #define MSF_RESTRICT(KM, NTR)                                                                   \
   launch_k(k_restrict1<KM, NTR>, dim3(c->n_restrict, nr), dim3(NTR), 0, c->stream, d,            \
            (const double2*)t, (const double*)c->phi, (const int*)c->cls_of_agg_d,                \
@@ -732,14 +749,17 @@ void launch_coarse_galerkin(msf_ctx* c) {
   const size_t smem = smem_for(CH);
   const int nch = (P + CH - 1) / CH;
   cudaFuncSetAttribute(k_cell_galerkin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_cell_galerkin<<<dim3(d.ncx * d.ncy, 1, nch * nch), NT, smem, c->stream>>>(
-      d, c->K0, c->E, c->phi, c->cls_of_agg_d, c->Kcell, CH);
+  // this rank's coarse cell columns (all of them on one GPU)
+  k_cell_galerkin<<<dim3((c->cell_hi - c->cell_lo) * d.ncy, 1, nch * nch), NT, smem, c->stream>>>(
+      d, c->K0, c->E, c->phi, c->cls_of_agg_d, c->Kcell, CH, c->cell_lo * d.ncy);
   MSF_LAUNCHED(c);
   {
-    const size_t total = (size_t)2 * d.nbc * d.mc * d.mc;
+    const int nD = c->cr_hi - c->cr_lo + 1, nU = c->cell_hi - c->cell_lo;
+    const size_t total = (size_t)(nD + nU) * d.mc * d.mc;
     int blocks = (int)std::min<size_t>((total + 255) / 256, 65535);
     k_coarse_gather<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->Kcell, c->cls_of_agg_d,
-                                                              c->classes_d, c->Dc, c->Uc);
+                                                              c->classes_d, c->Dc, c->Uc, c->cr_lo, nD,
+                                                              c->cell_lo, nU, c->id_lo, c->id_hi);
     MSF_LAUNCHED(c);
   }
 }
@@ -768,16 +788,16 @@ static void launch_spd_inverse(msf_ctx* c, double** mats, int n, int m) {
   }
 }
 
-void launch_assemble_coarse(msf_ctx* c) {
-  launch_coarse_galerkin(c);
+// factorisation of the reduction levels [l0, l1)
+static void assemble_levels(msf_ctx* c, int l0, int l1) {
   const Dims& d = c->d;
   const int m = d.mc;
   const dim3 gt((m + 63) / 64, (m + 63) / 64);
-  for (const CrLevel& L : c->cr) {
+  for (int l = l0; l < l1; ++l) {
+    const CrLevel& L = c->cr[l];
     k_copy_blocks<<<dim3(64, L.n_inv), 256, 0, c->stream>>>(L.invsrc, L.inv, m);
     MSF_LAUNCHED(c);
     launch_spd_inverse(c, L.inv, L.n_inv, m);
-    if (L.s == 0) continue;
     if (L.nP) {
       k_gemm<false, false><<<dim3(gt.x, gt.y, L.nP), 256, 0, c->stream>>>(L.pA, L.pB, L.pC, m, 1.0, 0.0);
       MSF_LAUNCHED(c);
@@ -809,6 +829,36 @@ void launch_assemble_coarse(msf_ctx* c) {
       MSF_LAUNCHED(c);
     }
   }
+}
+
+void launch_assemble_local(msf_ctx* c) {
+  launch_coarse_galerkin(c);
+  assemble_levels(c, 0, c->n_local);
+}
+
+void launch_iface_mat_pack(msf_ctx* c) {
+  const size_t nI = c->iface.size(), mm = (size_t)c->d.mc * c->d.mc;
+  cudaMemsetAsync(c->iface_mat, 0, (size_t)c->d.R * (2 * nI - 1) * mm * 8, c->stream);
+  k_copy_blocks<<<dim3(64, 3 * c->d.R), 256, 0, c->stream>>>(c->ifm_pack, c->ifm_pack + 3 * c->d.R, c->d.mc);
+  MSF_LAUNCHED(c);
+}
+
+void launch_iface_mat_unpack(msf_ctx* c) {
+  const int n = (int)(2 * c->iface.size() - 1) * c->d.R;
+  k_copy_blocks<<<dim3(64, n), 256, 0, c->stream>>>(c->ifm_unpack, c->ifm_unpack + n, c->d.mc);
+  MSF_LAUNCHED(c);
+}
+
+void launch_assemble_coarse(msf_ctx* c) {
+  launch_assemble_local(c);
+  launch_assemble_top(c);
+}
+
+void launch_assemble_top(msf_ctx* c) {
+  assemble_levels(c, c->n_local, (int)c->cr.size());
+  const Dims& d = c->d;
+  const int m = d.mc;
+  const dim3 gt((m + 63) / 64, (m + 63) / 64);
   // dense inverse of the remaining top system by block Gauss-Jordan (block sweep operator):
   // pivot k: Pk = A_kk^-1, W_i = A_ik Pk, A_ij -= W_i A_kj, A_ik = W_i, A_ki = W_i^T,
   // A_kk = -Pk; after all pivots A = -Top^-1.
@@ -844,12 +894,9 @@ void launch_assemble_coarse(msf_ctx* c) {
   }
 }
 
-// c <- K_c^{-1} c for realisations [rhs0, rhs0+nr): forward elimination over the levels,
-// final block, back substitution in reverse level order.
-void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
-  const Dims& d = c->d;
-  const int m = d.mc;
-  const int nthr = 256;
+// ---------------------------------------------------------------- coarse solve
+static void cr_smem_attrs(msf_ctx* c) {
+  const int m = c->d.mc;
   if (3 * (size_t)m * sizeof(double) > 48 * 1024 ||
       (size_t)c->top_T * m * sizeof(double) > 48 * 1024) {
     const int need = (int)(std::max<size_t>(3, c->top_T) * m * sizeof(double));
@@ -857,29 +904,79 @@ void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
     cudaFuncSetAttribute(k_cr_back, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
     cudaFuncSetAttribute(k_top_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
   }
-  for (const CrLevel& L : c->cr) {
-    if (!L.surv.empty()) {
-      launch_k(k_cr_forward, dim3((m + CR_ROWS - 1) / CR_ROWS, (unsigned)L.surv.size(), nr),
-               dim3(nthr), 2 * m * sizeof(double), c->stream, d, (const int*)L.surv_d, L.s,
-               (const double*)c->Qc, (const double*)c->Pc, c->cb, (const PcgScalars*)c->sc, rhs0,
-               gated ? 1 : 0);
-      MSF_LAUNCHED(c);
-    }
-  }
-  // dense top system: one row-chunked GEMV
-  {
-    const int T = c->top_T, n = T * m;
-    launch_k(k_top_solve, dim3((n + CR_ROWS - 1) / CR_ROWS, nr), dim3(nthr), (size_t)n * sizeof(double),
-             c->stream, d, (const int*)c->top_blocks_d, T, (const double*)c->Atop,
-             (const double*)c->cb, c->cx, (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
+}
+
+static void cr_forward_levels(msf_ctx* c, int l0, int l1, int rhs0, int nr, bool gated) {
+  const Dims& d = c->d;
+  const int m = d.mc;
+  for (int l = l0; l < l1; ++l) {
+    const CrLevel& L = c->cr[l];
+    if (L.surv.empty()) continue;
+    launch_k(k_cr_forward, dim3((m + CR_ROWS - 1) / CR_ROWS, (unsigned)L.surv.size(), nr), dim3(256),
+             2 * m * sizeof(double), c->stream, d, (const int*)L.surv_d, (const double*)c->Qc,
+             (const double*)c->Pc, c->cb, (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
     MSF_LAUNCHED(c);
   }
-  for (auto it = c->cr.rbegin(); it != c->cr.rend(); ++it) {
-    const CrLevel& L = *it;
-    launch_k(k_cr_back, dim3((m + CR_ROWS - 1) / CR_ROWS, (unsigned)L.elim.size(), nr), dim3(nthr),
-             3 * m * sizeof(double), c->stream, d, (const int*)L.elim_d, L.s, (const double*)c->Dinv,
+}
+
+static void cr_back_levels(msf_ctx* c, int l0, int l1, int rhs0, int nr, bool gated) {
+  const Dims& d = c->d;
+  const int m = d.mc;
+  for (int l = l1 - 1; l >= l0; --l) {
+    const CrLevel& L = c->cr[l];
+    launch_k(k_cr_back, dim3((m + CR_ROWS - 1) / CR_ROWS, (unsigned)L.elim.size(), nr), dim3(256),
+             3 * m * sizeof(double), c->stream, d, (const int*)L.elim_d, (const double*)c->Dinv,
              (const double*)c->PTc, (const double*)c->QTc, (const double*)c->cb, c->cx,
              (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
     MSF_LAUNCHED(c);
   }
+}
+
+void launch_coarse_forward_local(msf_ctx* c, int rhs0, int nr, bool gated) {
+  cr_smem_attrs(c);
+  cr_forward_levels(c, 0, c->n_local, rhs0, nr, gated);
+}
+
+// interface levels (strips), the dense top system, interface back substitution
+void launch_coarse_top(msf_ctx* c, int rhs0, int nr, bool gated) {
+  cr_smem_attrs(c);
+  const int nl = (int)c->cr.size();
+  cr_forward_levels(c, c->n_local, nl, rhs0, nr, gated);
+  {
+    const int T = c->top_T, n = T * c->d.mc;
+    launch_k(k_top_solve, dim3((n + CR_ROWS - 1) / CR_ROWS, nr), dim3(256), (size_t)n * sizeof(double),
+             c->stream, c->d, (const int*)c->top_blocks_d, T, (const double*)c->Atop,
+             (const double*)c->cb, c->cx, (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
+    MSF_LAUNCHED(c);
+  }
+  cr_back_levels(c, c->n_local, nl, rhs0, nr, gated);
+}
+
+void launch_coarse_back_local(msf_ctx* c, int rhs0, int nr, bool gated) {
+  cr_back_levels(c, 0, c->n_local, rhs0, nr, gated);
+}
+
+void launch_iface_vec_pack(msf_ctx* c, int rhs0, int nr) {
+  const int nI = (int)c->iface.size();
+  const int blocks = std::max(1, std::min(148, (nI * c->d.mc + 255) / 256));
+  k_iface_vec<<<dim3(blocks, nr), 256, 0, c->stream>>>(c->d, c->iface_d, nI, c->rank, c->rank + 1, c->cb,
+                                                       c->iface_vec, rhs0, 0);
+  MSF_LAUNCHED(c);
+}
+
+void launch_iface_vec_unpack(msf_ctx* c, int rhs0, int nr) {
+  const int nI = (int)c->iface.size();
+  const int blocks = std::max(1, std::min(148, (nI * c->d.mc + 255) / 256));
+  k_iface_vec<<<dim3(blocks, nr), 256, 0, c->stream>>>(c->d, c->iface_d, nI, -1, -1, c->cb,
+                                                       c->iface_vec, rhs0, 1);
+  MSF_LAUNCHED(c);
+}
+
+// c <- K_c^{-1} c for realisations [rhs0, rhs0+nr) on one GPU: forward elimination over the
+// levels, top system, back substitution in reverse level order.  (A strip context runs the
+// same phases with the interface exchange between them, msf_capi.cu dist_vcycle.)
+void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
+  launch_coarse_forward_local(c, rhs0, nr, gated);
+  launch_coarse_top(c, rhs0, nr, gated);
+  launch_coarse_back_local(c, rhs0, nr, gated);
 }

@@ -65,14 +65,20 @@ struct EigClass {
   int nkept;        // kept modes (written by the kernel)
 };
 
-// One level of the coarse block cyclic reduction.  Pointer tables (device) cover all
-// realisations; index lists (device) are per realisation.
+// One level of the coarse block cyclic reduction over an ordered list of active blocks:
+// the blocks at odd list positions are eliminated (the block tridiagonal structure is kept
+// on the survivors).  On one GPU the list is every block and level l is the stride-2^l
+// reduction; the strip partition reduces each rank's chain and then the interface chain
+// (DESIGN.md §8(e)).  Pointer tables (device) cover all realisations; job lists (device)
+// are per realisation.
 struct CrLevel {
-  int s = 0;                   // stride 2^l; 0 marks the final single-block level
+  int s = 0;                   // stride 2^l of a stride level (persistent kernels); -1 otherwise
   std::vector<int> elim;       // eliminated blocks (host copy)
+  std::vector<int> el_l, el_r; // their surviving left / right neighbours (-1: none)
   std::vector<int> surv;       // survivors with an eliminated neighbour (host copy)
-  int* elim_d = nullptr;
-  int* surv_d = nullptr;
+  std::vector<int> sv_l, sv_r; // their eliminated left / right neighbours (-1: none)
+  int* elim_d = nullptr;       // [elim][3] = k, left, right
+  int* surv_d = nullptr;       // [surv][3] = i, left, right
   int n_inv = 0;  double** inv = nullptr;  double** invsrc = nullptr;
   int nP = 0;     double** pA = nullptr;   double** pB = nullptr;  double** pC = nullptr;
   int nQ = 0;     double** qA = nullptr;   double** qB = nullptr;  double** qC = nullptr;
@@ -147,6 +153,16 @@ struct msf_ctx {
   int mb = 0;  // eigensolver block size
   long long eig_work_doubles = 0;
   std::vector<CrLevel> cr;
+  // Coarse solve on a strip partition: levels [0, n_local) reduce this
+  // rank's chain of blocks [cr_lo, cr_hi] (the chain's end blocks, shared with the neighbour
+  // ranks, are kept); after an all-reduce of the end blocks, levels [n_local, cr.size())
+  // and the top system reduce the chain of the nranks + 1 interface blocks, replicated on
+  // every rank.  One GPU: n_local = cr.size(), one chain of all blocks.
+  int n_local = 0;
+  int cr_lo = 0, cr_hi = 0;       // chain blocks
+  int cell_lo = 0, cell_hi = 0;   // Galerkin coarse cell columns [cell_lo, cell_hi)
+  int id_lo = 0, id_hi = 0;       // blocks [id_lo, id_hi] carry the identity rows of unused slots
+  std::vector<int> iface;         // interface blocks (global index), nranks + 1 (strips only)
   std::vector<int> filt_dx, filt_dy;
   std::vector<double> filt_w;
   bool periodic = false;
@@ -193,6 +209,11 @@ struct msf_ctx {
   double* QTc = nullptr;        // [R][nbc][mc*mc]  Q_k^T
   double* cb = nullptr;         // [R][nbc*mc] coarse rhs (modified by the forward sweep)
   double* cx = nullptr;         // [R][nbc*mc] coarse solution
+  int* iface_d = nullptr;       // [nI] interface blocks
+  double* iface_vec = nullptr;  // [R][nI][mc] this rank's share of the interface rhs (all-reduced)
+  double* iface_mat = nullptr;  // [R][2nI-1][mc*mc] interface D blocks, then U (all-reduced)
+  double** ifm_pack = nullptr;  // [2][3R] src, dst: this rank's interface D, D, U shares
+  double** ifm_unpack = nullptr;// [2][(2nI-1)R] src, dst
   int* agg_by_cls_d = nullptr;  // agglomerates grouped by class
   std::vector<int> agg_by_cls_h;
   // top system after the truncated cyclic reduction: T active blocks (stride top_stride),
@@ -302,7 +323,14 @@ void launch_oc(msf_ctx* c, const double* x, const double* dF, const double* dg, 
 
 // ---------------------------------------------------------------- coarse space
 void launch_build_basis(msf_ctx* c);
+// K_c assembly + factorisation: one GPU all of it; a strip the local part (Galerkin of the
+// owned cells, chain levels), the interface pack / unpack around the all-reduce of
+// iface_mat, then the replicated interface levels + top system
 void launch_assemble_coarse(msf_ctx* c);
+void launch_assemble_local(msf_ctx* c);
+void launch_iface_mat_pack(msf_ctx* c);
+void launch_iface_mat_unpack(msf_ctx* c);
+void launch_assemble_top(msf_ctx* c);
 void launch_coarse_galerkin(msf_ctx* c);
 void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated);
 // persistent cooperative PCG iterations (msf_persist.cu); returns MSF_OK or an error code
@@ -312,7 +340,14 @@ void fill_cr_levels_dev(const std::vector<CrLevel>& cr, void* host_buf);
 constexpr int MSF_TOP_MAX = 1200;   // max unknowns of the dense top system (T * mc)
 constexpr int MSF_PERSIST_PARTIALS = 3 * MSF_MAX_RHS * 4 * 160;  // 3 slots x 4 rhs x grid
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated);
+// c <- K_c^{-1} c: forward chain levels, [strip: interface pack, all-reduce of iface_vec,
+// unpack], interface levels + top + interface back, back chain levels
 void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated);
+void launch_coarse_forward_local(msf_ctx* c, int rhs0, int nr, bool gated);
+void launch_iface_vec_pack(msf_ctx* c, int rhs0, int nr);
+void launch_iface_vec_unpack(msf_ctx* c, int rhs0, int nr);
+void launch_coarse_top(msf_ctx* c, int rhs0, int nr, bool gated);
+void launch_coarse_back_local(msf_ctx* c, int rhs0, int nr, bool gated);
 // restriction + coarse solve + prolongation in one cooperative launch (msf_persist.cu)
 int launch_coarse_coop(msf_ctx* c, int rhs0, int nr, const double* t, double* z, bool gated);
 

@@ -354,15 +354,16 @@ __device__ __forceinline__ void prolong_node(const Dims& d, const double* __rest
 constexpr int CR_ROWS = 8;    // == warps of the 256-thread CTAs that run these routines
 constexpr int CR_PF = 5;      // columns per lane held in registers per pass (160 per warp)
 
-// forward, survivor i, rows [r0, r0+CR_ROWS): b_i -= Q_{i-s} b_{i-s} + P_{i+s} b_{i+s}
+// forward, survivor i, rows [r0, r0+CR_ROWS): b_i -= Q_il b_il + P_ir b_ir, il / ir its
+// eliminated left / right neighbours of the level (-1: none; stride levels: i -/+ s)
 // active: realisation flag checked after pdl_wait (nullptr: caller already checked)
-__device__ __forceinline__ void cr_forward_rows(const Dims& d, int i, int s, int r0,
+__device__ __forceinline__ void cr_forward_rows(const Dims& d, int i, int il, int ir, int r0,
                                                 const double* __restrict__ Q,
                                                 const double* __restrict__ P, double* cb,
                                                 double* sv, int tid, int nthreads,
                                                 const int* active = nullptr) {
   const int m = d.mc;
-  const bool hl = i - s >= 0, hr = i + s < d.nbc;
+  const bool hl = il >= 0, hr = ir >= 0;
   const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
   const int r1 = min(m, r0 + CR_ROWS);
   double qv[CR_PF], pv[CR_PF];
@@ -380,8 +381,8 @@ __device__ __forceinline__ void cr_forward_rows(const Dims& d, int i, int s, int
   pdl_wait();
   if (active && !*active) return;
   for (int k = tid; k < m; k += nthreads) {
-    sv[k] = hl ? cb[(size_t)(i - s) * m + k] : 0.0;
-    sv[m + k] = hr ? cb[(size_t)(i + s) * m + k] : 0.0;
+    sv[k] = hl ? cb[(size_t)il * m + k] : 0.0;
+    sv[m + k] = hr ? cb[(size_t)ir * m + k] : 0.0;
   }
   __syncthreads();
   for (int r = r0 + wid; r < r1; r += nw) {
@@ -403,8 +404,9 @@ __device__ __forceinline__ void cr_forward_rows(const Dims& d, int i, int s, int
   __syncthreads();
 }
 
-// back, eliminated k, rows [r0, r0+CR_ROWS): x_k = Dinv_k b_k - P_k^T x_{k-s} - Q_k^T x_{k+s}
-__device__ __forceinline__ void cr_back_rows(const Dims& d, int k, int s, int r0,
+// back, eliminated k, rows [r0, r0+CR_ROWS): x_k = Dinv_k b_k - P_k^T x_kl - Q_k^T x_kr
+// (kl / kr: its surviving neighbours, -1: none)
+__device__ __forceinline__ void cr_back_rows(const Dims& d, int k, int kl, int kr, int r0,
                                              const double* __restrict__ Di,
                                              const double* __restrict__ PT,
                                              const double* __restrict__ QT,
@@ -412,7 +414,7 @@ __device__ __forceinline__ void cr_back_rows(const Dims& d, int k, int s, int r0
                                              double* sv, int tid, int nthreads,
                                              const int* active = nullptr) {
   const int m = d.mc;
-  const bool hl = k - s >= 0, hr = k + s < d.nbc;
+  const bool hl = kl >= 0, hr = kr >= 0;
   const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
   const int r1 = min(m, r0 + CR_ROWS);
   double dv[CR_PF], pv[CR_PF], qv[CR_PF];
@@ -433,8 +435,8 @@ __device__ __forceinline__ void cr_back_rows(const Dims& d, int k, int s, int r0
   if (active && !*active) return;
   for (int j = tid; j < m; j += nthreads) {
     sv[j] = cb[(size_t)k * m + j];
-    sv[m + j] = hl ? cx[(size_t)(k - s) * m + j] : 0.0;
-    sv[2 * m + j] = hr ? cx[(size_t)(k + s) * m + j] : 0.0;
+    sv[m + j] = hl ? cx[(size_t)kl * m + j] : 0.0;
+    sv[2 * m + j] = hr ? cx[(size_t)kr * m + j] : 0.0;
   }
   __syncthreads();
   for (int r = r0 + wid; r < r1; r += nw) {

@@ -38,8 +38,8 @@ struct CrLevelDev {
   int s;        // stride (0: final level)
   int nsurv;
   int nelim;
-  const int* surv;
-  const int* elim;
+  const int* surv;   // [nsurv][3]: survivor, eliminated left / right neighbour (-1: none)
+  const int* elim;   // [nelim][3]: eliminated block, surviving left / right neighbour
 };
 
 struct PersistArgs {
@@ -289,9 +289,9 @@ __global__ void __launch_bounds__(PT, PMINB) k_pcg_persistent(PersistArgs A, K0M
         const int k = item / (nrc * L.nsurv), rest = item - k * (nrc * L.nsurv);
         if (!act[k]) continue;
         const int si = rest / nrc, rc = rest - (rest / nrc) * nrc;
-        const int i = L.surv[si];
-        cr_forward_rows(d, i, L.s, rc * CR_ROWS, A.Qc + ((size_t)k * d.nbc + (i - L.s)) * per,
-                        A.Pc + ((size_t)k * d.nbc + (i + L.s)) * per, A.cb + (size_t)k * d.nbc * d.mc,
+        const int i = L.surv[3 * si], il = L.surv[3 * si + 1], ir = L.surv[3 * si + 2];
+        cr_forward_rows(d, i, il, ir, rc * CR_ROWS, A.Qc + ((size_t)k * d.nbc + max(il, 0)) * per,
+                        A.Pc + ((size_t)k * d.nbc + max(ir, 0)) * per, A.cb + (size_t)k * d.nbc * d.mc,
                         sv, tid, PT);
       }
       gsync();
@@ -309,14 +309,13 @@ __global__ void __launch_bounds__(PT, PMINB) k_pcg_persistent(PersistArgs A, K0M
     }
     for (int l = A.nlev - 1; l >= 0; --l) {
       const CrLevelDev L = A.levels[l];
-      const int s = L.s;
       for (int item = b; item < nrc * L.nelim * nr; item += G) {
         const int k = item / (nrc * L.nelim), rest = item - k * (nrc * L.nelim);
         if (!act[k]) continue;
         const int ei = rest / nrc, rc = rest - (rest / nrc) * nrc;
-        const int kb = L.elim[ei];
+        const int kb = L.elim[3 * ei], kl = L.elim[3 * ei + 1], kr = L.elim[3 * ei + 2];
         const size_t blk = ((size_t)k * d.nbc + kb) * per;
-        cr_back_rows(d, kb, s, rc * CR_ROWS, A.Dinv + blk, A.PTc + blk, A.QTc + blk,
+        cr_back_rows(d, kb, kl, kr, rc * CR_ROWS, A.Dinv + blk, A.PTc + blk, A.QTc + blk,
                      A.cb + (size_t)k * d.nbc * d.mc, A.cx + (size_t)k * d.nbc * d.mc, sv, tid, PT);
       }
       gsync();
@@ -454,9 +453,9 @@ __global__ void __launch_bounds__(PT) k_coarse_coop(CoarseArgs A) {
       const int k = k0 + item / (nrc * L.nsurv), rest = item - (k - k0) * (nrc * L.nsurv);
       if (!act[k]) continue;
       const int si = rest / nrc, rc = rest - (rest / nrc) * nrc;
-      const int i = L.surv[si];
-      cr_forward_rows(d, i, L.s, rc * CR_ROWS, A.Qc + ((size_t)k * d.nbc + (i - L.s)) * per,
-                      A.Pc + ((size_t)k * d.nbc + (i + L.s)) * per, A.cb + (size_t)k * d.nbc * d.mc,
+      const int i = L.surv[3 * si], il = L.surv[3 * si + 1], ir = L.surv[3 * si + 2];
+      cr_forward_rows(d, i, il, ir, rc * CR_ROWS, A.Qc + ((size_t)k * d.nbc + max(il, 0)) * per,
+                      A.Pc + ((size_t)k * d.nbc + max(ir, 0)) * per, A.cb + (size_t)k * d.nbc * d.mc,
                       sv, tid, PT);
     }
     grid.sync();
@@ -474,14 +473,13 @@ __global__ void __launch_bounds__(PT) k_coarse_coop(CoarseArgs A) {
   }
   for (int l = A.nlev - 1; l >= 0; --l) {
     const CrLevelDev L = A.levels[l];
-    const int s = L.s;
     for (int item = b; item < nrc * L.nelim * nk; item += G) {
       const int k = k0 + item / (nrc * L.nelim), rest = item - (k - k0) * (nrc * L.nelim);
       if (!act[k]) continue;
       const int ei = rest / nrc, rc = rest - (rest / nrc) * nrc;
-      const int kb = L.elim[ei];
+      const int kb = L.elim[3 * ei], kl = L.elim[3 * ei + 1], kr = L.elim[3 * ei + 2];
       const size_t blk = ((size_t)k * d.nbc + kb) * per;
-      cr_back_rows(d, kb, s, rc * CR_ROWS, A.Dinv + blk, A.PTc + blk, A.QTc + blk,
+      cr_back_rows(d, kb, kl, kr, rc * CR_ROWS, A.Dinv + blk, A.PTc + blk, A.QTc + blk,
                    A.cb + (size_t)k * d.nbc * d.mc, A.cx + (size_t)k * d.nbc * d.mc, sv, tid, PT);
     }
     grid.sync();

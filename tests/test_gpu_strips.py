@@ -3,10 +3,20 @@ into 2-4 strips, each rank a separate C-ABI context; the ranks run in lockstep i
 process on one B200 (MSF_TRANSPORT_GROUP: halos are device copies, all-reduces a
 rank-ordered sum), so the partitioned arithmetic is checked without a second GPU.
 
-Bars: against the oracle exactly those of tests/test_gpu_parity.py (iterations +-1 at
-tol 1e-8, displacement 1e-8, compliance the fp64-attainable bar); against the single-GPU
-CUDA path, which differs only in the summation order of the dot products and of R_c t,
-iterations +-1, displacement 1e-9, compliance 1e-11."""
+The partitioned arithmetic (halo'd smoother, distributed K_c factorisation and coarse
+solve) differs from the single-GPU path only in rounding: the summation
+order of the dot products and of the chain-end blocks shared by two ranks, and, for
+strips not aligned with the cyclic-reduction strides, the elimination order of K_c.  It is
+checked deterministically one level down: the group's coarse solve and V-cycle against the
+single-GPU ones (relative 1e-11 / 1e-12).
+
+Bars of the solves: displacement 1e-8 against the oracle and 1e-9 against the single-GPU
+path, compliance the fp64-attainable bar (tests/test_gpu_parity.py) and 1e-11.  Iteration
+counts: +-2.  The eroded realisation of robust_32x16 (137 iterations on 1,122 DOF) is
+chaotic under rounding: the single-GPU path with the design tile perturbed by 1e-15
+(relative) takes 136 or 137 iterations (40 seeds), two strips 136, 137 or 139 (12 seeds;
+139 for the unperturbed tile), while the two V-cycles agree to 1e-14 (scratch run,
+DESIGN.md §8(e)).  Every other realisation here matches the single-GPU count exactly."""
 import numpy as np
 import pytest
 
@@ -78,8 +88,8 @@ def test_strip_pcg_vs_oracle_and_single(name, nranks):
     its_s, comp_s, _ = m.pcg_solve(tol=1e-8)
     assert not nc
     for k in range(spec.n_rhs):
-        assert abs(its_g[k] - ref["iters"][k]) <= 1, (its_g, ref["iters"])
-        assert abs(its_g[k] - its_s[k]) <= 1, (its_g, its_s)
+        assert abs(its_g[k] - ref["iters"][k]) <= 2, (its_g, ref["iters"])
+        assert abs(its_g[k] - its_s[k]) <= 2, (its_g, its_s)
     ref = problem.solve(spec, x, fx, f, tol=1e-12)
     its_g, comp_g, _ = g.pcg_solve(tol=1e-12)
     u_s = torch.empty(spec.n_rhs * spec.n_dof, dtype=torch.float64, device=DEV)
@@ -92,6 +102,32 @@ def test_strip_pcg_vs_oracle_and_single(name, nranks):
         tc = compliance_tol(spec, ref["E_el"][k], f, fx)
         assert abs(comp_g[k] - ref["comps"][k]) <= tc * abs(ref["comps"][k]), tc
         assert abs(comp_g[k] - comp_s[k]) <= max(1e-11, tc) * abs(comp_s[k])
+    g.close()
+
+
+@pytest.mark.parametrize("name,nranks", CASES)
+def test_strip_coarse_solve_and_vcycle_vs_single(name, nranks):
+    """The distributed K_c (chain levels per rank, all-reduced interface system) solves
+    K_c c = b like the single-GPU cyclic reduction, and one partitioned V-cycle (halo'd
+    colour phases, distributed coarse correction, halo after the prolongation) equals the
+    single-GPU V-cycle, for every realisation."""
+    spec, _ = STRIP_SPECS[name]
+    x = W.design_tile(spec)
+    g = group_for(spec, nranks, x)
+    m = single_for(spec, x)
+    inf = m.info()
+    gen = torch.Generator(device="cpu").manual_seed(5)
+    for k in range(spec.n_rhs):
+        b = torch.randn(inf["coarse_slots"], dtype=torch.float64, generator=gen).to(DEV)
+        xs = torch.empty_like(b)
+        m.coarse_solve(k, b, xs)
+        xg = g.coarse_solve(k, b)
+        assert (xg - xs).norm() <= 1e-11 * xs.norm(), k
+        r = torch.randn(spec.n_dof, dtype=torch.float64, generator=gen).to(DEV)
+        zs = torch.empty_like(r)
+        m.precond_apply(k, r, zs)
+        zg = g.precond_apply(k, r)
+        assert (zg - zs).norm() <= 1e-12 * zs.norm(), k
     g.close()
 
 
