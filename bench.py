@@ -11,7 +11,8 @@ second (whole job, all ranks).
 
 N > 1 (torchrun): the grid of the SAME workload is strip-partitioned over the ranks
 (msf_dist_setup with the NCCL transport; halo exchanges and all-reduces
-inside the library, coarse space replicated), so the total work is fixed (strong scaling);
+inside the library, K_c distributed by block chains with a replicated interface system), so
+the total work is fixed (strong scaling);
 value = n_dof x PCG iterations / max-over-ranks time.  --mode replicas instead runs an
 independent copy per rank (weak scaling).  BASELINE configs[4] (--config c4_mbb_5120x2560)
 is the paper-sized strip-scaling study.
@@ -291,7 +292,7 @@ def run_ours(args, spec):
                    "realisations": spec.n_rhs, "coarse_cell": f"{spec.cx}x{spec.cy}",
                    "n_modes": spec.n_modes, "tile": f"{spec.tile_x}x{spec.tile_y}",
                    "tol": tol,
-                   "parallelism": (f"{ws} strips (NCCL halo + all-reduce, replicated coarse solve)"
+                   "parallelism": (f"{ws} strips (NCCL halos + all-reduces, distributed K_c chains + replicated interface system)"
                                    if strips else "single GPU" if ws == 1
                                    else f"{ws} independent replicas"),
                    "pcg_iters_per_step": iters_step, "n_agg_classes": inf["n_classes"],
@@ -304,8 +305,8 @@ def run_ours(args, spec):
         # every timed kernel (all realisations active, PCG launch configuration): average ms per
         # launch-set, algorithmic GB/s and its fraction of the measured HBM peak
         "kernels": {k: {"ms": v[0],
-                        "alg_GBps": v[1] / (v[0] / 1e3) / 1e9 if v[0] > 0 else None,
-                        "hbm_frac": v[1] / (v[0] / 1e3) / 1e9 / peak if v[0] > 0 else None}
+                        "alg_GBps": v[1] / (v[0] / 1e3) / 1e9 if v[0] > 0 and v[1] > 0 else None,
+                        "hbm_frac": v[1] / (v[0] / 1e3) / 1e9 / peak if v[0] > 0 and v[1] > 0 else None}
                     for k, v in kb.items()},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,

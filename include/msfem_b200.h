@@ -180,7 +180,12 @@ int msf_launch_count(msf_ctx* ctx, int64_t* count, int reset);
  * i = 0 operator apply q = K p (+ p.q), 1 one Gauss-Seidel colour sweep, 2 restriction,
  * 3 coarse solve (all cyclic-reduction levels), 4 prolongation, 5 residual t = r - K z,
  * 6 full V-cycle, 7 one PCG iteration (graph), 8 PCG update fused with the zero-start colour-0
- * phase, 9 p update.  ms and bytes hold 10 entries. */
+ * phase, 9 p update, 10 K_c assembly: Galerkin products + chain levels (a strip: its own
+ * cells and chain), 11 K_c assembly: interface levels + top system, 12 coarse solve:
+ * forward chain levels, 13 coarse solve: interface levels + top (+ back), 14 coarse solve:
+ * back chain levels (10-14 on one GPU: the same split of the whole chain; a strip's 10-14
+ * are its per-rank shares, without the exchanges).  ms and bytes hold 15 entries; the
+ * factors are valid again when it returns. */
 int msf_bench_kernels(msf_ctx* ctx, int reps, double* ms, double* bytes);
 
 /* ---- strip partition over ranks (multi-GPU) -------------------------

@@ -340,18 +340,20 @@ class Msfem:
 
     def bench_kernels(self, reps=20):
         """Per-kernel average ms and algorithmic bytes per launch (see msf_bench_kernels)."""
-        ms = (ctypes.c_double * 10)()
-        by = (ctypes.c_double * 10)()
+        ms = (ctypes.c_double * 15)()
+        by = (ctypes.c_double * 15)()
         self._check(self.lib.msf_bench_kernels(self.ctx, reps, ms, by))
         names = ["apply", "sgs_colour", "restrict", "coarse_solve", "prolong", "residual",
-                 "vcycle", "pcg_iteration", "update_f0", "p_update"]
+                 "vcycle", "pcg_iteration", "update_f0", "p_update", "assemble_local",
+                 "assemble_top", "coarse_fwd_local", "coarse_top", "coarse_back_local"]
         return {n: (ms[i], by[i]) for i, n in enumerate(names)}
 
 
 class MsfemGroup:
     """All ranks of a strip partition as contexts of this process on one device
     (MSF_TRANSPORT_GROUP): replicated steps run per rank, the communicating steps
-    (PCG, sensitivities) through the group entry points.  Proves the partitioned path on a
+    (K_c assembly, PCG, sensitivities, the coarse-solve / V-cycle diagnostics) through the
+    group entry points.  Proves the partitioned path on a
     single GPU; production multi-GPU runs use one process per GPU with NCCL."""
 
     def __init__(self, problem: MsfProblem, fixed_mask, load, nranks, stream=None):

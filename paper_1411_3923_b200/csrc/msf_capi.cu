@@ -1523,6 +1523,26 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   bytes[7] = bytes[0] + bytes[6] + R * nn * 16 * 6 + R * nn * 16 * 2 + R * nn * 16 * 3;
   bytes[8] = R * (nn * 16 * 6 + ne * 8 + nn / 4 * 16 * 2) + nn / 4;    // p q u r -> u r, F0
   bytes[9] = R * nn * 16 * 3;                                          // z, p -> p
+  // coarse phases of this rank: chain levels (forward Q, P; back Dinv, P^T, Q^T), interface
+  // levels + top; assembly entries carry no byte count
+  {
+    const double mm = (double)d.mc * d.mc * 8;
+    double fwd = 0.0, back = 0.0, top = 0.0;
+    for (size_t l = 0; l < c->cr.size(); ++l) {
+      const CrLevel& L = c->cr[l];
+      if ((int)l < c->n_local) {
+        fwd += L.surv.size() * 2 * mm;
+        back += L.elim.size() * 3 * mm;
+      } else {
+        top += L.surv.size() * 2 * mm + L.elim.size() * 3 * mm;
+      }
+    }
+    top += (double)c->top_T * c->top_T * mm;
+    bytes[10] = bytes[11] = 0.0;
+    bytes[12] = R * fwd;
+    bytes[13] = R * top;
+    bytes[14] = R * back;
+  }
   // keep every realisation active during the timing, restore afterwards
   std::vector<PcgScalars> saved(R);
   CK(cudaMemcpyAsync(saved.data(), c->sc, R * sizeof(PcgScalars), cudaMemcpyDeviceToHost, c->stream));
@@ -1557,6 +1577,14 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
         case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
         case 8: launch_update_f0(c, 0, R); break;
         case 9: launch_pcg_p(c, 0, R, false); break;
+        case 10: launch_assemble_local(c); break;
+        case 11:   // a strip re-reads the all-reduced interface blocks before the top part
+          if (!c->iface.empty()) launch_iface_mat_unpack(c);
+          launch_assemble_top(c);
+          break;
+        case 12: launch_coarse_forward_local(c, 0, R, false); break;
+        case 13: launch_coarse_top(c, 0, R, false); break;
+        case 14: launch_coarse_back_local(c, 0, R, false); break;
       }
     }
     cudaEventRecord(e0, c->stream);
@@ -1572,6 +1600,14 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
         case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
         case 8: launch_update_f0(c, 0, R); break;
         case 9: launch_pcg_p(c, 0, R, false); break;
+        case 10: launch_assemble_local(c); break;
+        case 11:   // a strip re-reads the all-reduced interface blocks before the top part
+          if (!c->iface.empty()) launch_iface_mat_unpack(c);
+          launch_assemble_top(c);
+          break;
+        case 12: launch_coarse_forward_local(c, 0, R, false); break;
+        case 13: launch_coarse_top(c, 0, R, false); break;
+        case 14: launch_coarse_back_local(c, 0, R, false); break;
       }
     }
     cudaEventRecord(e1, c->stream);
@@ -1581,7 +1617,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
     return (double)t / reps;
   };
   const int ntimed = c->comm ? 6 : 8;
-  for (int i = 0; i < 10; ++i) ms[i] = (i < ntimed || i >= 8) ? timeit(i) : -1.0;
+  for (int i = 0; i < MSF_BENCH_ENTRIES; ++i) ms[i] = (i < ntimed || i >= 8) ? timeit(i) : -1.0;
   if (ms[7] > 0) ms[7] /= c->graph_iters;   // the graph holds graph_iters iterations
   if (!gR) ms[7] = -1.0;
   cudaEventDestroy(e0);

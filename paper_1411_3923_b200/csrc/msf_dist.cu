@@ -1,7 +1,8 @@
 // Cross-rank transport of the strip-partitioned PCG: one PCG iteration
-// needs (a) halo exchanges of the smoother iterate z after every colour phase (one node
-// column per neighbour and realisation) and (b) sum all-reduces of the dot products and of
-// the restricted coarse residual R_c t (the coarse solve itself is replicated).
+// needs (a) halo exchanges of the smoother iterate z after every colour phase and after the
+// prolongation (one node column per neighbour and realisation) and (b) sum all-reduces of
+// the dot products and of the chain-end coarse rhs (K_c is distributed by block chains; the
+// interface system is replicated).  The assembly all-reduces the interface blocks of K_c.
 //
 //   MSF_TRANSPORT_NCCL : one process per GPU; NCCL send/recv + all-reduce on the context's
 //                        stream (captured into the per-iteration CUDA graph).  libnccl is

@@ -337,6 +337,7 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated);
 int launch_pcg_persistent(msf_ctx* c, int nr);
 size_t cr_levels_dev_bytes(int nlev);
 void fill_cr_levels_dev(const std::vector<CrLevel>& cr, void* host_buf);
+constexpr int MSF_BENCH_ENTRIES = 15;   // msf_bench_kernels
 constexpr int MSF_TOP_MAX = 1200;   // max unknowns of the dense top system (T * mc)
 constexpr int MSF_PERSIST_PARTIALS = 3 * MSF_MAX_RHS * 4 * 160;  // 3 slots x 4 rhs x grid
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated);

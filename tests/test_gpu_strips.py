@@ -15,8 +15,8 @@ path, compliance the fp64-attainable bar (tests/test_gpu_parity.py) and 1e-11.  
 counts: +-2.  The eroded realisation of robust_32x16 (137 iterations on 1,122 DOF) is
 chaotic under rounding: the single-GPU path with the design tile perturbed by 1e-15
 (relative) takes 136 or 137 iterations (40 seeds), two strips 136, 137 or 139 (12 seeds;
-139 for the unperturbed tile), while the two V-cycles agree to 1e-14 (scratch run,
-DESIGN.md §8(e)).  Every other realisation here matches the single-GPU count exactly."""
+139 for the unperturbed tile), while the two V-cycles agree to 1e-14 (scripts/rounding_spread.py,
+profiles/r01_rounding_spread.txt).  Every other realisation here matches the single-GPU count exactly."""
 import numpy as np
 import pytest
 
