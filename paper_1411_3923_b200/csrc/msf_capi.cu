@@ -524,16 +524,15 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     c->id_hi = (nranks == 1 || last) ? d.ncx : c->sb.C1 - 1;
   }
   {
-    // restriction work list: agglomerates grouped by class (consecutive CTAs share a basis
-    // in L2); a strip keeps those whose box meets its node columns
-    std::vector<std::vector<int>> members(c->n_cls);
-    for (int a = 0; a < d.n_agg; ++a) members[P.cls_of_agg[a]].push_back(a);
+    // restriction work list: agglomerates in grid order, so the four boxes that overlap on a
+    // node run close together and t is read from DRAM once (the class bases, a few MB, stay
+    // in L2 in any order; grouping by class made configs[4] read t four times: 812 MB vs
+    // 210 MB, profiles/r01_summary.md).  A strip keeps the agglomerates of its chain.
     c->agg_by_cls_h.clear();
-    for (int k = 0; k < c->n_cls; ++k)
-      for (int a : members[k]) {
-        const int I = a / (d.ncy + 1);
-        if (I >= c->cr_lo && I <= c->cr_hi) c->agg_by_cls_h.push_back(a);
-      }
+    for (int a = 0; a < d.n_agg; ++a) {
+      const int I = a / (d.ncy + 1);
+      if (I >= c->cr_lo && I <= c->cr_hi) c->agg_by_cls_h.push_back(a);
+    }
     c->n_restrict = (int)c->agg_by_cls_h.size();
     c->agg_by_cls_d = (int*)take((size_t)d.n_agg * 4);
   }
@@ -554,6 +553,13 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (const char* e = std::getenv("MSF_BLOCKED_INV_MIN")) c->blocked_inv_min = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("MSF_RESTRICT_THREADS")) c->restrict_threads = std::atoi(e);
   if (const char* e = std::getenv("MSF_APPLY_DIRECT")) c->apply_direct = std::string(e) != "0";
+  if (const char* e = std::getenv("MSF_APPLY_SW")) c->apply_sw = std::string(e) != "0";
+  if (const char* e = std::getenv("MSF_APPLY_TMA")) c->apply_tma = std::string(e) != "0";
+  if (const char* e = std::getenv("MSF_RESIDUAL_TMA")) c->residual_tma = std::string(e) != "0";
+  if (const char* e = std::getenv("MSF_SW_KX")) {
+    const int k = std::atoi(e);
+    c->apply_sw_kx = (k == 2 || k == 4 || k == 8) ? k : 0;
+  }
   c->sc = (PcgScalars*)take(R * sizeof(PcgScalars));
   c->partials = (double*)take((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
   c->apart = (double*)take(R * (size_t)P.max_partials * 8);

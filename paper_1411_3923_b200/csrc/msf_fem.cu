@@ -12,6 +12,11 @@
 //   * PCG dot products: warp-shuffle + shared-memory block reduction, per-block partials,
 //     the last block to finish reduces the partials in a fixed order (deterministic) and
 //     updates the per-realisation scalars (alpha, beta, convergence) on the device.
+#include <cuda.h>            // CUtensorMap (TMA descriptors)
+#include <cudaTypedefs.h>    // PFN_cuTensorMapEncodeTiled
+
+#include <cstring>
+
 #include "msf_kern.cuh"
 
 using namespace msfk;
@@ -126,6 +131,304 @@ __global__ void __launch_bounds__(NTHR) k_apply(Dims d, K0Mat K, const double* _
         counters[rhs * 8] = 0;
       }
     }
+  }
+}
+
+// ------------------------------------------------------------------ sliding-window operator apply
+// Thread per (node row iy, run of KX consecutive node columns): the 3x3 neighbourhood of x and
+// the 2x2 element moduli slide along the columns in registers, so a node costs three
+// coalesced double2 loads (its new column, rows iy-1..iy+1), two moduli and almost no index
+// arithmetic.  (ncu, configs[4]: the one-node-per-thread form below is issue-bound, 67% of
+// issue slots on address and bounds arithmetic for 13 loads per node, at 2.3 TB/s.)
+template <int MODE, int KX>
+__global__ void __launch_bounds__(NTHR) k_apply_sw(Dims d, K0Mat K, const double* __restrict__ Eall,
+                                                   const double2* __restrict__ xall,
+                                                   double2* __restrict__ yall,
+                                                   const double2* __restrict__ ball,
+                                                   const uint8_t* __restrict__ fixn, PcgScalars* sc,
+                                                   double* partials, unsigned* counters, int rhs0,
+                                                   int gated, int dot, int max_partials,
+                                                   double* dsum, double* apart) {
+  pdl_launch();
+  pdl_wait();
+  const int rhs = rhs0 + blockIdx.z;
+  if (gated && !sc[rhs].active) return;
+  __shared__ double red[NTHR / 32 + 1];
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int iy = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ix0 = (blockIdx.y * blockDim.y + threadIdx.y) * KX;
+  const double* E = Eall + (size_t)rhs * d.estride;
+  const double2* x = xall + (size_t)rhs * d.nn;
+  double dv = 0.0;
+  if (iy < d.nny && ix0 < d.nnx) {
+    const bool ylo = iy >= 1, yhi = iy + 1 < d.nny;   // node rows iy-1, iy+1 exist
+    const bool ehi = iy < d.nely;                      // element row iy exists (iy-1: ylo)
+    const double2 zero = make_double2(0.0, 0.0);
+    double2 w[3][3];  // node (ix-1+i, iy-1+j)
+    double e[2][2];   // element (ix-1+i, iy-1+j)
+    auto load_col = [&](int gx, double2 (&col)[3]) {
+      if (gx >= 0 && gx < d.nnx) {
+        const double2* p = x + (size_t)gx * d.nny + iy;
+        col[0] = ylo ? __ldg(p - 1) : zero;
+        col[1] = __ldg(p);
+        col[2] = yhi ? __ldg(p + 1) : zero;
+      } else {
+        col[0] = col[1] = col[2] = zero;
+      }
+    };
+    auto load_ecol = [&](int ex, double (&ec)[2]) {
+      if (ex >= 0 && ex < d.nelx) {
+        const double* p = E + (size_t)ex * d.nely + iy;
+        ec[0] = ylo ? __ldg(p - 1) : 0.0;
+        ec[1] = ehi ? __ldg(p) : 0.0;
+      } else {
+        ec[0] = ec[1] = 0.0;
+      }
+    };
+    load_col(ix0 - 1, w[0]);
+    load_col(ix0, w[1]);
+    load_ecol(ix0 - 1, e[0]);
+#pragma unroll
+    for (int s = 0; s < KX; ++s) {
+      const int ix = ix0 + s;
+      load_col(ix + 1, w[2]);
+      load_ecol(ix, e[1]);
+      if (ix < d.nnx) {
+        double ox, oy, dxx, dxy, dyx, dyy;
+        apply_node(K, e, w, ox, oy, dxx, dxy, dyx, dyy);
+        const size_t n = (size_t)ix * d.nny + iy;
+        const uint8_t fm = fixn[n];
+        double2 out;
+        if (MODE == 1) {
+          const double2 bb = ball[(size_t)rhs * d.nn + n];
+          out = make_double2(bb.x - ox, bb.y - oy);
+        } else {
+          out = make_double2(ox, oy);
+        }
+        if (fm & 1) out.x = 0.0;
+        if (fm & 2) out.y = 0.0;
+        yall[(size_t)rhs * d.nn + n] = out;
+        dv += w[1][1].x * out.x + w[1][1].y * out.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        w[0][j] = w[1][j];
+        w[1][j] = w[2][j];
+      }
+      e[0][0] = e[1][0];
+      e[0][1] = e[1][1];
+    }
+  }
+  if (dot == 2) {
+    // partial only (no fence / ticket): the consumer (k_update_f0) reduces the partials
+    const double s = block_sum_all(dv, red, tid, NTHR);
+    if (tid == 0) apart[(size_t)rhs * max_partials + blockIdx.y * gridDim.x + blockIdx.x] = s;
+  } else if (dot) {
+    const double s = block_sum_all(dv, red, tid, NTHR);
+    const unsigned nblk = gridDim.x * gridDim.y;
+    const int slot = blockIdx.y * gridDim.x + blockIdx.x;
+    if (arrive_last(s, partials + (size_t)rhs * max_partials, slot, counters + rhs * 8, nblk, tid)) {
+      const double tot = reduce_partials(partials + (size_t)rhs * max_partials, nblk, red, tid, NTHR);
+      if (tid == 0) {
+        fin_or_park(sc, dsum, rhs, FIN_PQ, tot, 0);
+        counters[rhs * 8] = 0;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ TMA-fed operator apply
+// Persistent CTAs stream halo'd tiles of x (10 x 128 node columns x rows, double2, from row
+// y0-1) and of the moduli (9 x 128, from row y0-2: the start of a box's inner dimension must
+// be 16-byte aligned) through a 3-stage shared-memory ring: one thread issues both
+// cp.async.bulk.tensor loads of a stage (completion counted on an mbarrier in bytes) while
+// the CTA computes the tile two stages back.  The tensor maps zero-fill outside the grid, so
+// the stencil needs no bounds logic; in flight data lives in shared memory, not registers.
+// Each thread slides along 4 node columns of one row (3 new double2 + 2 moduli per node from
+// shared memory, conflict-free).  Tiles: 8 columns x 126 rows of outputs.
+constexpr int TMA_TX = 8, TMA_TY = 126, TMA_STAGES = 3;
+constexpr int TMA_XS = (TMA_TX + 2) * 256;   // doubles per stage: x tile [10][128] double2
+constexpr int TMA_ES = (TMA_TX + 1) * 128;   //                    E tile [9][128]
+constexpr int TMA_STAGE = TMA_XS + TMA_ES;
+constexpr size_t TMA_SMEM = (size_t)TMA_STAGES * TMA_STAGE * sizeof(double) + 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NTHR, 2) k_apply_tma(const __grid_constant__ CUtensorMap tmx,
+                                                      const __grid_constant__ CUtensorMap tme, Dims d,
+                                                      K0Mat K, const double2* __restrict__ ball,
+                                                      double2* __restrict__ yall,
+                                                      const uint8_t* __restrict__ fixn, PcgScalars* sc,
+                                                      double* partials, unsigned* counters, int rhs0,
+                                                      int nr, int gated, int dot, int max_partials,
+                                                      double* dsum, double* apart) {
+  // persistent grid: the dependent kernel is signalled after the tile loop (at entry its
+  // early CTAs competed with the resident tiles: +2% per PCG iteration on configs[4])
+  extern __shared__ __align__(128) unsigned char tsm_raw[];
+  // stage ring 128-byte aligned by hand (static shared memory precedes the dynamic window)
+  double* tsm = reinterpret_cast<double*>(tsm_raw + ((128u - (smem_u32(tsm_raw) & 127u)) & 127u));
+  __shared__ __align__(8) uint64_t full[TMA_STAGES];
+  __shared__ double red[NTHR / 32 + 1];
+  const int tid = threadIdx.x;
+  const int ntx = (d.nnx + TMA_TX - 1) / TMA_TX, nty = (d.nny + TMA_TY - 1) / TMA_TY;
+  const int per = ntx * nty, ntiles = per * nr;
+  if (tid == 0) {
+    for (int s = 0; s < TMA_STAGES; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();   // x (and the realisation flags) come from the preceding kernels
+  // the CTA's tiles t = blockIdx.x + k gridDim.x (y fastest within a column strip, realisation
+  // slowest); tiles of converged realisations are skipped identically by every thread
+  auto active = [&](int t) { return !gated || sc[rhs0 + t / per].active; };
+  auto next_tile = [&](int t) {
+    for (t += gridDim.x; t < ntiles && !active(t); t += gridDim.x) {}
+    return t;
+  };
+  int t_issue = blockIdx.x;
+  if (t_issue < ntiles && !active(t_issue)) t_issue = next_tile(t_issue);
+  int n_issued = 0;
+  auto issue = [&]() {   // thread 0: next active tile into stage n_issued % STAGES
+    if (t_issue >= ntiles) return;
+    const int rr = t_issue / per, tl = t_issue - rr * per;
+    const int tx = tl / nty, ty = tl - tx * nty;
+    const int x0 = tx * TMA_TX, y0 = ty * TMA_TY;
+    const int st = n_issued % TMA_STAGES;
+    double* base = tsm + st * TMA_STAGE;
+    mbar_expect_tx(&full[st], TMA_STAGE * sizeof(double));
+    tma_load_3d(base, &tmx, 2 * (y0 - 1), x0 - 1, rhs0 + rr, &full[st]);
+    tma_load_3d(base + TMA_XS, &tme, y0 - 2, x0 - 1, rhs0 + rr, &full[st]);
+    ++n_issued;
+    t_issue = next_tile(t_issue);
+  };
+  if (tid == 0)
+    for (int s = 0; s < TMA_STAGES; ++s) issue();
+  double dv[MSF_MAX_RHS] = {0.0, 0.0, 0.0, 0.0};
+  const int r = tid & 127, lc0 = (tid >> 7) * 4;
+  int t = blockIdx.x;
+  if (t < ntiles && !active(t)) t = next_tile(t);
+  for (int n_used = 0; t < ntiles; ++n_used, t = next_tile(t)) {
+    const int st = n_used % TMA_STAGES;
+    mbar_wait(&full[st], (uint32_t)(n_used / TMA_STAGES) & 1u);
+    const int rr = t / per, tl = t - rr * per;
+    const int tx = tl / nty, ty = tl - tx * nty;
+    const int x0 = tx * TMA_TX, y0 = ty * TMA_TY;
+    const int rhs = rhs0 + rr, iy = y0 + r;
+    const double2* xs = reinterpret_cast<const double2*>(tsm + st * TMA_STAGE);   // [10][128]
+    const double* es = tsm + st * TMA_STAGE + TMA_XS;                              // [9][128]
+    if (r < TMA_TY && iy < d.nny) {
+      // Dirichlet masks of the thread's 4 nodes, loaded before the stencil work (a global
+      // load per node issued just before its store was the top stall)
+      uint8_t fm4[4];
+      double2 bb4[4];   // MODE 1: the right-hand side, likewise loaded up front
+#pragma unroll
+      for (int sx = 0; sx < 4; ++sx) {
+        const int ix = x0 + lc0 + sx;
+        const size_t n = (size_t)min(ix, d.nnx - 1) * d.nny + iy;
+        fm4[sx] = ix < d.nnx ? fixn[n] : (uint8_t)0;
+        if (MODE == 1) bb4[sx] = ball[(size_t)rhs * d.nn + n];
+      }
+      double2 w[3][3];   // node (ix-1+i, iy-1+j)    = x tile (lc+i, r+j)
+      double e[2][2];    // element (ix-1+i, iy-1+j) = E tile (lc+i, r+j+1): the E box starts
+                         // at row y0-2 (TMA needs a 16-byte aligned start of the inner dim)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) w[i][j] = xs[(lc0 + i) * 128 + r + j];
+      e[0][0] = es[lc0 * 128 + r + 1];
+      e[0][1] = es[lc0 * 128 + r + 2];
+      double dsum_t = 0.0;
+#pragma unroll
+      for (int sx = 0; sx < 4; ++sx) {
+        const int lc = lc0 + sx, ix = x0 + lc;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) w[2][j] = xs[(lc + 2) * 128 + r + j];
+        e[1][0] = es[(lc + 1) * 128 + r + 1];
+        e[1][1] = es[(lc + 1) * 128 + r + 2];
+        if (ix < d.nnx) {
+          double ox, oy, dxx, dxy, dyx, dyy;
+          apply_node(K, e, w, ox, oy, dxx, dxy, dyx, dyy);
+          const size_t n = (size_t)ix * d.nny + iy;
+          const uint8_t fm = fm4[sx];
+          double2 out;
+          if (MODE == 1) {
+            out = make_double2(bb4[sx].x - ox, bb4[sx].y - oy);
+          } else {
+            out = make_double2(ox, oy);
+          }
+          if (fm & 1) out.x = 0.0;
+          if (fm & 2) out.y = 0.0;
+          yall[(size_t)rhs * d.nn + n] = out;
+          dsum_t += w[1][1].x * out.x + w[1][1].y * out.y;
+        }
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          w[0][j] = w[1][j];
+          w[1][j] = w[2][j];
+        }
+        e[0][0] = e[1][0];
+        e[0][1] = e[1][1];
+      }
+#pragma unroll
+      for (int q = 0; q < MSF_MAX_RHS; ++q)
+        if (q == rr) dv[q] += dsum_t;
+    }
+    __syncthreads();   // every thread is done with this stage
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue();
+    }
+  }
+  pdl_launch();
+  if (!dot) return;
+#pragma unroll
+  for (int q = 0; q < MSF_MAX_RHS; ++q) {
+    if (q >= nr) break;
+    const int rhs = rhs0 + q;
+    if (gated && !sc[rhs].active) continue;   // uniform: no block of this realisation arrives
+    const double sblk = block_sum_all(dv[q], red, tid, NTHR);
+    if (dot == 2) {
+      if (tid == 0) apart[(size_t)rhs * max_partials + blockIdx.x] = sblk;
+    } else if (arrive_last(sblk, partials + (size_t)rhs * max_partials, blockIdx.x, counters + rhs * 8,
+                           gridDim.x, tid)) {
+      const double tot = reduce_partials(partials + (size_t)rhs * max_partials, gridDim.x, red, tid, NTHR);
+      if (tid == 0) {
+        fin_or_park(sc, dsum, rhs, FIN_PQ, tot, 0);
+        counters[rhs * 8] = 0;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -487,6 +790,82 @@ int sgs_colour_partials_needed(const Dims& d) {
 // Fine-grid launchers run on this rank's grid c->dl with the moduli c->E_loc (the whole grid
 // on one GPU); reductions park their sums in c->dsum on a strip context.
 // direct-load apply (default; MSF_APPLY_DIRECT=0 selects the shared-memory tile kernel)
+// TMA descriptors of the operator apply: kind 0 = node vector x (dims 2 nny doubles, nnx
+// columns, R realisations), kind 1 = moduli (nely, nelx, R); cached per base pointer.
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }();
+  return fn;
+}
+
+// Copies the descriptor out (the cache vector may reallocate on the next insertion).
+static bool tmap_for(msf_ctx* c, const void* base, int kind, CUtensorMap* out) {
+  for (const msf_ctx::TmapSlot& t : c->tmaps)
+    if (t.ptr == base && t.kind == kind) {
+      std::memcpy(out, t.bytes, sizeof(CUtensorMap));
+      return true;
+    }
+  auto enc = tmap_encode();
+  if (!enc) return false;
+  const Dims& d = c->dl;
+  msf_ctx::TmapSlot slot{};
+  slot.ptr = base;
+  slot.kind = kind;
+  static_assert(sizeof(CUtensorMap) <= sizeof(slot.bytes), "tensor map size");
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(slot.bytes);
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r;
+  if (kind == 0) {
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * d.nny, (cuuint64_t)d.nnx, (cuuint64_t)d.R};
+    const cuuint64_t strides[2] = {(cuuint64_t)2 * d.nny * 8, (cuuint64_t)2 * d.nn * 8};
+    const cuuint32_t box[3] = {256, TMA_TX + 2, 1};
+    r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[3] = {(cuuint64_t)d.nely, (cuuint64_t)d.nelx, (cuuint64_t)d.R};
+    const cuuint64_t strides[2] = {(cuuint64_t)d.nely * 8, (cuuint64_t)d.estride * 8};
+    const cuuint32_t box[3] = {128, TMA_TX + 1, 1};
+    r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) return false;
+  c->tmaps.push_back(slot);
+  std::memcpy(out, slot.bytes, sizeof(CUtensorMap));
+  return true;
+}
+
+template <int MODE>
+static bool launch_apply_tma(msf_ctx* c, int rhs0, int nr, const double* x, double* y,
+                             const double* bvec, bool gated, int dmode) {
+  const Dims& d = c->dl;
+  // 16-byte global strides / base alignment of the moduli map; a grid of at least one tile
+  if (!c->apply_tma || (d.nely & 1) || (d.estride & 1) || d.nny < TMA_TY || d.nnx < TMA_TX)
+    return false;
+  CUtensorMap mx, me;
+  if (!tmap_for(c, x, 0, &mx) || !tmap_for(c, c->E_loc, 1, &me)) return false;
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_apply_tma<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
+    return true;
+  }();
+  (void)attr;
+  const long long ntiles = (long long)((d.nnx + TMA_TX - 1) / TMA_TX) * ((d.nny + TMA_TY - 1) / TMA_TY) * nr;
+  const int grid = (int)std::min<long long>(ntiles, 2 * 148);
+  launch_k(k_apply_tma<MODE>, dim3(grid), dim3(NTHR), TMA_SMEM, c->stream, mx, me, d, c->K0,
+           (const double2*)bvec, (double2*)y, c->fixn, c->sc, c->partials, c->counters, rhs0, nr,
+           gated ? 1 : 0, dmode, c->max_partials, c->dsum, c->apart);
+  c->apart_n = dmode == 2 ? grid : 0;
+  MSF_LAUNCHED(c);
+  return true;
+}
+
 template <int MODE>
 static bool launch_apply_direct(msf_ctx* c, int rhs0, int nr, const double* x, double* y,
                                 const double* bvec, bool gated, bool dot) {
@@ -495,6 +874,28 @@ static bool launch_apply_direct(msf_ctx* c, int rhs0, int nr, const double* x, d
   // p.Ap on one GPU: partials only, reduced by the next kernel (k_update_f0); strips need the
   // all-reduce, so the last-block finalisation parks the local sum
   const int dmode = !dot ? 0 : c->comm ? 1 : 2;
+  if ((MODE == 0 || c->residual_tma) && launch_apply_tma<MODE>(c, rhs0, nr, x, y, bvec, gated, dmode))
+    return true;
+  if (c->apply_sw && MODE == 0) {
+    // columns per thread: the longest run that still gives >= 4 CTAs per SM (measured: the
+    // residual form, which also streams b, is faster one node per thread)
+    const int by = (d.nny + 31) / 32;
+    int kx = 8;
+    while (kx > 2 && (long long)by * ((d.nnx + 8 * kx - 1) / (8 * kx)) * nr < 4 * 148) kx /= 2;
+    if (c->apply_sw_kx) kx = c->apply_sw_kx;
+    const dim3 grid(by, (d.nnx + 8 * kx - 1) / (8 * kx), nr);
+#define MSF_SW(KX)                                                                                  \
+  launch_k(k_apply_sw<MODE, KX>, grid, dim3(32, 8), 0, c->stream, d, c->K0, (const double*)c->E_loc, \
+           (const double2*)x, (double2*)y, (const double2*)bvec, c->fixn, c->sc, c->partials,        \
+           c->counters, rhs0, gated ? 1 : 0, dmode, c->max_partials, c->dsum, c->apart)
+    if (kx == 8) MSF_SW(8);
+    else if (kx == 4) MSF_SW(4);
+    else MSF_SW(2);
+#undef MSF_SW
+    c->apart_n = dmode == 2 ? (int)(grid.x * grid.y) : 0;
+    MSF_LAUNCHED(c);
+    return true;
+  }
   launch_k(k_apply_direct<MODE>, dim3((d.nny + 31) / 32, (d.nnx + 7) / 8, nr), dim3(32, 8), 0,
            c->stream, d, c->K0, (const double*)c->E_loc, (const double2*)x, (double2*)y,
            (const double2*)bvec, c->fixn, c->sc, c->partials, c->counters, rhs0, gated ? 1 : 0,

@@ -240,6 +240,16 @@ struct msf_ctx {
   int blocked_inv_min = 256;
   int restrict_threads = 0;
   bool apply_direct = true;     // operator apply with direct (L1) neighbourhood loads
+  bool apply_sw = true;         // ... as a sliding window along x (env MSF_APPLY_SW=0: per node)
+  int apply_sw_kx = 0;          // columns per thread of the sliding window (0: from the grid size)
+  bool apply_tma = true;        // operator apply fed by TMA tiles (env MSF_APPLY_TMA=0: off)
+  bool residual_tma = true;     // ... also for the residual t = r - K z (env MSF_RESIDUAL_TMA=0)
+  struct TmapSlot {             // cached TMA descriptor (CUtensorMap, 128 B) per base pointer
+    const void* ptr;
+    int kind;
+    alignas(64) unsigned char bytes[128];
+  };
+  std::vector<TmapSlot> tmaps;
   double* apart = nullptr;      // [R][max_partials] operator p.Ap partials (one GPU)
   int apart_n = 0;              // partial count left by the last matvec (0: none pending)     // threads per agglomerate CTA (0: from the box size)    // m from which SPD block inverses use the blocked path
 

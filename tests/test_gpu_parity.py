@@ -97,6 +97,29 @@ def test_matvec(name):
             assert np.abs(host(y) - ref).max() <= 1e-13 * np.abs(ref).max()
 
 
+# grids large enough for the TMA-fed operator apply (>= 126 node rows, even nely): ragged last
+# tiles in x (nnx = 8k + 1) and y (nny = 126k + 5 / + 1), several realisations
+TMA_SPECS = {
+    "tma_160x130": W.small_spec(nelx=160, nely=130, cx=10, cy=10, tile=(16, 10), rmin=1.5,
+                                beta=4.0, etas=(0.6, 0.4, 0.3), dilated=2, seed=31),
+    "tma_96x252_mbb": W.small_spec(nelx=96, nely=252, cx=8, cy=12, bc="mbb", seed=32),
+}
+
+
+@pytest.mark.parametrize("name", list(TMA_SPECS))
+def test_matvec_tma_tiles(name):
+    spec = TMA_SPECS[name]
+    m, x = ctx_for(spec)
+    fx, f, K0, E, A, _ = oracle_setup(spec, x)
+    V = W.random_vectors(spec.n_dof, 2, seed=7)
+    for k in range(spec.n_rhs):
+        for v in V:
+            y = torch.empty(spec.n_dof, dtype=torch.float64, device=DEV)
+            m.matvec(k, dev(v), y)
+            ref = A[k] @ v
+            assert np.abs(host(y) - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
 @pytest.mark.parametrize("name", ["cant_16x8", "mbb_24x12", "ragged_36x20"])
 def test_symmetric_gauss_seidel(name):
     spec = SPECS[name]
