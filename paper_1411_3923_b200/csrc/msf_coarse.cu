@@ -75,6 +75,70 @@ __global__ void __launch_bounds__(NTR) k_restrict1(Dims d, const double2* __rest
   }
 }
 
+// One WARP per (agglomerate, realisation): lanes stride the agglomerate's clipped box (y
+// fastest, the position stepped incrementally), the KM sums are reduced by shuffles only (no
+// shared memory, no block barrier), 8 agglomerates per CTA.  (One 256-thread CTA per
+// agglomerate spent its time in CTA turnover and block reductions: ~4 loop passes per CTA.)
+template <int KM>
+__global__ void __launch_bounds__(256) k_restrict_warp(Dims d, const double2* __restrict__ tall,
+                                                       const double* __restrict__ phi,
+                                                       const int* __restrict__ cls_of_agg,
+                                                       const int* __restrict__ agg_list, int n_agg,
+                                                       double* cball, const PcgScalars* sc, int rhs0,
+                                                       int gated) {
+  pdl_launch();
+  pdl_wait();
+  const int rhs = rhs0 + blockIdx.y;
+  if (gated && !sc[rhs].active) return;
+  const int lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (slot >= n_agg) return;
+  const int agg = agg_list[slot];
+  const int I = agg / (d.ncy + 1), J = agg - (agg / (d.ncy + 1)) * (d.ncy + 1);
+  const double2* ph = reinterpret_cast<const double2*>(phi) + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes;
+  const double2* t = tall + (size_t)rhs * d.nn;
+  const int gx0 = I * d.cx - d.cx - d.gox, gy0 = J * d.cy - d.cy;
+  // interior of the padded box (chi vanishes on its boundary ring), clipped to the strip
+  const int ix_lo = max(1, -gx0), ix_hi = min(d.bx - 2, d.nnx - 1 - gx0);
+  const int iy_lo = max(1, -gy0), iy_hi = min(d.by - 2, d.nny - 1 - gy0);
+  const int w = iy_hi - iy_lo + 1, h = ix_hi - ix_lo + 1;
+  double acc[KM];
+#pragma unroll
+  for (int a = 0; a < KM; ++a) acc[a] = 0.0;
+  // position of element k = lane + 32 i of the w-by-h box, stepped without divisions
+  int px = lane / w, py = lane - (lane / w) * w;
+  const int step_x = 32 / w, step_y = 32 - (32 / w) * w;
+  const int n = w * h;
+#pragma unroll 4
+  for (int k = lane; k < n; k += 32) {
+    const int bx = ix_lo + px, by = iy_lo + py;
+    const double2 tv = t[(size_t)(gx0 + bx) * d.nny + (gy0 + by)];
+    const int bn = bx * d.by + by;
+#pragma unroll
+    for (int a = 0; a < KM; ++a) {
+      if (a < d.kmax) {
+        const double2 pv = __ldg(ph + (size_t)a * d.box_nodes + bn);
+        acc[a] = fma(pv.x, tv.x, fma(pv.y, tv.y, acc[a]));
+      }
+    }
+    px += step_x;
+    py += step_y;
+    if (py >= w) {
+      py -= w;
+      ++px;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < KM; ++a) {
+    if (a < d.kmax) {
+      double v = acc[a];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == a) cball[(size_t)rhs * d.nbc * d.mc + (size_t)agg * d.kmax + a] = v;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ per-realisation prolongation
 // z(n) += sum_{I,J,a} phi_{I,J,a}(n) x_c[slot(I,J,a)], one (node, realisation) per thread.
 template <int KM>
@@ -710,6 +774,22 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
     else if (d.kmax <= 8) MSF_RESTRICT(8, NTR); \
     else MSF_RESTRICT(16, NTR);                 \
   } while (0)
+  // one warp per agglomerate when that gives >= 32 warps per SM (configs[4]: 320 -> 230 us per
+  // launch); otherwise one CTA per agglomerate (configs[1] at one realisation, 2145 warps:
+  // 15 vs 20 us)
+  if (c->restrict_warp && (long long)c->n_restrict * nr >= 32LL * 148) {
+#define MSF_RESTRICT_W(KM)                                                                         \
+  launch_k(k_restrict_warp<KM>, dim3((c->n_restrict + 7) / 8, nr), dim3(256), 0, c->stream, d,        \
+           (const double2*)t, (const double*)c->phi, (const int*)c->cls_of_agg_d,                     \
+           (const int*)c->agg_by_cls_d, c->n_restrict, c->cb, (const PcgScalars*)c->sc, rhs0,         \
+           gated ? 1 : 0)
+    if (d.kmax <= 4) MSF_RESTRICT_W(4);
+    else if (d.kmax <= 8) MSF_RESTRICT_W(8);
+    else MSF_RESTRICT_W(16);
+#undef MSF_RESTRICT_W
+    MSF_LAUNCHED(c);
+    return;
+  }
   // threads per agglomerate CTA: 256 measured fastest (512 / 1024: 19 / 40 us vs 15 us at one
   // realisation on configs[1]; larger block reductions, fewer CTAs per SM)
   const int ntr = c->restrict_threads > 0 ? c->restrict_threads : 256;

@@ -214,7 +214,8 @@ struct msf_ctx {
   double* iface_mat = nullptr;  // [R][2nI-1][mc*mc] interface D blocks, then U (all-reduced)
   double** ifm_pack = nullptr;  // [2][3R] src, dst: this rank's interface D, D, U shares
   double** ifm_unpack = nullptr;// [2][(2nI-1)R] src, dst
-  int* agg_by_cls_d = nullptr;  // agglomerates grouped by class
+  int* agg_by_cls_d = nullptr;  // restriction work list (agglomerates in grid order)
+  bool restrict_warp = true;    // restriction one warp per agglomerate (env MSF_RESTRICT_WARP=0)
   std::vector<int> agg_by_cls_h;
   // top system after the truncated cyclic reduction: T active blocks (stride top_stride),
   // dense inverse stored block-major [R][T][T][mc*mc] as -Top^{-1}
