@@ -19,7 +19,8 @@ def main(path):
         u = r[ui]
         v = v * 1e3 if u in ("us", "usecond") else (v * 1e6 if u in ("ms", "msecond") else v)
         seq.append((r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", ""), v))
-    starts = [i for i, (k, _) in enumerate(seq) if k.startswith(("k_apply<0", "k_apply_direct<0"))]
+    starts = [i for i, (k, _) in enumerate(seq)
+              if k.startswith(("k_apply<0", "k_apply_direct<0", "k_apply_tma<0", "k_apply_sw<0"))]
     agg, cnt, tot = collections.defaultdict(float), collections.defaultdict(int), 0.0
     for a, b in zip(starts[:-1], starts[1:]):
         for k, v in seq[a:b]:
