@@ -105,6 +105,102 @@ __device__ void cta_inverse(double* S, int m, double* rowk, double* colk, int* s
   __syncthreads();
 }
 
+// The same SPD inverse by the BLOCK sweep operator, pivot blocks K of IB = 8: with P = A_KK^-1,
+//   A_ij -= A_iK P A_Kj,  A_iK <- A_iK P,  A_Kj <- P A_Kj,  A_KK <- -P   (i, j outside K),
+// which equals sweeping the pivots of K one by one; after all blocks S = -A^-1 (negated at the
+// end).  3 block barriers per 8 pivots instead of 2 per pivot (cta_inverse: 75% of
+// k_eigen_factor in ncu, configs[1]).  Scratch: sc >= 3 m IB + IB IB doubles.
+constexpr int IB = 8;
+__device__ void cta_inverse_blocked(double* S, int m, double* scr, int* status) {
+  const int tid = threadIdx.x, jl = tid & 31, ig = tid >> 5;
+  constexpr int RG = NT / 32;
+  double* rowK = scr;              // [IB][m]  A_Kj (original)
+  double* Y = rowK + IB * m;       // [m][IB]  A_iK P
+  double* Z = Y + IB * m;          // [IB][m]  P A_Kj
+  double* Pb = Z + IB * m;         // [IB][IB] -P after the warp sweep
+  for (int k0 = 0; k0 < m; k0 += IB) {
+    const int bk = min(IB, m - k0);
+    for (int e = tid; e < bk * m; e += NT) {
+      const int b = e / m, j = e - b * m;
+      rowK[b * m + j] = S[(k0 + b) * m + j];
+    }
+    __syncthreads();
+    if (ig == 0) {
+      // warp 0: sweep of the bk x bk pivot block -> Pb = -A_KK^-1
+      for (int e = jl; e < bk * bk; e += 32) Pb[e] = rowK[(e / bk) * m + k0 + e % bk];
+      __syncwarp();
+      for (int k = 0; k < bk; ++k) {
+        const double piv = Pb[k * bk + k];
+        if (!(piv > 0.0) && jl == 0) atomicExch(status, 2);
+        const double ip = 1.0 / piv;
+        double nv[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int e = jl + 32 * q;
+          if (e < bk * bk) {
+            const int i = e / bk, j = e - (e / bk) * bk;
+            const double aij = Pb[e], aik = Pb[i * bk + k], akj = Pb[k * bk + j];
+            nv[q] = (i == k) ? ((j == k) ? -ip : akj * ip) : ((j == k) ? aik * ip : fma(-aik * ip, akj, aij));
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (jl + 32 * q < bk * bk) Pb[jl + 32 * q] = nv[q];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // Y = A_iK P, Z = P A_Kj  (P = -Pb)
+    for (int e = tid; e < m * bk; e += NT) {
+      const int i = e / bk, b = e - (e / bk) * bk;
+      double y = 0.0;
+      for (int c = 0; c < bk; ++c) y = fma(S[i * m + k0 + c], -Pb[c * bk + b], y);
+      Y[i * IB + b] = y;
+    }
+    for (int e = tid; e < bk * m; e += NT) {
+      const int b = e / m, j = e - b * m;
+      double z = 0.0;
+      for (int c = 0; c < bk; ++c) z = fma(-Pb[b * bk + c], rowK[c * m + j], z);
+      Z[b * m + j] = z;
+    }
+    __syncthreads();
+    // S update; the thread's columns j = jl + 32 u keep their A_Kj in registers
+    double rk[3][IB];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int j = jl + 32 * u;
+#pragma unroll
+      for (int b = 0; b < IB; ++b) rk[u][b] = (j < m && b < bk) ? rowK[b * m + j] : 0.0;
+    }
+    for (int i = ig; i < m; i += RG) {
+      const bool iK = i >= k0 && i < k0 + bk;
+      double yi[IB];
+#pragma unroll
+      for (int b = 0; b < IB; ++b) yi[b] = b < bk ? Y[i * IB + b] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int j = jl + 32 * u;
+        if (j >= m) continue;
+        const bool jK = j >= k0 && j < k0 + bk;
+        double v;
+        if (iK && jK) v = Pb[(i - k0) * bk + (j - k0)];
+        else if (iK) v = Z[(i - k0) * m + j];
+        else if (jK) v = Y[i * IB + (j - k0)];
+        else {
+          v = S[i * m + j];
+#pragma unroll
+          for (int b = 0; b < IB; ++b) v = fma(-yi[b], rk[u][b], v);
+        }
+        S[i * m + j] = v;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < m * m; e += NT) S[e] = -S[e];
+  __syncthreads();
+}
+
 __device__ __forceinline__ double hash_uniform(unsigned long long x) {
   x += 0x9E3779B97F4A7C15ull;
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -253,7 +349,10 @@ __device__ void small_gen_eig(double* G, double* H, int mb, double* theta, doubl
 // Thread-block cluster per class: EIG_CL CTAs share the per-iteration work of one class
 // (8x the threads of a single CTA on these latency-bound loops); phases are separated by
 // cluster barriers (release / acquire: global writes of one CTA are visible to the others).
-constexpr int EIG_CL = 8;
+#ifndef MSF_EIG_CL
+#define MSF_EIG_CL 8
+#endif
+constexpr int EIG_CL = MSF_EIG_CL;   // <= 8: the workspace holds 8 x 16 residual partials per class
 
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
@@ -362,7 +461,9 @@ __global__ void __launch_bounds__(NT) k_eigen_factor(Dims d, K0Mat K, const doub
         smem_gemm44(T, 1, ml, Wv, S, ml, -1.0, 1.0);                 // S -= U^T W
       }
       __syncthreads();
-      cta_inverse(S, ml, rowk, colk, status);
+      // T and Wv are dead here (W_I is in global memory): scratch of the blocked inverse
+      if (ml <= 96) cta_inverse_blocked(S, ml, T, status);
+      else cta_inverse(S, ml, rowk, colk, status);
       double* SI = Sinv + (size_t)I * ml * ml;
       for (int e = threadIdx.x; e < ml * ml; e += NT) {
         SI[e] = S[e];
