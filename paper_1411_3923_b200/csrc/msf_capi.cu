@@ -557,6 +557,7 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (const char* e = std::getenv("MSF_APPLY_TMA")) c->apply_tma = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_RESIDUAL_TMA")) c->residual_tma = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_RESTRICT_WARP")) c->restrict_warp = std::string(e) != "0";
+  if (const char* e = std::getenv("MSF_INV_BLOCKED_SMEM")) c->inv_blocked_smem = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_SW_KX")) {
     const int k = std::atoi(e);
     c->apply_sw_kx = (k == 2 || k == 4 || k == 8) ? k : 0;

@@ -581,6 +581,20 @@ __global__ void __launch_bounds__(1024) k_spd_inverse_smem(double** mats, int m,
   for (int e = tid; e < m * m; e += 1024) A[e] = -S[e];
 }
 
+// The same inverses by the blocked sweep (msfk::inverse_blocked, 8-pivot panels, 512 threads):
+// 3 barriers per 8 pivots instead of 2 per pivot; m <= 160 with the matrix and the panel
+// scratch in shared memory.
+__global__ void __launch_bounds__(512) k_spd_inverse_smem_blk(double** mats, int m, int* status) {
+  extern __shared__ double smi[];
+  double* S = smi;              // [m*m]
+  double* scr = S + m * m;      // [3 m IB + IB IB]
+  double* A = mats[blockIdx.x];
+  for (int e = threadIdx.x; e < m * m; e += 512) S[e] = A[e];
+  __syncthreads();
+  msfinv::inverse_blocked<512, 5>(S, m, scr, status, 1);
+  for (int e = threadIdx.x; e < m * m; e += 512) A[e] = S[e];
+}
+
 __global__ void k_copy_blocks(double** src, double** dst, int m) {
   const double* s = src[blockIdx.y];
   double* t = dst[blockIdx.y];
@@ -857,6 +871,12 @@ static void launch_spd_inverse(msf_ctx* c, double** mats, int n, int m) {
       k_binv_panels<<<dim3(T, 2, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_P, c->binv_R);
       c->launches += 4;
     }
+  } else if (c->inv_blocked_smem && m <= 160 &&
+             (size_t)(m * m + 3 * m * msfinv::IB + msfinv::IB * msfinv::IB) * sizeof(double) <= 220 * 1024) {
+    const size_t smem = (size_t)(m * m + 3 * m * msfinv::IB + msfinv::IB * msfinv::IB) * sizeof(double);
+    cudaFuncSetAttribute(k_spd_inverse_smem_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_spd_inverse_smem_blk<<<n, 512, smem, c->stream>>>(mats, m, c->factor_status);
+    MSF_LAUNCHED(c);
   } else if ((size_t)(m * m + 2 * m) * sizeof(double) <= 200 * 1024) {
     const size_t smem = (size_t)(m * m + 2 * m) * sizeof(double);
     cudaFuncSetAttribute(k_spd_inverse_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -5,6 +5,7 @@
 #pragma once
 
 #include "msf_internal.cuh"
+#include "msf_inverse.cuh"
 
 namespace msfk {
 
