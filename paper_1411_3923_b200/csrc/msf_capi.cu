@@ -1,5 +1,6 @@
 // C ABI of the B200 MsFEM-PCG library (include/msfem_b200.h): host-side plan, workspace
 // carving, PCG driver (one PCG iteration captured once as a CUDA graph), design step.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -748,6 +749,15 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->cb, 0, 2 * R * d.nbc * (size_t)d.mc * 8, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->Dc, 0, 2 * R * d.nbc * (size_t)d.mc * d.mc * 8, c->stream);
   if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
+  {
+    const char* e = std::getenv("MSF_CUBLAS");
+    cublasHandle_t h = nullptr;
+    if (ce == cudaSuccess && !(e && std::string(e) == "0") && cublasCreate(&h) == CUBLAS_STATUS_SUCCESS) {
+      cublasSetStream(h, c->stream);
+      cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);   // plain fp64 (no emulation, no reduced precision)
+      c->cublas = h;
+    }
+  }
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->sc_host, MSF_MAX_RHS * sizeof(PcgScalars));
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->scal_host, 80 * 8);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
@@ -775,6 +785,7 @@ int msf_destroy(msf_ctx* c) {
   dist_comm_destroy(c);
   destroy_graphs(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->cublas) cublasDestroy((cublasHandle_t)c->cublas);
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->scal_host) cudaFreeHost(c->scal_host);
   delete c;
@@ -784,6 +795,7 @@ int msf_destroy(msf_ctx* c) {
 int msf_set_stream(msf_ctx* c, void* stream) {
   if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
   c->stream = (cudaStream_t)stream;
+  if (c->cublas) cublasSetStream((cublasHandle_t)c->cublas, c->stream);
   destroy_graphs(c);
   return MSF_OK;
 }

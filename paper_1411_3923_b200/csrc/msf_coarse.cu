@@ -9,6 +9,8 @@
 //     exact coarse solve by block cyclic reduction: per level the odd blocks are
 //     eliminated with explicit SPD inverses (batched sweep operator) and batched GEMMs,
 //     so every level is parallel across blocks and realisations.
+#include <cublas_v2.h>
+
 #include "msf_kern.cuh"
 
 #include <algorithm>
@@ -888,24 +890,36 @@ static void launch_spd_inverse(msf_ctx* c, double** mats, int n, int m) {
   }
 }
 
+// Batched m x m products of the K_c factorisation, row-major C = alpha op(A) op(B) + beta C over
+// device pointer tables.  cuBLAS batched DGEMM (a plain library GEMM, outside the PCG path;
+// column-major: C^T = op(B)^T op(A)^T), or the hand-written k_gemm (MSF_CUBLAS=0).  configs[3]:
+// the products were 67% of a 1.86 s assembly at about 23% of the FP64 peak.
+template <bool TA, bool TB>
+static void gemm_batched(msf_ctx* c, double** As, double** Bs, double** Cs, int m, double alpha,
+                         double beta, int count) {
+  if (count <= 0) return;
+  if (c->cublas) {
+    cublasDgemmBatched((cublasHandle_t)c->cublas, TB ? CUBLAS_OP_T : CUBLAS_OP_N,
+                       TA ? CUBLAS_OP_T : CUBLAS_OP_N, m, m, m, &alpha, (const double* const*)Bs, m,
+                       (const double* const*)As, m, &beta, Cs, m, count);
+    return;
+  }
+  const dim3 gt((m + 63) / 64, (m + 63) / 64, count);
+  k_gemm<TA, TB><<<gt, 256, 0, c->stream>>>(As, Bs, Cs, m, alpha, beta);
+  MSF_LAUNCHED(c);
+}
+
 // factorisation of the reduction levels [l0, l1)
 static void assemble_levels(msf_ctx* c, int l0, int l1) {
   const Dims& d = c->d;
   const int m = d.mc;
-  const dim3 gt((m + 63) / 64, (m + 63) / 64);
-  for (int l = l0; l < l1; ++l) {
+    for (int l = l0; l < l1; ++l) {
     const CrLevel& L = c->cr[l];
     k_copy_blocks<<<dim3(64, L.n_inv), 256, 0, c->stream>>>(L.invsrc, L.inv, m);
     MSF_LAUNCHED(c);
     launch_spd_inverse(c, L.inv, L.n_inv, m);
-    if (L.nP) {
-      k_gemm<false, false><<<dim3(gt.x, gt.y, L.nP), 256, 0, c->stream>>>(L.pA, L.pB, L.pC, m, 1.0, 0.0);
-      MSF_LAUNCHED(c);
-    }
-    if (L.nQ) {
-      k_gemm<true, false><<<dim3(gt.x, gt.y, L.nQ), 256, 0, c->stream>>>(L.qA, L.qB, L.qC, m, 1.0, 0.0);
-      MSF_LAUNCHED(c);
-    }
+    gemm_batched<false, false>(c, L.pA, L.pB, L.pC, m, 1.0, 0.0, L.nP);
+    gemm_batched<true, false>(c, L.qA, L.qB, L.qC, m, 1.0, 0.0, L.nQ);
     {
       const dim3 tg((m + 31) / 32, (m + 31) / 32, L.nP);
       k_transpose_blocks<<<tg, dim3(32, 8), 0, c->stream>>>(L.pC, c->Pc, c->PTc, m);
@@ -916,18 +930,9 @@ static void assemble_levels(msf_ctx* c, int l0, int l1) {
         MSF_LAUNCHED(c);
       }
     }
-    if (L.nDl) {
-      k_gemm<false, true><<<dim3(gt.x, gt.y, L.nDl), 256, 0, c->stream>>>(L.dlA, L.dlB, L.dlC, m, -1.0, 1.0);
-      MSF_LAUNCHED(c);
-    }
-    if (L.nDr) {
-      k_gemm<false, false><<<dim3(gt.x, gt.y, L.nDr), 256, 0, c->stream>>>(L.drA, L.drB, L.drC, m, -1.0, 1.0);
-      MSF_LAUNCHED(c);
-    }
-    if (L.nU) {
-      k_gemm<false, false><<<dim3(gt.x, gt.y, L.nU), 256, 0, c->stream>>>(L.uA, L.uB, L.uC, m, -1.0, 0.0);
-      MSF_LAUNCHED(c);
-    }
+    gemm_batched<false, true>(c, L.dlA, L.dlB, L.dlC, m, -1.0, 1.0, L.nDl);
+    gemm_batched<false, false>(c, L.drA, L.drB, L.drC, m, -1.0, 1.0, L.nDr);
+    gemm_batched<false, false>(c, L.uA, L.uB, L.uC, m, -1.0, 0.0, L.nU);
   }
 }
 
@@ -958,8 +963,7 @@ void launch_assemble_top(msf_ctx* c) {
   assemble_levels(c, c->n_local, (int)c->cr.size());
   const Dims& d = c->d;
   const int m = d.mc;
-  const dim3 gt((m + 63) / 64, (m + 63) / 64);
-  // dense inverse of the remaining top system by block Gauss-Jordan (block sweep operator):
+    // dense inverse of the remaining top system by block Gauss-Jordan (block sweep operator):
   // pivot k: Pk = A_kk^-1, W_i = A_ik Pk, A_ij -= W_i A_kj, A_ik = W_i, A_ki = W_i^T,
   // A_kk = -Pk; after all pivots A = -Top^-1.
   const int T = c->top_T;
@@ -975,14 +979,8 @@ void launch_assemble_top(msf_ctx* c) {
     MSF_LAUNCHED(c);
     launch_spd_inverse(c, S.inv, S.nI, m);
     MSF_LAUNCHED(c);
-    if (S.nW) {
-      k_gemm<false, false><<<dim3(gt.x, gt.y, S.nW), 256, 0, c->stream>>>(S.wA, S.wB, S.wC, m, 1.0, 0.0);
-      MSF_LAUNCHED(c);
-    }
-    if (S.nU) {
-      k_gemm<false, false><<<dim3(gt.x, gt.y, S.nU), 256, 0, c->stream>>>(S.uA, S.uB, S.uC, m, -1.0, 1.0);
-      MSF_LAUNCHED(c);
-    }
+    gemm_batched<false, false>(c, S.wA, S.wB, S.wC, m, 1.0, 0.0, S.nW);
+    gemm_batched<false, false>(c, S.uA, S.uB, S.uC, m, -1.0, 1.0, S.nU);
     if (S.nC) {
       k_copy_blocks_ex<false><<<dim3(tg.x, tg.y, S.nC), dim3(32, 8), 0, c->stream>>>(S.cps, S.cpd, m, 1.0);
       MSF_LAUNCHED(c);

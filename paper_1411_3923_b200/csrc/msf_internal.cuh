@@ -239,6 +239,8 @@ struct msf_ctx {
   double* binv_P = nullptr;     // blocked inverse scratch: [n_max][64*64] pivot inverses
   double* binv_R = nullptr;     //                          [n_max][64*m] row panels
   int blocked_inv_min = 256;
+  void* cublas = nullptr;       // cublasHandle_t of the factorisation GEMMs (null: k_gemm;
+                                // env MSF_CUBLAS=0)
   bool inv_blocked_smem = true; // m x m inverses below blocked_inv_min: blocked sweep in shared
                                 // memory (env MSF_INV_BLOCKED_SMEM=0: pivot-by-pivot sweep)
   int restrict_threads = 0;
