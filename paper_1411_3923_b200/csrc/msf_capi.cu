@@ -337,6 +337,8 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     P.binv_n = nmax;
     add(nmax * 64 * 64 * 8);
     add(nmax * 64 * (size_t)d.mc * 8);
+    add(nmax * 64 * (size_t)d.mc * 8);       // pivot column copies
+    add(2 * nmax * sizeof(double*));         // their pointer tables
   }
   add(R * sizeof(PcgScalars));
   add((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
@@ -551,6 +553,9 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
   c->binv_P = (double*)take(P.binv_n * 64 * 64 * 8);
   c->binv_R = (double*)take(P.binv_n * 64 * (size_t)d.mc * 8);
+  c->binv_C = (double*)take(P.binv_n * 64 * (size_t)d.mc * 8);
+  c->binv_Rp = (double**)take(2 * P.binv_n * sizeof(double*));
+  c->binv_Cp = c->binv_Rp + P.binv_n;
   if (const char* e = std::getenv("MSF_BLOCKED_INV_MIN")) c->blocked_inv_min = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("MSF_RESTRICT_THREADS")) c->restrict_threads = std::atoi(e);
   if (const char* e = std::getenv("MSF_APPLY_DIRECT")) c->apply_direct = std::string(e) != "0";
@@ -740,6 +745,12 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->factor_status, 0, 2 * MSF_MAX_RHS * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->counters, 0, R * 8 * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->sc, 0, R * sizeof(PcgScalars), c->stream);
+  std::vector<double*> binv_ptrs(2 * P.binv_n);
+  for (size_t i = 0; i < P.binv_n; ++i) {
+    binv_ptrs[i] = c->binv_R + i * 64 * (size_t)d.mc;
+    binv_ptrs[P.binv_n + i] = c->binv_C + i * 64 * (size_t)d.mc;
+  }
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->binv_Rp, binv_ptrs.data(), binv_ptrs.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->scal, 0, 64 * 8, c->stream);
   if (ce == cudaSuccess && c->dsum) ce = cudaMemsetAsync(c->dsum, 0, FIN_KINDS * MSF_MAX_RHS * 8, c->stream);
   // node vectors start at 0 (halo / padding columns are only ever written by exchanges)

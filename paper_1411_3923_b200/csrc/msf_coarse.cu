@@ -518,10 +518,24 @@ __global__ void __launch_bounds__(256) k_binv_trailing(double** mats, int m, int
   gemm_tile_store(A + (size_t)i0 * m + j0, m, min(64, m - i0), min(64, m - j0), acc, -1.0, 1.0);
 }
 
+// Cbuf[m][64] (per matrix) = A[:, p cols]: the pivot column panel, copied before a full-matrix
+// trailing GEMM (cuBLAS path) modifies it
+__global__ void __launch_bounds__(256) k_binv_colcopy(double** mats, int m, int p0, int pb, double* Cbuf) {
+  const double* A = mats[blockIdx.y];
+  double* Cp = Cbuf + (size_t)blockIdx.y * m * GB;
+  for (int e = blockIdx.x * 256 + threadIdx.x; e < m * pb; e += gridDim.x * 256) {
+    const int r = e / pb, cc = e - (e / pb) * pb;
+    Cp[(size_t)r * GB + cc] = A[(size_t)r * m + p0 + cc];
+  }
+}
+
 // y = 0: A[i-tile, p cols] = -A[i-tile, p cols] P (i-tile != p), A_pp = P (i-tile == p)
 // y = 1: A[p rows, j-tile] = R[:, j-tile] (j-tile != p)
+// (Cbuf non-null: the p columns are read from the copy Cbuf, the trailing GEMM having updated
+// the whole matrix)
 __global__ void __launch_bounds__(256) k_binv_panels(double** mats, int m, int p0, int pb,
-                                                     const double* Pbuf, const double* Rbuf) {
+                                                     const double* Pbuf, const double* Rbuf,
+                                                     const double* Cbuf) {
   __shared__ double As[64][33];
   __shared__ double Bs[32][65];
   double* A = mats[blockIdx.z];
@@ -536,7 +550,8 @@ __global__ void __launch_bounds__(256) k_binv_panels(double** mats, int m, int p
       return;
     }
     double acc[4][4] = {};
-    gemm_tile_acc(A + (size_t)t0 * m + p0, m, P, GB, tn, pb, pb, acc, As, Bs);
+    if (Cbuf) gemm_tile_acc(Cbuf + (size_t)blockIdx.z * m * GB + (size_t)t0 * GB, GB, P, GB, tn, pb, pb, acc, As, Bs);
+    else gemm_tile_acc(A + (size_t)t0 * m + p0, m, P, GB, tn, pb, pb, acc, As, Bs);
     gemm_tile_store(A + (size_t)t0 * m + p0, m, tn, pb, acc, -1.0, 0.0);
   } else {
     if (t == pt) return;
@@ -869,9 +884,23 @@ static void launch_spd_inverse(msf_ctx* c, double** mats, int n, int m) {
       const int p0 = pt * GB, pb = std::min(GB, m - p0);
       k_binv_pivot<<<n, 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_P, c->factor_status);
       k_binv_rowpanel<<<dim3(T, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_P, c->binv_R);
-      k_binv_trailing<<<dim3(T, T, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_R);
-      k_binv_panels<<<dim3(T, 2, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_P, c->binv_R);
-      c->launches += 4;
+      if (c->cublas && c->binv_Cp) {
+        // trailing update A -= A[:, p] R as one batched GEMM over the whole matrix (the p row and
+        // column panels are rewritten by k_binv_panels from R and the column copy):
+        // column-major A^T -= R^T Cp^T
+        k_binv_colcopy<<<dim3((m * pb + 255) / 256 < 64 ? (m * pb + 255) / 256 : 64, n), 256, 0, c->stream>>>(
+            mats, m, p0, pb, c->binv_C);
+        const double mone = -1.0, one = 1.0;
+        cublasDgemmBatched((cublasHandle_t)c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, m, m, pb, &mone,
+                           (const double* const*)c->binv_Rp, m, (const double* const*)c->binv_Cp, GB, &one,
+                           mats, m, n);
+        k_binv_panels<<<dim3(T, 2, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_P, c->binv_R, c->binv_C);
+        c->launches += 4;
+      } else {
+        k_binv_trailing<<<dim3(T, T, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_R);
+        k_binv_panels<<<dim3(T, 2, n), 256, 0, c->stream>>>(mats, m, p0, pb, c->binv_P, c->binv_R, nullptr);
+        c->launches += 4;
+      }
     }
   } else if (c->inv_blocked_smem && m <= 160 &&
              (size_t)(m * m + 3 * m * msfinv::IB + msfinv::IB * msfinv::IB) * sizeof(double) <= 220 * 1024) {

@@ -238,6 +238,9 @@ struct msf_ctx {
   int* factor_status = nullptr; // [R] nonzero on failed pivot
   double* binv_P = nullptr;     // blocked inverse scratch: [n_max][64*64] pivot inverses
   double* binv_R = nullptr;     //                          [n_max][64*m] row panels
+  double* binv_C = nullptr;     //                          [n_max][m*64] pivot column copies
+  double** binv_Rp = nullptr;   // [n_max] device pointers to the R / C panels (cuBLAS trailing
+  double** binv_Cp = nullptr;   // update; null when m < blocked_inv_min everywhere)
   int blocked_inv_min = 256;
   void* cublas = nullptr;       // cublasHandle_t of the factorisation GEMMs (null: k_gemm;
                                 // env MSF_CUBLAS=0)
