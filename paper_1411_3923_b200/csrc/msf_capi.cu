@@ -78,6 +78,7 @@ struct Plan {
   std::vector<int> top_blocks;
   size_t top_ptrs = 0;
   size_t binv_n = 1;          // matrices per blocked-inverse batch (scratch sizing)
+  size_t galerkin_G_doubles = 0;
   size_t jobs_bytes = 0;
   int max_partials = 0;
   size_t total = 0;
@@ -310,6 +311,13 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   add(P.classes.size() * d.kmax * 8);        // lam
   add((size_t)P.eig_doubles * 8);            // eig work
   add(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);     // Kcell
+  {
+    // G scratch of the GEMM Galerkin products: up to 32M doubles, at least one cell
+    const size_t per_cell = (size_t)5 * d.cx * d.cy * 4 * d.kmax;
+    const size_t cells = std::max<size_t>(1, std::min<size_t>((size_t)d.ncx * d.ncy, (32u << 20) / per_cell));
+    P.galerkin_G_doubles = cells * per_cell;
+    add(P.galerkin_G_doubles * 8);
+  }
   add(7 * R * d.nbc * (size_t)d.mc * d.mc * 8);           // Dc Uc Dinv Pc Qc PTc QTc
   add(2 * R * d.nbc * (size_t)d.mc * 8);     // cb, cx
   {
@@ -503,6 +511,8 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   c->lam = (double*)take((size_t)c->n_cls * d.kmax * 8);
   c->eig_work = (double*)take((size_t)P.eig_doubles * 8);
   c->Kcell = (double*)take(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);
+  c->galerkin_G_doubles = P.galerkin_G_doubles;
+  c->galerkin_G = (double*)take(P.galerkin_G_doubles * 8);
   const size_t blk = R * d.nbc * (size_t)d.mc * d.mc;
   double* cm = (double*)take(7 * blk * 8);
   c->Dc = cm; c->Uc = cm + blk; c->Dinv = cm + 2 * blk; c->Pc = cm + 3 * blk; c->Qc = cm + 4 * blk;
@@ -564,6 +574,7 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (const char* e = std::getenv("MSF_RESIDUAL_TMA")) c->residual_tma = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_RESTRICT_WARP")) c->restrict_warp = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_INV_BLOCKED_SMEM")) c->inv_blocked_smem = std::string(e) != "0";
+  if (const char* e = std::getenv("MSF_GALERKIN_GEMM")) c->galerkin_gemm = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_SW_KX")) {
     const int k = std::atoi(e);
     c->apply_sw_kx = (k == 2 || k == 4 || k == 8) ? k : 0;

@@ -14,6 +14,7 @@
 #include "msf_kern.cuh"
 
 #include <algorithm>
+#include <cmath>
 
 using namespace msfk;
 
@@ -292,6 +293,50 @@ __global__ void __launch_bounds__(NT) k_cell_galerkin(Dims d, K0Mat K, const dou
 #pragma unroll
       for (int r = 0; r < MSF_MAX_RHS; ++r)
         if (r < R) Kcell[((size_t)r * d.ncx * d.ncy + cell) * P * P + (size_t)(p0 + p) * P + (q0 + q)] = acc[r];
+  }
+}
+
+// Galerkin products as one GEMM per cell (the same sum, re-associated): with K0 = L^T L
+// (L = Lambda^1/2 Q^T over the 5 nonzero eigenpairs of the element matrix, host),
+//   Kcell = sum_e E_e Phi_e^T K0 Phi_e = G^T G,   G = [sqrt(E_e) L Phi_e]_e   ((5 nel) x P),
+// G built here (columns in chunks of CH staged like k_cell_galerkin), G^T G by cuBLAS strided
+// batched DGEMM over the cells of a chunk.  (k_cell_galerkin: 3-5% of the FP64 peak on
+// configs[3] / [4], 232 / 41 ms.)
+struct LMat {
+  double v[5 * 8];
+};
+__global__ void __launch_bounds__(NT) k_galerkin_G(Dims d, LMat L, const double* __restrict__ Eall,
+                                                   const double* __restrict__ phi,
+                                                   const int* __restrict__ cls_of_agg, int rhs,
+                                                   int cell0, int CH, double* G) {
+  extern __shared__ double gsm[];   // [ncn * 2][CH]
+  const int cell = cell0 + blockIdx.x;
+  const int CI = cell / d.ncy, CJ = cell - (cell / d.ncy) * d.ncy;
+  const int P = 4 * d.kmax, p0 = blockIdx.z * CH, pw = min(CH, P - p0);
+  const int ncn_y = d.cy + 1, nel = d.cx * d.cy;
+  stage_cell_cols(d, phi, cls_of_agg, CI, CJ, p0, pw, CH, gsm);
+  __syncthreads();
+  double* Gc = G + (size_t)blockIdx.x * 5 * nel * P;
+  const double* E = Eall + (size_t)rhs * d.ne;
+  for (int k = threadIdx.x; k < nel * CH; k += NT) {
+    const int el = k / CH, q = k - (k / CH) * CH;
+    if (q >= pw) continue;
+    const int lex = el / d.cy, ley = el - (el / d.cy) * d.cy;
+    const double se = sqrt(E[(size_t)(CI * d.cx + lex) * d.nely + CJ * d.cy + ley]);
+    double ph[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int b = i >> 1, comp = i & 1;
+      const int nx = lex + ((b == 1 || b == 2) ? 1 : 0), ny = ley + ((b >= 2) ? 1 : 0);
+      ph[i] = gsm[((nx * ncn_y + ny) * 2 + comp) * CH + q];
+    }
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+      double t = 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t = fma(L.v[l * 8 + i], ph[i], t);
+      Gc[((size_t)el * 5 + l) * P + p0 + q] = se * t;
+    }
   }
 }
 
@@ -846,9 +891,104 @@ void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
   MSF_LAUNCHED(c);
 }
 
+// Factor K0 = L^T L: Jacobi eigendecomposition of the 8 x 8 element matrix, the 5 eigenpairs
+// above the rigid-body null space.  Returns false if the rank is not 5.
+static bool factor_K0(const K0Mat& K, LMat& L) {
+  double A[8][8], V[8][8];
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      A[i][j] = K.v[i * 8 + j];
+      V[i][j] = i == j ? 1.0 : 0.0;
+    }
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int i = 0; i < 8; ++i)
+      for (int j = i + 1; j < 8; ++j) off += A[i][j] * A[i][j];
+    if (off < 1e-30) break;
+    for (int p = 0; p < 8; ++p)
+      for (int q = p + 1; q < 8; ++q) {
+        if (std::fabs(A[p][q]) < 1e-300) continue;
+        const double th = (A[q][q] - A[p][p]) / (2.0 * A[p][q]);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < 8; ++k) {
+          const double akp = A[k][p], akq = A[k][q];
+          A[k][p] = cs * akp - sn * akq;
+          A[k][q] = sn * akp + cs * akq;
+        }
+        for (int k = 0; k < 8; ++k) {
+          const double apk = A[p][k], aqk = A[q][k];
+          A[p][k] = cs * apk - sn * aqk;
+          A[q][k] = sn * apk + cs * aqk;
+        }
+        for (int k = 0; k < 8; ++k) {
+          const double vkp = V[k][p], vkq = V[k][q];
+          V[k][p] = cs * vkp - sn * vkq;
+          V[k][q] = sn * vkp + cs * vkq;
+        }
+      }
+  }
+  double lmax = 0.0;
+  for (int i = 0; i < 8; ++i) lmax = std::max(lmax, A[i][i]);
+  int l = 0;
+  for (int i = 0; i < 8; ++i) {
+    if (A[i][i] <= 1e-12 * lmax) continue;
+    if (l == 5) return false;
+    const double sq = std::sqrt(A[i][i]);
+    for (int k = 0; k < 8; ++k) L.v[l * 8 + k] = sq * V[k][i];
+    ++l;
+  }
+  return l == 5;
+}
+
+static bool galerkin_gemm(msf_ctx* c) {
+  const Dims& d = c->d;
+  // large cell products only: configs[3] (256 elements x 64 columns) 0.78 -> 0.56 s assembly,
+  // configs[4] (400 x 16) 122 -> 117 ms; at 256 x 16 (configs[1]) the per-cell kernel wins
+  if (!c->cublas || !c->galerkin_gemm || !c->galerkin_G || d.cx * d.cy * 4 * d.kmax < 5000) return false;
+  static thread_local LMat L;
+  static thread_local double Lnu = -1.0;
+  if (Lnu != c->p.nu) {
+    if (!factor_K0(c->K0, L)) return false;
+    Lnu = c->p.nu;
+  }
+  const int P = 4 * d.kmax, nel = d.cx * d.cy;
+  const size_t per_cell = (size_t)5 * nel * P;
+  const int CH = std::min(P, 16);
+  const int nch = (P + CH - 1) / CH;
+  const size_t smem = (size_t)(d.cx + 1) * (d.cy + 1) * 2 * CH * sizeof(double);
+  cudaFuncSetAttribute(k_galerkin_G, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int c_lo = c->cell_lo * d.ncy, c_hi = c->cell_hi * d.ncy;
+  const int chunk = (int)std::max<size_t>(1, c->galerkin_G_doubles / per_cell);
+  for (int r = 0; r < d.R; ++r)
+    for (int c0 = c_lo; c0 < c_hi; c0 += chunk) {
+      const int nc = std::min(chunk, c_hi - c0);
+      k_galerkin_G<<<dim3(nc, 1, nch), NT, smem, c->stream>>>(d, L, c->E, c->phi, c->cls_of_agg_d, r, c0, CH,
+                                                             c->galerkin_G);
+      MSF_LAUNCHED(c);
+      // Kcell (P x P, symmetric) = G^T G; G row-major (5 nel) x P = column-major G^T (P x 5 nel)
+      const double one = 1.0, zero = 0.0;
+      double* Kc = c->Kcell + ((size_t)r * d.ncx * d.ncy + c0) * P * P;
+      cublasDgemmStridedBatched((cublasHandle_t)c->cublas, CUBLAS_OP_N, CUBLAS_OP_T, P, P, 5 * nel, &one,
+                                c->galerkin_G, P, (long long)per_cell, c->galerkin_G, P, (long long)per_cell,
+                                &zero, Kc, P, (long long)P * P, nc);
+    }
+  return true;
+}
+
 void launch_coarse_galerkin(msf_ctx* c) {
   const Dims& d = c->d;
   const int P = 4 * d.kmax;
+  if (galerkin_gemm(c)) {
+    const int nD = c->cr_hi - c->cr_lo + 1, nU = c->cell_hi - c->cell_lo;
+    const size_t total = (size_t)(nD + nU) * d.mc * d.mc;
+    int blocks = (int)std::min<size_t>((total + 255) / 256, 65535);
+    k_coarse_gather<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->Kcell, c->cls_of_agg_d,
+                                                              c->classes_d, c->Dc, c->Uc, c->cr_lo, nD,
+                                                              c->cell_lo, nU, c->id_lo, c->id_hi);
+    MSF_LAUNCHED(c);
+    return;
+  }
   const size_t ncn2 = (size_t)(d.cx + 1) * (d.cy + 1) * 2;
   // largest column chunk whose staged bases fit in shared memory (<= 16 so CH^2 <= NT)
   int CH = std::min(P, 16);

@@ -242,6 +242,9 @@ struct msf_ctx {
   double** binv_Rp = nullptr;   // [n_max] device pointers to the R / C panels (cuBLAS trailing
   double** binv_Cp = nullptr;   // update; null when m < blocked_inv_min everywhere)
   int blocked_inv_min = 256;
+  bool galerkin_gemm = true;    // Galerkin cell products as G^T G by cuBLAS (env MSF_GALERKIN_GEMM=0)
+  double* galerkin_G = nullptr; // scratch for G of a chunk of cells
+  size_t galerkin_G_doubles = 0;
   void* cublas = nullptr;       // cublasHandle_t of the factorisation GEMMs (null: k_gemm;
                                 // env MSF_CUBLAS=0)
   bool inv_blocked_smem = true; // m x m inverses below blocked_inv_min: blocked sweep in shared
