@@ -194,11 +194,28 @@ def test_coarse_basis_spans_and_eigenvalues(name):
             assert span_distance(got, ref) <= 1e-7, (I, J)
 
 
+# cells large enough (elements x basis columns >= 5000) for the G^T G / cuBLAS Galerkin products
+GALERKIN_GEMM_SPECS = {
+    "cells20_60x40": W.small_spec(nelx=60, nely=40, cx=20, cy=20, tile=(20, 20), rmin=1.5, beta=4.0,
+                                  etas=(0.6, 0.4), dilated=1, seed=33, Emin=1e-6),
+    "cells16_modes6_48x32": W.small_spec(nelx=48, nely=32, cx=16, cy=16, n_modes=6, bc="mbb", seed=34),
+}
+
+
 @pytest.mark.parametrize("name", list(SPECS))
 def test_galerkin_coarse_matrix(name):
     """K_c blocks equal R_g A R_g^T computed by the oracle's sparse product from the
     GPU basis (checks the per-cell dense contraction and the block gather)."""
-    spec = SPECS[name]
+    check_galerkin(SPECS[name])
+
+
+@pytest.mark.parametrize("name", list(GALERKIN_GEMM_SPECS))
+def test_galerkin_coarse_matrix_gemm_path(name):
+    """The same check on cells that take the G^T G (cuBLAS) Galerkin path."""
+    check_galerkin(GALERKIN_GEMM_SPECS[name])
+
+
+def check_galerkin(spec):
     m, x = ctx_for(spec)
     m.build_coarse_basis()
     m.assemble_coarse()
