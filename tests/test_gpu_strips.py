@@ -42,6 +42,9 @@ STRIP_SPECS = {
     "ragged_36x20": (SPECS["ragged_36x20"], (2, 3)),
     # cx odd: ranks with and without padding
     "odd_30x12": (W.small_spec(nelx=30, nely=12, cx=3, cy=3, seed=41, Emin=1e-6), (3, 4)),
+    # 20 x 20-element cells: the G^T G (cuBLAS) Galerkin products over each rank's cells
+    "cells20_60x40": (W.small_spec(nelx=60, nely=40, cx=20, cy=20, tile=(20, 20), rmin=1.5, beta=4.0,
+                                   etas=(0.6, 0.4), dilated=1, seed=33, Emin=1e-6), (2, 3)),
 }
 CASES = [(n, r) for n, (_, rs) in STRIP_SPECS.items() for r in rs]
 
