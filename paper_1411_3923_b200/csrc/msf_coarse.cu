@@ -1067,7 +1067,7 @@ template <bool TA, bool TB>
 static void gemm_batched(msf_ctx* c, double** As, double** Bs, double** Cs, int m, double alpha,
                          double beta, int count) {
   if (count <= 0) return;
-  if (c->cublas) {
+  if (c->cublas && m >= 64) {   // small blocks (configs[0]: m = 28) stay on k_gemm
     cublasDgemmBatched((cublasHandle_t)c->cublas, TB ? CUBLAS_OP_T : CUBLAS_OP_N,
                        TA ? CUBLAS_OP_T : CUBLAS_OP_N, m, m, m, &alpha, (const double* const*)Bs, m,
                        (const double* const*)As, m, &beta, Cs, m, count);
