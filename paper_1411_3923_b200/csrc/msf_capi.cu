@@ -75,6 +75,8 @@ struct Plan {
   std::vector<CrLevel> cr;
   int n_local = 0;            // chain levels (the rest: interface levels, strips only)
   std::vector<int> iface;     // interface blocks (strips only)
+  int nslot = 0;              // stored K_c blocks per realisation
+  std::vector<int> slot;      // [nbc] storage slot of each block (-1: not stored)
   std::vector<int> top_blocks;
   size_t top_ptrs = 0;
   size_t binv_n = 1;          // matrices per blocked-inverse batch (scratch sizing)
@@ -269,6 +271,20 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     P.iface.push_back(d.ncx);
     P.top_blocks = reduce(P.iface, (size_t)top_max, false);
   }
+  // storage slots of the K_c factor blocks: all blocks on one GPU; a strip keeps its chain
+  // (slots 0..) and the remaining interface blocks (memory about 1/nranks of the blocks)
+  P.slot.assign(d.nbc, -1);
+  if (nranks == 1) {
+    for (int i = 0; i < d.nbc; ++i) P.slot[i] = i;
+    P.nslot = d.nbc;
+  } else {
+    const int lo = P.sb.C0, hi = (rank == nranks - 1) ? d.ncx : P.sb.C1;
+    int ns = 0;
+    for (int i = lo; i <= hi; ++i) P.slot[i] = ns++;
+    for (int i : P.iface)
+      if (P.slot[i] < 0) P.slot[i] = ns++;
+    P.nslot = ns;
+  }
   size_t ptrs = 0, ints = 0;
   for (CrLevel& L : P.cr) {
     int nq = 0;
@@ -318,7 +334,8 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     P.galerkin_G_doubles = cells * per_cell;
     add(P.galerkin_G_doubles * 8);
   }
-  add(7 * R * d.nbc * (size_t)d.mc * d.mc * 8);           // Dc Uc Dinv Pc Qc PTc QTc
+  add(7 * R * (size_t)P.nslot * d.mc * d.mc * 8);          // Dc Uc Dinv Pc Qc PTc QTc
+  add((size_t)d.nbc * 4);                                  // slot map
   add(2 * R * d.nbc * (size_t)d.mc * 8);     // cb, cx
   {
     const size_t nI = P.iface.size(), mm = (size_t)d.mc * d.mc;
@@ -513,8 +530,11 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   c->Kcell = (double*)take(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);
   c->galerkin_G_doubles = P.galerkin_G_doubles;
   c->galerkin_G = (double*)take(P.galerkin_G_doubles * 8);
-  const size_t blk = R * d.nbc * (size_t)d.mc * d.mc;
+  c->nslot = P.nslot;
+  c->slot_h = P.slot;
+  const size_t blk = R * (size_t)P.nslot * d.mc * d.mc;
   double* cm = (double*)take(7 * blk * 8);
+  c->slot_d = (int*)take((size_t)d.nbc * 4);
   c->Dc = cm; c->Uc = cm + blk; c->Dinv = cm + 2 * blk; c->Pc = cm + 3 * blk; c->Qc = cm + 4 * blk;
   c->PTc = cm + 5 * blk; c->QTc = cm + 6 * blk;
   c->cb = (double*)take(2 * R * d.nbc * (size_t)d.mc * 8);
@@ -595,7 +615,7 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     std::vector<double*> ptrs;
     std::vector<int> ints;
     const size_t per = (size_t)d.mc * d.mc;
-    auto B = [&](double* base, int rhs, int k) { return base + ((size_t)rhs * d.nbc + k) * per; };
+    auto B = [&](double* base, int rhs, int k) { return base + ((size_t)rhs * c->nslot + c->slot_h[k]) * per; };
     struct Fix { size_t inv, P, Q, Dl, Dr, U, elim, surv; };
     std::vector<Fix> fixes;
     for (CrLevel& L : c->cr) {
@@ -706,16 +726,16 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
       auto S = [&](int rhs, size_t j) { return c->iface_mat + ((size_t)rhs * (2 * nI - 1) + j) * mmb; };
       const int a = rank, b = rank + 1;
       for (int rhs = 0; rhs < d.R; ++rhs) {
-        ip.push_back(c->Dc + ((size_t)rhs * d.nbc + c->iface[a]) * mmb);
-        ip.push_back(c->Dc + ((size_t)rhs * d.nbc + c->iface[b]) * mmb);
-        ip.push_back(c->Uc + ((size_t)rhs * d.nbc + c->iface[a]) * mmb);
+        ip.push_back(c->Dc + ((size_t)rhs * c->nslot + c->slot_h[c->iface[a]]) * mmb);
+        ip.push_back(c->Dc + ((size_t)rhs * c->nslot + c->slot_h[c->iface[b]]) * mmb);
+        ip.push_back(c->Uc + ((size_t)rhs * c->nslot + c->slot_h[c->iface[a]]) * mmb);
       }
       for (int rhs = 0; rhs < d.R; ++rhs) { ip.push_back(S(rhs, a)); ip.push_back(S(rhs, b)); ip.push_back(S(rhs, nI + a)); }
       for (int rhs = 0; rhs < d.R; ++rhs)
         for (size_t j = 0; j < 2 * nI - 1; ++j) iu.push_back(S(rhs, j));
       for (int rhs = 0; rhs < d.R; ++rhs)
         for (size_t j = 0; j < 2 * nI - 1; ++j)
-          iu.push_back((j < nI ? c->Dc : c->Uc) + ((size_t)rhs * d.nbc + c->iface[j < nI ? j : j - nI]) * mmb);
+          iu.push_back((j < nI ? c->Dc : c->Uc) + ((size_t)rhs * c->nslot + c->slot_h[c->iface[j < nI ? j : j - nI]]) * mmb);
       cudaMemcpyAsync(c->ifm_pack, ip.data(), ip.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
       cudaMemcpyAsync(c->ifm_unpack, iu.data(), iu.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
       cudaMemcpyAsync(c->iface_d, c->iface.data(), nI * 4, cudaMemcpyHostToDevice, c->stream);
@@ -769,7 +789,8 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   // coarse vectors and K_c blocks start at 0: a strip reads (with zero weights) the coarse
   // solution of the blocks next to its chain, which it never writes
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->cb, 0, 2 * R * d.nbc * (size_t)d.mc * 8, c->stream);
-  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->Dc, 0, 2 * R * d.nbc * (size_t)d.mc * d.mc * 8, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->Dc, 0, 2 * R * (size_t)c->nslot * d.mc * d.mc * 8, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->slot_d, c->slot_h.data(), d.nbc * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
   {
     const char* e = std::getenv("MSF_CUBLAS");

@@ -348,7 +348,8 @@ __global__ void __launch_bounds__(NT) k_galerkin_G(Dims d, LMat L, const double*
 __global__ void k_coarse_gather(Dims d, const double* __restrict__ Kcell,
                                 const int* __restrict__ cls_of_agg,
                                 const EigClass* __restrict__ cls, double* Dall, double* Uall,
-                                int dlo, int nD, int ulo, int nU, int idlo, int idhi) {
+                                int dlo, int nD, int ulo, int nU, int idlo, int idhi, int slot0,
+                                int nslot) {
   const int km = d.kmax, P = 4 * km, m = d.mc;
   const size_t per = (size_t)m * m;
   const size_t total = (size_t)(nD + nU) * per;
@@ -379,7 +380,7 @@ __global__ void k_coarse_gather(Dims d, const double* __restrict__ Kcell,
           v += Kc[((size_t)CI * d.ncy + CJ) * P * P + (size_t)pr * P + pc];
         }
     }
-    double* dst = (isU ? Uall : Dall) + ((size_t)rhs * d.nbc + I) * per;
+    double* dst = (isU ? Uall : Dall) + ((size_t)rhs * nslot + (I - slot0)) * per;   // chain slots
     dst[e] = v;
   }
 }
@@ -723,6 +724,7 @@ __global__ void __launch_bounds__(256) k_gemm(double** As, double** Bs, double**
 // ------------------------------------------------------------------ cyclic-reduction solve
 // forward, survivors i (jobs [i, il, ir]): b_i -= Q_il b_il + P_ir b_ir
 __global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restrict__ surv,
+                                                    const int* __restrict__ slot, int nslot,
                                                     const double* __restrict__ Qall,
                                                     const double* __restrict__ Pall,
                                                     double* cball, const PcgScalars* sc,
@@ -733,13 +735,17 @@ __global__ void __launch_bounds__(256) k_cr_forward(Dims d, const int* __restric
   const int* job = surv + 3 * blockIdx.y;
   const int i = job[0], il = job[1], ir = job[2];
   const size_t per = (size_t)d.mc * d.mc;
-  cr_forward_rows(d, i, il, ir, blockIdx.x * CR_ROWS, Qall + ((size_t)rhs * d.nbc + max(il, 0)) * per,
-                  Pall + ((size_t)rhs * d.nbc + max(ir, 0)) * per, cball + (size_t)rhs * d.nbc * d.mc,
+  // matrices by storage slot (a strip stores its chain and the interface blocks only),
+  // vectors by global block
+  const int sl = il >= 0 ? slot[il] : 0, sr = ir >= 0 ? slot[ir] : 0;
+  cr_forward_rows(d, i, il, ir, blockIdx.x * CR_ROWS, Qall + ((size_t)rhs * nslot + sl) * per,
+                  Pall + ((size_t)rhs * nslot + sr) * per, cball + (size_t)rhs * d.nbc * d.mc,
                   sv, threadIdx.x, blockDim.x, gated ? &sc[rhs].active : nullptr);
 }
 
 // back, eliminated k (jobs [k, kl, kr]): x_k = Dinv_k b_k - P_k^T x_kl - Q_k^T x_kr
 __global__ void __launch_bounds__(256) k_cr_back(Dims d, const int* __restrict__ elim,
+                                                 const int* __restrict__ slot, int nslot,
                                                  const double* __restrict__ Dinv,
                                                  const double* __restrict__ PTall,
                                                  const double* __restrict__ QTall,
@@ -751,7 +757,7 @@ __global__ void __launch_bounds__(256) k_cr_back(Dims d, const int* __restrict__
   const int* job = elim + 3 * blockIdx.y;
   const int k = job[0], kl = job[1], kr = job[2];
   const size_t per = (size_t)d.mc * d.mc;
-  const size_t blk = ((size_t)rhs * d.nbc + k) * per;
+  const size_t blk = ((size_t)rhs * nslot + slot[k]) * per;
   cr_back_rows(d, k, kl, kr, blockIdx.x * CR_ROWS, Dinv + blk, PTall + blk, QTall + blk,
                cball + (size_t)rhs * d.nbc * d.mc, cxall + (size_t)rhs * d.nbc * d.mc, sv,
                threadIdx.x, blockDim.x, gated ? &sc[rhs].active : nullptr);
@@ -778,7 +784,8 @@ __global__ void k_transpose_blocks(double** src, const double* src_base, double*
 // Top (T*m x T*m, block-major) from the diagonal / coupling blocks of the active blocks tb[]
 // left after the truncated cyclic reduction.
 __global__ void k_build_top(Dims d, const int* __restrict__ tb, int T, const double* __restrict__ Dall,
-                            const double* __restrict__ Uall, double* Atop) {
+                            const double* __restrict__ Uall, double* Atop, const int* __restrict__ slot,
+                            int nslot) {
   const int rhs = blockIdx.y, m = d.mc;
   const size_t mm = (size_t)m * m, per = (size_t)T * T * mm;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < per;
@@ -786,10 +793,10 @@ __global__ void k_build_top(Dims d, const int* __restrict__ tb, int T, const dou
     const int blk = (int)(e / mm), w = (int)(e - (size_t)blk * mm);
     const int bi = blk / T, bj = blk - bi * T, rr = w / m, cc = w - (w / m) * m;
     double v = 0.0;
-    const size_t base = (size_t)rhs * d.nbc;
-    if (bi == bj) v = Dall[(base + tb[bi]) * mm + (size_t)rr * m + cc];
-    else if (bj == bi + 1) v = Uall[(base + tb[bi]) * mm + (size_t)rr * m + cc];
-    else if (bi == bj + 1) v = Uall[(base + tb[bj]) * mm + (size_t)cc * m + rr];
+    const size_t base = (size_t)rhs * nslot;
+    if (bi == bj) v = Dall[(base + slot[tb[bi]]) * mm + (size_t)rr * m + cc];
+    else if (bj == bi + 1) v = Uall[(base + slot[tb[bi]]) * mm + (size_t)rr * m + cc];
+    else if (bi == bj + 1) v = Uall[(base + slot[tb[bj]]) * mm + (size_t)cc * m + rr];
     Atop[(size_t)rhs * per + e] = v;
   }
 }
@@ -985,7 +992,8 @@ void launch_coarse_galerkin(msf_ctx* c) {
     int blocks = (int)std::min<size_t>((total + 255) / 256, 65535);
     k_coarse_gather<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->Kcell, c->cls_of_agg_d,
                                                               c->classes_d, c->Dc, c->Uc, c->cr_lo, nD,
-                                                              c->cell_lo, nU, c->id_lo, c->id_hi);
+                                                              c->cell_lo, nU, c->id_lo, c->id_hi, c->cr_lo,
+                                                              c->nslot);
     MSF_LAUNCHED(c);
     return;
   }
@@ -1010,7 +1018,8 @@ void launch_coarse_galerkin(msf_ctx* c) {
     int blocks = (int)std::min<size_t>((total + 255) / 256, 65535);
     k_coarse_gather<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->Kcell, c->cls_of_agg_d,
                                                               c->classes_d, c->Dc, c->Uc, c->cr_lo, nD,
-                                                              c->cell_lo, nU, c->id_lo, c->id_hi);
+                                                              c->cell_lo, nU, c->id_lo, c->id_hi, c->cr_lo,
+                                                              c->nslot);
     MSF_LAUNCHED(c);
   }
 }
@@ -1139,7 +1148,8 @@ void launch_assemble_top(msf_ctx* c) {
   {
     const size_t per = (size_t)T * T * m * m;
     const int blocks = (int)std::min<size_t>((per + 255) / 256, 65535);
-    k_build_top<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->top_blocks_d, T, c->Dc, c->Uc, c->Atop);
+    k_build_top<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->top_blocks_d, T, c->Dc, c->Uc, c->Atop,
+                                                          c->slot_d, c->nslot);
     MSF_LAUNCHED(c);
   }
   const dim3 tg((m + 31) / 32, (m + 31) / 32);
@@ -1180,7 +1190,8 @@ static void cr_forward_levels(msf_ctx* c, int l0, int l1, int rhs0, int nr, bool
     const CrLevel& L = c->cr[l];
     if (L.surv.empty()) continue;
     launch_k(k_cr_forward, dim3((m + CR_ROWS - 1) / CR_ROWS, (unsigned)L.surv.size(), nr), dim3(256),
-             2 * m * sizeof(double), c->stream, d, (const int*)L.surv_d, (const double*)c->Qc,
+             2 * m * sizeof(double), c->stream, d, (const int*)L.surv_d, (const int*)c->slot_d, c->nslot,
+             (const double*)c->Qc,
              (const double*)c->Pc, c->cb, (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
     MSF_LAUNCHED(c);
   }
@@ -1192,7 +1203,8 @@ static void cr_back_levels(msf_ctx* c, int l0, int l1, int rhs0, int nr, bool ga
   for (int l = l1 - 1; l >= l0; --l) {
     const CrLevel& L = c->cr[l];
     launch_k(k_cr_back, dim3((m + CR_ROWS - 1) / CR_ROWS, (unsigned)L.elim.size(), nr), dim3(256),
-             3 * m * sizeof(double), c->stream, d, (const int*)L.elim_d, (const double*)c->Dinv,
+             3 * m * sizeof(double), c->stream, d, (const int*)L.elim_d, (const int*)c->slot_d, c->nslot,
+             (const double*)c->Dinv,
              (const double*)c->PTc, (const double*)c->QTc, (const double*)c->cb, c->cx,
              (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
     MSF_LAUNCHED(c);

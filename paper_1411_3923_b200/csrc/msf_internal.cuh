@@ -200,7 +200,12 @@ struct msf_ctx {
   double* eig_work = nullptr;
 
   double* Kcell = nullptr;      // [R][ncells][(4k)^2]
-  double* Dc = nullptr;         // [R][nbc][mc*mc]
+  // K_c factor blocks are stored per realisation in nslot slots: every block on one GPU
+  // (slot = block), the chain [cr_lo, cr_hi] then the other interface blocks on a strip
+  int nslot = 0;
+  std::vector<int> slot_h;      // [nbc] slot of each block, -1: not stored on this rank
+  int* slot_d = nullptr;
+  double* Dc = nullptr;         // [R][nslot][mc*mc]
   double* Uc = nullptr;         // [R][nbc][mc*mc]
   double* Dinv = nullptr;       // [R][nbc][mc*mc]
   double* Pc = nullptr;         // [R][nbc][mc*mc]
