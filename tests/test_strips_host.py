@@ -152,3 +152,103 @@ def test_gloo_halo_protocol_world2(pkg, spec_kw):
         h1 = min(b["own1"] + 1, spec.nelx + 1) - lo
         np.testing.assert_array_equal(xl[h0:h1], xg.reshape(-1, nny, 2)[lo + h0:lo + h1])
         assert abs(dot - dot_ref) <= 1e-12 * abs(dot_ref)
+
+
+def _cell_couplings(nbc, m, seed):
+    """K_c of a chain of nbc blocks from per-cell SPD couplings [[A_k, B_k], [B_k^T, C_k]]
+    (cell k couples blocks k, k+1), like the Galerkin assembly: D_k = C_{k-1} + A_k."""
+    rng = np.random.default_rng(seed)
+    cells = []
+    for _ in range(nbc - 1):
+        G = rng.standard_normal((2 * m, 3 * m))
+        Kk = G @ G.T + 0.5 * np.eye(2 * m)
+        cells.append(Kk)
+    K = np.zeros((nbc * m, nbc * m))
+    for k, Kk in enumerate(cells):
+        K[k * m:(k + 2) * m, k * m:(k + 2) * m] += Kk
+    return cells, K
+
+
+def _coarse_worker(rank, world, port, bounds, nbc, m, seed, out_q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cells, _ = _cell_couplings(nbc, m, seed)
+        b_glob = np.random.default_rng(seed + 1).standard_normal(nbc * m)
+        C0 = bounds[rank]["C0"]
+        C1 = bounds[rank]["C1"] if rank < world - 1 else nbc - 1
+        # this rank's chain matrix from ITS cells only (end blocks: partial sums)
+        L = C1 - C0 + 1
+        M = np.zeros((L * m, L * m))
+        for k in range(C0, bounds[rank]["C1"]):
+            j = k - C0
+            M[j * m:(j + 2) * m, j * m:(j + 2) * m] += cells[k]
+        # rhs: interior blocks whole, the chain ends split with the neighbour (restriction partials)
+        b = b_glob[C0 * m:(C1 + 1) * m].copy()
+        if rank > 0:
+            b[:m] *= 0.5
+        if rank < world - 1:
+            b[-m:] *= 0.5
+        ends = np.r_[np.arange(m), np.arange((L - 1) * m, L * m)]
+        inner = np.arange(m, (L - 1) * m)
+        Mee, Mei, Mii = M[np.ix_(ends, ends)], M[np.ix_(ends, inner)], M[np.ix_(inner, inner)]
+        if inner.size:
+            S = Mee - Mei @ np.linalg.solve(Mii, Mei.T)
+            g = b[ends] - Mei @ np.linalg.solve(Mii, b[inner])
+        else:
+            S, g = Mee, b[ends]
+        # interface system over the nranks + 1 chain ends, all-reduced
+        nI = world + 1
+        Sg = np.zeros((nI * m, nI * m))
+        gg = np.zeros(nI * m)
+        idx = np.r_[np.arange(rank * m, (rank + 1) * m), np.arange((rank + 1) * m, (rank + 2) * m)]
+        Sg[np.ix_(idx, idx)] = S
+        gg[idx] = g
+        St, gt = torch.from_numpy(Sg), torch.from_numpy(gg)
+        dist.all_reduce(St)
+        dist.all_reduce(gt)
+        xI = np.linalg.solve(St.numpy(), gt.numpy())
+        xe = xI[idx]
+        x = np.zeros(L * m)
+        x[ends] = xe
+        if inner.size:
+            x[inner] = np.linalg.solve(Mii, b[inner] - Mei.T @ xe)
+        out_q.put((rank, C0, C1, x))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nelx,cx", [(2, 16, 2), (3, 18, 2), (2, 12, 4)])
+def test_gloo_distributed_coarse_solve(pkg, world, nelx, cx):
+    """The interface decomposition of the distributed K_c: each rank builds
+    its chain from its own coarse cells (partial end blocks, split end rhs), reduces it to the
+    two ends, the interface system is all-reduced over gloo and solved redundantly, the chain
+    is back-substituted; the chains of all ranks equal the dense solve of the whole K_c.
+    Chain ends come from the library's strip planner."""
+    import torch.multiprocessing as mp
+    spec = W.small_spec(nelx=nelx, nely=4, cx=cx, cy=2)
+    prob = pkg.problem_from_spec(spec)
+    bounds = [pkg.strip_bounds(prob, r, world) for r in range(world)]
+    nbc, m = nelx // cx + 1, 3
+    _, K = _cell_couplings(nbc, m, seed=11)
+    b_glob = np.random.default_rng(12).standard_normal(nbc * m)
+    x_ref = np.linalg.solve(K, b_glob)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_coarse_worker, args=(r, world, port, bounds, nbc, m, 11, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    covered = np.zeros(nbc, dtype=int)
+    for rank, C0, C1, x in res:
+        np.testing.assert_allclose(x, x_ref[C0 * m:(C1 + 1) * m], rtol=0, atol=1e-10 * np.abs(x_ref).max())
+        covered[C0:C1 + 1] += 1
+    assert (covered >= 1).all()
