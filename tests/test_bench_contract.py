@@ -51,3 +51,35 @@ def test_our_arm_line():
     assert e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 1000
     assert d["config"]["pcg_iters_per_step"] == [592, 86, 36]
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """The driver's N > 1 launch of the reference arm: rank 0 alone prints one line, every
+    rank exits 0."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port),
+                          os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+                          "--warmup", "0", "--config", "c0_cantilever_96x48"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+@pytest.mark.gpu
+def test_our_arm_strips_mode_one_rank():
+    """The NCCL strip path (1-rank communicator) through bench.py: same workload, iteration
+    counts and a valid line."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    d = run_bench("--mode", "strips", "--steps", "2", "--warmup", "3", "--no-cpu-baseline")
+    assert d["config"]["pcg_iters_per_step"] == [592, 86, 36]
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 1000
