@@ -128,6 +128,43 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+SCALEUP_CONFIG = "c4_mbb_5120x2560"
+
+
+def scaleup_kernels(dev, peak):
+    """Per-kernel times and HBM fractions (msf_bench_kernels, PCG launch configuration) on the
+    north star's ~26M-DOF robust problem (BASELINE configs[4]), at one and three active
+    realisations: evidence for the matvec / preconditioner roofline at that size.  Runs after
+    the timed region on rank 0 of a one-GPU run."""
+    import torch
+    from paper_1411_3923_b200 import Msfem
+    spec = W.CONFIGS[SCALEUP_CONFIG]
+    m = Msfem.from_spec(spec, device=dev)
+    m.filter_project(torch.as_tensor(W.design_tile(spec), device=dev))
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    out = {"workload": SCALEUP_CONFIG, "n_dof": spec.n_dof, "peak_GBps": peak}
+    names = ["apply", "residual", "sgs_colour", "update_f0", "p_update", "restrict", "prolong",
+             "coarse_solve", "vcycle", "pcg_iteration"]
+    for nr in (1, spec.n_rhs):
+        os.environ["MSF_BENCH_NR"] = str(nr)
+        kb = m.bench_kernels(reps=10)
+        tab = {}
+        for k in names:
+            ms, by = kb[k]
+            if ms <= 0:
+                continue
+            per = 7 if k == "sgs_colour" else 1   # one colour launch of the 7-launch sweep
+            gbps = by / per / (ms / per / 1e3) / 1e9
+            tab[k] = {"ms": ms / per, "alg_GBps": gbps, "hbm_frac": gbps / peak}
+        out[f"realisations_{nr}"] = tab
+    os.environ.pop("MSF_BENCH_NR", None)
+    m.close()
+    del m
+    torch.cuda.empty_cache()
+    return out
+
+
 def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -312,6 +349,8 @@ def run_ours(args, spec):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
+        # north star: matvec / preconditioner >= 60% of HBM on 1 B200 for the ~26M-DOF problem
+        "kernels_26M": (scaleup_kernels(dev, peak) if ws == 1 and not args.no_scaleup else None),
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
@@ -327,6 +366,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scaleup", action="store_true",
+                    help="skip the per-kernel table of configs[4] (kernels_26M) after the timed region")
     ap.add_argument("--mode", default="auto", choices=["auto", "strips", "replicas"],
                     help="auto: strip partition when N > 1; strips: NCCL strip path even at N = 1; "
                          "replicas: independent copies per rank")

@@ -51,6 +51,11 @@ def test_our_arm_line():
     assert e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 1000
     assert d["config"]["pcg_iters_per_step"] == [592, 86, 36]
+    k26 = d["kernels_26M"]
+    assert k26["workload"] == "c4_mbb_5120x2560" and k26["n_dof"] == 26229762
+    for nr in ("realisations_1", "realisations_3"):
+        assert {"apply", "sgs_colour", "vcycle", "pcg_iteration"} <= set(k26[nr])
+        assert all(v["hbm_frac"] > 0 for v in k26[nr].values())
 
 
 def test_reference_arm_under_torchrun_two_ranks():
