@@ -62,3 +62,42 @@ def test_edge_pcg_parity(name):
         assert rel(ug[k], ref["us"][k]) <= 1e-8, k
         tc = compliance_tol(spec, ref["E_el"][k], f, fx)
         assert abs(comps[k] - ref["comps"][k]) <= tc * abs(ref["comps"][k]), (k, tc)
+
+
+@pytest.mark.parametrize("env", [{"MSF_PCG_MODE": "persistent"}, {"MSF_COARSE_COOP": "1"},
+                                 {"MSF_PCG_MODE": "stream"}, {"MSF_APPLY_TMA": "0", "MSF_RESIDUAL_TMA": "0"},
+                                 {"MSF_CUBLAS": "0"}])
+def test_opt_in_modes_match_default(env):
+    """The opt-in execution modes (read at context setup) solve
+    the same problem as the default graph path: iterations +-1, solutions to 1e-9."""
+    import os
+    from test_gpu_parity import SPECS
+    spec = SPECS["robust_32x16"]
+    x = W.design_tile(spec)
+
+    def solve():
+        m = Msfem.from_spec(spec)
+        m.filter_project(dev(x))
+        m.build_coarse_basis()
+        m.assemble_coarse()
+        u = torch.empty(spec.n_rhs * spec.n_dof, dtype=torch.float64, device=DEV)
+        its, comps, nc = m.pcg_solve(tol=1e-10, u=u)
+        m.close()
+        return its, comps, host(u), nc
+
+    its0, comps0, u0, _ = solve()
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        its1, comps1, u1, nc = solve()
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert not nc
+    for k in range(spec.n_rhs):
+        assert abs(its1[k] - its0[k]) <= 1, (env, its0, its1)
+        assert abs(comps1[k] - comps0[k]) <= 1e-9 * abs(comps0[k])
+    assert np.linalg.norm(u1 - u0) <= 1e-9 * np.linalg.norm(u0)
