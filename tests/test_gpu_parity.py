@@ -103,6 +103,8 @@ TMA_SPECS = {
     "tma_160x130": W.small_spec(nelx=160, nely=130, cx=10, cy=10, tile=(16, 10), rmin=1.5,
                                 beta=4.0, etas=(0.6, 0.4, 0.3), dilated=2, seed=31),
     "tma_96x252_mbb": W.small_spec(nelx=96, nely=252, cx=8, cy=12, bc="mbb", seed=32),
+    # odd nely (moduli rows not 16-byte aligned): the large-grid fallback kernels
+    "fallback_odd_nely_96x133": W.small_spec(nelx=96, nely=133, cx=8, cy=7, seed=35),
 }
 
 
