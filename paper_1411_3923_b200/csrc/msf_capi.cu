@@ -819,6 +819,22 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     c->sgs_nb_err = (int*)(c->sgs_nb_flags + tiles * MSF_MAX_RHS);
     c->sgs_nb_max_ctas = sgs_nb_max_ctas(c);
   }
+  {
+    // restriction groups of same-class agglomerates (k_restrict_batch), when they batch well
+    const char* e = std::getenv("MSF_RESTRICT_BATCH");
+    const int B = c->dl.kmax <= 4 ? 4 : c->dl.kmax <= 8 ? 2 : 0;
+    if (ce == cudaSuccess && B && !(e && std::string(e) == "0")) {
+      std::vector<int> groups;
+      const int ng = restrict_groups(c->dl, c->agg_by_cls_h, c->cls_of_agg, B, groups);
+      if ((long long)ng * B * 4 <= (long long)c->n_restrict * 5) {   // >= 80% of slots filled
+        ce = cudaMalloc((void**)&c->rgroups_d, groups.size() * 4);
+        if (ce == cudaSuccess)
+          ce = cudaMemcpy(c->rgroups_d, groups.data(), groups.size() * 4, cudaMemcpyHostToDevice);
+        c->n_rgroups = ng;
+        c->rgroup_B = B;
+      }
+    }
+  }
   if (ce == cudaSuccess && c->graph_loop) ce = cudaMallocHost((void**)&c->loop_cnt_host, sizeof(int));
   if (ce == cudaSuccess && c->graph_loop) ce = cudaMalloc((void**)&c->loop_cnt, sizeof(int));
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
@@ -852,6 +868,7 @@ int msf_destroy(msf_ctx* c) {
   if (c->loop_cnt_host) cudaFreeHost(c->loop_cnt_host);
   if (c->loop_cnt) cudaFree(c->loop_cnt);
   if (c->sgs_nb_flags) cudaFree(c->sgs_nb_flags);
+  if (c->rgroups_d) cudaFree(c->rgroups_d);
   delete c;
   return MSF_OK;
 }

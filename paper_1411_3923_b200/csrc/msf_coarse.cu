@@ -9,6 +9,8 @@
 //     exact coarse solve by block cyclic reduction: per level the odd blocks are
 //     eliminated with explicit SPD inverses (batched sweep operator) and batched GEMMs,
 //     so every level is parallel across blocks and realisations.
+#include <array>
+#include <map>
 #include <cublas_v2.h>
 
 #include "msf_kern.cuh"
@@ -140,6 +142,88 @@ __global__ void __launch_bounds__(256) k_restrict_warp(Dims d, const double2* __
       if (lane == a) cball[(size_t)rhs * d.nbc * d.mc + (size_t)agg * d.kmax + a] = v;
     }
   }
+}
+
+// One WARP per group of B agglomerates of the same class and the same clipped box (host:
+// restrict_groups).  The members share the basis, so each lane loads phi_a(node) once and
+// applies it to the B members' t at the same box position: the class-basis traffic through
+// L2/L1, which bounds k_restrict_warp (64 B per node, mode and agglomerate against 16 B of
+// t), falls by B.  Same per-agglomerate sums and summation order as k_restrict_warp.
+template <int KM, int B>
+__global__ void __launch_bounds__(256) k_restrict_batch(Dims d, const double2* __restrict__ tall,
+                                                        const double* __restrict__ phi,
+                                                        const int* __restrict__ cls_of_agg,
+                                                        const int* __restrict__ groups, int n_groups,
+                                                        double* cball, const PcgScalars* sc, int rhs0,
+                                                        int gated) {
+  pdl_launch();
+  pdl_wait();
+  const int rhs = rhs0 + blockIdx.y;
+  if (gated && !sc[rhs].active) return;
+  const int lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (slot >= n_groups) return;
+  int agg[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) agg[b] = __ldg(groups + (size_t)slot * B + b);
+  const int a0 = agg[0];
+  const int I = a0 / (d.ncy + 1), J = a0 - (a0 / (d.ncy + 1)) * (d.ncy + 1);
+  const double2* ph = reinterpret_cast<const double2*>(phi) + (size_t)cls_of_agg[a0] * d.kmax * d.box_nodes;
+  const double2* t = tall + (size_t)rhs * d.nn;
+  const int gx0 = I * d.cx - d.cx - d.gox, gy0 = J * d.cy - d.cy;
+  const int ix_lo = max(1, -gx0), ix_hi = min(d.bx - 2, d.nnx - 1 - gx0);
+  const int iy_lo = max(1, -gy0), iy_hi = min(d.by - 2, d.nny - 1 - gy0);
+  const int w = iy_hi - iy_lo + 1, h = ix_hi - ix_lo + 1;
+  long long toff[B];   // t offset of each member's box origin (padding slots repeat member 0)
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int ab = agg[b] >= 0 ? agg[b] : a0;
+    const int Ib = ab / (d.ncy + 1), Jb = ab - (ab / (d.ncy + 1)) * (d.ncy + 1);
+    toff[b] = (long long)(Ib * d.cx - d.cx - d.gox) * d.nny + (Jb * d.cy - d.cy);
+  }
+  double acc[B][KM];
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int a = 0; a < KM; ++a) acc[b][a] = 0.0;
+  int px = lane / w, py = lane - (lane / w) * w;
+  const int step_x = 32 / w, step_y = 32 - (32 / w) * w;
+  const int n = w * h;
+#pragma unroll 2
+  for (int k = lane; k < n; k += 32) {
+    const int bx = ix_lo + px, by = iy_lo + py;
+    const int bn = bx * d.by + by;
+    double2 pv[KM];
+#pragma unroll
+    for (int a = 0; a < KM; ++a)
+      pv[a] = a < d.kmax ? __ldg(ph + (size_t)a * d.box_nodes + bn) : make_double2(0.0, 0.0);
+    const long long rel = (long long)bx * d.nny + by;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const double2 tv = t[toff[b] + rel];
+#pragma unroll
+      for (int a = 0; a < KM; ++a)
+        if (a < d.kmax) acc[b][a] = fma(pv[a].x, tv.x, fma(pv[a].y, tv.y, acc[b][a]));
+    }
+    px += step_x;
+    py += step_y;
+    if (py >= w) {
+      py -= w;
+      ++px;
+    }
+  }
+  double* cb = cball + (size_t)rhs * d.nbc * d.mc;
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int a = 0; a < KM; ++a) {
+      if (a < d.kmax) {
+        double v = acc[b][a];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == ((b * KM + a) & 31) && agg[b] >= 0) cb[(size_t)agg[b] * d.kmax + a] = v;
+      }
+    }
 }
 
 // ------------------------------------------------------------------ per-realisation prolongation
@@ -843,6 +927,39 @@ __global__ void __launch_bounds__(256) k_top_solve(Dims d, const int* __restrict
 }  // namespace
 
 // ================================================================== host side
+// Restriction groups for k_restrict_batch: the work list (grid order) split into groups of B
+// agglomerates with the same class and the same clipped box, each group filled in grid order
+// (members of a periodic class lie a period apart, so the group's boxes are close in memory).
+// Returns the number of groups; groups (n x B, padded with -1).
+int restrict_groups(const Dims& d, const std::vector<int>& work, const std::vector<int>& cls,
+                    int B, std::vector<int>& groups) {
+  groups.clear();
+  std::map<std::array<int, 5>, int> open;   // key -> group being filled
+  for (int a : work) {
+    const int I = a / (d.ncy + 1), J = a % (d.ncy + 1);
+    const int gx0 = I * d.cx - d.cx - d.gox, gy0 = J * d.cy - d.cy;
+    const std::array<int, 5> key = {cls[a], std::max(1, -gx0), std::min(d.bx - 2, d.nnx - 1 - gx0),
+                                    std::max(1, -gy0), std::min(d.by - 2, d.nny - 1 - gy0)};
+    auto it = open.find(key);
+    int gi;
+    if (it == open.end()) {
+      gi = (int)(groups.size() / B);
+      groups.resize(groups.size() + B, -1);
+    } else {
+      gi = it->second;
+    }
+    int* g = groups.data() + (size_t)gi * B;
+    int fill = 0;
+    while (g[fill] >= 0) ++fill;
+    g[fill] = a;
+    if (fill + 1 == B)
+      open.erase(key);
+    else
+      open[key] = gi;
+  }
+  return (int)(groups.size() / B);
+}
+
 void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) {
   // global coarse fields, this rank's node columns; a strip restricts the agglomerates of its
   // chain [cr_lo, cr_hi] (the chain's end blocks get the partial sums of its owned nodes)
@@ -860,6 +977,22 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
   // one warp per agglomerate when that gives >= 32 warps per SM (configs[4]: 320 -> 230 us per
   // launch); otherwise one CTA per agglomerate (configs[1] at one realisation, 2145 warps:
   // 15 vs 20 us)
+  // same-class groups when they still give >= 1000 warps: configs[4] 224 -> 178 us at one
+  // realisation (664 -> 495 at three), configs[1] at three realisations 37 -> 23 us; with
+  // fewer warps (configs[1], one realisation: 537) the per-agglomerate CTAs below are faster
+  // (15 vs 22 us)
+  if (c->n_rgroups > 0 && (long long)c->n_rgroups * nr >= 1000) {
+#define MSF_RESTRICT_B(KM, B)                                                                      \
+  launch_k(k_restrict_batch<KM, B>, dim3((c->n_rgroups + 7) / 8, nr), dim3(256), 0, c->stream, d,   \
+           (const double2*)t, (const double*)c->phi, (const int*)c->cls_of_agg_d,                     \
+           (const int*)c->rgroups_d, c->n_rgroups, c->cb, (const PcgScalars*)c->sc, rhs0,            \
+           gated ? 1 : 0)
+    if (c->rgroup_B == 4) MSF_RESTRICT_B(4, 4);
+    else MSF_RESTRICT_B(8, 2);
+#undef MSF_RESTRICT_B
+    MSF_LAUNCHED(c);
+    return;
+  }
   if (c->restrict_warp && (long long)c->n_restrict * nr >= 32LL * 148) {
 #define MSF_RESTRICT_W(KM)                                                                         \
   launch_k(k_restrict_warp<KM>, dim3((c->n_restrict + 7) / 8, nr), dim3(256), 0, c->stream, d,        \

@@ -221,6 +221,10 @@ struct msf_ctx {
   double** ifm_unpack = nullptr;// [2][(2nI-1)R] src, dst
   int* agg_by_cls_d = nullptr;  // restriction work list (agglomerates in grid order)
   bool restrict_warp = true;    // restriction one warp per agglomerate (env MSF_RESTRICT_WARP=0)
+  // restriction one warp per group of same-class agglomerates (k_restrict_batch; env
+  // MSF_RESTRICT_BATCH=0: off); n_rgroups = 0 when not used
+  int n_rgroups = 0, rgroup_B = 0;
+  int* rgroups_d = nullptr;
   std::vector<int> agg_by_cls_h;
   // top system after the truncated cyclic reduction: T active blocks (stride top_stride),
   // dense inverse stored block-major [R][T][T][mc*mc] as -Top^{-1}
@@ -306,6 +310,8 @@ struct msf_ctx {
   int sgs_nb_max_ctas = 0;
 };
 int sgs_nb_max_ctas(msf_ctx* c);
+int restrict_groups(const Dims& d, const std::vector<int>& work, const std::vector<int>& cls,
+                    int B, std::vector<int>& groups);
 
 // ---------------------------------------------------------------- launch bookkeeping
 #define MSF_LAUNCHED(ctx) ((ctx)->launches++)
