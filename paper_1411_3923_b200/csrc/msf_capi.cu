@@ -223,7 +223,9 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
         P.cls_of_agg[agg] = it->second;
       }
     }
-  P.mb = std::min(d.kmax + 8, MSF_MAX_BLOCK_EIG);
+  int guard = 8;   // guard vectors of the subspace iteration (env MSF_EIG_GUARD)
+  if (const char* e = std::getenv("MSF_EIG_GUARD")) guard = std::max(1, std::atoi(e));
+  P.mb = std::min(d.kmax + guard, MSF_MAX_BLOCK_EIG);
   P.mb = std::min(P.mb, min_free);
   if (P.mb < d.kmax) { msg = "an agglomerate has fewer free DOFs than n_modes"; return MSF_ERR_ARG; }
   P.eig_doubles = 0;
@@ -826,7 +828,9 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     if (ce == cudaSuccess && B && !(e && std::string(e) == "0")) {
       std::vector<int> groups;
       const int ng = restrict_groups(c->dl, c->agg_by_cls_h, c->cls_of_agg, B, groups);
-      if ((long long)ng * B * 4 <= (long long)c->n_restrict * 5) {   // >= 80% of slots filled
+      const bool force = e && std::string(e) == "force";   // tests: every launch, any fill
+      c->rgroup_force = force;
+      if (force || (long long)ng * B * 4 <= (long long)c->n_restrict * 5) {   // >= 80% filled
         ce = cudaMalloc((void**)&c->rgroups_d, groups.size() * 4);
         if (ce == cudaSuccess)
           ce = cudaMemcpy(c->rgroups_d, groups.data(), groups.size() * 4, cudaMemcpyHostToDevice);

@@ -981,7 +981,7 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
   // realisation (664 -> 495 at three), configs[1] at three realisations 37 -> 23 us; with
   // fewer warps (configs[1], one realisation: 537) the per-agglomerate CTAs below are faster
   // (15 vs 22 us)
-  if (c->n_rgroups > 0 && (long long)c->n_rgroups * nr >= 1000) {
+  if (c->n_rgroups > 0 && ((long long)c->n_rgroups * nr >= 1000 || c->rgroup_force)) {
 #define MSF_RESTRICT_B(KM, B)                                                                      \
   launch_k(k_restrict_batch<KM, B>, dim3((c->n_rgroups + 7) / 8, nr), dim3(256), 0, c->stream, d,   \
            (const double2*)t, (const double*)c->phi, (const int*)c->cls_of_agg_d,                     \

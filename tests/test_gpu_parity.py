@@ -406,3 +406,39 @@ def test_threshold_mode_contrast_flat():
         assert abs(it[0] - ref["iters"][0]) <= 1
         its.append(it[0])
     assert max(its) - min(its) <= 0.2 * max(its) + 2
+
+
+GROUPED_SPECS = {
+    "robust_32x16": SPECS["robust_32x16"],
+    "ragged_36x20": SPECS["ragged_36x20"],   # 5 modes: groups of 2
+    "periodic_48x24": W.small_spec(nelx=48, nely=24, cx=4, cy=4, tile=(8, 8), rmin=1.5, beta=4.0,
+                                   etas=(0.6, 0.4), dilated=1, bc="mbb", seed=25),
+}
+
+
+@pytest.mark.parametrize("name", list(GROUPED_SPECS))
+def test_grouped_restriction(name, monkeypatch):
+    """The restriction over groups of same-class agglomerates (k_restrict_batch, forced on
+    every launch) gives the oracle's two-level preconditioner (R8) and the oracle's PCG
+    iteration counts (+-1) on periodic designs, boundary-clipped boxes included."""
+    monkeypatch.setenv("MSF_RESTRICT_BATCH", "force")
+    spec = GROUPED_SPECS[name]
+    m, x = ctx_for(spec)
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    fx, f, K0, E, A, _ = oracle_setup(spec, x)
+    R, _ = msfem.build_coarse_basis(spec.nelx, spec.nely, spec.cx, spec.cy, spec.n_modes,
+                                    E[spec.dilated], K0, fx)
+    groups = msfem.gs_groups(spec.nelx, spec.nely, fx)
+    for k in range(spec.n_rhs):
+        M = msfem.TwoLevelPreconditioner(A[k], R, groups, fx)
+        r = W.random_vectors(spec.n_dof, 1, seed=30 + k)[0]
+        r[fx == 1] = 0
+        z = torch.empty(spec.n_dof, dtype=torch.float64, device=DEV)
+        m.precond_apply(k, dev(r), z)
+        assert rel(host(z), M(r)) <= 1e-7
+    ref = problem.solve(spec, x, fx, f, tol=1e-8)
+    its, comps, noconv = m.pcg_solve(tol=1e-8)
+    assert not noconv
+    for k in range(spec.n_rhs):
+        assert abs(its[k] - ref["iters"][k]) <= 1, (its, ref["iters"])
