@@ -149,8 +149,15 @@ __global__ void __launch_bounds__(256) k_restrict_warp(Dims d, const double2* __
 // applies it to the B members' t at the same box position: the class-basis traffic through
 // L2/L1, which bounds k_restrict_warp (64 B per node, mode and agglomerate against 16 B of
 // t), falls by B.  Same per-agglomerate sums and summation order as k_restrict_warp.
+#ifndef MSF_RB_MINB
+#define MSF_RB_MINB 2
+#endif
+#ifndef MSF_RB_UNROLL
+#define MSF_RB_UNROLL 1
+#endif
+constexpr int RB_UNROLL = MSF_RB_UNROLL;
 template <int KM, int B>
-__global__ void __launch_bounds__(256) k_restrict_batch(Dims d, const double2* __restrict__ tall,
+__global__ void __launch_bounds__(256, MSF_RB_MINB) k_restrict_batch(Dims d, const double2* __restrict__ tall,
                                                         const double* __restrict__ phi,
                                                         const int* __restrict__ cls_of_agg,
                                                         const int* __restrict__ groups, int n_groups,
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(256) k_restrict_batch(Dims d, const double2* _
   int px = lane / w, py = lane - (lane / w) * w;
   const int step_x = 32 / w, step_y = 32 - (32 / w) * w;
   const int n = w * h;
-#pragma unroll 2
+#pragma unroll RB_UNROLL
   for (int k = lane; k < n; k += 32) {
     const int bx = ix_lo + px, by = iy_lo + py;
     const int bn = bx * d.by + by;
