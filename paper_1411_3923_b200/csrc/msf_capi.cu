@@ -29,11 +29,6 @@ static void destroy_graphs(msf_ctx* c) {
       if (g) cudaGraphExecDestroy(g);
       g = nullptr;
     }
-  for (auto& row : c->loop_graph)
-    for (auto& g : row) {
-      if (g) cudaGraphExecDestroy(g);
-      g = nullptr;
-    }
 }
 
 // programmatic dependent launch for the PCG kernels (launch_k); MSF_PDL=0 disables
@@ -489,8 +484,6 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     c->persistent = (mode && std::string(mode) == "persistent") && transport == 0;
     c->stream_iters = mode && std::string(mode) == "stream";
     if (const char* gi = std::getenv("MSF_GRAPH_ITERS")) c->graph_iters = std::max(1, std::min(64, std::atoi(gi)));
-    if (const char* gl = std::getenv("MSF_GRAPH_LOOP")) c->graph_loop = std::string(gl) == "1";
-    if (transport != 0 || c->graph_iters != 1) c->graph_loop = false;
     const char* cc = std::getenv("MSF_COARSE_COOP");
     c->coarse_coop = transport == 0 && cc && std::string(cc) == "1";   // opt-in: measured slower
     if (std::getenv("MSF_PERSIST_PROFILE")) {   // debug only: phase timeline buffer
@@ -839,8 +832,6 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
       }
     }
   }
-  if (ce == cudaSuccess && c->graph_loop) ce = cudaMallocHost((void**)&c->loop_cnt_host, sizeof(int));
-  if (ce == cudaSuccess && c->graph_loop) ce = cudaMalloc((void**)&c->loop_cnt, sizeof(int));
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
   if (ce != cudaSuccess) {
     std::string m = std::string("setup: ") + cudaGetErrorString(ce);
@@ -869,8 +860,6 @@ int msf_destroy(msf_ctx* c) {
   if (c->cublas) cublasDestroy((cublasHandle_t)c->cublas);
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->scal_host) cudaFreeHost(c->scal_host);
-  if (c->loop_cnt_host) cudaFreeHost(c->loop_cnt_host);
-  if (c->loop_cnt) cudaFree(c->loop_cnt);
   if (c->sgs_nb_flags) cudaFree(c->sgs_nb_flags);
   if (c->rgroups_d) cudaFree(c->rgroups_d);
   delete c;
@@ -1259,99 +1248,9 @@ static int range_graph(msf_ctx* c, int rhs0, int nr, cudaGraphExec_t* out) {
   return MSF_OK;
 }
 
-// Graph for the realisations [rhs0, rhs0 + nr) whose WHILE node repeats one PCG iteration
-// (the body, captured with its programmatic dependent launches) until k_pcg_p clears the
-// condition: the active count of the range changed (a realisation converged or hit max_it).
-// Returns nonzero when the driver or toolkit rejects any step; the caller then falls back to
-// the host-polled range graphs.
-static int loop_graph(msf_ctx* c, int rhs0, int nr, cudaGraphExec_t* out) {
-  cudaGraphExec_t& slot = c->loop_graph[rhs0][nr];
-  if (!slot) {
-    cudaGraph_t g = nullptr;
-    if (cudaGraphCreate(&g, 0) != cudaSuccess) return 1;
-    cudaGraphConditionalHandle h;
-    cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
-    cudaGraphNode_t node;
-    cudaGraphNodeParams np{};
-    np.type = cudaGraphNodeTypeConditional;
-    np.conditional.handle = h;
-    np.conditional.type = cudaGraphCondTypeWhile;
-    np.conditional.size = 1;
-    if (e == cudaSuccess) e = cudaGraphAddNode(&node, g, nullptr, 0, &np);
-    cudaGraph_t body = e == cudaSuccess ? np.conditional.phGraph_out[0] : nullptr;
-    cudaStream_t user = c->stream;
-    if (e == cudaSuccess) {
-      c->stream = c->cap_stream;
-      e = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
-                                        cudaStreamCaptureModeThreadLocal);
-      const long long before = c->launches;
-      if (e == cudaSuccess) {
-        c->loop_cond = (unsigned long long)h;
-        enqueue_iteration(c, rhs0, nr);
-        c->loop_cond = 0;
-        c->pcg_launches = c->launches - before;
-        cudaGraph_t cap = nullptr;
-        e = cudaStreamEndCapture(c->stream, &cap);
-      }
-      c->launches = before;
-      c->stream = user;
-    }
-    if (e == cudaSuccess) e = cudaGraphInstantiate(&slot, g, 0);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) {
-      std::fprintf(stderr, "msfem: device-side PCG loop unavailable (%s); host-polled graphs\n",
-                   cudaGetErrorString(e));
-      cudaGetLastError();
-      slot = nullptr;
-      return 1;
-    }
-  }
-  *out = slot;
-  return 0;
-}
-
-// The iterations of a range run on the device until its active set changes; the host then
-// reads the scalars, narrows the range and launches the next range's loop.
-static int run_loop_iterations(msf_ctx* c, int nr, int max_it) {
-  int lo = 0, hi = nr, cnt = nr;
-  int before[MSF_MAX_RHS] = {0, 0, 0, 0};
-  for (int launches = 0; launches <= max_it + 1; ++launches) {
-    cudaGraphExec_t g = nullptr;
-    if (loop_graph(c, lo, hi - lo, &g)) {
-      if (launches == 0) return -1;   // not supported here: host-polled graphs instead
-      return msf_fail(c, MSF_ERR_CUDA, "device-side PCG loop graph failed after its first use");
-    }
-    *c->loop_cnt_host = cnt;
-    CK(cudaMemcpyAsync(c->loop_cnt, c->loop_cnt_host, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaGraphLaunch(g, c->stream));
-    int rc = read_scalars(c, nr);
-    if (rc) return rc;
-    int ran = 0;
-    for (int k = lo; k < hi; ++k) ran = std::max(ran, c->sc_host[k].iters - before[k]);
-    for (int k = 0; k < nr; ++k) before[k] = c->sc_host[k].iters;
-    c->launches += c->pcg_launches * ran;
-    lo = nr;
-    hi = -1;
-    cnt = 0;
-    for (int k = 0; k < nr; ++k)
-      if (c->sc_host[k].active) {
-        lo = std::min(lo, k);
-        hi = std::max(hi, k + 1);
-      }
-    if (hi < 0) return MSF_OK;
-    for (int k = lo; k < hi; ++k) cnt += c->sc_host[k].active;
-  }
-  return msf_fail(c, MSF_ERR_CUDA, "device-side PCG loop did not terminate");
-}
-
 // PCG iterations as CUDA-graph launches of one captured iteration; the host polls the
 // device-side `active` flags every 8 iterations (converged realisations are no-ops).
 static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
-  if (c->graph_loop) {
-    int rc = run_loop_iterations(c, nr, max_it);
-    if (rc != -1) return rc;
-    c->graph_loop = false;
-  }
   if (c->stream_iters) {
     // kernels launched directly on the stream (programmatic dependent launches chain them)
     const int check_every = 8;

@@ -801,20 +801,11 @@ __global__ void k_finalize(PcgScalars* sc, const double* __restrict__ dsum, int 
 }
 
 // p = z + beta p  (p = z at init)
-// p = z + beta p.  loop_cond != 0 (inside the device-side iteration loop): block 0 keeps the
-// loop running while the number of active realisations of the range is unchanged.
 __global__ void __launch_bounds__(VB) k_pcg_p(Dims d, const double2* __restrict__ zall,
                                               double2* pall, const PcgScalars* sc, int init,
-                                              int rhs0, unsigned long long loop_cond,
-                                              const int* loop_cnt) {
+                                              int rhs0) {
   pdl_launch();
   pdl_wait();
-  if (loop_cond && blockIdx.x == 0 && blockIdx.z == 0 && threadIdx.x == 0) {
-    int cnt = 0;
-    for (int k = 0; k < (int)gridDim.z; ++k) cnt += sc[rhs0 + k].active;
-    cudaGraphSetConditional((cudaGraphConditionalHandle)loop_cond,
-                            (cnt > 0 && cnt == *loop_cnt) ? 1u : 0u);
-  }
   const int rhs = rhs0 + blockIdx.z;
   if (!sc[rhs].active) return;
   const double beta = init ? 0.0 : sc[rhs].beta;
@@ -1177,7 +1168,7 @@ void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it) {
 void launch_pcg_p(msf_ctx* c, int rhs0, int nr, bool init) {
   launch_k(k_pcg_p, dim3(vec_blocks(c->dl), 1, nr), dim3(VB), 0, c->stream,
            c->dl, (const double2*)c->z, (double2*)c->pv, (const PcgScalars*)c->sc, init ? 1 : 0,
-           rhs0, init ? 0ull : c->loop_cond, (const int*)c->loop_cnt);
+           rhs0);
   MSF_LAUNCHED(c);
 }
 

@@ -295,14 +295,6 @@ struct msf_ctx {
   // one graph per contiguous active realisation range [rhs0, rhs0 + nr): converged
   // realisations drop out of the launch grids instead of exiting from every CTA
   cudaGraphExec_t range_graph[MSF_MAX_RHS][MSF_MAX_RHS + 1] = {};
-  // device-side iteration loop (opt-in, env MSF_GRAPH_LOOP=1): per range, a graph whose WHILE
-  // node repeats one iteration until the active set of the range changes; k_pcg_p sets the
-  // condition, so the host waits once per convergence event instead of every 8 iterations
-  bool graph_loop = false;          // measured no faster than host polling
-  unsigned long long loop_cond = 0;  // cudaGraphConditionalHandle while capturing a loop body
-  int* loop_cnt = nullptr;           // device: active realisations of the range at loop entry
-  int* loop_cnt_host = nullptr;      // pinned staging of *loop_cnt
-  cudaGraphExec_t loop_graph[MSF_MAX_RHS][MSF_MAX_RHS + 1] = {};
   // Gauss-Seidel sweep as one neighbour-synchronised launch (k_sgs_sweep_nb; opt-in, env
   // MSF_SGS_NB=1), used when its grid fits on the GPU at once (sgs_nb_max_ctas)
   bool sgs_nb = false;               // measured slower than the colour launches

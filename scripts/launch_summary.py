@@ -1,12 +1,16 @@
 """Per-PCG-iteration kernel breakdown from an ncu launch list
-(ncu --metrics gpu__time_duration.sum --csv --log-file X.csv ...): markdown table."""
+(ncu --metrics gpu__time_duration.sum --csv --log-file X.csv ...): markdown table.
+With --all: every launch of the list (e.g. one whole bench step), share of the total.
+Reads .csv or .csv.gz."""
 import collections
 import csv
+import gzip
 import sys
 
 
-def main(path):
-    rows = list(csv.reader(open(path)))
+def main(path, whole=False):
+    f = gzip.open(path, "rt") if path.endswith(".gz") else open(path)
+    rows = list(csv.reader(f))
     hdr = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hdr]
     ki, mi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
@@ -19,6 +23,18 @@ def main(path):
         u = r[ui]
         v = v * 1e3 if u in ("us", "usecond") else (v * 1e6 if u in ("ms", "msecond") else v)
         seq.append((r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", ""), v))
+    if whole:
+        agg, cnt = collections.defaultdict(float), collections.defaultdict(int)
+        for k, v in seq:
+            agg[k.split("<")[0]] += v
+            cnt[k.split("<")[0]] += 1
+        tot = sum(agg.values())
+        print(f"{len(seq)} launches; serialised kernel time {tot / 1e6:.2f} ms\n")
+        print("| kernel | ms | launches | share |")
+        print("|---|---|---|---|")
+        for k, v in sorted(agg.items(), key=lambda x: -x[1]):
+            print(f"| {k} | {v / 1e6:.3f} | {cnt[k]} | {v / tot * 100:.1f}% |")
+        return
     starts = [i for i, (k, _) in enumerate(seq)
               if k.startswith(("k_apply<0", "k_apply_direct<0", "k_apply_tma<0", "k_apply_sw<0"))]
     agg, cnt, tot = collections.defaultdict(float), collections.defaultdict(int), 0.0
@@ -37,4 +53,4 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], "--all" in sys.argv[2:])

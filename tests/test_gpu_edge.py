@@ -66,8 +66,7 @@ def test_edge_pcg_parity(name):
 
 @pytest.mark.parametrize("env", [{"MSF_PCG_MODE": "persistent"}, {"MSF_COARSE_COOP": "1"},
                                  {"MSF_PCG_MODE": "stream"}, {"MSF_APPLY_TMA": "0", "MSF_RESIDUAL_TMA": "0"},
-                                 {"MSF_CUBLAS": "0"}, {"MSF_GRAPH_LOOP": "1"},
-                                 {"MSF_SGS_NB": "1"}])
+                                 {"MSF_CUBLAS": "0"}, {"MSF_SGS_NB": "1"}])
 def test_opt_in_modes_match_default(env):
     """The opt-in execution modes (read at context setup) solve
     the same problem as the default graph path: iterations +-1, solutions to 1e-9."""
