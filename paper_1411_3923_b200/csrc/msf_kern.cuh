@@ -151,6 +151,18 @@ __device__ __forceinline__ double apply_tile(const Dims& d, const K0Mat& K, cons
 // `colour`.  FWD: x then y ; BWD: y then x ; both: the F3B3 phase.  ZERO: first forward
 // phase from z = 0 (writes zeros to the quad's other nodes).  Returns r.z over the whole
 // quad when RZ (after the final backward phase).  Per-thread.
+#ifndef MSF_GS_RCP
+#define MSF_GS_RCP 1
+#endif
+// 1/x for the Gauss-Seidel pivots: the hardware approximation refined by two Newton steps
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = fma(y, fma(-x, y, 1.0), y);
+  y = fma(y, fma(-x, y, 1.0), y);
+  return y;
+}
+
 template <bool FWD, bool BWD, bool ZERO, bool RZ>
 __device__ __forceinline__ double sgs_quad(const Dims& d, const K0Mat& K, const double* __restrict__ E,
                                            const double2* __restrict__ r, double2* z,
@@ -191,15 +203,24 @@ __device__ __forceinline__ double sgs_quad(const Dims& d, const K0Mat& K, const 
     const uint8_t fm = fixn[n];
     double2 zn = zloc[1][1];
     double rx = rv.x - ox, ry = rv.y - oy;
+#if MSF_GS_RCP
+    // reciprocals of the pivots: off the dependent chain, <= 2 ulp from the quotient
+    const double ixx = rcp_nr(dxx), iyy = rcp_nr(dyy);
+#define MSF_DIVX(a) ((a) * ixx)
+#define MSF_DIVY(a) ((a) * iyy)
+#else
+#define MSF_DIVX(a) ((a) / dxx)
+#define MSF_DIVY(a) ((a) / dyy)
+#endif
     if (FWD) {
       if (!(fm & 1)) {
-        const double dz = rx / dxx;
+        const double dz = MSF_DIVX(rx);
         zn.x += dz;
         ry -= dyx * dz;
         rx -= dxx * dz;
       }
       if (!(fm & 2)) {
-        const double dz = ry / dyy;
+        const double dz = MSF_DIVY(ry);
         zn.y += dz;
         rx -= dxy * dz;
         ry -= dyy * dz;
@@ -207,11 +228,13 @@ __device__ __forceinline__ double sgs_quad(const Dims& d, const K0Mat& K, const 
     }
     if (BWD) {
       if (!(fm & 2)) {
-        const double dz = ry / dyy;
+        const double dz = MSF_DIVY(ry);
         zn.y += dz;
         rx -= dxy * dz;
       }
-      if (!(fm & 1)) zn.x += rx / dxx;
+      if (!(fm & 1)) zn.x += MSF_DIVX(rx);
+#undef MSF_DIVX
+#undef MSF_DIVY
     }
     z[n] = zn;
     if (RZ) dot = rv.x * zn.x + rv.y * zn.y;
