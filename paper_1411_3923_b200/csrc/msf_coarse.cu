@@ -1018,7 +1018,8 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
   const int ntr = c->restrict_threads > 0 ? c->restrict_threads : 256;
   if (ntr >= 1024) MSF_RESTRICT_T(1024);
   else if (ntr >= 512) MSF_RESTRICT_T(512);
-  else MSF_RESTRICT_T(256);
+  else if (ntr >= 256) MSF_RESTRICT_T(256);
+  else MSF_RESTRICT_T(128);
 #undef MSF_RESTRICT_T
 #undef MSF_RESTRICT
   MSF_LAUNCHED(c);
