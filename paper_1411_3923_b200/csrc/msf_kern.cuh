@@ -19,6 +19,15 @@ namespace msfk {
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Build switches of the Gauss-Seidel arithmetic (R7a): MSF_GS_RCP pivots by refined
+// reciprocal; MSF_F0_DIAG zero-start phase without the (vanishing) stencil.
+#ifndef MSF_GS_RCP
+#define MSF_GS_RCP 1
+#endif
+#ifndef MSF_F0_DIAG
+#define MSF_F0_DIAG 1
+#endif
+
 // ------------------------------------------------------------------ Q4 node stencil
 // local index a of the centre node inside element (sx,sy) = (ix-1+sx, iy-1+sy)
 __device__ __forceinline__ constexpr int a_of(int sx, int sy) {
@@ -29,6 +38,10 @@ __device__ __forceinline__ constexpr int DYB(int b) { return (b >= 2) ? 1 : 0; }
 
 // (K z)_node and the node's own 2x2 diagonal block from the 4 element moduli E[sx][sy]
 // and the 3x3 neighbourhood z[i][j] = node (ix-1+i, iy-1+j)  (Eq. 4-5).
+// SYM: the pivot block's lower row is taken from its upper one (make_K0: K0 is bitwise
+// symmetric with equal diagonal entries, so this is bitwise the same result with 8 fewer
+// FMAs; the choice only moves register allocation, see launch_sgs_phase).
+template <bool SYM = true>
 __device__ __forceinline__ void apply_node(const K0Mat& K, const double (&E)[2][2],
                                            const double2 (&z)[3][3], double& ox, double& oy,
                                            double& dxx, double& dxy, double& dyx, double& dyy) {
@@ -52,8 +65,31 @@ __device__ __forceinline__ void apply_node(const K0Mat& K, const double (&E)[2][
       oy = fma(e, ay, oy);
       dxx = fma(e, K.v[(2 * a) * 8 + 2 * a], dxx);
       dxy = fma(e, K.v[(2 * a) * 8 + 2 * a + 1], dxy);
-      dyx = fma(e, K.v[(2 * a + 1) * 8 + 2 * a], dyx);
-      dyy = fma(e, K.v[(2 * a + 1) * 8 + 2 * a + 1], dyy);
+      if (!SYM) {
+        dyx = fma(e, K.v[(2 * a + 1) * 8 + 2 * a], dyx);
+        dyy = fma(e, K.v[(2 * a + 1) * 8 + 2 * a + 1], dyy);
+      }
+    }
+  if (SYM) {
+    dyx = dxy;
+    dyy = dxx;
+  }
+}
+
+// The node's own 2x2 block of K from the 4 element moduli.  make_K0's element matrix is
+// bitwise symmetric with one diagonal value, so the block is [dxx dxy; dxy dxx] and these
+// are bitwise the dxx, dxy (= dyx), dyy of apply_node.
+__device__ __forceinline__ void diag_node(const K0Mat& K, const double (&E)[2][2], double& dxx,
+                                          double& dxy) {
+  dxx = dxy = 0.0;
+#pragma unroll
+  for (int sx = 0; sx < 2; ++sx)
+#pragma unroll
+    for (int sy = 0; sy < 2; ++sy) {
+      const int a = a_of(sx, sy);
+      const double e = E[sx][sy];
+      dxx = fma(e, K.v[(2 * a) * 8 + 2 * a], dxx);
+      dxy = fma(e, K.v[(2 * a) * 8 + 2 * a + 1], dxy);
     }
 }
 
@@ -151,9 +187,6 @@ __device__ __forceinline__ double apply_tile(const Dims& d, const K0Mat& K, cons
 // `colour`.  FWD: x then y ; BWD: y then x ; both: the F3B3 phase.  ZERO: first forward
 // phase from z = 0 (writes zeros to the quad's other nodes).  Returns r.z over the whole
 // quad when RZ (after the final backward phase).  Per-thread.
-#ifndef MSF_GS_RCP
-#define MSF_GS_RCP 1
-#endif
 // 1/x for the Gauss-Seidel pivots: the hardware approximation refined by two Newton steps
 __device__ __forceinline__ double rcp_nr(double x) {
   double y;
@@ -163,7 +196,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return y;
 }
 
-template <bool FWD, bool BWD, bool ZERO, bool RZ>
+template <bool FWD, bool BWD, bool ZERO, bool RZ, bool SYM = true>
 __device__ __forceinline__ double sgs_quad(const Dims& d, const K0Mat& K, const double* __restrict__ E,
                                            const double2* __restrict__ r, double2* z,
                                            const uint8_t* __restrict__ fixn, int qx, int qy,
@@ -197,7 +230,15 @@ __device__ __forceinline__ double sgs_quad(const Dims& d, const K0Mat& K, const 
                          : make_double2(0.0, 0.0);
       }
     double ox, oy, dxx, dxy, dyx, dyy;
-    apply_node(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
+    if (ZERO && MSF_F0_DIAG) {
+      // z = 0 around the node: (K z) vanishes, only the pivot block is needed
+      ox = oy = 0.0;
+      diag_node(K, Eloc, dxx, dxy);
+      dyx = dxy;
+      dyy = dxx;
+    } else {
+      apply_node<SYM>(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
+    }
     const size_t n = (size_t)ix * d.nny + iy;
     const double2 rv = r[n];
     const uint8_t fm = fixn[n];
