@@ -806,6 +806,7 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->sc_host, MSF_MAX_RHS * sizeof(PcgScalars));
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->scal_host, 80 * 8);
   if (const char* e = std::getenv("MSF_SGS_NB")) c->sgs_nb = std::string(e) == "1";
+  if (const char* e = std::getenv("MSF_PROLONG_NR")) c->prolong_nr = std::string(e) != "0";
   if (transport != 0) c->sgs_nb = false;
   if (ce == cudaSuccess && c->sgs_nb) {
     const size_t tiles = (size_t)((c->dl.nny + 1) / 2 + 31) / 32 * (((c->dl.nnx + 1) / 2 + 7) / 8);

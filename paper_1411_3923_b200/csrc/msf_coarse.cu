@@ -281,6 +281,73 @@ __global__ void __launch_bounds__(NT) k_prolong1(Dims d, const double* __restric
   *z = zv;
 }
 
+// Prolongation for NR > 1 active realisations, one node per thread for all of them: the
+// realisations share the coarse basis, so phi is loaded once per (covering
+// agglomerate, mode) and applied to each realisation's coefficients (k_prolong1 loads it
+// once per realisation).  Per realisation the sum runs in k_prolong1's order: z is bitwise
+// the same.
+template <int KM, int NR>
+__global__ void __launch_bounds__(NT) k_prolong_nr(Dims d, const double* __restrict__ phi,
+                                                   const int* __restrict__ cls_of_agg,
+                                                   const double* __restrict__ cxall, double2* zall,
+                                                   const PcgScalars* sc, int rhs0, int gated) {
+  pdl_launch();
+  pdl_wait();
+  bool act[NR];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    act[k] = !gated || sc[rhs0 + k].active;
+    any |= act[k];
+  }
+  if (!any) return;
+  const int iy = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int ix = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (ix >= d.nnx || iy >= d.nny) return;
+  const size_t cstride = (size_t)d.nbc * d.mc;
+  const double* xc = cxall + (size_t)rhs0 * cstride;
+  const int gix = ix + d.gox;
+  const int I0 = gix / d.cx, J0 = iy / d.cy;
+  double sx[NR], sy[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) sx[k] = sy[k] = 0.0;
+#pragma unroll
+  for (int di = 0; di < 2; ++di) {
+    const int I = I0 + di;
+    const int px = gix - (I * d.cx - d.cx);
+    if (I > d.ncx || px >= d.bx) continue;
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj) {
+      const int J = J0 + dj;
+      const int py = iy - (J * d.cy - d.cy);
+      if (J > d.ncy || py >= d.by) continue;
+      const int agg = I * (d.ncy + 1) + J;
+      const double* ph = phi + (size_t)cls_of_agg[agg] * d.kmax * d.box_nodes * 2 + (size_t)(px * d.by + py) * 2;
+#pragma unroll
+      for (int a = 0; a < KM; ++a) {
+        if (a < d.kmax) {
+          const double2 pv = __ldg(reinterpret_cast<const double2*>(ph + (size_t)a * d.box_nodes * 2));
+#pragma unroll
+          for (int k = 0; k < NR; ++k) {
+            const double cv = __ldg(xc + k * cstride + (size_t)agg * d.kmax + a);
+            sx[k] = fma(pv.x, cv, sx[k]);
+            sy[k] = fma(pv.y, cv, sy[k]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    if (!act[k]) continue;
+    double2* z = zall + (size_t)(rhs0 + k) * d.nn + (size_t)ix * d.nny + iy;
+    double2 zv = *z;
+    zv.x += sx[k];
+    zv.y += sy[k];
+    *z = zv;
+  }
+}
+
 // ------------------------------------------------------------------ Galerkin cell products
 // Kcell[rhs][cell][p][q] = sum_{e in cell} E_e Phi_e[:,p]^T K0 Phi_e[:,q],  p,q in 0..4k-1,
 // p = corner*k + a, corner = ci*2 + cj for coarse node (CI+ci, CJ+cj).  The (4k)x(4k) output
@@ -1028,6 +1095,22 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
   const Dims& d = c->dl;   // every local node, halo included (identical increments on both ranks)
   dim3 g((d.nny + 31) / 32, (d.nnx + 7) / 8, 1);
+  if (nr > 1 && nr <= 3 && d.kmax <= 8 && c->prolong_nr) {
+#define MSF_PROLONG_NR(KM, NR)                                                                    \
+  launch_k(k_prolong_nr<KM, NR>, g, dim3(NT), 0, c->stream, d, (const double*)c->phi,              \
+           (const int*)c->cls_of_agg_d, (const double*)c->cx, (double2*)z, (const PcgScalars*)c->sc, \
+           rhs0, gated ? 1 : 0)
+    if (d.kmax <= 4) {
+      if (nr == 2) MSF_PROLONG_NR(4, 2);
+      else MSF_PROLONG_NR(4, 3);
+    } else {
+      if (nr == 2) MSF_PROLONG_NR(8, 2);
+      else MSF_PROLONG_NR(8, 3);
+    }
+#undef MSF_PROLONG_NR
+    MSF_LAUNCHED(c);
+    return;
+  }
 #define MSF_PROLONG(KM)                                                                           \
   launch_k(k_prolong1<KM>, dim3(g.x, g.y, nr), dim3(NT), 0, c->stream, d, (const double*)c->phi,    \
            (const int*)c->cls_of_agg_d, (const double*)c->cx, (double2*)z, (const PcgScalars*)c->sc, \

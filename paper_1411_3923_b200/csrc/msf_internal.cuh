@@ -224,7 +224,9 @@ struct msf_ctx {
   // restriction one warp per group of same-class agglomerates (k_restrict_batch; env
   // MSF_RESTRICT_BATCH=0: off); n_rgroups = 0 when not used
   int n_rgroups = 0, rgroup_B = 0;
-  bool rgroup_force = false;        // env MSF_RESTRICT_BATCH=force: grouped kernel on every launch
+  bool rgroup_force = false;
+  bool prolong_nr = true;            // several realisations per prolongation thread (k_prolong_nr;
+                                     // env MSF_PROLONG_NR=0: one launch-z per realisation)        // env MSF_RESTRICT_BATCH=force: grouped kernel on every launch
   int* rgroups_d = nullptr;
   std::vector<int> agg_by_cls_h;
   // top system after the truncated cyclic reduction: T active blocks (stride top_stride),
