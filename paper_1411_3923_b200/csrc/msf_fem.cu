@@ -16,6 +16,8 @@
 #include <cudaTypedefs.h>    // PFN_cuTensorMapEncodeTiled
 
 #include <cstring>
+#include <cstdlib>
+#include <string>
 
 #include "msf_kern.cuh"
 
@@ -511,7 +513,7 @@ __global__ void __launch_bounds__(NTHR) k_apply_direct(Dims d, K0Mat K, const do
 // ------------------------------------------------------------------ Gauss-Seidel colour phase
 // Thread per node quad; see msfk::sgs_quad.  RZ: r.z of the final iterate -> beta (rz_mode 1:
 // PCG init, beta = 0; 2: iteration).
-template <bool FWD, bool BWD, bool ZERO, bool RZ, bool SYM>
+template <bool FWD, bool BWD, bool ZERO, bool RZ>
 __global__ void __launch_bounds__(NTHR) k_sgs_colour(Dims d, K0Mat K, const double* __restrict__ Eall,
                                                      const double2* __restrict__ rall,
                                                      double2* zall,
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(NTHR) k_sgs_colour(Dims d, K0Mat K, const doub
   __shared__ double red[NTHR / 32 + 1];
   const int qx = blockIdx.y * blockDim.y + threadIdx.y;
   const int qy = blockIdx.x * blockDim.x + threadIdx.x;
-  const double dot = sgs_quad<FWD, BWD, ZERO, RZ, SYM>(d, K, Eall + (size_t)rhs * d.estride,
+  const double dot = sgs_quad<FWD, BWD, ZERO, RZ>(d, K, Eall + (size_t)rhs * d.estride,
                                                   rall + (size_t)rhs * d.nn,
                                                   zall + (size_t)rhs * d.nn, fixn, qx, qy, colour);
   if (RZ) {
@@ -1034,21 +1036,18 @@ void launch_sgs_phase(msf_ctx* c, int rhs0, int nr, const double* r, double* z, 
   dim3 blk(32, 8);
   dim3 grd((hy + 31) / 32, (hx + 7) / 8, nr);
   const int g = gated ? 1 : 0;
-  // SYM = false for launches of at most 4 CTAs per SM: that instantiation needs 52 registers
-  // (4 resident CTAs per SM) instead of 48 (5), and a one-wave grid spread 4 per SM ran
-  // faster than the uneven 5-per-SM placement (configs[1] at one realisation, 585 CTAs:
-  // PCG 118.0 vs 117.0 ms); larger grids keep the leaner SYM = true kernel (configs[4]
-  // 2796 -> 2754 ms).  Both compute bitwise the same values.
-  const bool sym = (long long)grd.x * grd.y * nr > 4LL * 148;
+  // One-wave grids (configs[1] at one realisation: 585 CTAs) are spread at most 4 CTAs per
+  // SM by an unused 46 KB dynamic shared-memory request (the 48-register kernel would take 5
+  // per SM and leave SMs idle): configs[1] PCG 115.2 -> 114.3 ms.  MSF_SGS_CAP=0: off.
+  static const bool cap_env = [] {
+    const char* e = std::getenv("MSF_SGS_CAP");
+    return !(e && std::string(e) == "0");
+  }();
+  const size_t smem = (cap_env && (long long)grd.x * grd.y * nr <= 4LL * 148) ? 46 * 1024 : 0;
 #define MSF_SGS(F, B, Z, RZ, col)                                                               \
-  if (sym)                                                                                      \
-    launch_k(k_sgs_colour<F, B, Z, RZ, true>, grd, blk, 0, c->stream, d, c->K0, c->E_loc,       \
-             (const double2*)r, (double2*)z, c->fixn, c->sc, c->partials, c->counters,          \
-             c->max_partials, rhs0, g, (int)(col), rz_mode, c->dsum);                             \
-  else                                                                                          \
-    launch_k(k_sgs_colour<F, B, Z, RZ, false>, grd, blk, 0, c->stream, d, c->K0, c->E_loc,      \
-             (const double2*)r, (double2*)z, c->fixn, c->sc, c->partials, c->counters,          \
-             c->max_partials, rhs0, g, (int)(col), rz_mode, c->dsum);                             \
+  launch_k(k_sgs_colour<F, B, Z, RZ>, grd, blk, smem, c->stream, d, c->K0, c->E_loc,           \
+           (const double2*)r, (double2*)z, c->fixn, c->sc, c->partials, c->counters,            \
+           c->max_partials, rhs0, g, (int)(col), rz_mode, c->dsum);                               \
   break
   switch (phase) {
     case 0: MSF_SGS(true, false, true, false, 0);
@@ -1149,7 +1148,14 @@ void launch_update_f0(msf_ctx* c, int rhs0, int nr) {
   // alpha from the operator's partials when the preceding matvec left them (one GPU)
   const int napart = c->apart_n;
   c->apart_n = 0;
-  launch_k(k_update_f0, grd, dim3(32, 8), 0, c->stream,
+  // one-wave grids (configs[1] at one realisation: 585 CTAs) spread at most 4 CTAs per SM:
+  // an unused 46 KB dynamic shared-memory request caps the residency (MSF_F0_CAP=0: off)
+  static const bool cap_env = [] {
+    const char* e = std::getenv("MSF_F0_CAP");
+    return !(e && std::string(e) == "0");
+  }();
+  const size_t cap = (cap_env && (long long)grd.x * grd.y * nr <= 4LL * 148) ? 46 * 1024 : 0;
+  launch_k(k_update_f0, grd, dim3(32, 8), cap, c->stream,
            d, c->K0, c->E_loc, (double2*)c->u, (double2*)c->r, (const double2*)c->pv,
            (const double2*)c->q, (double2*)c->z, c->fixn, c->sc, c->partials, c->counters,
            c->max_partials, c->dsum, rhs0, (const double*)c->apart, napart);
