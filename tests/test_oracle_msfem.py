@@ -208,3 +208,107 @@ def test_contrast_flat_iterations():
     hi = [its[e] for e in (1e-3, 1e-6, 1e-9)]
     assert max(hi) - min(hi) <= 0.1 * max(hi) + 1
     assert its[1e0] <= min(hi)
+
+
+# ---------------------------------------------------------------- round-2 pins
+def test_local_problem_moduli_mapping_brute_force():
+    """Pin of local_problem's element-moduli mapping (Eq. 9, l.128-130: K_omega is
+    the stiffness of the elements of omega_i).  Brute force: assemble the WHOLE grid with
+    the moduli zeroed outside the agglomerate box; its rows/columns of the box DOFs must be
+    K_omega.  The grid is non-square and E heterogeneous, so a transposed E index, a
+    shifted box or a wrong local node order all fail."""
+    nelx, nely, cx, cy = 12, 6, 4, 3
+    K0 = fem.element_stiffness(0.3)
+    rng = np.random.default_rng(21)
+    E = rng.uniform(0.1, 2.0, nelx * nely)
+    fixed = np.zeros(2 * (nelx + 1) * (nely + 1), dtype=np.int8)
+    ex, ey = np.meshgrid(np.arange(nelx), np.arange(nely), indexing="ij")
+    ex, ey = ex.ravel(), ey.ravel()                     # element id = ex*nely + ey
+    for (I, J) in [(0, 0), (1, 1), (3, 2), (2, 0)]:
+        ex0, ex1, ey0, ey1 = msfem.agglomerate_box(I, J, nelx, nely, cx, cy)
+        inside = (ex >= ex0) & (ex < ex1) & (ey >= ey0) & (ey < ey1)
+        Kg = fem.assemble(nelx, nely, np.where(inside, E, 0.0), K0).toarray()
+        Kl, D, gdof, dix, diy = msfem.local_problem(I, J, nelx, nely, cx, cy, E, K0, fixed)
+        assert np.abs(Kl - Kg[np.ix_(gdof, gdof)]).max() < 1e-14 * np.abs(Kg).max()
+        # every DOF the box's elements touch is a local DOF
+        touched = np.flatnonzero(np.abs(Kg).sum(axis=1) > 0)
+        assert set(touched) <= set(gdof)
+    # one coarse cell covering the grid: K_omega is the global free-DOF stiffness
+    fx = np.zeros(2 * (nelx + 1) * (nely + 1), dtype=np.int8)
+    fx[:2 * (nely + 1)] = 1                                # left edge clamped
+    Kl, D, gdof, *_ = msfem.local_problem(0, 0, nelx, nely, nelx, nely, E, K0, fx)
+    Kg = fem.assemble(nelx, nely, E, K0).toarray()
+    free = np.flatnonzero(fx == 0)
+    assert np.array_equal(gdof, free)
+    assert np.abs(Kl - Kg[np.ix_(free, free)]).max() < 1e-14 * np.abs(Kg).max()
+
+
+def test_local_eigenpairs_diagonal_weighting():
+    """Pin of the §3.2 weighting M_omega = diag(K_omega).
+    (a) A one-element agglomerate with nothing fixed: diag(E K0) = E k11 I (the Q4 element
+        matrix has one diagonal value), so lambda = eig(K0) / K0[0,0] for every E.
+    (b) The pencil (K_omega, diag K_omega) is invariant under E -> alpha E on a
+        heterogeneous agglomerate (D = I or D = mass would scale lambda by alpha)."""
+    K0 = fem.element_stiffness(0.3)
+    assert np.ptp(np.diag(K0)) < 1e-15          # one diagonal value (to rounding)
+    ref = np.linalg.eigvalsh(K0) / K0[0, 0]
+    nelx, nely = 4, 3
+    fixed = np.zeros(2 * (nelx + 1) * (nely + 1), dtype=np.int8)
+    for Ev in (1.0, 7.5, 1e-6):
+        E = np.full(nelx * nely, Ev)
+        Kl, D, *_ = msfem.local_problem(0, 0, nelx, nely, 1, 1, E, K0, fixed)
+        assert Kl.shape == (8, 8)
+        lam, _ = msfem.local_eigenpairs(Kl, D, 8)
+        assert np.abs(lam - ref).max() < 1e-12
+    spec = W.small_spec(nelx=16, nely=8, cx=4, cy=4)
+    fx = W.fixed_mask(spec)
+    E = np.random.default_rng(22).uniform(1e-3, 1.0, spec.n_el)
+    lam1 = msfem.local_eigenpairs(*msfem.local_problem(2, 1, 16, 8, 4, 4, E, K0, fx)[:2], 6)[0]
+    lam2 = msfem.local_eigenpairs(*msfem.local_problem(2, 1, 16, 8, 4, 4, 300.0 * E, K0, fx)[:2], 6)[0]
+    assert np.abs(lam1 - lam2).max() < 1e-10 * max(1.0, np.abs(lam1).max())
+    # the weighting is the diagonal itself: Rayleigh quotient of the unit vector e_i is 1
+    Kl, D, *_ = msfem.local_problem(2, 1, 16, 8, 4, 4, E, K0, fx)
+    assert np.array_equal(D, np.diag(Kl))
+
+
+def test_coarse_basis_partition_of_unity_weighting():
+    """Pin of phi_{i,j} = chi_i psi_j inside build_coarse_basis.
+    (a) Rows of R vanish on the nodes of the agglomerate boundary that lie inside the
+        domain (chi_i = 0 there; a bare psi does not vanish on a Neumann boundary).
+    (b) With no Dirichlet DOFs and uniform E every agglomerate's first 3 modes span the
+        rigid-body modes, and sum_i chi_i = 1 makes the three GLOBAL rigid-body modes lie in
+        span(R^T) exactly; the unweighted box-restricted modes do not span them.
+    (c) On the agglomerate's own coarse node chi = 1 (row = psi there)."""
+    nelx, nely, cx, cy = 12, 8, 4, 4
+    ncx, ncy = msfem.coarse_grid(nelx, nely, cx, cy)
+    K0 = fem.element_stiffness(0.3)
+    n_dof = 2 * (nelx + 1) * (nely + 1)
+    fixed = np.zeros(n_dof, dtype=np.int8)
+    E = np.ones(nelx * nely)
+    R, _ = msfem.build_coarse_basis(nelx, nely, cx, cy, 3, E, K0, fixed)
+    Rd = R.toarray()
+    node_ix = np.repeat(np.arange(nelx + 1), nely + 1)
+    node_iy = np.tile(np.arange(nely + 1), nelx + 1)
+    dix, diy = np.repeat(node_ix, 2), np.repeat(node_iy, 2)
+    row = 0
+    for I in range(ncx + 1):
+        for J in range(ncy + 1):
+            ex0, ex1, ey0, ey1 = msfem.agglomerate_box(I, J, nelx, nely, cx, cy)
+            on_bdry = (((dix == ex0) & (ex0 > 0)) | ((dix == ex1) & (ex1 < nelx))
+                       | ((diy == ey0) & (ey0 > 0)) | ((diy == ey1) & (ey1 < nely)))
+            on_bdry &= (dix >= ex0) & (dix <= ex1) & (diy >= ey0) & (diy <= ey1)
+            for _ in range(3):
+                assert np.abs(Rd[row, on_bdry]).max() == 0.0
+                outside = (dix < ex0) | (dix > ex1) | (diy < ey0) | (diy > ey1)
+                assert np.abs(Rd[row, outside]).max() == 0.0
+                row += 1
+            # (c): at the coarse node, chi = 1 so the row carries psi, which (for the
+            # rigid modes of a unit-E agglomerate) does not vanish identically there
+            at = (dix == I * cx) & (diy == J * cy)
+            assert np.abs(Rd[row - 3:row][:, at]).max() > 0.0
+    assert row == Rd.shape[0]
+    x, y = node_ix.astype(float), node_iy.astype(float)
+    for v in (np.tile([1.0, 0.0], x.size), np.tile([0.0, 1.0], x.size),
+              np.ravel(np.stack([-y, x], axis=1))):
+        c = np.linalg.lstsq(Rd.T, v, rcond=None)[0]
+        assert np.linalg.norm(Rd.T @ c - v) < 1e-10 * np.linalg.norm(v)
