@@ -1,6 +1,8 @@
 """Benchmark of the B200 MsFEM-PCG hot path (BASELINE.json metric).
 
-A *step* is one pass of the whole hot path over the configs[1] workload:
+A *step* is one pass of the whole hot path over the configs[4] workload
+(MBB 5120x2560, 26,229,762 DOF, the paper's largest size, PAPER.md l.439 -- the config the
+BASELINE metric is quoted on, and it fits one B200):
 filter_project (3 Heaviside realisations) -> build_coarse_basis (dilated realisation) ->
 assemble_coarse (3 Galerkin K_c + factorisations) -> pcg_solve (3 realisations, tol 1e-8,
 x0 = 0) -> sensitivities -> oc_update, always from the same seeded design tile, so every
@@ -14,8 +16,9 @@ N > 1 (torchrun): the grid of the SAME workload is strip-partitioned over the ra
 inside the library, K_c distributed by block chains with a replicated interface system), so
 the total work is fixed (strong scaling);
 value = n_dof x PCG iterations / max-over-ranks time.  --mode replicas instead runs an
-independent copy per rank (weak scaling).  BASELINE configs[4] (--config c4_mbb_5120x2560)
-is the paper-sized strip-scaling study.
+independent copy per rank (weak scaling).  After the timed region a one-GPU run also
+records the configs[3] contrast sweep (E_min 1e-3 / 1e-6 / 1e-9: PCG iterations and
+DOF*iter/s per contrast).
 """
 from __future__ import annotations
 
@@ -36,7 +39,7 @@ import workloads as W  # noqa: E402
 
 METRIC = "PCG DOF*iterations/s (matvec+2-level precond), 3 robust realisations"
 UNIT = "DOF*iter/s"
-DEFAULT_CONFIG = "c1_mbb_1024x512"
+DEFAULT_CONFIG = "c4_mbb_5120x2560"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -103,9 +106,13 @@ class ClockSampler:
 
 
 def cpu_sample_spec(spec):
-    """Bounded sample of the same workload for the oracle: the configs[1] recipe (tile,
-    filter, projection, 3 realisations, coarse cells, modes, tolerance) on a 128x64 grid."""
-    return spec.replace(name=spec.name + "_cpu_sample_128x64", nelx=128, nely=64)
+    """Bounded sample of the same workload for the oracle: the recipe (tile, filter,
+    projection, 3 realisations, coarse cells, modes, tolerance) on a sub-grid of 8 x 4 coarse
+    cells (configs[4]: 160x80 elements; about 10-30 s of oracle work)."""
+    nx, ny = 8 * spec.cx, 4 * spec.cy
+    nx += (-nx) % spec.tile_x
+    ny += (-ny) % spec.tile_y
+    return spec.replace(name=f"{spec.name}_cpu_sample_{nx}x{ny}", nelx=nx, nely=ny)
 
 
 def oracle_sample(spec):
@@ -128,40 +135,42 @@ def host_threads():
         return os.cpu_count() or 1
 
 
-SCALEUP_CONFIG = "c4_mbb_5120x2560"
+SWEEP_CONFIG = "c3_square_2048"
 
 
-def scaleup_kernels(dev, peak):
-    """Per-kernel times and HBM fractions (msf_bench_kernels, PCG launch configuration) on the
-    north star's ~26M-DOF robust problem (BASELINE configs[4]), at one and three active
-    realisations: evidence for the matvec / preconditioner roofline at that size.  Runs after
-    the timed region on rank 0 of a one-GPU run."""
+def contrast_sweep(dev):
+    """BASELINE configs[3]: the contrast-independence sweep.  For each
+    E_min, one warm-up and one timed design pass (filter/project, basis, K_c assembly, PCG)
+    on a fresh context; reports PCG iterations, PCG-only and whole-pass DOF*iter/s.  Runs
+    after the timed region on rank 0 of a one-GPU run."""
     import torch
     from paper_1411_3923_b200 import Msfem
-    spec = W.CONFIGS[SCALEUP_CONFIG]
-    m = Msfem.from_spec(spec, device=dev)
-    m.filter_project(torch.as_tensor(W.design_tile(spec), device=dev))
-    m.build_coarse_basis()
-    m.assemble_coarse()
-    out = {"workload": SCALEUP_CONFIG, "n_dof": spec.n_dof, "peak_GBps": peak}
-    names = ["apply", "residual", "sgs_colour", "update_f0", "p_update", "restrict", "prolong",
-             "coarse_solve", "vcycle", "pcg_iteration"]
-    for nr in (1, spec.n_rhs):
-        os.environ["MSF_BENCH_NR"] = str(nr)
-        kb = m.bench_kernels(reps=10)
-        tab = {}
-        for k in names:
-            ms, by = kb[k]
-            if ms <= 0:
-                continue
-            per = 7 if k == "sgs_colour" else 1   # one colour launch of the 7-launch sweep
-            gbps = by / per / (ms / per / 1e3) / 1e9
-            tab[k] = {"ms": ms / per, "alg_GBps": gbps, "hbm_frac": gbps / peak}
-        out[f"realisations_{nr}"] = tab
-    os.environ.pop("MSF_BENCH_NR", None)
-    m.close()
-    del m
-    torch.cuda.empty_cache()
+    base = W.CONFIGS[SWEEP_CONFIG]
+    out = {"workload": SWEEP_CONFIG, "n_dof": base.n_dof, "rows": []}
+    for emin in (1e-3, 1e-6, 1e-9):
+        spec = base.replace(Emin=emin)
+        m = Msfem.from_spec(spec, device=dev)
+        x = torch.as_tensor(W.design_tile(spec), device=dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        for rep in range(2):
+            ev[0].record(m.stream)
+            m.filter_project(x)
+            m.build_coarse_basis()
+            m.assemble_coarse()
+            ev[1].record(m.stream)
+            its, comps, nc = m.pcg_solve(tol=spec.tol, max_it=20000)
+            ev[2].record(m.stream)
+            torch.cuda.synchronize(dev)
+        setup_ms, pcg_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+        out["rows"].append({"Emin": emin, "pcg_iters": its, "converged": not nc,
+                            "pcg_ms": pcg_ms, "basis_assembly_ms": setup_ms,
+                            "dof_iter_per_s_pcg": spec.n_dof * sum(its) / (pcg_ms / 1e3),
+                            "dof_iter_per_s_pass": spec.n_dof * sum(its) / ((pcg_ms + setup_ms) / 1e3)})
+        m.close()
+        del m
+        torch.cuda.empty_cache()
+    its = [sum(r["pcg_iters"]) for r in out["rows"]]
+    out["iters_spread_1e-6_to_1e-9"] = abs(its[2] - its[1]) / max(its[1:])
     return out
 
 
@@ -290,8 +299,12 @@ def run_ours(args, spec):
     d2h = nt * 8 + spec.n_rhs * (4 + 8) + 16
 
     # ---- roofline of the dominant kernel (live CUDA-event timing, PCG launch config;
-    # on a strip the kernels run on that rank's strip)
+    # on a strip the kernels run on that rank's strip): all realisations active, and the
+    # one-realisation configuration most PCG iterations of a step run in
     kb = m.bench_kernels(reps=20)
+    os.environ["MSF_BENCH_NR"] = "1"
+    kb1 = m.bench_kernels(reps=20)
+    os.environ.pop("MSF_BENCH_NR", None)
     per_iter_count = {"apply": 1, "sgs_colour": 2, "restrict": 1, "coarse_solve": 1,
                       "prolong": 1, "residual": 1}
     share = {k: kb[k][0] * n for k, n in per_iter_count.items()}
@@ -345,14 +358,20 @@ def run_ours(args, spec):
                         "alg_GBps": v[1] / (v[0] / 1e3) / 1e9 if v[0] > 0 and v[1] > 0 else None,
                         "hbm_frac": v[1] / (v[0] / 1e3) / 1e9 / peak if v[0] > 0 and v[1] > 0 else None}
                     for k, v in kb.items()},
+        "kernels_1rhs": {k: {"ms": v[0],
+                             "hbm_frac": v[1] / (v[0] / 1e3) / 1e9 / peak if v[0] > 0 and v[1] > 0 else None}
+                         for k, v in kb1.items()},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
-        # north star: matvec / preconditioner >= 60% of HBM on 1 B200 for the ~26M-DOF problem
-        "kernels_26M": (scaleup_kernels(dev, peak) if ws == 1 and not args.no_scaleup else None),
         "clocks": clocks,
     }
+    if ws == 1 and not args.no_sweep:
+        m.close()
+        del m
+        torch.cuda.empty_cache()
+        line["contrast_sweep"] = contrast_sweep(dev)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -366,8 +385,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-scaleup", action="store_true",
-                    help="skip the per-kernel table of configs[4] (kernels_26M) after the timed region")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the configs[3] contrast sweep after the timed region")
     ap.add_argument("--mode", default="auto", choices=["auto", "strips", "replicas"],
                     help="auto: strip partition when N > 1; strips: NCCL strip path even at N = 1; "
                          "replicas: independent copies per rank")

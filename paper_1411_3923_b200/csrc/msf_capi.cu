@@ -463,6 +463,7 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   c->sb = P.sb;
   c->rank = rank;
   c->nranks = nranks;
+  c->n_sm = prop.multiProcessorCount;
   c->K0 = make_K0(p->nu);
   c->stream = (cudaStream_t)stream;
   c->ws = (char*)workspace;

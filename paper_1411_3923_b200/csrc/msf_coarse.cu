@@ -1067,7 +1067,7 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
     MSF_LAUNCHED(c);
     return;
   }
-  if (c->restrict_warp && (long long)c->n_restrict * nr >= 32LL * 148) {
+  if (c->restrict_warp && (long long)c->n_restrict * nr >= 32LL * c->n_sm) {
 #define MSF_RESTRICT_W(KM)                                                                         \
   launch_k(k_restrict_warp<KM>, dim3((c->n_restrict + 7) / 8, nr), dim3(256), 0, c->stream, d,        \
            (const double2*)t, (const double*)c->phi, (const int*)c->cls_of_agg_d,                     \
@@ -1461,7 +1461,7 @@ void launch_coarse_back_local(msf_ctx* c, int rhs0, int nr, bool gated) {
 
 void launch_iface_vec_pack(msf_ctx* c, int rhs0, int nr) {
   const int nI = (int)c->iface.size();
-  const int blocks = std::max(1, std::min(148, (nI * c->d.mc + 255) / 256));
+  const int blocks = std::max(1, std::min(c->n_sm, (nI * c->d.mc + 255) / 256));
   k_iface_vec<<<dim3(blocks, nr), 256, 0, c->stream>>>(c->d, c->iface_d, nI, c->rank, c->rank + 1, c->cb,
                                                        c->iface_vec, rhs0, 0);
   MSF_LAUNCHED(c);
@@ -1469,7 +1469,7 @@ void launch_iface_vec_pack(msf_ctx* c, int rhs0, int nr) {
 
 void launch_iface_vec_unpack(msf_ctx* c, int rhs0, int nr) {
   const int nI = (int)c->iface.size();
-  const int blocks = std::max(1, std::min(148, (nI * c->d.mc + 255) / 256));
+  const int blocks = std::max(1, std::min(c->n_sm, (nI * c->d.mc + 255) / 256));
   k_iface_vec<<<dim3(blocks, nr), 256, 0, c->stream>>>(c->d, c->iface_d, nI, -1, -1, c->cb,
                                                        c->iface_vec, rhs0, 1);
   MSF_LAUNCHED(c);

@@ -204,16 +204,19 @@ int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int rhs0, 
     if (rc) return rc;
     for (int k = rhs0; k < rhs0 + nr; ++k) {
       double* v = c->*vec + (size_t)k * 2 * d.nn;
+      // every call is checked; on a failure the group is still closed before returning, so
+      // the communicator is never left inside an open group
       if (c->rank > 0) {
-        A.Send(v + (size_t)d.own_lo * col, col, ncclDouble, c->rank - 1, comm, c->stream);
-        A.Recv(v + (size_t)(d.own_lo - 1) * col, col, ncclDouble, c->rank - 1, comm, c->stream);
+        if (!rc) rc = nccl_check(c, A.Send(v + (size_t)d.own_lo * col, col, ncclDouble, c->rank - 1, comm, c->stream), "ncclSend (halo, left)");
+        if (!rc) rc = nccl_check(c, A.Recv(v + (size_t)(d.own_lo - 1) * col, col, ncclDouble, c->rank - 1, comm, c->stream), "ncclRecv (halo, left)");
       }
       if (c->rank < c->nranks - 1) {
-        A.Send(v + (size_t)(d.own_hi - 1) * col, col, ncclDouble, c->rank + 1, comm, c->stream);
-        A.Recv(v + (size_t)d.own_hi * col, col, ncclDouble, c->rank + 1, comm, c->stream);
+        if (!rc) rc = nccl_check(c, A.Send(v + (size_t)(d.own_hi - 1) * col, col, ncclDouble, c->rank + 1, comm, c->stream), "ncclSend (halo, right)");
+        if (!rc) rc = nccl_check(c, A.Recv(v + (size_t)d.own_hi * col, col, ncclDouble, c->rank + 1, comm, c->stream), "ncclRecv (halo, right)");
       }
     }
-    return nccl_check(c, A.GroupEnd(), "ncclGroupEnd (halo)");
+    const int rce = nccl_check(c, A.GroupEnd(), "ncclGroupEnd (halo)");
+    return rc ? rc : rce;
   }
   for (size_t r = 0; r + 1 < cs.size(); ++r) {
     msf_ctx* a = cs[r];

@@ -962,7 +962,7 @@ static bool launch_apply_tma(msf_ctx* c, int rhs0, int nr, const double* x, doub
   }();
   (void)attr;
   const long long ntiles = (long long)((d.nnx + TMA_TX - 1) / TMA_TX) * ((d.nny + TMA_TY - 1) / TMA_TY) * nr;
-  const int grid = (int)std::min<long long>(ntiles, 2 * 148);
+  const int grid = (int)std::min<long long>(ntiles, 2LL * c->n_sm);
   launch_k(k_apply_tma<MODE>, dim3(grid), dim3(NTHR), TMA_SMEM, c->stream, mx, me, d, c->K0,
            (const double2*)bvec, (double2*)y, c->fixn, c->sc, c->partials, c->counters, rhs0, nr,
            gated ? 1 : 0, dmode, c->max_partials, c->dsum, c->apart);
@@ -986,7 +986,7 @@ static bool launch_apply_direct(msf_ctx* c, int rhs0, int nr, const double* x, d
     // residual form, which also streams b, is faster one node per thread)
     const int by = (d.nny + 31) / 32;
     int kx = 8;
-    while (kx > 2 && (long long)by * ((d.nnx + 8 * kx - 1) / (8 * kx)) * nr < 4 * 148) kx /= 2;
+    while (kx > 2 && (long long)by * ((d.nnx + 8 * kx - 1) / (8 * kx)) * nr < 4LL * c->n_sm) kx /= 2;
     if (c->apply_sw_kx) kx = c->apply_sw_kx;
     const dim3 grid(by, (d.nnx + 8 * kx - 1) / (8 * kx), nr);
 #define MSF_SW(KX)                                                                                  \
@@ -1043,7 +1043,7 @@ void launch_sgs_phase(msf_ctx* c, int rhs0, int nr, const double* r, double* z, 
     const char* e = std::getenv("MSF_SGS_CAP");
     return !(e && std::string(e) == "0");
   }();
-  const size_t smem = (cap_env && (long long)grd.x * grd.y * nr <= 4LL * 148) ? 46 * 1024 : 0;
+  const size_t smem = (cap_env && (long long)grd.x * grd.y * nr <= 4LL * c->n_sm) ? 46 * 1024 : 0;
 #define MSF_SGS(F, B, Z, RZ, col)                                                               \
   launch_k(k_sgs_colour<F, B, Z, RZ>, grd, blk, smem, c->stream, d, c->K0, c->E_loc,           \
            (const double2*)r, (double2*)z, c->fixn, c->sc, c->partials, c->counters,            \
@@ -1154,7 +1154,7 @@ void launch_update_f0(msf_ctx* c, int rhs0, int nr) {
     const char* e = std::getenv("MSF_F0_CAP");
     return !(e && std::string(e) == "0");
   }();
-  const size_t cap = (cap_env && (long long)grd.x * grd.y * nr <= 4LL * 148) ? 46 * 1024 : 0;
+  const size_t cap = (cap_env && (long long)grd.x * grd.y * nr <= 4LL * c->n_sm) ? 46 * 1024 : 0;
   launch_k(k_update_f0, grd, dim3(32, 8), cap, c->stream,
            d, c->K0, c->E_loc, (double2*)c->u, (double2*)c->r, (const double2*)c->pv,
            (const double2*)c->q, (double2*)c->z, c->fixn, c->sc, c->partials, c->counters,

@@ -134,6 +134,7 @@ struct msf_ctx {
   Dims d{};            // global grid (coarse space, filter, moduli, basis)
   Dims dl{};           // fine grid of this rank (== d on one GPU)
   int rank = 0, nranks = 1;
+  int n_sm = 148;             // multiprocessors of the device (read at setup; grid sizing rules)
   StripBounds sb{};
   msf_comm* comm = nullptr;   // null: single GPU
   double* E_loc = nullptr;    // E + first local element column (stride dl.estride)
