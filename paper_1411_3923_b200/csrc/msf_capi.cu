@@ -73,6 +73,8 @@ struct Plan {
   std::vector<double> fw;
   double wsum = 1.0;
   std::vector<CrLevel> cr;
+  bool use_nd = false;        // nested-dissection coarse solve (single GPU)
+  NdPlan nd;
   int n_local = 0;            // chain levels (the rest: interface levels, strips only)
   std::vector<int> iface;     // interface blocks (strips only)
   int nslot = 0;              // stored K_c blocks per realisation
@@ -250,11 +252,10 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     return act;
   };
   if (nranks == 1) {
-    // one chain of all blocks: level l eliminates the odd multiples of 2^l
-    std::vector<int> all(d.nbc);
-    for (int i = 0; i < d.nbc; ++i) all[i] = i;
-    P.top_blocks = reduce(all, (size_t)top_max, true);
-    P.n_local = (int)P.cr.size();
+    // nested dissection of the coarse node grid (msf_nd.cu)
+    if (!nd_build_plan(d, P.nd)) { msg = "internal: nested-dissection plan"; return MSF_ERR_ARG; }
+    P.use_nd = true;
+    P.n_local = 0;
   } else {
     // strip partition: this rank's chain [C0, C1] down to its two ends,
     // then the interface chain C0_0 = 0, C0_1, ..., C0_{N-1}, ncx (replicated)
@@ -277,8 +278,7 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   // (slots 0..) and the remaining interface blocks (memory about 1/nranks of the blocks)
   P.slot.assign(d.nbc, -1);
   if (nranks == 1) {
-    for (int i = 0; i < d.nbc; ++i) P.slot[i] = i;
-    P.nslot = d.nbc;
+    P.nslot = 0;   // nested dissection: no block-tridiagonal copies of K_c
   } else {
     const int lo = P.sb.C0, hi = (rank == nranks - 1) ? d.ncx : P.sb.C1;
     int ns = 0;
@@ -356,6 +356,7 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     add(P.top_ptrs * sizeof(double*));       // top job tables
     add(T * 4);                              // top block list
   }
+  if (P.use_nd) add(nd_workspace_bytes(d, P.nd));
   add(2 * MSF_MAX_RHS * 4);                  // factor_status
   {
     // blocked-inverse scratch for the largest batch (a reduction level or the top pivots)
@@ -482,11 +483,11 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   {
     const char* mode = std::getenv("MSF_PCG_MODE");
     // default: graph-launched iterations (measured faster); opt-in persistent
-    c->persistent = (mode && std::string(mode) == "persistent") && transport == 0;
+    c->persistent = (mode && std::string(mode) == "persistent") && transport == 0 && !P.use_nd;
     c->stream_iters = mode && std::string(mode) == "stream";
     if (const char* gi = std::getenv("MSF_GRAPH_ITERS")) c->graph_iters = std::max(1, std::min(64, std::atoi(gi)));
     const char* cc = std::getenv("MSF_COARSE_COOP");
-    c->coarse_coop = transport == 0 && cc && std::string(cc) == "1";   // opt-in: measured slower
+    c->coarse_coop = transport == 0 && cc && std::string(cc) == "1" && !P.use_nd;   // opt-in: measured slower
     if (std::getenv("MSF_PERSIST_PROFILE")) {   // debug only: phase timeline buffer
       cudaMalloc(&c->prof_d, 32 * 64 * sizeof(unsigned long long));
       cudaMemset(c->prof_d, 0, 32 * 64 * sizeof(unsigned long long));
@@ -582,6 +583,14 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     c->top_W = (double*)take(R * T * mm * 8);
     c->top_jobs_d = (char*)take(P.top_ptrs * sizeof(double*));
     c->top_blocks_d = (int*)take(T * 4);
+  }
+  c->use_nd = P.use_nd;
+  if (c->use_nd) {
+    c->nd = P.nd;
+    if (nd_setup(c, cur) != cudaSuccess) {
+      delete c;
+      return msf_fail(nullptr, MSF_ERR_CUDA, "setup: nested-dissection plan upload");
+    }
   }
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
   c->binv_P = (double*)take(P.binv_n * 64 * 64 * 8);
@@ -1556,6 +1565,22 @@ int msf_get_coarse_blocks(msf_ctx* c, int rhs, double* D_host, double* U_host) {
   if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
   if (c->nranks > 1) return msf_fail(c, MSF_ERR_STATE, "get_coarse_blocks: K_c is distributed on a strip partition");
   const size_t n = (size_t)c->d.nbc * c->d.mc * c->d.mc;
+  if (c->use_nd) {
+    // K_c is never stored as blocks on the nested-dissection path: gather a copy from the
+    // cell products (diagnostic read-out only)
+    double* DU = nullptr;
+    CK(cudaMalloc(&DU, 2 * (size_t)c->d.R * n * 8));
+    launch_coarse_gather(c, DU, DU + (size_t)c->d.R * n, c->d.nbc);
+    cudaError_t e = cudaSuccess;
+    if (D_host) e = cudaMemcpyAsync(D_host, DU + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess && U_host)
+      e = cudaMemcpyAsync(U_host, DU + (size_t)c->d.R * n + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(DU);
+    CK(e);
+    CKL("get_coarse_blocks");
+    return MSF_OK;
+  }
   // Dc/Uc are overwritten by the factorisation: re-gather, copy out, re-factorise.
   launch_coarse_galerkin(c);
   if (D_host) CK(cudaMemcpyAsync(D_host, c->Dc + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1615,7 +1640,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
       const double mm = (double)d.mc * d.mc * 8;
       cr += L.surv.size() * 2 * mm + L.elim.size() * 3 * mm;   // forward Q,P ; back Dinv,P,Q
     }
-    bytes[3] = R * cr;
+    bytes[3] = c->use_nd ? R * (double)c->nd.solve_bytes : R * cr;
   }
   bytes[4] = R * (nn * 32) + (double)c->n_cls * d.kmax * d.box_nodes * 16 + R * (double)d.n_agg * d.kmax * 8;
   bytes[5] = R * (nn * 16 * 3 + ne * 8) + nn;                        // z, r, E -> t
@@ -1664,52 +1689,35 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  auto run = [&](int which) {
+    switch (which) {
+      case 0: launch_matvec(c, 0, R, c->pv, c->q, false, true); break;
+      case 1: launch_sgs(c, 0, R, c->r, c->z, false); break;
+      case 2: launch_restrict(c, 0, R, c->t, false); break;
+      case 3: launch_coarse_solve(c, 0, R, false); break;
+      case 4: launch_prolong(c, 0, R, c->z, false); break;
+      case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
+      case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
+      case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
+      case 8: launch_update_f0(c, 0, R); break;
+      case 9: launch_pcg_p(c, 0, R, false); break;
+      case 10:   // whole K_c assembly + factorisation (nested dissection) / chain part (strips)
+        if (c->use_nd) launch_assemble_coarse(c);
+        else launch_assemble_local(c);
+        break;
+      case 11:   // a strip re-reads the all-reduced interface blocks before the top part
+        if (!c->iface.empty()) launch_iface_mat_unpack(c);
+        launch_assemble_top(c);
+        break;
+      case 12: launch_coarse_forward_local(c, 0, R, false); break;
+      case 13: launch_coarse_top(c, 0, R, false); break;
+      case 14: launch_coarse_back_local(c, 0, R, false); break;
+    }
+  };
   auto timeit = [&](int which) -> double {
-    for (int w = 0; w < 2; ++w) {
-      switch (which) {
-        case 0: launch_matvec(c, 0, R, c->pv, c->q, false, true); break;
-        case 1: launch_sgs(c, 0, R, c->r, c->z, false); break;
-        case 2: launch_restrict(c, 0, R, c->t, false); break;
-        case 3: launch_coarse_solve(c, 0, R, false); break;
-        case 4: launch_prolong(c, 0, R, c->z, false); break;
-        case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
-        case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
-        case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
-        case 8: launch_update_f0(c, 0, R); break;
-        case 9: launch_pcg_p(c, 0, R, false); break;
-        case 10: launch_assemble_local(c); break;
-        case 11:   // a strip re-reads the all-reduced interface blocks before the top part
-          if (!c->iface.empty()) launch_iface_mat_unpack(c);
-          launch_assemble_top(c);
-          break;
-        case 12: launch_coarse_forward_local(c, 0, R, false); break;
-        case 13: launch_coarse_top(c, 0, R, false); break;
-        case 14: launch_coarse_back_local(c, 0, R, false); break;
-      }
-    }
+    for (int w = 0; w < 2; ++w) run(which);
     cudaEventRecord(e0, c->stream);
-    for (int i = 0; i < reps; ++i) {
-      switch (which) {
-        case 0: launch_matvec(c, 0, R, c->pv, c->q, false, true); break;
-        case 1: launch_sgs(c, 0, R, c->r, c->z, false); break;
-        case 2: launch_restrict(c, 0, R, c->t, false); break;
-        case 3: launch_coarse_solve(c, 0, R, false); break;
-        case 4: launch_prolong(c, 0, R, c->z, false); break;
-        case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
-        case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
-        case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
-        case 8: launch_update_f0(c, 0, R); break;
-        case 9: launch_pcg_p(c, 0, R, false); break;
-        case 10: launch_assemble_local(c); break;
-        case 11:   // a strip re-reads the all-reduced interface blocks before the top part
-          if (!c->iface.empty()) launch_iface_mat_unpack(c);
-          launch_assemble_top(c);
-          break;
-        case 12: launch_coarse_forward_local(c, 0, R, false); break;
-        case 13: launch_coarse_top(c, 0, R, false); break;
-        case 14: launch_coarse_back_local(c, 0, R, false); break;
-      }
-    }
+    for (int i = 0; i < reps; ++i) run(which);
     cudaEventRecord(e1, c->stream);
     cudaEventSynchronize(e1);
     float t = 0.f;
@@ -1717,7 +1725,8 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
     return (double)t / reps;
   };
   const int ntimed = c->comm ? 6 : 8;
-  for (int i = 0; i < MSF_BENCH_ENTRIES; ++i) ms[i] = (i < ntimed || i >= 8) ? timeit(i) : -1.0;
+  for (int i = 0; i < MSF_BENCH_ENTRIES; ++i)
+    ms[i] = ((i < ntimed || i >= 8) && !(c->use_nd && i > 10)) ? timeit(i) : -1.0;
   if (ms[7] > 0) ms[7] /= c->graph_iters;   // the graph holds graph_iters iterations
   if (!gR) ms[7] = -1.0;
   cudaEventDestroy(e0);

@@ -1207,20 +1207,11 @@ static bool galerkin_gemm(msf_ctx* c) {
   return true;
 }
 
-void launch_coarse_galerkin(msf_ctx* c) {
+// Galerkin cell products Kcell = Phi_C^T (E K0) Phi_C of this rank's coarse cells (Eq. 10)
+void launch_galerkin_cells(msf_ctx* c) {
   const Dims& d = c->d;
   const int P = 4 * d.kmax;
-  if (galerkin_gemm(c)) {
-    const int nD = c->cr_hi - c->cr_lo + 1, nU = c->cell_hi - c->cell_lo;
-    const size_t total = (size_t)(nD + nU) * d.mc * d.mc;
-    int blocks = (int)std::min<size_t>((total + 255) / 256, 65535);
-    k_coarse_gather<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->Kcell, c->cls_of_agg_d,
-                                                              c->classes_d, c->Dc, c->Uc, c->cr_lo, nD,
-                                                              c->cell_lo, nU, c->id_lo, c->id_hi, c->cr_lo,
-                                                              c->nslot);
-    MSF_LAUNCHED(c);
-    return;
-  }
+  if (galerkin_gemm(c)) return;
   const size_t ncn2 = (size_t)(d.cx + 1) * (d.cy + 1) * 2;
   // largest column chunk whose staged bases fit in shared memory (<= 16 so CH^2 <= NT)
   int CH = std::min(P, 16);
@@ -1236,16 +1227,23 @@ void launch_coarse_galerkin(msf_ctx* c) {
   k_cell_galerkin<<<dim3((c->cell_hi - c->cell_lo) * d.ncy, 1, nch * nch), NT, smem, c->stream>>>(
       d, c->K0, c->E, c->phi, c->cls_of_agg_d, c->Kcell, CH, c->cell_lo * d.ncy);
   MSF_LAUNCHED(c);
-  {
-    const int nD = c->cr_hi - c->cr_lo + 1, nU = c->cell_hi - c->cell_lo;
-    const size_t total = (size_t)(nD + nU) * d.mc * d.mc;
-    int blocks = (int)std::min<size_t>((total + 255) / 256, 65535);
-    k_coarse_gather<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->Kcell, c->cls_of_agg_d,
-                                                              c->classes_d, c->Dc, c->Uc, c->cr_lo, nD,
-                                                              c->cell_lo, nU, c->id_lo, c->id_hi, c->cr_lo,
-                                                              c->nslot);
-    MSF_LAUNCHED(c);
-  }
+}
+
+// Block-tridiagonal copies D_I, U_I of K_c (this rank's chain) gathered from the cell products
+void launch_coarse_gather(msf_ctx* c, double* D, double* U, int nslot) {
+  const Dims& d = c->d;
+  const int nD = c->cr_hi - c->cr_lo + 1, nU = c->cell_hi - c->cell_lo;
+  const size_t total = (size_t)(nD + nU) * d.mc * d.mc;
+  int blocks = (int)std::min<size_t>((total + 255) / 256, 65535);
+  k_coarse_gather<<<dim3(blocks, d.R), 256, 0, c->stream>>>(d, c->Kcell, c->cls_of_agg_d, c->classes_d, D, U,
+                                                            c->cr_lo, nD, c->cell_lo, nU, c->id_lo, c->id_hi,
+                                                            c->cr_lo, nslot);
+  MSF_LAUNCHED(c);
+}
+
+void launch_coarse_galerkin(msf_ctx* c) {
+  launch_galerkin_cells(c);
+  launch_coarse_gather(c, c->Dc, c->Uc, c->nslot);
 }
 
 // In-place inverses of n SPD m x m matrices (device pointer table mats): the one-CTA sweep for
@@ -1357,6 +1355,11 @@ void launch_iface_mat_unpack(msf_ctx* c) {
 }
 
 void launch_assemble_coarse(msf_ctx* c) {
+  if (c->use_nd) {
+    launch_galerkin_cells(c);
+    launch_nd_factor(c);
+    return;
+  }
   launch_assemble_local(c);
   launch_assemble_top(c);
 }
@@ -1479,6 +1482,10 @@ void launch_iface_vec_unpack(msf_ctx* c, int rhs0, int nr) {
 // levels, top system, back substitution in reverse level order.  (A strip context runs the
 // same phases with the interface exchange between them, msf_capi.cu dist_vcycle.)
 void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
+  if (c->use_nd) {
+    launch_nd_solve(c, rhs0, nr, gated);
+    return;
+  }
   launch_coarse_forward_local(c, rhs0, nr, gated);
   launch_coarse_top(c, rhs0, nr, gated);
   launch_coarse_back_local(c, rhs0, nr, gated);

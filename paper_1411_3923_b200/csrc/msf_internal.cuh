@@ -98,6 +98,40 @@ struct TopStep {
   double** ngs = nullptr; double** ngd = nullptr;                                  // A_kk = -Pk
 };
 
+// Nested-dissection coarse solve (msf_nd.cu): one front per box of the recursive dissection
+// of the coarse node grid.  S = the box's separator (or all nodes of a leaf box), B = the
+// ring of nodes around the box; the front matrix F (n_f x n_f, n_f = (s_n + b_n) kmax,
+// row-major, S first) holds after the factorisation -A^{-1}, B A^{-1}, A^{-1} B^T and the
+// Schur complement.
+struct NdFront {
+  int s_n, b_n;       // nodes of S / B
+  int node_off;       // nodes[node_off ..]: s_n S nodes then b_n B nodes (global coarse node ids)
+  int ch0, ch1;       // children fronts (-1: none)
+  int chmap_off;      // chmap[chmap_off + 2 j + q]: index of front node j in child q's B list (-1)
+  int level;          // height in the dissection tree (leaves 0)
+  int vmap_off;       // vmap[vmap_off + j] (int4) for the n_f front variables
+  long long F_off;    // doubles, per realisation
+  long long u_off;    // doubles (b_n kmax update vector), per realisation
+};
+
+struct NdPlan {
+  struct List {       // task list in `lists`: fronts[n] then prefix sums of per-front counts
+    int off = 0, n = 0, total = 0, total2 = 0, total3 = 0;
+    int RW = 1, RB = 8;   // solve lists: rows per warp pass, rows per CTA
+  };
+  std::vector<NdFront> fr;
+  std::vector<int> nodes, chmap, lists, vmap;
+  int root = -1, H = 0;
+  bool ok = true;
+  long long F_total = 0, u_total = 0, scr_doubles = 0;
+  int max_act = 0, max_nf = 0;
+  std::vector<List> asmb, fwd, back;          // per level: assembly tiles, solve row blocks
+  std::vector<std::vector<List>> panel;       // per level, per 64-pivot panel
+  std::vector<int> lev_smax, lev_nfmax;       // per level: max s and n_f
+  std::vector<int> lev_fwd_smem, lev_back_smem;  // per level: solve launch shared memory
+  long long solve_bytes = 0;                  // matrix bytes streamed per solve and realisation
+};
+
 // Device-side dot products awaiting the cross-rank all-reduce (strip partition): kernels
 // that end in a reduction write their local sum to dsum[kind][rhs] instead of finalising the
 // PCG scalars; k_finalize applies the same update to the all-reduced sums.
@@ -154,6 +188,19 @@ struct msf_ctx {
   int mb = 0;  // eigensolver block size
   long long eig_work_doubles = 0;
   std::vector<CrLevel> cr;
+  // nested-dissection coarse solve (single GPU; msf_nd.cu)
+  bool use_nd = false;
+  NdPlan nd;
+  double* nd_F = nullptr;       // [R][F_total] fronts
+  double* nd_u = nullptr;       // [R][u_total] update vectors of the forward sweep
+  double* nd_Q = nullptr;       // sweep scratch: pivot blocks, row panels
+  double* nd_Ar = nullptr;
+  double* nd_Rp = nullptr;
+  NdFront* nd_fr = nullptr;
+  int* nd_nodes = nullptr;
+  int* nd_chmap = nullptr;
+  int* nd_lists = nullptr;
+  int* nd_vmap = nullptr;       // int4 per front variable
   // Coarse solve on a strip partition: levels [0, n_local) reduce this
   // rank's chain of blocks [cr_lo, cr_hi] (the chain's end blocks, shared with the neighbour
   // ranks, are kept); after an all-reduce of the end blocks, levels [n_local, cr.size())
@@ -394,6 +441,17 @@ void launch_coarse_top(msf_ctx* c, int rhs0, int nr, bool gated);
 void launch_coarse_back_local(msf_ctx* c, int rhs0, int nr, bool gated);
 // restriction + coarse solve + prolongation in one cooperative launch (msf_persist.cu)
 int launch_coarse_coop(msf_ctx* c, int rhs0, int nr, const double* t, double* z, bool gated);
+
+// nested dissection (msf_nd.cu)
+bool nd_build_plan(const Dims& d, NdPlan& P);
+size_t nd_workspace_bytes(const Dims& d, const NdPlan& P);
+cudaError_t nd_setup(msf_ctx* c, char*& cur);
+void launch_nd_factor(msf_ctx* c);
+void launch_nd_solve(msf_ctx* c, int rhs0, int nr, bool gated);
+// Galerkin cell products K_cell (and, gather = true, the block-tridiagonal D / U copies for
+// the cyclic reduction or a diagnostic read-out into D, U)
+void launch_galerkin_cells(msf_ctx* c);
+void launch_coarse_gather(msf_ctx* c, double* D, double* U, int nslot);
 
 // ---------------------------------------------------------------- helpers
 int msf_fail(msf_ctx* c, int code, const std::string& msg);
