@@ -1,6 +1,5 @@
 // C ABI of the B200 MsFEM-PCG library (include/msfem_b200.h): host-side plan, workspace
 // carving, PCG driver (one PCG iteration captured once as a CUDA graph), design step.
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -72,18 +71,7 @@ struct Plan {
   std::vector<int> fdx, fdy;
   std::vector<double> fw;
   double wsum = 1.0;
-  std::vector<CrLevel> cr;
-  bool use_nd = false;        // nested-dissection coarse solve (single GPU)
-  NdPlan nd;
-  int n_local = 0;            // chain levels (the rest: interface levels, strips only)
-  std::vector<int> iface;     // interface blocks (strips only)
-  int nslot = 0;              // stored K_c blocks per realisation
-  std::vector<int> slot;      // [nbc] storage slot of each block (-1: not stored)
-  std::vector<int> top_blocks;
-  size_t top_ptrs = 0;
-  size_t binv_n = 1;          // matrices per blocked-inverse batch (scratch sizing)
-  size_t galerkin_G_doubles = 0;
-  size_t jobs_bytes = 0;
+  NdPlan nd;                  // nested-dissection coarse solve (msf_nd.cu)
   int max_partials = 0;
   size_t total = 0;
 };
@@ -109,40 +97,6 @@ int validate(const msf_problem* p, std::string& msg) {
 }
 
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
-
-// One cyclic-reduction level over the ordered active blocks act: the blocks at odd positions
-// that are not protected are eliminated; each keeps its (surviving) list neighbours, each
-// survivor next to an eliminated block records it.  act shrinks to the survivors.  Returns
-// false when nothing is eliminable.
-bool cr_level(std::vector<int>& act, const std::vector<char>& prot, int s, CrLevel& L) {
-  const int n = (int)act.size();
-  std::vector<char> el(n, 0);
-  bool any = false;
-  for (int q = 1; q < n; q += 2)
-    if (!prot[act[q]]) el[q] = 1, any = true;
-  if (!any) return false;
-  L.s = s;
-  for (int q = 0; q < n; ++q)
-    if (el[q]) {
-      L.elim.push_back(act[q]);
-      L.el_l.push_back(act[q - 1]);
-      L.el_r.push_back(q + 1 < n ? act[q + 1] : -1);
-    }
-  std::vector<int> keep;
-  for (int q = 0; q < n; ++q) {
-    if (el[q]) continue;
-    keep.push_back(act[q]);
-    const int l = (q > 0 && el[q - 1]) ? act[q - 1] : -1;
-    const int r = (q + 1 < n && el[q + 1]) ? act[q + 1] : -1;
-    if (l >= 0 || r >= 0) {
-      L.surv.push_back(act[q]);
-      L.sv_l.push_back(l);
-      L.sv_r.push_back(r);
-    }
-  }
-  act.swap(keep);
-  return true;
-}
 
 int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& msg,
               int rank = 0, int nranks = 1) {
@@ -233,79 +187,20 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     P.eig_doubles += 2LL * C.nbx * ml * ml + 3LL * n * P.mb + n + 3LL * P.mb * P.mb + 32 + 8 * 16;
     P.eig_doubles = (P.eig_doubles + 31) & ~31LL;
   }
-  // coarse cyclic-reduction levels.  Truncated: stop once at most top_max blocks remain;
-  // they form a dense top system inverted explicitly.  Default 1 block (plain cyclic
-  // reduction): a multi-block explicit inverse loses accuracy at high contrast (measured
-  // rel. error 7e-2 on a cond 3e12 K_c with 9 blocks), the per-level m x m Schur inverses
-  // do not.
-  P.cr.clear();
-  P.iface.clear();
-  int top_max = 1;
-  if (const char* e = std::getenv("MSF_TOP_BLOCKS")) top_max = std::max(1, std::atoi(e));
-  std::vector<char> prot(d.nbc, 0);
-  auto reduce = [&](std::vector<int> act, size_t keep, bool stride) {
-    for (int s = 1; act.size() > keep; s *= 2) {
-      CrLevel L;
-      if (!cr_level(act, prot, stride ? s : -1, L)) break;
-      P.cr.push_back(L);
-    }
-    return act;
-  };
-  if (nranks == 1) {
-    // nested dissection of the coarse node grid (msf_nd.cu)
-    if (!nd_build_plan(d, P.nd)) { msg = "internal: nested-dissection plan"; return MSF_ERR_ARG; }
-    P.use_nd = true;
-    P.n_local = 0;
-  } else {
-    // strip partition: this rank's chain [C0, C1] down to its two ends,
-    // then the interface chain C0_0 = 0, C0_1, ..., C0_{N-1}, ncx (replicated)
-    const int lo = P.sb.C0, hi = (rank == nranks - 1) ? d.ncx : P.sb.C1;
-    std::vector<int> chain;
-    for (int i = lo; i <= hi; ++i) chain.push_back(i);
-    prot[lo] = prot[hi] = 1;
-    reduce(chain, 2, false);
-    prot[lo] = prot[hi] = 0;
-    P.n_local = (int)P.cr.size();
-    for (int j = 0; j < nranks; ++j) {
+  // nested dissection of the coarse node grid (msf_nd.cu); on a strip partition the first
+  // coarse column of every rank > 0 is an interface separator
+  {
+    std::vector<int> icol(nranks, 0);
+    for (int j = 1; j < nranks; ++j) {
       StripBounds b{};
       if ((rc = strip_bounds(d, j, nranks, b, msg))) return rc;
-      P.iface.push_back(b.C0);
+      icol[j] = b.C0;
     }
-    P.iface.push_back(d.ncx);
-    P.top_blocks = reduce(P.iface, (size_t)top_max, false);
+    if (!nd_build_plan(d, P.nd, rank, nranks, icol)) {
+      msg = "internal: nested-dissection plan";
+      return MSF_ERR_ARG;
+    }
   }
-  // storage slots of the K_c factor blocks: all blocks on one GPU; a strip keeps its chain
-  // (slots 0..) and the remaining interface blocks (memory about 1/nranks of the blocks)
-  P.slot.assign(d.nbc, -1);
-  if (nranks == 1) {
-    P.nslot = 0;   // nested dissection: no block-tridiagonal copies of K_c
-  } else {
-    const int lo = P.sb.C0, hi = (rank == nranks - 1) ? d.ncx : P.sb.C1;
-    int ns = 0;
-    for (int i = lo; i <= hi; ++i) P.slot[i] = ns++;
-    for (int i : P.iface)
-      if (P.slot[i] < 0) P.slot[i] = ns++;
-    P.nslot = ns;
-  }
-  size_t ptrs = 0, ints = 0;
-  for (CrLevel& L : P.cr) {
-    int nq = 0;
-    for (int r : L.el_r) nq += r >= 0 ? 1 : 0;
-    L.n_inv = (int)L.elim.size() * d.R;
-    L.nP = (int)L.elim.size() * d.R;
-    L.nQ = nq * d.R;
-    L.nDl = (int)L.elim.size() * d.R;
-    L.nDr = nq * d.R;
-    L.nU = nq * d.R;
-    ptrs += 2 * L.n_inv + 3 * (L.nP + L.nQ + L.nDl + L.nDr + L.nU);
-    ints += 3 * (L.elim.size() + L.surv.size());
-  }
-  {
-    const long long T = (long long)P.top_blocks.size(), R = d.R;
-    P.top_ptrs = (size_t)T * (2 * R + 3 * R * (T - 1) + 3 * R * (T - 1) * (T - 1) +
-                              3 * R * (T - 1) + 2 * R);
-  }
-  P.jobs_bytes = align_up(ptrs * sizeof(double*)) + align_up(ints * sizeof(int));
   P.max_partials = std::max(apply_partials_needed(d), sgs_colour_partials_needed(d));
 
   // workspace size (node vectors on this rank's strip; moduli of the whole grid)
@@ -329,49 +224,13 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   add(P.classes.size() * d.kmax * 8);        // lam
   add((size_t)P.eig_doubles * 8);            // eig work
   add(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);     // Kcell
-  {
-    // G scratch of the GEMM Galerkin products: up to 32M doubles, at least one cell
-    const size_t per_cell = (size_t)5 * d.cx * d.cy * 4 * d.kmax;
-    const size_t cells = std::max<size_t>(1, std::min<size_t>((size_t)d.ncx * d.ncy, (32u << 20) / per_cell));
-    P.galerkin_G_doubles = cells * per_cell;
-    add(P.galerkin_G_doubles * 8);
-  }
-  add(7 * R * (size_t)P.nslot * d.mc * d.mc * 8);          // Dc Uc Dinv Pc Qc PTc QTc
-  add((size_t)d.nbc * 4);                                  // slot map
   add(2 * R * d.nbc * (size_t)d.mc * 8);     // cb, cx
-  {
-    const size_t nI = P.iface.size(), mm = (size_t)d.mc * d.mc;
-    add(nI * 4);                                          // iface blocks
-    add(R * nI * d.mc * 8);                               // iface_vec
-    add(nI ? R * (2 * nI - 1) * mm * 8 : 0);              // iface_mat
-    add((2 * 3 * R + (nI ? 2 * (2 * nI - 1) * R : 0)) * sizeof(double*));  // pack tables
-  }
   add((size_t)d.n_agg * 4);                  // agg_by_cls
-  add(P.jobs_bytes);
-  {
-    const size_t T = P.top_blocks.size(), mm = (size_t)d.mc * d.mc;
-    add(R * T * T * mm * 8);                 // Atop
-    add(R * mm * 8);                         // Pk
-    add(R * T * mm * 8);                     // W
-    add(P.top_ptrs * sizeof(double*));       // top job tables
-    add(T * 4);                              // top block list
-  }
-  if (P.use_nd) add(nd_workspace_bytes(d, P.nd));
+  add(nd_workspace_bytes(d, P.nd));
   add(2 * MSF_MAX_RHS * 4);                  // factor_status
-  {
-    // blocked-inverse scratch for the largest batch (a reduction level or the top pivots)
-    size_t nmax = (size_t)d.R;
-    for (const CrLevel& L : P.cr) nmax = std::max(nmax, (size_t)L.n_inv);
-    P.binv_n = nmax;
-    add(nmax * 64 * 64 * 8);
-    add(nmax * 64 * (size_t)d.mc * 8);
-    add(nmax * 64 * (size_t)d.mc * 8);       // pivot column copies
-    add(2 * nmax * sizeof(double*));         // their pointer tables
-  }
   add(R * sizeof(PcgScalars));
-  add((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
+  add(R * (size_t)P.max_partials * 8);       // partials
   add(R * (size_t)P.max_partials * 8);       // apart
-  add(cr_levels_dev_bytes((int)P.cr.size()));
   add(R * 8 * 4);                            // counters
   add(64 * 8);                               // scal
   P.total = t + 256;
@@ -474,26 +333,11 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   c->n_cls = (int)P.classes.size();
   c->mb = P.mb;
   c->eig_work_doubles = P.eig_doubles;
-  c->cr = P.cr;
   c->filt_dx = P.fdx; c->filt_dy = P.fdy; c->filt_w = P.fw;
   c->n_filt = (int)P.fw.size();
   c->filt_wsum = P.wsum;
   c->max_partials = P.max_partials;
   c->periodic = (p->tile_x != p->nelx || p->tile_y != p->nely);
-  {
-    const char* mode = std::getenv("MSF_PCG_MODE");
-    // default: graph-launched iterations (measured faster); opt-in persistent
-    c->persistent = (mode && std::string(mode) == "persistent") && transport == 0 && !P.use_nd;
-    c->stream_iters = mode && std::string(mode) == "stream";
-    if (const char* gi = std::getenv("MSF_GRAPH_ITERS")) c->graph_iters = std::max(1, std::min(64, std::atoi(gi)));
-    const char* cc = std::getenv("MSF_COARSE_COOP");
-    c->coarse_coop = transport == 0 && cc && std::string(cc) == "1" && !P.use_nd;   // opt-in: measured slower
-    if (std::getenv("MSF_PERSIST_PROFILE")) {   // debug only: phase timeline buffer
-      cudaMalloc(&c->prof_d, 32 * 64 * sizeof(unsigned long long));
-      cudaMemset(c->prof_d, 0, 32 * 64 * sizeof(unsigned long long));
-    }
-  }
-
   const Dims& d = c->d;
   const size_t R = d.R, nn = c->dl.nn, ne = d.ne, nt = d.nt;
   char* cur = (char*)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
@@ -532,33 +376,14 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   c->lam = (double*)take((size_t)c->n_cls * d.kmax * 8);
   c->eig_work = (double*)take((size_t)P.eig_doubles * 8);
   c->Kcell = (double*)take(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);
-  c->galerkin_G_doubles = P.galerkin_G_doubles;
-  c->galerkin_G = (double*)take(P.galerkin_G_doubles * 8);
-  c->nslot = P.nslot;
-  c->slot_h = P.slot;
-  const size_t blk = R * (size_t)P.nslot * d.mc * d.mc;
-  double* cm = (double*)take(7 * blk * 8);
-  c->slot_d = (int*)take((size_t)d.nbc * 4);
-  c->Dc = cm; c->Uc = cm + blk; c->Dinv = cm + 2 * blk; c->Pc = cm + 3 * blk; c->Qc = cm + 4 * blk;
-  c->PTc = cm + 5 * blk; c->QTc = cm + 6 * blk;
   c->cb = (double*)take(2 * R * d.nbc * (size_t)d.mc * 8);
   c->cx = c->cb + R * d.nbc * (size_t)d.mc;
   {
-    const size_t nI = P.iface.size(), mm = (size_t)d.mc * d.mc;
-    c->iface = P.iface;
-    c->iface_d = (int*)take(nI * 4);
-    c->iface_vec = (double*)take(R * nI * d.mc * 8);
-    c->iface_mat = (double*)take(nI ? R * (2 * nI - 1) * mm * 8 : 0);
-    c->ifm_pack = (double**)take((2 * 3 * R + (nI ? 2 * (2 * nI - 1) * R : 0)) * sizeof(double*));
-    c->ifm_unpack = c->ifm_pack + 2 * 3 * R;
-    c->n_local = P.n_local;
     const bool last = rank == nranks - 1;
     c->cr_lo = c->sb.C0;
     c->cr_hi = (nranks == 1 || last) ? d.ncx : c->sb.C1;
     c->cell_lo = c->sb.C0;
     c->cell_hi = c->sb.C1;
-    c->id_lo = c->sb.C0;
-    c->id_hi = (nranks == 1 || last) ? d.ncx : c->sb.C1 - 1;
   }
   {
     // restriction work list: agglomerates in grid order, so the four boxes that overlap on a
@@ -573,186 +398,37 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     c->n_restrict = (int)c->agg_by_cls_h.size();
     c->agg_by_cls_d = (int*)take((size_t)d.n_agg * 4);
   }
-  c->jobs_d = (char*)take(P.jobs_bytes);
-  {
-    const size_t T = P.top_blocks.size(), mm = (size_t)d.mc * d.mc;
-    c->top_blocks = P.top_blocks;
-    c->top_T = (int)T;
-    c->Atop = (double*)take(R * T * T * mm * 8);
-    c->top_Pk = (double*)take(R * mm * 8);
-    c->top_W = (double*)take(R * T * mm * 8);
-    c->top_jobs_d = (char*)take(P.top_ptrs * sizeof(double*));
-    c->top_blocks_d = (int*)take(T * 4);
-  }
-  c->use_nd = P.use_nd;
-  if (c->use_nd) {
-    c->nd = P.nd;
-    if (nd_setup(c, cur) != cudaSuccess) {
-      delete c;
-      return msf_fail(nullptr, MSF_ERR_CUDA, "setup: nested-dissection plan upload");
-    }
+  c->nd = P.nd;
+  if (nd_setup(c, cur) != cudaSuccess) {
+    delete c;
+    return msf_fail(nullptr, MSF_ERR_CUDA, "setup: nested-dissection plan upload");
   }
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
-  c->binv_P = (double*)take(P.binv_n * 64 * 64 * 8);
-  c->binv_R = (double*)take(P.binv_n * 64 * (size_t)d.mc * 8);
-  c->binv_C = (double*)take(P.binv_n * 64 * (size_t)d.mc * 8);
-  c->binv_Rp = (double**)take(2 * P.binv_n * sizeof(double*));
-  c->binv_Cp = c->binv_Rp + P.binv_n;
-  if (const char* e = std::getenv("MSF_BLOCKED_INV_MIN")) c->blocked_inv_min = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("MSF_RESTRICT_THREADS")) c->restrict_threads = std::atoi(e);
   if (const char* e = std::getenv("MSF_APPLY_DIRECT")) c->apply_direct = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_APPLY_SW")) c->apply_sw = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_APPLY_TMA")) c->apply_tma = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_RESIDUAL_TMA")) c->residual_tma = std::string(e) != "0";
-  if (const char* e = std::getenv("MSF_RESTRICT_WARP")) c->restrict_warp = std::string(e) != "0";
-  if (const char* e = std::getenv("MSF_INV_BLOCKED_SMEM")) c->inv_blocked_smem = std::string(e) != "0";
-  if (const char* e = std::getenv("MSF_GALERKIN_GEMM")) c->galerkin_gemm = std::string(e) != "0";
+  if (const char* e = std::getenv("MSF_RESTRICT_WARP")) {
+    c->restrict_warp = std::string(e) != "0";
+    c->restrict_warp_force = std::string(e) == "force";   // tests: every launch
+  }
+  {
+    const char* e = std::getenv("MSF_PDL");   // read at every setup (tests toggle it)
+    g_msf_pdl = !(e && std::string(e) == "0");
+  }
   if (const char* e = std::getenv("MSF_SW_KX")) {
     const int k = std::atoi(e);
     c->apply_sw_kx = (k == 2 || k == 4 || k == 8) ? k : 0;
   }
   c->sc = (PcgScalars*)take(R * sizeof(PcgScalars));
-  c->partials = (double*)take((R * (size_t)P.max_partials + MSF_PERSIST_PARTIALS) * 8);
+  c->partials = (double*)take(R * (size_t)P.max_partials * 8);
   c->apart = (double*)take(R * (size_t)P.max_partials * 8);
-  c->cr_levels_d = take(cr_levels_dev_bytes((int)c->cr.size()));
   c->counters = (unsigned*)take(R * 8 * 4);
   c->scal = (double*)take(64 * 8);
   if ((size_t)(cur - (char*)workspace) > workspace_bytes) {
     delete c;
     return msf_fail(nullptr, MSF_ERR_SPACE, "internal: workspace carve overflow");
-  }
-
-  // CR pointer tables
-  {
-    std::vector<double*> ptrs;
-    std::vector<int> ints;
-    const size_t per = (size_t)d.mc * d.mc;
-    auto B = [&](double* base, int rhs, int k) { return base + ((size_t)rhs * c->nslot + c->slot_h[k]) * per; };
-    struct Fix { size_t inv, P, Q, Dl, Dr, U, elim, surv; };
-    std::vector<Fix> fixes;
-    for (CrLevel& L : c->cr) {
-      Fix F{};
-      F.inv = ptrs.size();
-      for (int rhs = 0; rhs < d.R; ++rhs)
-        for (int k : L.elim) ptrs.push_back(B(c->Dinv, rhs, k));
-      for (int rhs = 0; rhs < d.R; ++rhs)
-        for (int k : L.elim) ptrs.push_back(B(c->Dc, rhs, k));
-      // eliminated k with surviving neighbours l (always) and r (if any); U_l couples l-k,
-      // U_k couples k-r:  P_k = U_l Dinv_k, Q_k = U_k^T Dinv_k, D_l -= P_k U_l^T,
-      // D_r -= Q_k U_k, U_l <- -P_k U_k (the new l-r coupling)
-      const size_t ne = L.elim.size();
-      std::vector<double*> a, b, cc;
-      auto flush = [&](size_t& off) {
-        off = ptrs.size();
-        ptrs.insert(ptrs.end(), a.begin(), a.end()); ptrs.insert(ptrs.end(), b.begin(), b.end()); ptrs.insert(ptrs.end(), cc.begin(), cc.end());
-        a.clear(); b.clear(); cc.clear();
-      };
-      for (int rhs = 0; rhs < d.R; ++rhs)
-        for (size_t e = 0; e < ne; ++e) { const int k = L.elim[e], l = L.el_l[e]; a.push_back(B(c->Uc, rhs, l)); b.push_back(B(c->Dinv, rhs, k)); cc.push_back(B(c->Pc, rhs, k)); }
-      flush(F.P);
-      for (int rhs = 0; rhs < d.R; ++rhs)
-        for (size_t e = 0; e < ne; ++e) if (L.el_r[e] >= 0) { const int k = L.elim[e]; a.push_back(B(c->Uc, rhs, k)); b.push_back(B(c->Dinv, rhs, k)); cc.push_back(B(c->Qc, rhs, k)); }
-      flush(F.Q);
-      for (int rhs = 0; rhs < d.R; ++rhs)
-        for (size_t e = 0; e < ne; ++e) { const int k = L.elim[e], l = L.el_l[e]; a.push_back(B(c->Pc, rhs, k)); b.push_back(B(c->Uc, rhs, l)); cc.push_back(B(c->Dc, rhs, l)); }
-      flush(F.Dl);
-      for (int rhs = 0; rhs < d.R; ++rhs)
-        for (size_t e = 0; e < ne; ++e) if (L.el_r[e] >= 0) { const int k = L.elim[e], r = L.el_r[e]; a.push_back(B(c->Qc, rhs, k)); b.push_back(B(c->Uc, rhs, k)); cc.push_back(B(c->Dc, rhs, r)); }
-      flush(F.Dr);
-      for (int rhs = 0; rhs < d.R; ++rhs)
-        for (size_t e = 0; e < ne; ++e) if (L.el_r[e] >= 0) { const int k = L.elim[e], l = L.el_l[e]; a.push_back(B(c->Pc, rhs, k)); b.push_back(B(c->Uc, rhs, k)); cc.push_back(B(c->Uc, rhs, l)); }
-      flush(F.U);
-      F.elim = ints.size();
-      for (size_t e = 0; e < ne; ++e) { ints.push_back(L.elim[e]); ints.push_back(L.el_l[e]); ints.push_back(L.el_r[e]); }
-      F.surv = ints.size();
-      for (size_t q = 0; q < L.surv.size(); ++q) { ints.push_back(L.surv[q]); ints.push_back(L.sv_l[q]); ints.push_back(L.sv_r[q]); }
-      fixes.push_back(F);
-    }
-    double** pd = (double**)c->jobs_d;
-    int* id = (int*)(c->jobs_d + align_up(ptrs.size() * sizeof(double*)));
-    for (size_t i = 0; i < c->cr.size(); ++i) {
-      CrLevel& L = c->cr[i];
-      const Fix& F = fixes[i];
-      L.inv = pd + F.inv; L.invsrc = L.inv + L.n_inv;
-      {
-        L.pA = pd + F.P; L.pB = L.pA + L.nP; L.pC = L.pB + L.nP;
-        L.qA = pd + F.Q; L.qB = L.qA + L.nQ; L.qC = L.qB + L.nQ;
-        L.dlA = pd + F.Dl; L.dlB = L.dlA + L.nDl; L.dlC = L.dlB + L.nDl;
-        L.drA = pd + F.Dr; L.drB = L.drA + L.nDr; L.drC = L.drB + L.nDr;
-        L.uA = pd + F.U; L.uB = L.uA + L.nU; L.uC = L.uB + L.nU;
-      }
-      L.elim_d = id + F.elim;
-      L.surv_d = id + F.surv;
-    }
-    cudaMemcpyAsync(c->jobs_d, ptrs.data(), ptrs.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
-    cudaMemcpyAsync(id, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream);
-    std::vector<char> lv(cr_levels_dev_bytes((int)c->cr.size()));
-    fill_cr_levels_dev(c->cr, lv.data());
-    cudaMemcpyAsync(c->cr_levels_d, lv.data(), lv.size(), cudaMemcpyHostToDevice, c->stream);
-    // top-system Gauss-Jordan tables: step k pivots on block k
-    const int T = c->top_T;
-    const size_t mmb = (size_t)d.mc * d.mc;
-    auto At = [&](int rhs, int i, int j) { return c->Atop + (((size_t)rhs * T + i) * T + j) * mmb; };
-    auto Pk = [&](int rhs) { return c->top_Pk + (size_t)rhs * mmb; };
-    auto Wi = [&](int rhs, int i) { return c->top_W + ((size_t)rhs * T + i) * mmb; };
-    std::vector<double*> tp;
-    struct Off { size_t invsrc, inv, wA, wB, wC, uA, uB, uC, cps, cpd, tpd, ngs, ngd; };
-    std::vector<Off> offs;
-    for (int k = 0; k < T; ++k) {
-      Off o{};
-      o.invsrc = tp.size(); for (int r = 0; r < d.R; ++r) tp.push_back(At(r, k, k));
-      o.inv = tp.size();    for (int r = 0; r < d.R; ++r) tp.push_back(Pk(r));
-      o.wA = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(At(r, i, k));
-      o.wB = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(Pk(r));
-      o.wC = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(Wi(r, i));
-      o.uA = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) for (int j = 0; j < T; ++j) if (i != k && j != k) tp.push_back(Wi(r, i));
-      o.uB = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) for (int j = 0; j < T; ++j) if (i != k && j != k) tp.push_back(At(r, k, j));
-      o.uC = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) for (int j = 0; j < T; ++j) if (i != k && j != k) tp.push_back(At(r, i, j));
-      o.cps = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(Wi(r, i));
-      o.cpd = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(At(r, i, k));
-      o.tpd = tp.size(); for (int r = 0; r < d.R; ++r) for (int i = 0; i < T; ++i) if (i != k) tp.push_back(At(r, k, i));
-      o.ngs = tp.size(); for (int r = 0; r < d.R; ++r) tp.push_back(Pk(r));
-      o.ngd = tp.size(); for (int r = 0; r < d.R; ++r) tp.push_back(At(r, k, k));
-      offs.push_back(o);
-    }
-    double** base = (double**)c->top_jobs_d;
-    c->top_steps.assign(T, TopStep());
-    for (int k = 0; k < T; ++k) {
-      TopStep& S = c->top_steps[k];
-      const Off& o = offs[k];
-      S.nI = d.R; S.invsrc = base + o.invsrc; S.inv = base + o.inv;
-      S.nW = d.R * (T - 1); S.wA = base + o.wA; S.wB = base + o.wB; S.wC = base + o.wC;
-      S.nU = d.R * (T - 1) * (T - 1); S.uA = base + o.uA; S.uB = base + o.uB; S.uC = base + o.uC;
-      S.nC = d.R * (T - 1); S.cps = base + o.cps; S.cpd = base + o.cpd; S.tpd = base + o.tpd;
-      S.ngs = base + o.ngs; S.ngd = base + o.ngd;
-    }
-    cudaMemcpyAsync(c->top_jobs_d, tp.data(), tp.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
-    cudaMemcpyAsync(c->top_blocks_d, c->top_blocks.data(), c->top_blocks.size() * 4, cudaMemcpyHostToDevice, c->stream);
-    // strip partition: interface share tables.  iface_mat slot j < nI holds D of interface
-    // block j, slot nI + j the coupling U of interface blocks j, j+1.  This rank contributes
-    // D of its chain ends (partial sums: each end block's Galerkin cells and chain Schur
-    // complements split over two ranks) and the complete U of its reduced chain.
-    std::vector<double*> ip, iu;
-    const size_t nI = c->iface.size();
-    if (nI) {
-      auto S = [&](int rhs, size_t j) { return c->iface_mat + ((size_t)rhs * (2 * nI - 1) + j) * mmb; };
-      const int a = rank, b = rank + 1;
-      for (int rhs = 0; rhs < d.R; ++rhs) {
-        ip.push_back(c->Dc + ((size_t)rhs * c->nslot + c->slot_h[c->iface[a]]) * mmb);
-        ip.push_back(c->Dc + ((size_t)rhs * c->nslot + c->slot_h[c->iface[b]]) * mmb);
-        ip.push_back(c->Uc + ((size_t)rhs * c->nslot + c->slot_h[c->iface[a]]) * mmb);
-      }
-      for (int rhs = 0; rhs < d.R; ++rhs) { ip.push_back(S(rhs, a)); ip.push_back(S(rhs, b)); ip.push_back(S(rhs, nI + a)); }
-      for (int rhs = 0; rhs < d.R; ++rhs)
-        for (size_t j = 0; j < 2 * nI - 1; ++j) iu.push_back(S(rhs, j));
-      for (int rhs = 0; rhs < d.R; ++rhs)
-        for (size_t j = 0; j < 2 * nI - 1; ++j)
-          iu.push_back((j < nI ? c->Dc : c->Uc) + ((size_t)rhs * c->nslot + c->slot_h[c->iface[j < nI ? j : j - nI]]) * mmb);
-      cudaMemcpyAsync(c->ifm_pack, ip.data(), ip.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
-      cudaMemcpyAsync(c->ifm_unpack, iu.data(), iu.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
-      cudaMemcpyAsync(c->iface_d, c->iface.data(), nI * 4, cudaMemcpyHostToDevice, c->stream);
-    }
-    cudaStreamSynchronize(c->stream);   // host staging buffers go out of scope
   }
 
   // fixed mask per node, load, filter table, classes
@@ -788,43 +464,18 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->factor_status, 0, 2 * MSF_MAX_RHS * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->counters, 0, R * 8 * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->sc, 0, R * sizeof(PcgScalars), c->stream);
-  std::vector<double*> binv_ptrs(2 * P.binv_n);
-  for (size_t i = 0; i < P.binv_n; ++i) {
-    binv_ptrs[i] = c->binv_R + i * 64 * (size_t)d.mc;
-    binv_ptrs[P.binv_n + i] = c->binv_C + i * 64 * (size_t)d.mc;
-  }
-  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->binv_Rp, binv_ptrs.data(), binv_ptrs.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->scal, 0, 64 * 8, c->stream);
   if (ce == cudaSuccess && c->dsum) ce = cudaMemsetAsync(c->dsum, 0, FIN_KINDS * MSF_MAX_RHS * 8, c->stream);
   // node vectors start at 0 (halo / padding columns are only ever written by exchanges)
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->u, 0, 6 * R * 2 * nn * 8, c->stream);
-  // coarse vectors and K_c blocks start at 0: a strip reads (with zero weights) the coarse
-  // solution of the blocks next to its chain, which it never writes
+  // coarse vectors start at 0: a strip reads (with zero weights) the coarse solution of the
+  // agglomerates next to its chain, which it never writes, and packs the interface entries of
+  // its (zero) neighbours' columns
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->cb, 0, 2 * R * d.nbc * (size_t)d.mc * 8, c->stream);
-  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->Dc, 0, 2 * R * (size_t)c->nslot * d.mc * d.mc * 8, c->stream);
-  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->slot_d, c->slot_h.data(), d.nbc * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
-  {
-    const char* e = std::getenv("MSF_CUBLAS");
-    cublasHandle_t h = nullptr;
-    if (ce == cudaSuccess && !(e && std::string(e) == "0") && cublasCreate(&h) == CUBLAS_STATUS_SUCCESS) {
-      cublasSetStream(h, c->stream);
-      cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);   // plain fp64 (no emulation, no reduced precision)
-      c->cublas = h;
-    }
-  }
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->sc_host, MSF_MAX_RHS * sizeof(PcgScalars));
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->scal_host, 80 * 8);
-  if (const char* e = std::getenv("MSF_SGS_NB")) c->sgs_nb = std::string(e) == "1";
   if (const char* e = std::getenv("MSF_PROLONG_NR")) c->prolong_nr = std::string(e) != "0";
-  if (transport != 0) c->sgs_nb = false;
-  if (ce == cudaSuccess && c->sgs_nb) {
-    const size_t tiles = (size_t)((c->dl.nny + 1) / 2 + 31) / 32 * (((c->dl.nnx + 1) / 2 + 7) / 8);
-    ce = cudaMalloc((void**)&c->sgs_nb_flags, tiles * MSF_MAX_RHS * 4 + 64);
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(c->sgs_nb_flags, 0, tiles * MSF_MAX_RHS * 4 + 64, c->stream);
-    c->sgs_nb_err = (int*)(c->sgs_nb_flags + tiles * MSF_MAX_RHS);
-    c->sgs_nb_max_ctas = sgs_nb_max_ctas(c);
-  }
   {
     // restriction groups of same-class agglomerates (k_restrict_batch), when they batch well
     const char* e = std::getenv("MSF_RESTRICT_BATCH");
@@ -868,10 +519,8 @@ int msf_destroy(msf_ctx* c) {
   dist_comm_destroy(c);
   destroy_graphs(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  if (c->cublas) cublasDestroy((cublasHandle_t)c->cublas);
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->scal_host) cudaFreeHost(c->scal_host);
-  if (c->sgs_nb_flags) cudaFree(c->sgs_nb_flags);
   if (c->rgroups_d) cudaFree(c->rgroups_d);
   delete c;
   return MSF_OK;
@@ -880,7 +529,6 @@ int msf_destroy(msf_ctx* c) {
 int msf_set_stream(msf_ctx* c, void* stream) {
   if (!c) return msf_fail(nullptr, MSF_ERR_ARG, "null ctx");
   c->stream = (cudaStream_t)stream;
-  if (c->cublas) cublasSetStream((cublasHandle_t)c->cublas, c->stream);
   destroy_graphs(c);
   return MSF_OK;
 }
@@ -939,15 +587,10 @@ int msf_assemble_coarse(msf_ctx* c) {
 static void enqueue_vcycle(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
                            int rz_mode = 0, bool f0_done = false) {
   launch_sgs_sweep(c, rhs0, nr, r, z, gated, !f0_done, 0, f0_done);  // z = SGS(0; r)
-  if (c->coarse_coop) {
-    launch_residual(c, rhs0, nr, r, z, c->t, gated);                  // t = r - K z
-    launch_coarse_coop(c, rhs0, nr, c->t, z, gated);                  // z += R^T Kc^-1 R t
-  } else {
-    launch_residual(c, rhs0, nr, r, z, c->t, gated);                  // t = r - K z
-    launch_restrict(c, rhs0, nr, c->t, gated);                        // c = R t
-    launch_coarse_solve(c, rhs0, nr, gated);
-    launch_prolong(c, rhs0, nr, z, gated);                            // z += R^T c
-  }
+  launch_residual(c, rhs0, nr, r, z, c->t, gated);                    // t = r - K z
+  launch_restrict(c, rhs0, nr, c->t, gated);                          // c = R t
+  launch_nd_solve(c, rhs0, nr, gated);                                // c <- K_c^{-1} c
+  launch_prolong(c, rhs0, nr, z, gated);                              // z += R^T c
   launch_sgs_sweep(c, rhs0, nr, r, z, gated, false, rz_mode, false); // z = SGS(z; r) (+ r.z)
 }
 
@@ -963,11 +606,7 @@ static void enqueue_iteration(msf_ctx* c, int rhs0, int nr) {
 static int read_scalars(msf_ctx* c, int nr) {
   CK(cudaMemcpyAsync(c->sc_host, c->sc, nr * sizeof(PcgScalars), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(c->scal_host + 64, c->factor_status, 2 * MSF_MAX_RHS * 4, cudaMemcpyDeviceToHost, c->stream));
-  if (c->sgs_nb_err)
-    CK(cudaMemcpyAsync(c->scal_host + 72, c->sgs_nb_err, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  if (c->sgs_nb_err && *(const int*)(c->scal_host + 72))
-    return msf_fail(c, MSF_ERR_CUDA, "single-launch Gauss-Seidel sweep: a neighbour wait timed out");
   const int* fs = (const int*)(c->scal_host + 64);
   for (int k = 0; k < 2 * MSF_MAX_RHS; ++k)
     if (fs[k])
@@ -1004,31 +643,27 @@ static int dist_sgs(const Ranks& cs, int rhs0, int nr, int first, int rz_mode) {
   return MSF_OK;
 }
 
-// Coarse correction on a strip partition: each rank restricts to and
-// reduces its own chain of K_c blocks; one all-reduce of the chain ends' rhs (nranks + 1
-// blocks) feeds the replicated interface system; each rank back-substitutes its chain and
-// prolongs onto its owned nodes; the left halo column needs the neighbour's chain, so z's
-// halo is exchanged.
+// Coarse correction on a strip partition: each rank restricts onto the
+// agglomerates of its chain (partial sums on the two interface columns) and solves the fronts
+// of its own box; the interface fronts' right-hand sides (partial restriction + box-root
+// updates) are all-reduced, the interface fronts solved on every rank, then each rank
+// back-substitutes its box and prolongs onto its owned nodes; the left halo column needs the
+// neighbour's chain, so z's halo is exchanged.
 static int dist_coarse(const Ranks& cs, int rhs0, int nr) {
   int rc;
   for (msf_ctx* c : cs) {
     launch_residual(c, rhs0, nr, c->r, c->z, c->t, true);
-    launch_restrict(c, rhs0, nr, c->t, true);     // R_c t of the chain, owned nodes
-    launch_coarse_forward_local(c, rhs0, nr, true);
+    launch_restrict(c, rhs0, nr, c->t, true);
+    launch_nd_solve_local_fwd(c, rhs0, nr, true);
   }
-  const size_t nI = cs[0]->iface.size();
-  if (nI) {
-    const size_t n = nI * cs[0]->d.mc;
-    for (msf_ctx* c : cs) launch_iface_vec_pack(c, rhs0, nr);
-    if ((rc = dist_allreduce(cs, &msf_ctx::iface_vec, rhs0 * n, nr * n))) return rc;
-    for (msf_ctx* c : cs) launch_iface_vec_unpack(c, rhs0, nr);
-  }
+  const size_t nv = (size_t)cs[0]->nd.vtop_total;
+  if (nv && (rc = dist_allreduce(cs, &msf_ctx::nd_vtop, rhs0 * nv, nr * nv))) return rc;
   for (msf_ctx* c : cs) {
-    launch_coarse_top(c, rhs0, nr, true);         // replicated interface system
-    launch_coarse_back_local(c, rhs0, nr, true);
+    launch_nd_solve_top(c, rhs0, nr, true);
+    launch_nd_solve_local_back(c, rhs0, nr, true);
     launch_prolong(c, rhs0, nr, c->z, true);
   }
-  if (nI) return dist_halo(cs, &msf_ctx::z, rhs0, nr);
+  if (cs[0]->nranks > 1) return dist_halo(cs, &msf_ctx::z, rhs0, nr);
   return MSF_OK;
 }
 
@@ -1039,9 +674,9 @@ static int dist_vcycle(const Ranks& cs, int rhs0, int nr, bool f0_done, int rz_m
   return dist_sgs(cs, rhs0, nr, 1, rz_mode);
 }
 
-// K_c assembly + factorisation on a strip partition: Galerkin products of the owned cells and
-// the chain levels per rank, all-reduce of the chain ends (D of the nranks + 1 interface
-// blocks, U of the reduced chains), replicated interface levels and top system.
+// K_c assembly + factorisation on a strip partition: Galerkin products of the owned cells,
+// the fronts of the rank's box and its partial interface fronts; one all-reduce of the
+// interface fronts (per realisation); the interface fronts factored on every rank.
 static int dist_assemble(const Ranks& cs) {
   msf_ctx* c0 = cs[0];
   for (msf_ctx* x : cs) {
@@ -1049,15 +684,15 @@ static int dist_assemble(const Ranks& cs) {
     if (!x->have_basis) return msf_fail(c0, MSF_ERR_STATE, "assemble_coarse before build_coarse_basis");
   }
   int rc;
-  for (msf_ctx* c : cs) launch_assemble_local(c);
-  const size_t nI = c0->iface.size();
-  if (nI) {
-    for (msf_ctx* c : cs) launch_iface_mat_pack(c);
-    const size_t n = (size_t)c0->d.R * (2 * nI - 1) * c0->d.mc * c0->d.mc;
-    if ((rc = dist_allreduce(cs, &msf_ctx::iface_mat, 0, n))) return rc;
-    for (msf_ctx* c : cs) launch_iface_mat_unpack(c);
+  for (msf_ctx* c : cs) {
+    launch_galerkin_cells(c);
+    launch_nd_factor_local(c);
   }
-  for (msf_ctx* c : cs) launch_assemble_top(c);
+  const size_t nt = (size_t)c0->nd.top_F, ft = (size_t)c0->nd.F_total;
+  if (nt)
+    for (int r = 0; r < c0->d.R; ++r)
+      if ((rc = dist_allreduce(cs, &msf_ctx::nd_F, r * ft, nt))) return rc;
+  for (msf_ctx* c : cs) launch_nd_factor_top(c);
   for (msf_ctx* c : cs) {
     int rc2 = msf_cuda_check(c, cudaGetLastError(), "dist assemble_coarse");
     if (rc2) return rc2;
@@ -1196,28 +831,11 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
   enqueue_vcycle(c, 0, nr, c->r, c->z, true, 1);
   launch_pcg_p(c, 0, nr, true);
   CKL("pcg init");
-  if (c->persistent) {
-    // all iterations in one cooperative launch (msf_persist.cu), no host round trips
-    int rc = launch_pcg_persistent(c, nr);
-    if (rc) return rc;
-    if (c->prof_d) {
-      std::vector<unsigned long long> pr(32 * 64);
-      CK(cudaMemcpy(pr.data(), c->prof_d, pr.size() * 8, cudaMemcpyDeviceToHost));
-      for (int it = 1; it < 4; ++it) {
-        std::fprintf(stderr, "persistent PCG iteration %d phase ends (us since start):", it);
-        const unsigned long long t0 = pr[it * 64 + 63];
-        for (int ph = 0; ph < 40 && pr[it * 64 + ph] > t0; ++ph)
-          std::fprintf(stderr, " %.1f", (pr[it * 64 + ph] - t0) * 1e-3);
-        std::fprintf(stderr, "\n");
-      }
-    }
-  } else {
-    int rc = run_graph_iterations(c, nr, max_it);
-    if (rc) return rc;
-  }
+  int rc = run_graph_iterations(c, nr, max_it);
+  if (rc) return rc;
   launch_compliance(c, nr);
   CKL("compliance");
-  int rc = read_scalars(c, nr);
+  rc = read_scalars(c, nr);
   if (rc) return rc;
   int noconv = 0;
   for (int k = 0; k < nr; ++k) {
@@ -1233,9 +851,9 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
   return MSF_OK;
 }
 
-// Graph of graph_iters PCG iterations for the realisations [rhs0, rhs0 + nr), captured on
-// first use on a private stream (the caller's may be the legacy stream, which cannot be
-// captured) and launched on the caller's stream.
+// Graph of one PCG iteration for the realisations [rhs0, rhs0 + nr), captured on first use
+// on a private stream (the caller's may be the legacy stream, which cannot be captured) and
+// launched on the caller's stream.
 static int range_graph(msf_ctx* c, int rhs0, int nr, cudaGraphExec_t* out) {
   cudaGraphExec_t& slot = c->range_graph[rhs0][nr];
   if (!slot) {
@@ -1244,9 +862,8 @@ static int range_graph(msf_ctx* c, int rhs0, int nr, cudaGraphExec_t* out) {
     c->stream = c->cap_stream;
     cudaError_t e1 = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
     const long long before = c->launches;
-    if (e1 == cudaSuccess)
-      for (int j = 0; j < c->graph_iters; ++j) enqueue_iteration(c, rhs0, nr);
-    c->pcg_launches = (c->launches - before) / c->graph_iters;
+    if (e1 == cudaSuccess) enqueue_iteration(c, rhs0, nr);
+    c->pcg_launches = c->launches - before;
     c->launches = before;
     cudaError_t e2 = e1 == cudaSuccess ? cudaStreamEndCapture(c->stream, &g) : e1;
     c->stream = user;
@@ -1260,34 +877,19 @@ static int range_graph(msf_ctx* c, int rhs0, int nr, cudaGraphExec_t* out) {
 }
 
 // PCG iterations as CUDA-graph launches of one captured iteration; the host polls the
-// device-side `active` flags every 8 iterations (converged realisations are no-ops).
+// device-side `active` flags every 8 iterations (converged realisations are no-ops).  Active
+// realisations are a contiguous range most of the time (the eroded realisation converges
+// last); each poll narrows [lo, hi) and switches to that range's graph.
 static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
-  if (c->stream_iters) {
-    // kernels launched directly on the stream (programmatic dependent launches chain them)
-    const int check_every = 8;
-    int done = 0;
-    for (int it = 0; it < max_it + check_every && !done; it += check_every) {
-      for (int j = 0; j < check_every; ++j) enqueue_iteration(c, 0, nr);
-      CKL("pcg iterations");
-      int rc = read_scalars(c, nr);
-      if (rc) return rc;
-      done = 1;
-      for (int k = 0; k < nr; ++k)
-        if (c->sc_host[k].active) done = 0;
-    }
-    return MSF_OK;
-  }
-  // active realisations are a contiguous range most of the time (the eroded realisation
-  // converges last); each poll narrows [lo, hi) and switches to that range's graph
   int lo = 0, hi = nr;
-  const int check_every = std::max(8, c->graph_iters);
+  const int check_every = 8;
   for (int it = 0; it < max_it + check_every; it += check_every) {
     cudaGraphExec_t g = nullptr;
     int rc = range_graph(c, lo, hi - lo, &g);
     if (rc) return rc;
-    for (int j = 0; j < check_every; j += c->graph_iters) {
+    for (int j = 0; j < check_every; ++j) {
       CK(cudaGraphLaunch(g, c->stream));
-      c->launches += c->pcg_launches * c->graph_iters;
+      c->launches += c->pcg_launches;
     }
     rc = read_scalars(c, nr);
     if (rc) return rc;
@@ -1355,24 +957,20 @@ int msf_group_coarse_solve(msf_group* g, int rhs, const double* b, double* x) {
   if (rhs < 0 || rhs >= c0->d.R) return msf_fail(c0, MSF_ERR_ARG, "rhs out of range");
   const size_t m = c0->d.mc, n = (size_t)c0->d.nbc * m;
   int rc;
-  // rank r holds b of blocks [C0, C1) (the last rank also ncx): its chain's right end block
-  // starts at 0, as the restriction leaves it with only this rank's share
+  // rank r holds b of its chain columns [C0, C1] except the right interface column (shared
+  // with the next rank, which holds it): the interface partial sums add up to b
   for (msf_ctx* c : cs) {
     double* cb = c->cb + rhs * n;
     CK(cudaMemcpyAsync(cb + c->cr_lo * m, b + c->cr_lo * m, (c->cr_hi - c->cr_lo + 1) * m * 8,
                        cudaMemcpyDeviceToDevice, c->stream));
     if (c->rank < c->nranks - 1) CK(cudaMemsetAsync(cb + c->cr_hi * m, 0, m * 8, c->stream));
-    launch_coarse_forward_local(c, rhs, 1, false);
+    launch_nd_solve_local_fwd(c, rhs, 1, false);
   }
-  if (!c0->iface.empty()) {
-    const size_t ni = c0->iface.size() * m;
-    for (msf_ctx* c : cs) launch_iface_vec_pack(c, rhs, 1);
-    if ((rc = dist_allreduce(cs, &msf_ctx::iface_vec, rhs * ni, ni))) return rc;
-    for (msf_ctx* c : cs) launch_iface_vec_unpack(c, rhs, 1);
-  }
+  const size_t nv = (size_t)c0->nd.vtop_total;
+  if (nv && (rc = dist_allreduce(cs, &msf_ctx::nd_vtop, rhs * nv, nv))) return rc;
   for (msf_ctx* c : cs) {
-    launch_coarse_top(c, rhs, 1, false);
-    launch_coarse_back_local(c, rhs, 1, false);
+    launch_nd_solve_top(c, rhs, 1, false);
+    launch_nd_solve_local_back(c, rhs, 1, false);
     const int hi = c->rank == c->nranks - 1 ? c->cr_hi + 1 : c->cr_hi;
     CK(cudaMemcpyAsync(x + c->cr_lo * m, c->cx + rhs * n + c->cr_lo * m, (hi - c->cr_lo) * m * 8,
                        cudaMemcpyDeviceToDevice, c->stream));
@@ -1528,7 +1126,7 @@ int msf_coarse_solve(msf_ctx* c, int rhs, const double* b, double* x) {
   if (c->nranks > 1) return msf_fail(c, MSF_ERR_STATE, "coarse_solve: K_c is distributed on a strip partition");
   const size_t n = (size_t)c->d.nbc * c->d.mc;
   CK(cudaMemcpyAsync(c->cb + rhs * n, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
-  launch_coarse_solve(c, rhs, 1, false);
+  launch_nd_solve(c, rhs, 1, false);
   CK(cudaMemcpyAsync(x, c->cx + rhs * n, n * 8, cudaMemcpyDeviceToDevice, c->stream));
   CKL("coarse_solve");
   int rc = read_scalars(c, 1);
@@ -1565,29 +1163,19 @@ int msf_get_coarse_blocks(msf_ctx* c, int rhs, double* D_host, double* U_host) {
   if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
   if (c->nranks > 1) return msf_fail(c, MSF_ERR_STATE, "get_coarse_blocks: K_c is distributed on a strip partition");
   const size_t n = (size_t)c->d.nbc * c->d.mc * c->d.mc;
-  if (c->use_nd) {
-    // K_c is never stored as blocks on the nested-dissection path: gather a copy from the
-    // cell products (diagnostic read-out only)
-    double* DU = nullptr;
-    CK(cudaMalloc(&DU, 2 * (size_t)c->d.R * n * 8));
-    launch_coarse_gather(c, DU, DU + (size_t)c->d.R * n, c->d.nbc);
-    cudaError_t e = cudaSuccess;
-    if (D_host) e = cudaMemcpyAsync(D_host, DU + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream);
-    if (e == cudaSuccess && U_host)
-      e = cudaMemcpyAsync(U_host, DU + (size_t)c->d.R * n + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    cudaFree(DU);
-    CK(e);
-    CKL("get_coarse_blocks");
-    return MSF_OK;
-  }
-  // Dc/Uc are overwritten by the factorisation: re-gather, copy out, re-factorise.
-  launch_coarse_galerkin(c);
-  if (D_host) CK(cudaMemcpyAsync(D_host, c->Dc + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream));
-  if (U_host) CK(cudaMemcpyAsync(U_host, c->Uc + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream));
-  launch_assemble_coarse(c);
+  // K_c is never stored as blocks: gather a block-tridiagonal copy from the cell products
+  // (diagnostic read-out only)
+  double* DU = nullptr;
+  CK(cudaMalloc(&DU, 2 * (size_t)c->d.R * n * 8));
+  launch_coarse_gather(c, DU, DU + (size_t)c->d.R * n, c->d.nbc);
+  cudaError_t e = cudaSuccess;
+  if (D_host) e = cudaMemcpyAsync(D_host, DU + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess && U_host)
+    e = cudaMemcpyAsync(U_host, DU + (size_t)c->d.R * n + rhs * n, n * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(DU);
+  CK(e);
   CKL("get_coarse_blocks");
-  CK(cudaStreamSynchronize(c->stream));
   return MSF_OK;
 }
 
@@ -1634,39 +1222,27 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   bytes[0] = R * (nn * 16 + ne * 8 + nn * 16) + nn;                  // p, E -> q
   bytes[1] = 7 * (R * (ne * 8 + nn * 16 + nn / 4 * 16 * 2) + nn / 4);  // 7 colour launches
   bytes[2] = R * nn * 16 + (double)c->n_cls * d.kmax * d.box_nodes * 16 + R * (double)d.n_agg * d.kmax * 8;
-  {
-    double cr = 0.0;
-    for (const CrLevel& L : c->cr) {
-      const double mm = (double)d.mc * d.mc * 8;
-      cr += L.surv.size() * 2 * mm + L.elim.size() * 3 * mm;   // forward Q,P ; back Dinv,P,Q
-    }
-    bytes[3] = c->use_nd ? R * (double)c->nd.solve_bytes : R * cr;
-  }
+  bytes[3] = R * (double)c->nd.solve_bytes;                          // fronts, forward + back
   bytes[4] = R * (nn * 32) + (double)c->n_cls * d.kmax * d.box_nodes * 16 + R * (double)d.n_agg * d.kmax * 8;
   bytes[5] = R * (nn * 16 * 3 + ne * 8) + nn;                        // z, r, E -> t
   bytes[6] = 2 * bytes[1] + bytes[2] + bytes[3] + bytes[4] + bytes[5];
   bytes[7] = bytes[0] + bytes[6] + R * nn * 16 * 6 + R * nn * 16 * 2 + R * nn * 16 * 3;
   bytes[8] = R * (nn * 16 * 6 + ne * 8 + nn / 4 * 16 * 2) + nn / 4;    // p q u r -> u r, F0
   bytes[9] = R * nn * 16 * 3;                                          // z, p -> p
-  // coarse phases of this rank: chain levels (forward Q, P; back Dinv, P^T, Q^T), interface
-  // levels + top; assembly entries carry no byte count
+  // coarse phases: this rank's box fronts (forward / back), the interface fronts; assembly
+  // entries carry no byte count
   {
-    const double mm = (double)d.mc * d.mc * 8;
-    double fwd = 0.0, back = 0.0, top = 0.0;
-    for (size_t l = 0; l < c->cr.size(); ++l) {
-      const CrLevel& L = c->cr[l];
-      if ((int)l < c->n_local) {
-        fwd += L.surv.size() * 2 * mm;
-        back += L.elim.size() * 3 * mm;
-      } else {
-        top += L.surv.size() * 2 * mm + L.elim.size() * 3 * mm;
-      }
+    double fl = 0.0, tp = 0.0;
+    const int k = d.kmax;
+    for (const NdFront& F : c->nd.fr) {
+      const double s = (double)F.s_n * k, nf = (double)(F.s_n + F.b_n) * k;
+      if (F.flags & 1) tp += 8 * ((nf - s) * s + s * nf);
+      else fl += 8 * (nf - s) * s;
     }
-    top += (double)c->top_T * c->top_T * mm;
     bytes[10] = bytes[11] = 0.0;
-    bytes[12] = R * fwd;
-    bytes[13] = R * top;
-    bytes[14] = R * back;
+    bytes[12] = R * fl;
+    bytes[13] = R * tp;
+    bytes[14] = R * ((double)c->nd.solve_bytes - fl - tp);
   }
   // keep every realisation active during the timing, restore afterwards
   std::vector<PcgScalars> saved(R);
@@ -1694,24 +1270,22 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
       case 0: launch_matvec(c, 0, R, c->pv, c->q, false, true); break;
       case 1: launch_sgs(c, 0, R, c->r, c->z, false); break;
       case 2: launch_restrict(c, 0, R, c->t, false); break;
-      case 3: launch_coarse_solve(c, 0, R, false); break;
+      case 3: launch_nd_solve(c, 0, R, false); break;
       case 4: launch_prolong(c, 0, R, c->z, false); break;
       case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
       case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
       case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
       case 8: launch_update_f0(c, 0, R); break;
       case 9: launch_pcg_p(c, 0, R, false); break;
-      case 10:   // whole K_c assembly + factorisation (nested dissection) / chain part (strips)
-        if (c->use_nd) launch_assemble_coarse(c);
-        else launch_assemble_local(c);
+      case 10:   // K_c assembly: Galerkin cell products + the factorisation (a strip: its part)
+        launch_galerkin_cells(c);
+        launch_nd_factor_local(c);
+        if (!c->comm) launch_nd_factor_top(c);
         break;
-      case 11:   // a strip re-reads the all-reduced interface blocks before the top part
-        if (!c->iface.empty()) launch_iface_mat_unpack(c);
-        launch_assemble_top(c);
-        break;
-      case 12: launch_coarse_forward_local(c, 0, R, false); break;
-      case 13: launch_coarse_top(c, 0, R, false); break;
-      case 14: launch_coarse_back_local(c, 0, R, false); break;
+      case 11: launch_galerkin_cells(c); break;
+      case 12: launch_nd_solve_local_fwd(c, 0, R, false); break;
+      case 13: launch_nd_solve_top(c, 0, R, false); break;
+      case 14: launch_nd_solve_local_back(c, 0, R, false); break;
     }
   };
   auto timeit = [&](int which) -> double {
@@ -1726,8 +1300,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   };
   const int ntimed = c->comm ? 6 : 8;
   for (int i = 0; i < MSF_BENCH_ENTRIES; ++i)
-    ms[i] = ((i < ntimed || i >= 8) && !(c->use_nd && i > 10)) ? timeit(i) : -1.0;
-  if (ms[7] > 0) ms[7] /= c->graph_iters;   // the graph holds graph_iters iterations
+    ms[i] = (i < ntimed || i >= 8) ? timeit(i) : -1.0;
   if (!gR) ms[7] = -1.0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

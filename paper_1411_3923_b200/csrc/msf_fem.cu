@@ -549,108 +549,6 @@ __global__ void __launch_bounds__(NTHR) k_sgs_colour(Dims d, K0Mat K, const doub
   }
 }
 
-// One Gauss-Seidel sweep (phases ph_first..7 of launch_sgs_phase's numbering: 1 F0, 2 F1,
-// 3 F2, 4 F3B3, 5 B2, 6 B1, 7 B0) as ONE launch.  Every CTA owns the same 64 x 16-node tile
-// as a k_sgs_colour CTA and runs the phases in order; instead of a kernel boundary (or a
-// grid-wide barrier) between phases, a CTA waits only for the <= 8 tiles around it to
-// finish the previous phase.  That is exactly the colour-phase dependency of reading R7: a
-// quad reads z of the nodes at distance 1, which lie in its own or a neighbouring tile, and
-// a tile may not overwrite nodes its neighbours still read in the previous phase.  Per-tile
-// progress counters (flags[rhs][tile]) increase monotonically across launches; all tiles
-// hold the same value at kernel entry, so the entry value is the phase-0 epoch.  All CTAs
-// must be co-resident (the host launches it cooperatively, only when they fit); each wait
-// is bounded and sets *err instead of hanging.  The arithmetic per node is sgs_quad's, so
-// the result is bitwise that of the 6-7 colour launches.
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-template <bool RZ>
-__global__ void __launch_bounds__(NTHR, 4) k_sgs_sweep_nb(Dims d, K0Mat K, const double* __restrict__ Eall,
-                                                       const double2* __restrict__ rall,
-                                                       double2* zall,
-                                                       const uint8_t* __restrict__ fixn,
-                                                       PcgScalars* sc, double* partials,
-                                                       unsigned* counters, int max_partials,
-                                                       int rhs0, int gated, int ph_first,
-                                                       int rz_mode, double* dsum,
-                                                       unsigned* flags, int* err) {
-  pdl_wait();
-  const int rhs = rhs0 + blockIdx.z;
-  if (gated && !sc[rhs].active) {
-    pdl_launch();
-    return;
-  }
-  __shared__ double red[NTHR / 32 + 1];
-  __shared__ unsigned s_base;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  const int ntile = gridDim.x * gridDim.y;
-  unsigned* fl = flags + (size_t)rhs * ntile;
-  const int me = blockIdx.y * gridDim.x + blockIdx.x;
-  if (tid == 0) s_base = ld_acquire_u32(fl + me);
-  __syncthreads();
-  const unsigned base = s_base;
-  const int qx = blockIdx.y * blockDim.y + threadIdx.y;
-  const int qy = blockIdx.x * blockDim.x + threadIdx.x;
-  const double* E = Eall + (size_t)rhs * d.estride;
-  const double2* r = rall + (size_t)rhs * d.nn;
-  double2* z = zall + (size_t)rhs * d.nn;
-  double dot = 0.0;
-  for (int ph = ph_first; ph <= 7; ++ph) {
-    if (ph > ph_first) {
-      if (tid < 9 && tid != 4) {
-        const int nx = (int)blockIdx.x + tid % 3 - 1, ny = (int)blockIdx.y + tid / 3 - 1;
-        if (nx >= 0 && nx < (int)gridDim.x && ny >= 0 && ny < (int)gridDim.y) {
-          const unsigned target = base + (unsigned)(ph - ph_first);
-          const unsigned* f = fl + ny * gridDim.x + nx;
-          for (long long spin = 0; (int)(ld_acquire_u32(f) - target) < 0; ++spin)
-            if (spin > (1ll << 24)) {
-              atomicExch(err, 1);
-              break;
-            }
-        }
-      }
-      __syncthreads();   // the acquire loads above order this CTA's later z loads
-    }
-    switch (ph) {
-      case 1: sgs_quad<true, false, false, false>(d, K, E, r, z, fixn, qx, qy, 0); break;
-      case 2: sgs_quad<true, false, false, false>(d, K, E, r, z, fixn, qx, qy, 1); break;
-      case 3: sgs_quad<true, false, false, false>(d, K, E, r, z, fixn, qx, qy, 2); break;
-      case 4: sgs_quad<true, true, false, false>(d, K, E, r, z, fixn, qx, qy, 3); break;
-      case 5: sgs_quad<false, true, false, false>(d, K, E, r, z, fixn, qx, qy, 2); break;
-      case 6: sgs_quad<false, true, false, false>(d, K, E, r, z, fixn, qx, qy, 1); break;
-      default:
-        if (RZ)
-          dot = sgs_quad<false, true, false, true>(d, K, E, r, z, fixn, qx, qy, 0);
-        else
-          sgs_quad<false, true, false, false>(d, K, E, r, z, fixn, qx, qy, 0);
-    }
-    if (ph < 7) {
-      __syncthreads();
-      if (tid == 0) st_release_u32(fl + me, base + (unsigned)(ph - ph_first + 1));
-    }
-  }
-  // the last phase needs no wait by anyone in this launch; entry epoch of the next launch
-  if (tid == 0) fl[me] = base + (unsigned)(7 - ph_first + 1);
-  pdl_launch();
-  if (RZ) {
-    const double sblk = block_sum_all(dot, red, tid, NTHR);
-    if (arrive_last(sblk, partials + (size_t)rhs * max_partials, me, counters + rhs * 8, ntile,
-                    tid)) {
-      const double tot = reduce_partials(partials + (size_t)rhs * max_partials, ntile, red, tid,
-                                         NTHR);
-      if (tid == 0) {
-        fin_or_park(sc, dsum, rhs, FIN_RZ, tot, rz_mode);
-        counters[rhs * 8] = 0;
-      }
-    }
-  }
-}
 
 // ------------------------------------------------------------------ PCG vector kernels
 constexpr int VB = 256;  // threads per block of the vector kernels
@@ -1070,66 +968,8 @@ void launch_sgs_phase(msf_ctx* c, int rhs0, int nr, const double* r, double* z, 
 
 // One symmetric GS sweep as 7 colour launches F0 F1 F2 F3B3 B2 B1 B0.  zero_start: z = 0 on
 // entry (fused into F0); rz_mode != 0: r.z and beta fused into B0.
-// the whole sweep as one neighbour-synchronised launch (k_sgs_sweep_nb) when its CTAs fit
-// on the GPU at once; returns false when the caller must launch the colour phases instead
-static bool launch_sgs_sweep_nb(msf_ctx* c, int rhs0, int nr, const double* r, double* z,
-                                bool gated, int ph_first, int rz_mode) {
-  if (!c->sgs_nb || !c->sgs_nb_flags) return false;
-  const Dims& d = c->dl;
-  const int hx = (d.nnx + 1) / 2, hy = (d.nny + 1) / 2;
-  dim3 blk(32, 8);
-  dim3 grd((hy + 31) / 32, (hx + 7) / 8, nr);
-  if ((long long)grd.x * grd.y * nr > c->sgs_nb_max_ctas) return false;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grd;
-  cfg.blockDim = blk;
-  cfg.stream = c->stream;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = g_msf_pdl ? 2 : 1;
-  const int g = gated ? 1 : 0;
-  cudaError_t e;
-  if (rz_mode)
-    e = cudaLaunchKernelEx(&cfg, k_sgs_sweep_nb<true>, d, c->K0, (const double*)c->E_loc,
-                           (const double2*)r, (double2*)z, (const uint8_t*)c->fixn, c->sc,
-                           c->partials, c->counters, c->max_partials, rhs0, g, ph_first, rz_mode,
-                           c->dsum, c->sgs_nb_flags, c->sgs_nb_err);
-  else
-    e = cudaLaunchKernelEx(&cfg, k_sgs_sweep_nb<false>, d, c->K0, (const double*)c->E_loc,
-                           (const double2*)r, (double2*)z, (const uint8_t*)c->fixn, c->sc,
-                           c->partials, c->counters, c->max_partials, rhs0, g, ph_first, rz_mode,
-                           c->dsum, c->sgs_nb_flags, c->sgs_nb_err);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    std::fprintf(stderr, "msfem: single-launch sweep rejected (%s); colour launches\n",
-                 cudaGetErrorString(e));
-    c->sgs_nb = false;
-    return false;
-  }
-  MSF_LAUNCHED(c);
-  return true;
-}
-
-int sgs_nb_max_ctas(msf_ctx* c) {
-  int per = 0, sms = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sgs_sweep_nb<true>, NTHR, 0) != cudaSuccess)
-    return 0;
-  int per2 = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_sgs_sweep_nb<false>, NTHR, 0) != cudaSuccess)
-    return 0;
-  return std::min(per, per2) * sms;
-}
-
 void launch_sgs_sweep(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
                       bool zero_start, int rz_mode, bool skip_f0) {
-  if (!zero_start && launch_sgs_sweep_nb(c, rhs0, nr, r, z, gated, skip_f0 ? 2 : 1, rz_mode))
-    return;
   if (zero_start)
     launch_sgs_phase(c, rhs0, nr, r, z, gated, 0, 0);
   else if (!skip_f0)

@@ -65,39 +65,6 @@ struct EigClass {
   int nkept;        // kept modes (written by the kernel)
 };
 
-// One level of the coarse block cyclic reduction over an ordered list of active blocks:
-// the blocks at odd list positions are eliminated (the block tridiagonal structure is kept
-// on the survivors).  On one GPU the list is every block and level l is the stride-2^l
-// reduction; the strip partition reduces each rank's chain and then the interface chain
-// (DESIGN.md §8(e)).  Pointer tables (device) cover all realisations; job lists (device)
-// are per realisation.
-struct CrLevel {
-  int s = 0;                   // stride 2^l of a stride level (persistent kernels); -1 otherwise
-  std::vector<int> elim;       // eliminated blocks (host copy)
-  std::vector<int> el_l, el_r; // their surviving left / right neighbours (-1: none)
-  std::vector<int> surv;       // survivors with an eliminated neighbour (host copy)
-  std::vector<int> sv_l, sv_r; // their eliminated left / right neighbours (-1: none)
-  int* elim_d = nullptr;       // [elim][3] = k, left, right
-  int* surv_d = nullptr;       // [surv][3] = i, left, right
-  int n_inv = 0;  double** inv = nullptr;  double** invsrc = nullptr;
-  int nP = 0;     double** pA = nullptr;   double** pB = nullptr;  double** pC = nullptr;
-  int nQ = 0;     double** qA = nullptr;   double** qB = nullptr;  double** qC = nullptr;
-  int nDl = 0;    double** dlA = nullptr;  double** dlB = nullptr; double** dlC = nullptr;
-  int nDr = 0;    double** drA = nullptr;  double** drB = nullptr; double** drC = nullptr;
-  int nU = 0;     double** uA = nullptr;   double** uB = nullptr;  double** uC = nullptr;
-};
-
-// One block Gauss-Jordan step (pivot block k) of the dense inverse of the top system left
-// after the truncated cyclic reduction.  Pointer tables (device) cover all realisations.
-struct TopStep {
-  int nI = 0;  double** invsrc = nullptr; double** inv = nullptr;           // Pk = inv(A_kk)
-  int nW = 0;  double** wA = nullptr; double** wB = nullptr; double** wC = nullptr;  // W_i = A_ik Pk
-  int nU = 0;  double** uA = nullptr; double** uB = nullptr; double** uC = nullptr;  // A_ij -= W_i A_kj
-  int nC = 0;  double** cps = nullptr; double** cpd = nullptr;                        // A_ik = W_i
-               double** tpd = nullptr;                                             // A_ki = W_i^T
-  double** ngs = nullptr; double** ngd = nullptr;                                  // A_kk = -Pk
-};
-
 // Nested-dissection coarse solve (msf_nd.cu): one front per box of the recursive dissection
 // of the coarse node grid.  S = the box's separator (or all nodes of a leaf box), B = the
 // ring of nodes around the box; the front matrix F (n_f x n_f, n_f = (s_n + b_n) kmax,
@@ -106,30 +73,37 @@ struct TopStep {
 struct NdFront {
   int s_n, b_n;       // nodes of S / B
   int node_off;       // nodes[node_off ..]: s_n S nodes then b_n B nodes (global coarse node ids)
-  int ch0, ch1;       // children fronts (-1: none)
+  int ch0, ch1;       // children fronts (-1: none on this rank)
   int chmap_off;      // chmap[chmap_off + 2 j + q]: index of front node j in child q's B list (-1)
-  int level;          // height in the dissection tree (leaves 0)
+  int level;          // height among fronts of its kind (box / interface), leaves 0
   int vmap_off;       // vmap[vmap_off + j] (int4) for the n_f front variables
-  long long F_off;    // doubles, per realisation
+  int flags;          // bit 0: interface front (replicated); bits 1, 2: child 0 / 1 is one
+  int vtop_off;       // interface fronts: offset of its variables in vtop (-1: box front)
+  long long F_off;    // doubles, per realisation (n_f rows, even leading dimension)
   long long u_off;    // doubles (b_n kmax update vector), per realisation
 };
 
 struct NdPlan {
   struct List {       // task list in `lists`: fronts[n] then prefix sums of per-front counts
     int off = 0, n = 0, total = 0, total2 = 0, total3 = 0;
-    int RW = 1, RB = 8;   // solve lists: rows per warp pass, rows per CTA
+    int RB = 8;       // solve lists: rows per CTA
+  };
+  struct Levels {     // a group of levels (this rank's box / the interface tree)
+    std::vector<List> asmb, fwd, back;        // per level: assembly tiles, solve row blocks
+    std::vector<std::vector<List>> panel;     // per level, per 64-pivot panel
+    std::vector<int> fwd_smem, back_smem;     // per level: solve launch shared memory
   };
   std::vector<NdFront> fr;
-  std::vector<int> nodes, chmap, lists, vmap;
-  int root = -1, H = 0;
+  std::vector<int> nodes, chmap, lists, vmap, packmap;
+  int root = -1, H = 0, TH = 0, n_top = 0;
   bool ok = true;
   long long F_total = 0, u_total = 0, scr_doubles = 0;
+  long long top_F = 0;         // doubles of the interface fronts (start of each realisation)
+  long long vtop_total = 0;    // interface fronts' right-hand-side entries per realisation
   int max_act = 0, max_nf = 0;
-  std::vector<List> asmb, fwd, back;          // per level: assembly tiles, solve row blocks
-  std::vector<std::vector<List>> panel;       // per level, per 64-pivot panel
-  std::vector<int> lev_smax, lev_nfmax;       // per level: max s and n_f
-  std::vector<int> lev_fwd_smem, lev_back_smem;  // per level: solve launch shared memory
-  long long solve_bytes = 0;                  // matrix bytes streamed per solve and realisation
+  Levels loc, top;
+  List tpart;                  // interface fronts: the rank's partial assembly (mode 1)
+  long long solve_bytes = 0;   // matrix bytes streamed per solve and realisation
 };
 
 // Device-side dot products awaiting the cross-rank all-reduce (strip partition): kernels
@@ -187,9 +161,7 @@ struct msf_ctx {
   int n_cls = 0;
   int mb = 0;  // eigensolver block size
   long long eig_work_doubles = 0;
-  std::vector<CrLevel> cr;
-  // nested-dissection coarse solve (single GPU; msf_nd.cu)
-  bool use_nd = false;
+  // nested-dissection coarse solve (msf_nd.cu)
   NdPlan nd;
   double* nd_F = nullptr;       // [R][F_total] fronts
   double* nd_u = nullptr;       // [R][u_total] update vectors of the forward sweep
@@ -201,16 +173,12 @@ struct msf_ctx {
   int* nd_chmap = nullptr;
   int* nd_lists = nullptr;
   int* nd_vmap = nullptr;       // int4 per front variable
-  // Coarse solve on a strip partition: levels [0, n_local) reduce this
-  // rank's chain of blocks [cr_lo, cr_hi] (the chain's end blocks, shared with the neighbour
-  // ranks, are kept); after an all-reduce of the end blocks, levels [n_local, cr.size())
-  // and the top system reduce the chain of the nranks + 1 interface blocks, replicated on
-  // every rank.  One GPU: n_local = cr.size(), one chain of all blocks.
-  int n_local = 0;
+  int* nd_pack = nullptr;       // int2 per interface-front variable (strip partition)
+  double* nd_vtop = nullptr;    // [R][vtop_total] interface fronts' right-hand sides
+  // strip partition: the agglomerate columns [cr_lo, cr_hi] this rank restricts onto (its
+  // coarse cells' corners; the two ends are interface columns shared with the neighbours)
   int cr_lo = 0, cr_hi = 0;       // chain blocks
   int cell_lo = 0, cell_hi = 0;   // Galerkin coarse cell columns [cell_lo, cell_hi)
-  int id_lo = 0, id_hi = 0;       // blocks [id_lo, id_hi] carry the identity rows of unused slots
-  std::vector<int> iface;         // interface blocks (global index), nranks + 1 (strips only)
   std::vector<int> filt_dx, filt_dy;
   std::vector<double> filt_w;
   bool periodic = false;
@@ -248,27 +216,11 @@ struct msf_ctx {
   double* eig_work = nullptr;
 
   double* Kcell = nullptr;      // [R][ncells][(4k)^2]
-  // K_c factor blocks are stored per realisation in nslot slots: every block on one GPU
-  // (slot = block), the chain [cr_lo, cr_hi] then the other interface blocks on a strip
-  int nslot = 0;
-  std::vector<int> slot_h;      // [nbc] slot of each block, -1: not stored on this rank
-  int* slot_d = nullptr;
-  double* Dc = nullptr;         // [R][nslot][mc*mc]
-  double* Uc = nullptr;         // [R][nbc][mc*mc]
-  double* Dinv = nullptr;       // [R][nbc][mc*mc]
-  double* Pc = nullptr;         // [R][nbc][mc*mc]
-  double* Qc = nullptr;         // [R][nbc][mc*mc]
-  double* PTc = nullptr;        // [R][nbc][mc*mc]  P_k^T (back substitution, row-major)
-  double* QTc = nullptr;        // [R][nbc][mc*mc]  Q_k^T
-  double* cb = nullptr;         // [R][nbc*mc] coarse rhs (modified by the forward sweep)
+  double* cb = nullptr;         // [R][nbc*mc] coarse rhs
   double* cx = nullptr;         // [R][nbc*mc] coarse solution
-  int* iface_d = nullptr;       // [nI] interface blocks
-  double* iface_vec = nullptr;  // [R][nI][mc] this rank's share of the interface rhs (all-reduced)
-  double* iface_mat = nullptr;  // [R][2nI-1][mc*mc] interface D blocks, then U (all-reduced)
-  double** ifm_pack = nullptr;  // [2][3R] src, dst: this rank's interface D, D, U shares
-  double** ifm_unpack = nullptr;// [2][(2nI-1)R] src, dst
   int* agg_by_cls_d = nullptr;  // restriction work list (agglomerates in grid order)
   bool restrict_warp = true;    // restriction one warp per agglomerate (env MSF_RESTRICT_WARP=0)
+  bool restrict_warp_force = false;   // ... on every launch (env MSF_RESTRICT_WARP=force; tests)
   // restriction one warp per group of same-class agglomerates (k_restrict_batch; env
   // MSF_RESTRICT_BATCH=0: off); n_rgroups = 0 when not used
   int n_rgroups = 0, rgroup_B = 0;
@@ -277,38 +229,7 @@ struct msf_ctx {
                                      // env MSF_PROLONG_NR=0: one launch-z per realisation)        // env MSF_RESTRICT_BATCH=force: grouped kernel on every launch
   int* rgroups_d = nullptr;
   std::vector<int> agg_by_cls_h;
-  // top system after the truncated cyclic reduction: T active blocks (stride top_stride),
-  // dense inverse stored block-major [R][T][T][mc*mc] as -Top^{-1}
-  std::vector<int> top_blocks;
-  int top_T = 0;
-  int* top_blocks_d = nullptr;
-  double* Atop = nullptr;       // [R][T*T][mc*mc]
-  double* top_Pk = nullptr;     // [R][mc*mc] scratch
-  double* top_W = nullptr;      // [R][T][mc*mc] scratch
-  std::vector<TopStep> top_steps;
-  char* top_jobs_d = nullptr;
-  void* cr_levels_d = nullptr;  // CrLevelDev[n levels] for the persistent PCG kernel
-  bool persistent = true;       // PCG driver: persistent cooperative kernel (else CUDA graph)
-  int graph_iters = 1;          // PCG iterations per captured graph (env MSF_GRAPH_ITERS)
-  bool stream_iters = false;    // PCG iterations launched on the stream instead of a graph
-  bool coarse_coop = true;      // V-cycle coarse part as one cooperative launch (single GPU)
-  int coop_grid = 0;            // its grid size (0: not yet computed)
-  void* prof_d = nullptr;       // debug phase timeline of the persistent kernel (env MSF_PERSIST_PROFILE)
-  char* jobs_d = nullptr;       // CR job tables
-  int* factor_status = nullptr; // [R] nonzero on failed pivot
-  double* binv_P = nullptr;     // blocked inverse scratch: [n_max][64*64] pivot inverses
-  double* binv_R = nullptr;     //                          [n_max][64*m] row panels
-  double* binv_C = nullptr;     //                          [n_max][m*64] pivot column copies
-  double** binv_Rp = nullptr;   // [n_max] device pointers to the R / C panels (cuBLAS trailing
-  double** binv_Cp = nullptr;   // update; null when m < blocked_inv_min everywhere)
-  int blocked_inv_min = 256;
-  bool galerkin_gemm = true;    // Galerkin cell products as G^T G by cuBLAS (env MSF_GALERKIN_GEMM=0)
-  double* galerkin_G = nullptr; // scratch for G of a chunk of cells
-  size_t galerkin_G_doubles = 0;
-  void* cublas = nullptr;       // cublasHandle_t of the factorisation GEMMs (null: k_gemm;
-                                // env MSF_CUBLAS=0)
-  bool inv_blocked_smem = true; // m x m inverses below blocked_inv_min: blocked sweep in shared
-                                // memory (env MSF_INV_BLOCKED_SMEM=0: pivot-by-pivot sweep)
+  int* factor_status = nullptr; // [2 * MSF_MAX_RHS] nonzero on failed pivot
   int restrict_threads = 0;
   bool apply_direct = true;     // operator apply with direct (L1) neighbourhood loads
   bool apply_sw = true;         // ... as a sliding window along x (env MSF_APPLY_SW=0: per node)
@@ -345,14 +266,7 @@ struct msf_ctx {
   // one graph per contiguous active realisation range [rhs0, rhs0 + nr): converged
   // realisations drop out of the launch grids instead of exiting from every CTA
   cudaGraphExec_t range_graph[MSF_MAX_RHS][MSF_MAX_RHS + 1] = {};
-  // Gauss-Seidel sweep as one neighbour-synchronised launch (k_sgs_sweep_nb; opt-in, env
-  // MSF_SGS_NB=1), used when its grid fits on the GPU at once (sgs_nb_max_ctas)
-  bool sgs_nb = false;               // measured slower than the colour launches
-  unsigned* sgs_nb_flags = nullptr;  // [MSF_MAX_RHS][tiles] per-tile phase counters
-  int* sgs_nb_err = nullptr;         // set by a wait that timed out
-  int sgs_nb_max_ctas = 0;
 };
-int sgs_nb_max_ctas(msf_ctx* c);
 int restrict_groups(const Dims& d, const std::vector<int>& work, const std::vector<int>& cls,
                     int B, std::vector<int>& groups);
 
@@ -413,43 +327,25 @@ void launch_oc(msf_ctx* c, const double* x, const double* dF, const double* dg, 
 
 // ---------------------------------------------------------------- coarse space
 void launch_build_basis(msf_ctx* c);
-// K_c assembly + factorisation: one GPU all of it; a strip the local part (Galerkin of the
-// owned cells, chain levels), the interface pack / unpack around the all-reduce of
-// iface_mat, then the replicated interface levels + top system
+// K_c assembly (Galerkin cell products) + nested-dissection factorisation, one GPU
 void launch_assemble_coarse(msf_ctx* c);
-void launch_assemble_local(msf_ctx* c);
-void launch_iface_mat_pack(msf_ctx* c);
-void launch_iface_mat_unpack(msf_ctx* c);
-void launch_assemble_top(msf_ctx* c);
-void launch_coarse_galerkin(msf_ctx* c);
 void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated);
-// persistent cooperative PCG iterations (msf_persist.cu); returns MSF_OK or an error code
-int launch_pcg_persistent(msf_ctx* c, int nr);
-size_t cr_levels_dev_bytes(int nlev);
-void fill_cr_levels_dev(const std::vector<CrLevel>& cr, void* host_buf);
-constexpr int MSF_BENCH_ENTRIES = 15;   // msf_bench_kernels
-constexpr int MSF_TOP_MAX = 1200;   // max unknowns of the dense top system (T * mc)
-constexpr int MSF_PERSIST_PARTIALS = 3 * MSF_MAX_RHS * 4 * 160;  // 3 slots x 4 rhs x grid
 void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated);
-// c <- K_c^{-1} c: forward chain levels, [strip: interface pack, all-reduce of iface_vec,
-// unpack], interface levels + top + interface back, back chain levels
-void launch_coarse_solve(msf_ctx* c, int rhs0, int nr, bool gated);
-void launch_coarse_forward_local(msf_ctx* c, int rhs0, int nr, bool gated);
-void launch_iface_vec_pack(msf_ctx* c, int rhs0, int nr);
-void launch_iface_vec_unpack(msf_ctx* c, int rhs0, int nr);
-void launch_coarse_top(msf_ctx* c, int rhs0, int nr, bool gated);
-void launch_coarse_back_local(msf_ctx* c, int rhs0, int nr, bool gated);
-// restriction + coarse solve + prolongation in one cooperative launch (msf_persist.cu)
-int launch_coarse_coop(msf_ctx* c, int rhs0, int nr, const double* t, double* z, bool gated);
+constexpr int MSF_BENCH_ENTRIES = 15;   // msf_bench_kernels
 
 // nested dissection (msf_nd.cu)
-bool nd_build_plan(const Dims& d, NdPlan& P);
+bool nd_build_plan(const Dims& d, NdPlan& P, int rank, int nranks, const std::vector<int>& icol);
 size_t nd_workspace_bytes(const Dims& d, const NdPlan& P);
 cudaError_t nd_setup(msf_ctx* c, char*& cur);
 void launch_nd_factor(msf_ctx* c);
+void launch_nd_factor_local(msf_ctx* c);
+void launch_nd_factor_top(msf_ctx* c);
 void launch_nd_solve(msf_ctx* c, int rhs0, int nr, bool gated);
-// Galerkin cell products K_cell (and, gather = true, the block-tridiagonal D / U copies for
-// the cyclic reduction or a diagnostic read-out into D, U)
+void launch_nd_solve_local_fwd(msf_ctx* c, int rhs0, int nr, bool gated);
+void launch_nd_solve_top(msf_ctx* c, int rhs0, int nr, bool gated);
+void launch_nd_solve_local_back(msf_ctx* c, int rhs0, int nr, bool gated);
+// Galerkin cell products K_cell of this rank's cells; a block-tridiagonal copy D / U of K_c
+// gathered from them (diagnostic read-out)
 void launch_galerkin_cells(msf_ctx* c);
 void launch_coarse_gather(msf_ctx* c, double* D, double* U, int nslot);
 

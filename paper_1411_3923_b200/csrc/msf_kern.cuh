@@ -410,153 +410,4 @@ __device__ __forceinline__ void prolong_node(const Dims& d, const double* __rest
   }
 }
 
-// ------------------------------------------------------------------ cyclic reduction
-// Row-chunked GEMVs: a CTA owns CR_ROWS rows of one block, one warp per row, lanes over the
-// (row-major, coalesced) columns; the neighbour vectors are staged in shared memory.  Each
-// level is latency-bound (a few m x m blocks), so every warp loads the first CR_PF*32
-// columns of its row into registers BEFORE the staging barrier: the matrix and the vector
-// round trips to DRAM overlap and a level costs about one memory latency.
-constexpr int CR_ROWS = 8;    // == warps of the 256-thread CTAs that run these routines
-constexpr int CR_PF = 5;      // columns per lane held in registers per pass (160 per warp)
-
-// forward, survivor i, rows [r0, r0+CR_ROWS): b_i -= Q_il b_il + P_ir b_ir, il / ir its
-// eliminated left / right neighbours of the level (-1: none; stride levels: i -/+ s)
-// active: realisation flag checked after pdl_wait (nullptr: caller already checked)
-__device__ __forceinline__ void cr_forward_rows(const Dims& d, int i, int il, int ir, int r0,
-                                                const double* __restrict__ Q,
-                                                const double* __restrict__ P, double* cb,
-                                                double* sv, int tid, int nthreads,
-                                                const int* active = nullptr) {
-  const int m = d.mc;
-  const bool hl = il >= 0, hr = ir >= 0;
-  const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
-  const int r1 = min(m, r0 + CR_ROWS);
-  double qv[CR_PF], pv[CR_PF];
-  auto load = [&](int r, int c0) {
-    const double* Qr = Q + (size_t)r * m;
-    const double* Pr = P + (size_t)r * m;
-#pragma unroll
-    for (int j = 0; j < CR_PF; ++j) {
-      const int c = c0 + lane + 32 * j;
-      qv[j] = (hl && c < m) ? __ldg(Qr + c) : 0.0;
-      pv[j] = (hr && c < m) ? __ldg(Pr + c) : 0.0;
-    }
-  };
-  if (r0 + wid < r1) load(r0 + wid, 0);   // constant during PCG: before the PDL wait
-  pdl_wait();
-  if (active && !*active) return;
-  for (int k = tid; k < m; k += nthreads) {
-    sv[k] = hl ? cb[(size_t)il * m + k] : 0.0;
-    sv[m + k] = hr ? cb[(size_t)ir * m + k] : 0.0;
-  }
-  __syncthreads();
-  for (int r = r0 + wid; r < r1; r += nw) {
-    double a0 = 0.0, a1 = 0.0;
-    for (int c0 = 0; c0 < m; c0 += 32 * CR_PF) {
-      if (c0 > 0 || r != r0 + wid) load(r, c0);
-#pragma unroll
-      for (int j = 0; j < CR_PF; ++j) {
-        const int c = c0 + lane + 32 * j;
-        if (c < m) {
-          a0 = fma(qv[j], sv[c], a0);
-          a1 = fma(pv[j], sv[m + c], a1);
-        }
-      }
-    }
-    const double acc = warp_sum(a0 + a1);
-    if (lane == 0) cb[(size_t)i * m + r] -= acc;
-  }
-  __syncthreads();
-}
-
-// back, eliminated k, rows [r0, r0+CR_ROWS): x_k = Dinv_k b_k - P_k^T x_kl - Q_k^T x_kr
-// (kl / kr: its surviving neighbours, -1: none)
-__device__ __forceinline__ void cr_back_rows(const Dims& d, int k, int kl, int kr, int r0,
-                                             const double* __restrict__ Di,
-                                             const double* __restrict__ PT,
-                                             const double* __restrict__ QT,
-                                             const double* __restrict__ cb, double* cx,
-                                             double* sv, int tid, int nthreads,
-                                             const int* active = nullptr) {
-  const int m = d.mc;
-  const bool hl = kl >= 0, hr = kr >= 0;
-  const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
-  const int r1 = min(m, r0 + CR_ROWS);
-  double dv[CR_PF], pv[CR_PF], qv[CR_PF];
-  auto load = [&](int r, int c0) {
-    const double* Dr = Di + (size_t)r * m;
-    const double* Pr = PT + (size_t)r * m;
-    const double* Qr = QT + (size_t)r * m;
-#pragma unroll
-    for (int j = 0; j < CR_PF; ++j) {
-      const int c = c0 + lane + 32 * j;
-      dv[j] = (c < m) ? __ldg(Dr + c) : 0.0;
-      pv[j] = (hl && c < m) ? __ldg(Pr + c) : 0.0;
-      qv[j] = (hr && c < m) ? __ldg(Qr + c) : 0.0;
-    }
-  };
-  if (r0 + wid < r1) load(r0 + wid, 0);   // constant during PCG: before the PDL wait
-  pdl_wait();
-  if (active && !*active) return;
-  for (int j = tid; j < m; j += nthreads) {
-    sv[j] = cb[(size_t)k * m + j];
-    sv[m + j] = hl ? cx[(size_t)kl * m + j] : 0.0;
-    sv[2 * m + j] = hr ? cx[(size_t)kr * m + j] : 0.0;
-  }
-  __syncthreads();
-  for (int r = r0 + wid; r < r1; r += nw) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int c0 = 0; c0 < m; c0 += 32 * CR_PF) {
-      if (c0 > 0 || r != r0 + wid) load(r, c0);
-#pragma unroll
-      for (int j = 0; j < CR_PF; ++j) {
-        const int c = c0 + lane + 32 * j;
-        if (c < m) {
-          a0 = fma(dv[j], sv[c], a0);
-          a1 = fma(pv[j], sv[m + c], a1);
-          a2 = fma(qv[j], sv[2 * m + c], a2);
-        }
-      }
-    }
-    const double acc = warp_sum(a0 - a1 - a2);
-    if (lane == 0) cx[(size_t)k * m + r] = acc;
-  }
-  __syncthreads();
-}
-
-// top system after the truncated cyclic reduction, rows [r0, r0+CR_ROWS) of
-// x_top = -A b_top with A = -Top^{-1} stored block-major (T x T blocks of m x m); b_top is
-// gathered from the active blocks tb[] of cb, x_top scattered into cx.
-__device__ __forceinline__ void top_solve_rows(const Dims& d, const int* __restrict__ tb, int T,
-                                               const double* __restrict__ A,
-                                               const double* __restrict__ cb, double* cx, int r0,
-                                               double* sv, int tid, int nthreads) {
-  const int m = d.mc, n = T * m;
-  const size_t mm = (size_t)m * m;
-  for (int j = tid; j < n; j += nthreads) {
-    const int bj = j / m;
-    sv[j] = cb[(size_t)tb[bj] * m + (j - bj * m)];
-  }
-  __syncthreads();
-  const int lane = tid & 31, wid = tid >> 5, nw = nthreads >> 5;
-  const int r1 = min(n, r0 + CR_ROWS);
-  for (int r = r0 + wid; r < r1; r += nw) {
-    const int bi = r / m, rr = r - bi * m;
-    double a0 = 0.0, a1 = 0.0;
-    for (int bj = 0; bj < T; ++bj) {
-      const double* Ar = A + ((size_t)bi * T + bj) * mm + (size_t)rr * m;
-      const double* v = sv + bj * m;
-      int c = lane;
-      for (; c + 32 < m; c += 64) {
-        a0 = fma(Ar[c], v[c], a0);
-        a1 = fma(Ar[c + 32], v[c + 32], a1);
-      }
-      for (; c < m; c += 32) a0 = fma(Ar[c], v[c], a0);
-    }
-    const double acc = warp_sum(a0 + a1);
-    if (lane == 0) cx[(size_t)tb[bi] * m + rr] = -acc;
-  }
-  __syncthreads();
-}
-
 }  // namespace msfk

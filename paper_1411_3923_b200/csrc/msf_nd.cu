@@ -49,17 +49,18 @@ __device__ __forceinline__ int nd_find(const int* __restrict__ P, int n, int x) 
 
 // Original K_c entry (coarse node gp, slot a; node gq, slot b) summed over the coarse cells
 // [clo, chi) x [0, ncy) common to both agglomerates (K_c = sum over cells of the Galerkin cell
-// products, Eq. 10); unused eigen-slots (a >= nkept) are identity rows added for the nodes of
-// columns [idlo, idhi].
+// products, Eq. 10; cells = false: none); unused eigen-slots (a >= nkept) are identity rows
+// (ident = false: left out).
 __device__ __forceinline__ double kc_entry(const Dims& d, const double* __restrict__ Kc,
                                            const int* __restrict__ cls_of_agg,
                                            const EigClass* __restrict__ cls, int gp, int a, int gq,
-                                           int b, int clo, int chi, int idlo, int idhi) {
+                                           int b, int clo, int chi, bool cells, bool ident) {
   const int Y = d.ncy + 1, k = d.kmax, P = 4 * k;
   const int Ip = gp / Y, Jp = gp - (gp / Y) * Y, Iq = gq / Y, Jq = gq - (gq / Y) * Y;
   if (abs(Ip - Iq) > 1 || abs(Jp - Jq) > 1) return 0.0;
   const int nka = cls[cls_of_agg[gp]].nkept, nkb = cls[cls_of_agg[gq]].nkept;
-  if (a >= nka || b >= nkb) return (gp == gq && a == b && Ip >= idlo && Ip <= idhi) ? 1.0 : 0.0;
+  if (a >= nka || b >= nkb) return (ident && gp == gq && a == b) ? 1.0 : 0.0;
+  if (!cells) return 0.0;
   double v = 0.0;
   const int CIlo = max(max(max(Ip, Iq) - 1, 0), clo), CIhi = min(min(Ip, Iq), chi - 1);
   const int CJlo = max(max(Jp, Jq) - 1, 0), CJhi = min(min(Jp, Jq), d.ncy - 1);
@@ -75,6 +76,12 @@ __device__ __forceinline__ double kc_entry(const Dims& d, const double* __restri
 // ------------------------------------------------------------------ assembly of the fronts
 // F = original entries of the rows / columns of S  +  extend-add of the children's F_BB.
 // Tasks: 64 x 64 tiles of the fronts of one level (list: fronts[n], tile prefix[n + 1]).
+// mode 0 (fronts of this rank's box): cell entries of the cells [clo, chi), identity rows of
+//   the unused eigen-slots, every child;
+// mode 1 (interface fronts, this rank's partial before the all-reduce): cell entries of the
+//   rank's cells and the rank's own box root (a local child) only;
+// mode 2 (interface fronts after the all-reduce, replicated): identity rows and the
+//   interface children, ADDED to the all-reduced partial sum.
 __global__ void __launch_bounds__(256) k_nd_assemble(Dims d, const NdFront* __restrict__ fr,
                                                      const int* __restrict__ nodes,
                                                      const int* __restrict__ chmap,
@@ -82,8 +89,7 @@ __global__ void __launch_bounds__(256) k_nd_assemble(Dims d, const NdFront* __re
                                                      const double* __restrict__ Kcell,
                                                      const int* __restrict__ cls_of_agg,
                                                      const EigClass* __restrict__ cls, double* Fall,
-                                                     long long Fstride, int clo, int chi, int idlo,
-                                                     int idhi) {
+                                                     long long Fstride, int clo, int chi, int mode) {
   const int li = nd_find(list + n, n, blockIdx.x);
   const int f = list[li], t = blockIdx.x - list[n + li];
   const NdFront F = fr[f];
@@ -112,15 +118,18 @@ __global__ void __launch_bounds__(256) k_nd_assemble(Dims d, const NdFront* __re
     double v = 0.0;
     if (pn < F.s_n || qn < F.s_n)
       v = kc_entry(d, Kc, cls_of_agg, cls, nodes[F.node_off + pn], a, nodes[F.node_off + qn], b, clo,
-                   chi, idlo, idhi);
+                   chi, mode != 2, mode != 1);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       if (ch[c] < 0) continue;
+      const bool ctop = (F.flags >> (1 + c)) & 1;
+      if ((mode == 1 && ctop) || (mode == 2 && !ctop)) continue;
       const int cp = chmap[F.chmap_off + 2 * pn + c], cq = chmap[F.chmap_off + 2 * qn + c];
       if (cp >= 0 && cq >= 0)
         v += Fr[coff[c] + (size_t)(cs[c] + cp * k + a) * cld[c] + cs[c] + cq * k + b];
     }
-    A[(size_t)i * ld + j] = v;
+    if (mode == 2) A[(size_t)i * ld + j] += v;
+    else A[(size_t)i * ld + j] = v;
   }
 }
 
@@ -414,6 +423,7 @@ __global__ void __launch_bounds__(256) k_nd_solve(Dims d, const NdFront* __restr
                                                   const double* __restrict__ Fall, long long Fstride,
                                                   double* uall, long long ustride,
                                                   const double* __restrict__ cball, double* cxall,
+                                                  const double* __restrict__ vtall, long long vstride,
                                                   const PcgScalars* sc, int rhs0, int gated) {
   extern __shared__ __align__(16) double nsm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(nsm);
@@ -449,6 +459,7 @@ __global__ void __launch_bounds__(256) k_nd_solve(Dims d, const NdFront* __restr
   const double* cb = cball + (size_t)rhs * d.nbc * d.mc;
   double* cx = cxall + (size_t)rhs * d.nbc * d.mc;
   double* u = uall + (size_t)rhs * ustride;
+  const double* vt = vtall + (size_t)rhs * vstride;
   const int4* vm = vmap + F.vmap_off;
   if (live) {
     for (int c = threadIdx.x; c < lenp; c += 256) {
@@ -456,7 +467,7 @@ __global__ void __launch_bounds__(256) k_nd_solve(Dims d, const NdFront* __restr
       if (c < len) {
         const int4 m = vm[c];
         if (c < s) {
-          x = cb[m.x];
+          x = m.w >= 0 ? vt[m.w] : cb[m.x];
           if (m.y >= 0) x += u[m.y];
           if (m.z >= 0) x += u[m.z];
         } else {
@@ -468,7 +479,7 @@ __global__ void __launch_bounds__(256) k_nd_solve(Dims d, const NdFront* __restr
     if (FWD)
       for (int r = threadIdx.x; r < nrow; r += 256) {
         const int4 m = vm[s + rb0 + r];
-        double x = 0.0;
+        double x = m.w >= 0 ? vt[m.w] : 0.0;
         if (m.y >= 0) x += u[m.y];
         if (m.z >= 0) x += u[m.z];
         vb[r] = x;
@@ -501,6 +512,28 @@ __global__ void __launch_bounds__(256) k_nd_solve(Dims d, const NdFront* __restr
   pdl_launch();
 }
 
+// Interface fronts' partial right-hand sides of this rank, for the all-reduce (strip partition):
+// vtop[i] = c[pm.x] (the rank's partial restriction, S variables) + u[pm.y] (its box root's
+// update, when the box root is a child of the front)
+__global__ void __launch_bounds__(256) k_nd_pack(const int2* __restrict__ pm, int n,
+                                                 const double* __restrict__ cball, long long cstride,
+                                                 const double* __restrict__ uall, long long ustride,
+                                                 double* vtall, long long vstride, const PcgScalars* sc,
+                                                 int rhs0, int gated) {
+  pdl_wait();
+  const int rhs = rhs0 + blockIdx.y;
+  if (gated && !sc[rhs].active) return;
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i < n) {
+    const int2 m = pm[i];
+    double v = 0.0;
+    if (m.x >= 0) v += cball[(size_t)rhs * cstride + m.x];
+    if (m.y >= 0) v += uall[(size_t)rhs * ustride + m.y];
+    vtall[(size_t)rhs * vstride + i] = v;
+  }
+  pdl_launch();
+}
+
 }  // namespace
 
 // ================================================================== host: plan
@@ -511,7 +544,8 @@ constexpr int ND_LEAF = 5;   // leaf boxes of at most 5 x 5 coarse nodes
 struct Builder {
   int X, Y, k;
   NdPlan& P;
-  std::vector<int> height;
+  int rank;
+  const std::vector<int>& icol;   // interface column of each rank > 0 (icol[r], r = 1..N-1)
 
   // ring of the box [x0, x1) x [y0, y1) inside the grid
   std::vector<int> ring(int x0, int x1, int y0, int y1) const {
@@ -526,26 +560,7 @@ struct Builder {
     return r;
   }
 
-  int rec(int x0, int x1, int y0, int y1) {
-    const int w = x1 - x0, h = y1 - y0;
-    if (w <= 0 || h <= 0) return -1;
-    std::vector<int> S;
-    int c0 = -1, c1 = -1;
-    if (w <= ND_LEAF && h <= ND_LEAF) {
-      for (int x = x0; x < x1; ++x)
-        for (int y = y0; y < y1; ++y) S.push_back(x * Y + y);
-    } else if (w >= h) {
-      const int xm = x0 + w / 2;
-      c0 = rec(x0, xm, y0, y1);
-      c1 = rec(xm + 1, x1, y0, y1);
-      for (int y = y0; y < y1; ++y) S.push_back(xm * Y + y);
-    } else {
-      const int ym = y0 + h / 2;
-      c0 = rec(x0, x1, y0, ym);
-      c1 = rec(x0, x1, ym + 1, y1);
-      for (int x = x0; x < x1; ++x) S.push_back(x * Y + ym);
-    }
-    const std::vector<int> B = ring(x0, x1, y0, y1);
+  int make(const std::vector<int>& S, const std::vector<int>& B, int c0, int c1, bool top) {
     NdFront F{};
     F.s_n = (int)S.size();
     F.b_n = (int)B.size();
@@ -553,6 +568,8 @@ struct Builder {
     F.ch0 = c0;
     F.ch1 = c1;
     F.chmap_off = (int)P.chmap.size();
+    F.flags = (top ? 1 : 0) | (c0 >= 0 && (P.fr[c0].flags & 1) ? 2 : 0) | (c1 >= 0 && (P.fr[c1].flags & 1) ? 4 : 0);
+    F.vtop_off = -1;
     P.nodes.insert(P.nodes.end(), S.begin(), S.end());
     P.nodes.insert(P.nodes.end(), B.begin(), B.end());
     // for every node of this front, its index in each child's boundary list (-1: none)
@@ -581,9 +598,49 @@ struct Builder {
         for (int j = 0; j < F.s_n + F.b_n; ++j) found += P.chmap[F.chmap_off + 2 * j + q] >= 0;
         if (found != P.fr[chs[q]].b_n) P.ok = false;
       }
-    F.level = std::max(c0 >= 0 ? P.fr[c0].level + 1 : 0, c1 >= 0 ? P.fr[c1].level + 1 : 0);
+    // level: height among fronts of the same kind (box subtree / interface tree)
+    int lv = 0;
+    for (int q = 0; q < 2; ++q)
+      if (chs[q] >= 0 && ((P.fr[chs[q]].flags & 1) == (top ? 1 : 0))) lv = std::max(lv, P.fr[chs[q]].level + 1);
+    F.level = lv;
     P.fr.push_back(F);
     return (int)P.fr.size() - 1;
+  }
+
+  // nested dissection of this rank's box (local fronts)
+  int rec(int x0, int x1, int y0, int y1) {
+    const int w = x1 - x0, h = y1 - y0;
+    if (w <= 0 || h <= 0) return -1;
+    std::vector<int> S;
+    int c0 = -1, c1 = -1;
+    if (w <= ND_LEAF && h <= ND_LEAF) {
+      for (int x = x0; x < x1; ++x)
+        for (int y = y0; y < y1; ++y) S.push_back(x * Y + y);
+    } else if (w >= h) {
+      const int xm = x0 + w / 2;
+      c0 = rec(x0, xm, y0, y1);
+      c1 = rec(xm + 1, x1, y0, y1);
+      for (int y = y0; y < y1; ++y) S.push_back(xm * Y + y);
+    } else {
+      const int ym = y0 + h / 2;
+      c0 = rec(x0, x1, y0, ym);
+      c1 = rec(x0, x1, ym + 1, y1);
+      for (int x = x0; x < x1; ++x) S.push_back(x * Y + ym);
+    }
+    return make(S, ring(x0, x1, y0, y1), c0, c1, false);
+  }
+
+  // ranks [ra, rb) over the node columns [gx0, gx1): a single rank is its box (built only by
+  // that rank); a group is split at the interface column of its middle rank, whose front is an
+  // interface front (replicated on every rank)
+  int group(int ra, int rb, int gx0, int gx1) {
+    if (rb - ra == 1) return ra == rank ? rec(gx0, gx1, 0, Y) : -1;
+    const int rm = (ra + rb) / 2, xm = icol[rm];
+    const int c0 = group(ra, rm, gx0, xm);
+    const int c1 = group(rm, rb, xm + 1, gx1);
+    std::vector<int> S;
+    for (int y = 0; y < Y; ++y) S.push_back(xm * Y + y);
+    return make(S, ring(gx0, gx1, 0, Y), c0, c1, true);
   }
 };
 
@@ -608,92 +665,58 @@ NdPlan::List add_list(NdPlan& P, const std::vector<int>& fronts, Fn... cnt) {
   return L;
 }
 
-}  // namespace
-
-// Builds the nested-dissection plan of the coarse node grid (one box: every node; the strip
-// partition uses the same builder per rank box).  Returns false on an internal inconsistency.
-bool nd_build_plan(const Dims& d, NdPlan& P) {
-  P = NdPlan();
-  const int X = d.ncx + 1, Y = d.ncy + 1, k = d.kmax;
-  Builder b{X, Y, k, P, {}};
-  P.root = b.rec(0, X, 0, Y);
-  if (!P.ok || P.root < 0) return false;
-  long long Fo = 0, uo = 0;
-  int H = 0;
-  for (NdFront& F : P.fr) {
-    const long long nf = (long long)(F.s_n + F.b_n) * k, ld = nf + (nf & 1);
-    F.F_off = Fo;
-    F.u_off = uo;
-    Fo += (nf * ld + 31) & ~31LL;   // 256-byte aligned fronts, even leading dimension
-    uo += (long long)F.b_n * k;
-    H = std::max(H, F.level + 1);
-  }
-  P.F_total = Fo;
-  P.u_total = uo;
-  // vmap: for every front variable its global coarse index and, for S / B variables, the
-  // absolute indices of the children's update entries that add into it (-1: none)
-  P.vmap.clear();
-  for (NdFront& F : P.fr) {
-    F.vmap_off = (int)(P.vmap.size() / 4);
-    const int nn = F.s_n + F.b_n;
-    for (int j = 0; j < nn; ++j)
-      for (int a = 0; a < k; ++a) {
-        int u[2] = {-1, -1};
-        const int chs[2] = {F.ch0, F.ch1};
-        for (int q = 0; q < 2; ++q) {
-          const int cp = chs[q] >= 0 ? P.chmap[F.chmap_off + 2 * j + q] : -1;
-          if (cp >= 0) u[q] = (int)(P.fr[chs[q]].u_off + (long long)cp * k + a);
-        }
-        P.vmap.insert(P.vmap.end(), {P.nodes[F.node_off + j] * k + a, u[0], u[1], 0});
-      }
-  }
-  P.H = H;
-  std::vector<std::vector<int>> lev(H);
-  for (int f = 0; f < (int)P.fr.size(); ++f) lev[P.fr[f].level].push_back(f);
-  P.asmb.resize(H);
-  P.fwd.resize(H);
-  P.back.resize(H);
-  P.panel.resize(H);
-  P.max_act = 1;
-  P.scr_doubles = NB;
+// the task lists of one group of levels (box subtree or interface tree)
+void level_lists(NdPlan& P, int k, const std::vector<std::vector<int>>& lev, NdPlan::Levels& Lv) {
+  const int H = (int)lev.size();
+  Lv.asmb.resize(H);
+  Lv.fwd.resize(H);
+  Lv.back.resize(H);
+  Lv.panel.resize(H);
+  Lv.fwd_smem.assign(H, 0);
+  Lv.back_smem.assign(H, 0);
+  auto nt = [k](const NdFront& F) { return (long long)((F.s_n + F.b_n) * k + NB - 1) / NB; };
+  // rows per solve CTA: the level's rows over about 4 CTAs per SM, a multiple of 8, at least 8,
+  // at most the largest front's rows and ND_STAGE bytes of staged rows (very long rows, k = 16:
+  // fewer rows than warps)
+  auto pick = [&](const std::vector<int>& fl, bool fwd, int& lmax) {
+    long long rows = 0;
+    int rmax = 0;
+    lmax = 0;
+    for (int f : fl) {
+      const NdFront& F = P.fr[f];
+      const int r = (fwd ? F.b_n : F.s_n) * k;
+      const int len = fwd ? F.s_n * k : (F.s_n + F.b_n) * k;
+      rows += r;
+      rmax = std::max(rmax, r);
+      lmax = std::max(lmax, len + (len & 1));
+    }
+    const long long want = std::max<long long>(8, (rows / (148LL * 4) + 7) / 8 * 8);
+    long long cap = ND_STAGE / (8LL * std::max(1, lmax));
+    if (cap < 8) {
+      long long p = 1;
+      while (p * 2 <= cap) p *= 2;
+      return (int)p;
+    }
+    cap = cap / 8 * 8;
+    return (int)std::min<long long>(std::min(want, cap), std::max(8, (rmax + 7) / 8 * 8));
+  };
+  auto smem = [](int lmax, int RB) {
+    return (int)(8 * (2 + (long long)lmax + ((RB + 1) & ~1) + (long long)RB * lmax));
+  };
   for (int h = 0; h < H; ++h) {
-    auto nt = [k](const NdFront& F) { return (long long)((F.s_n + F.b_n) * k + NB - 1) / NB; };
-    P.asmb[h] = add_list(P, lev[h], [&](const NdFront& F) { return nt(F) * nt(F); });
+    Lv.asmb[h] = add_list(P, lev[h], [&](const NdFront& F) { return nt(F) * nt(F); });
     std::vector<int> fw;
     for (int f : lev[h])
       if (P.fr[f].b_n > 0) fw.push_back(f);
-    // rows per CTA: the level's rows spread over about 8 CTAs per SM; levels with few rows
-    // (the top of the tree) one row per warp (RW = 1, RB = 8), else 4 rows per warp and RB a
-    // multiple of 32 up to the largest front of the level
-    // rows per CTA: the level's rows over about 4 CTAs per SM, a multiple of 8, at least 8,
-    // at most the largest front's rows and ND_STAGE bytes of staged rows
-    auto pick = [&](const std::vector<int>& fl, bool fwd) {
-      long long rows = 0;
-      int rmax = 0, lmax = 0;
-      for (int f : fl) {
-        const NdFront& F = P.fr[f];
-        const int r = (fwd ? F.b_n : F.s_n) * k;
-        const int len = fwd ? F.s_n * k : (F.s_n + F.b_n) * k;
-        rows += r;
-        rmax = std::max(rmax, r);
-        lmax = std::max(lmax, len + (len & 1));
-      }
-      const long long want = std::max<long long>(8, (rows / (148LL * 4) + 7) / 8 * 8);
-      long long cap = ND_STAGE / (8LL * std::max(1, lmax));
-      if (cap < 8) {   // very long rows (k = 16): fewer rows than warps per CTA
-        long long p = 1;
-        while (p * 2 <= cap) p *= 2;
-        return (int)p;
-      }
-      cap = cap / 8 * 8;
-      return (int)std::min<long long>(std::min(want, cap), std::max(8, (rmax + 7) / 8 * 8));
-    };
-    int RB = pick(fw, true);
-    P.fwd[h] = add_list(P, fw, [&](const NdFront& F) { return (long long)(F.b_n * k + RB - 1) / RB; });
-    P.fwd[h].RB = RB;
-    RB = pick(lev[h], false);
-    P.back[h] = add_list(P, lev[h], [&](const NdFront& F) { return (long long)(F.s_n * k + RB - 1) / RB; });
-    P.back[h].RB = RB;
+    int lmax = 0;
+    int RB = pick(fw, true, lmax);
+    Lv.fwd[h] = add_list(P, fw, [&](const NdFront& F) { return (long long)(F.b_n * k + RB - 1) / RB; });
+    Lv.fwd[h].RB = RB;
+    Lv.fwd_smem[h] = smem(lmax, RB);
+    RB = pick(lev[h], false, lmax);
+    Lv.back[h] = add_list(P, lev[h], [&](const NdFront& F) { return (long long)(F.s_n * k + RB - 1) / RB; });
+    Lv.back[h].RB = RB;
+    Lv.back_smem[h] = smem(lmax, RB);
     int smax = 0;
     for (int f : lev[h]) smax = std::max(smax, P.fr[f].s_n * k);
     for (int pt = 0; pt * NB < smax; ++pt) {
@@ -703,32 +726,118 @@ bool nd_build_plan(const Dims& d, NdPlan& P) {
       NdPlan::List L = add_list(
           P, act, [&](const NdFront& F) { return nt(F); }, [&](const NdFront& F) { return nt(F) * nt(F); },
           [&](const NdFront& F) { return (long long)(F.s_n + F.b_n) * k; });
-      // totals of the 2nd / 3rd prefix
       L.total2 = P.lists[L.off + 2 * L.n + 1 + L.n];
       L.total3 = P.lists[L.off + 3 * L.n + 2 + L.n];
-      P.panel[h].push_back(L);
+      Lv.panel[h].push_back(L);
       P.max_act = std::max(P.max_act, L.n);
       P.scr_doubles = std::max(P.scr_doubles, (long long)NB * L.total3);
     }
   }
-  P.lev_smax.assign(H, 0);
-  P.lev_nfmax.assign(H, 0);
-  P.lev_fwd_smem.assign(H, 0);
-  P.lev_back_smem.assign(H, 0);
-  for (const NdFront& F : P.fr) {
-    P.lev_smax[F.level] = std::max(P.lev_smax[F.level], F.s_n * k);
-    P.lev_nfmax[F.level] = std::max(P.lev_nfmax[F.level], (F.s_n + F.b_n) * k);
-    P.max_nf = std::max(P.max_nf, (F.s_n + F.b_n) * k);
+}
+
+}  // namespace
+
+// Builds the nested-dissection plan of the coarse node grid for rank `rank` of `nranks`
+// (DESIGN.md §8(e)): the interface columns icol[1..N-1] (the first coarse column of each rank
+// > 0) are the separators of a bisection over the ranks (interface fronts, replicated); each
+// rank dissects its own box between them (local fronts).  One GPU: one box, every node.
+// Returns false on an internal inconsistency.
+bool nd_build_plan(const Dims& d, NdPlan& P, int rank, int nranks, const std::vector<int>& icol) {
+  P = NdPlan();
+  const int X = d.ncx + 1, Y = d.ncy + 1, k = d.kmax;
+  Builder b{X, Y, k, P, rank, icol};
+  P.root = b.group(0, nranks, 0, X);
+  if (!P.ok) return false;
+  // storage: interface fronts first (identical layout on every rank: one all-reduce), then
+  // the rank's box fronts; 256-byte aligned, even leading dimension
+  long long Fo = 0, uo = 0, vo = 0;
+  int H = 0, TH = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (NdFront& F : P.fr) {
+      const bool top = F.flags & 1;
+      if (top != (pass == 0)) continue;
+      const long long nf = (long long)(F.s_n + F.b_n) * k, ld = nf + (nf & 1);
+      F.F_off = Fo;
+      F.u_off = uo;
+      Fo += (nf * ld + 31) & ~31LL;
+      uo += (long long)F.b_n * k;
+      if (top) {
+        F.vtop_off = (int)vo;
+        vo += nf;
+        TH = std::max(TH, F.level + 1);
+        P.n_top++;
+      } else {
+        H = std::max(H, F.level + 1);
+      }
+    }
+    if (pass == 0) P.top_F = Fo;
   }
-  // shared memory of the solve launches: barrier, rhs, row updates, staged rows
-  for (int h = 0; h < H; ++h) {
-    auto bytes = [](int len, int RB) {
-      const long long lenp = len + (len & 1);
-      return (int)(8 * (2 + lenp + ((RB + 1) & ~1) + (long long)RB * lenp));
-    };
-    P.lev_fwd_smem[h] = bytes(P.lev_smax[h], P.fwd[h].RB);
-    P.lev_back_smem[h] = bytes(P.lev_nfmax[h], P.back[h].RB);
+  // every rank's realisation stride is the same (its box fronts padded to the largest box's),
+  // so that the interface fronts of every realisation sit at the same offsets on all ranks
+  // (the in-process group all-reduces them through one offset)
+  long long locmax = Fo - P.top_F;
+  for (int q = 0; q < nranks && nranks > 1; ++q) {
+    if (q == rank) continue;
+    NdPlan Q;
+    Builder bq{X, Y, k, Q, q, icol};
+    bq.group(0, nranks, 0, X);
+    long long lf = 0;
+    for (const NdFront& F : Q.fr)
+      if (!(F.flags & 1)) {
+        const long long nf = (long long)(F.s_n + F.b_n) * k, ld = nf + (nf & 1);
+        lf += (nf * ld + 31) & ~31LL;
+      }
+    locmax = std::max(locmax, lf);
   }
+  P.F_total = P.top_F + locmax;
+  P.u_total = uo;
+  P.vtop_total = vo;
+  P.H = H;
+  P.TH = TH;
+  // vmap: for every front variable its global coarse index, the absolute indices of the
+  // children's update entries that add into it (-1: none; interface fronts: interface
+  // children only) and, for interface fronts, its index in vtop (-1: box front)
+  P.vmap.clear();
+  P.packmap.assign(2 * vo, -1);
+  for (NdFront& F : P.fr) {
+    F.vmap_off = (int)(P.vmap.size() / 4);
+    const bool top = F.flags & 1;
+    const int nn = F.s_n + F.b_n;
+    for (int j = 0; j < nn; ++j)
+      for (int a = 0; a < k; ++a) {
+        int u[2] = {-1, -1};
+        const int chs[2] = {F.ch0, F.ch1};
+        for (int q = 0; q < 2; ++q) {
+          const int cp = chs[q] >= 0 ? P.chmap[F.chmap_off + 2 * j + q] : -1;
+          if (cp < 0) continue;
+          const int ui = (int)(P.fr[chs[q]].u_off + (long long)cp * k + a);
+          const bool ctop = P.fr[chs[q]].flags & 1;
+          if (!top || ctop) u[q] = ui;
+          else P.packmap[2 * (F.vtop_off + j * k + a) + 1] = ui;   // the box root's update
+        }
+        const int g = P.nodes[F.node_off + j] * k + a;
+        if (top && j < F.s_n) P.packmap[2 * (F.vtop_off + j * k + a)] = g;
+        P.vmap.insert(P.vmap.end(), {g, u[0], u[1], top ? F.vtop_off + j * k + a : -1});
+      }
+  }
+  std::vector<std::vector<int>> lev(H), tlev(TH), tall;
+  tall.resize(1);
+  for (int f = 0; f < (int)P.fr.size(); ++f) {
+    if (P.fr[f].flags & 1) {
+      tlev[P.fr[f].level].push_back(f);
+      tall[0].push_back(f);
+    } else {
+      lev[P.fr[f].level].push_back(f);
+    }
+  }
+  P.max_act = 1;
+  P.scr_doubles = NB;
+  level_lists(P, k, lev, P.loc);
+  level_lists(P, k, tlev, P.top);
+  auto nt = [k](const NdFront& F) { return (long long)((F.s_n + F.b_n) * k + NB - 1) / NB; };
+  P.tpart = add_list(P, tall[0], [&](const NdFront& F) { return nt(F) * nt(F); });
+  P.max_nf = 0;
+  for (const NdFront& F : P.fr) P.max_nf = std::max(P.max_nf, (F.s_n + F.b_n) * k);
   // bytes streamed per solve and realisation (forward B x S blocks, back S rows)
   P.solve_bytes = 0;
   for (const NdFront& F : P.fr) {
@@ -743,7 +852,8 @@ size_t nd_workspace_bytes(const Dims& d, const NdPlan& P) {
   const size_t R = d.R;
   return al(R * P.F_total * 8) + al(R * P.u_total * 8) + al(2 * R * (size_t)P.max_act * NB * NB * 8) +
          2 * al(R * (size_t)P.scr_doubles * 8) + al(P.fr.size() * sizeof(NdFront)) +
-         al(P.nodes.size() * 4) + al(P.chmap.size() * 4) + al(P.lists.size() * 4) + al(P.vmap.size() * 4);
+         al(P.nodes.size() * 4) + al(P.chmap.size() * 4) + al(P.lists.size() * 4) + al(P.vmap.size() * 4) +
+         al(P.packmap.size() * 4) + al(R * (size_t)std::max<long long>(1, P.vtop_total) * 8);
 }
 
 // carve + upload (called at setup)
@@ -765,17 +875,23 @@ cudaError_t nd_setup(msf_ctx* c, char*& cur) {
   c->nd_chmap = (int*)take(P.chmap.size() * 4);
   c->nd_lists = (int*)take(P.lists.size() * 4);
   c->nd_vmap = (int*)take(P.vmap.size() * 4);
+  c->nd_pack = (int*)take(P.packmap.size() * 4);
+  c->nd_vtop = (double*)take(R * (size_t)std::max<long long>(1, P.vtop_total) * 8);
   cudaError_t e = cudaMemcpyAsync(c->nd_fr, P.fr.data(), P.fr.size() * sizeof(NdFront), cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->nd_nodes, P.nodes.data(), P.nodes.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->nd_chmap, P.chmap.data(), P.chmap.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->nd_lists, P.lists.data(), P.lists.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->nd_vmap, P.vmap.data(), P.vmap.size() * 4, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess && !P.packmap.empty())
+    e = cudaMemcpyAsync(c->nd_pack, P.packmap.data(), P.packmap.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->nd_u, 0, R * P.u_total * 8, c->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->nd_vtop, 0, R * (size_t)std::max<long long>(1, P.vtop_total) * 8, c->stream);
   return e;
 }
 
-// Fronts' assembly + blocked sweep, level by level (leaves first), all realisations.
-void launch_nd_factor(msf_ctx* c) {
+namespace {
+
+void factor_levels(msf_ctx* c, const NdPlan::Levels& Lv, int mode) {
   const NdPlan& P = c->nd;
   const Dims& d = c->d;
   const int R = d.R;
@@ -787,14 +903,15 @@ void launch_nd_factor(msf_ctx* c) {
     attrs = true;
   }
   const long long Fs = P.F_total;
-  for (int h = 0; h < P.H; ++h) {
-    const NdPlan::List& A = P.asmb[h];
+  for (size_t h = 0; h < Lv.asmb.size(); ++h) {
+    const NdPlan::List& A = Lv.asmb[h];
+    if (A.total == 0) continue;
     k_nd_assemble<<<dim3(A.total, R), 256, 0, c->stream>>>(
         d, c->nd_fr, c->nd_nodes, c->nd_chmap, c->nd_lists + A.off, A.n, c->Kcell, c->cls_of_agg_d,
-        c->classes_d, c->nd_F, Fs, 0, d.ncx, 0, d.ncx);
+        c->classes_d, c->nd_F, Fs, c->cell_lo, c->cell_hi, mode);
     MSF_LAUNCHED(c);
-    for (size_t pt = 0; pt < P.panel[h].size(); ++pt) {
-      const NdPlan::List& L = P.panel[h][pt];
+    for (size_t pt = 0; pt < Lv.panel[h].size(); ++pt) {
+      const NdPlan::List& L = Lv.panel[h][pt];
       PanelArgs pa{c->nd_lists + L.off, L.n, (int)pt, c->nd_Q, c->nd_Q + (size_t)R * P.max_act * NB * NB,
                    c->nd_Ar, c->nd_Rp, (long long)P.max_act * NB * NB, P.scr_doubles};
       k_nd_pivot<<<dim3(L.n, R), 256, 2 * NB * (NB + 1) * 8, c->stream>>>(d, c->nd_fr, c->nd_F, Fs, pa, c->factor_status);
@@ -806,32 +923,80 @@ void launch_nd_factor(msf_ctx* c) {
   }
 }
 
-// c <- K_c^{-1} c for realisations [rhs0, rhs0 + nr): forward levels (leaves to root), back
-// levels (root to leaves); cb is read, cx written.
-void launch_nd_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
+void solve_levels(msf_ctx* c, const NdPlan::Levels& Lv, bool fwd, int rhs0, int nr, bool gated) {
   const NdPlan& P = c->nd;
   const Dims& d = c->d;
-  const int k = d.kmax;
   static bool smem_set = false;
   if (!smem_set) {
     cudaFuncSetAttribute(k_nd_solve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_nd_solve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     smem_set = true;
   }
-  auto go = [&](const NdPlan::List& L, bool fwd, size_t smem) {
-    if (L.total == 0) return;
-    if (fwd)
-      launch_k(k_nd_solve<true>, dim3(L.total, nr), dim3(256), smem, c->stream, d, (const NdFront*)c->nd_fr,
-               (const int4*)c->nd_vmap, (const int*)(c->nd_lists + L.off), L.n, L.RB, (const double*)c->nd_F,
-               (long long)P.F_total, c->nd_u, (long long)P.u_total, (const double*)c->cb, c->cx,
-               (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
-    else
-      launch_k(k_nd_solve<false>, dim3(L.total, nr), dim3(256), smem, c->stream, d, (const NdFront*)c->nd_fr,
-               (const int4*)c->nd_vmap, (const int*)(c->nd_lists + L.off), L.n, L.RB, (const double*)c->nd_F,
-               (long long)P.F_total, c->nd_u, (long long)P.u_total, (const double*)c->cb, c->cx,
-               (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
+  const int H = (int)Lv.fwd.size();
+  for (int i = 0; i < H; ++i) {
+    const int h = fwd ? i : H - 1 - i;
+    const NdPlan::List& L = fwd ? Lv.fwd[h] : Lv.back[h];
+    if (L.total == 0) continue;
+    const size_t smem = (size_t)(fwd ? Lv.fwd_smem[h] : Lv.back_smem[h]);
+    auto kern = fwd ? k_nd_solve<true> : k_nd_solve<false>;
+    launch_k(kern, dim3(L.total, nr), dim3(256), smem, c->stream, d, (const NdFront*)c->nd_fr,
+             (const int4*)c->nd_vmap, (const int*)(c->nd_lists + L.off), L.n, L.RB, (const double*)c->nd_F,
+             (long long)P.F_total, c->nd_u, (long long)P.u_total, (const double*)c->cb, c->cx,
+             (const double*)c->nd_vtop, (long long)std::max<long long>(1, P.vtop_total),
+             (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
     MSF_LAUNCHED(c);
-  };
-  for (int h = 0; h < P.H; ++h) go(P.fwd[h], true, (size_t)P.lev_fwd_smem[h]);
-  for (int h = P.H - 1; h >= 0; --h) go(P.back[h], false, (size_t)P.lev_back_smem[h]);
+  }
+}
+
+}  // namespace
+
+// K_c factorisation, box part: this rank's fronts level by level (leaves first), then its
+// partial sums of the interface fronts (cell entries of its cells, its box root's Schur
+// complement) -- all-reduced over the ranks before launch_nd_factor_top.  All realisations.
+void launch_nd_factor_local(msf_ctx* c) {
+  factor_levels(c, c->nd.loc, 0);
+  const NdPlan::List& T = c->nd.tpart;
+  if (T.total > 0) {
+    k_nd_assemble<<<dim3(T.total, c->d.R), 256, 0, c->stream>>>(
+        c->d, c->nd_fr, c->nd_nodes, c->nd_chmap, c->nd_lists + T.off, T.n, c->Kcell, c->cls_of_agg_d,
+        c->classes_d, c->nd_F, c->nd.F_total, c->cell_lo, c->cell_hi, 1);
+    MSF_LAUNCHED(c);
+  }
+}
+
+// interface fronts (replicated): identity rows + interface children, then the sweep
+void launch_nd_factor_top(msf_ctx* c) { factor_levels(c, c->nd.top, 2); }
+
+void launch_nd_factor(msf_ctx* c) {
+  launch_nd_factor_local(c);
+  launch_nd_factor_top(c);
+}
+
+// Coarse solve phases for realisations [rhs0, rhs0 + nr): forward over the box fronts (+ the
+// interface partial right-hand sides, all-reduced by the caller on a strip partition),
+// forward + back over the interface fronts, back over the box fronts.  cb is read, cx written.
+void launch_nd_solve_local_fwd(msf_ctx* c, int rhs0, int nr, bool gated) {
+  solve_levels(c, c->nd.loc, true, rhs0, nr, gated);
+  const long long n = c->nd.vtop_total;
+  if (n > 0) {
+    launch_k(k_nd_pack, dim3((unsigned)((n + 255) / 256), nr), dim3(256), 0, c->stream, (const int2*)c->nd_pack,
+             (int)n, (const double*)c->cb, (long long)c->d.nbc * c->d.mc, (const double*)c->nd_u,
+             (long long)c->nd.u_total, c->nd_vtop, (long long)n, (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
+    MSF_LAUNCHED(c);
+  }
+}
+
+void launch_nd_solve_top(msf_ctx* c, int rhs0, int nr, bool gated) {
+  solve_levels(c, c->nd.top, true, rhs0, nr, gated);
+  solve_levels(c, c->nd.top, false, rhs0, nr, gated);
+}
+
+void launch_nd_solve_local_back(msf_ctx* c, int rhs0, int nr, bool gated) {
+  solve_levels(c, c->nd.loc, false, rhs0, nr, gated);
+}
+
+void launch_nd_solve(msf_ctx* c, int rhs0, int nr, bool gated) {
+  launch_nd_solve_local_fwd(c, rhs0, nr, gated);
+  launch_nd_solve_top(c, rhs0, nr, gated);
+  launch_nd_solve_local_back(c, rhs0, nr, gated);
 }

@@ -64,15 +64,17 @@ def test_edge_pcg_parity(name):
         assert abs(comps[k] - ref["comps"][k]) <= tc * abs(ref["comps"][k]), (k, tc)
 
 
-@pytest.mark.parametrize("env", [{"MSF_PCG_MODE": "persistent"}, {"MSF_COARSE_COOP": "1"},
-                                 {"MSF_PCG_MODE": "stream"}, {"MSF_APPLY_TMA": "0", "MSF_RESIDUAL_TMA": "0"},
-                                 {"MSF_CUBLAS": "0"}, {"MSF_SGS_NB": "1"}])
+@pytest.mark.parametrize("env", [{"MSF_APPLY_TMA": "0", "MSF_RESIDUAL_TMA": "0"}, {"MSF_PDL": "0"},
+                                 {"MSF_RESTRICT_BATCH": "force"}, {"MSF_RESTRICT_BATCH": "0", "MSF_RESTRICT_WARP": "force"},
+                                 {"MSF_RESTRICT_BATCH": "0", "MSF_RESTRICT_WARP": "0"}, {"MSF_PROLONG_NR": "0"}])
 def test_opt_in_modes_match_default(env):
-    """The opt-in execution modes (read at context setup) solve
-    the same problem as the default graph path: iterations +-1, solutions to 1e-9."""
+    """The run-time switches (read at context setup) solve the
+    same problem as the default graph path: iterations +-1, solutions to 1e-9.  The spec is
+    large enough that each switch changes the kernel that runs: 129 node rows and an even
+    nely (the TMA-fed operator and residual by default), 561 agglomerates x 3 realisations."""
     import os
-    from test_gpu_parity import SPECS
-    spec = SPECS["robust_32x16"]
+    spec = W.small_spec(nelx=256, nely=128, cx=8, cy=8, tile=(32, 32), rmin=2.5, beta=8.0,
+                        etas=(0.7, 0.5, 0.3), dilated=2, bc="mbb", seed=29, Emin=1e-6)
     x = W.design_tile(spec)
 
     def solve():

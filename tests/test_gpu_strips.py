@@ -91,8 +91,8 @@ def test_strip_pcg_vs_oracle_and_single(name, nranks):
     its_s, comp_s, _ = m.pcg_solve(tol=1e-8)
     assert not nc
     for k in range(spec.n_rhs):
-        assert abs(its_g[k] - ref["iters"][k]) <= 2, (its_g, ref["iters"])
-        assert abs(its_g[k] - its_s[k]) <= 2, (its_g, its_s)
+        assert abs(its_g[k] - ref["iters"][k]) <= 1, (its_g, ref["iters"])
+        assert abs(its_g[k] - its_s[k]) <= 1, (its_g, its_s)
     ref = problem.solve(spec, x, fx, f, tol=1e-12)
     its_g, comp_g, _ = g.pcg_solve(tol=1e-12)
     u_s = torch.empty(spec.n_rhs * spec.n_dof, dtype=torch.float64, device=DEV)
@@ -110,10 +110,12 @@ def test_strip_pcg_vs_oracle_and_single(name, nranks):
 
 @pytest.mark.parametrize("name,nranks", CASES)
 def test_strip_coarse_solve_and_vcycle_vs_single(name, nranks):
-    """The distributed K_c (chain levels per rank, all-reduced interface system) solves
-    K_c c = b like the single-GPU cyclic reduction, and one partitioned V-cycle (halo'd
-    colour phases, distributed coarse correction, halo after the prolongation) equals the
-    single-GPU V-cycle, for every realisation."""
+    """The distributed K_c (each rank's box fronts, all-reduced interface fronts; DESIGN.md
+    §8(e)) solves K_c c = b like the single-GPU nested dissection, and one partitioned V-cycle
+    (halo'd colour phases, distributed coarse correction, halo after the prolongation) equals
+    the single-GPU V-cycle, for every realisation.  Both bars are 1e-11: the partition makes
+    the interface columns separators, so the elimination order -- hence the rounding --
+    differs from the single-GPU dissection."""
     spec, _ = STRIP_SPECS[name]
     x = W.design_tile(spec)
     g = group_for(spec, nranks, x)
@@ -130,7 +132,7 @@ def test_strip_coarse_solve_and_vcycle_vs_single(name, nranks):
         zs = torch.empty_like(r)
         m.precond_apply(k, r, zs)
         zg = g.precond_apply(k, r)
-        assert (zg - zs).norm() <= 1e-12 * zs.norm(), k
+        assert (zg - zs).norm() <= 1e-11 * zs.norm(), k
     g.close()
 
 
