@@ -149,6 +149,11 @@ int msf_matvec(msf_ctx* ctx, int rhs, const double* x, double* y);
 int msf_precond_apply(msf_ctx* ctx, int rhs, const double* r, double* z);
 /* One symmetric Gauss-Seidel sweep (reading R7) on K z = r, z updated in place. */
 int msf_sgs(msf_ctx* ctx, int rhs, const double* r, double* z);
+/* msf_sgs with flags: bit 0 starts from z = 0 (z's input is ignored; the pre-smoothing form
+ * of the V-cycle), bit 1 runs the sweep as the seven colour-phase launches of the strip
+ * partition instead of the streaming kernel (the two are bitwise equal; parity tests).
+ * Unknown flag bits: MSF_ERR_ARG. */
+int msf_sgs_ex(msf_ctx* ctx, int rhs, const double* r, double* z, int flags);
 /* c = K_c^{-1} b for realisation rhs; b, c: device [n_coarse_slots] (slot layout:
  * ((I*(ncy+1)+J)*n_modes + a), unused slots carry identity rows). */
 int msf_coarse_solve(msf_ctx* ctx, int rhs, const double* b, double* c);

@@ -27,7 +27,7 @@ EXPORTS = [
     "msf_workspace_bytes", "msf_setup_mesh", "msf_destroy", "msf_set_stream", "msf_last_error",
     "msf_filter_project", "msf_set_physical", "msf_build_coarse_basis", "msf_assemble_coarse",
     "msf_pcg_solve", "msf_sensitivities", "msf_oc_update", "msf_design_iteration",
-    "msf_design_iteration_host", "msf_matvec", "msf_precond_apply", "msf_sgs",
+    "msf_design_iteration_host", "msf_matvec", "msf_precond_apply", "msf_sgs", "msf_sgs_ex",
     "msf_coarse_solve", "msf_get_basis", "msf_get_coarse_blocks", "msf_get_physical",
     "msf_info", "msf_launch_count", "msf_bench_kernels",
     "msf_strip_bounds", "msf_dist_workspace_bytes", "msf_dist_setup", "msf_nccl_unique_id",
@@ -74,6 +74,7 @@ def load_library(path: str = LIB_PATH):
         "msf_design_iteration": [V, V, V, D, I, D, D, D, i32p, dp, dp, dp],
         "msf_design_iteration_host": [V, V, V, D, I, D, D, D, i32p, dp, dp, dp],
         "msf_matvec": [V, I, V, V], "msf_precond_apply": [V, I, V, V], "msf_sgs": [V, I, V, V],
+        "msf_sgs_ex": [V, I, V, V, I],
         "msf_coarse_solve": [V, I, V, V], "msf_get_basis": [V, V, V, V],
         "msf_get_coarse_blocks": [V, I, V, V], "msf_get_physical": [V, I, V, V],
         "msf_info": [V, i64p], "msf_launch_count": [V, i64p, I],
@@ -287,8 +288,12 @@ class Msfem:
     def precond_apply(self, rhs, r, z):
         self._check(self.lib.msf_precond_apply(self.ctx, rhs, _ptr(r), _ptr(z)))
 
-    def sgs(self, rhs, r, z):
-        self._check(self.lib.msf_sgs(self.ctx, rhs, _ptr(r), _ptr(z)))
+    def sgs(self, rhs, r, z, zero_start=False, phases=False):
+        flags = (1 if zero_start else 0) | (2 if phases else 0)
+        if flags:
+            self._check(self.lib.msf_sgs_ex(self.ctx, rhs, _ptr(r), _ptr(z), flags))
+        else:
+            self._check(self.lib.msf_sgs(self.ctx, rhs, _ptr(r), _ptr(z)))
 
     def coarse_solve(self, rhs, b, c):
         self._check(self.lib.msf_coarse_solve(self.ctx, rhs, _ptr(b), _ptr(c)))
@@ -343,8 +348,8 @@ class Msfem:
         ms = (ctypes.c_double * 15)()
         by = (ctypes.c_double * 15)()
         self._check(self.lib.msf_bench_kernels(self.ctx, reps, ms, by))
-        names = ["apply", "sgs_colour", "restrict", "coarse_solve", "prolong", "residual",
-                 "vcycle", "pcg_iteration", "update_f0", "p_update", "assemble_local",
+        names = ["apply", "sgs_sweep", "restrict", "coarse_solve", "prolong", "residual",
+                 "vcycle", "pcg_iteration", "sgs_pre_update", "p_update", "assemble_local",
                  "assemble_top", "coarse_fwd_local", "coarse_top", "coarse_back_local"]
         return {n: (ms[i], by[i]) for i, n in enumerate(names)}
 

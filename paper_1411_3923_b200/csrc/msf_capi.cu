@@ -23,11 +23,12 @@ static void destroy_graphs(msf_ctx* c) {
   if (c->iter_graph) cudaGraphExecDestroy(c->iter_graph);
   c->iter_graph = nullptr;
   c->iter_graph_R = -1;
-  for (auto& row : c->range_graph)
-    for (auto& g : row) {
-      if (g) cudaGraphExecDestroy(g);
-      g = nullptr;
-    }
+  for (auto& par : c->range_graph)
+    for (auto& row : par)
+      for (auto& g : row) {
+        if (g) cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
 }
 
 // programmatic dependent launch for the PCG kernels (launch_k); MSF_PDL=0 disables
@@ -201,7 +202,8 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
       return MSF_ERR_ARG;
     }
   }
-  P.max_partials = std::max(apply_partials_needed(d), sgs_colour_partials_needed(d));
+  P.max_partials = std::max({apply_partials_needed(d), sgs_colour_partials_needed(d),
+                             sgs_stream_partials_needed(P.dl)});
 
   // workspace size (node vectors on this rank's strip; moduli of the whole grid)
   const size_t R = d.R, nn = P.dl.nn, ne = d.ne, nt = d.nt;
@@ -210,13 +212,18 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   add(FIN_KINDS * MSF_MAX_RHS * 8);          // dsum
   add(nn);                                   // fixn
   add(d.nn);                                 // fixg
+  {
+    int fc, fp;
+    sgs_fix_layout(P.dl, fc, fp);
+    add((size_t)P.dl.nnx * fc);                // fixs
+  }
   add(2 * nn * 8);                           // f
   add(nt * 8 * 5);                           // x_tile, xt, dF, dg, x_new
   add(R * nt * 8);                           // xbar
   add(4 * nt * 8);                           // tile_tmp
   add(std::max(ne, 2 * nt) * 8);             // dc_el
   add(R * ne * 8);                           // E
-  add(6 * R * 2 * nn * 8);                   // u r z p q t
+  add(7 * R * 2 * nn * 8);                   // u r z p q t r2
   add(P.fw.size() * (8 + 4 + 4));            // filter
   add(d.n_agg * 4);                          // cls_of_agg
   add(P.classes.size() * sizeof(EigClass));  // classes
@@ -348,6 +355,8 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   }
   c->fixn = (uint8_t*)take(nn);
   c->fixg = (uint8_t*)take(d.nn);
+  sgs_fix_layout(c->dl, c->fs_col, c->fs_plane);
+  c->fixs = (uint8_t*)take((size_t)c->dl.nnx * c->fs_col);
   c->f = (double*)take(2 * nn * 8);
   c->x_tile = (double*)take(nt * 8 * 5);
   c->xt_tile = c->x_tile + nt;
@@ -359,13 +368,14 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   c->dc_el = (double*)take(std::max(ne, 2 * nt) * 8);
   c->E = (double*)take(R * ne * 8);
   c->E_loc = c->E + (size_t)c->dl.gox * d.nely;
-  double* vec = (double*)take(6 * R * 2 * nn * 8);
+  double* vec = (double*)take(7 * R * 2 * nn * 8);
   c->u = vec;
   c->r = vec + 1 * R * 2 * nn;
   c->z = vec + 2 * R * 2 * nn;
   c->pv = vec + 3 * R * 2 * nn;
   c->q = vec + 4 * R * 2 * nn;
   c->t = vec + 5 * R * 2 * nn;
+  c->r2 = vec + 6 * R * 2 * nn;
   char* fb = (char*)take(P.fw.size() * (8 + 4 + 4));
   c->filt_w_d = (double*)fb;
   c->filt_dx_d = (int*)(fb + P.fw.size() * 8);
@@ -454,6 +464,9 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   for (size_t n = 0; n < (size_t)d.nn; ++n) fixg[n] = (fixed_mask[2 * n] ? 1 : 0) | (fixed_mask[2 * n + 1] ? 2 : 0);
   ce = cudaMemcpyAsync(c->fixn, fixn.data(), nn, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->fixg, fixg.data(), d.nn, cudaMemcpyHostToDevice, c->stream);
+  std::vector<uint8_t> fixs;
+  sgs_fix_build(c->dl, fixn.data(), fixs);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->fixs, fixs.data(), fixs.size(), cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->f, floc.data(), 2 * nn * 8, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_w_d, P.fw.data(), P.fw.size() * 8, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_dx_d, P.fdx.data(), P.fdx.size() * 4, cudaMemcpyHostToDevice, c->stream);
@@ -467,7 +480,7 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->scal, 0, 64 * 8, c->stream);
   if (ce == cudaSuccess && c->dsum) ce = cudaMemsetAsync(c->dsum, 0, FIN_KINDS * MSF_MAX_RHS * 8, c->stream);
   // node vectors start at 0 (halo / padding columns are only ever written by exchanges)
-  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->u, 0, 6 * R * 2 * nn * 8, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->u, 0, 7 * R * 2 * nn * 8, c->stream);
   // coarse vectors start at 0: a strip reads (with zero weights) the coarse solution of the
   // agglomerates next to its chain, which it never writes, and packs the interface entries of
   // its (zero) neighbours' columns
@@ -583,23 +596,28 @@ int msf_assemble_coarse(msf_ctx* c) {
 
 // two-level V-cycle z = M^{-1} r for realisations [0, nr) (reading R8)
 // rz_mode (fused into the post-smoothing): 0 none, 1 rz at PCG init, 2 rz + beta
-// f0_done: the zero-start colour-0 phase already ran (fused into the PCG update).
+// rnew != null: the pre-smoothing first applies the PCG update rnew = r - alpha q
+// (||rnew||^2 -> convergence) and the V-cycle runs on rnew
 static void enqueue_vcycle(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,
-                           int rz_mode = 0, bool f0_done = false) {
-  launch_sgs_sweep(c, rhs0, nr, r, z, gated, !f0_done, 0, f0_done);  // z = SGS(0; r)
-  launch_residual(c, rhs0, nr, r, z, c->t, gated);                    // t = r - K z
-  launch_restrict(c, rhs0, nr, c->t, gated);                          // c = R t
-  launch_nd_solve(c, rhs0, nr, gated);                                // c <- K_c^{-1} c
-  launch_prolong(c, rhs0, nr, z, gated);                              // z += R^T c
-  launch_sgs_sweep(c, rhs0, nr, r, z, gated, false, rz_mode, false); // z = SGS(z; r) (+ r.z)
+                           int rz_mode = 0, double* rnew = nullptr) {
+  const bool upd = rnew != nullptr;
+  launch_sgs_stream(c, rhs0, nr, r, rnew, nullptr, z, gated, true, upd, 0);  // z = SGS(0; r)
+  if (upd) r = rnew;
+  launch_residual(c, rhs0, nr, r, z, c->t, gated);                          // t = r - K z
+  launch_restrict(c, rhs0, nr, c->t, gated);                                // c = R t
+  launch_nd_solve(c, rhs0, nr, gated);                                      // c <- K_c^{-1} c
+  launch_prolong(c, rhs0, nr, z, c->t, gated);                              // t = z + R^T c
+  launch_sgs_stream(c, rhs0, nr, r, nullptr, c->t, z, gated, false, false, rz_mode);  // z = SGS(t; r)
 }
 
-// one PCG iteration for the realisations [rhs0, rhs0 + nr)
-static void enqueue_iteration(msf_ctx* c, int rhs0, int nr) {
-  launch_matvec(c, rhs0, nr, c->pv, c->q, true, true);   // q = K p, alpha
-  launch_update_f0(c, rhs0, nr);                         // u, r, ||r||, z = F0(0; r)
-  enqueue_vcycle(c, rhs0, nr, c->r, c->z, true, 2, true);
-  launch_pcg_p(c, rhs0, nr, false);
+// one PCG iteration for the realisations [rhs0, rhs0 + nr); the residual moves from r to r2
+// (odd: r2 to r)
+static void enqueue_iteration(msf_ctx* c, int rhs0, int nr, int parity) {
+  double* ra = parity ? c->r2 : c->r;
+  double* rb = parity ? c->r : c->r2;
+  launch_matvec(c, rhs0, nr, c->pv, c->q, true, true);   // q = K p (p.q partials)
+  enqueue_vcycle(c, rhs0, nr, ra, c->z, true, 2, rb);     // alpha, r, ||r||, z = M^{-1} r, beta
+  launch_pcg_p(c, rhs0, nr, 1);                           // u += alpha p, p = z + beta p
 }
 
 
@@ -661,7 +679,7 @@ static int dist_coarse(const Ranks& cs, int rhs0, int nr) {
   for (msf_ctx* c : cs) {
     launch_nd_solve_top(c, rhs0, nr, true);
     launch_nd_solve_local_back(c, rhs0, nr, true);
-    launch_prolong(c, rhs0, nr, c->z, true);
+    launch_prolong(c, rhs0, nr, c->z, c->z, true);
   }
   if (cs[0]->nranks > 1) return dist_halo(cs, &msf_ctx::z, rhs0, nr);
   return MSF_OK;
@@ -709,14 +727,14 @@ static int dist_iteration(const Ranks& cs, int rhs0, int nr) {
   if ((rc = dist_reduce(cs, FIN_RR, rhs0, nr, true, 0))) return rc;
   if ((rc = dist_halo(cs, &msf_ctx::z, rhs0, nr))) return rc;
   if ((rc = dist_vcycle(cs, rhs0, nr, true, 2))) return rc;
-  for (msf_ctx* c : cs) launch_pcg_p(c, rhs0, nr, false);
+  for (msf_ctx* c : cs) launch_pcg_p(c, rhs0, nr, 2);
   return MSF_OK;
 }
 
 // graph of one strip-partition iteration for realisations [rhs0, rhs0 + nr) (kernels + NCCL)
 static int dist_range_graph(const Ranks& cs, int rhs0, int nr, cudaGraphExec_t* out) {
   msf_ctx* c = cs[0];
-  cudaGraphExec_t& slot = c->range_graph[rhs0][nr];
+  cudaGraphExec_t& slot = c->range_graph[0][rhs0][nr];
   if (!slot) {
     cudaGraph_t g;
     cudaStream_t user = c->stream;
@@ -753,7 +771,7 @@ static int dist_pcg_solve(const Ranks& cs, int nr, double tol, int max_it, int32
   for (msf_ctx* x : cs) launch_pcg_init(x, nr, tol, max_it);
   if ((rc = dist_reduce(cs, FIN_F, 0, nr, false, 0))) return rc;
   if ((rc = dist_vcycle(cs, 0, nr, false, 1))) return rc;
-  for (msf_ctx* x : cs) launch_pcg_p(x, 0, nr, true);
+  for (msf_ctx* x : cs) launch_pcg_p(x, 0, nr, 0);
   CKL("dist pcg init");
   // one process per GPU: each active range's iteration (kernels + NCCL) is a CUDA graph; the
   // active flags derive from all-reduced sums, so every rank narrows the range identically
@@ -829,10 +847,11 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
   const long long l0 = c->launches;
   launch_pcg_init(c, nr, tol, max_it);
   enqueue_vcycle(c, 0, nr, c->r, c->z, true, 1);
-  launch_pcg_p(c, 0, nr, true);
+  launch_pcg_p(c, 0, nr, 0);
   CKL("pcg init");
   int rc = run_graph_iterations(c, nr, max_it);
   if (rc) return rc;
+  launch_pcg_p(c, 0, nr, 3);   // the converging iteration's u += alpha p
   launch_compliance(c, nr);
   CKL("compliance");
   rc = read_scalars(c, nr);
@@ -854,15 +873,15 @@ int msf_pcg_solve(msf_ctx* c, int n_rhs, double tol, int max_it, double* u, int3
 // Graph of one PCG iteration for the realisations [rhs0, rhs0 + nr), captured on first use
 // on a private stream (the caller's may be the legacy stream, which cannot be captured) and
 // launched on the caller's stream.
-static int range_graph(msf_ctx* c, int rhs0, int nr, cudaGraphExec_t* out) {
-  cudaGraphExec_t& slot = c->range_graph[rhs0][nr];
+static int range_graph(msf_ctx* c, int rhs0, int nr, int parity, cudaGraphExec_t* out) {
+  cudaGraphExec_t& slot = c->range_graph[parity][rhs0][nr];
   if (!slot) {
     cudaGraph_t g;
     cudaStream_t user = c->stream;
     c->stream = c->cap_stream;
     cudaError_t e1 = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
     const long long before = c->launches;
-    if (e1 == cudaSuccess) enqueue_iteration(c, rhs0, nr);
+    if (e1 == cudaSuccess) enqueue_iteration(c, rhs0, nr, parity);
     c->pcg_launches = c->launches - before;
     c->launches = before;
     cudaError_t e2 = e1 == cudaSuccess ? cudaStreamEndCapture(c->stream, &g) : e1;
@@ -884,13 +903,16 @@ static int run_graph_iterations(msf_ctx* c, int nr, int max_it) {
   int lo = 0, hi = nr;
   const int check_every = 8;
   for (int it = 0; it < max_it + check_every; it += check_every) {
-    cudaGraphExec_t g = nullptr;
-    int rc = range_graph(c, lo, hi - lo, &g);
-    if (rc) return rc;
-    for (int j = 0; j < check_every; ++j) {
-      CK(cudaGraphLaunch(g, c->stream));
+    cudaGraphExec_t g[2] = {nullptr, nullptr};
+    for (int par = 0; par < 2; ++par) {
+      int rc = range_graph(c, lo, hi - lo, par, &g[par]);
+      if (rc) return rc;
+    }
+    for (int j = 0; j < check_every; ++j) {   // check_every even: iteration it + j has parity j
+      CK(cudaGraphLaunch(g[j & 1], c->stream));
       c->launches += c->pcg_launches;
     }
+    int rc;
     rc = read_scalars(c, nr);
     if (rc) return rc;
     lo = nr;
@@ -1105,19 +1127,28 @@ int msf_precond_apply(msf_ctx* c, int rhs, const double* r, double* z) {
   return MSF_OK;
 }
 
-int msf_sgs(msf_ctx* c, int rhs, const double* r, double* z) {
+int msf_sgs_ex(msf_ctx* c, int rhs, const double* r, double* z, int flags) {
   if (!c || !r || !z) return msf_fail(c, MSF_ERR_ARG, "null argument");
   if (c->comm) return msf_fail(c, MSF_ERR_STATE, "sgs: not available on a strip context");
   if (!c->have_E) return msf_fail(c, MSF_ERR_STATE, "sgs before filter_project");
   if (rhs < 0 || rhs >= c->d.R) return msf_fail(c, MSF_ERR_ARG, "rhs out of range");
+  if (flags & ~3) return msf_fail(c, MSF_ERR_ARG, "sgs_ex: unknown flags");
+  const bool zero = flags & 1, phases = flags & 2;
   const size_t off = (size_t)rhs * 2 * c->dl.nn;
   launch_mask_copy(c, r, c->r + off, c->dl.nn);
-  launch_mask_copy(c, z, c->z + off, c->dl.nn);
-  launch_sgs(c, rhs, 1, c->r, c->z, false);
+  if (phases) {
+    if (!zero) launch_mask_copy(c, z, c->z + off, c->dl.nn);
+    launch_sgs_sweep(c, rhs, 1, c->r, c->z, false, zero, 0, false);
+  } else {
+    if (!zero) launch_mask_copy(c, z, c->t + off, c->dl.nn);
+    launch_sgs_stream(c, rhs, 1, c->r, nullptr, c->t, c->z, false, zero, false, 0);
+  }
   CK(cudaMemcpyAsync(z, c->z + off, (size_t)2 * c->dl.nn * 8, cudaMemcpyDeviceToDevice, c->stream));
   CKL("sgs");
   return MSF_OK;
 }
+
+int msf_sgs(msf_ctx* c, int rhs, const double* r, double* z) { return msf_sgs_ex(c, rhs, r, z, 0); }
 
 int msf_coarse_solve(msf_ctx* c, int rhs, const double* b, double* x) {
   if (!c || !b || !x) return msf_fail(c, MSF_ERR_ARG, "null argument");
@@ -1220,15 +1251,16 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   const double nn = c->dl.nn, ne = (double)c->dl.nelx * c->dl.nely;
   // algorithmic bytes per launch: every operand touched once
   bytes[0] = R * (nn * 16 + ne * 8 + nn * 16) + nn;                  // p, E -> q
-  bytes[1] = 7 * (R * (ne * 8 + nn * 16 + nn / 4 * 16 * 2) + nn / 4);  // 7 colour launches
+  bytes[1] = R * (ne * 8 + nn * 16 * 3) + nn;                       // E, z, r -> z (one sweep)
   bytes[2] = R * nn * 16 + (double)c->n_cls * d.kmax * d.box_nodes * 16 + R * (double)d.n_agg * d.kmax * 8;
   bytes[3] = R * (double)c->nd.solve_bytes;                          // fronts, forward + back
   bytes[4] = R * (nn * 32) + (double)c->n_cls * d.kmax * d.box_nodes * 16 + R * (double)d.n_agg * d.kmax * 8;
   bytes[5] = R * (nn * 16 * 3 + ne * 8) + nn;                        // z, r, E -> t
-  bytes[6] = 2 * bytes[1] + bytes[2] + bytes[3] + bytes[4] + bytes[5];
-  bytes[7] = bytes[0] + bytes[6] + R * nn * 16 * 6 + R * nn * 16 * 2 + R * nn * 16 * 3;
-  bytes[8] = R * (nn * 16 * 6 + ne * 8 + nn / 4 * 16 * 2) + nn / 4;    // p q u r -> u r, F0
-  bytes[9] = R * nn * 16 * 3;                                          // z, p -> p
+  bytes[8] = R * (ne * 8 + nn * 16 * 4) + nn;                        // E, r, q -> r, z (pre-sweep)
+  bytes[9] = R * nn * 16 * 5;                                          // z, p, u -> p, u
+  // V-cycle from r (pre-sweep E, r -> z); PCG iteration (pre-sweep with the r update)
+  bytes[6] = R * (ne * 8 + nn * 32) + nn + bytes[1] + bytes[2] + bytes[3] + bytes[4] + bytes[5];
+  bytes[7] = bytes[0] + bytes[8] + bytes[1] + bytes[2] + bytes[3] + bytes[4] + bytes[5] + bytes[9];
   // coarse phases: this rank's box fronts (forward / back), the interface fronts; assembly
   // entries carry no byte count
   {
@@ -1259,7 +1291,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   CK(cudaMemcpyAsync(c->sc, act.data(), R * sizeof(PcgScalars), cudaMemcpyHostToDevice, c->stream));
   cudaGraphExec_t gR = nullptr;
   if (!c->comm) {
-    int rc = range_graph(c, 0, R, &gR);
+    int rc = range_graph(c, 0, R, 0, &gR);
     if (rc) return rc;
   }
   cudaEvent_t e0, e1;
@@ -1268,15 +1300,15 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   auto run = [&](int which) {
     switch (which) {
       case 0: launch_matvec(c, 0, R, c->pv, c->q, false, true); break;
-      case 1: launch_sgs(c, 0, R, c->r, c->z, false); break;
+      case 1: launch_sgs_stream(c, 0, R, c->r, nullptr, c->t, c->z, false, false, false, 0); break;
       case 2: launch_restrict(c, 0, R, c->t, false); break;
       case 3: launch_nd_solve(c, 0, R, false); break;
-      case 4: launch_prolong(c, 0, R, c->z, false); break;
+      case 4: launch_prolong(c, 0, R, c->z, c->t, false); break;
       case 5: launch_residual(c, 0, R, c->r, c->z, c->t, false); break;
       case 6: enqueue_vcycle(c, 0, R, c->r, c->z, false); break;
       case 7: if (gR) cudaGraphLaunch(gR, c->stream); break;
-      case 8: launch_update_f0(c, 0, R); break;
-      case 9: launch_pcg_p(c, 0, R, false); break;
+      case 8: launch_sgs_stream(c, 0, R, c->r, c->r2, nullptr, c->z, false, true, true, 0); break;
+      case 9: launch_pcg_p(c, 0, R, 1); break;
       case 10:   // K_c assembly: Galerkin cell products + the factorisation (a strip: its part)
         launch_galerkin_cells(c);
         launch_nd_factor_local(c);

@@ -233,11 +233,13 @@ __global__ void __launch_bounds__(256, MSF_RB_MINB) k_restrict_batch(Dims d, con
 }
 
 // ------------------------------------------------------------------ per-realisation prolongation
-// z(n) += sum_{I,J,a} phi_{I,J,a}(n) x_c[slot(I,J,a)], one (node, realisation) per thread.
+// zout(n) = zin(n) + sum_{I,J,a} phi_{I,J,a}(n) x_c[slot(I,J,a)], one (node, realisation) per
+// thread (zout == zin: in place).
 template <int KM>
 __global__ void __launch_bounds__(NT) k_prolong1(Dims d, const double* __restrict__ phi,
                                                  const int* __restrict__ cls_of_agg,
-                                                 const double* __restrict__ cxall, double2* zall,
+                                                 const double* __restrict__ cxall,
+                                                 const double2* zin, double2* zall,
                                                  const PcgScalars* sc, int rhs0, int gated) {
   pdl_launch();
   pdl_wait();
@@ -273,11 +275,11 @@ __global__ void __launch_bounds__(NT) k_prolong1(Dims d, const double* __restric
       }
     }
   }
-  double2* z = zall + (size_t)rhs * d.nn + (size_t)ix * d.nny + iy;
-  double2 zv = *z;
+  const size_t n = (size_t)rhs * d.nn + (size_t)ix * d.nny + iy;
+  double2 zv = zin[n];
   zv.x += sx;
   zv.y += sy;
-  *z = zv;
+  zall[n] = zv;
 }
 
 // Prolongation for NR > 1 active realisations, one node per thread for all of them: the
@@ -288,7 +290,8 @@ __global__ void __launch_bounds__(NT) k_prolong1(Dims d, const double* __restric
 template <int KM, int NR>
 __global__ void __launch_bounds__(NT) k_prolong_nr(Dims d, const double* __restrict__ phi,
                                                    const int* __restrict__ cls_of_agg,
-                                                   const double* __restrict__ cxall, double2* zall,
+                                                   const double* __restrict__ cxall,
+                                                   const double2* zin, double2* zall,
                                                    const PcgScalars* sc, int rhs0, int gated) {
   pdl_launch();
   pdl_wait();
@@ -339,11 +342,11 @@ __global__ void __launch_bounds__(NT) k_prolong_nr(Dims d, const double* __restr
 #pragma unroll
   for (int k = 0; k < NR; ++k) {
     if (!act[k]) continue;
-    double2* z = zall + (size_t)(rhs0 + k) * d.nn + (size_t)ix * d.nny + iy;
-    double2 zv = *z;
+    const size_t n = (size_t)(rhs0 + k) * d.nn + (size_t)ix * d.nny + iy;
+    double2 zv = zin[n];
     zv.x += sx[k];
     zv.y += sy[k];
-    *z = zv;
+    zall[n] = zv;
   }
 }
 
@@ -592,13 +595,14 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
   MSF_LAUNCHED(c);
 }
 
-void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
+void launch_prolong(msf_ctx* c, int rhs0, int nr, const double* zin, double* z, bool gated) {
   const Dims& d = c->dl;   // every local node, halo included (identical increments on both ranks)
   dim3 g((d.nny + 31) / 32, (d.nnx + 7) / 8, 1);
   if (nr > 1 && nr <= 3 && d.kmax <= 8 && c->prolong_nr) {
 #define MSF_PROLONG_NR(KM, NR)                                                                    \
   launch_k(k_prolong_nr<KM, NR>, g, dim3(NT), 0, c->stream, d, (const double*)c->phi,              \
-           (const int*)c->cls_of_agg_d, (const double*)c->cx, (double2*)z, (const PcgScalars*)c->sc, \
+           (const int*)c->cls_of_agg_d, (const double*)c->cx, (const double2*)zin, (double2*)z,         \
+           (const PcgScalars*)c->sc,                                                              \
            rhs0, gated ? 1 : 0)
     if (d.kmax <= 4) {
       if (nr == 2) MSF_PROLONG_NR(4, 2);
@@ -613,7 +617,8 @@ void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated) {
   }
 #define MSF_PROLONG(KM)                                                                           \
   launch_k(k_prolong1<KM>, dim3(g.x, g.y, nr), dim3(NT), 0, c->stream, d, (const double*)c->phi,    \
-           (const int*)c->cls_of_agg_d, (const double*)c->cx, (double2*)z, (const PcgScalars*)c->sc, \
+           (const int*)c->cls_of_agg_d, (const double*)c->cx, (const double2*)zin, (double2*)z,         \
+           (const PcgScalars*)c->sc,                                                              \
            rhs0, gated ? 1 : 0)
   if (d.kmax <= 4) MSF_PROLONG(4);
   else if (d.kmax <= 8) MSF_PROLONG(8);

@@ -1,6 +1,6 @@
-// Matrix-free Q4 stiffness operator, multicolour symmetric Gauss-Seidel and the PCG vector
-// kernels of the B200 MsFEM path (single-purpose kernels; the persistent PCG kernel in
-// msf_persist.cu runs the same device functions from msf_kern.cuh).
+// Matrix-free Q4 stiffness operator, multicolour symmetric Gauss-Seidel phases and the PCG
+// vector kernels of the B200 MsFEM path (the streaming sweep of msf_sgs.cu runs the same
+// Gauss-Seidel node arithmetic, msfk::gs_node).
 //
 //   * y = P K(xbar) P x  with  K = sum_e (Emin + xbar_e^p (E0-Emin)) K0   (Eq. 4-5,
 //     lines 73/84; reading R2: Dirichlet DOFs eliminated).  Node-centric gather: each thread
@@ -26,76 +26,6 @@ using namespace msfk;
 namespace {
 
 constexpr int NTHR = TILE_THREADS;
-
-// Writes this block's partial, returns true in the last block to arrive.
-__device__ bool arrive_last(double v, double* partials, int slot, unsigned* counter,
-                            unsigned total, int tid) {
-  __shared__ unsigned s_ticket;
-  if (tid == 0) {
-    partials[slot] = v;
-    __threadfence();
-    s_ticket = atomicAdd(counter, 1u);
-  }
-  __syncthreads();
-  return s_ticket == total - 1;
-}
-
-// In the last block: deterministic sum of partials[0..n).  Eight independent loads per
-// thread are in flight at once (the last block is the serial tail of every PCG reduction).
-__device__ double reduce_partials(const double* partials, int n, double* sm, int tid,
-                                  int nthreads) {
-  double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  int i = tid;
-  for (; i + 7 * nthreads < n; i += 8 * nthreads) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s[j] += __ldcg(partials + i + j * nthreads);
-  }
-  for (int j = 0; i < n; i += nthreads, ++j) s[j & 7] += __ldcg(partials + i);
-  const double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
-  return block_sum_all(t, sm, tid, nthreads);
-}
-
-// PCG scalar update from a completed (global) dot product (reading R9)
-__device__ __forceinline__ void fin_scalar(PcgScalars& S, int kind, double tot, int rz_mode) {
-  switch (kind) {
-    case FIN_PQ:
-      S.pq = tot;
-      S.alpha = S.rz / tot;
-      break;
-    case FIN_RR:
-      S.rr = tot;
-      S.iters += 1;
-      if (tot <= S.tol2 * S.fnorm2) {
-        S.active = 0;
-      } else if (S.iters >= S.max_it) {
-        S.active = 0;
-        S.noconv = 1;
-      }
-      break;
-    case FIN_RZ:
-      S.beta = (rz_mode == 1) ? 0.0 : tot / S.rz;
-      S.rz = tot;
-      break;
-    case FIN_F:
-      S.fnorm2 = tot;
-      S.rr = tot;
-      S.active = (tot > 0.0 && !(tot <= S.tol2 * tot)) ? 1 : 0;
-      break;
-    default:
-      S.comp = tot;
-      break;
-  }
-}
-
-// last block of a reduction: finalise in place (one GPU) or park the local sum for the
-// cross-rank all-reduce (strip partition, dsum != null)
-__device__ __forceinline__ void fin_or_park(PcgScalars* sc, double* dsum, int rhs, int kind,
-                                            double tot, int rz_mode) {
-  if (dsum)
-    dsum[kind * MSF_MAX_RHS + rhs] = tot;
-  else
-    fin_scalar(sc[rhs], kind, tot, rz_mode);
-}
 
 // ------------------------------------------------------------------ operator apply
 // MODE 0: y = P K P x ; MODE 1: y = b - P K P x.  dot: accumulate x.y (p.Ap) and set
@@ -700,23 +630,37 @@ __global__ void k_finalize(PcgScalars* sc, const double* __restrict__ dsum, int 
   fin_scalar(sc[rhs], kind, dsum[kind * MSF_MAX_RHS + rhs], rz_mode);
 }
 
-// p = z + beta p  (p = z at init)
+// PCG direction update (reading R9).  mode 0: p = z (init); 1: u += alpha p, then
+// p = z + beta p (the solution update of the iteration, deferred to here so that it reads
+// the p it needs once); 2: p = z + beta p (strip partition: u was updated by k_update_f0);
+// 3: u += alpha p for every realisation, ungated (after the last iteration: the iteration
+// that converged skipped mode 1).
 __global__ void __launch_bounds__(VB) k_pcg_p(Dims d, const double2* __restrict__ zall,
-                                              double2* pall, const PcgScalars* sc, int init,
-                                              int rhs0) {
+                                              double2* pall, double2* uall, const PcgScalars* sc,
+                                              int mode, int rhs0) {
   pdl_launch();
   pdl_wait();
   const int rhs = rhs0 + blockIdx.z;
-  if (!sc[rhs].active) return;
-  const double beta = init ? 0.0 : sc[rhs].beta;
+  if (mode != 3 && !sc[rhs].active) return;
+  const double beta = mode == 0 ? 0.0 : sc[rhs].beta;
+  const double alpha = sc[rhs].alpha;
   const double2* z = zall + (size_t)rhs * d.nn;
   double2* p = pall + (size_t)rhs * d.nn;
+  double2* u = uall + (size_t)rhs * d.nn;
   for (int i = blockIdx.x * VB + threadIdx.x; i < d.nn; i += gridDim.x * VB) {
-    const double2 zv = z[i];
-    double2 pv = init ? make_double2(0.0, 0.0) : p[i];
-    pv.x = fma(beta, pv.x, zv.x);
-    pv.y = fma(beta, pv.y, zv.y);
-    p[i] = pv;
+    double2 pv = mode == 0 ? make_double2(0.0, 0.0) : p[i];
+    if (mode == 1 || mode == 3) {
+      double2 uv = u[i];
+      uv.x = fma(alpha, pv.x, uv.x);
+      uv.y = fma(alpha, pv.y, uv.y);
+      u[i] = uv;
+    }
+    if (mode != 3) {
+      const double2 zv = z[i];
+      pv.x = fma(beta, pv.x, zv.x);
+      pv.y = fma(beta, pv.y, zv.y);
+      p[i] = pv;
+    }
   }
 }
 
@@ -1022,10 +966,10 @@ void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it) {
   MSF_LAUNCHED(c);
 }
 
-void launch_pcg_p(msf_ctx* c, int rhs0, int nr, bool init) {
+void launch_pcg_p(msf_ctx* c, int rhs0, int nr, int mode) {
   launch_k(k_pcg_p, dim3(vec_blocks(c->dl), 1, nr), dim3(VB), 0, c->stream,
-           c->dl, (const double2*)c->z, (double2*)c->pv, (const PcgScalars*)c->sc, init ? 1 : 0,
-           rhs0);
+           c->dl, (const double2*)c->z, (double2*)c->pv, (double2*)c->u, (const PcgScalars*)c->sc,
+           mode, rhs0);
   MSF_LAUNCHED(c);
 }
 

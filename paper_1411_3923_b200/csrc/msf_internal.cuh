@@ -187,6 +187,8 @@ struct msf_ctx {
   uint8_t* fixn = nullptr;      // per-node bitmask: bit0 x fixed, bit1 y fixed (this rank's strip;
                                 // halo / padding columns = 3)
   uint8_t* fixg = nullptr;      // the same for the whole grid (local eigenproblems)
+  uint8_t* fixs = nullptr;      // fixn in the streaming sweep's planar padded layout (msf_sgs.cu)
+  int fs_col = 0, fs_plane = 0;
   double* f = nullptr;          // load [2*nn]
   double* x_tile = nullptr;     // design [nt]
   double* xt_tile = nullptr;    // filtered [nt]
@@ -194,6 +196,7 @@ struct msf_ctx {
   double* E = nullptr;          // element moduli [R*ne]
   double* u = nullptr;          // solutions [R*2nn]
   double* r = nullptr;
+  double* r2 = nullptr;         // second residual buffer (odd PCG iterations, one GPU)
   double* z = nullptr;
   double* pv = nullptr;
   double* q = nullptr;
@@ -265,7 +268,9 @@ struct msf_ctx {
   int iter_graph_R = -1;
   // one graph per contiguous active realisation range [rhs0, rhs0 + nr): converged
   // realisations drop out of the launch grids instead of exiting from every CTA
-  cudaGraphExec_t range_graph[MSF_MAX_RHS][MSF_MAX_RHS + 1] = {};
+  // [parity]: the PCG residual alternates between r and r2 (the pre-smoothing writes the
+  // updated residual out of place), so even and odd iterations are two graphs
+  cudaGraphExec_t range_graph[2][MSF_MAX_RHS][MSF_MAX_RHS + 1] = {};
 };
 int restrict_groups(const Dims& d, const std::vector<int>& work, const std::vector<int>& cls,
                     int B, std::vector<int>& groups);
@@ -311,7 +316,21 @@ void launch_finalize(msf_ctx* c, int kind, int rhs0, int nr, bool gated, int rz_
 void launch_update_f0(msf_ctx* c, int rhs0, int nr);
 void launch_mask_copy(msf_ctx* c, const double* x, double* y, int n2nn);
 void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it);
-void launch_pcg_p(msf_ctx* c, int rhs0, int nr, bool init);
+// mode 0: p = z (init); 1: u += alpha p, p = z + beta p; 2: p = z + beta p; 3: u += alpha p
+// (all realisations, after the last iteration)
+void launch_pcg_p(msf_ctx* c, int rhs0, int nr, int mode);
+// streaming symmetric Gauss-Seidel sweep (msf_sgs.cu): z = SGS(z; r), zero_start: from z = 0;
+// upd: r -= alpha q first (alpha from the operator's partials, ||r||^2 -> convergence);
+// rz_mode != 0: r.z -> beta
+// zin: the starting iterate (not read when zero_start; must differ from z: other CTAs read
+// their halo of it while this one writes)
+// upd: the updated residual goes to rout (r is read only)
+void launch_sgs_stream(msf_ctx* c, int rhs0, int nr, const double* r, double* rout,
+                       const double* zin, double* z, bool gated, bool zero_start, bool upd,
+                       int rz_mode);
+void sgs_fix_layout(const Dims& d, int& fs_col, int& fs_plane);
+void sgs_fix_build(const Dims& d, const uint8_t* fixn, std::vector<uint8_t>& out);
+int sgs_stream_partials_needed(const Dims& d);
 void launch_compliance(msf_ctx* c, int nr);
 
 // ---------------------------------------------------------------- filter / design
@@ -330,7 +349,8 @@ void launch_build_basis(msf_ctx* c);
 // K_c assembly (Galerkin cell products) + nested-dissection factorisation, one GPU
 void launch_assemble_coarse(msf_ctx* c);
 void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated);
-void launch_prolong(msf_ctx* c, int rhs0, int nr, double* z, bool gated);
+// z = zin + R^T c (zin == z: in place)
+void launch_prolong(msf_ctx* c, int rhs0, int nr, const double* zin, double* z, bool gated);
 constexpr int MSF_BENCH_ENTRIES = 15;   // msf_bench_kernels
 
 // nested dissection (msf_nd.cu)

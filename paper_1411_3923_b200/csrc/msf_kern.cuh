@@ -1,6 +1,5 @@
-// Device-side building blocks of the B200 MsFEM-PCG path, shared by the single-purpose
-// kernels (msf_fem.cu, msf_coarse.cu) and the persistent PCG kernel (msf_persist.cu) so
-// that both execute the same arithmetic.  All functions are called by a whole CTA unless
+// Device-side building blocks of the B200 MsFEM-PCG path, shared by the kernels of
+// msf_fem.cu, msf_sgs.cu and msf_coarse.cu so that they execute the same arithmetic.  All functions are called by a whole CTA unless
 // stated otherwise.
 #pragma once
 
@@ -36,6 +35,23 @@ __device__ __forceinline__ constexpr int a_of(int sx, int sy) {
 __device__ __forceinline__ constexpr int DXB(int b) { return (b == 1 || b == 2) ? 1 : 0; }
 __device__ __forceinline__ constexpr int DYB(int b) { return (b >= 2) ? 1 : 0; }
 
+// make_K0's element matrix has 8 distinct entries: K0[i][j] = K0[0][K0_IDX(i, j)] (the index
+// table of the closed form, msf_fem.cu make_K0).  The stencil loops read K0 through this table,
+// so only K.v[0..7] are live (8 uniform register pairs instead of up to 64: sm_100 keeps the
+// DFMA constant operands of a kernel parameter in uniform registers, and 64 of them spilled).
+// The values are the same entries, so the arithmetic is bitwise unchanged.
+__device__ __forceinline__ constexpr int K0_IDX(int i, int j) {
+  return (i == 0)   ? j
+         : (i == 1) ? (j == 0 ? 1 : j == 1 ? 0 : 9 - j)
+         : (i == 2) ? (j == 0 ? 2 : j == 1 ? 7 : j == 2 ? 0 : j == 3 ? 5 : j == 4 ? 6 : j == 5 ? 3 : j == 6 ? 4 : 1)
+         : (i == 3) ? (j == 0 ? 3 : j == 1 ? 6 : j == 2 ? 5 : j == 3 ? 0 : j == 4 ? 7 : j == 5 ? 2 : j == 6 ? 1 : 4)
+         : (i == 4) ? (j < 4 ? j + 4 : j - 4)
+         : (i == 5) ? (j == 0 ? 5 : j == 1 ? 4 : j == 2 ? 3 : j == 3 ? 2 : j == 4 ? 1 : j == 5 ? 0 : j == 6 ? 7 : 6)
+         : (i == 6) ? (j == 0 ? 6 : j == 1 ? 3 : j == 2 ? 4 : j == 3 ? 1 : j == 4 ? 2 : j == 5 ? 7 : j == 6 ? 0 : 5)
+                    : (j == 0 ? 7 : j == 1 ? 2 : j == 2 ? 1 : j == 3 ? 4 : j == 4 ? 3 : j == 5 ? 6 : j == 6 ? 5 : 0);
+}
+#define MSF_K0(K, i, j) ((K).v[K0_IDX((i), (j))])
+
 // (K z)_node and the node's own 2x2 diagonal block from the 4 element moduli E[sx][sy]
 // and the 3x3 neighbourhood z[i][j] = node (ix-1+i, iy-1+j)  (Eq. 4-5).
 // SYM: the pivot block's lower row is taken from its upper one (make_K0: K0 is bitwise
@@ -55,19 +71,19 @@ __device__ __forceinline__ void apply_node(const K0Mat& K, const double (&E)[2][
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const double2 v = z[sx + DXB(b)][sy + DYB(b)];
-        ax = fma(K.v[(2 * a) * 8 + 2 * b], v.x, ax);
-        ax = fma(K.v[(2 * a) * 8 + 2 * b + 1], v.y, ax);
-        ay = fma(K.v[(2 * a + 1) * 8 + 2 * b], v.x, ay);
-        ay = fma(K.v[(2 * a + 1) * 8 + 2 * b + 1], v.y, ay);
+        ax = fma(MSF_K0(K, 2 * a, 2 * b), v.x, ax);
+        ax = fma(MSF_K0(K, 2 * a, 2 * b + 1), v.y, ax);
+        ay = fma(MSF_K0(K, 2 * a + 1, 2 * b), v.x, ay);
+        ay = fma(MSF_K0(K, 2 * a + 1, 2 * b + 1), v.y, ay);
       }
       const double e = E[sx][sy];
       ox = fma(e, ax, ox);
       oy = fma(e, ay, oy);
-      dxx = fma(e, K.v[(2 * a) * 8 + 2 * a], dxx);
-      dxy = fma(e, K.v[(2 * a) * 8 + 2 * a + 1], dxy);
+      dxx = fma(e, MSF_K0(K, 2 * a, 2 * a), dxx);
+      dxy = fma(e, MSF_K0(K, 2 * a, 2 * a + 1), dxy);
       if (!SYM) {
-        dyx = fma(e, K.v[(2 * a + 1) * 8 + 2 * a], dyx);
-        dyy = fma(e, K.v[(2 * a + 1) * 8 + 2 * a + 1], dyy);
+        dyx = fma(e, MSF_K0(K, 2 * a + 1, 2 * a), dyx);
+        dyy = fma(e, MSF_K0(K, 2 * a + 1, 2 * a + 1), dyy);
       }
     }
   if (SYM) {
@@ -88,8 +104,8 @@ __device__ __forceinline__ void diag_node(const K0Mat& K, const double (&E)[2][2
     for (int sy = 0; sy < 2; ++sy) {
       const int a = a_of(sx, sy);
       const double e = E[sx][sy];
-      dxx = fma(e, K.v[(2 * a) * 8 + 2 * a], dxx);
-      dxy = fma(e, K.v[(2 * a) * 8 + 2 * a + 1], dxy);
+      dxx = fma(e, MSF_K0(K, 2 * a, 2 * a), dxx);
+      dxy = fma(e, MSF_K0(K, 2 * a, 2 * a + 1), dxy);
     }
 }
 
@@ -117,6 +133,80 @@ __device__ __forceinline__ double block_sum_all(double v, double* sm, int tid, i
   __syncthreads();
   return s;
 }
+
+// ------------------------------------------------------------------ cross-CTA reductions
+// Every PCG reduction: block sums -> per-CTA partials -> the last CTA to arrive sums the
+// partials in a fixed order (deterministic) and finalises the PCG scalar.
+// Writes this block's partial, returns true in the last block to arrive.
+__device__ __forceinline__ bool arrive_last(double v, double* partials, int slot, unsigned* counter,
+                            unsigned total, int tid) {
+  __shared__ unsigned s_ticket;
+  if (tid == 0) {
+    partials[slot] = v;
+    __threadfence();
+    s_ticket = atomicAdd(counter, 1u);
+  }
+  __syncthreads();
+  return s_ticket == total - 1;
+}
+
+// In the last block: deterministic sum of partials[0..n).  Eight independent loads per
+// thread are in flight at once (the last block is the serial tail of every PCG reduction).
+__device__ __forceinline__ double reduce_partials(const double* partials, int n, double* sm, int tid,
+                                  int nthreads) {
+  double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int i = tid;
+  for (; i + 7 * nthreads < n; i += 8 * nthreads) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] += __ldcg(partials + i + j * nthreads);
+  }
+  for (int j = 0; i < n; i += nthreads, ++j) s[j & 7] += __ldcg(partials + i);
+  const double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  return block_sum_all(t, sm, tid, nthreads);
+}
+
+// PCG scalar update from a completed (global) dot product (reading R9)
+__device__ __forceinline__ void fin_scalar(PcgScalars& S, int kind, double tot, int rz_mode) {
+  switch (kind) {
+    case FIN_PQ:
+      S.pq = tot;
+      S.alpha = S.rz / tot;
+      break;
+    case FIN_RR:
+      S.rr = tot;
+      S.iters += 1;
+      if (tot <= S.tol2 * S.fnorm2) {
+        S.active = 0;
+      } else if (S.iters >= S.max_it) {
+        S.active = 0;
+        S.noconv = 1;
+      }
+      break;
+    case FIN_RZ:
+      S.beta = (rz_mode == 1) ? 0.0 : tot / S.rz;
+      S.rz = tot;
+      break;
+    case FIN_F:
+      S.fnorm2 = tot;
+      S.rr = tot;
+      S.active = (tot > 0.0 && !(tot <= S.tol2 * tot)) ? 1 : 0;
+      break;
+    default:
+      S.comp = tot;
+      break;
+  }
+}
+
+// last block of a reduction: finalise in place (one GPU) or park the local sum for the
+// cross-rank all-reduce (strip partition, dsum != null)
+__device__ __forceinline__ void fin_or_park(PcgScalars* sc, double* dsum, int rhs, int kind,
+                                            double tot, int rz_mode) {
+  if (dsum)
+    dsum[kind * MSF_MAX_RHS + rhs] = tot;
+  else
+    fin_scalar(sc[rhs], kind, tot, rz_mode);
+}
+
 
 // ------------------------------------------------------------------ operator tile
 // y = P K P x (MODE 0) or y = b - P K P x (MODE 1) on one 8x32-node tile (ix0, iy0) with a
@@ -182,11 +272,7 @@ __device__ __forceinline__ double apply_tile(const Dims& d, const K0Mat& K, cons
   return dv;
 }
 
-// ------------------------------------------------------------------ Gauss-Seidel quad
-// One colour phase (reading R7) for node quad (qx, qy): updates the quad's node of
-// `colour`.  FWD: x then y ; BWD: y then x ; both: the F3B3 phase.  ZERO: first forward
-// phase from z = 0 (writes zeros to the quad's other nodes).  Returns r.z over the whole
-// quad when RZ (after the final backward phase).  Per-thread.
+// ------------------------------------------------------------------ Gauss-Seidel
 // 1/x for the Gauss-Seidel pivots: the hardware approximation refined by two Newton steps
 __device__ __forceinline__ double rcp_nr(double x) {
   double y;
@@ -196,6 +282,67 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return y;
 }
 
+// One Gauss-Seidel node update (reading R7): the 2x2 block of the node is relaxed in place,
+// x then y (FWD), y then x (BWD), or both (the F3B3 phase).  Eloc / zloc: the 4 element moduli
+// and the 3x3 neighbourhood of the node (zloc[1][1] = its current value), rv its residual
+// entry, fm its Dirichlet bits.  ZERO: z = 0 around the node, only the pivot block is needed.
+// Shared by the colour-phase kernels and the streaming sweep (msf_sgs.cu), so both execute
+// the same arithmetic.  Per-thread.
+template <bool FWD, bool BWD, bool ZERO, bool SYM = true>
+__device__ __forceinline__ double2 gs_node(const K0Mat& K, const double (&Eloc)[2][2],
+                                         const double2 (&zloc)[3][3], double2 rv, uint8_t fm) {
+  double ox, oy, dxx, dxy, dyx, dyy;
+  if (ZERO && MSF_F0_DIAG) {
+    // z = 0 around the node: (K z) vanishes, only the pivot block is needed
+    ox = oy = 0.0;
+    diag_node(K, Eloc, dxx, dxy);
+    dyx = dxy;
+    dyy = dxx;
+  } else {
+    apply_node<SYM>(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
+  }
+  double2 zn = zloc[1][1];
+  double rx = rv.x - ox, ry = rv.y - oy;
+#if MSF_GS_RCP
+  // reciprocals of the pivots: off the dependent chain, <= 2 ulp from the quotient
+  const double ixx = rcp_nr(dxx), iyy = rcp_nr(dyy);
+#define MSF_DIVX(a) ((a) * ixx)
+#define MSF_DIVY(a) ((a) * iyy)
+#else
+#define MSF_DIVX(a) ((a) / dxx)
+#define MSF_DIVY(a) ((a) / dyy)
+#endif
+  if (FWD) {
+    if (!(fm & 1)) {
+      const double dz = MSF_DIVX(rx);
+      zn.x += dz;
+      ry -= dyx * dz;
+      rx -= dxx * dz;
+    }
+    if (!(fm & 2)) {
+      const double dz = MSF_DIVY(ry);
+      zn.y += dz;
+      rx -= dxy * dz;
+      ry -= dyy * dz;
+    }
+  }
+  if (BWD) {
+    if (!(fm & 2)) {
+      const double dz = MSF_DIVY(ry);
+      zn.y += dz;
+      rx -= dxy * dz;
+    }
+    if (!(fm & 1)) zn.x += MSF_DIVX(rx);
+#undef MSF_DIVX
+#undef MSF_DIVY
+  }
+  return zn;
+}
+
+// One colour phase (reading R7) for node quad (qx, qy): updates the quad's node of
+// `colour`.  FWD: x then y ; BWD: y then x ; both: the F3B3 phase.  ZERO: first forward
+// phase from z = 0 (writes zeros to the quad's other nodes).  Returns r.z over the whole
+// quad when RZ (after the final backward phase).  Per-thread.
 template <bool FWD, bool BWD, bool ZERO, bool RZ, bool SYM = true>
 __device__ __forceinline__ double sgs_quad(const Dims& d, const K0Mat& K, const double* __restrict__ E,
                                            const double2* __restrict__ r, double2* z,
@@ -229,54 +376,10 @@ __device__ __forceinline__ double sgs_quad(const Dims& d, const K0Mat& K, const 
                          ? z[(size_t)gx * d.nny + gy]
                          : make_double2(0.0, 0.0);
       }
-    double ox, oy, dxx, dxy, dyx, dyy;
-    if (ZERO && MSF_F0_DIAG) {
-      // z = 0 around the node: (K z) vanishes, only the pivot block is needed
-      ox = oy = 0.0;
-      diag_node(K, Eloc, dxx, dxy);
-      dyx = dxy;
-      dyy = dxx;
-    } else {
-      apply_node<SYM>(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
-    }
     const size_t n = (size_t)ix * d.nny + iy;
     const double2 rv = r[n];
     const uint8_t fm = fixn[n];
-    double2 zn = zloc[1][1];
-    double rx = rv.x - ox, ry = rv.y - oy;
-#if MSF_GS_RCP
-    // reciprocals of the pivots: off the dependent chain, <= 2 ulp from the quotient
-    const double ixx = rcp_nr(dxx), iyy = rcp_nr(dyy);
-#define MSF_DIVX(a) ((a) * ixx)
-#define MSF_DIVY(a) ((a) * iyy)
-#else
-#define MSF_DIVX(a) ((a) / dxx)
-#define MSF_DIVY(a) ((a) / dyy)
-#endif
-    if (FWD) {
-      if (!(fm & 1)) {
-        const double dz = MSF_DIVX(rx);
-        zn.x += dz;
-        ry -= dyx * dz;
-        rx -= dxx * dz;
-      }
-      if (!(fm & 2)) {
-        const double dz = MSF_DIVY(ry);
-        zn.y += dz;
-        rx -= dxy * dz;
-        ry -= dyy * dz;
-      }
-    }
-    if (BWD) {
-      if (!(fm & 2)) {
-        const double dz = MSF_DIVY(ry);
-        zn.y += dz;
-        rx -= dxy * dz;
-      }
-      if (!(fm & 1)) zn.x += MSF_DIVX(rx);
-#undef MSF_DIVX
-#undef MSF_DIVY
-    }
+    const double2 zn = gs_node<FWD, BWD, ZERO, SYM>(K, Eloc, zloc, rv, fm);
     z[n] = zn;
     if (RZ) dot = rv.x * zn.x + rv.y * zn.y;
   }

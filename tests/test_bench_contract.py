@@ -53,7 +53,7 @@ def test_our_arm_line():
     its = d["config"]["pcg_iters_per_step"]
     assert len(its) == 3 and its[0] > its[1] > its[2] > 0   # eroded > intermediate > dilated
     for tab in (d["kernels"], d["kernels_1rhs"]):
-        assert {"apply", "sgs_colour", "vcycle", "pcg_iteration"} <= set(tab)
+        assert {"apply", "sgs_sweep", "sgs_pre_update", "vcycle", "pcg_iteration"} <= set(tab)
     sw = d["contrast_sweep"]
     assert sw["workload"] == "c3_square_2048" and [r["Emin"] for r in sw["rows"]] == [1e-3, 1e-6, 1e-9]
     assert all(r["converged"] and r["dof_iter_per_s_pcg"] > 0 for r in sw["rows"])

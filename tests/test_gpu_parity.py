@@ -137,6 +137,56 @@ def test_symmetric_gauss_seidel(name):
     assert np.abs(host(z) - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
+# grids that span several 112-row bands and several column runs of the streaming sweep
+# (msf_sgs.cu), with ragged last bands / runs, both boundary conditions, several realisations
+SGS_SPECS = {
+    "bands_160x130": TMA_SPECS["tma_160x130"],
+    "bands_96x252_mbb": TMA_SPECS["tma_96x252_mbb"],
+    "bands_odd_96x133": TMA_SPECS["fallback_odd_nely_96x133"],
+    "bands_400x230": W.small_spec(nelx=400, nely=230, cx=10, cy=10, tile=(20, 10), rmin=1.5,
+                                  beta=4.0, etas=(0.6, 0.4), dilated=1, seed=36),
+}
+
+
+@pytest.mark.parametrize("zero", [False, True])
+@pytest.mark.parametrize("name", list(SGS_SPECS))
+def test_symmetric_gauss_seidel_bands(name, zero):
+    """The streaming sweep against the oracle's SGS (reading R7) on multi-band grids, from a
+    random z and from z = 0 (the pre-smoothing form)."""
+    spec = SGS_SPECS[name]
+    m, x = ctx_for(spec)
+    fx, f, K0, E, A, _ = oracle_setup(spec, x)
+    groups = msfem.gs_groups(spec.nelx, spec.nely, fx)
+    r, z0 = W.random_vectors(spec.n_dof, 2, seed=16)
+    r[fx == 1] = 0
+    z0[fx == 1] = 0
+    if zero:
+        z0[:] = 0
+    for k in range(spec.n_rhs):
+        z = dev(z0)
+        m.sgs(k, dev(r), z, zero_start=zero)
+        ref = msfem.symmetric_gauss_seidel(A[k], z0, r, groups)
+        assert np.abs(host(z) - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name", list(SGS_SPECS) + ["cant_16x8", "ragged_36x20"])
+def test_sgs_stream_bitwise_equals_colour_phases(name):
+    """The streaming sweep computes every node update with the colour-phase kernels'
+    arithmetic (msfk::gs_node) from the same inputs, so the two forms are bitwise equal."""
+    spec = SGS_SPECS.get(name) or SPECS[name]
+    m, x = ctx_for(spec)
+    fx = W.fixed_mask(spec)
+    r, z0 = W.random_vectors(spec.n_dof, 2, seed=17)
+    r[fx == 1] = 0
+    z0[fx == 1] = 0
+    for k in range(spec.n_rhs):
+        for zero in (False, True):
+            za, zb = dev(z0), dev(z0)
+            m.sgs(k, dev(r), za, zero_start=zero)
+            m.sgs(k, dev(r), zb, zero_start=zero, phases=True)
+            assert np.array_equal(host(za), host(zb)), (k, zero)
+
+
 def gpu_basis_matrix(m, spec):
     """Dense R_c rows (kept modes only) from the GPU's padded-box basis."""
     phi, nk, lam = m.get_basis()

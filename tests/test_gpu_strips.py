@@ -175,8 +175,10 @@ def test_strip_rejects_per_rank_solve_and_too_many_ranks():
 def test_nccl_transport_one_rank_equals_single_gpu():
     """The NCCL transport end to end on one GPU (libnccl loaded at run time, a 1-rank
     communicator, all-reduces captured in the per-iteration CUDA graph): a full design
-    iteration gives the single-GPU context's iterations, compliances and design exactly
-    (a 1-rank all-reduce is the identity; no halos)."""
+    iteration gives the single-GPU context's iterations, and its compliances and design to
+    the north-star compliance bar 1e-10 (a 1-rank all-reduce is the identity and there are no
+    halos, but the strip path runs the sweep as colour phases with their own dot-product
+    partials, the single-GPU path the streaming sweep: the sums differ in rounding)."""
     import paper_1411_3923_b200 as pkg
     spec = SPECS["robust_32x16"]
     x = W.design_tile(spec)
@@ -190,9 +192,9 @@ def test_nccl_transport_one_rank_equals_single_gpu():
     its_n, comp_n, F_n, g_n = mn.design_iteration(dev(x), xa, tol=1e-10)
     its_s, comp_s, F_s, g_s = ms.design_iteration(dev(x), xb, tol=1e-10)
     assert its_n == its_s
-    np.testing.assert_allclose(comp_n, comp_s, rtol=1e-13)
-    assert abs(F_n - F_s) <= 1e-13 * abs(F_s)
-    np.testing.assert_allclose(host(xa), host(xb), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(comp_n, comp_s, rtol=1e-10)
+    assert abs(F_n - F_s) <= 1e-10 * abs(F_s)
+    np.testing.assert_allclose(host(xa), host(xb), rtol=0, atol=1e-9)
     mn.close()
 
 
