@@ -25,7 +25,7 @@ using namespace msfk;
 
 namespace {
 
-constexpr int SG_T = 256;    // threads: 4 phase slots x 64 colour rows
+constexpr int SG_T = 128;    // threads: 4 phase-slot warps x 32 lanes, two colour rows per lane
 constexpr int SG_H = 128;    // buffered node rows per column (band + 8-row halos)
 constexpr int SG_HP = 64;    // ... per parity plane
 constexpr int SG_IN = 112;   // band rows: buffer rows [SG_LO, SG_LO + SG_IN)
@@ -60,19 +60,18 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// One node of phase (FWD, BWD, Z0) at ring slots (c-1, c, c+1), buffer row ly.
-template <bool FWD, bool BWD, bool Z0>
-__device__ __forceinline__ void sg_node(const K0Mat& K, SgRing& S, int sm, int s0, int sp, int ly) {
+// Two nodes (buffer rows ly0, ly1 of one column) of phase (FWD, BWD, Z0) at ring slots
+// (c-1, c, c+1), computed together so that their independent FMA chains interleave.  A node
+// whose DOFs are both fixed (or outside the grid) comes back unchanged from gs_node.
+template <bool Z0>
+__device__ __forceinline__ void sg_gather(const SgRing& S, int sm, int s0, int sp, int ly,
+                                          double (&Eloc)[2][2], double2 (&zloc)[3][3]) {
   const int pl = ly & 1, k = ly >> 1;
-  const uint8_t fm = S.f[s0][pl][k];
-  if (fm == 3) return;   // both DOFs fixed, or outside the grid: z stays
   const int pm = (ly - 1) & 1, km = (ly - 1) >> 1, pp = (ly + 1) & 1, kp = (ly + 1) >> 1;
-  double Eloc[2][2];
   Eloc[0][0] = S.e[sm][pm][km];
   Eloc[0][1] = S.e[sm][pl][k];
   Eloc[1][0] = S.e[s0][pm][km];
   Eloc[1][1] = S.e[s0][pl][k];
-  double2 zloc[3][3];
   if (Z0) {
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -89,7 +88,26 @@ __device__ __forceinline__ void sg_node(const K0Mat& K, SgRing& S, int sm, int s
     zloc[2][1] = S.z[sp][pl][k];
     zloc[2][2] = S.z[sp][pp][kp];
   }
-  S.z[s0][pl][k] = gs_node<FWD, BWD, Z0>(K, Eloc, zloc, S.r[s0][pl][k], fm);
+}
+
+template <bool FWD, bool BWD, bool Z0>
+__device__ __forceinline__ void sg_node2(const K0Mat& K, SgRing& S, int sm, int s0, int sp,
+                                         int ly0, int ly1, bool v0, bool v1) {
+  double E0[2][2], E1[2][2];
+  double2 z0[3][3], z1[3][3];
+  sg_gather<Z0>(S, sm, s0, sp, ly0, E0, z0);
+  sg_gather<Z0>(S, sm, s0, sp, ly1, E1, z1);
+  const double2 r0 = S.r[s0][ly0 & 1][ly0 >> 1], r1 = S.r[s0][ly1 & 1][ly1 >> 1];
+  const uint8_t f0 = S.f[s0][ly0 & 1][ly0 >> 1], f1 = S.f[s0][ly1 & 1][ly1 >> 1];
+#ifdef MSF_SGS_EXP_NOCOMPUTE   // A/B experiment: the sweep's data movement alone
+  const double2 n0 = make_double2(z0[1][1].x + E0[0][0] + r0.x + f0, z0[0][0].y + z0[2][2].y + E0[1][1] + E1[0][1]);
+  const double2 n1 = make_double2(z1[1][1].x + E1[0][0] + r1.x + f1, z1[0][0].y + z1[2][2].y + E1[1][1] + E0[1][0]);
+#else
+  const double2 n0 = gs_node<FWD, BWD, Z0>(K, E0, z0, r0, f0);
+  const double2 n1 = gs_node<FWD, BWD, Z0>(K, E1, z1, r1, f1);
+#endif
+  if (v0) S.z[s0][ly0 & 1][ly0 >> 1] = n0;
+  if (v1) S.z[s0][ly1 & 1][ly1 >> 1] = n1;
 }
 
 template <bool ZERO, bool UPD, bool RZ>
@@ -137,34 +155,29 @@ __global__ void __launch_bounds__(SG_T, 2)
   auto slot = [&](int c) { return (c - cs) % SG_NR; };
   // column c into its ring slot: z (or q), r, moduli, Dirichlet bits
   auto issue = [&](int c) {
+#ifdef MSF_SGS_EXP_NOLOAD   // A/B experiment: the sweep's arithmetic alone
+    return;
+#endif
     if (c > c_last) return;
-    const int sl = slot(c);
+    const int sl = slot(c), ly = tid, pl = ly & 1, k = ly >> 1;
     if (c < 0 || c >= d.nnx) {   // outside the grid: zero values, both DOFs fixed
-      if (tid < SG_H) {
-        const int pl = tid & 1, k = tid >> 1;
-        S.z[sl][pl][k] = make_double2(0.0, 0.0);
-        S.r[sl][pl][k] = make_double2(0.0, 0.0);
-        S.e[sl][pl][k] = 0.0;
-        S.f[sl][pl][k] = 3;
-      }
+      S.z[sl][pl][k] = make_double2(0.0, 0.0);
+      S.r[sl][pl][k] = make_double2(0.0, 0.0);
+      S.e[sl][pl][k] = 0.0;
+      S.f[sl][pl][k] = 3;
       return;
     }
-    if (tid < SG_H) {
-      const int ly = tid, gy = Yb + ly, pl = ly & 1, k = ly >> 1;
-      const bool v = gy >= 0 && gy < d.nny;
-      const size_t n = (size_t)c * d.nny + (v ? gy : 0);
-      if (!ZERO) cpa16(&S.z[sl][pl][k], zin + n, v);
-      else if (UPD) cpa16(&S.z[sl][pl][k], q + n, v);
-      const bool ve = gy >= 0 && gy < d.nely && c < d.nelx;
-      cpa8(&S.e[sl][pl][k], E + (ve ? (size_t)c * d.nely + gy : 0), ve);
-    } else {
-      const int ly = tid - SG_H, gy = Yb + ly, pl = ly & 1, k = ly >> 1;
-      const bool v = gy >= 0 && gy < d.nny;
-      cpa16(&S.r[sl][pl][k], r + (size_t)c * d.nny + (v ? gy : 0), v);
-      if (ly < 16) {   // 2 planes x 64 bytes of the planar padded mask (setup: fixs)
-        const int p2 = ly >> 3, ch = ly & 7;
-        cpa8(&S.f[sl][p2][ch * 8], fixs + (size_t)c * fs_col + p2 * fs_plane + (Y0 >> 1) + ch * 8, true);
-      }
+    const int gy = Yb + ly;
+    const bool v = gy >= 0 && gy < d.nny;
+    const size_t n = (size_t)c * d.nny + (v ? gy : 0);
+    if (!ZERO) cpa16(&S.z[sl][pl][k], zin + n, v);
+    else if (UPD) cpa16(&S.z[sl][pl][k], q + n, v);
+    cpa16(&S.r[sl][pl][k], r + n, v);
+    const bool ve = gy >= 0 && gy < d.nely && c < d.nelx;
+    cpa8(&S.e[sl][pl][k], E + (ve ? (size_t)c * d.nely + gy : 0), ve);
+    if (tid < 16) {   // 2 planes x 64 bytes of the planar padded mask (setup: fixs)
+      const int p2 = tid >> 3, ch = tid & 7;
+      cpa8(&S.f[sl][p2][ch * 8], fixs + (size_t)c * fs_col + p2 * fs_plane + (Y0 >> 1) + ch * 8, true);
     }
   };
 
@@ -178,7 +191,7 @@ __global__ void __launch_bounds__(SG_T, 2)
     __syncthreads();        // ... for every thread; step s - 1 is complete everywhere
     issue(s - 1 + SG_P);    // into the slot of column s - 16, last read at step s - 1
     cpa_commit();
-    if (ZERO && tid < SG_H) {
+    if (ZERO) {
       // column s - 1 becomes the sweep's input: z = 0 (UPD: r -= alpha q, q from z's slot)
       const int tc = s - 1;
       if (tc <= c_last) {
@@ -196,8 +209,8 @@ __global__ void __launch_bounds__(SG_T, 2)
     {
       // column s - 15 is final (phase 7 ran on it at step s - 1): band rows to global
       const int wc = s - 15;
-      const int i = tid - SG_H;
-      if (i >= 0 && i < SG_IN && wc >= X0 && wc < X1 && Y0 + i < d.nny) {
+      const int i = tid;
+      if (i < SG_IN && wc >= X0 && wc < X1 && Y0 + i < d.nny) {
         const int ly = SG_LO + i, sl = slot(wc), pl = ly & 1, k = ly >> 1;
         const size_t n = (size_t)wc * d.nny + (Y0 + i);
         const double2 zv = S.z[sl][pl][k];
@@ -214,22 +227,24 @@ __global__ void __launch_bounds__(SG_T, 2)
       }
     }
     {
-      // phases: even s -> F0, F2, B2, B0 (even columns), odd s -> F1, F3B3, B1 (odd columns)
-      const int ph = 2 * (tid >> 6) + 1 + (s & 1);
+      // phases: even s -> F0, F2, B2, B0 (even columns), odd s -> F1, F3B3, B1 (odd columns);
+      // warp w runs phase 2w + 1 (+1 on odd steps) on the colour rows lane and lane + 32
+      const int ph = 2 * (tid >> 5) + 1 + (s & 1);
       if (ph <= 7) {
         const int c = s - 2 * ph;
         if (c >= X0 - SG_DEP + ph && c < X1 + SG_DEP - ph && c >= 0 && c < d.nnx) {
           const int colour = (ph <= 4) ? ph - 1 : 7 - ph;
-          const int ly = 2 * (tid & 63) + (colour >> 1);
-          if (ly >= 1 + ph && ly < SG_H - 1 - ph) {
-            const int sm = slot(c - 1), s0 = slot(c), sp = slot(c + 1);
-            switch (ph) {
-              case 1: sg_node<true, false, ZERO>(K, S, sm, s0, sp, ly); break;
-              case 2:
-              case 3: sg_node<true, false, false>(K, S, sm, s0, sp, ly); break;
-              case 4: sg_node<true, true, false>(K, S, sm, s0, sp, ly); break;
-              default: sg_node<false, true, false>(K, S, sm, s0, sp, ly); break;
-            }
+          const int lyA = 2 * (tid & 31) + (colour >> 1), lyB = lyA + 64;
+          // rows outside [1 + ph, 127 - ph) are computed from a valid row and not stored
+          const bool vA = lyA >= 1 + ph, vB = lyB < SG_H - 1 - ph;
+          const int ly0 = vA ? lyA : lyA + 2 * ((2 + ph - lyA) / 2), ly1 = vB ? lyB : lyB - 2 * ((lyB - (SG_H - 2 - ph)) / 2 + 1);
+          const int s0 = slot(c), sm = s0 == 0 ? SG_NR - 1 : s0 - 1, sp = s0 == SG_NR - 1 ? 0 : s0 + 1;
+          switch (ph) {
+            case 1: sg_node2<true, false, ZERO>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
+            case 2:
+            case 3: sg_node2<true, false, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
+            case 4: sg_node2<true, true, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
+            default: sg_node2<false, true, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
           }
         }
       }

@@ -23,7 +23,7 @@ def main():
             objs.append(obj)
         out = os.path.join(out_dir, name + ".so")
         subprocess.check_call([B.NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-                               "-o", out, *objs, "-lcudart", "-lcublas", "-ldl"])
+                               "-o", out, *objs, "-lcudart", "-ldl"])
     print(out)
 
 
