@@ -232,7 +232,7 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   add((size_t)P.eig_doubles * 8);            // eig work
   add(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);     // Kcell
   add(2 * R * d.nbc * (size_t)d.mc * 8);     // cb, cx
-  add((size_t)d.n_agg * 4);                  // agg_by_cls
+  add(xfer_workspace_bytes(d));              // cell-class transfer plan + restriction partials
   add(nd_workspace_bytes(d, P.nd));
   add(2 * MSF_MAX_RHS * 4);                  // factor_status
   add(R * sizeof(PcgScalars));
@@ -395,34 +395,20 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     c->cell_lo = c->sb.C0;
     c->cell_hi = c->sb.C1;
   }
-  {
-    // restriction work list: agglomerates in grid order, so the four boxes that overlap on a
-    // node run close together and t is read from DRAM once (the class bases, a few MB, stay
-    // in L2 in any order; grouping by class made configs[4] read t four times: 812 MB vs
-    // 210 MB, profiles/r01_summary.md).  A strip keeps the agglomerates of its chain.
-    c->agg_by_cls_h.clear();
-    for (int a = 0; a < d.n_agg; ++a) {
-      const int I = a / (d.ncy + 1);
-      if (I >= c->cr_lo && I <= c->cr_hi) c->agg_by_cls_h.push_back(a);
-    }
-    c->n_restrict = (int)c->agg_by_cls_h.size();
-    c->agg_by_cls_d = (int*)take((size_t)d.n_agg * 4);
-  }
   c->nd = P.nd;
   if (nd_setup(c, cur) != cudaSuccess) {
     delete c;
     return msf_fail(nullptr, MSF_ERR_CUDA, "setup: nested-dissection plan upload");
   }
+  if (xfer_setup(c, cur) != 0) {
+    delete c;
+    return msf_fail(nullptr, MSF_ERR_CUDA, "setup: coarse-cell transfer plan (n_modes > 16 unsupported)");
+  }
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
-  if (const char* e = std::getenv("MSF_RESTRICT_THREADS")) c->restrict_threads = std::atoi(e);
   if (const char* e = std::getenv("MSF_APPLY_DIRECT")) c->apply_direct = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_APPLY_SW")) c->apply_sw = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_APPLY_TMA")) c->apply_tma = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_RESIDUAL_TMA")) c->residual_tma = std::string(e) != "0";
-  if (const char* e = std::getenv("MSF_RESTRICT_WARP")) {
-    c->restrict_warp = std::string(e) != "0";
-    c->restrict_warp_force = std::string(e) == "force";   // tests: every launch
-  }
   {
     const char* e = std::getenv("MSF_PDL");   // read at every setup (tests toggle it)
     g_msf_pdl = !(e && std::string(e) == "0");
@@ -473,7 +459,6 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_dy_d, P.fdy.data(), P.fdy.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->cls_of_agg_d, P.cls_of_agg.data(), d.n_agg * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->classes_d, P.classes.data(), c->n_cls * sizeof(EigClass), cudaMemcpyHostToDevice, c->stream);
-  if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->agg_by_cls_d, c->agg_by_cls_h.data(), c->agg_by_cls_h.size() * 4, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->factor_status, 0, 2 * MSF_MAX_RHS * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->counters, 0, R * 8 * 4, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->sc, 0, R * sizeof(PcgScalars), c->stream);
@@ -488,25 +473,6 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->sc_host, MSF_MAX_RHS * sizeof(PcgScalars));
   if (ce == cudaSuccess) ce = cudaMallocHost((void**)&c->scal_host, 80 * 8);
-  if (const char* e = std::getenv("MSF_PROLONG_NR")) c->prolong_nr = std::string(e) != "0";
-  {
-    // restriction groups of same-class agglomerates (k_restrict_batch), when they batch well
-    const char* e = std::getenv("MSF_RESTRICT_BATCH");
-    const int B = c->dl.kmax <= 4 ? 4 : c->dl.kmax <= 8 ? 2 : 0;
-    if (ce == cudaSuccess && B && !(e && std::string(e) == "0")) {
-      std::vector<int> groups;
-      const int ng = restrict_groups(c->dl, c->agg_by_cls_h, c->cls_of_agg, B, groups);
-      const bool force = e && std::string(e) == "force";   // tests: every launch, any fill
-      c->rgroup_force = force;
-      if (force || (long long)ng * B * 4 <= (long long)c->n_restrict * 5) {   // >= 80% filled
-        ce = cudaMalloc((void**)&c->rgroups_d, groups.size() * 4);
-        if (ce == cudaSuccess)
-          ce = cudaMemcpy(c->rgroups_d, groups.data(), groups.size() * 4, cudaMemcpyHostToDevice);
-        c->n_rgroups = ng;
-        c->rgroup_B = B;
-      }
-    }
-  }
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
   if (ce != cudaSuccess) {
     std::string m = std::string("setup: ") + cudaGetErrorString(ce);
@@ -534,7 +500,6 @@ int msf_destroy(msf_ctx* c) {
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->sc_host) cudaFreeHost(c->sc_host);
   if (c->scal_host) cudaFreeHost(c->scal_host);
-  if (c->rgroups_d) cudaFree(c->rgroups_d);
   delete c;
   return MSF_OK;
 }

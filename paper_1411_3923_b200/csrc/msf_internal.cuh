@@ -147,7 +147,6 @@ struct msf_ctx {
   msf_comm* comm = nullptr;   // null: single GPU
   double* E_loc = nullptr;    // E + first local element column (stride dl.estride)
   double* dsum = nullptr;     // [FIN_KINDS][MSF_MAX_RHS] local sums (strip partition only)
-  int n_restrict = 0;         // agglomerates restricted by this rank (agg_by_cls_d prefix)
   K0Mat K0{};
   cudaStream_t stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream used only to capture graphs
@@ -221,19 +220,13 @@ struct msf_ctx {
   double* Kcell = nullptr;      // [R][ncells][(4k)^2]
   double* cb = nullptr;         // [R][nbc*mc] coarse rhs
   double* cx = nullptr;         // [R][nbc*mc] coarse solution
-  int* agg_by_cls_d = nullptr;  // restriction work list (agglomerates in grid order)
-  bool restrict_warp = true;    // restriction one warp per agglomerate (env MSF_RESTRICT_WARP=0)
-  bool restrict_warp_force = false;   // ... on every launch (env MSF_RESTRICT_WARP=force; tests)
-  // restriction one warp per group of same-class agglomerates (k_restrict_batch; env
-  // MSF_RESTRICT_BATCH=0: off); n_rgroups = 0 when not used
-  int n_rgroups = 0, rgroup_B = 0;
-  bool rgroup_force = false;
-  bool prolong_nr = true;            // several realisations per prolongation thread (k_prolong_nr;
-                                     // env MSF_PROLONG_NR=0: one launch-z per realisation)        // env MSF_RESTRICT_BATCH=force: grouped kernel on every launch
-  int* rgroups_d = nullptr;
-  std::vector<int> agg_by_cls_h;
+  // coarse-cell-class restriction / prolongation (msf_xfer.cu)
+  int xf_G = 1, xf_ntasks = 0, xf_n_cls = 0;   // 16-column groups, CTA tasks, cell classes
+  void* xf_cls = nullptr;       // XferClass[]
+  void* xf_tasks = nullptr;     // XferTask[]
+  int* xf_cells = nullptr;      // this rank's cells sorted by class
+  double* xf_part = nullptr;    // [R][ncx * ncy][16 G] restriction column sums per cell
   int* factor_status = nullptr; // [2 * MSF_MAX_RHS] nonzero on failed pivot
-  int restrict_threads = 0;
   bool apply_direct = true;     // operator apply with direct (L1) neighbourhood loads
   bool apply_sw = true;         // ... as a sliding window along x (env MSF_APPLY_SW=0: per node)
   int apply_sw_kx = 0;          // columns per thread of the sliding window (0: from the grid size)
@@ -272,8 +265,6 @@ struct msf_ctx {
   // updated residual out of place), so even and odd iterations are two graphs
   cudaGraphExec_t range_graph[2][MSF_MAX_RHS][MSF_MAX_RHS + 1] = {};
 };
-int restrict_groups(const Dims& d, const std::vector<int>& work, const std::vector<int>& cls,
-                    int B, std::vector<int>& groups);
 
 // ---------------------------------------------------------------- launch bookkeeping
 #define MSF_LAUNCHED(ctx) ((ctx)->launches++)
@@ -348,6 +339,9 @@ void launch_oc(msf_ctx* c, const double* x, const double* dF, const double* dg, 
 void launch_build_basis(msf_ctx* c);
 // K_c assembly (Galerkin cell products) + nested-dissection factorisation, one GPU
 void launch_assemble_coarse(msf_ctx* c);
+// restriction / prolongation by coarse-cell class (msf_xfer.cu)
+int xfer_setup(msf_ctx* c, char*& cur);
+size_t xfer_workspace_bytes(const Dims& d);
 void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated);
 // z = zin + R^T c (zin == z: in place)
 void launch_prolong(msf_ctx* c, int rhs0, int nr, const double* zin, double* z, bool gated);

@@ -458,21 +458,26 @@ def test_threshold_mode_contrast_flat():
     assert max(its) - min(its) <= 0.2 * max(its) + 2
 
 
-GROUPED_SPECS = {
+TRANSFER_SPECS = {
     "robust_32x16": SPECS["robust_32x16"],
-    "ragged_36x20": SPECS["ragged_36x20"],   # 5 modes: groups of 2
+    "ragged_36x20": SPECS["ragged_36x20"],   # 5 modes: two 16-column groups per pattern entry
     "periodic_48x24": W.small_spec(nelx=48, nely=24, cx=4, cy=4, tile=(8, 8), rmin=1.5, beta=4.0,
                                    etas=(0.6, 0.4), dilated=1, bc="mbb", seed=25),
+    # 16 modes: four column groups; 12 x 8 coarse cells of 4 x 4 (several cell classes)
+    "modes16_48x32": W.small_spec(nelx=48, nely=32, cx=4, cy=4, tile=(8, 8), rmin=1.5, beta=4.0,
+                                  etas=(0.6, 0.4), dilated=1, seed=26, n_modes=16),
+    # coarse cells of 20 x 20 (pattern of 882 entries: four 256-thread chunks), ragged classes
+    "cells20_120x80": W.small_spec(nelx=120, nely=80, cx=20, cy=20, tile=(40, 40), rmin=2.5,
+                                   beta=8.0, etas=(0.7, 0.5, 0.3), dilated=2, bc="mbb", seed=28),
 }
 
 
-@pytest.mark.parametrize("name", list(GROUPED_SPECS))
-def test_grouped_restriction(name, monkeypatch):
-    """The restriction over groups of same-class agglomerates (k_restrict_batch, forced on
-    every launch) gives the oracle's two-level preconditioner (R8) and the oracle's PCG
-    iteration counts (+-1) on periodic designs, boundary-clipped boxes included."""
-    monkeypatch.setenv("MSF_RESTRICT_BATCH", "force")
-    spec = GROUPED_SPECS[name]
+@pytest.mark.parametrize("name", list(TRANSFER_SPECS))
+def test_cell_class_transfer(name):
+    """Restriction / prolongation by coarse-cell class (msf_xfer.cu) give the oracle's
+    two-level preconditioner (R8) and the oracle's PCG iteration counts (+-1) on periodic
+    designs, boundary-clipped boxes, 1, 2 and 4 column groups and multi-chunk patterns."""
+    spec = TRANSFER_SPECS[name]
     m, x = ctx_for(spec)
     m.build_coarse_basis()
     m.assemble_coarse()
