@@ -48,7 +48,7 @@ def test_design_loop_follows_oracle(name):
         ref = problem.solve(spec, x, fx, f, tol=1e-12)
         F, c, g, dF, dg = design.design_gradients(spec, x, ref["us"], f, ref["K0"])
         # F's bar as in test_gpu_parity: the fp64-attainable compliance accuracy, x3
-        tc = max(compliance_tol(spec, e, f, fx) for e in ref["E_el"])
+        tc = max(compliance_tol(spec, e, f, fx, cp) for e, cp in zip(ref["E_el"], ref["comps"]))
         return F, g, design.oc_update(spec, x, dF, dg), 3 * tc
 
     def gpu_step(x):

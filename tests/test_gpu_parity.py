@@ -48,16 +48,22 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
-def compliance_tol(spec, E_el, f, fx):
-    """Parity bar for compliance: 1e-10 relative, unless fp64
-    cannot reach it for this operator.  |c - c*| = |f^T K^-1 r| <= ||u*|| ||r||, so with
-    the fp64 floor r_floor = true residual of the oracle's direct solve the attainable
-    relative accuracy is ||u*|| ||r_floor|| / c*; the bar is max(1e-10, 10x that)."""
+def compliance_tol(spec, E_el, f, fx, c_pcg):
+    """Parity bar for compliance: the north-star 1e-10 relative,
+    unless fp64 cannot reach it for this operator.  The attainable floor is MEASURED: the
+    oracle's own PCG at tol 1e-12 (c_pcg) against its direct sparse solve (c*); the bar is
+    max(1e-10, 10 |c_pcg - c*| / c*).  The achieved error is printed by the callers."""
     K = fem.assemble(spec.nelx, spec.nely, E_el, fem.element_stiffness(spec.nu))
     u = fem.solve_direct(K, f, fx)
-    r = f - fem.constrained_operator(K, fx) @ u
     c = f @ u
-    return max(1e-10, 10 * np.linalg.norm(u) * np.linalg.norm(r) / abs(c))
+    return max(1e-10, 10 * abs(c_pcg - c) / abs(c))
+
+
+def check_compliance(spec, ref, comps, f, fx, k, what=""):
+    tc = compliance_tol(spec, ref["E_el"][k], f, fx, ref["comps"][k])
+    err = abs(comps[k] - ref["comps"][k]) / abs(ref["comps"][k])
+    print(f"compliance {spec.name}{what} rhs {k}: rel err {err:.2e} (bar {tc:.2e})")
+    assert err <= tc, (k, err, tc)
 
 
 SPECS = {
@@ -359,8 +365,73 @@ def test_pcg_parity(name):
     ug = host(u).reshape(spec.n_rhs, spec.n_dof)
     for k in range(spec.n_rhs):
         assert rel(ug[k], ref["us"][k]) <= 1e-8
-        tc = compliance_tol(spec, ref["E_el"][k], f, fx)
-        assert abs(comps[k] - ref["comps"][k]) <= tc * abs(ref["comps"][k]), tc
+        check_compliance(spec, ref, comps, f, fx, k)
+
+
+# sizes that take the kernels of the full-size path: >= 126 node rows with even nely (TMA-fed
+# operator and residual), several 112-row bands and column runs of the streaming sweep,
+# 20 x 20 coarse cells (four-warp-tile cell patterns) and 3 realisations
+PATH_SPECS = {
+    "path_256x128": W.small_spec(nelx=256, nely=128, cx=8, cy=8, tile=(32, 32), rmin=2.5, beta=8.0,
+                                 etas=(0.7, 0.5, 0.3), dilated=2, bc="mbb", seed=29, Emin=1e-6),
+    "path_160x140_c20": W.small_spec(nelx=160, nely=140, cx=20, cy=20, tile=(40, 20), rmin=2.5,
+                                     beta=8.0, etas=(0.7, 0.5, 0.3), dilated=2, bc="mbb", seed=33),
+}
+
+
+@pytest.mark.parametrize("name", list(PATH_SPECS))
+def test_pcg_parity_full_path_kernels(name):
+    """The oracle's PCG iteration counts (+-1), its V-cycle (1e-7, element-wise through the
+    TMA residual, the cell-class transfer and the streaming sweeps) and its tight solve
+    (displacements 1e-8, compliance at the measured floor) on grids that run every kernel of
+    the full-size configuration."""
+    spec = PATH_SPECS[name]
+    m, x = ctx_for(spec)
+    m.build_coarse_basis()
+    m.assemble_coarse()
+    fx, f, K0, E, A, _ = oracle_setup(spec, x)
+    R, _ = msfem.build_coarse_basis(spec.nelx, spec.nely, spec.cx, spec.cy, spec.n_modes,
+                                    E[spec.dilated], K0, fx)
+    groups = msfem.gs_groups(spec.nelx, spec.nely, fx)
+    for k in range(spec.n_rhs):
+        M = msfem.TwoLevelPreconditioner(A[k], R, groups, fx)
+        r = W.random_vectors(spec.n_dof, 1, seed=40 + k)[0]
+        r[fx == 1] = 0
+        z = torch.empty(spec.n_dof, dtype=torch.float64, device=DEV)
+        m.precond_apply(k, dev(r), z)
+        assert rel(host(z), M(r)) <= 1e-7
+    ref = problem.solve(spec, x, fx, f, tol=1e-8)
+    its, comps, noconv = m.pcg_solve(tol=1e-8)
+    assert not noconv
+    for k in range(spec.n_rhs):
+        assert abs(its[k] - ref["iters"][k]) <= 1, (its, ref["iters"])
+    # tight solve.  On these grids (eroded realisation: ~350-1400 iterations, contrast 1e6-1e9)
+    # ONE-ULP relative changes of the element moduli and of the element matrix (the GPU's pow and
+    # closed-form K0 vs the oracle's, and the element-wise matvec vs the assembled K differ at
+    # that level) already move the exact solution by more than 1e-8: the bars are 10x that
+    # measured sensitivity, and the true residual under the oracle's operator must match the
+    # oracle PCG's own.
+    u = torch.empty(spec.n_rhs * spec.n_dof, dtype=torch.float64, device=DEV)
+    its, comps, noconv = m.pcg_solve(tol=1e-12, u=u)
+    ug = host(u).reshape(spec.n_rhs, spec.n_dof)
+    ref = problem.solve(spec, x, fx, f, tol=1e-12)
+    rng = np.random.default_rng(0)
+    K0p = K0 * (1.0 + 2.0 ** -52 * rng.choice([-1.0, 1.0], size=K0.shape))
+    K0p = 0.5 * (K0p + K0p.T)
+    for k in range(spec.n_rhs):
+        Kd = fem.assemble(spec.nelx, spec.nely, E[k], K0)
+        ud = fem.solve_direct(Kd, f, fx)
+        Ep = E[k] * (1.0 + 2.0 ** -52 * rng.choice([-1.0, 1.0], size=E[k].shape))
+        up = fem.solve_direct(fem.assemble(spec.nelx, spec.nely, Ep, K0p), f, fx)
+        du, dc = rel(up, ud), abs(f @ up - f @ ud) / abs(f @ ud)
+        eu, ec = rel(ug[k], ud), abs(comps[k] - f @ ud) / abs(f @ ud)
+        res_g = np.linalg.norm(f * (fx == 0) - A[k] @ ug[k]) / np.linalg.norm(f)
+        res_o = np.linalg.norm(f * (fx == 0) - A[k] @ ref["us"][k]) / np.linalg.norm(f)
+        print(f"{name} rhs {k}: u err {eu:.2e} (1-ulp E, K0 sensitivity {du:.2e}), compliance err "
+              f"{ec:.2e} ({dc:.2e}), true residual {res_g:.2e} (oracle PCG {res_o:.2e})")
+        assert eu <= max(1e-8, 10 * du), (k, eu, du)
+        assert ec <= max(1e-10, 10 * dc), (k, ec, dc)
+        assert res_g <= max(1e-11, 10 * res_o), (k, res_g, res_o)
 
 
 def test_config0_full_size_pcg():
@@ -395,7 +466,7 @@ def test_sensitivities_and_oc(name):
     dFg = torch.empty(nt, dtype=torch.float64, device=DEV)
     dgg = torch.empty(nt, dtype=torch.float64, device=DEV)
     Fg, gg, cg = m.sensitivities(kappa=spec.kappa, volfrac=spec.volfrac, dF=dFg, dg=dgg)
-    tc = max(compliance_tol(spec, e, f, fx) for e in ref["E_el"])
+    tc = max(compliance_tol(spec, e, f, fx, cp) for e, cp in zip(ref["E_el"], ref["comps"]))
     assert abs(Fg - F) <= 3 * tc * abs(F)
     assert abs(gg - g) <= 1e-12
     assert np.abs(host(dFg) - dF).max() <= 1e-8 * np.abs(dF).max()
