@@ -405,17 +405,10 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
     return msf_fail(nullptr, MSF_ERR_CUDA, "setup: coarse-cell transfer plan (n_modes > 16 unsupported)");
   }
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
-  if (const char* e = std::getenv("MSF_APPLY_DIRECT")) c->apply_direct = std::string(e) != "0";
-  if (const char* e = std::getenv("MSF_APPLY_SW")) c->apply_sw = std::string(e) != "0";
   if (const char* e = std::getenv("MSF_APPLY_TMA")) c->apply_tma = std::string(e) != "0";
-  if (const char* e = std::getenv("MSF_RESIDUAL_TMA")) c->residual_tma = std::string(e) != "0";
   {
     const char* e = std::getenv("MSF_PDL");   // read at every setup (tests toggle it)
     g_msf_pdl = !(e && std::string(e) == "0");
-  }
-  if (const char* e = std::getenv("MSF_SW_KX")) {
-    const int k = std::atoi(e);
-    c->apply_sw_kx = (k == 2 || k == 4 || k == 8) ? k : 0;
   }
   c->sc = (PcgScalars*)take(R * sizeof(PcgScalars));
   c->partials = (double*)take(R * (size_t)P.max_partials * 8);

@@ -25,46 +25,7 @@ using namespace msfk;
 
 namespace {
 
-constexpr int NTHR = TILE_THREADS;
-
-// ------------------------------------------------------------------ operator apply
-// MODE 0: y = P K P x ; MODE 1: y = b - P K P x.  dot: accumulate x.y (p.Ap) and set
-// alpha = rz / pq in the last block.
-template <int MODE>
-__global__ void __launch_bounds__(NTHR) k_apply(Dims d, K0Mat K, const double* __restrict__ Eall,
-                                                const double2* __restrict__ xall,
-                                                double2* __restrict__ yall,
-                                                const double2* __restrict__ ball,
-                                                const uint8_t* __restrict__ fixn, PcgScalars* sc,
-                                                double* partials, unsigned* counters, int rhs0,
-                                                int gated, int dot, int max_partials,
-                                                double* dsum) {
-  pdl_launch();
-  pdl_wait();
-  const int rhs = rhs0 + blockIdx.z;
-  if (gated && !sc[rhs].active) return;
-  __shared__ TileSmem S;
-  __shared__ double red[NTHR / 32 + 1];
-  const int tid = threadIdx.y * TY + threadIdx.x;
-  const double dv = apply_tile<MODE>(d, K, Eall + (size_t)rhs * d.estride, xall + (size_t)rhs * d.nn,
-                                     yall + (size_t)rhs * d.nn,
-                                     MODE == 1 ? ball + (size_t)rhs * d.nn : nullptr, fixn,
-                                     blockIdx.y * TX, blockIdx.x * TY, tid, S);
-  if (dot) {
-    const double s = block_sum_all(dv, red, tid, NTHR);
-    const unsigned nblk = gridDim.x * gridDim.y;
-    const int slot = blockIdx.y * gridDim.x + blockIdx.x;
-    if (arrive_last(s, partials + (size_t)rhs * max_partials, slot, counters + rhs * 8, nblk,
-                    tid)) {
-      const double tot = reduce_partials(partials + (size_t)rhs * max_partials, nblk, red, tid,
-                                         NTHR);
-      if (tid == 0) {
-        fin_or_park(sc, dsum, rhs, FIN_PQ, tot, 0);
-        counters[rhs * 8] = 0;
-      }
-    }
-  }
-}
+constexpr int NTHR = 256;   // threads per CTA of the operator and colour-phase kernels
 
 // ------------------------------------------------------------------ sliding-window operator apply
 // Thread per (node row iy, run of KX consecutive node columns): the 3x3 neighbourhood of x and
@@ -698,10 +659,6 @@ inline int vec_blocks(const Dims& d) {
   return b < 65535 ? b : 65535;
 }
 
-dim3 apply_grid(const Dims& d, int nr) {
-  return dim3((d.nny + TY - 1) / TY, (d.nnx + TX - 1) / TX, nr);
-}
-
 }  // namespace
 
 // ================================================================== host launchers
@@ -723,9 +680,8 @@ K0Mat make_K0(double nu) {
   return K;
 }
 
-int apply_partials_needed(const Dims& d) {
-  dim3 g = apply_grid(d, 1);
-  int a = (int)(g.x * g.y);
+int apply_partials_needed(const Dims& d) {   // one partial per CTA of k_apply_direct's grid
+  const int a = ((d.nny + 31) / 32) * ((d.nnx + 7) / 8);
   return a > 592 ? a : 592;
 }
 
@@ -736,7 +692,6 @@ int sgs_colour_partials_needed(const Dims& d) {
 
 // Fine-grid launchers run on this rank's grid c->dl with the moduli c->E_loc (the whole grid
 // on one GPU); reductions park their sums in c->dsum on a strip context.
-// direct-load apply (default; MSF_APPLY_DIRECT=0 selects the shared-memory tile kernel)
 // TMA descriptors of the operator apply: kind 0 = node vector x (dims 2 nny doubles, nnx
 // columns, R realisations), kind 1 = moduli (nely, nelx, R); cached per base pointer.
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
@@ -813,23 +768,23 @@ static bool launch_apply_tma(msf_ctx* c, int rhs0, int nr, const double* x, doub
   return true;
 }
 
+// Operator apply (MODE 0) / residual (MODE 1) on this rank's grid: the TMA-fed tile kernel
+// when the grid allows it (even nely, >= one 8 x 126 tile), else the sliding-window apply /
+// one-node-per-thread residual (odd nely or small grids, e.g. most test grids).
 template <int MODE>
-static bool launch_apply_direct(msf_ctx* c, int rhs0, int nr, const double* x, double* y,
-                                const double* bvec, bool gated, bool dot) {
-  if (!c->apply_direct) return false;
+static void launch_apply(msf_ctx* c, int rhs0, int nr, const double* x, double* y,
+                         const double* bvec, bool gated, bool dot) {
   const Dims& d = c->dl;
-  // p.Ap on one GPU: partials only, reduced by the next kernel (k_update_f0); strips need the
-  // all-reduce, so the last-block finalisation parks the local sum
+  // p.Ap on one GPU: partials only, reduced by the next kernel (the pre-smoothing); strips need
+  // the all-reduce, so the last-block finalisation parks the local sum
   const int dmode = !dot ? 0 : c->comm ? 1 : 2;
-  if ((MODE == 0 || c->residual_tma) && launch_apply_tma<MODE>(c, rhs0, nr, x, y, bvec, gated, dmode))
-    return true;
-  if (c->apply_sw && MODE == 0) {
+  if (launch_apply_tma<MODE>(c, rhs0, nr, x, y, bvec, gated, dmode)) return;
+  if (MODE == 0) {
     // columns per thread: the longest run that still gives >= 4 CTAs per SM (measured: the
     // residual form, which also streams b, is faster one node per thread)
     const int by = (d.nny + 31) / 32;
     int kx = 8;
     while (kx > 2 && (long long)by * ((d.nnx + 8 * kx - 1) / (8 * kx)) * nr < 4LL * c->n_sm) kx /= 2;
-    if (c->apply_sw_kx) kx = c->apply_sw_kx;
     const dim3 grid(by, (d.nnx + 8 * kx - 1) / (8 * kx), nr);
 #define MSF_SW(KX)                                                                                  \
   launch_k(k_apply_sw<MODE, KX>, grid, dim3(32, 8), 0, c->stream, d, c->K0, (const double*)c->E_loc, \
@@ -841,7 +796,7 @@ static bool launch_apply_direct(msf_ctx* c, int rhs0, int nr, const double* x, d
 #undef MSF_SW
     c->apart_n = dmode == 2 ? (int)(grid.x * grid.y) : 0;
     MSF_LAUNCHED(c);
-    return true;
+    return;
   }
   launch_k(k_apply_direct<MODE>, dim3((d.nny + 31) / 32, (d.nnx + 7) / 8, nr), dim3(32, 8), 0,
            c->stream, d, c->K0, (const double*)c->E_loc, (const double2*)x, (double2*)y,
@@ -849,26 +804,16 @@ static bool launch_apply_direct(msf_ctx* c, int rhs0, int nr, const double* x, d
            dmode, c->max_partials, c->dsum, c->apart);
   c->apart_n = dmode == 2 ? ((d.nny + 31) / 32) * ((d.nnx + 7) / 8) : 0;
   MSF_LAUNCHED(c);
-  return true;
 }
 
 void launch_matvec(msf_ctx* c, int rhs0, int nr, const double* x, double* y, bool gated,
                    bool dot_pq) {
-  if (launch_apply_direct<0>(c, rhs0, nr, x, y, nullptr, gated, dot_pq)) return;
-  launch_k(k_apply<0>, apply_grid(c->dl, nr), dim3(TY, TX), 0, c->stream,
-           c->dl, c->K0, c->E_loc, (const double2*)x, (double2*)y, (const double2*)nullptr, c->fixn,
-           c->sc, c->partials, c->counters, rhs0, gated ? 1 : 0, dot_pq ? 1 : 0, c->max_partials,
-           c->dsum);
-  MSF_LAUNCHED(c);
+  launch_apply<0>(c, rhs0, nr, x, y, nullptr, gated, dot_pq);
 }
 
 void launch_residual(msf_ctx* c, int rhs0, int nr, const double* b, const double* x, double* y,
                      bool gated) {
-  if (launch_apply_direct<1>(c, rhs0, nr, x, y, b, gated, false)) return;
-  launch_k(k_apply<1>, apply_grid(c->dl, nr), dim3(TY, TX), 0, c->stream,
-           c->dl, c->K0, c->E_loc, (const double2*)x, (double2*)y, (const double2*)b, c->fixn,
-           c->sc, c->partials, c->counters, rhs0, gated ? 1 : 0, 0, c->max_partials, c->dsum);
-  MSF_LAUNCHED(c);
+  launch_apply<1>(c, rhs0, nr, x, y, b, gated, false);
 }
 
 void launch_sgs_phase(msf_ctx* c, int rhs0, int nr, const double* r, double* z, bool gated,

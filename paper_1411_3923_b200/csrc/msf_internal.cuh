@@ -227,11 +227,7 @@ struct msf_ctx {
   int* xf_cells = nullptr;      // this rank's cells sorted by class
   double* xf_part = nullptr;    // [R][ncx * ncy][16 G] restriction column sums per cell
   int* factor_status = nullptr; // [2 * MSF_MAX_RHS] nonzero on failed pivot
-  bool apply_direct = true;     // operator apply with direct (L1) neighbourhood loads
-  bool apply_sw = true;         // ... as a sliding window along x (env MSF_APPLY_SW=0: per node)
-  int apply_sw_kx = 0;          // columns per thread of the sliding window (0: from the grid size)
-  bool apply_tma = true;        // operator apply fed by TMA tiles (env MSF_APPLY_TMA=0: off)
-  bool residual_tma = true;     // ... also for the residual t = r - K z (env MSF_RESIDUAL_TMA=0)
+  bool apply_tma = true;        // operator apply / residual fed by TMA tiles (env MSF_APPLY_TMA=0: off)
   struct TmapSlot {             // cached TMA descriptor (CUtensorMap, 128 B) per base pointer
     const void* ptr;
     int kind;

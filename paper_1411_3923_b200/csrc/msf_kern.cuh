@@ -208,70 +208,6 @@ __device__ __forceinline__ void fin_or_park(PcgScalars* sc, double* dsum, int rh
 }
 
 
-// ------------------------------------------------------------------ operator tile
-// y = P K P x (MODE 0) or y = b - P K P x (MODE 1) on one 8x32-node tile (ix0, iy0) with a
-// one-node halo staged in shared memory; returns this thread's x.y contribution.
-constexpr int TX = 8;
-constexpr int TY = 32;
-constexpr int TILE_THREADS = TX * TY;
-struct TileSmem {
-  double2 xs[TX + 2][TY + 2];
-  double Es[TX + 1][TY + 1];
-};
-
-template <int MODE>
-__device__ __forceinline__ double apply_tile(const Dims& d, const K0Mat& K, const double* __restrict__ E,
-                                             const double2* __restrict__ x, double2* __restrict__ y,
-                                             const double2* __restrict__ b,
-                                             const uint8_t* __restrict__ fixn, int ix0, int iy0,
-                                             int tid, TileSmem& S) {
-  for (int k = tid; k < (TX + 2) * (TY + 2); k += TILE_THREADS) {
-    const int i = k / (TY + 2), j = k - i * (TY + 2);
-    const int gx = ix0 - 1 + i, gy = iy0 - 1 + j;
-    double2 v = make_double2(0.0, 0.0);
-    if (gx >= 0 && gx < d.nnx && gy >= 0 && gy < d.nny) v = x[(size_t)gx * d.nny + gy];
-    S.xs[i][j] = v;
-  }
-  for (int k = tid; k < (TX + 1) * (TY + 1); k += TILE_THREADS) {
-    const int i = k / (TY + 1), j = k - i * (TY + 1);
-    const int ex = ix0 - 1 + i, ey = iy0 - 1 + j;
-    S.Es[i][j] = (ex >= 0 && ex < d.nelx && ey >= 0 && ey < d.nely) ? E[(size_t)ex * d.nely + ey] : 0.0;
-  }
-  __syncthreads();
-  const int li = tid / TY, lj = tid - (tid / TY) * TY;
-  const int ix = ix0 + li, iy = iy0 + lj;
-  double dv = 0.0;
-  if (ix < d.nnx && iy < d.nny) {
-    double Eloc[2][2];
-    double2 zloc[3][3];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) Eloc[a][c] = S.Es[li + a][lj + c];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) zloc[a][c] = S.xs[li + a][lj + c];
-    double ox, oy, dxx, dxy, dyx, dyy;
-    apply_node(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
-    const size_t n = (size_t)ix * d.nny + iy;
-    const uint8_t fm = fixn[n];
-    double2 out;
-    if (MODE == 1) {
-      const double2 bb = b[n];
-      out = make_double2(bb.x - ox, bb.y - oy);
-    } else {
-      out = make_double2(ox, oy);
-    }
-    if (fm & 1) out.x = 0.0;
-    if (fm & 2) out.y = 0.0;
-    y[n] = out;
-    dv = zloc[1][1].x * out.x + zloc[1][1].y * out.y;
-  }
-  __syncthreads();   // smem reused by the next tile
-  return dv;
-}
-
 // ------------------------------------------------------------------ Gauss-Seidel
 // 1/x for the Gauss-Seidel pivots: the hardware approximation refined by two Newton steps
 __device__ __forceinline__ double rcp_nr(double x) {

@@ -20,6 +20,7 @@
 #include "msf_kern.cuh"
 
 #include <algorithm>
+#include <climits>
 
 using namespace msfk;
 
@@ -152,29 +153,53 @@ __global__ void __launch_bounds__(SG_T, 2)
   }
 
   const int cs = X0 - SG_DEP, c_last = X1 + SG_DEP - 1;   // buffered columns [cs, c_last]
-  auto slot = [&](int c) { return (c - cs) % SG_NR; };
-  // column c into its ring slot: z (or q), r, moduli, Dirichlet bits
-  auto issue = [&](int c) {
+  auto wrap = [](int x) { return x >= SG_NR ? x - SG_NR : (x < 0 ? x + SG_NR : x); };
+  // ---- per-thread constants (the step loop only moves the column)
+  // issue / transform / write-back row of this thread
+  const int pl_t = tid & 1, k_t = tid >> 1, gy_t = Yb + tid;
+  const bool vz_t = gy_t >= 0 && gy_t < d.nny, ve_t = gy_t >= 0 && gy_t < d.nely;
+  const int gyc_t = vz_t ? gy_t : 0, gye_t = ve_t ? gy_t : 0;
+  // node tasks: warp w runs phase 2w + 1 on even steps (F0 F2 B2 B0, even columns) and 2w + 2
+  // on odd steps (F1 F3B3 B1, odd columns), colour rows lane and lane + 32 of the phase's row
+  // parity; rows outside [1 + ph, 127 - ph) are computed from a valid row and not stored
+  const int wp = tid >> 5, lane = tid & 31;
+  // (even-step / odd-step values as named scalars: an array indexed by the step parity would
+  // live in local memory)
+  int ph0, ly00, ly10, slo0, shi0, ph1, ly01, ly11, slo1, shi1;
+  bool vA0, vB0, vA1, vB1;
+  auto task_consts = [&](int par, int& ph, int& ly0, int& ly1, bool& vA, bool& vB, int& slo, int& shi) {
+    ph = 2 * wp + 1 + par;
+    const int colour = (ph <= 4) ? ph - 1 : 7 - ph;
+    const int lyA = 2 * lane + (colour >> 1), lyB = lyA + 64;
+    vA = lyA >= 1 + ph;
+    vB = lyB < SG_H - 1 - ph;
+    ly0 = vA ? lyA : lyA + 2 * ((2 + ph - lyA) / 2);
+    ly1 = vB ? lyB : lyB - 2 * ((lyB - (SG_H - 2 - ph)) / 2 + 1);
+    // steps at which the phase's column s - 2 ph lies in [X0 - 7 + ph, X1 + 7 - ph) and the grid
+    slo = max(X0 - SG_DEP + ph, 0) + 2 * ph;
+    shi = ph <= 7 ? min(X1 + SG_DEP - ph, d.nnx) + 2 * ph : INT_MIN;
+  };
+  task_consts(0, ph0, ly00, ly10, vA0, vB0, slo0, shi0);
+  task_consts(1, ph1, ly01, ly11, vA1, vB1, slo1, shi1);
+  // column c into ring slot sl: z (or q), r, moduli, Dirichlet bits (this thread: row tid)
+  auto issue = [&](int c, int sl) {
 #ifdef MSF_SGS_EXP_NOLOAD   // A/B experiment: the sweep's arithmetic alone
     return;
 #endif
     if (c > c_last) return;
-    const int sl = slot(c), ly = tid, pl = ly & 1, k = ly >> 1;
     if (c < 0 || c >= d.nnx) {   // outside the grid: zero values, both DOFs fixed
-      S.z[sl][pl][k] = make_double2(0.0, 0.0);
-      S.r[sl][pl][k] = make_double2(0.0, 0.0);
-      S.e[sl][pl][k] = 0.0;
-      S.f[sl][pl][k] = 3;
+      S.z[sl][pl_t][k_t] = make_double2(0.0, 0.0);
+      S.r[sl][pl_t][k_t] = make_double2(0.0, 0.0);
+      S.e[sl][pl_t][k_t] = 0.0;
+      S.f[sl][pl_t][k_t] = 3;
       return;
     }
-    const int gy = Yb + ly;
-    const bool v = gy >= 0 && gy < d.nny;
-    const size_t n = (size_t)c * d.nny + (v ? gy : 0);
-    if (!ZERO) cpa16(&S.z[sl][pl][k], zin + n, v);
-    else if (UPD) cpa16(&S.z[sl][pl][k], q + n, v);
-    cpa16(&S.r[sl][pl][k], r + n, v);
-    const bool ve = gy >= 0 && gy < d.nely && c < d.nelx;
-    cpa8(&S.e[sl][pl][k], E + (ve ? (size_t)c * d.nely + gy : 0), ve);
+    const size_t n = (size_t)c * d.nny + gyc_t;
+    if (!ZERO) cpa16(&S.z[sl][pl_t][k_t], zin + n, vz_t);
+    else if (UPD) cpa16(&S.z[sl][pl_t][k_t], q + n, vz_t);
+    cpa16(&S.r[sl][pl_t][k_t], r + n, vz_t);
+    const bool ve = ve_t && c < d.nelx;
+    cpa8(&S.e[sl][pl_t][k_t], E + (ve ? (size_t)c * d.nely + gye_t : 0), ve);
     if (tid < 16) {   // 2 planes x 64 bytes of the planar padded mask (setup: fixs)
       const int p2 = tid >> 3, ch = tid & 7;
       cpa8(&S.f[sl][p2][ch * 8], fixs + (size_t)c * fs_col + p2 * fs_plane + (Y0 >> 1) + ch * 8, true);
@@ -182,70 +207,60 @@ __global__ void __launch_bounds__(SG_T, 2)
   };
 
   for (int c = cs; c < cs + SG_P; ++c) {
-    issue(c);
+    issue(c, c - cs);
     cpa_commit();
   }
   double dot = 0.0;
-  for (int s = cs + 1; s <= X1 + 14; ++s) {
+  int sl = 1;   // ring slot of column s (slot(c) = (c - cs) mod SG_NR)
+  for (int s = cs + 1; s <= X1 + 14; ++s, sl = sl + 1 == SG_NR ? 0 : sl + 1) {
     cpa_wait<SG_P - 1>();   // column s - 1 has landed (this thread's copies) ...
     __syncthreads();        // ... for every thread; step s - 1 is complete everywhere
-    issue(s - 1 + SG_P);    // into the slot of column s - 16, last read at step s - 1
+    issue(s - 1 + SG_P, wrap(sl - 1 + SG_P));   // into the slot of column s - 16, last read at step s - 1
     cpa_commit();
-    if (ZERO) {
+    if (ZERO && s - 1 <= c_last) {
       // column s - 1 becomes the sweep's input: z = 0 (UPD: r -= alpha q, q from z's slot)
-      const int tc = s - 1;
-      if (tc <= c_last) {
-        const int sl = slot(tc), pl = tid & 1, k = tid >> 1;
-        if (UPD) {
-          double2 rv = S.r[sl][pl][k];
-          const double2 qv = S.z[sl][pl][k];
-          rv.x = fma(-alpha, qv.x, rv.x);
-          rv.y = fma(-alpha, qv.y, rv.y);
-          S.r[sl][pl][k] = rv;
-        }
-        S.z[sl][pl][k] = make_double2(0.0, 0.0);
+      const int st = wrap(sl - 1);
+      if (UPD) {
+        double2 rv = S.r[st][pl_t][k_t];
+        const double2 qv = S.z[st][pl_t][k_t];
+        rv.x = fma(-alpha, qv.x, rv.x);
+        rv.y = fma(-alpha, qv.y, rv.y);
+        S.r[st][pl_t][k_t] = rv;
       }
+      S.z[st][pl_t][k_t] = make_double2(0.0, 0.0);
     }
     {
       // column s - 15 is final (phase 7 ran on it at step s - 1): band rows to global
-      const int wc = s - 15;
-      const int i = tid;
+      const int wc = s - 15, i = tid;
       if (i < SG_IN && wc >= X0 && wc < X1 && Y0 + i < d.nny) {
-        const int ly = SG_LO + i, sl = slot(wc), pl = ly & 1, k = ly >> 1;
+        const int ly = SG_LO + i, sw = wrap(sl - 15);
         const size_t n = (size_t)wc * d.nny + (Y0 + i);
-        const double2 zv = S.z[sl][pl][k];
+        const double2 zv = S.z[sw][ly & 1][ly >> 1];
         z[n] = zv;
         if (UPD) {
-          const double2 rv = S.r[sl][pl][k];
+          const double2 rv = S.r[sw][ly & 1][ly >> 1];
           rout[n] = rv;
           dot += rv.x * rv.x + rv.y * rv.y;
         }
         if (RZ) {
-          const double2 rv = S.r[sl][pl][k];
+          const double2 rv = S.r[sw][ly & 1][ly >> 1];
           dot += rv.x * zv.x + rv.y * zv.y;
         }
       }
     }
     {
-      // phases: even s -> F0, F2, B2, B0 (even columns), odd s -> F1, F3B3, B1 (odd columns);
-      // warp w runs phase 2w + 1 (+1 on odd steps) on the colour rows lane and lane + 32
-      const int ph = 2 * (tid >> 5) + 1 + (s & 1);
-      if (ph <= 7) {
-        const int c = s - 2 * ph;
-        if (c >= X0 - SG_DEP + ph && c < X1 + SG_DEP - ph && c >= 0 && c < d.nnx) {
-          const int colour = (ph <= 4) ? ph - 1 : 7 - ph;
-          const int lyA = 2 * (tid & 31) + (colour >> 1), lyB = lyA + 64;
-          // rows outside [1 + ph, 127 - ph) are computed from a valid row and not stored
-          const bool vA = lyA >= 1 + ph, vB = lyB < SG_H - 1 - ph;
-          const int ly0 = vA ? lyA : lyA + 2 * ((2 + ph - lyA) / 2), ly1 = vB ? lyB : lyB - 2 * ((lyB - (SG_H - 2 - ph)) / 2 + 1);
-          const int s0 = slot(c), sm = s0 == 0 ? SG_NR - 1 : s0 - 1, sp = s0 == SG_NR - 1 ? 0 : s0 + 1;
-          switch (ph) {
-            case 1: sg_node2<true, false, ZERO>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
-            case 2:
-            case 3: sg_node2<true, false, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
-            case 4: sg_node2<true, true, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
-            default: sg_node2<false, true, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
-          }
+      const bool odd = s & 1;
+      const int ph = odd ? ph1 : ph0;
+      if (s >= (odd ? slo1 : slo0) && s < (odd ? shi1 : shi0)) {
+        const int s0 = wrap(sl - 2 * ph), sm = s0 == 0 ? SG_NR - 1 : s0 - 1, sp = s0 == SG_NR - 1 ? 0 : s0 + 1;
+        const int ly0 = odd ? ly01 : ly00, ly1 = odd ? ly11 : ly10;
+        const bool vA = odd ? vA1 : vA0, vB = odd ? vB1 : vB0;
+        switch (ph) {
+          case 1: sg_node2<true, false, ZERO>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
+          case 2:
+          case 3: sg_node2<true, false, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
+          case 4: sg_node2<true, true, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
+          default: sg_node2<false, true, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
         }
       }
     }

@@ -1,10 +1,14 @@
-"""Summarise ncu --set full reports (raw page) into a markdown table row per kernel."""
+"""Summarise ncu --set full reports (raw page) into a markdown table row per kernel.
+Columns: time, DRAM read / write, DRAM % of peak, warps active %, issue active %, FP64 pipe %,
+DMMA (fp64 tensor) pipe %, L1 / L2 hit rates, registers, grid, top stall reasons."""
 import csv, io, subprocess, sys
 KEYS = [("gpu__time_duration.sum", "us", 1e-3), ("dram__bytes_read.sum", "MB", 1e-6),
         ("dram__bytes_write.sum", "MB", 1e-6),
         ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "%", 1),
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "%", 1),
+        ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "%", 1),
         ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "%", 1),
+        ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "%", 1),
         ("l1tex__t_sector_hit_rate.pct", "%", 1), ("lts__t_sector_hit_rate.pct", "%", 1),
         ("launch__registers_per_thread", "", 1), ("launch__grid_size", "", 1)]
 STALLS = ["long_scoreboard", "short_scoreboard", "wait", "barrier", "math_pipe_throttle",
@@ -27,8 +31,15 @@ for path in sys.argv[1:]:
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")[:60]
         cells = []
         for k, u, sc in KEYS:
+            if k not in hdr:
+                cells.append("-")
+                continue
             i = hdr.index(k)
-            v = float(r[i].replace(",", ""))
+            try:
+                v = float(r[i].replace(",", ""))
+            except ValueError:
+                cells.append("-")
+                continue
             if u in ("us", "MB"):
                 v = units_scale(units[i], v) * (1e-3 if u == "us" else 1e-6)
             cells.append(f"{v:.3g}")

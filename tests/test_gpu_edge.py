@@ -63,7 +63,7 @@ def test_edge_pcg_parity(name):
         check_compliance(spec, ref, comps, f, fx, k)
 
 
-@pytest.mark.parametrize("env", [{"MSF_APPLY_TMA": "0", "MSF_RESIDUAL_TMA": "0"}, {"MSF_PDL": "0"}])
+@pytest.mark.parametrize("env", [{"MSF_APPLY_TMA": "0"}, {"MSF_PDL": "0"}])
 def test_opt_in_modes_match_default(env):
     """The run-time switches (read at context setup) solve the
     same problem as the default graph path: iterations +-1, solutions to 1e-9.  The spec is
