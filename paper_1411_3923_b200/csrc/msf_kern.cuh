@@ -224,7 +224,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // entry, fm its Dirichlet bits.  ZERO: z = 0 around the node, only the pivot block is needed.
 // Shared by the colour-phase kernels and the streaming sweep (msf_sgs.cu), so both execute
 // the same arithmetic.  Per-thread.
-template <bool FWD, bool BWD, bool ZERO, bool SYM = true>
+template <bool FWD, bool BWD, bool ZERO>
 __device__ __forceinline__ double2 gs_node(const K0Mat& K, const double (&Eloc)[2][2],
                                          const double2 (&zloc)[3][3], double2 rv, uint8_t fm) {
   double ox, oy, dxx, dxy, dyx, dyy;
@@ -235,13 +235,14 @@ __device__ __forceinline__ double2 gs_node(const K0Mat& K, const double (&Eloc)[
     dyx = dxy;
     dyy = dxx;
   } else {
-    apply_node<SYM>(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
+    apply_node<true>(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
   }
   double2 zn = zloc[1][1];
   double rx = rv.x - ox, ry = rv.y - oy;
 #if MSF_GS_RCP
-  // reciprocals of the pivots: off the dependent chain, <= 2 ulp from the quotient
-  const double ixx = rcp_nr(dxx), iyy = rcp_nr(dyy);
+  // reciprocal of the pivot (dyy == dxx bitwise, R7b): off the dependent chain, <= 2 ulp from
+  // the quotient
+  const double ixx = rcp_nr(dxx), iyy = ixx;
 #define MSF_DIVX(a) ((a) * ixx)
 #define MSF_DIVY(a) ((a) * iyy)
 #else
@@ -315,7 +316,7 @@ __device__ __forceinline__ double sgs_quad(const Dims& d, const K0Mat& K, const 
     const size_t n = (size_t)ix * d.nny + iy;
     const double2 rv = r[n];
     const uint8_t fm = fixn[n];
-    const double2 zn = gs_node<FWD, BWD, ZERO, SYM>(K, Eloc, zloc, rv, fm);
+    const double2 zn = gs_node<FWD, BWD, ZERO>(K, Eloc, zloc, rv, fm);
     z[n] = zn;
     if (RZ) dot = rv.x * zn.x + rv.y * zn.y;
   }
