@@ -232,7 +232,7 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   add((size_t)P.eig_doubles * 8);            // eig work
   add(R * d.ncx * d.ncy * 16 * d.kmax * d.kmax * 8);     // Kcell
   add(2 * R * d.nbc * (size_t)d.mc * 8);     // cb, cx
-  add(xfer_workspace_bytes(d));              // cell-class transfer plan + restriction partials
+  add(xfer_workspace_bytes(d, P.cls_of_agg, P.sb.C0, P.sb.C1));   // cell-class transfer + Galerkin plan
   add(nd_workspace_bytes(d, P.nd));
   add(2 * MSF_MAX_RHS * 4);                  // factor_status
   add(R * sizeof(PcgScalars));

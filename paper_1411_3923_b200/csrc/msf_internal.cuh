@@ -226,6 +226,12 @@ struct msf_ctx {
   void* xf_tasks = nullptr;     // XferTask[]
   int* xf_cells = nullptr;      // this rank's cells sorted by class
   double* xf_part = nullptr;    // [R][ncx * ncy][16 G] restriction column sums per cell
+  // Galerkin products by cell class (msf_xfer.cu): element matrices of every class
+  // [class][cx * cy][packed upper triangle], GEMM tile tasks, packed column -> (p, q)
+  double* gal_M = nullptr;
+  int4* gal_tasks = nullptr;
+  int2* gal_pq = nullptr;
+  int gal_ntasks = 0;
   int* factor_status = nullptr; // [2 * MSF_MAX_RHS] nonzero on failed pivot
   bool apply_tma = true;        // operator apply / residual fed by TMA tiles (env MSF_APPLY_TMA=0: off)
   struct TmapSlot {             // cached TMA descriptor (CUtensorMap, 128 B) per base pointer
@@ -337,7 +343,7 @@ void launch_build_basis(msf_ctx* c);
 void launch_assemble_coarse(msf_ctx* c);
 // restriction / prolongation by coarse-cell class (msf_xfer.cu)
 int xfer_setup(msf_ctx* c, char*& cur);
-size_t xfer_workspace_bytes(const Dims& d);
+size_t xfer_workspace_bytes(const Dims& d, const std::vector<int>& cls_of_agg, int C0, int C1);
 void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated);
 // z = zin + R^T c (zin == z: in place)
 void launch_prolong(msf_ctx* c, int rhs0, int nr, const double* zin, double* z, bool gated);

@@ -36,6 +36,9 @@ constexpr int NCC = 64;    // cells per task
 constexpr int CW = NCC / 8, NI = CW / 8;   // cells / 8-cell DMMA tiles per warp
 constexpr int XNJ = 16;    // Phi columns per pass (one column group)
 constexpr int SPJ = 20;    // shared row stride of Phi chunks / coarse coefficients (conflict-free)
+constexpr int GT = 64;     // Galerkin GEMM tile (rows x packed columns)
+constexpr int GK = 32;     // Galerkin GEMM k-chunk (elements)
+constexpr int GPAD = GT + 4;   // shared row stride of the GEMM panels (conflict-free fragments)
 
 struct XferClass {   // device: one coarse-cell class
   int cls[4];        // agglomerate class of corner (di, dj) = (q >> 1, q & 1)
@@ -61,6 +64,7 @@ __device__ __forceinline__ uint32_t xs_u32(const void* p) { return (uint32_t)__c
 __device__ __forceinline__ void xcp16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(xs_u32(dst)), "l"(src) : "memory");
 }
+// D = A B + C on the fp64 tensor cores, m8n8k4 (lane = 4 g + t: A(g, t), B(t, g), C(g, 2t + {0,1}))
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
@@ -330,6 +334,140 @@ __global__ void __launch_bounds__(256) k_restrict_aggs(Dims d, const double* __r
   cball[(size_t)rhs * d.nbc * d.mc + ((size_t)I * (d.ncy + 1) + J) * d.kmax + a] = s;
 }
 
+// ------------------------------------------------------------------ Galerkin cell products
+// Kcell[rhs][cell][p][q] = sum_{e in cell} E_e Phi_e^T K0 Phi_e (Eq. 10, per coarse
+// cell; p, q = corner * k + mode).  For the cells of one class Phi_e is the same, so
+//     Kcell[rhs][cell] = sum_e E[rhs][cell, e] M_k[e],   M_k[e] = Phi_e^T K0 Phi_e,
+// i.e. one GEMM per class, C[(cell, rhs) x pq] = A[(cell, rhs) x e] . B[e x pq], with B the
+// class's element matrices (upper triangle p <= q, packed) -- on the fp64 tensor cores.
+
+// M_k[e][s] for class k, element e = lex * cy + ley of the cell, packed column s = (p, q):
+// V = K0 Phi_e, then M = Phi_e^T V (the arithmetic of the per-element products of round 1)
+__global__ void __launch_bounds__(256) k_galerkin_M(Dims d, K0Mat K, const XferClass* __restrict__ cls,
+                                                    const double* __restrict__ phi,
+                                                    const int2* __restrict__ pq, int psp, double* M) {
+  extern __shared__ double gsm[];
+  const int k = blockIdx.y, e = blockIdx.x, P = 4 * d.kmax;
+  const XferClass C = cls[k];
+  const int lex = e / d.cy, ley = e - (e / d.cy) * d.cy;
+  double* Ph = gsm;            // [8][P]
+  double* V = gsm + 8 * P;     // [8][P]
+  for (int t = threadIdx.x; t < 8 * P; t += blockDim.x) {
+    const int i = t / P, p = t - (t / P) * P;
+    const int b = i >> 1, comp = i & 1;
+    const int lx = lex + ((b == 1 || b == 2) ? 1 : 0), ly = ley + ((b >= 2) ? 1 : 0);
+    const int corner = p / d.kmax, a = p - corner * d.kmax;
+    const int di = corner >> 1, dj = corner & 1;
+    const int px = lx + d.cx * (1 - di), py = ly + d.cy * (1 - dj);
+    Ph[t] = phi[(((size_t)C.cls[corner] * d.kmax + a) * d.box_nodes + px * d.by + py) * 2 + comp];
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 8 * P; t += blockDim.x) {
+    const int i = t / P, q = t - (t / P) * P;
+    double v = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v = fma(K.v[i * 8 + j], Ph[j * P + q], v);
+    V[t] = v;
+  }
+  __syncthreads();
+  double* Mk = M + ((size_t)k * d.cx * d.cy + e) * psp;
+  for (int s = threadIdx.x; s < psp; s += blockDim.x) {
+    const int2 c = pq[s];
+    double t = 0.0;
+    if (c.x >= 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t = fma(Ph[i * P + c.x], V[i * P + c.y], t);
+    }
+    Mk[s] = t;
+  }
+}
+
+// One 64 x 64 tile of C = A B for class k: rows r0 .. r0 + 63 = (class cell, realisation)
+// pairs, packed columns q0 .. q0 + 63; k-chunks of 32 elements staged k-major in shared
+// memory; DMMA m8n8k4, 8 warps as 2 x 4, each a 32 x 16 sub-tile.  C(p, q) goes to Kcell[p][q]
+// and Kcell[q][p].
+__global__ void __launch_bounds__(256) k_galerkin_gemm(Dims d, const XferClass* __restrict__ cls,
+                                                       const int4* __restrict__ tasks,
+                                                       const int* __restrict__ cells,
+                                                       const double* __restrict__ Eall,
+                                                       const double* __restrict__ M,
+                                                       const int2* __restrict__ pq, int psp,
+                                                       double* Kcell) {
+  __shared__ __align__(16) double sA[GK][GPAD];   // A^T chunk: [element][row]
+  __shared__ __align__(16) double sB[GK][GPAD];   // B chunk:   [element][column]
+  __shared__ long long rbase[GT];                 // row -> E offset of its cell (realisation incl.)
+  __shared__ int eoff[GK];
+  const int4 T = tasks[blockIdx.x];
+  const XferClass C = cls[T.x];
+  const int R = d.R, nel = d.cx * d.cy, P = 4 * d.kmax;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  const int m0 = (w >> 2) * 32, n0 = (w & 3) * 16;
+  // rows of this tile: (class cell c, realisation r), row = c * R + r < T.w (= cells x R)
+  for (int m = tid; m < GT; m += 256) {
+    const int row = T.y + m, c = row / R, r = row - c * R;
+    long long b = -1;
+    if (row < T.w) {
+      const int cell = cells[C.cell_off + c];
+      const int CI = cell / d.ncy, CJ = cell - CI * d.ncy;
+      b = (long long)r * d.ne + (long long)(CI * d.cx) * d.nely + CJ * d.cy;
+    }
+    rbase[m] = b;
+  }
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) (&acc[0][0][0])[i] = 0.0;
+  const double* Mk = M + (size_t)T.x * nel * psp + T.z;
+  for (int e0 = 0; e0 < nel; e0 += GK) {
+    __syncthreads();   // rbase ready / previous chunk consumed
+    for (int kk = tid; kk < GK; kk += 256) {
+      const int e = e0 + kk;
+      eoff[kk] = e < nel ? (e / d.cy) * d.nely + (e - (e / d.cy) * d.cy) : -1;
+    }
+    __syncthreads();
+    for (int t = tid; t < GK * GT; t += 256) {
+      const int kk = t / GT, x = t - kk * GT;
+      const long long rb = rbase[x];
+      const int eo = eoff[kk];
+      sA[kk][x] = (rb >= 0 && eo >= 0) ? __ldg(Eall + rb + eo) : 0.0;
+      sB[kk][x] = eo >= 0 ? __ldg(Mk + (size_t)(e0 + kk) * psp + x) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k0 = 0; k0 < GK; k0 += 4) {
+      double a[4], bq[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = sA[k0 + t4][m0 + mi * 8 + g];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) bq[ni] = sB[k0 + t4][n0 + ni * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], bq[ni]);
+    }
+  }
+  // C(g, 2 t4 + h) of fragment (mi, ni): row m0 + mi*8 + g, packed column n0 + ni*8 + 2 t4 + h
+  const size_t cs = (size_t)P * P;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int m = m0 + mi * 8 + g;
+    if (rbase[m] < 0) continue;
+    const int row = T.y + m, c = row / R, r = row - c * R;
+    const int cell = cells[C.cell_off + c];
+    double* Kc = Kcell + ((size_t)r * d.ncx * d.ncy + cell) * cs;
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s = T.z + n0 + ni * 8 + 2 * t4 + h;
+        if (s >= psp) continue;
+        const int2 ij = pq[s];
+        if (ij.x < 0) continue;
+        Kc[(size_t)ij.x * P + ij.y] = acc[mi][ni][h];
+        Kc[(size_t)ij.y * P + ij.x] = acc[mi][ni][h];
+      }
+  }
+}
+
 size_t restrict_smem(const Dims& d) {
   const int ny = d.cy + 1;
   return (2 * (size_t)NCC * tile_stride(ny) + 2 * (size_t)col_pad(ny) * SPJ) * sizeof(double);
@@ -341,22 +479,19 @@ size_t prolong_smem(const Dims& d) {
 
 }  // namespace
 
-// Host plan of the cell-class transfer for this rank's cells [C0, C1) (all cells on one GPU).
-int xfer_setup(msf_ctx* c, char*& cur) {
-  const Dims& d = c->d;
-  const int G = (4 * d.kmax + XNJ - 1) / XNJ;
-  // entry tiles of a pattern column: 2 (cy + 1) <= 56
-  if (G < 1 || G > 4 || 2 * (d.cy + 1) > 56 || prolong_smem(d) > 200 * 1024) return -1;
-  const int C0 = c->sb.C0, C1 = c->sb.C1;
+namespace {
+// Cell classes of the cells [C0, C1) x [0, ncy): key = the four corner agglomerate classes and
+// whether the cell owns the closing node column / row; members in grid order.
+void cell_classes(const Dims& d, const std::vector<int>& cls_of_agg, int C0, int C1,
+                  std::vector<XferClass>& K, std::vector<std::vector<int>>& members) {
   std::map<std::vector<int>, int> key2k;
-  std::vector<XferClass> K;
-  std::vector<std::vector<int>> members;
+  K.clear();
+  members.clear();
   for (int CI = C0; CI < C1; ++CI)
     for (int CJ = 0; CJ < d.ncy; ++CJ) {
       const int lastx = CI == d.ncx - 1, lasty = CJ == d.ncy - 1;
       std::vector<int> key(6);
-      for (int q = 0; q < 4; ++q)
-        key[q] = c->cls_of_agg[(CI + (q >> 1)) * (d.ncy + 1) + CJ + (q & 1)];
+      for (int q = 0; q < 4; ++q) key[q] = cls_of_agg[(CI + (q >> 1)) * (d.ncy + 1) + CJ + (q & 1)];
       key[4] = lastx;
       key[5] = lasty;
       auto it = key2k.find(key);
@@ -375,15 +510,44 @@ int xfer_setup(msf_ctx* c, char*& cur) {
       }
       members[k].push_back(CI * d.ncy + CJ);
     }
+}
+
+// Galerkin GEMM layout: packed upper-triangle column count (P = 4k) padded to whole 64-column
+// tiles; row tiles of 64 (cell, realisation) pairs
+int gal_psp(const Dims& d) {
+  const int P = 4 * d.kmax, PS = P * (P + 1) / 2;
+  return (PS + GT - 1) / GT * GT;
+}
+}  // namespace
+
+// Host plan of the cell-class transfer and Galerkin products for this rank's cells [C0, C1)
+// (all cells on one GPU).
+int xfer_setup(msf_ctx* c, char*& cur) {
+  const Dims& d = c->d;
+  const int G = (4 * d.kmax + XNJ - 1) / XNJ;
+  // entry tiles of a pattern column: 2 (cy + 1) <= 56
+  if (G < 1 || G > 4 || 2 * (d.cy + 1) > 56 || prolong_smem(d) > 200 * 1024) return -1;
+  std::vector<XferClass> K;
+  std::vector<std::vector<int>> members;
+  cell_classes(d, c->cls_of_agg, c->sb.C0, c->sb.C1, K, members);
   std::vector<int> cells;
   std::vector<XferTask> tasks;
+  std::vector<int4> gtasks;   // Galerkin GEMM tiles: (class, first row, first column, -)
+  const int R = d.R, psp = gal_psp(d);
   for (size_t k = 0; k < K.size(); ++k) {
     K[k].cell_off = (int)cells.size();
     cells.insert(cells.end(), members[k].begin(), members[k].end());
     const int ncell = (int)members[k].size();
     for (int c0 = 0; c0 < ncell; c0 += NCC)
       tasks.push_back(XferTask{(int)k, c0, std::min(NCC, ncell - c0), 0});
+    for (int r0 = 0; r0 < ncell * R; r0 += GT)
+      for (int q0 = 0; q0 < psp; q0 += GT) gtasks.push_back(make_int4((int)k, r0, q0, ncell * R));
   }
+  // packed upper triangle: column s -> (p, q), p <= q
+  const int P = 4 * d.kmax;
+  std::vector<int2> pq(psp, make_int2(-1, -1));
+  for (int p = 0, s = 0; p < P; ++p)
+    for (int q = p; q < P; ++q) pq[s++] = make_int2(p, q);
   auto take = [&](size_t bytes) {
     char* r = cur;
     cur += (bytes + 255) & ~(size_t)255;
@@ -396,21 +560,36 @@ int xfer_setup(msf_ctx* c, char*& cur) {
   c->xf_tasks = take(tasks.size() * sizeof(XferTask));
   c->xf_cells = (int*)take(cells.size() * 4);
   c->xf_part = (double*)take((size_t)d.R * d.ncx * d.ncy * G * XNJ * 8);
+  c->gal_ntasks = (int)gtasks.size();
+  c->gal_tasks = (int4*)take(gtasks.size() * sizeof(int4));
+  c->gal_pq = (int2*)take(pq.size() * sizeof(int2));
+  c->gal_M = (double*)take(K.size() * (size_t)d.cx * d.cy * psp * 8);
   cudaFuncSetAttribute(k_prolong_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prolong_smem(d));
   cudaFuncSetAttribute(k_restrict_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)restrict_smem(d));
   cudaError_t e = cudaMemcpyAsync(c->xf_cls, K.data(), K.size() * sizeof(XferClass), cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->xf_tasks, tasks.data(), tasks.size() * sizeof(XferTask), cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->xf_cells, cells.data(), cells.size() * 4, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->gal_tasks, gtasks.data(), gtasks.size() * sizeof(int4), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->gal_pq, pq.data(), pq.size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream);
   return e == cudaSuccess ? 0 : -2;
 }
 
-size_t xfer_workspace_bytes(const Dims& d) {
+size_t xfer_workspace_bytes(const Dims& d, const std::vector<int>& cls_of_agg, int C0, int C1) {
   const int G = (4 * d.kmax + XNJ - 1) / XNJ;
+  std::vector<XferClass> K;
+  std::vector<std::vector<int>> members;
+  cell_classes(d, cls_of_agg, C0, C1, K, members);
+  size_t ntask = 0, ngt = 0;
+  const int psp = gal_psp(d);
+  for (const auto& m : members) {
+    ntask += (m.size() + NCC - 1) / NCC;
+    ngt += ((m.size() * d.R + GT - 1) / GT) * (psp / GT);
+  }
   const size_t ncell = (size_t)d.ncx * d.ncy;
-  // worst case: one class per cell, one task per cell
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  return al(ncell * sizeof(XferClass)) + al(ncell * sizeof(XferTask)) + al(ncell * 4) +
-         al((size_t)d.R * ncell * G * XNJ * 8);
+  return al(K.size() * sizeof(XferClass)) + al(ntask * sizeof(XferTask)) + al(ncell * 4) +
+         al((size_t)d.R * ncell * G * XNJ * 8) + al(ngt * sizeof(int4)) + al(psp * sizeof(int2)) +
+         al(K.size() * (size_t)d.cx * d.cy * psp * 8);
 }
 
 void launch_prolong(msf_ctx* c, int rhs0, int nr, const double* zin, double* z, bool gated) {
@@ -432,5 +611,20 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
   launch_k(k_restrict_aggs, dim3((naggs * d.kmax + 255) / 256, nr), dim3(256), 0, c->stream, d,
            (const double*)c->xf_part, c->xf_G * XNJ, c->cr_lo, c->cr_hi, c->sb.C0, c->sb.C1, c->cb,
            (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
+  MSF_LAUNCHED(c);
+}
+
+// Galerkin cell products Kcell = Phi_C^T (E K0) Phi_C of this rank's coarse cells (Eq. 10),
+// all realisations: the class element matrices M_k, then one DMMA GEMM tile per task
+void launch_galerkin_cells(msf_ctx* c) {
+  const Dims& d = c->d;
+  const int psp = gal_psp(d), P = 4 * d.kmax;
+  k_galerkin_M<<<dim3(d.cx * d.cy, c->xf_n_cls), 256, 16 * P * sizeof(double), c->stream>>>(
+      d, c->K0, (const XferClass*)c->xf_cls, (const double*)c->phi, (const int2*)c->gal_pq, psp,
+      c->gal_M);
+  MSF_LAUNCHED(c);
+  k_galerkin_gemm<<<dim3(c->gal_ntasks), 256, 0, c->stream>>>(
+      d, (const XferClass*)c->xf_cls, (const int4*)c->gal_tasks, (const int*)c->xf_cells,
+      (const double*)c->E, (const double*)c->gal_M, (const int2*)c->gal_pq, psp, c->Kcell);
   MSF_LAUNCHED(c);
 }

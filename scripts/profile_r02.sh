@@ -17,11 +17,11 @@ if [ "${1:-A}" = A ]; then
   gzip -f $O/launches_step.csv
   cap sgs_pre 'k_sgs_stream<\(bool\)1, \(bool\)1' 0 1
   cap sgs_post 'k_sgs_stream<\(bool\)0, \(bool\)0, \(bool\)0' 1 1
-  cap apply 'k_apply_tma<0' 1 1
-  cap residual 'k_apply_tma<1' 1 1
   cap restrict 'k_restrict_cells' 1 1
   cap prolong 'k_prolong_cells' 1 1
 else
+  cap apply 'k_apply_tma<\(int\)0' 1 1
+  cap residual 'k_apply_tma<\(int\)1' 1 1
   cap pcg_p 'k_pcg_p' 1 1
   cap nd_solve 'k_nd_solve' 0 6
   cap nd_factor 'k_nd_trailing|k_nd_panels|k_nd_rowpanel|k_nd_pivot|k_nd_assemble' 0 8
