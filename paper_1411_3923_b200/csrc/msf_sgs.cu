@@ -61,45 +61,48 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Two nodes (buffer rows ly0, ly1 of one column) of phase (FWD, BWD, Z0) at ring slots
-// (c-1, c, c+1), computed together so that their independent FMA chains interleave.  A node
-// whose DOFs are both fixed (or outside the grid) comes back unchanged from gs_node.
-template <bool Z0>
-__device__ __forceinline__ void sg_gather(const SgRing& S, int sm, int s0, int sp, int ly,
+// The moduli and the 3x3 neighbourhood of the node at plane index k of row parity YP (buffer
+// row ly = 2 k + YP) at ring slots (c-1, c, c+1).  With YP a template parameter the parity
+// planes of rows ly-1 / ly / ly+1 are compile-time, so every load is a slot base plus an
+// immediate offset (the row arithmetic per load was the largest integer cost of the sweep).
+template <bool Z0, int YP>
+__device__ __forceinline__ void sg_gather(const SgRing& S, int sm, int s0, int sp, int k,
                                           double (&Eloc)[2][2], double2 (&zloc)[3][3]) {
-  const int pl = ly & 1, k = ly >> 1;
-  const int pm = (ly - 1) & 1, km = (ly - 1) >> 1, pp = (ly + 1) & 1, kp = (ly + 1) >> 1;
-  Eloc[0][0] = S.e[sm][pm][km];
-  Eloc[0][1] = S.e[sm][pl][k];
-  Eloc[1][0] = S.e[s0][pm][km];
-  Eloc[1][1] = S.e[s0][pl][k];
+  constexpr int PM = 1 - YP, DM = YP - 1, DP = YP;   // row ly-1 / ly+1: plane 1-YP, k+DM / k+DP
+  Eloc[0][0] = S.e[sm][PM][k + DM];
+  Eloc[0][1] = S.e[sm][YP][k];
+  Eloc[1][0] = S.e[s0][PM][k + DM];
+  Eloc[1][1] = S.e[s0][YP][k];
   if (Z0) {
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int b = 0; b < 3; ++b) zloc[a][b] = make_double2(0.0, 0.0);
   } else {
-    zloc[0][0] = S.z[sm][pm][km];
-    zloc[0][1] = S.z[sm][pl][k];
-    zloc[0][2] = S.z[sm][pp][kp];
-    zloc[1][0] = S.z[s0][pm][km];
-    zloc[1][1] = S.z[s0][pl][k];
-    zloc[1][2] = S.z[s0][pp][kp];
-    zloc[2][0] = S.z[sp][pm][km];
-    zloc[2][1] = S.z[sp][pl][k];
-    zloc[2][2] = S.z[sp][pp][kp];
+    zloc[0][0] = S.z[sm][PM][k + DM];
+    zloc[0][1] = S.z[sm][YP][k];
+    zloc[0][2] = S.z[sm][PM][k + DP];
+    zloc[1][0] = S.z[s0][PM][k + DM];
+    zloc[1][1] = S.z[s0][YP][k];
+    zloc[1][2] = S.z[s0][PM][k + DP];
+    zloc[2][0] = S.z[sp][PM][k + DM];
+    zloc[2][1] = S.z[sp][YP][k];
+    zloc[2][2] = S.z[sp][PM][k + DP];
   }
 }
 
-template <bool FWD, bool BWD, bool Z0>
+// Two nodes (plane indices k0, k1 of row parity YP in one column) of phase (FWD, BWD, Z0) at
+// ring slots (c-1, c, c+1), computed together so that their independent FMA chains
+// interleave.  A node whose DOFs are both fixed (or outside the grid) comes back unchanged.
+template <bool FWD, bool BWD, bool Z0, int YP>
 __device__ __forceinline__ void sg_node2(const K0Mat& K, SgRing& S, int sm, int s0, int sp,
-                                         int ly0, int ly1, bool v0, bool v1) {
+                                         int k0, int k1, bool v0, bool v1) {
   double E0[2][2], E1[2][2];
   double2 z0[3][3], z1[3][3];
-  sg_gather<Z0>(S, sm, s0, sp, ly0, E0, z0);
-  sg_gather<Z0>(S, sm, s0, sp, ly1, E1, z1);
-  const double2 r0 = S.r[s0][ly0 & 1][ly0 >> 1], r1 = S.r[s0][ly1 & 1][ly1 >> 1];
-  const uint8_t f0 = S.f[s0][ly0 & 1][ly0 >> 1], f1 = S.f[s0][ly1 & 1][ly1 >> 1];
+  sg_gather<Z0, YP>(S, sm, s0, sp, k0, E0, z0);
+  sg_gather<Z0, YP>(S, sm, s0, sp, k1, E1, z1);
+  const double2 r0 = S.r[s0][YP][k0], r1 = S.r[s0][YP][k1];
+  const uint8_t f0 = S.f[s0][YP][k0], f1 = S.f[s0][YP][k1];
 #ifdef MSF_SGS_EXP_NOCOMPUTE   // A/B experiment: the sweep's data movement alone
   const double2 n0 = make_double2(z0[1][1].x + E0[0][0] + r0.x + f0, z0[0][0].y + z0[2][2].y + E0[1][1] + E1[0][1]);
   const double2 n1 = make_double2(z1[1][1].x + E1[0][0] + r1.x + f1, z1[0][0].y + z1[2][2].y + E1[1][1] + E0[1][0]);
@@ -107,8 +110,8 @@ __device__ __forceinline__ void sg_node2(const K0Mat& K, SgRing& S, int sm, int 
   const double2 n0 = gs_node<FWD, BWD, Z0>(K, E0, z0, r0, f0);
   const double2 n1 = gs_node<FWD, BWD, Z0>(K, E1, z1, r1, f1);
 #endif
-  if (v0) S.z[s0][ly0 & 1][ly0 >> 1] = n0;
-  if (v1) S.z[s0][ly1 & 1][ly1 >> 1] = n1;
+  if (v0) S.z[s0][YP][k0] = n0;
+  if (v1) S.z[s0][YP][k1] = n1;
 }
 
 template <bool ZERO, bool UPD, bool RZ>
@@ -255,12 +258,15 @@ __global__ void __launch_bounds__(SG_T, 2)
         const int s0 = wrap(sl - 2 * ph), sm = s0 == 0 ? SG_NR - 1 : s0 - 1, sp = s0 == SG_NR - 1 ? 0 : s0 + 1;
         const int ly0 = odd ? ly01 : ly00, ly1 = odd ? ly11 : ly10;
         const bool vA = odd ? vA1 : vA0, vB = odd ? vB1 : vB0;
+        // colour rows: phases 1, 2, 6, 7 (colours 0, 1) even, phases 3, 4, 5 (colours 2, 3) odd
+        const int k0 = ly0 >> 1, k1 = ly1 >> 1;
         switch (ph) {
-          case 1: sg_node2<true, false, ZERO>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
-          case 2:
-          case 3: sg_node2<true, false, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
-          case 4: sg_node2<true, true, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
-          default: sg_node2<false, true, false>(K, S, sm, s0, sp, ly0, ly1, vA, vB); break;
+          case 1: sg_node2<true, false, ZERO, 0>(K, S, sm, s0, sp, k0, k1, vA, vB); break;
+          case 2: sg_node2<true, false, false, 0>(K, S, sm, s0, sp, k0, k1, vA, vB); break;
+          case 3: sg_node2<true, false, false, 1>(K, S, sm, s0, sp, k0, k1, vA, vB); break;
+          case 4: sg_node2<true, true, false, 1>(K, S, sm, s0, sp, k0, k1, vA, vB); break;
+          case 5: sg_node2<false, true, false, 1>(K, S, sm, s0, sp, k0, k1, vA, vB); break;
+          default: sg_node2<false, true, false, 0>(K, S, sm, s0, sp, k0, k1, vA, vB); break;
         }
       }
     }
