@@ -31,9 +31,16 @@ using namespace msfk;
 
 namespace {
 
-constexpr int XT = 256;    // threads per CTA: 8 warps x CW cells
-constexpr int NCC = 64;    // cells per task
-constexpr int CW = NCC / 8, NI = CW / 8;   // cells / 8-cell DMMA tiles per warp
+#ifndef MSF_XFER_XT
+#define MSF_XFER_XT 256
+#endif
+#ifndef MSF_XFER_NCC
+#define MSF_XFER_NCC 64
+#endif
+constexpr int XT = MSF_XFER_XT;    // threads per CTA: XT / 32 warps x CW cells
+constexpr int NCC = MSF_XFER_NCC;  // cells per task
+constexpr int CW = NCC / (XT / 32), NI = CW / 8;   // cells / 8-cell DMMA tiles per warp
+static_assert(NI >= 1 && CW % 8 == 0, "each warp takes whole 8-cell DMMA tiles");
 constexpr int XNJ = 16;    // Phi columns per pass (one column group)
 constexpr int SPJ = 20;    // shared row stride of Phi chunks / coarse coefficients (conflict-free)
 constexpr int GT = 64;     // Galerkin GEMM tile (rows x packed columns)

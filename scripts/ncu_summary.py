@@ -17,7 +17,7 @@ def units_scale(u, v):
     u = u.strip()
     if u in ("nsecond", "ns"): return v
     if u in ("usecond", "us"): return v * 1e3
-    if u in ("msecond",): return v * 1e6
+    if u in ("msecond", "ms"): return v * 1e6
     if u in ("byte",): return v
     if u in ("Kbyte", "KB"): return v * 1e3
     if u in ("Mbyte", "MB"): return v * 1e6
