@@ -321,11 +321,13 @@ def run_ours(args, spec):
     dom_ms, dom_bytes = kb[dom]
     peak, peak_src = hbm_peak()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-    traffic = None
+    traffic = fp64_frac = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(dom)
+            tj = json.load(open(tfile))
+            traffic = tj.get(dom)
+            fp64_frac = tj.get(dom + "_fp64_pipe_frac")
         except Exception:
             traffic = None
     inf = m.info()
@@ -356,6 +358,8 @@ def run_ours(args, spec):
         "roofline": {"kernel": KERNEL_NAMES.get(dom, dom),
                      "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     # the sweeps are FP64-issue/latency-bound, not HBM-bound: ncu FP64 pipe share
+                     "ncu_fp64_pipe_frac": fp64_frac,
                      "alg_bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
                      "peak_source": peak_src},
         # every timed kernel (all realisations active, PCG launch configuration): average ms per
