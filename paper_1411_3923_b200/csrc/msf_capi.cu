@@ -203,7 +203,7 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     }
   }
   P.max_partials = std::max({apply_partials_needed(d), sgs_colour_partials_needed(d),
-                             sgs_stream_partials_needed(P.dl)});
+                             sgs_stream_partials_needed(P.dl), sgs_warp_partials_needed(P.dl)});
 
   // workspace size (node vectors on this rank's strip; moduli of the whole grid)
   const size_t R = d.R, nn = P.dl.nn, ne = d.ne, nt = d.nt;
@@ -406,6 +406,7 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   }
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
   if (const char* e = std::getenv("MSF_APPLY_TMA")) c->apply_tma = std::string(e) != "0";
+  if (const char* e = std::getenv("MSF_SGS_WARP")) c->sgs_warp = std::string(e) != "0";
   {
     const char* e = std::getenv("MSF_PDL");   // read at every setup (tests toggle it)
     g_msf_pdl = !(e && std::string(e) == "0");

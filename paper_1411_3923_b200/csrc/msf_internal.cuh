@@ -233,6 +233,7 @@ struct msf_ctx {
   int2* gal_pq = nullptr;
   int gal_ntasks = 0;
   int* factor_status = nullptr; // [2 * MSF_MAX_RHS] nonzero on failed pivot
+  bool sgs_warp = true;         // sweeps by k_sgs_warp (env MSF_SGS_WARP=0: k_sgs_stream)
   bool apply_tma = true;        // operator apply / residual fed by TMA tiles (env MSF_APPLY_TMA=0: off)
   struct TmapSlot {             // cached TMA descriptor (CUtensorMap, 128 B) per base pointer
     const void* ptr;
@@ -321,6 +322,11 @@ void launch_pcg_p(msf_ctx* c, int rhs0, int nr, int mode);
 void launch_sgs_stream(msf_ctx* c, int rhs0, int nr, const double* r, double* rout,
                        const double* zin, double* z, bool gated, bool zero_start, bool upd,
                        int rz_mode);
+// the same sweep with the iterate in registers, one warp per band (msf_sgsw.cu)
+void launch_sgs_warp(msf_ctx* c, int rhs0, int nr, const double* r, double* rout,
+                     const double* zin, double* z, bool gated, bool zero_start, bool upd,
+                     int rz_mode);
+int sgs_warp_partials_needed(const Dims& d);
 void sgs_fix_layout(const Dims& d, int& fs_col, int& fs_plane);
 void sgs_fix_build(const Dims& d, const uint8_t* fixn, std::vector<uint8_t>& out);
 int sgs_stream_partials_needed(const Dims& d);

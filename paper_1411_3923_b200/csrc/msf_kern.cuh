@@ -57,7 +57,10 @@ __device__ __forceinline__ constexpr int K0_IDX(int i, int j) {
 // SYM: the pivot block's lower row is taken from its upper one (make_K0: K0 is bitwise
 // symmetric with equal diagonal entries, so this is bitwise the same result with 8 fewer
 // FMAs; the choice only moves register allocation, see launch_sgs_phase).
-template <bool SYM = true>
+// NZ: bit 3 i + j set = z[i][j] may be nonzero.  A term whose z is exactly +0 leaves its
+// accumulator bitwise unchanged (acc + K * 0 = acc), so a caller that KNOWS a neighbour is still
+// zero (the first forward phases of a sweep from z = 0) may drop its bit: same result, fewer FMAs.
+template <bool SYM = true, int NZ = 0x1ff>
 __device__ __forceinline__ void apply_node(const K0Mat& K, const double (&E)[2][2],
                                            const double2 (&z)[3][3], double& ox, double& oy,
                                            double& dxx, double& dxy, double& dyx, double& dyy) {
@@ -70,6 +73,7 @@ __device__ __forceinline__ void apply_node(const K0Mat& K, const double (&E)[2][
       double ax = 0.0, ay = 0.0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
+        if (!((NZ >> (3 * (sx + DXB(b)) + sy + DYB(b))) & 1)) continue;
         const double2 v = z[sx + DXB(b)][sy + DYB(b)];
         ax = fma(MSF_K0(K, 2 * a, 2 * b), v.x, ax);
         ax = fma(MSF_K0(K, 2 * a, 2 * b + 1), v.y, ax);
@@ -224,7 +228,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // entry, fm its Dirichlet bits.  ZERO: z = 0 around the node, only the pivot block is needed.
 // Shared by the colour-phase kernels and the streaming sweep (msf_sgs.cu), so both execute
 // the same arithmetic.  Per-thread.
-template <bool FWD, bool BWD, bool ZERO>
+template <bool FWD, bool BWD, bool ZERO, int NZ = 0x1ff>
 __device__ __forceinline__ double2 gs_node(const K0Mat& K, const double (&Eloc)[2][2],
                                          const double2 (&zloc)[3][3], double2 rv, uint8_t fm) {
   double ox, oy, dxx, dxy, dyx, dyy;
@@ -235,7 +239,7 @@ __device__ __forceinline__ double2 gs_node(const K0Mat& K, const double (&Eloc)[
     dyx = dxy;
     dyy = dxx;
   } else {
-    apply_node<true>(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
+    apply_node<true, NZ>(K, Eloc, zloc, ox, oy, dxx, dxy, dyx, dyy);
   }
   double2 zn = zloc[1][1];
   double rx = rv.x - ox, ry = rv.y - oy;

@@ -314,6 +314,10 @@ size_t sgs_stream_smem() { return SG_SMEM; }
 void launch_sgs_stream(msf_ctx* c, int rhs0, int nr, const double* r, double* rout,
                        const double* zin, double* z, bool gated, bool zero_start, bool upd,
                        int rz_mode) {
+  if (c->sgs_warp && (long long)c->dl.nnx * c->fs_col < (1ll << 31)) {   // 32-bit indices there
+    launch_sgs_warp(c, rhs0, nr, r, rout, zin, z, gated, zero_start, upd, rz_mode);
+    return;
+  }
   const Dims& d = c->dl;
   const int nyb = (d.nny + SG_IN - 1) / SG_IN;
   // one wave at 2 CTAs per SM; runs of at least 32 columns
