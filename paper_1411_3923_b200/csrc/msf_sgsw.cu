@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(SW_T, SW_WARPS)
                const double2* __restrict__ qall, const uint8_t* __restrict__ fixs, int fs_col,
                int fs_plane, PcgScalars* sc, double* partials, unsigned* counters, int max_partials,
                double* dsum, const double* __restrict__ apart, int napart, int rhs0, int gated,
-               int rz_mode, int nyb, int nxs) {
+               int rz_mode, int nyb, int nxb, int nextra) {
   extern __shared__ __align__(16) unsigned char sw_raw[];
   __shared__ double red[SW_T / 32 + 1];
   pdl_wait();
@@ -146,7 +146,18 @@ __global__ void __launch_bounds__(SW_T, SW_WARPS)
   double dot = 0.0;
   const int unit = blockIdx.x;   // (band, column run) of this warp
   {
-    const int ib = unit % nyb, ir = unit / nyb;
+    // bands [0, nextra) are cut into nxb + 1 column runs, the others into nxb (the grid fills the
+    // resident warp slots of the device exactly); consecutive CTAs take neighbouring bands of the
+    // same run, whose halo rows they share through L2
+    int ib, ir;
+    if (unit < nxb * nyb) {
+      ir = unit / nyb;
+      ib = unit - ir * nyb;
+    } else {
+      ir = nxb;
+      ib = unit - nxb * nyb;
+    }
+    const int nxs = ib < nextra ? nxb + 1 : nxb;
     const int Y0 = ib * SW_BAND, Yb = Y0 - SW_LO;   // Yb even: lane row parity = node row parity
     const int X0 = (int)((long long)ir * d.nnx / nxs), X1 = (int)((long long)(ir + 1) * d.nnx / nxs);
     const double* E = Eall + (size_t)rhs * d.estride;
@@ -324,10 +335,11 @@ void launch_sgs_warp(msf_ctx* c, int rhs0, int nr, const double* r, double* rout
   const Dims& d = c->dl;
   const int nyb = (d.nny + SW_BAND - 1) / SW_BAND;
   // one wave of SW_WARPS one-warp CTAs per SM; runs of at least 32 columns
-  int nxs = std::max(1, (c->n_sm * SW_WARPS) / (nyb * nr));
-  nxs = std::min(nxs, std::max(1, d.nnx / 32));
-  nxs = std::min(nxs, std::max(1, c->max_partials / nyb));   // one partial per CTA
-  const int nblk = nyb * nxs;
+  int units = std::max(nyb, (c->n_sm * SW_WARPS) / nr);
+  units = std::min(units, nyb * std::max(1, d.nnx / 32));
+  units = std::min(units, std::max(nyb, c->max_partials));   // one partial per CTA
+  const int nxb = units / nyb, nextra = units - nxb * nyb;
+  const int nblk = units;
   const dim3 grid(nblk, nr);
   int napart = 0;
   if (upd) {
@@ -346,7 +358,7 @@ void launch_sgs_warp(msf_ctx* c, int rhs0, int nr, const double* r, double* rout
              (const double*)c->E_loc, (const double2*)r, (double2*)rout,                         \
              (const double2*)(zero_start ? z : zin), (double2*)z, (const double2*)c->q, c->fixs, \
              c->fs_col, c->fs_plane, c->sc, c->partials, c->counters, c->max_partials, c->dsum,  \
-             (const double*)c->apart, napart, rhs0, gated ? 1 : 0, rz_mode, nyb, nxs);           \
+             (const double*)c->apart, napart, rhs0, gated ? 1 : 0, rz_mode, nyb, nxb, nextra);           \
   } while (0)
   if (zero_start) {
     if (upd) MSF_SW(true, true, false);
