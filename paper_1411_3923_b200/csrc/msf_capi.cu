@@ -120,7 +120,7 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   d.gox = 0; d.own_lo = 0; d.own_hi = d.nnx; d.estride = d.ne;
   // this rank's strip (the whole grid on one GPU)
   if (nranks == 1 && rank == 0) {
-    P.sb = StripBounds{0, d.nnx, 0, d.nnx, 0, d.nelx, 0, d.ncx};
+    P.sb = StripBounds{1, 0, d.nnx, 0, d.nnx, 0, d.nelx, 0, d.ncx};
   } else if ((rc = strip_bounds(d, rank, nranks, P.sb, msg))) {
     return rc;
   }
@@ -426,17 +426,20 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   // them untouched and they drop out of every dot product; their values come from the
   // neighbour's halo exchange.  Kernels never mask their inputs, so the owned stencils see
   // the halo values.)
-  std::vector<uint8_t> fixn(nn);
+  // The streaming sweep of a wide-halo strip recomputes the neighbour's updates on its halo
+  // columns, so its mask layout (fixs) carries the TRUE Dirichlet bits there.
+  std::vector<uint8_t> fixn(nn), fixt(nn);
   std::vector<double> floc(2 * nn, 0.0);
   const size_t nny = d.nny, goff = (size_t)c->dl.gox * nny;
   for (size_t n = 0; n < nn; ++n) {
     const int lx = (int)(n / nny);
+    const size_t g = goff + n;
+    fixt[n] = (fixed_mask[2 * g] ? 1 : 0) | (fixed_mask[2 * g + 1] ? 2 : 0);
     if (lx < c->dl.own_lo || lx >= c->dl.own_hi) {
       fixn[n] = 3;
       continue;
     }
-    const size_t g = goff + n;
-    fixn[n] = (fixed_mask[2 * g] ? 1 : 0) | (fixed_mask[2 * g + 1] ? 2 : 0);
+    fixn[n] = fixt[n];
     floc[2 * n] = load[2 * g];
     floc[2 * n + 1] = load[2 * g + 1];
   }
@@ -445,7 +448,7 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   ce = cudaMemcpyAsync(c->fixn, fixn.data(), nn, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->fixg, fixg.data(), d.nn, cudaMemcpyHostToDevice, c->stream);
   std::vector<uint8_t> fixs;
-  sgs_fix_build(c->dl, fixn.data(), fixs);
+  sgs_fix_build(c->dl, c->sb.halo > 1 ? fixt.data() : fixn.data(), fixs);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->fixs, fixs.data(), fixs.size(), cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->f, floc.data(), 2 * nn * 8, cudaMemcpyHostToDevice, c->stream);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(c->filt_w_d, P.fw.data(), P.fw.size() * 8, cudaMemcpyHostToDevice, c->stream);
@@ -624,12 +627,12 @@ static int dist_sgs(const Ranks& cs, int rhs0, int nr, int first, int rz_mode) {
 // agglomerates of its chain (partial sums on the two interface columns) and solves the fronts
 // of its own box; the interface fronts' right-hand sides (partial restriction + box-root
 // updates) are all-reduced, the interface fronts solved on every rank, then each rank
-// back-substitutes its box and prolongs onto its owned nodes; the left halo column needs the
-// neighbour's chain, so z's halo is exchanged.
-static int dist_coarse(const Ranks& cs, int rhs0, int nr) {
+// back-substitutes its box and prolongs onto its owned nodes (zout = z: in place, then z's
+// halo column is exchanged; zout = t: the wide-halo path exchanges t itself).
+static int dist_coarse(const Ranks& cs, int rhs0, int nr, double* msf_ctx::*rvec, bool wide) {
   int rc;
   for (msf_ctx* c : cs) {
-    launch_residual(c, rhs0, nr, c->r, c->z, c->t, true);
+    launch_residual(c, rhs0, nr, c->*rvec, c->z, c->t, true);
     launch_restrict(c, rhs0, nr, c->t, true);
     launch_nd_solve_local_fwd(c, rhs0, nr, true);
   }
@@ -638,17 +641,49 @@ static int dist_coarse(const Ranks& cs, int rhs0, int nr) {
   for (msf_ctx* c : cs) {
     launch_nd_solve_top(c, rhs0, nr, true);
     launch_nd_solve_local_back(c, rhs0, nr, true);
-    launch_prolong(c, rhs0, nr, c->z, c->z, true);
+    launch_prolong(c, rhs0, nr, c->z, wide ? c->t : c->z, true);
   }
-  if (cs[0]->nranks > 1) return dist_halo(cs, &msf_ctx::z, rhs0, nr);
+  if (cs[0]->nranks > 1)
+    return wide ? dist_halo(cs, &msf_ctx::t, rhs0, nr, MSF_STRIP_HALO) : dist_halo(cs, &msf_ctx::z, rhs0, nr);
   return MSF_OK;
 }
 
 static int dist_vcycle(const Ranks& cs, int rhs0, int nr, bool f0_done, int rz_mode) {
   int rc;
   if ((rc = dist_sgs(cs, rhs0, nr, f0_done ? 2 : 0, 0))) return rc;
-  if ((rc = dist_coarse(cs, rhs0, nr))) return rc;
+  if ((rc = dist_coarse(cs, rhs0, nr, &msf_ctx::r, false))) return rc;
   return dist_sgs(cs, rhs0, nr, 1, rz_mode);
+}
+
+// Wide-halo strips (every strip >= MSF_STRIP_HALO node columns): the V-cycle of the one-GPU
+// path, each symmetric sweep ONE streaming kernel over the owned columns.  The sweep reads its
+// 7-column dependency halo of the inputs from the strip's halo columns (exchanged ONCE per
+// sweep) and recomputes the neighbour's updates there, exactly as neighbouring column runs do
+// on one GPU, so every owned value is bitwise the one-GPU one.
+//   z = SGS(0; r); t = z + R^T K_c^{-1} R (r - K z); z = SGS(t; r)
+// rin: the residual; rout != null: the PCG update rout = rin - alpha q fused into the
+// pre-smoothing (q's halo exchanged first; the sweep also writes rout on its halo columns, so
+// the residual's halo stays valid without an exchange of its own).
+static int dist_vcycle_wide(const Ranks& cs, int rhs0, int nr, double* msf_ctx::*rin,
+                            double* msf_ctx::*rout, bool gated, int rz_mode) {
+  int rc;
+  const int W = MSF_STRIP_HALO;
+  const bool upd = rout != nullptr;
+  if (upd) {
+    if ((rc = dist_halo(cs, &msf_ctx::q, rhs0, nr, W))) return rc;
+  } else if ((rc = dist_halo(cs, rin, rhs0, nr, W))) {
+    return rc;
+  }
+  for (msf_ctx* c : cs)
+    launch_sgs_stream(c, rhs0, nr, c->*rin, upd ? c->*rout : nullptr, nullptr, c->z, gated, true, upd, 0);
+  double* msf_ctx::*rv = upd ? rout : rin;
+  if (upd && (rc = dist_reduce(cs, FIN_RR, rhs0, nr, true, 0))) return rc;
+  if ((rc = dist_halo(cs, &msf_ctx::z, rhs0, nr))) return rc;          // the residual's stencil
+  if ((rc = dist_coarse(cs, rhs0, nr, rv, true))) return rc;            // t = z + R^T K_c^{-1} R (r - K z)
+  for (msf_ctx* c : cs)
+    launch_sgs_stream(c, rhs0, nr, c->*rv, nullptr, c->t, c->z, gated, false, false, rz_mode);
+  if (rz_mode && (rc = dist_reduce(cs, FIN_RZ, rhs0, nr, true, rz_mode))) return rc;
+  return dist_halo(cs, &msf_ctx::z, rhs0, nr, W);   // p = z + beta p on every local column
 }
 
 // K_c assembly + factorisation on a strip partition: Galerkin products of the owned cells,
@@ -678,10 +713,18 @@ static int dist_assemble(const Ranks& cs) {
   return MSF_OK;
 }
 
-static int dist_iteration(const Ranks& cs, int rhs0, int nr) {
+static int dist_iteration(const Ranks& cs, int rhs0, int nr, int parity) {
   int rc;
   for (msf_ctx* c : cs) launch_matvec(c, rhs0, nr, c->pv, c->q, true, true);
   if ((rc = dist_reduce(cs, FIN_PQ, rhs0, nr, true, 0))) return rc;
+  if (cs[0]->sb.halo > 1) {
+    // wide halos: the one-GPU iteration (residual alternating between r and r2)
+    double* msf_ctx::*ra = parity ? &msf_ctx::r2 : &msf_ctx::r;
+    double* msf_ctx::*rb = parity ? &msf_ctx::r : &msf_ctx::r2;
+    if ((rc = dist_vcycle_wide(cs, rhs0, nr, ra, rb, true, 2))) return rc;
+    for (msf_ctx* c : cs) launch_pcg_p(c, rhs0, nr, 1);   // u += alpha p, p = z + beta p
+    return MSF_OK;
+  }
   for (msf_ctx* c : cs) launch_update_f0(c, rhs0, nr);
   if ((rc = dist_reduce(cs, FIN_RR, rhs0, nr, true, 0))) return rc;
   if ((rc = dist_halo(cs, &msf_ctx::z, rhs0, nr))) return rc;
@@ -691,9 +734,9 @@ static int dist_iteration(const Ranks& cs, int rhs0, int nr) {
 }
 
 // graph of one strip-partition iteration for realisations [rhs0, rhs0 + nr) (kernels + NCCL)
-static int dist_range_graph(const Ranks& cs, int rhs0, int nr, cudaGraphExec_t* out) {
+static int dist_range_graph(const Ranks& cs, int rhs0, int nr, int parity, cudaGraphExec_t* out) {
   msf_ctx* c = cs[0];
-  cudaGraphExec_t& slot = c->range_graph[0][rhs0][nr];
+  cudaGraphExec_t& slot = c->range_graph[parity][rhs0][nr];
   if (!slot) {
     cudaGraph_t g;
     cudaStream_t user = c->stream;
@@ -701,7 +744,7 @@ static int dist_range_graph(const Ranks& cs, int rhs0, int nr, cudaGraphExec_t* 
     cudaError_t e1 = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
     const long long before = c->launches;
     int rc_it = MSF_OK;
-    if (e1 == cudaSuccess) rc_it = dist_iteration(cs, rhs0, nr);
+    if (e1 == cudaSuccess) rc_it = dist_iteration(cs, rhs0, nr, parity);
     c->pcg_launches = c->launches - before;
     c->launches = before;
     cudaError_t e2 = e1 == cudaSuccess ? cudaStreamEndCapture(c->stream, &g) : e1;
@@ -729,7 +772,9 @@ static int dist_pcg_solve(const Ranks& cs, int nr, double tol, int max_it, int32
   int rc;
   for (msf_ctx* x : cs) launch_pcg_init(x, nr, tol, max_it);
   if ((rc = dist_reduce(cs, FIN_F, 0, nr, false, 0))) return rc;
-  if ((rc = dist_vcycle(cs, 0, nr, false, 1))) return rc;
+  const bool wide = c->sb.halo > 1;
+  if ((rc = wide ? dist_vcycle_wide(cs, 0, nr, &msf_ctx::r, nullptr, false, 1) : dist_vcycle(cs, 0, nr, false, 1)))
+    return rc;
   for (msf_ctx* x : cs) launch_pcg_p(x, 0, nr, 0);
   CKL("dist pcg init");
   // one process per GPU: each active range's iteration (kernels + NCCL) is a CUDA graph; the
@@ -738,13 +783,14 @@ static int dist_pcg_solve(const Ranks& cs, int nr, double tol, int max_it, int32
   const int check_every = 8;
   int lo = 0, hi = nr;
   for (int it = 0; it < max_it + check_every; it += check_every) {
-    cudaGraphExec_t g = nullptr;
-    if (graph && (rc = dist_range_graph(cs, lo, hi - lo, &g))) return rc;
-    for (int j = 0; j < check_every; ++j) {
+    cudaGraphExec_t g[2] = {nullptr, nullptr};
+    for (int par = 0; graph && par < 2; ++par)
+      if ((rc = dist_range_graph(cs, lo, hi - lo, par, &g[par]))) return rc;
+    for (int j = 0; j < check_every; ++j) {   // check_every even: iteration it + j has parity j
       if (graph) {
-        CK(cudaGraphLaunch(g, c->stream));
+        CK(cudaGraphLaunch(g[j & 1], c->stream));
         c->launches += c->pcg_launches;
-      } else if ((rc = dist_iteration(cs, lo, hi - lo))) {
+      } else if ((rc = dist_iteration(cs, lo, hi - lo, j & 1))) {
         return rc;
       }
     }
@@ -758,6 +804,8 @@ static int dist_pcg_solve(const Ranks& cs, int nr, double tol, int max_it, int32
       }
     if (hi < 0) break;
   }
+  if (wide)
+    for (msf_ctx* x : cs) launch_pcg_p(x, 0, nr, 3);   // the converging iteration's u += alpha p
   for (msf_ctx* x : cs) launch_compliance(x, nr);
   if ((rc = dist_reduce(cs, FIN_COMP, 0, nr, false, 0))) return rc;
   int noconv = 0;
@@ -983,7 +1031,8 @@ int msf_group_precond_apply(msf_group* g, int rhs, const double* r, double* z) {
     CK(cudaStreamSynchronize(c->stream));
     launch_mask_copy(c, r + (size_t)c->dl.gox * col, c->r + (size_t)rhs * 2 * c->dl.nn, c->dl.nn);
   }
-  int rc = dist_vcycle(cs, rhs, 1, false, 0);
+  int rc = c0->sb.halo > 1 ? dist_vcycle_wide(cs, rhs, 1, &msf_ctx::r, nullptr, false, 0)
+                           : dist_vcycle(cs, rhs, 1, false, 0);
   if (rc) return rc;
   for (size_t i = 0; i < cs.size(); ++i) {
     msf_ctx* c = cs[i];

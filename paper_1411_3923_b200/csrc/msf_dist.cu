@@ -19,6 +19,8 @@
 
 #include "msf_internal.cuh"
 
+#include <algorithm>
+
 #define MSF_MAX_GROUP 8
 
 struct msf_group {
@@ -115,9 +117,17 @@ int strip_bounds(const Dims& d, int rank, int nranks, StripBounds& b, std::strin
   b.own1 = (rank == nranks - 1) ? d.nelx + 1 : b.C1 * d.cx;
   b.e0 = b.C0 * d.cx;
   b.e1 = b.C1 * d.cx;
+  // wide halos (streaming sweep) when every strip is at least that wide: a halo then lies
+  // wholly inside the neighbouring strip
+  int minw = d.nelx + 1;
+  for (int r = 0; r < nranks; ++r) {
+    const int c0 = (int)((long long)r * d.ncx / nranks), c1 = (int)((long long)(r + 1) * d.ncx / nranks);
+    minw = std::min(minw, (c1 - c0) * d.cx);
+  }
+  b.halo = (nranks > 1 && minw >= MSF_STRIP_HALO) ? MSF_STRIP_HALO : 1;
   int lo = 0;
-  if (rank > 0) lo = ((b.own0 - 1) % 2 == 0) ? b.own0 - 1 : b.own0 - 2;  // even: same colours
-  const int hi = (rank == nranks - 1) ? d.nelx + 1 : b.own1 + 1;
+  if (rank > 0) lo = ((b.own0 - b.halo) % 2 == 0) ? b.own0 - b.halo : b.own0 - b.halo - 1;  // even: same colours
+  const int hi = (rank == nranks - 1) ? d.nelx + 1 : b.own1 + b.halo;
   b.gox = lo;
   b.ncols = hi - lo;
   return MSF_OK;
@@ -191,14 +201,15 @@ int dist_allreduce(const std::vector<msf_ctx*>& cs, double* msf_ctx::*buf, size_
 }
 
 // halo exchange of the node vector ctx->*vec for realisations [rhs0, rhs0 + nr): every rank sends its
-// first / last owned node column to the left / right neighbour's halo column
-int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int rhs0, int nr) {
+// first / last w owned node columns to the left / right neighbour's w halo columns
+int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int rhs0, int nr, int w) {
   msf_ctx* c0 = cs[0];
   if (c0->comm->kind == MSF_TRANSPORT_NCCL) {
     NcclApi& A = nccl();
     msf_ctx* c = c0;
     const Dims& d = c->dl;
     const size_t col = (size_t)2 * d.nny;   // doubles per node column
+    const size_t wc = (size_t)w * col;
     ncclComm_t comm = (ncclComm_t)c->comm->nccl;
     int rc = nccl_check(c, A.GroupStart(), "ncclGroupStart");
     if (rc) return rc;
@@ -207,12 +218,12 @@ int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int rhs0, 
       // every call is checked; on a failure the group is still closed before returning, so
       // the communicator is never left inside an open group
       if (c->rank > 0) {
-        if (!rc) rc = nccl_check(c, A.Send(v + (size_t)d.own_lo * col, col, ncclDouble, c->rank - 1, comm, c->stream), "ncclSend (halo, left)");
-        if (!rc) rc = nccl_check(c, A.Recv(v + (size_t)(d.own_lo - 1) * col, col, ncclDouble, c->rank - 1, comm, c->stream), "ncclRecv (halo, left)");
+        if (!rc) rc = nccl_check(c, A.Send(v + (size_t)d.own_lo * col, wc, ncclDouble, c->rank - 1, comm, c->stream), "ncclSend (halo, left)");
+        if (!rc) rc = nccl_check(c, A.Recv(v + (size_t)(d.own_lo - w) * col, wc, ncclDouble, c->rank - 1, comm, c->stream), "ncclRecv (halo, left)");
       }
       if (c->rank < c->nranks - 1) {
-        if (!rc) rc = nccl_check(c, A.Send(v + (size_t)(d.own_hi - 1) * col, col, ncclDouble, c->rank + 1, comm, c->stream), "ncclSend (halo, right)");
-        if (!rc) rc = nccl_check(c, A.Recv(v + (size_t)d.own_hi * col, col, ncclDouble, c->rank + 1, comm, c->stream), "ncclRecv (halo, right)");
+        if (!rc) rc = nccl_check(c, A.Send(v + (size_t)(d.own_hi - w) * col, wc, ncclDouble, c->rank + 1, comm, c->stream), "ncclSend (halo, right)");
+        if (!rc) rc = nccl_check(c, A.Recv(v + (size_t)d.own_hi * col, wc, ncclDouble, c->rank + 1, comm, c->stream), "ncclRecv (halo, right)");
       }
     }
     const int rce = nccl_check(c, A.GroupEnd(), "ncclGroupEnd (halo)");
@@ -225,13 +236,13 @@ int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int rhs0, 
     const size_t pa = (size_t)2 * a->dl.nn * sizeof(double), pb = (size_t)2 * b->dl.nn * sizeof(double);
     char* va = (char*)(a->*vec) + (size_t)rhs0 * pa;
     char* vb = (char*)(b->*vec) + (size_t)rhs0 * pb;
-    // a's last owned column -> b's left halo ; b's first owned column -> a's right halo
-    cudaError_t e = cudaMemcpy2DAsync(vb + (size_t)(b->dl.own_lo - 1) * colb, pb,
-                                      va + (size_t)(a->dl.own_hi - 1) * colb, pa, colb, nr,
+    // a's last w owned columns -> b's left halo ; b's first w owned columns -> a's right halo
+    cudaError_t e = cudaMemcpy2DAsync(vb + (size_t)(b->dl.own_lo - w) * colb, pb,
+                                      va + (size_t)(a->dl.own_hi - w) * colb, pa, w * colb, nr,
                                       cudaMemcpyDeviceToDevice, c0->stream);
     if (e == cudaSuccess)
       e = cudaMemcpy2DAsync(va + (size_t)a->dl.own_hi * colb, pa,
-                            vb + (size_t)b->dl.own_lo * colb, pb, colb, nr,
+                            vb + (size_t)b->dl.own_lo * colb, pb, w * colb, nr,
                             cudaMemcpyDeviceToDevice, c0->stream);
     int rc = msf_cuda_check(c0, e, "group halo copy");
     if (rc) return rc;

@@ -116,7 +116,14 @@ struct msf_group;   // in-process rank group (msf_dist.cu)
 // Strip partition of the fine grid over ranks: rank r owns the node
 // columns of coarse columns [C0, C1) and keeps a one-column halo on each side (plus one
 // padding column on the left when needed to keep the 4-colour parity of the global grid).
+// Halo width (node columns per side) of a strip whose sweeps run as ONE streaming kernel: the
+// 7 columns the seven colour phases reach into the neighbour, rounded up so that the first
+// local column stays even.  Strips narrower than this keep the one-column halo and the
+// colour-phase sweep (a halo exchange after every phase).
+constexpr int MSF_STRIP_HALO = 8;
+
 struct StripBounds {
+  int halo;          // halo node columns per interior side: MSF_STRIP_HALO or 1
   int own0, own1;    // owned global node columns [own0, own1)
   int gox, ncols;    // local node columns = global [gox, gox + ncols)
   int e0, e1;        // owned global element columns
@@ -128,7 +135,7 @@ int dist_comm_create(msf_ctx* c, int transport, void* handle);
 void dist_comm_destroy(msf_ctx* c);
 int dist_allreduce(const std::vector<msf_ctx*>& cs, double* msf_ctx::*buf, size_t off,
                    size_t count);
-int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int rhs0, int nr);
+int dist_halo(const std::vector<msf_ctx*>& cs, double* msf_ctx::*vec, int rhs0, int nr, int w = 1);
 std::vector<msf_ctx*> group_ranks(msf_group* g);
 
 struct msf_comm {

@@ -314,7 +314,8 @@ size_t sgs_stream_smem() { return SG_SMEM; }
 void launch_sgs_stream(msf_ctx* c, int rhs0, int nr, const double* r, double* rout,
                        const double* zin, double* z, bool gated, bool zero_start, bool upd,
                        int rz_mode) {
-  if (c->sgs_warp && (long long)c->dl.nnx * c->fs_col < (1ll << 31)) {   // 32-bit indices there
+  // (a wide-halo strip always takes it: k_sgs_stream sweeps all local columns)
+  if ((c->sgs_warp || c->sb.halo > 1) && (long long)c->dl.nnx * c->fs_col < (1ll << 31)) {   // 32-bit indices there
     launch_sgs_warp(c, rhs0, nr, r, rout, zin, z, gated, zero_start, upd, rz_mode);
     return;
   }

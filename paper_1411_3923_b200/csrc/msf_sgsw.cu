@@ -159,7 +159,13 @@ __global__ void __launch_bounds__(SW_T, SW_WARPS)
     }
     const int nxs = ib < nextra ? nxb + 1 : nxb;
     const int Y0 = ib * SW_BAND, Yb = Y0 - SW_LO;   // Yb even: lane row parity = node row parity
-    const int X0 = (int)((long long)ir * d.nnx / nxs), X1 = (int)((long long)(ir + 1) * d.nnx / nxs);
+    // column runs over this rank's owned columns (one GPU: all of them)
+    const int nown = d.own_hi - d.own_lo;
+    const int X0 = d.own_lo + (int)((long long)ir * nown / nxs), X1 = d.own_lo + (int)((long long)(ir + 1) * nown / nxs);
+    // wide-halo strip: the first / last run also writes the updated residual of the halo columns
+    // it swept redundantly (r' = r - alpha q is exact there: q's halo was exchanged), so that the
+    // residual's halo is valid for the next sweeps without an exchange of its own
+    const bool lh = UPD && ir == 0 && d.own_lo > 0, rh = UPD && ir == nxs - 1 && d.own_hi < d.nnx;
     const double* E = Eall + (size_t)rhs * d.estride;
     const double2* r = rall + (size_t)rhs * d.nn;
     double2* rout = UPD ? routall + (size_t)rhs * d.nn : nullptr;
@@ -215,7 +221,8 @@ __global__ void __launch_bounds__(SW_T, SW_WARPS)
 
     // steps s = sb, sb + 2, ..., se: columns s, s + 1 enter; columns s - 7, s - 6 leave
     const int sb = (X0 - SW_DEP) & ~1;
-    const int se = (X1 + SW_DEP) & ~1;   // smallest even s with s - 7 >= X1 - 1
+    const int se0 = (X1 + SW_DEP) & ~1;   // smallest even s with s - 7 >= X1 - 1
+    const int se = rh ? se0 + 8 : se0;    // ... the right halo's columns up to se0 + 1 leave too
     double2 W[9][2];
 #pragma unroll
     for (int j = 0; j < 9; ++j) W[j][0] = W[j][1] = make_double2(0.0, 0.0);
@@ -287,6 +294,11 @@ __global__ void __launch_bounds__(SW_T, SW_WARPS)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int wc = s - 7 + q, j = 8 - q, ss = sk[7 - q];
+          if (UPD && ((lh && wc >= sb && wc >= 0 && wc < X0) || (rh && wc >= X1 && wc <= se0 + 1 && wc < d.nnx))) {
+            const int n = wc * d.nny;
+            if (vn0) rout[n + gn0] = S.s[ss].r[0][lane];
+            if (vn1) rout[n + gn1] = S.s[ss].r[1][lane];
+          }
           if (wc >= X0 && wc < X1) {
             const int n = wc * d.nny;
 #pragma unroll
@@ -336,7 +348,7 @@ void launch_sgs_warp(msf_ctx* c, int rhs0, int nr, const double* r, double* rout
   const int nyb = (d.nny + SW_BAND - 1) / SW_BAND;
   // one wave of SW_WARPS one-warp CTAs per SM; runs of at least 32 columns
   int units = std::max(nyb, (c->n_sm * SW_WARPS) / nr);
-  units = std::min(units, nyb * std::max(1, d.nnx / 32));
+  units = std::min(units, nyb * std::max(1, (d.own_hi - d.own_lo) / 32));
   units = std::min(units, std::max(nyb, c->max_partials));   // one partial per CTA
   const int nxb = units / nyb, nextra = units - nxb * nyb;
   const int nblk = units;

@@ -7,16 +7,17 @@ single-GPU MEASUREMENTS (this pool has one GPU per box):
 * the strip partition over N = 2, 4, 8 ranks, all ranks as contexts of one process on the
   one GPU (MSF_TRANSPORT_GROUP): every rank's own kernels, timed by msf_bench_kernels on that
   rank's context in the PCG launch configuration at 1 and 3 active realisations: the
-  fine-grid kernels of one PCG iteration on its strip (apply, 2 SGS sweeps, residual,
-  restriction, prolongation, update + F0, p update), its share of the coarse solve (forward
-  and back over its chain of K_c blocks, the replicated interface system) and of the
-  assembly (Galerkin products + chain factorisation of its cells, the replicated interface
-  factorisation).  A step takes the slowest rank;
+  fine-grid kernels of one PCG iteration on its wide-halo strip (apply, pre-smoothing sweep
+  with the residual update, residual, restriction, prolongation, post-smoothing sweep,
+  direction / solution update), its share of the coarse solve (forward and back over its box
+  of the nested dissection, the replicated interface fronts) and of the assembly (Galerkin
+  products + box factorisation, the replicated interface factorisation).  A step takes the
+  slowest rank;
 * ASSUMED (not measurable on one GPU): t_comm per NCCL operation over NVLink (default 8 us);
-  15 halo exchanges + 4 all-reduces per PCG iteration; the all-reduce of
-  the interface blocks at assembly, R (2N+1) m^2 doubles at --allreduce-gbps (default 300).
+  4 halo exchanges + 4 all-reduces per PCG iteration (wide-halo strips); the
+  all-reduce of the interface fronts at assembly at --allreduce-gbps (default 300).
 
-T_iter(N, k) = max_r [fine_r(k) + coarse_r(k)] + [N > 1] 19 t_comm ;  the step sums over the
+T_iter(N, k) = max_r [fine_r(k) + coarse_r(k)] + [N > 1] 8 t_comm ;  the step sums over the
 iterations with k active realisations, plus setup + assembly.  Prints a markdown table."""
 import argparse
 import json
@@ -31,14 +32,15 @@ import torch  # noqa: E402
 import workloads as W  # noqa: E402
 from paper_1411_3923_b200 import Msfem, MsfemGroup  # noqa: E402
 
-FINE = ["apply", "restrict", "prolong", "residual", "update_f0", "p_update"]
+FINE = ["apply", "sgs_pre_update", "residual", "restrict", "prolong", "sgs_sweep", "p_update"]
+N_COMM = 8   # NCCL operations per PCG iteration: halos q, z, t, z + all-reduces p.q, |r|^2, interface rhs, r.z
 COARSE = ["coarse_fwd_local", "coarse_top", "coarse_back_local"]
 
 
 def rank_times(m, nr, reps):
     os.environ["MSF_BENCH_NR"] = str(nr)
     kb = m.bench_kernels(reps=reps)
-    fine = sum(kb[k][0] for k in FINE) + 2 * kb["sgs_colour"][0]
+    fine = sum(kb[k][0] for k in FINE)
     coarse = sum(kb[k][0] for k in COARSE)
     return fine, coarse, kb["assemble_local"][0], kb["assemble_top"][0]
 
@@ -90,7 +92,7 @@ def main():
         asm = max(t[0][2] for t in per) + max(t[0][3] for t in per)
         ar_bytes = spec.n_rhs * (2 * N + 1) * mc * mc * 8
         rows.append(dict(N=N, fine1=worst1[0], coarse1=worst1[1], fine3=worst3[0],
-                         coarse3=worst3[1], comm=19 * a.t_comm_us * 1e-3, assemble=asm,
+                         coarse3=worst3[1], comm=N_COMM * a.t_comm_us * 1e-3, assemble=asm,
                          allreduce=ar_bytes / (a.allreduce_gbps * 1e9) * 1e3))
     for r in rows:
         it1 = r["fine1"] + r["coarse1"] + r["comm"]

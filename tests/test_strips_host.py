@@ -29,20 +29,30 @@ def pkg():
 
 
 @pytest.mark.parametrize("nelx,cx,nranks", [(16, 4, 2), (16, 4, 4), (30, 3, 3), (30, 3, 4),
-                                            (36, 4, 3), (1024, 16, 8), (5120, 20, 8)])
+                                            (36, 4, 3), (32, 8, 3), (60, 20, 3), (1024, 16, 8),
+                                            (5120, 20, 8)])
 def test_strip_bounds(pkg, nelx, cx, nranks):
     spec = W.small_spec(nelx=nelx, nely=8, cx=cx, cy=4)
     prob = pkg.problem_from_spec(spec)
     owned = np.zeros(nelx + 1, dtype=int)
     elems = np.zeros(nelx, dtype=int)
+    # halo width: 8 node columns per side (the streaming sweep's dependency
+    # halo) when every strip is at least 8 columns wide, else one column (colour-phase sweep)
+    ncx = nelx // cx
+    minw = min(((r + 1) * ncx // nranks - r * ncx // nranks) * cx for r in range(nranks))
+    h = 8 if minw >= 8 else 1
     for r in range(nranks):
         b = pkg.strip_bounds(prob, r, nranks)
         owned[b["own0"]:b["own1"]] += 1
         elems[b["e0"]:b["e1"]] += 1
         assert b["gox"] % 2 == 0                         # colour parity of the global grid
         lo, hi = b["gox"], b["gox"] + b["ncols"]          # local node columns [lo, hi)
-        assert lo <= max(b["own0"] - 1, 0) and hi >= min(b["own1"] + 1, nelx + 1)
-        assert b["own0"] - lo <= 2 and hi - b["own1"] <= 1   # at most padding + halo
+        assert lo <= max(b["own0"] - h, 0) and hi >= min(b["own1"] + h, nelx + 1)
+        assert b["own0"] - lo <= h + 1 and hi - b["own1"] <= h   # at most padding + halo
+        if r > 0:
+            assert b["own0"] - lo >= h
+        if r < nranks - 1:
+            assert hi - b["own1"] == h
         assert b["e0"] == b["C0"] * cx and b["e1"] == b["C1"] * cx
         assert b["C1"] > b["C0"]
     assert (owned == 1).all() and (elems == 1).all()
