@@ -138,9 +138,19 @@ def host_threads():
 
 SWEEP_CONFIG = "c3_square_2048"
 # bench_kernels entries -> the kernel they launch
-KERNEL_NAMES = {"apply": "k_apply_tma<0>", "sgs_pre_update": "k_sgs_stream<ZERO,UPD> (pre-smoothing + r update)",
-                "sgs_sweep": "k_sgs_stream (post-smoothing sweep)", "residual": "k_apply_tma<1>",
+KERNEL_NAMES = {"apply": "k_apply_tma<0>", "sgs_pre_update": "k_sgs_warp<ZERO,UPD> (pre-smoothing + r update)",
+                "sgs_sweep": "k_sgs_warp<RZ> (post-smoothing sweep)", "residual": "k_apply_tma<1>",
                 "p_update": "k_pcg_p (u, p update)"}
+# FP64 work of the sweeps (FP64 instructions per step of the SASS loop,
+# 2 flops per DFMA, per node swept, without the halo redundancy) and the FP64 peak measured
+# with scripts/dfma_probe.cu on this pool's B200 (63.7 of 64 DFMA/clk/SM at 1965 MHz).
+FP64_FLOP_PER_NODE = {"sgs_sweep": 315.0, "sgs_pre_update": 233.0}
+FP64_PEAK_TFLOPS = 36.7
+
+
+def inf_nodes(m, spec, nranks):
+    """Nodes the timed kernels sweep on this rank (a strip: its share)."""
+    return (spec.nelx + 1) * (spec.nely + 1) / nranks
 
 
 def contrast_sweep(dev):
@@ -330,6 +340,14 @@ def run_ours(args, spec):
             fp64_frac = tj.get(dom + "_fp64_pipe_frac")
         except Exception:
             traffic = None
+    fp64_roof = None
+    if dom in FP64_FLOP_PER_NODE:
+        nn_loc = inf_nodes(m, spec, ws if strips else 1)
+        fl = FP64_FLOP_PER_NODE[dom] * nn_loc * spec.n_rhs
+        fp64_roof = {"flop_per_launch": fl, "achieved_tflops": fl / (dom_ms / 1e3) / 1e12,
+                     "peak_tflops": FP64_PEAK_TFLOPS,
+                     "frac": fl / (dom_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                     "peak_source": "measured (scripts/dfma_probe.cu, dependent-free DFMA stream)"}
     inf = m.info()
     if rank != 0:
         if ws > 1:
@@ -361,7 +379,10 @@ def run_ours(args, spec):
                      # the sweeps are FP64-issue/latency-bound, not HBM-bound: ncu FP64 pipe share
                      "ncu_fp64_pipe_frac": fp64_frac,
                      "alg_bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     # the same launch against the FP64 roofline (the sweeps issue ~1 DFMA per 2
+                     # instructions; ncu: FP64 pipe 45-57% busy incl. the halo redundancy)
+                     "fp64": fp64_roof},
         # every timed kernel (all realisations active, PCG launch configuration): average ms per
         # launch-set, algorithmic GB/s and its fraction of the measured HBM peak
         "kernels": {k: {"ms": v[0],

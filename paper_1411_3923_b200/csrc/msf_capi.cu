@@ -1308,7 +1308,7 @@ int msf_bench_kernels(msf_ctx* c, int reps, double* ms, double* bytes) {
   auto run = [&](int which) {
     switch (which) {
       case 0: launch_matvec(c, 0, R, c->pv, c->q, false, true); break;
-      case 1: launch_sgs_stream(c, 0, R, c->r, nullptr, c->t, c->z, false, false, false, 0); break;
+      case 1: launch_sgs_stream(c, 0, R, c->r, nullptr, c->t, c->z, false, false, false, 2); break;   // the PCG's post-smoothing (r.z -> beta)
       case 2: launch_restrict(c, 0, R, c->t, false); break;
       case 3: launch_nd_solve(c, 0, R, false); break;
       case 4: launch_prolong(c, 0, R, c->z, c->t, false); break;
