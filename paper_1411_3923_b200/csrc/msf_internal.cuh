@@ -229,6 +229,7 @@ struct msf_ctx {
   double* cx = nullptr;         // [R][nbc*mc] coarse solution
   // coarse-cell-class restriction / prolongation (msf_xfer.cu)
   int xf_G = 1, xf_ntasks = 0, xf_n_cls = 0;   // 16-column groups, CTA tasks, cell classes
+  int xf_nch = 1;                              // pattern-column chunks per cell group
   void* xf_cls = nullptr;       // XferClass[]
   void* xf_tasks = nullptr;     // XferTask[]
   int* xf_cells = nullptr;      // this rank's cells sorted by class

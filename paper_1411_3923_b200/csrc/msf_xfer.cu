@@ -53,9 +53,19 @@ struct XferClass {   // device: one coarse-cell class
   int cell_off;      // first cell in the class-sorted cell list
   int pad;
 };
-struct XferTask {    // device: (class, cells [c0, c0 + nc) of the class list), nc <= NCC
-  int k, c0, nc, pad;
+struct XferTask {    // device: (class, cells [c0, c0 + nc) of the class list, nc <= NCC, column
+  int k, c0, nc, ch;  // chunk ch of the pattern: columns [ch nx / nch, (ch + 1) nx / nch))
 };
+// Pattern-column chunks per cell group: a CTA walks its columns in sequence (two barriers per
+// column, ~2 us each), so a whole 20-column pattern is a ~45 us pipeline however few cells there
+// are; when the cell groups alone do not fill the device (3 CTAs resident per SM: small grids,
+// the strips of a partition) the pattern is cut into chunks for more, shorter CTAs.  Chunks of
+// at least 4 columns.  (With the device already full, chunks only repeat the per-CTA prologue:
+// configs[4] on one GPU, 4 chunks: restriction 0.094 -> 0.084 ms but prolongation 0.143 -> 0.163.)
+inline int xfer_nchunk(const Dims& d, size_t ngroups) {
+  const int want = (int)((444 + ngroups - 1) / std::max<size_t>(ngroups, 1));
+  return std::max(1, std::min(want, d.cx / 4));
+}
 
 // entries of one pattern column (2 ny, (node row, DOF)) padded to whole 8-row DMMA tiles, and
 // the shared row stride of a column tile (stride = 4 or 12 mod 16 doubles: the fragment loads
@@ -123,7 +133,7 @@ __global__ void __launch_bounds__(XT) k_restrict_cells(Dims d, const XferClass* 
                                                        const double* __restrict__ phi,
                                                        const double2* __restrict__ tall,
                                                        double* part, const PcgScalars* sc,
-                                                       int rhs0, int gated, int G) {
+                                                       int rhs0, int gated, int G, int nch) {
   extern __shared__ __align__(16) double xsm[];
   __shared__ int cid[NCC];
   __shared__ long long cbase[NCC];
@@ -151,9 +161,10 @@ __global__ void __launch_bounds__(XT) k_restrict_cells(Dims d, const XferClass* 
   if (gated && !sc[rhs].active) return;   // uniform
   __syncthreads();
   const double* t = reinterpret_cast<const double*>(tall + (size_t)rhs * d.nn);
-  const int GJ = G * XNJ, nsteps = G * C.nx;
+  const int lx0 = T.ch * C.nx / nch, ncol = (T.ch + 1) * C.nx / nch - lx0;   // this task's columns
+  const int GJ = G * XNJ, nsteps = G * ncol;
   auto stage = [&](int i) {   // step i = (group, column) into buffer i & 1
-    const int g = i / C.nx, lx = i - g * C.nx;
+    const int g = i / ncol, lx = lx0 + i - g * ncol;
     stage_phi_col(d, C, phi, g, lx, SP(i & 1));
     load_col_tile(d, C, cbase, T.nc, t, lx, Tt(i & 1), st);
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -161,8 +172,8 @@ __global__ void __launch_bounds__(XT) k_restrict_cells(Dims d, const XferClass* 
   stage(0);
   double acc[2][NI][2];
   for (int i = 0; i < nsteps; ++i) {
-    const int g = i / C.nx, lx = i - g * C.nx;
-    if (lx == 0) {
+    const int g = i / ncol, lc = i - g * ncol;
+    if (lc == 0) {
 #pragma unroll
       for (int k = 0; k < 4 * NI; ++k) (&acc[0][0][0])[k] = 0.0;
     }
@@ -182,7 +193,7 @@ __global__ void __launch_bounds__(XT) k_restrict_cells(Dims d, const XferClass* 
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
     }
-    if (lx == C.nx - 1) {
+    if (lc == ncol - 1) {
       // C(gq, 2 tq + h) of (mi, ni): column mi*8 + gq, cell CW w + ni*8 + 2 tq + h
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
@@ -192,7 +203,7 @@ __global__ void __launch_bounds__(XT) k_restrict_cells(Dims d, const XferClass* 
           for (int h = 0; h < 2; ++h) {
             const int c = CW * w + ni * 8 + 2 * tq + h;
             if (c < T.nc)
-              part[((size_t)rhs * d.ncx * d.ncy + cid[c]) * GJ + g * XNJ + mi * 8 + gq] = acc[mi][ni][h];
+              part[(((size_t)rhs * d.ncx * d.ncy + cid[c]) * nch + T.ch) * GJ + g * XNJ + mi * 8 + gq] = acc[mi][ni][h];
           }
     }
   }
@@ -210,7 +221,7 @@ __global__ void __launch_bounds__(XT) k_prolong_cells(Dims d, const XferClass* _
                                                       const double* __restrict__ xall,
                                                       const double2* zin, double2* tout,
                                                       const PcgScalars* sc, int rhs0, int gated,
-                                                      int G) {
+                                                      int G, int nch) {
   extern __shared__ __align__(16) double xsm[];
   __shared__ int cid[NCC];
   __shared__ long long cbase[NCC];
@@ -252,21 +263,22 @@ __global__ void __launch_bounds__(XT) k_prolong_cells(Dims d, const XferClass* _
   }
   const double* zi0 = reinterpret_cast<const double*>(zin + (size_t)rhs * d.nn);
   double* to = reinterpret_cast<double*>(tout + (size_t)rhs * d.nn);
-  const int nsteps = G * C.nx;
+  const int lx0 = T.ch * C.nx / nch, ncol = (T.ch + 1) * C.nx / nch - lx0;   // this task's columns
+  const int nsteps = G * ncol;
   auto stage = [&](int i) {
-    const int g = i / C.nx, lx = i - g * C.nx;
+    const int g = i / ncol, lx = lx0 + i - g * ncol;
     stage_phi_col(d, C, phi, g, lx, SP(i & 1));
     load_col_tile(d, C, cbase, T.nc, g ? to : zi0, lx, Zt(i & 1), st);
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   stage(0);
   for (int i = 0; i < nsteps; ++i) {
-    const int g = i / C.nx, lx = i - g * C.nx;
+    const int g = i / ncol, lx = lx0 + i - g * ncol;
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();   // step i's data (and X) visible; step i - 1's buffers free
     // G > 1: group g + 1 re-reads this column after this step stores it, so it is never
     // prefetched across a group boundary
-    if (i + 1 < nsteps && (G == 1 || (i + 1) % C.nx != 0)) stage(i + 1);
+    if (i + 1 < nsteps && (G == 1 || (i + 1) % ncol != 0)) stage(i + 1);
     const double* S = SP(i & 1);
     double* Z = Zt(i & 1);
     const double* Xg = X + (size_t)g * NCC * SPJ;
@@ -303,7 +315,7 @@ __global__ void __launch_bounds__(XT) k_prolong_cells(Dims d, const XferClass* _
       for (int c = w; c < T.nc; c += XT / 32)
         *reinterpret_cast<double2*>(to + 2 * (cbase[c] + (long long)lx * d.nny + lane)) =
             *reinterpret_cast<const double2*>(Z + (size_t)c * st + 2 * lane);
-    if (G > 1 && (i + 1) % C.nx == 0 && i + 1 < nsteps) {
+    if (G > 1 && (i + 1) % ncol == 0 && i + 1 < nsteps) {
       __syncthreads();   // the group's last column is stored before the next group reads it
       stage(i + 1);
     }
@@ -313,7 +325,7 @@ __global__ void __launch_bounds__(XT) k_prolong_cells(Dims d, const XferClass* _
 // c[slot(I, J, a)] = sum over the (up to) four cells of agglomerate (I, J) in this rank's cell
 // columns [C0, C1) of the column (corner of (I, J), a) of their partials, in a fixed order
 __global__ void __launch_bounds__(256) k_restrict_aggs(Dims d, const double* __restrict__ part,
-                                                       int GJ, int I0, int I1, int C0, int C1,
+                                                       int GJ, int nch, int I0, int I1, int C0, int C1,
                                                        double* cball, const PcgScalars* sc,
                                                        int rhs0, int gated) {
   pdl_launch();
@@ -335,7 +347,8 @@ __global__ void __launch_bounds__(256) k_restrict_aggs(Dims d, const double* __r
       const int CJ = J - 1 + dj;
       if (CJ < 0 || CJ >= d.ncy) continue;
       const int corner = (1 - di) * 2 + (1 - dj);   // (I, J) = (CI + 1 - di, CJ + 1 - dj)
-      s += part[((size_t)rhs * d.ncx * d.ncy + CI * d.ncy + CJ) * GJ + corner * d.kmax + a];
+      const double* pc = part + ((size_t)rhs * d.ncx * d.ncy + CI * d.ncy + CJ) * nch * GJ + corner * d.kmax + a;
+      for (int ch = 0; ch < nch; ++ch) s += pc[(size_t)ch * GJ];   // the cell's column chunks, in order
     }
   }
   cball[(size_t)rhs * d.nbc * d.mc + ((size_t)I * (d.ncy + 1) + J) * d.kmax + a] = s;
@@ -541,12 +554,15 @@ int xfer_setup(msf_ctx* c, char*& cur) {
   std::vector<XferTask> tasks;
   std::vector<int4> gtasks;   // Galerkin GEMM tiles: (class, first row, first column, -)
   const int R = d.R, psp = gal_psp(d);
+  size_t ngroups = 0;
+  for (const auto& m : members) ngroups += (m.size() + NCC - 1) / NCC;
+  const int nch = xfer_nchunk(d, ngroups);
   for (size_t k = 0; k < K.size(); ++k) {
     K[k].cell_off = (int)cells.size();
     cells.insert(cells.end(), members[k].begin(), members[k].end());
     const int ncell = (int)members[k].size();
     for (int c0 = 0; c0 < ncell; c0 += NCC)
-      tasks.push_back(XferTask{(int)k, c0, std::min(NCC, ncell - c0), 0});
+      for (int ch = 0; ch < nch; ++ch) tasks.push_back(XferTask{(int)k, c0, std::min(NCC, ncell - c0), ch});
     for (int r0 = 0; r0 < ncell * R; r0 += GT)
       for (int q0 = 0; q0 < psp; q0 += GT) gtasks.push_back(make_int4((int)k, r0, q0, ncell * R));
   }
@@ -561,12 +577,13 @@ int xfer_setup(msf_ctx* c, char*& cur) {
     return (void*)r;
   };
   c->xf_G = G;
+  c->xf_nch = nch;
   c->xf_ntasks = (int)tasks.size();
   c->xf_n_cls = (int)K.size();
   c->xf_cls = take(K.size() * sizeof(XferClass));
   c->xf_tasks = take(tasks.size() * sizeof(XferTask));
   c->xf_cells = (int*)take(cells.size() * 4);
-  c->xf_part = (double*)take((size_t)d.R * d.ncx * d.ncy * G * XNJ * 8);
+  c->xf_part = (double*)take((size_t)d.R * d.ncx * d.ncy * nch * G * XNJ * 8);
   c->gal_ntasks = (int)gtasks.size();
   c->gal_tasks = (int4*)take(gtasks.size() * sizeof(int4));
   c->gal_pq = (int2*)take(pq.size() * sizeof(int2));
@@ -586,16 +603,18 @@ size_t xfer_workspace_bytes(const Dims& d, const std::vector<int>& cls_of_agg, i
   std::vector<XferClass> K;
   std::vector<std::vector<int>> members;
   cell_classes(d, cls_of_agg, C0, C1, K, members);
-  size_t ntask = 0, ngt = 0;
+  size_t ntask = 0, ngt = 0, ngroups = 0;
   const int psp = gal_psp(d);
+  for (const auto& m : members) ngroups += (m.size() + NCC - 1) / NCC;
+  const int nch = xfer_nchunk(d, ngroups);
   for (const auto& m : members) {
-    ntask += (m.size() + NCC - 1) / NCC;
+    ntask += nch * ((m.size() + NCC - 1) / NCC);
     ngt += ((m.size() * d.R + GT - 1) / GT) * (psp / GT);
   }
   const size_t ncell = (size_t)d.ncx * d.ncy;
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
   return al(K.size() * sizeof(XferClass)) + al(ntask * sizeof(XferTask)) + al(ncell * 4) +
-         al((size_t)d.R * ncell * G * XNJ * 8) + al(ngt * sizeof(int4)) + al(psp * sizeof(int2)) +
+         al((size_t)d.R * ncell * nch * G * XNJ * 8) + al(ngt * sizeof(int4)) + al(psp * sizeof(int2)) +
          al(K.size() * (size_t)d.cx * d.cy * psp * 8);
 }
 
@@ -603,7 +622,7 @@ void launch_prolong(msf_ctx* c, int rhs0, int nr, const double* zin, double* z, 
   launch_k(k_prolong_cells, dim3(c->xf_ntasks, nr), dim3(XT), prolong_smem(c->d), c->stream, c->dl,
            (const XferClass*)c->xf_cls, (const XferTask*)c->xf_tasks, (const int*)c->xf_cells,
            (const double*)c->phi, (const double*)c->cx, (const double2*)zin, (double2*)z,
-           (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0, c->xf_G);
+           (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0, c->xf_G, c->xf_nch);
   MSF_LAUNCHED(c);
 }
 
@@ -612,11 +631,11 @@ void launch_restrict(msf_ctx* c, int rhs0, int nr, const double* t, bool gated) 
   launch_k(k_restrict_cells, dim3(c->xf_ntasks, nr), dim3(XT), restrict_smem(c->d), c->stream, d,
            (const XferClass*)c->xf_cls, (const XferTask*)c->xf_tasks, (const int*)c->xf_cells,
            (const double*)c->phi, (const double2*)t, c->xf_part, (const PcgScalars*)c->sc, rhs0,
-           gated ? 1 : 0, c->xf_G);
+           gated ? 1 : 0, c->xf_G, c->xf_nch);
   MSF_LAUNCHED(c);
   const int naggs = (c->cr_hi - c->cr_lo + 1) * (d.ncy + 1);
   launch_k(k_restrict_aggs, dim3((naggs * d.kmax + 255) / 256, nr), dim3(256), 0, c->stream, d,
-           (const double*)c->xf_part, c->xf_G * XNJ, c->cr_lo, c->cr_hi, c->sb.C0, c->sb.C1, c->cb,
+           (const double*)c->xf_part, c->xf_G * XNJ, c->xf_nch, c->cr_lo, c->cr_hi, c->sb.C0, c->sb.C1, c->cb,
            (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
   MSF_LAUNCHED(c);
 }
