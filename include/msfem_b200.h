@@ -196,19 +196,21 @@ int msf_bench_kernels(msf_ctx* ctx, int reps, double* ms, double* bytes);
 /* ---- strip partition over ranks (multi-GPU) -------------------------
  * The fine grid is cut into strips of whole coarse-cell columns, one per rank.  Rank r
  * owns the node columns of coarse columns [C0, C1) (the last rank also owns column nelx),
- * stores its strip plus a one-node-column halo on each side (and one padding column on the
- * left when needed so that its first local column is even: the 4-colour Gauss-Seidel order
- * of reading R7 is the global one), and runs every fine-grid kernel on it.  The moduli of
- * the whole grid and the spectral basis are replicated.  K_c is distributed by block
- * columns: rank r computes the Galerkin products of its coarse cells and reduces its chain
- * of blocks [C0, C1] (C1 = ncx on the last rank) to the chain's two end blocks; one sum
- * all-reduce of the end blocks gives every rank the block-tridiagonal interface system on
- * the nranks + 1 blocks C0_0 = 0, C0_1, ..., ncx, which is reduced (and later solved)
- * redundantly on every rank.  Per PCG iteration: 15 halo exchanges of the smoother iterate
- * (one per colour phase, one after the prolongation), sum all-reduces of p.Ap, ||r||^2,
- * r.z and of the chain-end coarse rhs ((nranks + 1) * m doubles per realisation).  Results
- * equal the single-GPU path up to the summation order of the dot products and the
- * elimination order of K_c (the interface blocks are eliminated last).
+ * stores its strip plus a halo on each interior side -- 8 node columns when every strip is
+ * at least 8 columns wide (the 7-column dependency halo of the streaming Gauss-Seidel sweep,
+ * rounded up), else one column -- and one padding column on the left when needed so that its
+ * first local column is even (the 4-colour Gauss-Seidel order of reading R7 is the global
+ * one), and runs every fine-grid kernel on it.  The moduli of the whole grid and the spectral
+ * basis are replicated.  K_c is distributed over the nested dissection of the coarse grid:
+ * rank r computes the Galerkin products of its coarse cells [C0, C1) and factors the fronts
+ * of its own box; the separators between the ranks' boxes (interface fronts) are summed by
+ * one all-reduce and factored (and later solved) redundantly on every rank.  Per PCG
+ * iteration on 8-column halos: 4 halo exchanges (q, the pre-smoothed z, the prolonged
+ * iterate, the post-smoothed z) and sum all-reduces of p.Ap, ||r||^2, r.z and of the
+ * interface fronts' right-hand sides; on one-column halos the sweeps run as colour phases with
+ * a halo exchange after each (15 exchanges).  Results equal the single-GPU path up to the
+ * summation order of the dot products and the elimination order of K_c (the interface
+ * separators are eliminated last).
  *
  * Transports: MSF_TRANSPORT_NCCL, handle = host pointer to the 128-byte NCCL unique id
  * (msf_nccl_unique_id on rank 0, broadcast by the caller), one process per GPU; all the
