@@ -76,9 +76,12 @@ __device__ __forceinline__ double2 shfl_down2(double2 v) {
 // sc / sm: ring slots of node column c = s + 1 - J and of c - 1.
 // NZ: the neighbours that may be nonzero (apply_node; a sweep from z = 0 knows which colours
 // are still untouched).
+// nb0 / nb1 / nb2: the neighbouring lane's row (above for P = 0, below for P = 1) of node columns
+// c - 1 / c / c + 1, shuffled by the caller (successive phases share them).
 template <int J, int P, bool FWD, bool BWD, bool Z0, int NZ = 0x1ff>
 __device__ __forceinline__ void sw_phase(const K0Mat& K, double2 (&W)[9][2], const SwRing& S, int sc,
-                                         int sm, unsigned long long fw, int lane) {
+                                         int sm, unsigned long long fw, int lane, double2 nb0,
+                                         double2 nb1, double2 nb2) {
   double Eloc[2][2];
   double2 zloc[3][3];
   // moduli of elements (c-1 .. c, y-1 .. y): y-1 is the odd row of the lane below (P = 0)
@@ -95,15 +98,15 @@ __device__ __forceinline__ void sw_phase(const K0Mat& K, double2 (&W)[9][2], con
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const int j = J + 1 - a;   // node column c - 1 + a
-      const double2 zero2 = make_double2(0.0, 0.0);
+      const double2 nb = a == 0 ? nb0 : a == 1 ? nb1 : nb2;
       if (P == 0) {
-        zloc[a][0] = ((NZ >> (3 * a)) & 1) ? shfl_up2(W[j][1]) : zero2;
+        zloc[a][0] = nb;
         zloc[a][1] = W[j][0];
         zloc[a][2] = W[j][1];
       } else {
         zloc[a][0] = W[j][0];
         zloc[a][1] = W[j][1];
-        zloc[a][2] = ((NZ >> (3 * a + 2)) & 1) ? shfl_down2(W[j][0]) : zero2;
+        zloc[a][2] = nb;
       }
     }
   }
@@ -277,17 +280,34 @@ __global__ void __launch_bounds__(SW_T, SW_WARPS)
       int sk[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) sk[k] = sl - k < 0 ? sl - k + SW_NR : sl - k;
-      sw_phase<1, 0, true, false, ZERO>(K, W, S, sk[0], sk[1], fw, lane);    // F0   column s
-      // from z = 0 the forward phases see only the colours already swept: F1 its horizontal
-      // neighbours (colour 0), F2 the vertical (0) and diagonal (1) ones, F3 all but itself
+      // The neighbouring lanes' rows, shuffled once and shared by successive phases: U[j] = the
+      // odd row of the lane below (window column j), D[j] = the even row of the lane above.  A
+      // phase changes one row of one window column, which no later phase of the step needs from
+      // the cache except where it is re-shuffled below (13 double2 shuffles per step, not 21).
+      // From z = 0 the forward phases see only the colours already swept: F1 its horizontal
+      // neighbours (colour 0), F2 the vertical (0) and diagonal (1) ones, F3 all but itself.
       constexpr int NZ_H = (1 << 1) | (1 << 7), NZ_V = (1 << 3) | (1 << 5);
       constexpr int NZ_D = (1 << 0) | (1 << 2) | (1 << 6) | (1 << 8), NZ_ALL = 0x1ff;
-      sw_phase<2, 0, true, false, false, ZERO ? NZ_H : NZ_ALL>(K, W, S, sk[1], sk[2], fw, lane);          // F1   s - 1
-      sw_phase<3, 1, true, false, false, ZERO ? (NZ_V | NZ_D) : NZ_ALL>(K, W, S, sk[2], sk[3], fw, lane);  // F2   s - 2
-      sw_phase<4, 1, true, true, false, ZERO ? (NZ_H | NZ_V | NZ_D) : NZ_ALL>(K, W, S, sk[3], sk[4], fw, lane);   // F3B3 s - 3
-      sw_phase<5, 1, false, true, false>(K, W, S, sk[4], sk[5], fw, lane);   // B2   s - 4
-      sw_phase<6, 0, false, true, false>(K, W, S, sk[5], sk[6], fw, lane);   // B1   s - 5
-      sw_phase<7, 0, false, true, false>(K, W, S, sk[6], sk[7], fw, lane);   // B0   s - 6
+      const double2 zz = make_double2(0.0, 0.0);
+      double2 U0 = zz, U1 = zz, U2 = zz, U3 = zz;
+      if (!ZERO) {
+        U0 = shfl_up2(W[0][1]);
+        U1 = shfl_up2(W[1][1]);
+        U2 = shfl_up2(W[2][1]);
+        U3 = shfl_up2(W[3][1]);
+      }
+      sw_phase<1, 0, true, false, ZERO>(K, W, S, sk[0], sk[1], fw, lane, U2, U1, U0);    // F0   column s
+      sw_phase<2, 0, true, false, false, ZERO ? NZ_H : NZ_ALL>(K, W, S, sk[1], sk[2], fw, lane, U3, U2, U1);          // F1   s - 1
+      const double2 D2 = shfl_down2(W[2][0]), D3 = shfl_down2(W[3][0]), D4 = shfl_down2(W[4][0]);
+      sw_phase<3, 1, true, false, false, ZERO ? (NZ_V | NZ_D) : NZ_ALL>(K, W, S, sk[2], sk[3], fw, lane, D4, D3, D2);  // F2   s - 2
+      const double2 D5 = shfl_down2(W[5][0]);
+      sw_phase<4, 1, true, true, false, ZERO ? (NZ_H | NZ_V | NZ_D) : NZ_ALL>(K, W, S, sk[3], sk[4], fw, lane, D5, D4, D3);   // F3B3 s - 3
+      const double2 D6 = shfl_down2(W[6][0]);
+      sw_phase<5, 1, false, true, false>(K, W, S, sk[4], sk[5], fw, lane, D6, D5, D4);   // B2   s - 4
+      const double2 U5 = shfl_up2(W[5][1]), U6 = shfl_up2(W[6][1]), U7 = shfl_up2(W[7][1]);
+      sw_phase<6, 0, false, true, false>(K, W, S, sk[5], sk[6], fw, lane, U7, U6, U5);   // B1   s - 5
+      const double2 U8 = shfl_up2(W[8][1]);
+      sw_phase<7, 0, false, true, false>(K, W, S, sk[6], sk[7], fw, lane, U8, U7, U6);   // B0   s - 6
 
       // columns s - 7 (window 8) and s - 6 (window 7) are final: band rows to global
       if (band) {
