@@ -203,7 +203,7 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
     }
   }
   P.max_partials = std::max({apply_partials_needed(d), sgs_colour_partials_needed(d),
-                             sgs_stream_partials_needed(P.dl), sgs_warp_partials_needed(P.dl)});
+                             sgs_warp_partials_needed(P.dl)});
 
   // workspace size (node vectors on this rank's strip; moduli of the whole grid)
   const size_t R = d.R, nn = P.dl.nn, ne = d.ne, nt = d.nt;
@@ -215,6 +215,11 @@ int make_plan(const msf_problem* p, const uint8_t* fixed, Plan& P, std::string& 
   {
     int fc, fp;
     sgs_fix_layout(P.dl, fc, fp);
+    // the streaming sweep addresses nodes, elements and mask bytes with 32-bit indices
+    if ((long long)P.dl.nnx * fc >= (1ll << 31) || (long long)P.dl.nn >= (1ll << 31)) {
+      msg = "grid too large: the Gauss-Seidel sweep uses 32-bit node indices (nodes per rank < 2^31)";
+      return MSF_ERR_ARG;
+    }
     add((size_t)P.dl.nnx * fc);                // fixs
   }
   add(2 * nn * 8);                           // f
@@ -406,7 +411,6 @@ static int setup_impl(const msf_problem* p, const uint8_t* fixed_mask, const dou
   }
   c->factor_status = (int*)take(2 * MSF_MAX_RHS * 4);
   if (const char* e = std::getenv("MSF_APPLY_TMA")) c->apply_tma = std::string(e) != "0";
-  if (const char* e = std::getenv("MSF_SGS_WARP")) c->sgs_warp = std::string(e) != "0";
   {
     const char* e = std::getenv("MSF_PDL");   // read at every setup (tests toggle it)
     g_msf_pdl = !(e && std::string(e) == "0");

@@ -1,5 +1,5 @@
 // Matrix-free Q4 stiffness operator, multicolour symmetric Gauss-Seidel phases and the PCG
-// vector kernels of the B200 MsFEM path (the streaming sweep of msf_sgs.cu runs the same
+// vector kernels of the B200 MsFEM path (the streaming sweep of msf_sgsw.cu runs the same
 // Gauss-Seidel node arithmetic, msfk::gs_node).
 //
 //   * y = P K(xbar) P x  with  K = sum_e (Emin + xbar_e^p (E0-Emin)) K0   (Eq. 4-5,

@@ -193,7 +193,7 @@ struct msf_ctx {
   uint8_t* fixn = nullptr;      // per-node bitmask: bit0 x fixed, bit1 y fixed (this rank's strip;
                                 // halo / padding columns = 3)
   uint8_t* fixg = nullptr;      // the same for the whole grid (local eigenproblems)
-  uint8_t* fixs = nullptr;      // fixn in the streaming sweep's planar padded layout (msf_sgs.cu)
+  uint8_t* fixs = nullptr;      // fixn in the streaming sweep's planar padded layout (msf_sgsw.cu)
   int fs_col = 0, fs_plane = 0;
   double* f = nullptr;          // load [2*nn]
   double* x_tile = nullptr;     // design [nt]
@@ -241,7 +241,6 @@ struct msf_ctx {
   int2* gal_pq = nullptr;
   int gal_ntasks = 0;
   int* factor_status = nullptr; // [2 * MSF_MAX_RHS] nonzero on failed pivot
-  bool sgs_warp = true;         // sweeps by k_sgs_warp (env MSF_SGS_WARP=0: k_sgs_stream)
   bool apply_tma = true;        // operator apply / residual fed by TMA tiles (env MSF_APPLY_TMA=0: off)
   struct TmapSlot {             // cached TMA descriptor (CUtensorMap, 128 B) per base pointer
     const void* ptr;
@@ -321,7 +320,7 @@ void launch_pcg_init(msf_ctx* c, int nr, double tol, int max_it);
 // mode 0: p = z (init); 1: u += alpha p, p = z + beta p; 2: p = z + beta p; 3: u += alpha p
 // (all realisations, after the last iteration)
 void launch_pcg_p(msf_ctx* c, int rhs0, int nr, int mode);
-// streaming symmetric Gauss-Seidel sweep (msf_sgs.cu): z = SGS(z; r), zero_start: from z = 0;
+// streaming symmetric Gauss-Seidel sweep (msf_sgsw.cu: the iterate in registers, one warp per band): z = SGS(z; r), zero_start: from z = 0;
 // upd: r -= alpha q first (alpha from the operator's partials, ||r||^2 -> convergence);
 // rz_mode != 0: r.z -> beta
 // zin: the starting iterate (not read when zero_start; must differ from z: other CTAs read
@@ -330,14 +329,9 @@ void launch_pcg_p(msf_ctx* c, int rhs0, int nr, int mode);
 void launch_sgs_stream(msf_ctx* c, int rhs0, int nr, const double* r, double* rout,
                        const double* zin, double* z, bool gated, bool zero_start, bool upd,
                        int rz_mode);
-// the same sweep with the iterate in registers, one warp per band (msf_sgsw.cu)
-void launch_sgs_warp(msf_ctx* c, int rhs0, int nr, const double* r, double* rout,
-                     const double* zin, double* z, bool gated, bool zero_start, bool upd,
-                     int rz_mode);
 int sgs_warp_partials_needed(const Dims& d);
 void sgs_fix_layout(const Dims& d, int& fs_col, int& fs_plane);
 void sgs_fix_build(const Dims& d, const uint8_t* fixn, std::vector<uint8_t>& out);
-int sgs_stream_partials_needed(const Dims& d);
 void launch_compliance(msf_ctx* c, int nr);
 
 // ---------------------------------------------------------------- filter / design

@@ -1,5 +1,5 @@
 // Device-side building blocks of the B200 MsFEM-PCG path, shared by the kernels of
-// msf_fem.cu, msf_sgs.cu and msf_coarse.cu so that they execute the same arithmetic.  All functions are called by a whole CTA unless
+// msf_fem.cu, msf_sgsw.cu and msf_coarse.cu so that they execute the same arithmetic.  All functions are called by a whole CTA unless
 // stated otherwise.
 #pragma once
 
@@ -226,7 +226,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // x then y (FWD), y then x (BWD), or both (the F3B3 phase).  Eloc / zloc: the 4 element moduli
 // and the 3x3 neighbourhood of the node (zloc[1][1] = its current value), rv its residual
 // entry, fm its Dirichlet bits.  ZERO: z = 0 around the node, only the pivot block is needed.
-// Shared by the colour-phase kernels and the streaming sweep (msf_sgs.cu), so both execute
+// Shared by the colour-phase kernels and the streaming sweep (msf_sgsw.cu), so both execute
 // the same arithmetic.  Per-thread.
 template <bool FWD, bool BWD, bool ZERO, int NZ = 0x1ff>
 __device__ __forceinline__ double2 gs_node(const K0Mat& K, const double (&Eloc)[2][2],

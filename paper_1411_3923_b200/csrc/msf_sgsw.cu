@@ -2,9 +2,9 @@
 // B2 B1 B0 of one symmetric sweep (readings R7, R8; "single pre- and
 // post-smoothing using symmetric Gauss-Seidel") with the iterate held in REGISTERS.
 //
-// k_sgs_stream (msf_sgs.cu) keeps a 20-column ring of z in shared memory and reads the 3x3
+// The first streaming form (k_sgs_stream, earlier in round 2) kept a 20-column ring of z in shared memory and read the 3x3
 // neighbourhood of every node update from it (10 LDS.128 per update; the shared-memory data
-// pipe, 54% busy, is its most loaded unit, and the CTA barrier per step keeps the four phase
+// pipe, 54% busy, was its most loaded unit, and the CTA barrier per step kept the four phase
 // warps in lock step).  Here every WARP owns a band of 64 node rows (two per lane: rows
 // Yb + 2 lane and Yb + 2 lane + 1; the 48 middle rows are the band's, 8 above and below are
 // halo) and a run of node columns, and marches along x two columns per step.  Each lane holds
@@ -20,11 +20,12 @@
 //
 // Halo rows / columns (7 each side, one per phase) are swept redundantly from the same inputs
 // with the same arithmetic (msfk::gs_node), so the result is bitwise the colour-phase sweep's.
-// Variants as k_sgs_stream: ZERO (z = 0 on entry), UPD (r' = r - alpha q fused in front, r' to
+// Variants: ZERO (z = 0 on entry), UPD (r' = r - alpha q fused in front, r' to
 // a second buffer, ||r'||^2 -> convergence), RZ (r.z of the result -> beta).
 #include "msf_kern.cuh"
 
 #include <algorithm>
+#include <vector>
 
 using namespace msfk;
 
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(SW_T, SW_WARPS)
 
     // r and the moduli of node column c into ring slot sl (thread-private slots)
     auto issue = [&](int c, int sl) {
-      // (32-bit node / element indices: launch_sgs_stream checks the grid size)
+      // (32-bit node / element indices: msf_setup_mesh checks the grid size)
       const bool vc = c >= 0 && c < d.nnx;
       const int n = (vc ? c : 0) * d.nny;
       sw_cpa16(&S.s[sl].r[0][lane], r + (n + gn0), vc && vn0);
@@ -361,9 +362,29 @@ __global__ void __launch_bounds__(SW_T, SW_WARPS)
 
 }  // namespace
 
-// Same contract as launch_sgs_stream (msf_sgs.cu).
-void launch_sgs_warp(msf_ctx* c, int rhs0, int nr, const double* r, double* rout, const double* zin,
-                     double* z, bool gated, bool zero_start, bool upd, int rz_mode) {
+// Dirichlet bits in the sweep's layout: per node column, two row-parity planes of fs_plane bytes;
+// node row gy sits at plane gy & 1, byte (gy >> 1) + 4; rows outside the grid (down to -8, up
+// past the last band's halo) hold 3.
+void sgs_fix_layout(const Dims& d, int& fs_col, int& fs_plane) {
+  fs_plane = ((d.nny + 1) / 2 + 4 + 64 + 8 + 15) & ~15;
+  fs_col = 2 * fs_plane;
+}
+
+void sgs_fix_build(const Dims& d, const uint8_t* fixn, std::vector<uint8_t>& out) {
+  int fc, fp;
+  sgs_fix_layout(d, fc, fp);
+  out.assign((size_t)d.nnx * fc, 3);
+  for (int ix = 0; ix < d.nnx; ++ix)
+    for (int iy = 0; iy < d.nny; ++iy)
+      out[(size_t)ix * fc + (iy & 1) * fp + (iy >> 1) + 4] = fixn[(size_t)ix * d.nny + iy];
+}
+
+// z = SGS(zin; r) (zero_start: from z = 0) for realisations [rhs0, rhs0 + nr) of this rank's
+// owned columns, out of place (neighbouring warps read their halo of zin while this one writes
+// z).  upd: r -= alpha q first, the updated residual to rout (PCG iteration; ||r||^2 ->
+// convergence).  rz_mode != 0: r.z of the result -> beta (1: PCG init, 2: iteration).
+void launch_sgs_stream(msf_ctx* c, int rhs0, int nr, const double* r, double* rout, const double* zin,
+                       double* z, bool gated, bool zero_start, bool upd, int rz_mode) {
   const Dims& d = c->dl;
   const int nyb = (d.nny + SW_BAND - 1) / SW_BAND;
   // one wave of SW_WARPS one-warp CTAs per SM; runs of at least 32 columns

@@ -144,7 +144,7 @@ def test_symmetric_gauss_seidel(name):
 
 
 # grids that span several 112-row bands and several column runs of the streaming sweep
-# (msf_sgs.cu), with ragged last bands / runs, both boundary conditions, several realisations
+# (msf_sgsw.cu), with ragged last bands / runs, both boundary conditions, several realisations
 SGS_SPECS = {
     "bands_160x130": TMA_SPECS["tma_160x130"],
     "bands_96x252_mbb": TMA_SPECS["tma_96x252_mbb"],
