@@ -409,7 +409,11 @@ __global__ void __launch_bounds__(256) k_nd_panels(Dims d, const NdFront* __rest
 // RB per level: whole leaf fronts per CTA at the bottom, 8 rows per CTA at the top, at most
 // ND_STAGE bytes of rows per CTA.  Dependents are signalled once the CTA's row copies are
 // issued (see k_nd_solve).
-constexpr int ND_STAGE = 96 * 1024;
+#ifndef MSF_ND_STAGE_KB
+#define MSF_ND_STAGE_KB 32
+#endif
+constexpr int ND_STAGE = MSF_ND_STAGE_KB * 1024;       // staged rows per CTA ...
+constexpr int ND_STAGE_MAX = 96 * 1024;                 // ... raised up to this for 8 rows of a long front
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -690,7 +694,11 @@ void level_lists(NdPlan& P, int k, const std::vector<std::vector<int>>& lev, NdP
       lmax = std::max(lmax, len + (len & 1));
     }
     const long long want = std::max<long long>(8, (rows / (148LL * 4) + 7) / 8 * 8);
-    long long cap = ND_STAGE / (8LL * std::max(1, lmax));
+    // (measured, configs[4] / configs[3] solve at one realisation: 96 KB stages 0.223 / 1.145 ms,
+    // 48 KB 0.214 / 1.043, 32 KB 0.210 / 1.074 -- small stages keep more CTAs, i.e. more row
+    // pipelines, per SM; but 8 rows, one per warp, are kept where they fit 96 KB)
+    const long long stage = std::min<long long>(ND_STAGE_MAX, std::max<long long>(ND_STAGE, 64LL * std::max(1, lmax)));
+    long long cap = stage / (8LL * std::max(1, lmax));
     if (cap < 8) {
       long long p = 1;
       while (p * 2 <= cap) p *= 2;
