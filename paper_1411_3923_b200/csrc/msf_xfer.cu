@@ -162,39 +162,48 @@ __global__ void __launch_bounds__(XT) k_restrict_cells(Dims d, const XferClass* 
   __syncthreads();
   const double* t = reinterpret_cast<const double*>(tall + (size_t)rhs * d.nn);
   const int lx0 = T.ch * C.nx / nch, ncol = (T.ch + 1) * C.nx / nch - lx0;   // this task's columns
+  // sub-step i = (column lc = i / G, column group g = i % G): the column tile is loaded once
+  // (buffer lc & 1) and contracted with each group's Phi block (buffer i & 1) into that group's
+  // accumulators, so t is read once however many basis columns there are
   const int GJ = G * XNJ, nsteps = G * ncol;
-  auto stage = [&](int i) {   // step i = (group, column) into buffer i & 1
-    const int g = i / ncol, lx = lx0 + i - g * ncol;
-    stage_phi_col(d, C, phi, g, lx, SP(i & 1));
-    load_col_tile(d, C, cbase, T.nc, t, lx, Tt(i & 1), st);
+  auto stage = [&](int i) {
+    const int lc = i / G, g = i - lc * G;
+    stage_phi_col(d, C, phi, g, lx0 + lc, SP(i & 1));
+    if (g == 0) load_col_tile(d, C, cbase, T.nc, t, lx0 + lc, Tt(lc & 1), st);
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   stage(0);
-  double acc[2][NI][2];
-  for (int i = 0; i < nsteps; ++i) {
-    const int g = i / ncol, lc = i - g * ncol;
-    if (lc == 0) {
+  double acc[4][2][NI][2];   // [group]
 #pragma unroll
-      for (int k = 0; k < 4 * NI; ++k) (&acc[0][0][0])[k] = 0.0;
+  for (int k = 0; k < 16 * NI; ++k) (&acc[0][0][0][0])[k] = 0.0;
+  for (int lc = 0; lc < ncol; ++lc) {
+    const double* B = Tt(lc & 1);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      if (g < G) {
+        const int i = lc * G + g;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();   // sub-step i's data visible; sub-step i - 1's compute done everywhere
+        if (i + 1 < nsteps) stage(i + 1);
+        const double* S = SP(i & 1);
+        for (int k0 = 0; k0 < ep; k0 += 4) {
+          double a[2], b[NI];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) a[mi] = S[(k0 + tq) * SPJ + mi * 8 + gq];
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) b[ni] = B[(size_t)(CW * w + ni * 8 + gq) * st + k0 + tq];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) dmma884(acc[g][mi][ni][0], acc[g][mi][ni][1], a[mi], b[ni]);
+        }
+      }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();   // step i's data visible; step i - 1's compute done everywhere
-    if (i + 1 < nsteps) stage(i + 1);
-    const double* S = SP(i & 1);
-    const double* B = Tt(i & 1);
-    for (int k0 = 0; k0 < ep; k0 += 4) {
-      double a[2], b[NI];
+  }
+  // C(gq, 2 tq + h) of (g, mi, ni): column g*16 + mi*8 + gq, cell CW w + ni*8 + 2 tq + h
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) a[mi] = S[(k0 + tq) * SPJ + mi * 8 + gq];
-#pragma unroll
-      for (int ni = 0; ni < NI; ++ni) b[ni] = B[(size_t)(CW * w + ni * 8 + gq) * st + k0 + tq];
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-    }
-    if (lc == ncol - 1) {
-      // C(gq, 2 tq + h) of (mi, ni): column mi*8 + gq, cell CW w + ni*8 + 2 tq + h
+  for (int g = 0; g < 4; ++g)
+    if (g < G) {
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -203,17 +212,16 @@ __global__ void __launch_bounds__(XT) k_restrict_cells(Dims d, const XferClass* 
           for (int h = 0; h < 2; ++h) {
             const int c = CW * w + ni * 8 + 2 * tq + h;
             if (c < T.nc)
-              part[(((size_t)rhs * d.ncx * d.ncy + cid[c]) * nch + T.ch) * GJ + g * XNJ + mi * 8 + gq] = acc[mi][ni][h];
+              part[(((size_t)rhs * d.ncx * d.ncy + cid[c]) * nch + T.ch) * GJ + g * XNJ + mi * 8 + gq] = acc[g][mi][ni][h];
           }
     }
-  }
 }
 
 // t = zin + R_c^T x on the task's cells for realisation rhs0 + blockIdx.y (if active): per
 // pattern column, Z_col[2ny x 64 cells] += Phi_col [2ny x 16] . X^T [16 x 64 cells] on the fp64
 // tensor cores (warp w: all entries x cells CW w .. CW w + CW - 1), the column tile moved in and
 // out with coalesced 16-byte pieces; the next column loads while this one computes.  More than
-// 16 basis columns (G > 1): group 0 reads zin, the later groups add to tout.
+// 16 basis columns (G > 1): the groups add to the column tile one after the other.
 __global__ void __launch_bounds__(XT) k_prolong_cells(Dims d, const XferClass* __restrict__ cls,
                                                       const XferTask* __restrict__ tasks,
                                                       const int* __restrict__ cells,
@@ -264,23 +272,24 @@ __global__ void __launch_bounds__(XT) k_prolong_cells(Dims d, const XferClass* _
   const double* zi0 = reinterpret_cast<const double*>(zin + (size_t)rhs * d.nn);
   double* to = reinterpret_cast<double*>(tout + (size_t)rhs * d.nn);
   const int lx0 = T.ch * C.nx / nch, ncol = (T.ch + 1) * C.nx / nch - lx0;   // this task's columns
+  // sub-step i = (column lc = i / G, column group g = i % G): the column tile is loaded once
+  // (buffer lc & 1), every group's Phi block (buffer i & 1) adds its part, and the column is
+  // stored once after the last group
   const int nsteps = G * ncol;
   auto stage = [&](int i) {
-    const int g = i / ncol, lx = lx0 + i - g * ncol;
-    stage_phi_col(d, C, phi, g, lx, SP(i & 1));
-    load_col_tile(d, C, cbase, T.nc, g ? to : zi0, lx, Zt(i & 1), st);
+    const int lc = i / G, g = i - lc * G;
+    stage_phi_col(d, C, phi, g, lx0 + lc, SP(i & 1));
+    if (g == 0) load_col_tile(d, C, cbase, T.nc, zi0, lx0 + lc, Zt(lc & 1), st);
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   stage(0);
   for (int i = 0; i < nsteps; ++i) {
-    const int g = i / ncol, lx = lx0 + i - g * ncol;
+    const int lc = i / G, g = i - lc * G, lx = lx0 + lc;
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();   // step i's data (and X) visible; step i - 1's buffers free
-    // G > 1: group g + 1 re-reads this column after this step stores it, so it is never
-    // prefetched across a group boundary
-    if (i + 1 < nsteps && (G == 1 || (i + 1) % ncol != 0)) stage(i + 1);
+    __syncthreads();   // sub-step i's data (and X) visible; sub-step i - 1's buffers free
+    if (i + 1 < nsteps) stage(i + 1);
     const double* S = SP(i & 1);
-    double* Z = Zt(i & 1);
+    double* Z = Zt(lc & 1);
     const double* Xg = X + (size_t)g * NCC * SPJ;
     double acc[7][NI][2];   // up to 7 entry tiles (2 ny <= 56)
 #pragma unroll
@@ -299,7 +308,8 @@ __global__ void __launch_bounds__(XT) k_prolong_cells(Dims d, const XferClass* _
         }
       }
     }
-    // C(gq, 2 tq + h) of (mi, ni): entry mi*8 + gq of cell CW w + ni*8 + 2 tq + h
+    // C(gq, 2 tq + h) of (mi, ni): entry mi*8 + gq of cell CW w + ni*8 + 2 tq + h (the warp's own
+    // cells: no other warp touches these tile rows between the groups)
 #pragma unroll
     for (int mi = 0; mi < 7; ++mi) {
       const int e = mi * 8 + gq;
@@ -310,14 +320,12 @@ __global__ void __launch_bounds__(XT) k_prolong_cells(Dims d, const XferClass* _
           for (int h = 0; h < 2; ++h) Z[(size_t)(CW * w + ni * 8 + 2 * tq + h) * st + e] += acc[mi][ni][h];
       }
     }
-    __syncthreads();
-    if (lane < C.ny)   // column back out, 16-byte pieces (warp w: cells w, w + 8, ...)
-      for (int c = w; c < T.nc; c += XT / 32)
-        *reinterpret_cast<double2*>(to + 2 * (cbase[c] + (long long)lx * d.nny + lane)) =
-            *reinterpret_cast<const double2*>(Z + (size_t)c * st + 2 * lane);
-    if (G > 1 && (i + 1) % ncol == 0 && i + 1 < nsteps) {
-      __syncthreads();   // the group's last column is stored before the next group reads it
-      stage(i + 1);
+    if (g == G - 1) {
+      __syncthreads();
+      if (lane < C.ny)   // column back out, 16-byte pieces (warp w: cells w, w + 8, ...)
+        for (int c = w; c < T.nc; c += XT / 32)
+          *reinterpret_cast<double2*>(to + 2 * (cbase[c] + (long long)lx * d.nny + lane)) =
+              *reinterpret_cast<const double2*>(Z + (size_t)c * st + 2 * lane);
     }
   }
 }
