@@ -86,7 +86,8 @@ struct NdFront {
 struct NdPlan {
   struct List {       // task list in `lists`: fronts[n] then prefix sums of per-front counts
     int off = 0, n = 0, total = 0, total2 = 0, total3 = 0;
-    int RB = 8;       // solve lists: rows per CTA
+    int RB = 8;       // solve lists: rows per stage
+    int NS = 1;       // ... stages per CTA (rows per CTA = RB NS)
   };
   struct Levels {     // a group of levels (this rank's box / the interface tree)
     std::vector<List> asmb, fwd, back;        // per level: assembly tiles, solve row blocks

@@ -409,6 +409,12 @@ __global__ void __launch_bounds__(256) k_nd_panels(Dims d, const NdFront* __rest
 // RB per level: whole leaf fronts per CTA at the bottom, 8 rows per CTA at the top, at most
 // ND_STAGE bytes of rows per CTA.  Dependents are signalled once the CTA's row copies are
 // issued (see k_nd_solve).
+#ifndef MSF_ND_NSMAX
+#define MSF_ND_NSMAX 4
+#endif
+#ifndef MSF_ND_NSDIV
+#define MSF_ND_NSDIV 2
+#endif
 #ifndef MSF_ND_STAGE_KB
 #define MSF_ND_STAGE_KB 32
 #endif
@@ -419,10 +425,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-template <bool FWD>
+template <bool FWD, bool MULTI>
 __global__ void __launch_bounds__(256) k_nd_solve(Dims d, const NdFront* __restrict__ fr,
                                                   const int4* __restrict__ vmap,
-                                                  const int* __restrict__ list, int n, int RB,
+                                                  const int* __restrict__ list, int n, int RB, int NS_,
                                                   const double* __restrict__ Fall, long long Fstride,
                                                   double* uall, long long ustride,
                                                   const double* __restrict__ cball, double* cxall,
@@ -430,16 +436,20 @@ __global__ void __launch_bounds__(256) k_nd_solve(Dims d, const NdFront* __restr
                                                   const PcgScalars* sc, int rhs0, int gated) {
   extern __shared__ __align__(16) double nsm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(nsm);
+  const int NS = MULTI ? NS_ : 1;   // one stage: the stage loop below folds away
   const int li = nd_find(list + n, n, blockIdx.x);
-  const int f = list[li], rb0 = (blockIdx.x - list[n + li]) * RB;
+  // the CTA takes NS stages of RB rows: the right-hand side is gathered once for all of them
+  // (long fronts: the gather is as long as a row)
+  const int f = list[li], rb0 = (blockIdx.x - list[n + li]) * RB * NS;
   const int rhs = rhs0 + blockIdx.y;
   const NdFront F = fr[f];
   const int k = d.kmax, s = F.s_n * k, nf = (F.s_n + F.b_n) * k, ld = nf + (nf & 1);
   const int rows = FWD ? nf - s : s, len = FWD ? s : nf, lenp = len + (len & 1);
-  const int nrow = min(rows, rb0 + RB) - rb0;
+  const int nrow_all = min(rows, rb0 + RB * NS) - rb0;   // rows of this CTA
+  const int nrow = min(nrow_all, RB);                      // ... of its first stage
   double* sv = nsm + 2;                    // [lenp] right-hand side
-  double* vb = sv + lenp;                  // [RB]   forward: children's updates of the rows
-  double* sA = vb + ((RB + 1) & ~1);       // [nrow][lenp] staged rows (16-byte aligned)
+  double* vb = sv + lenp;                  // [RB NS] forward: children's updates of the rows
+  double* sA = vb + ((RB * NS + 1) & ~1);  // [RB][lenp] staged rows (16-byte aligned)
   const double* A = Fall + (size_t)rhs * Fstride + F.F_off + (size_t)(FWD ? s : 0) * ld;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -484,7 +494,7 @@ __global__ void __launch_bounds__(256) k_nd_solve(Dims d, const NdFront* __restr
       sv[c] = x;
     }
     if (FWD)
-      for (int r = threadIdx.x; r < nrow; r += 256) {
+      for (int r = threadIdx.x; r < nrow_all; r += 256) {
         const int4 m = vm[s + rb0 + r];
         double x = m.w >= 0 ? vt[m.w] : 0.0;
         if (m.y >= 0) x += u[m.y];
@@ -493,24 +503,47 @@ __global__ void __launch_bounds__(256) k_nd_solve(Dims d, const NdFront* __restr
       }
   }
   __syncthreads();
-  asm volatile(
-      "{\n.reg .pred P1;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
-      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(smem_u32(bar))
-      : "memory");
-  if (!live) return;
-  for (int r = wid; r < nrow; r += 8) {
-    const double* Ar = sA + (size_t)r * lenp;
-    double a0 = 0.0, a1 = 0.0;
-    int c = lane;
-    for (; c + 32 < len; c += 64) {
-      a0 = fma(Ar[c], sv[c], a0);
-      a1 = fma(Ar[c + 32], sv[c + 32], a1);
+  for (int j = 0, r0 = 0; r0 < nrow_all; ++j, r0 += RB) {
+    const int nr = min(nrow_all - r0, RB);
+    if (j > 0) {
+      // next stage into the same buffer: every warp is done reading it (barrier), and the generic
+      // reads are ordered before the async-proxy writes
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                     "r"((unsigned)(nr * lenp * 8))
+                     : "memory");
+      }
+      __syncthreads();
+      if (wid == 0)
+        for (int r = lane; r < nr; r += 32)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(sA + (size_t)r * lenp)),
+              "l"(A + (size_t)(rb0 + r0 + r) * ld), "r"((unsigned)(lenp * 8)), "r"(smem_u32(bar))
+              : "memory");
     }
-    if (c < len) a0 = fma(Ar[c], sv[c], a0);
-    const double t = warp_sum(a0 + a1);
-    if (lane == 0) {
-      if (FWD) u[F.u_off + rb0 + r] = vb[r] - t;
-      else cx[vm[rb0 + r].x] = -t;
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(smem_u32(bar)),
+        "r"((unsigned)(j & 1))
+        : "memory");
+    if (!live) continue;
+    for (int r = wid; r < nr; r += 8) {
+      const double* Ar = sA + (size_t)r * lenp;
+      double a0 = 0.0, a1 = 0.0;
+      int c = lane;
+      for (; c + 32 < len; c += 64) {
+        a0 = fma(Ar[c], sv[c], a0);
+        a1 = fma(Ar[c + 32], sv[c + 32], a1);
+      }
+      if (c < len) a0 = fma(Ar[c], sv[c], a0);
+      const double t = warp_sum(a0 + a1);
+      if (lane == 0) {
+        if (FWD) u[F.u_off + rb0 + r0 + r] = vb[r0 + r] - t;
+        else cx[vm[rb0 + r0 + r].x] = -t;
+      }
     }
   }
 }
@@ -707,8 +740,17 @@ void level_lists(NdPlan& P, int k, const std::vector<std::vector<int>>& lev, NdP
     cap = cap / 8 * 8;
     return (int)std::min<long long>(std::min(want, cap), std::max(8, (rmax + 7) / 8 * 8));
   };
-  auto smem = [](int lmax, int RB) {
-    return (int)(8 * (2 + (long long)lmax + ((RB + 1) & ~1) + (long long)RB * lmax));
+  auto smem = [](int lmax, int RB, int NS) {
+    return (int)(8 * (2 + (long long)lmax + ((RB * NS + 1) & ~1) + (long long)RB * lmax));
+  };
+  // stages per CTA: a long front's right-hand-side gather (index map + values, ~32 B per entry)
+  // is as long as a row, so CTAs of 8 rows spent a third of their time on it; up to 4 stages per
+  // CTA where the level still leaves 3 CTAs per SM (short fronts: 1 stage, as before)
+  auto stages = [&](const std::vector<int>& fl, bool fwd, int RB, int lmax) {
+    if (lmax < 512) return 1;
+    long long rows = 0;
+    for (int f : fl) rows += (long long)(fwd ? P.fr[f].b_n : P.fr[f].s_n) * k;
+    return (int)std::max<long long>(1, std::min<long long>(MSF_ND_NSMAX, rows / ((long long)RB * 148 * MSF_ND_NSDIV)));
   };
   for (int h = 0; h < H; ++h) {
     Lv.asmb[h] = add_list(P, lev[h], [&](const NdFront& F) { return nt(F) * nt(F); });
@@ -717,13 +759,17 @@ void level_lists(NdPlan& P, int k, const std::vector<std::vector<int>>& lev, NdP
       if (P.fr[f].b_n > 0) fw.push_back(f);
     int lmax = 0;
     int RB = pick(fw, true, lmax);
-    Lv.fwd[h] = add_list(P, fw, [&](const NdFront& F) { return (long long)(F.b_n * k + RB - 1) / RB; });
+    int NS = stages(fw, true, RB, lmax);
+    Lv.fwd[h] = add_list(P, fw, [&](const NdFront& F) { return (long long)(F.b_n * k + RB * NS - 1) / (RB * NS); });
     Lv.fwd[h].RB = RB;
-    Lv.fwd_smem[h] = smem(lmax, RB);
+    Lv.fwd[h].NS = NS;
+    Lv.fwd_smem[h] = smem(lmax, RB, NS);
     RB = pick(lev[h], false, lmax);
-    Lv.back[h] = add_list(P, lev[h], [&](const NdFront& F) { return (long long)(F.s_n * k + RB - 1) / RB; });
+    NS = stages(lev[h], false, RB, lmax);
+    Lv.back[h] = add_list(P, lev[h], [&](const NdFront& F) { return (long long)(F.s_n * k + RB * NS - 1) / (RB * NS); });
     Lv.back[h].RB = RB;
-    Lv.back_smem[h] = smem(lmax, RB);
+    Lv.back[h].NS = NS;
+    Lv.back_smem[h] = smem(lmax, RB, NS);
     int smax = 0;
     for (int f : lev[h]) smax = std::max(smax, P.fr[f].s_n * k);
     for (int pt = 0; pt * NB < smax; ++pt) {
@@ -935,8 +981,10 @@ void solve_levels(msf_ctx* c, const NdPlan::Levels& Lv, bool fwd, int rhs0, int 
   const Dims& d = c->d;
   static bool smem_set = false;
   if (!smem_set) {
-    cudaFuncSetAttribute(k_nd_solve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_nd_solve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_nd_solve<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_nd_solve<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_nd_solve<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_nd_solve<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     smem_set = true;
   }
   const int H = (int)Lv.fwd.size();
@@ -945,9 +993,10 @@ void solve_levels(msf_ctx* c, const NdPlan::Levels& Lv, bool fwd, int rhs0, int 
     const NdPlan::List& L = fwd ? Lv.fwd[h] : Lv.back[h];
     if (L.total == 0) continue;
     const size_t smem = (size_t)(fwd ? Lv.fwd_smem[h] : Lv.back_smem[h]);
-    auto kern = fwd ? k_nd_solve<true> : k_nd_solve<false>;
+    auto kern = L.NS > 1 ? (fwd ? k_nd_solve<true, true> : k_nd_solve<false, true>)
+                         : (fwd ? k_nd_solve<true, false> : k_nd_solve<false, false>);
     launch_k(kern, dim3(L.total, nr), dim3(256), smem, c->stream, d, (const NdFront*)c->nd_fr,
-             (const int4*)c->nd_vmap, (const int*)(c->nd_lists + L.off), L.n, L.RB, (const double*)c->nd_F,
+             (const int4*)c->nd_vmap, (const int*)(c->nd_lists + L.off), L.n, L.RB, L.NS, (const double*)c->nd_F,
              (long long)P.F_total, c->nd_u, (long long)P.u_total, (const double*)c->cb, c->cx,
              (const double*)c->nd_vtop, (long long)std::max<long long>(1, P.vtop_total),
              (const PcgScalars*)c->sc, rhs0, gated ? 1 : 0);
