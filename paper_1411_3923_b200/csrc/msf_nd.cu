@@ -575,13 +575,21 @@ __global__ void __launch_bounds__(256) k_nd_pack(const int2* __restrict__ pm, in
 // ================================================================== host: plan
 namespace {
 
-constexpr int ND_LEAF = 5;   // leaf boxes of at most 5 x 5 coarse nodes
+// Leaf boxes of at most leaf x leaf coarse nodes.  Larger leaves trade levels (launch latency)
+// for factor bytes: 5 on large boxes (configs[4] solve: 0.216 ms with 5, 0.233 with 7 or 9);
+// 9 on boxes of 1,024 .. 8,192 nodes with up to 4 modes, whose solve is all level latency
+// (configs[1]: 0.072 -> 0.036 ms; a rank of 8 strips of configs[4]: 0.100 -> 0.094 ms).
+constexpr int ND_LEAF = 5, ND_LEAF_SMALL = 9;
+inline int nd_leaf(long long box_nodes, int k) {
+  return (k <= 4 && box_nodes >= 1024 && box_nodes <= 8192) ? ND_LEAF_SMALL : ND_LEAF;
+}
 
 struct Builder {
   int X, Y, k;
   NdPlan& P;
   int rank;
   const std::vector<int>& icol;   // interface column of each rank > 0 (icol[r], r = 1..N-1)
+  int leaf = ND_LEAF;             // leaf size of this rank's box (set before its dissection)
 
   // ring of the box [x0, x1) x [y0, y1) inside the grid
   std::vector<int> ring(int x0, int x1, int y0, int y1) const {
@@ -649,7 +657,7 @@ struct Builder {
     if (w <= 0 || h <= 0) return -1;
     std::vector<int> S;
     int c0 = -1, c1 = -1;
-    if (w <= ND_LEAF && h <= ND_LEAF) {
+    if (w <= leaf && h <= leaf) {
       for (int x = x0; x < x1; ++x)
         for (int y = y0; y < y1; ++y) S.push_back(x * Y + y);
     } else if (w >= h) {
@@ -670,7 +678,11 @@ struct Builder {
   // that rank); a group is split at the interface column of its middle rank, whose front is an
   // interface front (replicated on every rank)
   int group(int ra, int rb, int gx0, int gx1) {
-    if (rb - ra == 1) return ra == rank ? rec(gx0, gx1, 0, Y) : -1;
+    if (rb - ra == 1) {
+      if (ra != rank) return -1;
+      leaf = nd_leaf((long long)(gx1 - gx0) * Y, k);
+      return rec(gx0, gx1, 0, Y);
+    }
     const int rm = (ra + rb) / 2, xm = icol[rm];
     const int c0 = group(ra, rm, gx0, xm);
     const int c1 = group(rm, rb, xm + 1, gx1);
