@@ -42,6 +42,9 @@ STRIP_SPECS = {
     "ragged_36x20": (SPECS["ragged_36x20"], (2, 3)),
     # cx odd: ranks with and without padding
     "odd_30x12": (W.small_spec(nelx=30, nely=12, cx=3, cy=3, seed=41, Emin=1e-6), (3, 4)),
+    # cx odd and strips of 27 node columns: 8-column halos (streaming sweep) behind a padding
+    # column (rank 1 owns from the odd column 27: its local grid starts at column 18)
+    "odd_wide_54x18": (W.small_spec(nelx=54, nely=18, cx=9, cy=9, seed=43, Emin=1e-6), (2,)),
     # 20 x 20-element cells: the G^T G (cuBLAS) Galerkin products over each rank's cells
     "cells20_60x40": (W.small_spec(nelx=60, nely=40, cx=20, cy=20, tile=(20, 20), rmin=1.5, beta=4.0,
                                    etas=(0.6, 0.4), dilated=1, seed=33, Emin=1e-6), (2, 3)),
