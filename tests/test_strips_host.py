@@ -29,7 +29,7 @@ def pkg():
 
 
 @pytest.mark.parametrize("nelx,cx,nranks", [(16, 4, 2), (16, 4, 4), (30, 3, 3), (30, 3, 4),
-                                            (36, 4, 3), (32, 8, 3), (60, 20, 3), (1024, 16, 8),
+                                            (36, 4, 3), (32, 8, 3), (60, 20, 3), (54, 9, 2), (1024, 16, 8),
                                             (5120, 20, 8)])
 def test_strip_bounds(pkg, nelx, cx, nranks):
     spec = W.small_spec(nelx=nelx, nely=8, cx=cx, cy=4)
