@@ -15,8 +15,8 @@ if [ "${1:-A}" = A ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none -c 30000 --csv --log-file $O/launches_step.csv \
       python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-sweep > $O/launches_bench.log 2>&1
   gzip -f $O/launches_step.csv
-  cap sgs_pre 'k_sgs_stream<\(bool\)1, \(bool\)1' 0 1
-  cap sgs_post 'k_sgs_stream<\(bool\)0, \(bool\)0, \(bool\)0' 1 1
+  cap sgs_pre 'k_sgs_warp<\(bool\)1, \(bool\)1' 0 1
+  cap sgs_post 'k_sgs_warp<\(bool\)0, \(bool\)0, \(bool\)1' 1 1
   cap restrict 'k_restrict_cells' 1 1
   cap prolong 'k_prolong_cells' 1 1
 else
